@@ -1,0 +1,267 @@
+/*
+ * kgdist_b200 — C ABI of the B200-native (sm_100a) training hot path of the
+ * partitioned RGCN + DistMult KG-embedding scheme (arXiv 2201.02791,
+ * reference package `kgdist`).
+ *
+ * The reference has no FFI: its boundary is the Python API re-exported by
+ * kgdist/__init__.py:8-41. Each entry point below replaces the numpy body of
+ * one reference function (cited as ref:<file>:<line>, ref = pkg/src/kgdist);
+ * the package `paper_2201_02791_b200` keeps the reference's Python names and
+ * calls these through ctypes.
+ *
+ * Conventions
+ *  - All pointers are DEVICE pointers unless noted; the caller owns every
+ *    buffer (PyTorch tensors on the Python side). Scratch space comes from a
+ *    caller workspace sized by the matching *_workspace_bytes() call.
+ *  - `stream` is a cudaStream_t passed as void*. Every call is asynchronous
+ *    on that stream; device-side failures (non-finite values, exhausted
+ *    resampling) are written to a device status word the caller checks at
+ *    its sync points.
+ *  - Ids are int32 local vertex ids, relation ids int32, values fp32.
+ *  - Return value kg_status maps 1:1 onto the reference's KGError classes
+ *    (ref:errors.py:8-49); kg_last_error() returns the message.
+ */
+#ifndef KGDIST_B200_H
+#define KGDIST_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define KG_ABI_VERSION 1
+
+typedef enum kg_status {
+  KG_OK = 0,
+  KG_ERR_VALIDATION = 1, /* ValidationError   */
+  KG_ERR_SHAPE = 2,      /* ShapeError        */
+  KG_ERR_INTEGRITY = 3,  /* IntegrityError    */
+  KG_ERR_SAMPLING = 4,   /* SamplingError     */
+  KG_ERR_NUMERIC = 5,    /* NumericError      */
+  KG_ERR_PROTOCOL = 6,   /* ProtocolError     */
+  KG_ERR_CUDA = 7        /* CUDA runtime failure (no reference analogue) */
+} kg_status;
+
+/* Device status-word bits (written by kernels, read by the host at syncs). */
+#define KG_FLAG_NONFINITE_SCORE 1u
+#define KG_FLAG_NONFINITE_LOSS 2u
+#define KG_FLAG_NONFINITE_PARAM 4u
+#define KG_FLAG_BAD_VERTEX 8u
+
+/* numpy PCG64 BitGenerator state (Generator.bit_generator.state). */
+typedef struct kg_pcg64 {
+  uint64_t state_hi, state_lo;
+  uint64_t inc_hi, inc_lo;
+  uint32_t has_uint32;
+  uint32_t uinteger;
+} kg_pcg64;
+
+/* Partition message graph resident in HBM (built by kg_view_build).
+ * Row v of the destination CSR lists messages entering v sorted by
+ * (relation, original order); the source CSR (CSC) lists messages leaving v
+ * sorted by (relation, original order). Self-loops are implicit (group 2R). */
+typedef struct kg_graph_csr {
+  int32_t n;          /* local vertices                                   */
+  int32_t R;          /* relations before inverse doubling                */
+  int64_t e;          /* message edges = 2 * edges                        */
+  int32_t* indptr;    /* [n+1]                                            */
+  int32_t* src;       /* [e]                                              */
+  int32_t* rel;       /* [e]                                              */
+  float* norm;        /* [e]   1 / c_{dst,rel}                            */
+  int32_t* c_indptr;  /* [n+1]                                            */
+  int32_t* c_dst;     /* [e]                                              */
+  int32_t* c_rel;     /* [e]                                              */
+  float* c_norm;      /* [e]                                              */
+  int32_t* rel_perm;  /* [e]   CSC positions grouped by relation          */
+  int32_t* rel_ptr;   /* [2R+1] group starts into rel_perm (+ end)        */
+} kg_graph_csr;
+
+/* One RGCN layer's parameters (ref:model.py:64-79). */
+typedef struct kg_layer_params {
+  int32_t d_in, d_out, B, G; /* G = 2R + 1 relation groups                 */
+  const float* bases;        /* (B, d_in, d_out)                           */
+  const float* coeffs;       /* (G, B)                                     */
+} kg_layer_params;
+
+/* ---------------------------------------------------------------------- */
+/* Library                                                                 */
+/* ---------------------------------------------------------------------- */
+int kg_abi_version(void);
+int kg_last_error(char* buf, int64_t n); /* host buffer */
+
+/* ---------------------------------------------------------------------- */
+/* Primitives (stable radix sort / scan) used by every stage below          */
+/* ---------------------------------------------------------------------- */
+int64_t kg_sort_workspace_bytes(int64_t n);
+kg_status kg_sort_pairs_u64(uint64_t* keys, uint32_t* vals, int64_t n, int key_bits, void* ws,
+                            int64_t ws_bytes, void* stream);
+int64_t kg_scan_workspace_bytes(int64_t n);
+kg_status kg_exclusive_scan_u32(const uint32_t* in, uint32_t* out, int64_t n, uint32_t* total, void* ws,
+                                int64_t ws_bytes, void* stream);
+
+/* ---------------------------------------------------------------------- */
+/* PCG64 host bookkeeping (host pointers)                                  */
+/* ---------------------------------------------------------------------- */
+/* Jump ahead `delta` next64 draws (numpy bit_generator.advance). */
+void kg_pcg64_advance(kg_pcg64* g, uint64_t delta);
+/* Account for `count` next_uint32 draws (buffered half-words included). */
+void kg_pcg64_consume32(kg_pcg64* g, uint64_t count);
+/* First `count` next64 outputs (host buffer), for self-checks. */
+void kg_pcg64_peek64(const kg_pcg64* g, uint64_t* out, int64_t count);
+
+/* ---------------------------------------------------------------------- */
+/* R1/R2  Partition view (replaces ref:partition.py:61-74 local ids and    */
+/*        ref:sampler.py:73-118 build_view)                                */
+/* ---------------------------------------------------------------------- */
+int64_t kg_view_workspace_bytes(int64_t m, int64_t num_entities);
+/* Local ids: core endpoints in first-appearance order over (h0,t0,h1,..),
+ * then support-only endpoints likewise. Inputs are global (m,3) triples.
+ * Writes local_ids[0..n_local), g2l[num_entities] (-1 if absent) and the
+ * count *n_local (device int32). */
+kg_status kg_view_local_ids(const int32_t* core, int64_t m_core, const int32_t* support, int64_t m_sup,
+                            int64_t num_entities, int32_t* local_ids, int32_t* g2l, int32_t* n_local,
+                            void* ws, int64_t ws_bytes, void* stream);
+/* Message graph: edges_global (m,3) core-then-support global triples.
+ * Outputs: edges_local (m,3); reference-order message arrays ref_src,
+ * ref_rel, msg_cnt [2m] (stable-by-destination, ref:sampler.py:91; norm =
+ * 1/msg_cnt); the working CSR/CSC in *g (arrays preallocated by caller,
+ * g->n and g->R set); sorted unique positive keys pos_keys[*n_keys]. */
+kg_status kg_view_build(const int32_t* edges_global, int64_t m, const int32_t* g2l, int32_t* edges_local,
+                        int32_t* ref_src, int32_t* ref_rel, int32_t* msg_cnt, const kg_graph_csr* g,
+                        int64_t* pos_keys, int32_t* n_keys, void* ws, int64_t ws_bytes, void* stream);
+
+/* ---------------------------------------------------------------------- */
+/* R3/R4  Constraint-based negatives (ref:sampler.py:60-70, 144-182)        */
+/* ---------------------------------------------------------------------- */
+/* neg = repeat(core, s); col[i] = 0 (head) if random() < 0.5 else 2;
+ * pending = 0..s*m-1. Consumes s*m next64 draws (host advances g). */
+kg_status kg_neg_init(const int32_t* core, int64_t m, int32_t s, kg_pcg64 g, int32_t* neg, int8_t* col,
+                      int32_t* pending, void* stream);
+int64_t kg_neg_round_workspace_bytes(int64_t window);
+/* One resampling round over the k pending rows (ascending): draws
+ * integers(pool_size, size=k) from a window of `window` uint32 positions,
+ * writes the corrupted entity, rejects originals and local positives.
+ * Outputs next_pending[*next_count] and *consumed32 (uint32 draws used;
+ * 0 => window too small, retry larger). */
+kg_status kg_neg_round(int32_t* neg, const int8_t* col, const int32_t* core, int32_t s,
+                       const int32_t* pending, int64_t k, int64_t pool_size, int32_t n_local, int32_t R,
+                       const int64_t* pos_keys, const int32_t* n_keys, kg_pcg64 g, int64_t window,
+                       int32_t* next_pending, int32_t* next_count, int64_t* consumed32, void* ws,
+                       int64_t ws_bytes, void* stream);
+/* is_positive over (k,3) local triples -> out[k] (0/1). */
+kg_status kg_is_positive(const int32_t* triples, int64_t k, int32_t n_local, int32_t R, const int64_t* pos_keys,
+                         const int32_t* n_keys, uint8_t* out, void* stream);
+
+/* ---------------------------------------------------------------------- */
+/* R5  Edge mini-batch stream (ref:sampler.py:202-232)                      */
+/* ---------------------------------------------------------------------- */
+/* Fisher-Yates swap targets js[i] for i = n-1..1 of rng.permutation(n)
+ * (bit-exact, masked rejection). U is a device buffer of W uint32 stream
+ * positions (W = kg_perm_draws_buffer_len(n)); *consumed32 = uint32 draws
+ * used, or -1 if W was too small (retry with a larger buffer). */
+int64_t kg_perm_draws_buffer_len(int64_t n);
+kg_status kg_perm_draws_buffered(int64_t n, kg_pcg64 g, uint32_t* U, int64_t W, int32_t* js, int64_t* consumed32,
+                                 void* stream);
+int64_t kg_perm_resolve_workspace_bytes(int64_t n);
+/* Final permutation from the swap targets without replaying the swaps. */
+kg_status kg_perm_resolve(const int32_t* js, int64_t n, int32_t* perm, void* ws, int64_t ws_bytes,
+                          void* stream);
+/* stream[k] = concat(pos, neg)[perm[k]], labels 1/0. */
+kg_status kg_stream_gather(const int32_t* pos, int64_t npos, const int32_t* neg, int64_t nneg,
+                           const int32_t* perm, int32_t* stream_triples, float* labels, void* stream);
+
+/* ---------------------------------------------------------------------- */
+/* R7/R8  Layered closure (ref:sampler.py:310-376)                          */
+/* ---------------------------------------------------------------------- */
+int64_t kg_closure_workspace_bytes(int32_t n);
+/* Seeds = endpoints of batch rows (start+q) mod total, q < b, of the
+ * (total,3) stream; or, when stream_triples == NULL, the ids seed_ids[b].
+ * Writes vertex_order (seeds ascending, then each hop's new sources
+ * ascending), pos[n] (-1 if absent) and counts[hops+1] (device). */
+kg_status kg_closure(const int32_t* stream_triples, int64_t total, int64_t start, int64_t b,
+                     const int32_t* seed_ids, const kg_graph_csr* g, int32_t hops, int32_t* vertex_order,
+                     int32_t* pos, int32_t* counts, void* ws, int64_t ws_bytes, void* stream);
+
+/* ---------------------------------------------------------------------- */
+/* R13-R17  RGCN layer forward / backward, DistMult + BCE                  */
+/* ---------------------------------------------------------------------- */
+int64_t kg_layer_workspace_bytes(int32_t n, int64_t e, int32_t d_in, int32_t d_out, int32_t B);
+/* ref:model.py:151-164, 216-220: Z[v] = sum_b (sum_{e->v} norm a[r,b] H[src]
+ * + a[2R,b] H[v]) V_b for v in A_t = vertex_order[0:counts[t]];
+ * H_out[v] = relu(Z) (relu != 0) or Z. H_in/H_out rows indexed by local id. */
+kg_status kg_rgcn_forward(const kg_graph_csr* g, const kg_layer_params* lp, const float* H_in, float* H_out,
+                          const int32_t* vertex_order, const int32_t* counts, int32_t t, int32_t relu,
+                          void* ws, int64_t ws_bytes, void* stream);
+/* ref:model.py:167-185, 286-296: gradients of one layer. dH_out holds
+ * dL/dA of the layer output for v in A_t (by local id); H_out (NULL for the
+ * last layer) supplies the ReLU mask. Writes d_bases (B,d_in,d_out),
+ * d_coeffs (G,B) and, if dH_in != NULL, dL/dH_in for v in A_{t+1}. */
+kg_status kg_rgcn_backward(const kg_graph_csr* g, const kg_layer_params* lp, const float* H_in,
+                           const float* H_out, const float* dH_out, float* dH_in, const int32_t* vertex_order,
+                           const int32_t* pos, const int32_t* counts, int32_t t, float* d_bases,
+                           float* d_coeffs, void* ws, int64_t ws_bytes, void* stream);
+int64_t kg_loss_workspace_bytes(int64_t b, int32_t n, int32_t d, int32_t R);
+/* ref:model.py:254-281: DistMult scores of batch rows (start+q) mod total,
+ * BCE loss (mean, device scalar), d_decoder (R,d) and dH (rows of the
+ * seeds, by local id). Non-finite score/loss sets bits in *flags. */
+kg_status kg_distmult_loss(const float* H, int32_t d, int32_t n_local, const float* decoder, int32_t R,
+                           const int32_t* stream_triples, const float* labels, int64_t total, int64_t start,
+                           int64_t b, const int32_t* vertex_order, const int32_t* counts, float* dH,
+                           float* d_decoder, float* loss_out, float* scores_out, uint32_t* flags, void* ws,
+                           int64_t ws_bytes, void* stream);
+
+/* ---------------------------------------------------------------------- */
+/* R19/R20  Reduction + optimizer (ref:trainer.py:63-151)                  */
+/* ---------------------------------------------------------------------- */
+int64_t kg_optim_workspace_bytes(int64_t n);
+/* Dense step on the flat block buffer. grads_all holds P payloads
+ * back to back (P*n); they are combined in the reference's pairwise-tree
+ * order and divided by P (ref:trainer.py:77-86) inside the same kernel.
+ * optimizer: 0 = sgd, 1 = adam. grad_clip <= 0 disables clipping. */
+kg_status kg_dense_step(float* params, float* m, float* v, const float* grads_all, int32_t P, int64_t n,
+                        int32_t optimizer, float lr, float beta1, float beta2, float eps, double bc1,
+                        double bc2, float grad_clip, uint32_t* flags, void* ws, int64_t ws_bytes,
+                        void* stream);
+/* Lazy sparse rows (ref:trainer.py:136-147): rows = vertex_order[0:counts[k]]
+ * of the (n,d) table; grad rows by local id. */
+kg_status kg_sparse_step(float* table, float* m, float* v, const float* grad, const int32_t* rows,
+                         const int32_t* counts, int32_t k, int32_t d, int32_t optimizer, float lr,
+                         float beta1, float beta2, float eps, double bc1, double bc2, int32_t n_max,
+                         void* stream);
+
+/* ---------------------------------------------------------------------- */
+/* R24-R26  Filtered evaluation (ref:evaluate.py:93-225)                   */
+/* ---------------------------------------------------------------------- */
+/* Ranks of every query triple against all N entities, tail side and head
+ * side, minus known collisions: tail_keys = sorted unique (h*R+r)*N+t of
+ * train+valid+test, head_keys = sorted unique (t*R+r)*N+h. Records are
+ * written in the reference order (per chunk: tail records, head records).
+ * policy: 0 mean, 1 optimistic, 2 pessimistic. */
+int64_t kg_eval_workspace_bytes(int64_t nq);
+kg_status kg_eval_filtered(const float* H, int32_t d, int32_t N, const float* decoder, int32_t R,
+                           const int32_t* queries, int64_t nq, const int64_t* tail_keys, int64_t n_tail,
+                           const int64_t* head_keys, int64_t n_head, int32_t policy, int32_t chunk,
+                           double* ranks, int32_t* ncand, void* ws, int64_t ws_bytes, void* stream);
+/* Sorted unique keys (a*R + r)*N + c of (k,3) triples with (a,c) = (col_a, col_c). */
+int64_t kg_known_keys_workspace_bytes(int64_t k);
+kg_status kg_known_keys(const int32_t* triples, int64_t k, int32_t col_a, int32_t col_c, int32_t N, int32_t R,
+                        int64_t* keys_out, int32_t* n_out, void* ws, int64_t ws_bytes, void* stream);
+
+/* ---------------------------------------------------------------------- */
+/* Host-side input producers (HOST pointers)        */
+/* ---------------------------------------------------------------------- */
+/* Edge loop of ref:graph.py:336-381 generate_synthetic: writes up to target
+ * (h,r,t) rows to out (int64) and returns the count; advances *g exactly as
+ * numpy's Generator (the caller continues with permutation()). */
+int64_t kg_generate_synthetic(int64_t num_entities, int32_t num_relations, int64_t target, kg_pcg64* g,
+                              int64_t* out, int64_t max_attempts);
+/* Greedy streaming vertex cut of ref:partition.py:141-191 over edges in
+ * `order` (int64); assign[e] = partition (int64). */
+kg_status kg_vertex_cut_assign(const int64_t* triples, int64_t m, int64_t num_entities, int32_t P,
+                               const int64_t* order, double balance_weight, int64_t cap, int64_t* assign);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* KGDIST_B200_H */

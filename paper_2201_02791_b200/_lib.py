@@ -1,0 +1,201 @@
+"""ctypes binding of the sm_100a kernel library (include/kgdist_b200.h).
+
+The library is built in-tree by `make` (or __graft_entry__.build()) into
+paper_2201_02791_b200/lib/libkgdist_b200.so. There is no CPU fallback: every
+compute entry point needs a CUDA device, and `require_cuda()` fails loudly
+when the device or the library is missing.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+from ctypes import POINTER, c_double, c_float, c_int, c_int8, c_int32, c_int64, c_uint32, c_uint64, c_void_p
+
+import numpy as np
+
+from .errors import STATUS_ERRORS, DeviceError, KGError
+
+LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "lib", "libkgdist_b200.so")
+ABI_VERSION = 1
+
+
+class KgPcg64(ctypes.Structure):
+    _fields_ = [("state_hi", c_uint64), ("state_lo", c_uint64), ("inc_hi", c_uint64),
+                ("inc_lo", c_uint64), ("has_uint32", c_uint32), ("uinteger", c_uint32)]
+
+
+class KgGraphCsr(ctypes.Structure):
+    _fields_ = [("n", c_int32), ("R", c_int32), ("e", c_int64),
+                ("indptr", c_void_p), ("src", c_void_p), ("rel", c_void_p), ("norm", c_void_p),
+                ("c_indptr", c_void_p), ("c_dst", c_void_p), ("c_rel", c_void_p), ("c_norm", c_void_p),
+                ("rel_perm", c_void_p), ("rel_ptr", c_void_p)]
+
+
+class KgLayerParams(ctypes.Structure):
+    _fields_ = [("d_in", c_int32), ("d_out", c_int32), ("B", c_int32), ("G", c_int32),
+                ("bases", c_void_p), ("coeffs", c_void_p)]
+
+
+P = c_void_p
+ST = c_int  # kg_status
+
+# name -> (restype, argtypes)
+_PROTOS = {
+    "kg_abi_version": (c_int, []),
+    "kg_last_error": (c_int, [ctypes.c_char_p, c_int64]),
+    "kg_sort_workspace_bytes": (c_int64, [c_int64]),
+    "kg_sort_pairs_u64": (ST, [P, P, c_int64, c_int, P, c_int64, P]),
+    "kg_scan_workspace_bytes": (c_int64, [c_int64]),
+    "kg_exclusive_scan_u32": (ST, [P, P, c_int64, P, P, c_int64, P]),
+    "kg_pcg64_advance": (None, [POINTER(KgPcg64), c_uint64]),
+    "kg_pcg64_consume32": (None, [POINTER(KgPcg64), c_uint64]),
+    "kg_pcg64_peek64": (None, [POINTER(KgPcg64), P, c_int64]),
+    "kg_view_workspace_bytes": (c_int64, [c_int64, c_int64]),
+    "kg_view_local_ids": (ST, [P, c_int64, P, c_int64, c_int64, P, P, P, P, c_int64, P]),
+    "kg_view_build": (ST, [P, c_int64, P, P, P, P, P, POINTER(KgGraphCsr), P, P, P, c_int64, P]),
+    "kg_neg_init": (ST, [P, c_int64, c_int32, KgPcg64, P, P, P, P]),
+    "kg_neg_round_workspace_bytes": (c_int64, [c_int64]),
+    "kg_neg_round": (ST, [P, P, P, c_int32, P, c_int64, c_int64, c_int32, c_int32, P, P, KgPcg64,
+                          c_int64, P, P, P, P, c_int64, P]),
+    "kg_is_positive": (ST, [P, c_int64, c_int32, c_int32, P, P, P, P]),
+    "kg_perm_draws_buffer_len": (c_int64, [c_int64]),
+    "kg_perm_draws_buffered": (ST, [c_int64, KgPcg64, P, c_int64, P, P, P]),
+    "kg_perm_resolve_workspace_bytes": (c_int64, [c_int64]),
+    "kg_perm_resolve": (ST, [P, c_int64, P, P, c_int64, P]),
+    "kg_stream_gather": (ST, [P, c_int64, P, c_int64, P, P, P, P]),
+    "kg_closure_workspace_bytes": (c_int64, [c_int32]),
+    "kg_closure": (ST, [P, c_int64, c_int64, c_int64, P, POINTER(KgGraphCsr), c_int32, P, P, P, P,
+                        c_int64, P]),
+    "kg_layer_workspace_bytes": (c_int64, [c_int32, c_int64, c_int32, c_int32, c_int32]),
+    "kg_rgcn_forward": (ST, [POINTER(KgGraphCsr), POINTER(KgLayerParams), P, P, P, P, c_int32, c_int32,
+                             P, c_int64, P]),
+    "kg_rgcn_backward": (ST, [POINTER(KgGraphCsr), POINTER(KgLayerParams), P, P, P, P, P, P, P, c_int32,
+                              P, P, P, c_int64, P]),
+    "kg_loss_workspace_bytes": (c_int64, [c_int64, c_int32, c_int32, c_int32]),
+    "kg_distmult_loss": (ST, [P, c_int32, c_int32, P, c_int32, P, P, c_int64, c_int64, c_int64, P, P, P,
+                              P, P, P, P, P, c_int64, P]),
+    "kg_optim_workspace_bytes": (c_int64, [c_int64]),
+    "kg_dense_step": (ST, [P, P, P, P, c_int32, c_int64, c_int32, c_float, c_float, c_float, c_float,
+                           c_double, c_double, c_float, P, P, c_int64, P]),
+    "kg_sparse_step": (ST, [P, P, P, P, P, P, c_int32, c_int32, c_int32, c_float, c_float, c_float,
+                            c_float, c_double, c_double, c_int32, P]),
+    "kg_eval_workspace_bytes": (c_int64, [c_int64]),
+    "kg_eval_filtered": (ST, [P, c_int32, c_int32, P, c_int32, P, c_int64, P, c_int64, P, c_int64,
+                              c_int32, c_int32, P, P, P, c_int64, P]),
+    "kg_known_keys_workspace_bytes": (c_int64, [c_int64]),
+    "kg_known_keys": (ST, [P, c_int64, c_int32, c_int32, c_int32, c_int32, P, P, P, c_int64, P]),
+    "kg_generate_synthetic": (c_int64, [c_int64, c_int32, c_int64, POINTER(KgPcg64), P, c_int64]),
+    "kg_vertex_cut_assign": (ST, [P, c_int64, c_int64, c_int32, P, c_double, c_int64, P]),
+}
+
+_lib = None
+
+
+def exported_symbols() -> list:
+    return sorted(_PROTOS)
+
+
+def load():
+    """Load the shared library (no device needed) and bind every prototype."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.isfile(LIB_PATH):
+        raise DeviceError(f"kernel library not built: {LIB_PATH} (run `make` or "
+                          f"__graft_entry__.build())")
+    lib = ctypes.CDLL(LIB_PATH)
+    for name, (res, args) in _PROTOS.items():
+        fn = getattr(lib, name)
+        fn.restype = res
+        fn.argtypes = args
+    if lib.kg_abi_version() != ABI_VERSION:
+        raise DeviceError("kernel library ABI version mismatch; rebuild")
+    _lib = lib
+    return lib
+
+
+def require_cuda():
+    """The compute path has no CPU fallback: fail loudly without a device."""
+    import torch
+    if not torch.cuda.is_available():
+        raise DeviceError("paper_2201_02791_b200 needs a CUDA device (B200, sm_100a); "
+                          "no CPU fallback exists")
+    return load()
+
+
+def last_error() -> str:
+    buf = ctypes.create_string_buffer(512)
+    load().kg_last_error(buf, 512)
+    return buf.value.decode(errors="replace")
+
+
+def check(status: int, what: str = "") -> None:
+    if status != 0:
+        cls = STATUS_ERRORS.get(int(status), KGError)
+        raise cls(f"{what}: {last_error()}" if what else last_error())
+
+
+def call(name: str, *args):
+    """Invoke a kg_status-returning entry point and raise on failure."""
+    fn = getattr(require_cuda(), name)
+    check(fn(*args), name)
+
+
+def ptr(t) -> int:
+    return 0 if t is None else t.data_ptr()
+
+
+def stream_handle() -> int:
+    import torch
+    return torch.cuda.current_stream().cuda_stream
+
+
+class Workspace:
+    """Grow-only scratch buffers keyed by purpose (one device allocation each)."""
+
+    def __init__(self, device):
+        self.device = device
+        self._bufs = {}
+
+    def get(self, key: str, nbytes: int):
+        import torch
+        nbytes = max(int(nbytes), 256)
+        buf = self._bufs.get(key)
+        if buf is None or buf.numel() < nbytes:
+            buf = torch.empty(nbytes + (nbytes >> 3), dtype=torch.uint8, device=self.device)
+            self._bufs[key] = buf
+        return buf
+
+
+# ---------------------------------------------------------------------------
+# numpy Generator <-> kg_pcg64
+# ---------------------------------------------------------------------------
+M64 = (1 << 64) - 1
+
+
+def pcg_from_numpy(gen: np.random.Generator) -> KgPcg64:
+    st = gen.bit_generator.state
+    if st.get("bit_generator") != "PCG64":
+        raise KGError("sampler streams require a numpy PCG64 Generator (np.random.default_rng)")
+    s, inc = st["state"]["state"], st["state"]["inc"]
+    return KgPcg64(s >> 64, s & M64, inc >> 64, inc & M64, st["has_uint32"], st["uinteger"])
+
+
+def pcg_to_numpy(g: KgPcg64, gen: np.random.Generator) -> None:
+    gen.bit_generator.state = {
+        "bit_generator": "PCG64",
+        "state": {"state": (g.state_hi << 64) | g.state_lo, "inc": (g.inc_hi << 64) | g.inc_lo},
+        "has_uint32": int(g.has_uint32), "uinteger": int(g.uinteger)}
+
+
+def pcg_copy(g: KgPcg64) -> KgPcg64:
+    return KgPcg64(g.state_hi, g.state_lo, g.inc_hi, g.inc_lo, g.has_uint32, g.uinteger)
+
+
+def pcg_advance(g: KgPcg64, delta: int) -> None:
+    load().kg_pcg64_advance(ctypes.byref(g), c_uint64(delta))
+
+
+def pcg_consume32(g: KgPcg64, count: int) -> None:
+    load().kg_pcg64_consume32(ctypes.byref(g), c_uint64(count))

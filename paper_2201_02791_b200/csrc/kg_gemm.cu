@@ -1,0 +1,158 @@
+// Dense contractions of the basis-factored RGCN layer (fp32, CUDA cores).
+//
+//   NN  C[p, :] = A[row(p), :] . B          rows gathered by an index list,
+//       output rows scattered (row ids), optional ReLU, M read from device
+//   TN  P_z[i, j] = sum_{p in split z} A[row(p), i] * Bm[p, j]   (split-K)
+//       followed by a fixed-order reduction over z (deterministic)
+//
+// These are the shapes X.V_b / acc.[V_0;..;V_{B-1}] / dS.V^T / X^T.dS of the
+// factored layer; K = B*d <= 512, N <= 512.
+#include "kg_gemm.cuh"
+
+namespace kg {
+
+constexpr int BM = 64, BN = 64, BK = 16, GT = 256;
+
+template <bool TRANS_A>
+__global__ void __launch_bounds__(GT) k_gemm(GemmArgs g) {
+  __shared__ float As[BK][BM + 4];
+  __shared__ float Bs[BK][BN + 4];
+  const int tid = threadIdx.x;
+  const int tx = tid % 16, ty = tid / 16;   // 16x16 threads, 4x4 outputs each
+  const int64_t M = g.M_dev ? (int64_t)g.M_dev[g.M_dev_index] : g.M;
+  const int64_t m0 = (int64_t)blockIdx.y * BM;
+  const int64_t n0 = (int64_t)blockIdx.x * BN;
+  // NN: M rows of output, reduce over K. TN: output rows = K_out (g.K), reduce over M rows.
+  const int64_t out_rows = TRANS_A ? g.K : M;
+  if (m0 >= out_rows) return;
+  int64_t k_lo = 0, k_hi = TRANS_A ? M : g.K;
+  if (TRANS_A) {
+    int64_t per = (M + gridDim.z - 1) / gridDim.z;
+    per = (per + BK - 1) / BK * BK;
+    k_lo = (int64_t)blockIdx.z * per;
+    k_hi = k_lo + per < M ? k_lo + per : M;
+  }
+  float acc[4][4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) acc[i][j] = 0.f;
+
+  for (int64_t k0 = k_lo; k0 < k_hi; k0 += BK) {
+    // load A tile (BM x BK) into As[k][m]
+    for (int idx = tid; idx < BM * BK; idx += GT) {
+      int mm, kk;
+      float v = 0.f;
+      if (!TRANS_A) {
+        kk = idx % BK;
+        mm = idx / BK;
+        int64_t m = m0 + mm, k = k0 + kk;
+        if (m < M && k < k_hi) {
+          int64_t row = g.a_rows ? g.a_rows[m] : m;
+          v = g.A[row * g.lda + k];
+        }
+      } else {
+        mm = idx % BM;
+        kk = idx / BM;
+        int64_t m = m0 + mm, k = k0 + kk;   // m = output row (feature), k = data row
+        if (m < g.K && k < k_hi) {
+          int64_t row = g.a_rows ? g.a_rows[k] : k;
+          v = g.A[row * g.lda + m];
+        }
+      }
+      As[kk][mm] = v;
+    }
+    for (int idx = tid; idx < BK * BN; idx += GT) {
+      int nn = idx % BN, kk = idx / BN;
+      int64_t k = k0 + kk, n = n0 + nn;
+      float v = 0.f;
+      if (k < k_hi && n < g.N) v = g.B[k * g.ldb + n];
+      Bs[kk][nn] = v;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int kk = 0; kk < BK; ++kk) {
+      float a[4], b[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) a[i] = As[kk][ty * 4 + i];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) b[j] = Bs[kk][tx * 4 + j];
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) acc[i][j] = fmaf(a[i], b[j], acc[i][j]);
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    int64_t m = m0 + ty * 4 + i;
+    if (m >= out_rows) continue;
+    if (!TRANS_A) {
+      int64_t row = g.c_rows ? g.c_rows[m] : m;
+      float* crow = g.C + row * g.ldc;
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        int64_t n = n0 + tx * 4 + j;
+        if (n < g.N) {
+          float v = acc[i][j];
+          if (g.relu) v = fmaxf(v, 0.f);
+          crow[n] = v;
+        }
+      }
+    } else {
+      float* crow = g.C + ((int64_t)blockIdx.z * g.K + m) * g.ldc;
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        int64_t n = n0 + tx * 4 + j;
+        if (n < g.N) crow[n] = acc[i][j];
+      }
+    }
+  }
+}
+
+// out[i] = sum_z part[z][i] (fixed order), i < count
+__global__ void k_reduce_splits(const float* __restrict__ part, int splits, int64_t count, float* __restrict__ out) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < count; i += (int64_t)gridDim.x * blockDim.x) {
+    float s = 0.f;
+    for (int z = 0; z < splits; ++z) s += part[(int64_t)z * count + i];
+    out[i] = s;
+  }
+}
+
+kg_status gemm_nn(const GemmArgs& g, cudaStream_t st) {
+  if (g.M_max <= 0 || g.N <= 0) return KG_OK;
+  dim3 grid((unsigned)ceil_div(g.N, BN), (unsigned)ceil_div(g.M_max, BM), 1);
+  k_gemm<false><<<grid, GT, 0, st>>>(g);
+  KG_CHECK_LAUNCH("k_gemm<nn>");
+  return KG_OK;
+}
+
+int tn_splits(int64_t rows_max) {
+  int64_t s = ceil_div(rows_max, 512);
+  int64_t cap = num_sms() * 2;
+  if (s > cap) s = cap;
+  if (s < 1) s = 1;
+  return (int)s;
+}
+
+size_t gemm_tn_workspace(int64_t rows_max, int64_t K, int64_t N) {
+  return align_up((size_t)tn_splits(rows_max) * K * N * sizeof(float));
+}
+
+kg_status gemm_tn(const GemmArgs& g, float* out, void* ws, cudaStream_t st) {
+  // g.K = output rows (features), g.N = output cols, g.M / M_dev = data rows
+  int splits = tn_splits(g.M_max);
+  GemmArgs h = g;
+  h.C = static_cast<float*>(ws);
+  h.ldc = g.N;
+  dim3 grid((unsigned)ceil_div(g.N, BN), (unsigned)ceil_div(g.K, BM), (unsigned)splits);
+  k_gemm<true><<<grid, GT, 0, st>>>(h);
+  KG_CHECK_LAUNCH("k_gemm<tn>");
+  int64_t cnt = g.K * g.N;
+  k_reduce_splits<<<persistent_blocks(cnt, 256, 4), 256, 0, st>>>(h.C, splits, cnt, out);
+  KG_CHECK_LAUNCH("k_reduce_splits");
+  return KG_OK;
+}
+
+}  // namespace kg

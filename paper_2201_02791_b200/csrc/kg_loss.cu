@@ -1,0 +1,325 @@
+// R16-R18: DistMult scoring fused with the BCE loss and its gradient
+// (ref:model.py:238-281).
+//
+//   g_i   = sum_k H[h_i,k] m[r_i,k] H[t_i,k]
+//   loss  = mean(softplus(g) - y g)          (deterministic two-level sum)
+//   dg_i  = (sigmoid(g_i) - y_i) / b
+//   d m_r = sum_{i: r_i = r} dg_i H[h_i] * H[t_i]
+//   dH_v  = sum_{i: h_i = v} dg_i m_{r_i} * H[t_i] + sum_{i: t_i = v} dg_i m_{r_i} * H[h_i]
+//
+// The two scatters are done without atomics: the batch's relation ids and
+// endpoint ids are stable-radix-sorted once, every group is cut into
+// sub-chunks of CH rows summed by one warp each, and a second pass adds the
+// sub-chunk partials of a group in order (hub rows get many warps, fixed
+// summation order -> bitwise reproducible).
+#include "kg_common.cuh"
+
+namespace kg {
+
+constexpr int CH = 64;
+
+struct LossArgs {
+  const float* H;
+  int d;
+  const float* dec;
+  const int32_t* tri;
+  const float* labels;
+  int64_t total, start, b;
+  float* dg;
+  float* per;
+  float* scores;
+  uint32_t* flags;
+};
+
+__device__ __forceinline__ int64_t row_of(const LossArgs& a, int64_t i) { return (a.start + i) % a.total; }
+
+__global__ void __launch_bounds__(256) k_score(LossArgs a) {
+  const int lane = lane_id();
+  const int warps = (gridDim.x * blockDim.x) >> 5;
+  for (int64_t i = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; i < a.b; i += warps) {
+    int64_t row = row_of(a, i);
+    int32_t h = a.tri[row * 3], r = a.tri[row * 3 + 1], t = a.tri[row * 3 + 2];
+    const float* Hh = a.H + (int64_t)h * a.d;
+    const float* Ht = a.H + (int64_t)t * a.d;
+    const float* M = a.dec + (int64_t)r * a.d;
+    float s = 0.f;
+    for (int k = lane; k < a.d; k += 32) s = fmaf(Hh[k] * M[k], Ht[k], s);
+    s = warp_sum(s);
+    if (lane == 0) {
+      float y = a.labels[row];
+      if (!isfinite(s)) atomicOr(a.flags, KG_FLAG_NONFINITE_SCORE);
+      float sp = fmaxf(s, 0.f) + log1pf(expf(-fabsf(s)));   // softplus = logaddexp(0, g)
+      a.per[i] = sp - y * s;
+      float sig = 1.f / (1.f + expf(-s));
+      a.dg[i] = (sig - y) / (float)a.b;
+      if (a.scores) a.scores[i] = s;
+    }
+  }
+}
+
+// deterministic mean: per-block partial (fixed order), then single-block final
+__global__ void k_block_sums(const float* __restrict__ x, int64_t n, double* __restrict__ part) {
+  __shared__ double red[256];
+  double s = 0.0;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) s += x[i];
+  red[threadIdx.x] = s;
+  __syncthreads();
+  for (int w = 128; w > 0; w >>= 1) {
+    if (threadIdx.x < w) red[threadIdx.x] += red[threadIdx.x + w];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) part[blockIdx.x] = red[0];
+}
+
+__global__ void k_final_mean(const double* __restrict__ part, int nb, int64_t n, float* __restrict__ out,
+                             uint32_t* __restrict__ flags) {
+  __shared__ double red[256];
+  double s = 0.0;
+  for (int i = threadIdx.x; i < nb; i += blockDim.x) s += part[i];
+  red[threadIdx.x] = s;
+  __syncthreads();
+  for (int w = 128; w > 0; w >>= 1) {
+    if (threadIdx.x < w) red[threadIdx.x] += red[threadIdx.x + w];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    double m = red[0] / (double)n;
+    *out = (float)m;
+    if (!isfinite(m)) atomicOr(flags, KG_FLAG_NONFINITE_LOSS);
+  }
+}
+
+// sort keys: relation ids (b) and endpoint ids (2b, occurrence o<b head, o>=b tail)
+__global__ void k_loss_keys(LossArgs a, uint32_t* __restrict__ rk, uint32_t* __restrict__ rv,
+                            uint32_t* __restrict__ vk, uint32_t* __restrict__ vv) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < a.b; i += (int64_t)gridDim.x * blockDim.x) {
+    int64_t row = row_of(a, i);
+    rk[i] = (uint32_t)a.tri[row * 3 + 1];
+    rv[i] = (uint32_t)i;
+    vk[i] = (uint32_t)a.tri[row * 3];
+    vv[i] = (uint32_t)i;
+    vk[a.b + i] = (uint32_t)a.tri[row * 3 + 2];
+    vv[a.b + i] = (uint32_t)(a.b + i);
+  }
+}
+
+__device__ __forceinline__ int64_t lower_bound_u32(const uint32_t* __restrict__ k, int64_t n, uint32_t x) {
+  int64_t lo = 0, hi = n;
+  while (lo < hi) {
+    int64_t mid = (lo + hi) >> 1;
+    if (k[mid] < x) lo = mid + 1;
+    else hi = mid;
+  }
+  return lo;
+}
+
+// group g has key gkey(g) = ids ? ids[g] : g ; bounds into the sorted keys
+__global__ void k_group_bounds(const uint32_t* __restrict__ keys, int64_t n, const int32_t* __restrict__ ids,
+                               const int32_t* __restrict__ ng_dev, int32_t ng_host, int32_t* __restrict__ lo,
+                               uint32_t* __restrict__ nsub) {
+  const int32_t ng = ng_dev ? *ng_dev : ng_host;
+  for (int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; g < ng; g += (int64_t)gridDim.x * blockDim.x) {
+    uint32_t key = ids ? (uint32_t)ids[g] : (uint32_t)g;
+    int64_t a = lower_bound_u32(keys, n, key);
+    int64_t e = lower_bound_u32(keys, n, key + 1);
+    lo[g] = (int32_t)a;
+    nsub[g] = (uint32_t)((e - a + CH - 1) / CH);
+  }
+}
+
+__global__ void k_group_len(const uint32_t* __restrict__ keys, int64_t n, const int32_t* __restrict__ ids,
+                            const int32_t* __restrict__ ng_dev, int32_t ng_host, int32_t* __restrict__ hi) {
+  const int32_t ng = ng_dev ? *ng_dev : ng_host;
+  for (int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; g < ng; g += (int64_t)gridDim.x * blockDim.x) {
+    uint32_t key = ids ? (uint32_t)ids[g] : (uint32_t)g;
+    hi[g] = (int32_t)lower_bound_u32(keys, n, key + 1);
+  }
+}
+
+// kind 0: d_dec rows (value = triple index); kind 1: dH rows (value = occurrence)
+template <int KIND>
+__global__ void __launch_bounds__(256) k_sub_partials(LossArgs a, const uint32_t* __restrict__ vals,
+                                                      const int32_t* __restrict__ lo, const int32_t* __restrict__ hi,
+                                                      const uint32_t* __restrict__ sub_start,
+                                                      const uint32_t* __restrict__ total_sub,
+                                                      const int32_t* __restrict__ ng_dev, int32_t ng_host,
+                                                      float* __restrict__ partial) {
+  const int32_t ng = ng_dev ? *ng_dev : ng_host;
+  const uint32_t S = *total_sub;
+  const int lane = lane_id();
+  const int warps = (gridDim.x * blockDim.x) >> 5;
+  for (int64_t s = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; s < S; s += warps) {
+    // group = last g with sub_start[g] <= s
+    int32_t l = 0, h = ng;
+    while (h - l > 1) {
+      int32_t mid = (l + h) >> 1;
+      if (sub_start[mid] <= s) l = mid;
+      else h = mid;
+    }
+    const int32_t g = l;
+    int64_t r0 = lo[g] + (int64_t)(s - sub_start[g]) * CH;
+    int64_t r1 = r0 + CH < hi[g] ? r0 + CH : hi[g];
+    float* out = partial + s * (int64_t)a.d;
+    for (int k0 = 0; k0 < a.d; k0 += 32) {
+      int k = k0 + lane;
+      float acc = 0.f;
+      if (k < a.d) {
+        for (int64_t j = r0; j < r1; ++j) {
+          uint32_t v = vals[j];
+          int64_t ti = (KIND == 1 && v >= a.b) ? v - a.b : v;
+          int64_t row = row_of(a, ti);
+          int32_t hh = a.tri[row * 3], rr = a.tri[row * 3 + 1], tt = a.tri[row * 3 + 2];
+          float dg = a.dg[ti];
+          float x;
+          if (KIND == 0) {
+            x = a.H[(int64_t)hh * a.d + k] * a.H[(int64_t)tt * a.d + k];
+          } else {
+            int32_t other = (v >= a.b) ? hh : tt;
+            x = a.dec[(int64_t)rr * a.d + k] * a.H[(int64_t)other * a.d + k];
+          }
+          acc = fmaf(dg, x, acc);
+        }
+        out[k] = acc;
+      }
+    }
+  }
+}
+
+__global__ void k_group_finish(const float* __restrict__ partial, const uint32_t* __restrict__ sub_start,
+                               const uint32_t* __restrict__ nsub, const int32_t* __restrict__ ids,
+                               const int32_t* __restrict__ ng_dev, int32_t ng_host, int d, float* __restrict__ out) {
+  const int32_t ng = ng_dev ? *ng_dev : ng_host;
+  const int64_t total = (int64_t)ng * d;
+  for (int64_t x = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; x < total; x += (int64_t)gridDim.x * blockDim.x) {
+    int64_t g = x / d;
+    int k = (int)(x - g * d);
+    float s = 0.f;
+    uint32_t a0 = sub_start[g], n0 = nsub[g];
+    for (uint32_t j = 0; j < n0; ++j) s += partial[(int64_t)(a0 + j) * d + k];
+    int64_t row = ids ? ids[g] : g;
+    out[row * d + k] = s;
+  }
+}
+
+struct SegWs {
+  int32_t* lo;
+  int32_t* hi;
+  uint32_t* nsub;
+  uint32_t* sub_start;
+  uint32_t* total;
+  float* partial;
+  char* scan;
+};
+
+static size_t seg_ws(int64_t nelem, int64_t ngroups, int d, SegWs* w, Arena& a) {
+  SegWs s;
+  s.lo = a.take<int32_t>(ngroups + 1);
+  s.hi = a.take<int32_t>(ngroups + 1);
+  s.nsub = a.take<uint32_t>(ngroups + 1);
+  s.sub_start = a.take<uint32_t>(ngroups + 1);
+  s.total = a.take<uint32_t>(4);
+  s.partial = a.take<float>((size_t)(nelem / CH + ngroups + 1) * d);
+  s.scan = a.take<char>(scan_workspace(ngroups + 1));
+  if (w) *w = s;
+  return a.used;
+}
+
+template <int KIND>
+static kg_status seg_reduce(const LossArgs& la, const uint32_t* keys, const uint32_t* vals, int64_t nelem,
+                            const int32_t* ids, const int32_t* ng_dev, int32_t ng_max, float* out, SegWs& w,
+                            cudaStream_t st) {
+  int gb = persistent_blocks(ng_max, 256, 8);
+  k_group_bounds<<<gb, 256, 0, st>>>(keys, nelem, ids, ng_dev, ng_max, w.lo, w.nsub);
+  k_group_len<<<gb, 256, 0, st>>>(keys, nelem, ids, ng_dev, ng_max, w.hi);
+  KG_CHECK_LAUNCH("group bounds");
+  // with a device-resident group count the caller zeroed nsub[0:ng_max] so the
+  // scan sees 0 beyond *ng_dev
+  kg_status s = exclusive_scan_u32(w.nsub, w.sub_start, ng_max, w.total, w.scan, scan_workspace(ng_max + 1), st);
+  if (s != KG_OK) return s;
+  int64_t max_sub = nelem / CH + ng_max + 1;
+  k_sub_partials<KIND><<<persistent_blocks(max_sub * 32, 256, 8), 256, 0, st>>>(la, vals, w.lo, w.hi, w.sub_start,
+                                                                               w.total, ng_dev, ng_max, w.partial);
+  KG_CHECK_LAUNCH("k_sub_partials");
+  k_group_finish<<<persistent_blocks((int64_t)ng_max * la.d, 256, 8), 256, 0, st>>>(w.partial, w.sub_start, w.nsub,
+                                                                                   ids, ng_dev, ng_max, la.d, out);
+  KG_CHECK_LAUNCH("k_group_finish");
+  return KG_OK;
+}
+
+static int bits_for(uint64_t maxval) {
+  int b = 0;
+  while (b < 64 && (maxval >> b) != 0) ++b;
+  return b;
+}
+
+}  // namespace kg
+
+using namespace kg;
+
+extern "C" {
+
+int64_t kg_loss_workspace_bytes(int64_t b, int32_t n, int32_t d, int32_t R) {
+  Arena a(nullptr, 0);
+  a.take<float>(b);          // dg
+  a.take<float>(b);          // per
+  a.take<double>(1024);      // block partials
+  a.take<uint32_t>(b);       // rk
+  a.take<uint32_t>(b);       // rv
+  a.take<uint32_t>(2 * b);   // vk
+  a.take<uint32_t>(2 * b);   // vv
+  a.take<char>(sort32_workspace(2 * b));
+  a.take<uint32_t>(n + 1);   // zero fill for nsub tail (memset range)
+  seg_ws(b, R, d, nullptr, a);
+  seg_ws(2 * b, n, d, nullptr, a);
+  return (int64_t)a.used + 4096;
+}
+
+kg_status kg_distmult_loss(const float* H, int32_t d, int32_t n_local, const float* decoder, int32_t R,
+                           const int32_t* tri,
+                           const float* labels, int64_t total, int64_t start, int64_t b, const int32_t* order,
+                           const int32_t* counts, float* dH, float* d_decoder, float* loss_out, float* scores_out,
+                           uint32_t* flags, void* ws, int64_t ws_bytes, void* stream) {
+  cudaStream_t st = as_stream(stream);
+  KG_REQUIRE(b >= 1 && total >= 1, KG_ERR_VALIDATION, "empty batch");
+  // n (local vertices) bound for seed groups: 2b distinct endpoints at most
+  int64_t ngmax = 2 * b;
+  Arena a(ws, (size_t)ws_bytes);
+  float* dg = a.take<float>(b);
+  float* per = a.take<float>(b);
+  double* part = a.take<double>(1024);
+  uint32_t* rk = a.take<uint32_t>(b);
+  uint32_t* rv = a.take<uint32_t>(b);
+  uint32_t* vk = a.take<uint32_t>(2 * b);
+  uint32_t* vv = a.take<uint32_t>(2 * b);
+  char* sws = a.take<char>(sort32_workspace(2 * b));
+  a.take<uint32_t>(ngmax + 1);
+  SegWs wr, wv;
+  seg_ws(b, R, d, &wr, a);
+  seg_ws(2 * b, ngmax, d, &wv, a);
+  KG_REQUIRE(a.used <= (size_t)ws_bytes && dg != nullptr, KG_ERR_VALIDATION, "loss workspace too small");
+
+  LossArgs la{H, d, decoder, tri, labels, total, start, b, dg, per, scores_out, flags};
+  k_score<<<persistent_blocks(b * 32, 256, 8), 256, 0, st>>>(la);
+  KG_CHECK_LAUNCH("k_score");
+  int nb = persistent_blocks(b, 256, 4);
+  if (nb > 1024) nb = 1024;
+  k_block_sums<<<nb, 256, 0, st>>>(per, b, part);
+  k_final_mean<<<1, 256, 0, st>>>(part, nb, b, loss_out, flags);
+  KG_CHECK_LAUNCH("loss mean");
+
+  k_loss_keys<<<persistent_blocks(b, 256, 8), 256, 0, st>>>(la, rk, rv, vk, vv);
+  KG_CHECK_LAUNCH("k_loss_keys");
+  kg_status s = sort_pairs_u32(rk, rv, b, bits_for((uint64_t)R), sws, sort32_workspace(2 * b), st);
+  if (s != KG_OK) return s;
+  s = sort_pairs_u32(vk, vv, 2 * b, bits_for((uint64_t)n_local), sws, sort32_workspace(2 * b), st);
+  if (s != KG_OK) return s;
+  KG_CUDA(cudaMemsetAsync(wr.nsub, 0, (R + 1) * sizeof(uint32_t), st));
+  KG_CUDA(cudaMemsetAsync(wv.nsub, 0, (ngmax + 1) * sizeof(uint32_t), st));
+  s = seg_reduce<0>(la, rk, rv, b, nullptr, nullptr, R, d_decoder, wr, st);
+  if (s != KG_OK) return s;
+  // seed groups: A_0 = order[0:counts[0]] (ascending, exactly the distinct endpoints)
+  s = seg_reduce<1>(la, vk, vv, 2 * b, order, counts, (int32_t)ngmax, dH, wv, st);
+  return s;
+}
+
+}  // extern "C"

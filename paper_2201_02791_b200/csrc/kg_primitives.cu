@@ -1,0 +1,347 @@
+// Device-wide primitives used by the view builder, the sampler and the
+// per-batch grouping: exclusive scan, stable LSD radix sort, flag compaction.
+//
+// Radix sort: 8-bit digits, tiles of 4096 keys (256 threads x 16 rounds).
+// Per pass: (1) per-tile digit histogram, (2) one exclusive scan over the
+// digit-major [256 x tiles] histogram, (3) stable scatter — inside a tile the
+// rank of a key among equal digits is built round by round from warp
+// match_any groups plus an ordered per-warp prefix, so the sort is stable
+// (the reference's np.argsort(kind="stable") order, sampler.py:91).
+#include "kg_common.cuh"
+
+#include <stdarg.h>
+#include <string.h>
+
+namespace kg {
+
+static thread_local char g_last_error[512] = "";
+
+void set_error(const char* fmt, ...) {
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(g_last_error, sizeof(g_last_error), fmt, ap);
+  va_end(ap);
+}
+
+kg_status from_cuda(cudaError_t e, const char* where) {
+  set_error("CUDA error %s at %s", cudaGetErrorString(e), where);
+  return KG_ERR_CUDA;
+}
+
+int num_sms() {
+  static int cached = 0;
+  if (cached == 0) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&cached, cudaDevAttrMultiProcessorCount, dev);
+    if (cached <= 0) cached = 148;
+  }
+  return cached;
+}
+
+// ---------------------------------------------------------------------------
+// Exclusive scan (uint32)
+// ---------------------------------------------------------------------------
+constexpr int SCAN_THREADS = 512;
+constexpr int SCAN_ITEMS = 8;
+constexpr int SCAN_TILE = SCAN_THREADS * SCAN_ITEMS;
+
+// Block-wide exclusive scan of SCAN_TILE values held in smem `s` (in place);
+// returns the tile total to every thread.
+__device__ uint32_t block_scan_tile(uint32_t* s) {
+  __shared__ uint32_t warp_tot[SCAN_THREADS / 32];
+  const int t = threadIdx.x;
+  uint32_t v[SCAN_ITEMS];
+  uint32_t run = 0;
+#pragma unroll
+  for (int j = 0; j < SCAN_ITEMS; ++j) {
+    v[j] = run;
+    run += s[t * SCAN_ITEMS + j];
+  }
+  // warp inclusive scan of per-thread totals
+  uint32_t inc = run;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    uint32_t y = __shfl_up_sync(0xffffffffu, inc, o);
+    if ((t & 31) >= o) inc += y;
+  }
+  if ((t & 31) == 31) warp_tot[t >> 5] = inc;
+  __syncthreads();
+  if (t < 32) {
+    uint32_t w = (t < SCAN_THREADS / 32) ? warp_tot[t] : 0;
+    uint32_t wi = w;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      uint32_t y = __shfl_up_sync(0xffffffffu, wi, o);
+      if (t >= o) wi += y;
+    }
+    if (t < SCAN_THREADS / 32) warp_tot[t] = wi - w;   // exclusive warp offsets
+    if (t == SCAN_THREADS / 32 - 1) warp_tot[SCAN_THREADS / 32 - 1 + 0] = wi - w;
+    __syncwarp();
+  }
+  __syncthreads();
+  uint32_t base = warp_tot[t >> 5] + (inc - run);
+#pragma unroll
+  for (int j = 0; j < SCAN_ITEMS; ++j) s[t * SCAN_ITEMS + j] = base + v[j];
+  __syncthreads();
+  // total = last element exclusive + its value is not kept; recompute from last thread
+  __shared__ uint32_t total;
+  if (t == SCAN_THREADS - 1) total = base + run;
+  __syncthreads();
+  return total;
+}
+
+__global__ void scan_tile_sums(const uint32_t* __restrict__ in, int64_t n, uint32_t* __restrict__ sums) {
+  __shared__ uint32_t s[SCAN_TILE];
+  int64_t base = (int64_t)blockIdx.x * SCAN_TILE;
+  for (int j = threadIdx.x; j < SCAN_TILE; j += SCAN_THREADS) {
+    int64_t i = base + j;
+    s[j] = i < n ? in[i] : 0u;
+  }
+  __syncthreads();
+  uint32_t tot = block_scan_tile(s);
+  if (threadIdx.x == 0) sums[blockIdx.x] = tot;
+}
+
+__global__ void scan_tiles_apply(const uint32_t* __restrict__ in, uint32_t* __restrict__ out, int64_t n,
+                                 const uint32_t* __restrict__ tile_off, uint32_t* total) {
+  __shared__ uint32_t s[SCAN_TILE];
+  int64_t base = (int64_t)blockIdx.x * SCAN_TILE;
+  for (int j = threadIdx.x; j < SCAN_TILE; j += SCAN_THREADS) {
+    int64_t i = base + j;
+    s[j] = i < n ? in[i] : 0u;
+  }
+  __syncthreads();
+  uint32_t tot = block_scan_tile(s);
+  uint32_t off = tile_off ? tile_off[blockIdx.x] : 0u;
+  for (int j = threadIdx.x; j < SCAN_TILE; j += SCAN_THREADS) {
+    int64_t i = base + j;
+    if (i < n) out[i] = s[j] + off;
+  }
+  if (total && blockIdx.x == gridDim.x - 1 && threadIdx.x == 0) *total = off + tot;
+}
+
+size_t scan_workspace(int64_t n) {
+  size_t bytes = 0;
+  int64_t m = n;
+  while (m > SCAN_TILE) {
+    int64_t tiles = ceil_div(m, SCAN_TILE);
+    bytes += align_up(tiles * sizeof(uint32_t));
+    m = tiles;
+  }
+  return bytes + 256;
+}
+
+kg_status exclusive_scan_u32(const uint32_t* in, uint32_t* out, int64_t n, uint32_t* total, void* ws,
+                             size_t ws_bytes, cudaStream_t st) {
+  if (n <= 0) {
+    if (total) KG_CUDA(cudaMemsetAsync(total, 0, sizeof(uint32_t), st));
+    return KG_OK;
+  }
+  if (n <= SCAN_TILE) {
+    scan_tiles_apply<<<1, SCAN_THREADS, 0, st>>>(in, out, n, nullptr, total);
+    KG_CHECK_LAUNCH("scan_tiles_apply");
+    return KG_OK;
+  }
+  KG_REQUIRE(ws_bytes >= scan_workspace(n), KG_ERR_VALIDATION, "scan workspace too small");
+  int64_t tiles = ceil_div(n, SCAN_TILE);
+  uint32_t* sums = static_cast<uint32_t*>(ws);
+  char* rest = static_cast<char*>(ws) + align_up(tiles * sizeof(uint32_t));
+  scan_tile_sums<<<(unsigned)tiles, SCAN_THREADS, 0, st>>>(in, n, sums);
+  KG_CHECK_LAUNCH("scan_tile_sums");
+  kg_status s = exclusive_scan_u32(sums, sums, tiles, nullptr, rest,
+                                   ws_bytes - align_up(tiles * sizeof(uint32_t)), st);
+  if (s != KG_OK) return s;
+  scan_tiles_apply<<<(unsigned)tiles, SCAN_THREADS, 0, st>>>(in, out, n, sums, total);
+  KG_CHECK_LAUNCH("scan_tiles_apply");
+  return KG_OK;
+}
+
+// ---------------------------------------------------------------------------
+// Stable LSD radix sort
+// ---------------------------------------------------------------------------
+constexpr int RS_THREADS = 256;
+constexpr int RS_ROUNDS = 16;
+constexpr int RS_TILE = RS_THREADS * RS_ROUNDS;
+constexpr int RS_WARPS = RS_THREADS / 32;
+
+template <typename K>
+__global__ void __launch_bounds__(RS_THREADS) radix_hist(const K* __restrict__ keys, int64_t n, int shift,
+                                                          uint32_t* __restrict__ hist, int64_t tiles) {
+  __shared__ uint32_t cnt[256];
+  cnt[threadIdx.x] = 0;
+  __syncthreads();
+  int64_t base = (int64_t)blockIdx.x * RS_TILE;
+#pragma unroll 4
+  for (int j = 0; j < RS_ROUNDS; ++j) {
+    int64_t i = base + j * RS_THREADS + threadIdx.x;
+    if (i < n) atomicAdd(&cnt[(unsigned)(keys[i] >> shift) & 255u], 1u);
+  }
+  __syncthreads();
+  hist[(int64_t)threadIdx.x * tiles + blockIdx.x] = cnt[threadIdx.x];
+}
+
+template <typename K>
+__global__ void __launch_bounds__(RS_THREADS) radix_scatter(const K* __restrict__ kin, const uint32_t* __restrict__ vin,
+                                                             K* __restrict__ kout, uint32_t* __restrict__ vout,
+                                                             int64_t n, int shift,
+                                                             const uint32_t* __restrict__ offs, int64_t tiles) {
+  __shared__ uint32_t base[256];
+  __shared__ uint32_t wcnt[RS_WARPS][256];
+  __shared__ uint32_t woff[RS_WARPS][256];
+  const int t = threadIdx.x, w = t >> 5;
+  base[t] = offs[(int64_t)t * tiles + blockIdx.x];
+#pragma unroll
+  for (int q = 0; q < RS_WARPS; ++q) wcnt[q][t] = 0;
+  __syncthreads();
+  int64_t tile0 = (int64_t)blockIdx.x * RS_TILE;
+  for (int j = 0; j < RS_ROUNDS; ++j) {
+    int64_t i = tile0 + j * RS_THREADS + t;
+    bool valid = i < n;
+    K key = valid ? kin[i] : K(0);
+    uint32_t val = valid ? vin[i] : 0u;
+    unsigned d = valid ? ((unsigned)(key >> shift) & 255u) : 256u;
+    unsigned peers = __match_any_sync(0xffffffffu, d);
+    unsigned rank = __popc(peers & lanemask_lt());
+    bool leader = (__ffs(peers) - 1) == (int)lane_id();
+    if (leader && valid) wcnt[w][d] = __popc(peers);
+    __syncthreads();
+    {
+      uint32_t run = base[t];
+#pragma unroll
+      for (int q = 0; q < RS_WARPS; ++q) {
+        uint32_t c = wcnt[q][t];
+        woff[q][t] = run;
+        run += c;
+        wcnt[q][t] = 0;
+      }
+      base[t] = run;
+    }
+    __syncthreads();
+    if (valid) {
+      uint32_t dst = woff[w][d] + rank;
+      kout[dst] = key;
+      vout[dst] = val;
+    }
+  }
+}
+
+template <typename K>
+static size_t sort_ws_bytes(int64_t n) {
+  int64_t tiles = ceil_div(n > 0 ? n : 1, RS_TILE);
+  int64_t hist = tiles * 256;
+  return align_up(n * sizeof(K)) + align_up(n * sizeof(uint32_t)) + align_up(hist * sizeof(uint32_t)) +
+         scan_workspace(hist) + 1024;
+}
+
+size_t sort_workspace(int64_t n) { return sort_ws_bytes<uint64_t>(n); }
+size_t sort32_workspace(int64_t n) { return sort_ws_bytes<uint32_t>(n); }
+
+template <typename K>
+static kg_status sort_pairs(K* keys, uint32_t* vals, int64_t n, int key_bits, void* ws, size_t ws_bytes,
+                            cudaStream_t st) {
+  if (n <= 1 || key_bits <= 0) return KG_OK;
+  KG_REQUIRE(ws_bytes >= sort_ws_bytes<K>(n), KG_ERR_VALIDATION, "sort workspace too small");
+  KG_REQUIRE(n < (int64_t(1) << 32), KG_ERR_VALIDATION, "sort supports < 2^32 items");
+  int64_t tiles = ceil_div(n, RS_TILE);
+  int64_t hist_n = tiles * 256;
+  Arena a(ws, ws_bytes);
+  K* k2 = a.take<K>(n);
+  uint32_t* v2 = a.take<uint32_t>(n);
+  uint32_t* hist = a.take<uint32_t>(hist_n);
+  char* scan_ws = a.take<char>(scan_workspace(hist_n));
+  int passes = (key_bits + 7) / 8;
+  K* ka = keys;
+  uint32_t* va = vals;
+  K* kb = k2;
+  uint32_t* vb = v2;
+  for (int p = 0; p < passes; ++p) {
+    int shift = 8 * p;
+    radix_hist<K><<<(unsigned)tiles, RS_THREADS, 0, st>>>(ka, n, shift, hist, tiles);
+    KG_CHECK_LAUNCH("radix_hist");
+    kg_status s = exclusive_scan_u32(hist, hist, hist_n, nullptr, scan_ws, scan_workspace(hist_n), st);
+    if (s != KG_OK) return s;
+    radix_scatter<K><<<(unsigned)tiles, RS_THREADS, 0, st>>>(ka, va, kb, vb, n, shift, hist, tiles);
+    KG_CHECK_LAUNCH("radix_scatter");
+    K* tk = ka; ka = kb; kb = tk;
+    uint32_t* tv = va; va = vb; vb = tv;
+  }
+  if (ka != keys) {
+    KG_CUDA(cudaMemcpyAsync(keys, ka, n * sizeof(K), cudaMemcpyDeviceToDevice, st));
+    KG_CUDA(cudaMemcpyAsync(vals, va, n * sizeof(uint32_t), cudaMemcpyDeviceToDevice, st));
+  }
+  return KG_OK;
+}
+
+kg_status sort_pairs_u64(uint64_t* keys, uint32_t* vals, int64_t n, int key_bits, void* ws, size_t ws_bytes,
+                         cudaStream_t st) {
+  return sort_pairs<uint64_t>(keys, vals, n, key_bits, ws, ws_bytes, st);
+}
+
+kg_status sort_pairs_u32(uint32_t* keys, uint32_t* vals, int64_t n, int key_bits, void* ws, size_t ws_bytes,
+                         cudaStream_t st) {
+  return sort_pairs<uint32_t>(keys, vals, n, key_bits > 32 ? 32 : key_bits, ws, ws_bytes, st);
+}
+
+// ---------------------------------------------------------------------------
+// Flag compaction: out[off + rank(i)] = i for flagged i, ascending.
+// ---------------------------------------------------------------------------
+__global__ void compact_scatter(const uint32_t* __restrict__ flags, const uint32_t* __restrict__ pos, int64_t n,
+                                int32_t* __restrict__ out, int32_t off_c, const int32_t* __restrict__ off_d,
+                                const uint32_t* __restrict__ total, int32_t* __restrict__ count_out) {
+  int32_t off = off_c + (off_d ? *off_d : 0);
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    if (flags[i]) out[off + pos[i]] = (int32_t)i;
+  }
+  if (count_out && blockIdx.x == 0 && threadIdx.x == 0) *count_out = (int32_t)*total;
+}
+
+size_t compact_workspace(int64_t n) { return align_up(n * sizeof(uint32_t)) + 256 + scan_workspace(n) + 256; }
+
+kg_status compact_flags(const uint32_t* flags, int64_t n, int32_t* out, int32_t* count_out, int32_t off_c,
+                        const int32_t* off_d, void* ws, size_t ws_bytes, cudaStream_t st) {
+  KG_REQUIRE(ws_bytes >= compact_workspace(n), KG_ERR_VALIDATION, "compact workspace too small");
+  Arena a(ws, ws_bytes);
+  uint32_t* pos = a.take<uint32_t>(n);
+  uint32_t* total = a.take<uint32_t>(1);
+  char* sws = a.take<char>(scan_workspace(n));
+  kg_status s = exclusive_scan_u32(flags, pos, n, total, sws, scan_workspace(n), st);
+  if (s != KG_OK) return s;
+  int blocks = persistent_blocks(n, 256, 8);
+  compact_scatter<<<blocks, 256, 0, st>>>(flags, pos, n, out, off_c, off_d, total, count_out);
+  KG_CHECK_LAUNCH("compact_scatter");
+  return KG_OK;
+}
+
+}  // namespace kg
+
+// ---------------------------------------------------------------------------
+// C ABI
+// ---------------------------------------------------------------------------
+extern "C" {
+
+int kg_abi_version(void) { return KG_ABI_VERSION; }
+
+int kg_last_error(char* buf, int64_t n) {
+  if (buf && n > 0) {
+    strncpy(buf, kg::g_last_error, (size_t)n - 1);
+    buf[n - 1] = 0;
+  }
+  return (int)strlen(kg::g_last_error);
+}
+
+int64_t kg_sort_workspace_bytes(int64_t n) { return (int64_t)kg::sort_workspace(n); }
+
+kg_status kg_sort_pairs_u64(uint64_t* keys, uint32_t* vals, int64_t n, int key_bits, void* ws, int64_t ws_bytes,
+                            void* stream) {
+  return kg::sort_pairs_u64(keys, vals, n, key_bits, ws, (size_t)ws_bytes, kg::as_stream(stream));
+}
+
+int64_t kg_scan_workspace_bytes(int64_t n) { return (int64_t)kg::scan_workspace(n); }
+
+kg_status kg_exclusive_scan_u32(const uint32_t* in, uint32_t* out, int64_t n, uint32_t* total, void* ws,
+                                int64_t ws_bytes, void* stream) {
+  return kg::exclusive_scan_u32(in, out, n, total, ws, (size_t)ws_bytes, kg::as_stream(stream));
+}
+
+}  // extern "C"

@@ -1,0 +1,564 @@
+// R3-R8: constraint-based negatives, the edge mini-batch stream and the
+// layered closure, all reproducing the reference's numpy index streams
+// bit-for-bit (ref:sampler.py:144-182, 202-232, 320-376).
+#include "kg_common.cuh"
+#include "kg_pcg64.cuh"
+
+namespace kg {
+
+static int grid_for(int64_t n) { return persistent_blocks(n, 256, 8); }
+
+// ---------------------------------------------------------------------------
+// uint32 stream generation (positional): U[p] for p in [0, W) from state g
+// ---------------------------------------------------------------------------
+constexpr int GEN_WORDS = 16;   // next64 words per thread
+
+__global__ void k_gen_u32(kg_pcg64 g, int64_t W, uint32_t* __restrict__ U) {
+  const u128 s0 = state_of(g), inc = inc_of(g);
+  const int64_t off = g.has_uint32 ? 1 : 0;
+  const int64_t nwords = (W - off + 1) / 2 + 1;
+  for (int64_t w0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) * GEN_WORDS; w0 < nwords;
+       w0 += (int64_t)gridDim.x * blockDim.x * GEN_WORDS) {
+    u128 s = apply_jump(pcg_jump((uint64_t)w0, inc), s0);
+    for (int j = 0; j < GEN_WORDS; ++j) {
+      int64_t w = w0 + j;
+      if (w >= nwords) break;
+      s = pcg_step(s, inc);
+      uint64_t x = pcg_output(s);
+      int64_t p = off + 2 * w;
+      if (p < W) U[p] = (uint32_t)x;
+      if (p + 1 < W) U[p + 1] = (uint32_t)(x >> 32);
+    }
+  }
+  if (g.has_uint32 && blockIdx.x == 0 && threadIdx.x == 0 && W > 0) U[0] = g.uinteger;
+}
+
+// ---------------------------------------------------------------------------
+// negatives
+// ---------------------------------------------------------------------------
+constexpr int COIN_PER_THREAD = 16;
+
+__global__ void k_neg_init(const int32_t* __restrict__ core, int64_t m, int32_t s, kg_pcg64 g,
+                           int32_t* __restrict__ neg, int8_t* __restrict__ col, int32_t* __restrict__ pending) {
+  const u128 s0 = state_of(g), inc = inc_of(g);
+  const int64_t total = m * s;
+  for (int64_t i0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) * COIN_PER_THREAD; i0 < total;
+       i0 += (int64_t)gridDim.x * blockDim.x * COIN_PER_THREAD) {
+    u128 st = apply_jump(pcg_jump((uint64_t)i0, inc), s0);
+    for (int j = 0; j < COIN_PER_THREAD; ++j) {
+      int64_t i = i0 + j;
+      if (i >= total) break;
+      st = pcg_step(st, inc);
+      uint64_t x = pcg_output(st);
+      // random() < 0.5  <=>  (x >> 11) * 2^-53 < 0.5  <=>  top bit clear
+      col[i] = (x >> 63) ? 2 : 0;
+      int64_t e = i / s;
+      neg[i * 3 + 0] = core[e * 3 + 0];
+      neg[i * 3 + 1] = core[e * 3 + 1];
+      neg[i * 3 + 2] = core[e * 3 + 2];
+      pending[i] = (int32_t)i;
+    }
+  }
+}
+
+__device__ __forceinline__ bool key_present(const int64_t* __restrict__ keys, int32_t nk, int64_t key) {
+  int32_t lo = 0, hi = nk;
+  while (lo < hi) {
+    int32_t mid = (lo + hi) >> 1;
+    if (keys[mid] < key) lo = mid + 1;
+    else hi = mid;
+  }
+  return lo < nk && keys[lo] == key;
+}
+
+__device__ __forceinline__ int64_t triple_key(int32_t h, int32_t r, int32_t t, int32_t n, int32_t R) {
+  return ((int64_t)h * R + r) * (int64_t)n + t;
+}
+
+__global__ void k_lemire_flags(const uint32_t* __restrict__ U, int64_t W, uint32_t n, uint32_t thr,
+                               uint32_t* __restrict__ flags) {
+  for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < W; p += (int64_t)gridDim.x * blockDim.x) {
+    uint64_t mm = (uint64_t)U[p] * n;
+    flags[p] = ((uint32_t)mm >= thr) ? 1u : 0u;
+  }
+}
+
+__global__ void k_neg_assign(const uint32_t* __restrict__ U, const uint32_t* __restrict__ flags,
+                             const uint32_t* __restrict__ rank, int64_t W, uint32_t n_pool,
+                             const int32_t* __restrict__ pending, int64_t k, int32_t* __restrict__ neg,
+                             const int8_t* __restrict__ col, const int32_t* __restrict__ core, int32_t s,
+                             int32_t n_local, int32_t R, const int64_t* __restrict__ keys,
+                             const int32_t* __restrict__ n_keys, uint32_t* __restrict__ bad,
+                             int64_t* __restrict__ consumed) {
+  const int32_t nk = *n_keys;
+  for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < W; p += (int64_t)gridDim.x * blockDim.x) {
+    if (!flags[p]) continue;
+    uint32_t q = rank[p];
+    if (q >= k) continue;
+    uint32_t draw = (uint32_t)(((uint64_t)U[p] * n_pool) >> 32);
+    int32_t row = pending[q];
+    int c = col[row];
+    neg[(int64_t)row * 3 + c] = (int32_t)draw;
+    int32_t orig = core[(int64_t)(row / s) * 3 + c];
+    int32_t h = neg[(int64_t)row * 3 + 0], r = neg[(int64_t)row * 3 + 1], t = neg[(int64_t)row * 3 + 2];
+    bool b = ((int32_t)draw == orig) || key_present(keys, nk, triple_key(h, r, t, n_local, R));
+    bad[q] = b ? 1u : 0u;
+    if (q == k - 1) *consumed = p + 1;
+  }
+}
+
+__global__ void k_scatter_pending(const uint32_t* __restrict__ bad, const uint32_t* __restrict__ rank, int64_t k,
+                                  const int32_t* __restrict__ pending, int32_t* __restrict__ next,
+                                  const uint32_t* __restrict__ total, int32_t* __restrict__ next_count) {
+  for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < k; q += (int64_t)gridDim.x * blockDim.x)
+    if (bad[q]) next[rank[q]] = pending[q];
+  if (blockIdx.x == 0 && threadIdx.x == 0) *next_count = (int32_t)*total;
+}
+
+__global__ void k_is_positive(const int32_t* __restrict__ tri, int64_t k, int32_t n, int32_t R,
+                              const int64_t* __restrict__ keys, const int32_t* __restrict__ n_keys,
+                              uint8_t* __restrict__ out) {
+  const int32_t nk = *n_keys;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < k; i += (int64_t)gridDim.x * blockDim.x)
+    out[i] = key_present(keys, nk, triple_key(tri[i * 3], tri[i * 3 + 1], tri[i * 3 + 2], n, R)) ? 1 : 0;
+}
+
+// ---------------------------------------------------------------------------
+// permutation: speculative single-warp Fisher-Yates draw
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ uint32_t smear(uint32_t x) {
+  x |= x >> 1; x |= x >> 2; x |= x >> 4; x |= x >> 8; x |= x >> 16;
+  return x;
+}
+
+constexpr int RING_Q = 1024;           // uint32 per quarter
+constexpr int RING = 4 * RING_Q;
+
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+  unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sa), "l"(gmem));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
+
+// One warp walks i = n-1 .. 1. For a 32-position window of the uint32 stream
+// every lane's acceptance is decided unless its masked value lies in
+// (i - lane, i]; the first such ambiguous lane is resolved exactly and the
+// window restarts after it. Positions stream through a 4-quarter smem ring
+// filled by cp.async two quarters ahead.
+__global__ void __launch_bounds__(32) k_perm_draws(const uint32_t* __restrict__ U, int64_t W, int64_t n,
+                                                   int32_t* __restrict__ js, int64_t* __restrict__ consumed) {
+  __shared__ __align__(16) uint32_t ring[RING];
+  const unsigned lane = lane_id();
+  int64_t issued = 0;   // quarters issued
+  auto issue = [&](int64_t q) {
+    int64_t base = q * RING_Q;
+    uint32_t* dst = ring + (q & 3) * RING_Q;
+    // 1024 uint32 = 256 x 16B; 8 per lane
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      int64_t e = base + (int64_t)(j * 32 + lane) * 4;
+      if (e + 4 <= W) cp_async16(dst + (j * 32 + lane) * 4, U + e);
+    }
+    cp_async_commit();
+  };
+  int64_t i = n - 1, p = 0;
+  bool ok = true;
+  while (i >= 1) {
+    int64_t need_q = (p + 31) / RING_Q;
+    while (issued <= need_q + 2) {
+      if (issued * RING_Q < W) issue(issued);
+      else cp_async_commit();   // keep group accounting uniform
+      ++issued;
+    }
+    if (p + 32 > W) { ok = false; break; }
+    // quarters issued after need_q: issued - 1 - need_q (>= 2); wait for need_q
+    cp_async_wait<2>();
+    __syncwarp();
+    uint32_t ii = (uint32_t)i;
+    uint32_t mask = smear(ii);
+    bool serial = ii < 64 || smear(ii - 31) != mask;
+    if (serial) {
+      // one exact draw for this i (lane 0), broadcast
+      int64_t pp = p;
+      uint32_t v = 0;
+      if (lane == 0) {
+        while (true) {
+          if (pp >= W) { pp = -1; break; }
+          // ring residency: pp stays within need_q window for this draw (<32 apart typical);
+          // fall back to global for safety beyond it
+          uint32_t u = (pp < (int64_t)(need_q + 1) * RING_Q) ? ring[pp & (RING - 1)] : U[pp];
+          ++pp;
+          v = u & mask;
+          if (v <= ii) break;
+        }
+      }
+      pp = __shfl_sync(0xffffffffu, pp, 0);
+      v = __shfl_sync(0xffffffffu, v, 0);
+      if (pp < 0) { ok = false; break; }
+      if (lane == 0) js[i] = (int32_t)v;
+      p = pp;
+      i -= 1;
+      continue;
+    }
+    uint32_t v = ring[(p + lane) & (RING - 1)] & mask;
+    bool acc_sure = v + lane <= ii;            // v <= i - lane
+    bool rej_sure = v > ii;
+    unsigned amb = __ballot_sync(0xffffffffu, !acc_sure && !rej_sure);
+    int f = amb ? __ffs(amb) - 1 : 32;
+    unsigned before = (f == 32) ? 0xffffffffu : ((1u << f) - 1u);
+    unsigned accm = __ballot_sync(0xffffffffu, acc_sure) & before;
+    if ((int)lane < f && acc_sure) {
+      uint32_t il = ii - __popc(accm & lanemask_lt());
+      js[il] = (int32_t)v;
+    }
+    int taken = f == 32 ? 32 : f + 1;
+    int accepts = __popc(accm);
+    if (f < 32) {
+      uint32_t il_f = ii - accepts;
+      uint32_t vf = __shfl_sync(0xffffffffu, v, f);
+      if (vf <= il_f) {
+        if (lane == 0) js[il_f] = (int32_t)vf;
+        accepts += 1;
+      }
+    }
+    p += taken;
+    i -= accepts;
+  }
+  cp_async_wait<0>();
+  if (lane == 0) *consumed = ok ? p : -1;
+}
+
+// group swap targets: members of group j are the i with js[i] == j (ascending)
+__global__ void k_group_count(const int32_t* __restrict__ js, int64_t n, uint32_t* __restrict__ cnt) {
+  for (int64_t i = 1 + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    atomicAdd(&cnt[js[i]], 1u);
+}
+
+__global__ void k_group_fill(const int32_t* __restrict__ js, int64_t n, const uint32_t* __restrict__ start,
+                             uint32_t* __restrict__ fill, int32_t* __restrict__ members) {
+  for (int64_t i = 1 + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    int32_t j = js[i];
+    uint32_t slot = atomicAdd(&fill[j], 1u);
+    members[start[j] + slot] = (int32_t)i;
+  }
+}
+
+// sort each (small) group ascending; T(p) = first member > p; ptr = T or self
+__global__ void k_group_sort_T(int32_t* __restrict__ members, const uint32_t* __restrict__ start,
+                               const uint32_t* __restrict__ cnt, int64_t n, int32_t* __restrict__ ptr) {
+  for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < n; p += (int64_t)gridDim.x * blockDim.x) {
+    uint32_t a = start[p], c = cnt[p];
+    int32_t* g = members + a;
+    for (uint32_t x = 1; x < c; ++x) {
+      int32_t key = g[x];
+      int32_t y = (int32_t)x - 1;
+      while (y >= 0 && g[y] > key) { g[y + 1] = g[y]; --y; }
+      g[y + 1] = key;
+    }
+    int32_t t = (int32_t)p;
+    for (uint32_t x = 0; x < c; ++x)
+      if (g[x] > (int32_t)p) { t = g[x]; break; }
+    ptr[p] = t;
+  }
+}
+
+__global__ void k_pointer_jump(int32_t* __restrict__ ptr, int64_t n) {
+  for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < n; p += (int64_t)gridDim.x * blockDim.x) {
+    int32_t q = ptr[p];
+    int32_t r = ptr[q];
+    if (r != q) ptr[p] = r;
+  }
+}
+
+__global__ void k_perm_final(const int32_t* __restrict__ js, int64_t n, const int32_t* __restrict__ members,
+                             const uint32_t* __restrict__ start, const uint32_t* __restrict__ cnt,
+                             const int32_t* __restrict__ root, int32_t* __restrict__ perm) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    if (i == 0) { perm[0] = root[0]; continue; }
+    int32_t j = js[i];
+    const int32_t* g = members + start[j];
+    uint32_t c = cnt[j];
+    int32_t succ = -1;
+    for (uint32_t x = 0; x < c; ++x)
+      if (g[x] == (int32_t)i) { if (x + 1 < c) succ = g[x + 1]; break; }
+    perm[i] = succ >= 0 ? root[succ] : j;
+  }
+}
+
+__global__ void k_stream_gather(const int32_t* __restrict__ pos, int64_t npos, const int32_t* __restrict__ neg,
+                                int64_t nneg, const int32_t* __restrict__ perm, int32_t* __restrict__ out,
+                                float* __restrict__ labels) {
+  int64_t total = npos + nneg;
+  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < total; k += (int64_t)gridDim.x * blockDim.x) {
+    int64_t i = perm[k];
+    const int32_t* src = i < npos ? pos + i * 3 : neg + (i - npos) * 3;
+    out[k * 3 + 0] = src[0];
+    out[k * 3 + 1] = src[1];
+    out[k * 3 + 2] = src[2];
+    labels[k] = i < npos ? 1.0f : 0.0f;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// closure
+// ---------------------------------------------------------------------------
+__global__ void k_closure_clear(int32_t* __restrict__ pos, uint32_t* __restrict__ flags, int64_t n) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    pos[i] = -1;
+    flags[i] = 0;
+  }
+}
+
+__global__ void k_mark_batch(const int32_t* __restrict__ tri, int64_t total, int64_t start, int64_t b,
+                             const int32_t* __restrict__ ids, int32_t n, uint32_t* __restrict__ flags,
+                             int32_t* __restrict__ bad) {
+  for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < b; q += (int64_t)gridDim.x * blockDim.x) {
+    if (tri) {
+      int64_t row = (start + q) % total;
+      int32_t h = tri[row * 3], t = tri[row * 3 + 2];
+      if (h < 0 || h >= n || t < 0 || t >= n) { *bad = 1; continue; }
+      flags[h] = 1u;
+      flags[t] = 1u;
+    } else {
+      int32_t v = ids[q];
+      if (v < 0 || v >= n) { *bad = 1; continue; }
+      flags[v] = 1u;
+    }
+  }
+}
+
+__global__ void k_set_pos(const int32_t* __restrict__ order, const int32_t* __restrict__ counts, int hop,
+                          int32_t* __restrict__ pos) {
+  int32_t lo = hop == 0 ? 0 : counts[hop - 1];
+  int32_t hi = counts[hop];
+  for (int64_t i = lo + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < hi; i += (int64_t)gridDim.x * blockDim.x)
+    pos[order[i]] = (int32_t)i;
+}
+
+// warp per active vertex: flag unplaced sources of its messages
+__global__ void k_mark_sources(const int32_t* __restrict__ order, const int32_t* __restrict__ counts, int hop,
+                               const int32_t* __restrict__ indptr, const int32_t* __restrict__ src,
+                               const int32_t* __restrict__ pos, uint32_t* __restrict__ flags) {
+  const int32_t active = counts[hop];
+  const int warps = (gridDim.x * blockDim.x) >> 5;
+  for (int64_t w = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; w < active; w += warps) {
+    int32_t v = order[w];
+    for (int32_t e = indptr[v] + (int32_t)lane_id(); e < indptr[v + 1]; e += 32) {
+      int32_t u = src[e];
+      if (pos[u] < 0) flags[u] = 1u;
+    }
+  }
+}
+
+__global__ void k_clear_u32(uint32_t* __restrict__ a, int64_t n) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) a[i] = 0;
+}
+
+__global__ void k_counts_next(int32_t* __restrict__ counts, int hop, const int32_t* __restrict__ added) {
+  counts[hop + 1] = counts[hop] + *added;
+}
+
+}  // namespace kg
+
+using namespace kg;
+
+extern "C" {
+
+// --- host PCG64 bookkeeping ----------------------------------------------
+void kg_pcg64_advance(kg_pcg64* g, uint64_t delta) {
+  u128 s = apply_jump(pcg_jump(delta, inc_of(*g)), state_of(*g));
+  g->state_hi = s.hi;
+  g->state_lo = s.lo;
+}
+
+void kg_pcg64_consume32(kg_pcg64* g, uint64_t count) {
+  if (count == 0) return;
+  if (g->has_uint32) {
+    g->has_uint32 = 0;   // numpy keeps the stale uinteger value
+    count -= 1;
+  }
+  uint64_t words = count / 2;
+  if (count & 1) {
+    u128 s = apply_jump(pcg_jump(words + 1, inc_of(*g)), state_of(*g));
+    uint64_t x = pcg_output(s);
+    g->state_hi = s.hi;
+    g->state_lo = s.lo;
+    g->has_uint32 = 1;
+    g->uinteger = (uint32_t)(x >> 32);
+  } else if (words) {
+    kg_pcg64_advance(g, words);
+  }
+}
+
+void kg_pcg64_peek64(const kg_pcg64* g, uint64_t* out, int64_t count) {
+  u128 s = state_of(*g), inc = inc_of(*g);
+  for (int64_t i = 0; i < count; ++i) {
+    s = pcg_step(s, inc);
+    out[i] = pcg_output(s);
+  }
+}
+
+// --- negatives -------------------------------------------------------------
+kg_status kg_neg_init(const int32_t* core, int64_t m, int32_t s, kg_pcg64 g, int32_t* neg, int8_t* col,
+                      int32_t* pending, void* stream) {
+  KG_REQUIRE(s >= 1 && m >= 1, KG_ERR_VALIDATION, "neg_init needs s >= 1 and m >= 1");
+  KG_REQUIRE(m * (int64_t)s < (int64_t(1) << 31), KG_ERR_VALIDATION, "too many negatives");
+  int64_t total = m * s;
+  int blocks = persistent_blocks(ceil_div(total, COIN_PER_THREAD), 256, 8);
+  k_neg_init<<<blocks, 256, 0, as_stream(stream)>>>(core, m, s, g, neg, col, pending);
+  KG_CHECK_LAUNCH("k_neg_init");
+  return KG_OK;
+}
+
+int64_t kg_neg_round_workspace_bytes(int64_t W) {
+  return (int64_t)(align_up(W * 4) * 5 + scan_workspace(W) + 8192);
+}
+
+kg_status kg_neg_round(int32_t* neg, const int8_t* col, const int32_t* core, int32_t s, const int32_t* pending,
+                       int64_t k, int64_t pool_size, int32_t n_local, int32_t R, const int64_t* pos_keys,
+                       const int32_t* n_keys, kg_pcg64 g, int64_t W, int32_t* next_pending,
+                       int32_t* next_count, int64_t* consumed, void* ws, int64_t ws_bytes, void* stream) {
+  cudaStream_t st = as_stream(stream);
+  KG_REQUIRE(pool_size >= 2 && pool_size <= 0xFFFFFFFFLL, KG_ERR_SAMPLING, "pool size out of range");
+  KG_REQUIRE(W >= k && k >= 1, KG_ERR_VALIDATION, "bad resampling window");
+  KG_REQUIRE(ws_bytes >= kg_neg_round_workspace_bytes(W), KG_ERR_VALIDATION, "neg workspace too small");
+  Arena a(ws, (size_t)ws_bytes);
+  uint32_t* U = a.take<uint32_t>(W);
+  uint32_t* flags = a.take<uint32_t>(W);
+  uint32_t* rank = a.take<uint32_t>(W);
+  uint32_t* bad = a.take<uint32_t>(W);
+  uint32_t* bad_rank = a.take<uint32_t>(W);
+  uint32_t* totals = a.take<uint32_t>(4);
+  char* sws = a.take<char>(scan_workspace(W));
+  uint32_t n = (uint32_t)pool_size;
+  KG_CUDA(cudaMemsetAsync(consumed, 0, sizeof(int64_t), st));
+  k_gen_u32<<<persistent_blocks(ceil_div(W / 2 + 2, GEN_WORDS), 256, 8), 256, 0, st>>>(g, W, U);
+  k_lemire_flags<<<grid_for(W), 256, 0, st>>>(U, W, n, lemire_threshold(n), flags);
+  KG_CHECK_LAUNCH("neg gen");
+  kg_status r = exclusive_scan_u32(flags, rank, W, totals, sws, scan_workspace(W), st);
+  if (r != KG_OK) return r;
+  k_neg_assign<<<grid_for(W), 256, 0, st>>>(U, flags, rank, W, n, pending, k, neg, col, core, s, n_local, R,
+                                            pos_keys, n_keys, bad, consumed);
+  KG_CHECK_LAUNCH("k_neg_assign");
+  r = exclusive_scan_u32(bad, bad_rank, k, totals + 1, sws, scan_workspace(W), st);
+  if (r != KG_OK) return r;
+  k_scatter_pending<<<grid_for(k), 256, 0, st>>>(bad, bad_rank, k, pending, next_pending, totals + 1, next_count);
+  KG_CHECK_LAUNCH("k_scatter_pending");
+  return KG_OK;
+}
+
+kg_status kg_is_positive(const int32_t* triples, int64_t k, int32_t n_local, int32_t R, const int64_t* pos_keys,
+                         const int32_t* n_keys, uint8_t* out, void* stream) {
+  if (k <= 0) return KG_OK;
+  k_is_positive<<<grid_for(k), 256, 0, as_stream(stream)>>>(triples, k, n_local, R, pos_keys, n_keys, out);
+  KG_CHECK_LAUNCH("k_is_positive");
+  return KG_OK;
+}
+
+// --- permutation -----------------------------------------------------------
+int64_t kg_perm_draws_buffer_len(int64_t n) {
+  // expected draws < 2n (acceptance >= 1/2 per attempt); generous slack
+  return ((2 * n + 8192 + 4 * 1024) / 1024 + 4) * 1024;
+}
+
+kg_status kg_perm_draws_buffered(int64_t n, kg_pcg64 g, uint32_t* U, int64_t W, int32_t* js, int64_t* consumed32,
+                                 void* stream) {
+  cudaStream_t st = as_stream(stream);
+  KG_REQUIRE(n >= 1 && n < (int64_t(1) << 31), KG_ERR_VALIDATION, "permutation size out of range");
+  if (n == 1) {
+    KG_CUDA(cudaMemsetAsync(consumed32, 0, sizeof(int64_t), st));
+    return KG_OK;
+  }
+  KG_REQUIRE(W % 4 == 0 && W >= 4096, KG_ERR_VALIDATION, "draw buffer must be a multiple of 4 >= 4096");
+  k_gen_u32<<<persistent_blocks(ceil_div(W / 2 + 2, GEN_WORDS), 256, 8), 256, 0, st>>>(g, W, U);
+  KG_CHECK_LAUNCH("perm gen");
+  k_perm_draws<<<1, 32, 0, st>>>(U, W, n, js, consumed32);
+  KG_CHECK_LAUNCH("k_perm_draws");
+  return KG_OK;
+}
+
+int64_t kg_perm_resolve_workspace_bytes(int64_t n) {
+  return (int64_t)(align_up(n * 4) * 5 + scan_workspace(n) + 4096);
+}
+
+kg_status kg_perm_resolve(const int32_t* js, int64_t n, int32_t* perm, void* ws, int64_t ws_bytes, void* stream) {
+  cudaStream_t st = as_stream(stream);
+  KG_REQUIRE(ws_bytes >= kg_perm_resolve_workspace_bytes(n), KG_ERR_VALIDATION, "perm workspace too small");
+  if (n == 1) {
+    KG_CUDA(cudaMemsetAsync(perm, 0, sizeof(int32_t), st));
+    return KG_OK;
+  }
+  Arena a(ws, (size_t)ws_bytes);
+  uint32_t* cnt = a.take<uint32_t>(n);
+  uint32_t* start = a.take<uint32_t>(n);
+  uint32_t* fill = a.take<uint32_t>(n);
+  int32_t* members = a.take<int32_t>(n);
+  int32_t* root = a.take<int32_t>(n);
+  char* sws = a.take<char>(scan_workspace(n));
+  KG_CUDA(cudaMemsetAsync(cnt, 0, n * 4, st));
+  KG_CUDA(cudaMemsetAsync(fill, 0, n * 4, st));
+  int gb = grid_for(n);
+  k_group_count<<<gb, 256, 0, st>>>(js, n, cnt);
+  kg_status r = exclusive_scan_u32(cnt, start, n, nullptr, sws, scan_workspace(n), st);
+  if (r != KG_OK) return r;
+  k_group_fill<<<gb, 256, 0, st>>>(js, n, start, fill, members);
+  k_group_sort_T<<<gb, 256, 0, st>>>(members, start, cnt, n, root);
+  int rounds = 1;
+  while ((int64_t(1) << rounds) < n) ++rounds;
+  for (int it = 0; it < rounds + 1; ++it) k_pointer_jump<<<gb, 256, 0, st>>>(root, n);
+  k_perm_final<<<gb, 256, 0, st>>>(js, n, members, start, cnt, root, perm);
+  KG_CHECK_LAUNCH("perm resolve");
+  return KG_OK;
+}
+
+kg_status kg_stream_gather(const int32_t* pos, int64_t npos, const int32_t* neg, int64_t nneg, const int32_t* perm,
+                           int32_t* stream_triples, float* labels, void* stream) {
+  if (npos + nneg == 0) return KG_OK;
+  k_stream_gather<<<grid_for(npos + nneg), 256, 0, as_stream(stream)>>>(pos, npos, neg, nneg, perm,
+                                                                        stream_triples, labels);
+  KG_CHECK_LAUNCH("k_stream_gather");
+  return KG_OK;
+}
+
+// --- closure -------------------------------------------------------------------
+int64_t kg_closure_workspace_bytes(int32_t n) {
+  return (int64_t)(align_up((int64_t)n * 4) + compact_workspace(n) + 4096);
+}
+
+kg_status kg_closure(const int32_t* tri, int64_t total, int64_t start, int64_t b, const int32_t* seed_ids,
+                     const kg_graph_csr* G, int32_t hops, int32_t* order, int32_t* pos, int32_t* counts,
+                     void* ws, int64_t ws_bytes, void* stream) {
+  cudaStream_t st = as_stream(stream);
+  const int32_t n = G->n;
+  KG_REQUIRE(hops >= 0, KG_ERR_VALIDATION, "hops must be >= 0");
+  KG_REQUIRE(b >= 1, KG_ERR_VALIDATION, "empty batch");
+  KG_REQUIRE(ws_bytes >= kg_closure_workspace_bytes(n), KG_ERR_VALIDATION, "closure workspace too small");
+  Arena a(ws, (size_t)ws_bytes);
+  uint32_t* flags = a.take<uint32_t>(n);
+  int32_t* bad = a.take<int32_t>(4);
+  char* cws = a.take<char>(compact_workspace(n));
+  int gn = grid_for(n);
+  k_closure_clear<<<gn, 256, 0, st>>>(pos, flags, n);
+  KG_CUDA(cudaMemsetAsync(bad, 0, 4, st));
+  k_mark_batch<<<grid_for(b), 256, 0, st>>>(tri, total, start, b, seed_ids, n, flags, bad);
+  KG_CHECK_LAUNCH("closure mark");
+  kg_status r = compact_flags(flags, n, order, counts, 0, nullptr, cws, compact_workspace(n), st);
+  if (r != KG_OK) return r;
+  k_set_pos<<<gn, 256, 0, st>>>(order, counts, 0, pos);
+  for (int h = 0; h < hops; ++h) {
+    k_clear_u32<<<gn, 256, 0, st>>>(flags, n);
+    k_mark_sources<<<persistent_blocks((int64_t)n * 32, 256, 8), 256, 0, st>>>(order, counts, h, G->indptr, G->src,
+                                                                              pos, flags);
+    // append newly reached vertices (ascending) after counts[h]
+    r = compact_flags(flags, n, order, bad + 1, 0, counts + h, cws, compact_workspace(n), st);
+    if (r != KG_OK) return r;
+    k_counts_next<<<1, 1, 0, st>>>(counts, h, bad + 1);
+    k_set_pos<<<gn, 256, 0, st>>>(order, counts, h + 1, pos);
+    KG_CHECK_LAUNCH("closure hop");
+  }
+  return KG_OK;
+}
+
+}  // extern "C"
