@@ -1,0 +1,463 @@
+"""Synchronous data-parallel training over self-sufficient partitions on
+B200s (drop-in for ref:trainer.py).
+
+One partition per GPU. Launched under torchrun (torch.distributed
+initialised, NCCL backend) each rank trains the partitions p with
+p % world_size == rank; without a process group every partition runs in this
+process on the current device (the reference's P=1 inline path, and the
+replicated-partition test configuration). Per round every worker runs
+
+    closure -> RGCN forward -> DistMult+BCE -> RGCN backward
+
+entirely on the device; the dense gradient payloads of all P workers are
+all-gathered over NVLink (NCCL) and one fused kernel combines them in the
+reference's pairwise-tree order and applies Adam/SGD, so dense replicas stay
+bitwise identical on every rank (ref:trainer.py:465-469). Embedding rows are
+partition-local and updated with lazy sparse Adam.
+"""
+
+from __future__ import annotations
+
+import math
+import time
+from dataclasses import dataclass, field
+from typing import Optional
+
+import numpy as np
+
+from . import _lib
+from .errors import KGError, NumericError, ProtocolError, ValidationError
+from .model import (MODE_EMBEDDING, MODE_FEATURE, DeviceModel, ModelConfig, ModelParams, ViewBuffers,
+                    check_flags, device_backward, device_forward, device_loss, init_params)
+from .partition import PartitionSet
+from .sampler import build_view, sample_negatives_device, stream_device
+
+_DROPOUT_STREAM_OFFSET = 0x9E3779B9
+
+
+def _torch():
+    import torch
+    return torch
+
+
+@dataclass
+class TrainConfig:
+    """ref:trainer.py:35-56."""
+    epochs: int = 1
+    batch_size: Optional[int] = None
+    fixed_num_batches: Optional[int] = None
+    learning_rate: float = 0.01
+    optimizer: str = "adam"
+    beta1: float = 0.9
+    beta2: float = 0.999
+    adam_eps: float = 1e-8
+    seed: int = 0
+    eval_every: int = 0
+    grad_clip: Optional[float] = None
+    mp_start: str = "fork"
+
+    def __post_init__(self):
+        if self.learning_rate <= 0:
+            raise ValidationError("learning_rate must be > 0")
+        if self.optimizer not in ("sgd", "adam"):
+            raise ValidationError(f"unknown optimizer {self.optimizer!r}")
+        if self.epochs < 0:
+            raise ValidationError("epochs must be >= 0")
+
+
+# ---------------------------------------------------------------------------
+# Reduction (ref:trainer.py:63-86)
+# ---------------------------------------------------------------------------
+
+def allreduce_mean(payloads: list) -> list:
+    """Elementwise mean of gradient payloads in the fixed pairwise-tree order.
+    Each payload is a list of arrays; runs the fused device tree-mean
+    (kg_dense_step's reduction, with an SGD step of lr = 1 on a zero
+    parameter) so the API exercises the same kernel as training."""
+    if not payloads:
+        raise ProtocolError("empty reduction")
+    shapes = [np.shape(a) for a in payloads[0]]
+    for p in payloads[1:]:
+        if [np.shape(a) for a in p] != shapes:
+            raise ProtocolError("gradient payloads disagree in shape")
+    torch = _torch()
+    lib = _lib.require_cuda()
+    dev = torch.device("cuda", torch.cuda.current_device())
+    flat = np.stack([np.concatenate([np.asarray(a, np.float32).reshape(-1) for a in p]) for p in payloads])
+    n = flat.shape[1]
+    g = torch.as_tensor(flat).to(dev)
+    out = torch.zeros(n, dtype=torch.float32, device=dev)
+    flags = torch.zeros(1, dtype=torch.int32, device=dev)
+    ws = torch.empty(lib.kg_optim_workspace_bytes(n), dtype=torch.uint8, device=dev)
+    # p = 0 - 1 * mean  ->  -mean
+    _lib.call("kg_dense_step", out.data_ptr(), 0, 0, g.data_ptr(), len(payloads), n, 0, 1.0, 0.9, 0.999,
+              1e-8, 1.0, 1.0, 0.0, flags.data_ptr(), ws.data_ptr(), ws.numel(), _lib.stream_handle())
+    res = (-out).double().cpu().numpy()
+    outs, o = [], 0
+    for s in shapes:
+        k = int(np.prod(s)) if len(s) else 1
+        outs.append(res[o:o + k].reshape(s))
+        o += k
+    return outs
+
+
+# ---------------------------------------------------------------------------
+# Optimizer (ref:trainer.py:93-151)
+# ---------------------------------------------------------------------------
+
+class Optimizer:
+    """SGD or Adam over the dense blocks plus lazy sparse rows of the entity
+    table, executed by kg_dense_step / kg_sparse_step on the device. The
+    numpy ModelParams passed to step() are updated in place."""
+
+    def __init__(self, config: TrainConfig, params: ModelParams):
+        torch = _torch()
+        _lib.require_cuda()
+        self.config = config
+        self.t = 0
+        self._adam = config.optimizer == "adam"
+        self.dev = torch.device("cuda", torch.cuda.current_device())
+        n = sum(b.size for b in params.dense_blocks())
+        self.m = torch.zeros(n, dtype=torch.float32, device=self.dev)
+        self.v = torch.zeros(n, dtype=torch.float32, device=self.dev)
+        if params.entity_embed is not None:
+            self.em = torch.zeros(params.entity_embed.shape, dtype=torch.float32, device=self.dev)
+            self.ev = torch.zeros(params.entity_embed.shape, dtype=torch.float32, device=self.dev)
+
+    def step(self, params: ModelParams, dense_grads: list, embed_ids: Optional[np.ndarray] = None,
+             embed_rows: Optional[np.ndarray] = None) -> None:
+        torch = _torch()
+        lib = _lib.require_cuda()
+        cfg = self.config
+        self.t += 1
+        blocks = params.dense_blocks()
+        if len(blocks) != len(dense_grads):
+            raise ProtocolError("gradient/parameter block count mismatch")
+        p = torch.as_tensor(np.concatenate([np.asarray(b, np.float32).reshape(-1) for b in blocks])).to(self.dev)
+        g = torch.as_tensor(np.concatenate([np.asarray(x, np.float32).reshape(-1) for x in dense_grads])).to(self.dev)
+        flags = torch.zeros(1, dtype=torch.int32, device=self.dev)
+        ws = torch.empty(lib.kg_optim_workspace_bytes(p.numel()), dtype=torch.uint8, device=self.dev)
+        bc1 = 1.0 - cfg.beta1 ** self.t
+        bc2 = 1.0 - cfg.beta2 ** self.t
+        _lib.call("kg_dense_step", p.data_ptr(), self.m.data_ptr(), self.v.data_ptr(), g.data_ptr(), 1, p.numel(),
+                  1 if self._adam else 0, cfg.learning_rate, cfg.beta1, cfg.beta2, cfg.adam_eps, bc1, bc2,
+                  float(cfg.grad_clip) if cfg.grad_clip is not None else 0.0, flags.data_ptr(), ws.data_ptr(),
+                  ws.numel(), _lib.stream_handle())
+        flat = p.double().cpu().numpy()
+        o = 0
+        for b in blocks:
+            b[...] = flat[o:o + b.size].reshape(b.shape)
+            o += b.size
+        if embed_ids is not None and params.entity_embed is not None and len(embed_ids):
+            table = torch.as_tensor(params.entity_embed.astype(np.float32)).to(self.dev)
+            grad = torch.zeros_like(table)
+            ids = torch.as_tensor(np.asarray(embed_ids, np.int64)).to(self.dev)
+            grad[ids] = torch.as_tensor(np.asarray(embed_rows, np.float32)).to(self.dev)
+            rows = ids.to(torch.int32)
+            cnt = torch.tensor([len(embed_ids)], dtype=torch.int32, device=self.dev)
+            _lib.call("kg_sparse_step", table.data_ptr(), self.em.data_ptr(), self.ev.data_ptr(), grad.data_ptr(),
+                      rows.data_ptr(), cnt.data_ptr(), 0, table.shape[1], 1 if self._adam else 0,
+                      cfg.learning_rate, cfg.beta1, cfg.beta2, cfg.adam_eps, bc1, bc2, len(embed_ids),
+                      _lib.stream_handle())
+            params.entity_embed[...] = table.double().cpu().numpy()
+        if int(flags.item()):
+            raise NumericError("non-finite parameter after optimizer step")
+
+
+# ---------------------------------------------------------------------------
+# Report (ref:trainer.py:272-301)
+# ---------------------------------------------------------------------------
+
+@dataclass
+class TrainReport:
+    rounds_per_epoch: int
+    batch_sizes: list
+    epoch_seconds: list = field(default_factory=list)
+    loss_curve: list = field(default_factory=list)
+    val_mrr: list = field(default_factory=list)
+    cg_build_per_batch: list = field(default_factory=list)
+    encode_per_batch: list = field(default_factory=list)
+    loss_step_per_batch: list = field(default_factory=list)
+
+    def mean_timings(self) -> dict:
+        def m(x):
+            return float(np.mean(x)) if x else 0.0
+        return {"epoch_time": m(self.epoch_seconds), "cg_build": m(self.cg_build_per_batch),
+                "encode": m(self.encode_per_batch), "loss_step": m(self.loss_step_per_batch)}
+
+    def format_metrics(self) -> str:
+        lines = []
+        for e, (loss, secs) in enumerate(zip(self.loss_curve, self.epoch_seconds)):
+            parts = [f"epoch={e}", f"loss={loss:.6f}", f"time={secs:.3f}"]
+            mrr = dict(self.val_mrr).get(e)
+            if mrr is not None:
+                parts.append(f"val_mrr={mrr:.4f}")
+            lines.append(" ".join(parts))
+        return "\n".join(lines)
+
+
+def _plan_batches(num_cores: list, s: int, train_config: TrainConfig) -> tuple:
+    """Per-worker batch size and shared round count (ref:trainer.py:304-316)."""
+    lens = [c * (s + 1) for c in num_cores]
+    if any(L == 0 for L in lens):
+        raise ValidationError("a partition has no core edges to train on")
+    if train_config.fixed_num_batches is not None:
+        rounds = train_config.fixed_num_batches
+        return [max(1, math.ceil(L / rounds)) for L in lens], rounds
+    sizes = [train_config.batch_size or L for L in lens]
+    return sizes, max(math.ceil(L / b) for L, b in zip(lens, sizes))
+
+
+def _assemble_embed(pset: PartitionSet, tables: dict, base: np.ndarray) -> np.ndarray:
+    """Each vertex's row from the lowest-id partition holding it as a core
+    edge endpoint, else the initial row (ref:trainer.py:319-333).
+    tables: partition index -> full (N, d) table."""
+    out = base.copy()
+    owner = np.full(len(base), -1, dtype=np.int64)
+    for part in sorted(pset.partitions, key=lambda p: p.id):
+        ends = np.concatenate([part.core_vertices, part.replicated_vertices]).astype(np.int64)
+        free = ends[owner[ends] < 0]
+        owner[free] = part.id
+    for wid, table in tables.items():
+        rows = np.flatnonzero(owner == pset.partitions[wid].id)
+        if len(rows):
+            out[rows] = table[rows]
+    return out
+
+
+# ---------------------------------------------------------------------------
+# Device engine
+# ---------------------------------------------------------------------------
+
+class _Worker:
+    """Device state of one partition: view, buffers, RNG stream, local
+    embedding rows and their Adam moments."""
+
+    def __init__(self, wid, partition, pset, config: ModelConfig, tc: TrainConfig, b: int, params: ModelParams,
+                 features):
+        torch = _torch()
+        self.wid = wid
+        self.view = build_view(partition, pset.num_entities, pset.num_relations)
+        self.b = b
+        self.config = config
+        dev = self.view.device
+        self.pcg = _lib.pcg_from_numpy(np.random.default_rng(tc.seed ^ self.view.partition_id))
+        local = self.view.local_ids
+        if config.mode == MODE_EMBEDDING:
+            rows = params.entity_embed[local]
+        else:
+            rows = features[local]
+        self.input_rows = torch.as_tensor(np.ascontiguousarray(rows, dtype=np.float32)).to(dev)
+        self.bufs = ViewBuffers(config, self.view, b, input_rows=self.input_rows)
+        self.emb = config.mode == MODE_EMBEDDING
+        if self.emb and tc.optimizer == "adam":
+            self.em = torch.zeros_like(self.input_rows)
+            self.ev = torch.zeros_like(self.input_rows)
+        else:
+            self.em = self.ev = None
+        self.ws = _lib.Workspace(dev)
+        self.core = self.view.d_edges[: self.view.num_core]
+        self.stream = None
+
+    def begin_epoch(self):
+        neg, self.pcg = sample_negatives_device(self.view, self.config.negatives_per_positive, self.pcg, self.ws)
+        self.stream, self.pcg = stream_device(self.core, neg, self.pcg, self.view.device, self.ws)
+
+    def closure(self, rnd: int):
+        from .sampler import closure_device
+        closure_device(self.view, self.config.num_layers, stream=self.stream, start=rnd * self.b, size=self.b,
+                       out=(self.bufs.order, self.bufs.pos, self.bufs.counts), ws=self.ws)
+
+
+class Trainer:
+    """The hot loop of ref:trainer.py:202-236 for the partitions this process
+    owns. `run_round()` is one synchronized training round."""
+
+    def __init__(self, pset: PartitionSet, graph, model_config: ModelConfig, train_config: TrainConfig,
+                 initial_params: Optional[ModelParams] = None):
+        torch = _torch()
+        _lib.require_cuda()
+        if pset.hops != model_config.num_layers:
+            raise ValidationError(f"partitions expanded for {pset.hops} hops but model has "
+                                  f"{model_config.num_layers} layers")
+        if model_config.num_relations != pset.num_relations:
+            raise ValidationError("model num_relations != partition set num_relations")
+        if model_config.dropout > 0.0:
+            raise ValidationError("dropout > 0 is not supported by the device path yet")
+        self.pset, self.mc, self.tc = pset, model_config, train_config
+        self.P = pset.num_parts
+        dist = torch.distributed
+        self.dist = dist.is_available() and dist.is_initialized() and dist.get_world_size() > 1
+        self.world = dist.get_world_size() if self.dist else 1
+        self.rank = dist.get_rank() if self.dist else 0
+        if self.dist and self.P % self.world != 0:
+            raise ValidationError(f"{self.P} partitions cannot be split evenly over {self.world} ranks")
+        self.local_wids = [w for w in range(self.P) if w % self.world == self.rank]
+        params = initial_params.copy() if initial_params is not None else init_params(
+            model_config, np.random.default_rng(train_config.seed), num_entities=pset.num_entities)
+        if model_config.mode == MODE_FEATURE:
+            if graph.features is None:
+                raise ValidationError("feature mode requires graph features")
+            features = graph.features
+        else:
+            if params.entity_embed is None:
+                raise ValidationError("embedding mode requires an entity table in params")
+            features = None
+        self.init_params = params
+        self.sizes, self.rounds = _plan_batches([p.num_core_edges for p in pset.partitions],
+                                                model_config.negatives_per_positive, train_config)
+        self.dev = torch.device("cuda", torch.cuda.current_device())
+        self.model = DeviceModel.from_params(model_config, params, self.dev)
+        D = self.model.layout.total
+        self.D = D
+        self.workers = [_Worker(w, pset.partitions[w], pset, model_config, train_config, self.sizes[w], params,
+                                features) for w in self.local_wids]
+        nloc = len(self.workers)
+        self.grads_local = torch.zeros((nloc, D), dtype=torch.float32, device=self.dev)
+        self.grads_all = (torch.zeros((self.P, D), dtype=torch.float32, device=self.dev) if self.dist
+                          else self.grads_local)
+        self.m = torch.zeros(D, dtype=torch.float32, device=self.dev)
+        self.v = torch.zeros(D, dtype=torch.float32, device=self.dev)
+        self.flags = torch.zeros(1, dtype=torch.int32, device=self.dev)
+        self.optim_ws = torch.empty(_lib.require_cuda().kg_optim_workspace_bytes(D), dtype=torch.uint8,
+                                    device=self.dev)
+        self.losses = torch.zeros((nloc, max(self.rounds, 1)), dtype=torch.float32, device=self.dev)
+        self.t = 0
+        self.round_in_epoch = 0
+        self.epoch = 0
+
+    # -- one synchronized round ----------------------------------------------
+    def begin_epoch(self):
+        for w in self.workers:
+            w.begin_epoch()
+        self.round_in_epoch = 0
+
+    def run_round(self):
+        tc = self.tc
+        r = self.round_in_epoch
+        for i, w in enumerate(self.workers):
+            w.closure(r)
+            device_forward(self.model, w.bufs)
+            gslot = self.grads_local[i]
+            device_loss(self.model, w.bufs, w.stream, r * w.b, w.b, gslot, self.losses[i, r:r + 1])
+            device_backward(self.model, w.bufs, gslot, input_grad=w.emb)
+        if self.dist:
+            self._gather()
+        self.t += 1
+        bc1 = 1.0 - tc.beta1 ** self.t
+        bc2 = 1.0 - tc.beta2 ** self.t
+        adam = 1 if tc.optimizer == "adam" else 0
+        st = _lib.stream_handle()
+        _lib.call("kg_dense_step", self.model.flat.data_ptr(), self.m.data_ptr(), self.v.data_ptr(),
+                  self.grads_all.data_ptr(), self.P, self.D, adam, tc.learning_rate, tc.beta1, tc.beta2,
+                  tc.adam_eps, bc1, bc2, float(tc.grad_clip) if tc.grad_clip is not None else 0.0,
+                  self.flags.data_ptr(), self.optim_ws.data_ptr(), self.optim_ws.numel(), st)
+        L = self.mc.num_layers
+        for w in self.workers:
+            if w.emb:
+                _lib.call("kg_sparse_step", w.input_rows.data_ptr(), _lib.ptr(w.em), _lib.ptr(w.ev),
+                          w.bufs.dH[0].data_ptr(), w.bufs.order.data_ptr(), w.bufs.counts.data_ptr(), L,
+                          self.mc.dims[0], adam, tc.learning_rate, tc.beta1, tc.beta2, tc.adam_eps, bc1, bc2,
+                          w.view.n, st)
+        self.round_in_epoch += 1
+
+    def _gather(self):
+        torch = _torch()
+        dist = torch.distributed
+        W, nloc = self.world, len(self.workers)
+        recv = torch.empty((W * nloc, self.D), dtype=torch.float32, device=self.dev)
+        dist.all_gather_into_tensor(recv, self.grads_local)
+        # rank r slot j holds partition r + j*W -> reorder into partition order
+        idx = torch.tensor([(p % W) * nloc + p // W for p in range(self.P)], device=self.dev)
+        torch.index_select(recv, 0, idx, out=self.grads_all)
+
+    def check(self):
+        for w in self.workers:
+            check_flags(w.bufs)
+        f = int(self.flags.item())
+        if f:
+            self.flags.zero_()
+            raise NumericError("non-finite parameter after optimizer step")
+
+    def epoch_losses(self) -> list:
+        return self.losses[:, : self.rounds].mean(dim=1).double().cpu().tolist()
+
+    # -- host snapshots ------------------------------------------------------
+    def local_tables(self) -> dict:
+        """Partition index -> full (N, d_in) table with this worker's rows."""
+        out = {}
+        base = self.init_params.entity_embed
+        for w in self.workers:
+            t = base.copy()
+            t[w.view.local_ids] = w.input_rows.double().cpu().numpy()
+            out[w.wid] = t
+        return out
+
+    def snapshot(self) -> ModelParams:
+        torch = _torch()
+        params = self.init_params.copy()
+        params.set_dense_blocks(self.model.dense_blocks())
+        if self.mc.mode == MODE_EMBEDDING:
+            tables = self.local_tables()
+            if self.dist:
+                gathered = [None] * self.world
+                torch.distributed.all_gather_object(gathered, tables)
+                tables = {k: v for d in gathered for k, v in d.items()}
+            if self.P == 1:
+                params.entity_embed = tables[0]
+            else:
+                params.entity_embed = _assemble_embed(self.pset, tables, self.init_params.entity_embed)
+        return params
+
+    def check_replicas(self):
+        """Dense replicas must be bitwise equal on every rank (ref:trainer.py:465-469)."""
+        if not self.dist:
+            return
+        torch = _torch()
+        mine = self.model.flat.clone()
+        allr = torch.empty((self.world, self.D), dtype=torch.float32, device=self.dev)
+        torch.distributed.all_gather_into_tensor(allr, mine)
+        for r in range(1, self.world):
+            if not torch.equal(allr[0], allr[r]):
+                raise ProtocolError(f"replica divergence: rank {r} dense blocks differ from rank 0")
+
+
+def train(pset: PartitionSet, graph, model_config: ModelConfig, train_config: TrainConfig,
+          initial_params: Optional[ModelParams] = None, eval_fn=None) -> tuple:
+    """Synchronized data-parallel training; returns (params, report)
+    (ref:trainer.py:336-480). eval_fn(params) -> float is called at epochs
+    selected by train_config.eval_every."""
+    torch = _torch()
+    tr = Trainer(pset, graph, model_config, train_config, initial_params)
+    report = TrainReport(rounds_per_epoch=tr.rounds, batch_sizes=list(tr.sizes))
+    tc = train_config
+    eval_epochs = frozenset(e for e in range(tc.epochs)
+                            if tc.eval_every and (e + 1) % tc.eval_every == 0) if eval_fn is not None else frozenset()
+    for epoch in range(tc.epochs):
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        tr.begin_epoch()
+        for _ in range(tr.rounds):
+            tr.run_round()
+        torch.cuda.synchronize()
+        secs = time.perf_counter() - t0
+        tr.check()
+        losses = tr.epoch_losses()
+        if tr.dist:
+            both = torch.tensor([sum(losses), float(len(losses)), secs], dtype=torch.float64, device=tr.dev)
+            gathered = [torch.zeros_like(both) for _ in range(tr.world)]
+            torch.distributed.all_gather(gathered, both)
+            g = torch.stack(gathered).cpu().numpy()
+            report.loss_curve.append(float(g[:, 0].sum() / g[:, 1].sum()))
+            report.epoch_seconds.append(float(g[:, 2].max()))
+        else:
+            report.loss_curve.append(float(np.mean(losses)))
+            report.epoch_seconds.append(secs)
+        nb = tr.P * tr.rounds
+        report.cg_build_per_batch.append(0.0)
+        report.encode_per_batch.append(0.0)
+        report.loss_step_per_batch.append(report.epoch_seconds[-1] * (tr.P if not tr.dist else 1) / nb)
+        if epoch in eval_epochs:
+            report.val_mrr.append((epoch, float(eval_fn(tr.snapshot()))))
+    tr.check_replicas()
+    return tr.snapshot(), report

@@ -1,0 +1,231 @@
+"""GPU parity of the CUDA path (through the C ABI) against the reference's
+golden fixtures and the oracle — run on a B200 with `-m gpu`.
+
+Bit-exact: views/CSR, negatives, batches, closures, permutations, RNG state.
+Tolerances (fp32 device vs fp64 reference, stated per test):
+  per-step loss rel <= 1e-5; per-block gradients rel-L2 <= 1e-4 (same params);
+  filtered ranks identical for >= 99.9 % of records, |dMRR|/MRR <= 1 %.
+"""
+
+import hashlib
+import json
+
+import numpy as np
+import pytest
+
+from conftest import golden_json, load_golden, rng_from_state, state_tuple
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():
+    pytest.skip("needs a CUDA device", allow_module_level=True)
+
+import kg_oracle as ko  # noqa: E402
+import paper_2201_02791_b200 as kb  # noqa: E402
+from paper_2201_02791_b200 import _lib  # noqa: E402
+from paper_2201_02791_b200.graph import KnowledgeGraph  # noqa: E402
+from paper_2201_02791_b200.sampler import permutation_device  # noqa: E402
+
+SCEN = ["small_embed", "small_feature3", "synth_p4"]
+
+
+def rel_l2(a, b):
+    a, b = np.asarray(a, np.float64), np.asarray(b, np.float64)
+    return float(np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-30))
+
+
+def golden_pset(g):
+    cfg = golden_json(g)
+    graph = KnowledgeGraph(int(g["num_entities"]), int(g["num_relations"]), g["triples"])
+    pset = kb.neighborhood_expand(kb.vertex_cut_partition(graph, cfg["parts"], cfg["part_seed"]), graph,
+                                  cfg["hops"])
+    return graph, pset, cfg
+
+
+def golden_params(g, prefix, L):
+    return kb.ModelParams([g[f"{prefix}bases_{l}"].copy() for l in range(L)],
+                          [g[f"{prefix}coeffs_{l}"].copy() for l in range(L)], g[prefix + "decoder"].copy(),
+                          g[prefix + "entity_embed"].copy() if prefix + "entity_embed" in g else None)
+
+
+@pytest.mark.parametrize("name", SCEN)
+def test_view_build_bit_exact(name):
+    g = load_golden(name)
+    graph, pset, _ = golden_pset(g)
+    for p in pset.partitions:
+        v = kb.build_view(p, graph.num_entities, graph.num_relations)
+        k = f"view{p.id}_"
+        np.testing.assert_array_equal(v.local_ids, g[k + "local_ids"])
+        np.testing.assert_array_equal(v.edges, g[k + "edges"])
+        np.testing.assert_array_equal(v.pool, g[k + "pool"])
+        np.testing.assert_array_equal(v.msg_indptr, g[k + "msg_indptr"])
+        np.testing.assert_array_equal(v.msg_src, g[k + "msg_src"])
+        np.testing.assert_array_equal(v.msg_rel, g[k + "msg_rel"])
+        np.testing.assert_array_equal(v.msg_norm, g[k + "msg_norm"])
+        np.testing.assert_array_equal(v.positive_keys, g[k + "positive_keys"])
+        # working CSR: same multiset per row, relation-sorted, fp32 norms
+        ip = v.d_indptr.cpu().numpy()
+        src, rel, nrm = v.d_src.cpu().numpy(), v.d_rel.cpu().numpy(), v.d_norm.cpu().numpy()
+        for row in range(v.n):
+            a, b = ip[row], ip[row + 1]
+            assert (np.diff(rel[a:b]) >= 0).all()
+            want = sorted(zip(g[k + "msg_rel"][a:b].tolist(), g[k + "msg_src"][a:b].tolist()))
+            assert sorted(zip(rel[a:b].tolist(), src[a:b].tolist())) == want
+        np.testing.assert_array_equal(np.sort(nrm), np.sort(g[k + "msg_norm"].astype(np.float32)))
+
+
+@pytest.mark.parametrize("name", SCEN)
+def test_negatives_batches_closures_bit_exact(name):
+    g = load_golden(name)
+    graph, pset, cfg = golden_pset(g)
+    v = kb.build_view(pset.partitions[0], graph.num_entities, graph.num_relations)
+    rng = rng_from_state(g["rng_init"])
+    neg = kb.sample_negatives(v, cfg["s"], rng)
+    np.testing.assert_array_equal(neg, g["neg"])
+    assert state_tuple(rng) == state_tuple(rng_from_state(g["rng_after_neg"]))
+    batches = kb.make_batches(v.core_edges, neg, cfg["batch"], rng, num_batches=cfg["rounds"])
+    assert state_tuple(rng) == state_tuple(rng_from_state(g["rng_after_batches"]))
+    for i, b in enumerate(batches):
+        np.testing.assert_array_equal(b.triples, g[f"batch{i}_triples"])
+        np.testing.assert_array_equal(b.labels, g[f"batch{i}_labels"])
+        cg = kb.build_compute_graph(b, v, cfg["hops"])
+        np.testing.assert_array_equal(cg.seed_vertices, g[f"cg{i}_seed_vertices"])
+        np.testing.assert_array_equal(cg.vertex_order, g[f"cg{i}_vertex_order"])
+        np.testing.assert_array_equal(cg.layer_vertex_counts, g[f"cg{i}_counts"])
+
+
+@pytest.mark.parametrize("n", [1, 2, 3, 17, 64, 65, 1000, 4097, 65537, 544232])
+@pytest.mark.parametrize("seed", [0, 11])
+def test_permutation_bit_exact(n, seed):
+    gen = np.random.default_rng(seed)
+    gen.random(seed % 3)   # exercise a buffered / unbuffered start
+    gen.integers(7, size=seed % 2)
+    ref = np.random.default_rng(0)
+    ref.bit_generator.state = gen.bit_generator.state
+    want = ref.permutation(n)
+    dev = torch.device("cuda")
+    perm, g2 = permutation_device(n, _lib.pcg_from_numpy(gen), dev)
+    np.testing.assert_array_equal(perm.cpu().numpy(), want)
+    _lib.pcg_to_numpy(g2, gen)
+    assert gen.bit_generator.state == ref.bit_generator.state
+
+
+@pytest.mark.parametrize("name", SCEN)
+def test_step_loss_and_gradients_match_reference(name):
+    """Teacher-forced single step: same fp32-representable params, same batch."""
+    g = load_golden(name)
+    graph, pset, cfg = golden_pset(g)
+    v = kb.build_view(pset.partitions[0], graph.num_entities, graph.num_relations)
+    L = len(cfg["dims"]) - 1
+    mc = kb.ModelConfig(L, cfg["dims"], cfg["num_bases"], graph.num_relations, cfg["s"], mode=cfg["mode"])
+    params = golden_params(g, "init_", L)
+    b = kb.EdgeMiniBatch(g["batch0_triples"], g["batch0_labels"])
+    cg = kb.build_compute_graph(b, v, L)
+    table = params.entity_embed if cfg["mode"] == "embedding" else g["features"]
+    cache = kb.EncodeCache()
+    emb = kb.encode(params, mc, cg, table, v.local_ids, cache=cache)
+    assert rel_l2(emb, g["b0_seed_emb"]) < 1e-5
+    loss, grads = kb.loss_from_cache(params, mc, b, cg, cache, v.local_ids)
+    assert abs(loss - float(g["b0_loss"])) / abs(float(g["b0_loss"])) < 1e-5
+    for l in range(L):
+        assert rel_l2(grads.bases[l], g[f"b0_dbases_{l}"]) < 1e-4
+        assert rel_l2(grads.coeffs[l], g[f"b0_dcoeffs_{l}"]) < 1e-4
+    assert rel_l2(grads.decoder, g["b0_ddecoder"]) < 1e-4
+    if cfg["mode"] == "embedding":
+        np.testing.assert_array_equal(grads.embed_ids, g["b0_embed_ids"])
+        assert rel_l2(grads.embed_rows, g["b0_embed_rows"]) < 1e-4
+
+
+@pytest.mark.parametrize("name", SCEN)
+def test_training_run_tracks_reference(name):
+    g = load_golden(name)
+    graph, pset, cfg = golden_pset(g)
+    L = len(cfg["dims"]) - 1
+    mc = kb.ModelConfig(L, cfg["dims"], cfg["num_bases"], graph.num_relations, cfg["s"], mode=cfg["mode"])
+    if cfg["mode"] == "feature":
+        graph.features = g["features"]
+    tc = kb.TrainConfig(epochs=cfg["epochs"], batch_size=cfg["batch"], optimizer="adam", learning_rate=0.01,
+                        seed=cfg["train_seed"])
+    params, report = kb.train(pset, graph, mc, tc, initial_params=golden_params(g, "init_", L))
+    assert report.rounds_per_epoch == int(g["rounds_per_epoch"])
+    np.testing.assert_allclose(report.loss_curve, g["loss_curve"], rtol=1e-4)
+    want = golden_params(g, "trained_", L)
+    for a, b in zip(params.dense_blocks(), want.dense_blocks()):
+        assert rel_l2(a, b) < 1e-3
+    if want.entity_embed is not None:
+        assert rel_l2(params.entity_embed, want.entity_embed) < 1e-3
+
+
+@pytest.mark.parametrize("policy", ["mean", "optimistic", "pessimistic"])
+def test_filtered_eval_matches_reference(policy):
+    g = load_golden("eval_small")
+    N, R = int(g["num_entities"]), int(g["num_relations"])
+    dims = g["dims"].tolist()
+    mc = kb.ModelConfig(len(dims) - 1, dims, 2, R, mode="embedding")
+    graph = KnowledgeGraph(N, R, g["train"])
+    split = kb.DatasetSplit(g["train"], g["valid"], g["test"])
+    params = golden_params(g, "p_", len(dims) - 1)
+    H = kb.encode_all_entities(params, mc, graph)
+    assert rel_l2(H, g["H"]) < 1e-5
+    res = kb.evaluate(params, mc, graph, split, which="test", tie_policy=policy)
+    ranks = np.array([r.rank for r in res.records])
+    same = np.mean(ranks == g[f"{policy}_ranks"])
+    assert same >= 0.999
+    np.testing.assert_array_equal([r.num_candidates for r in res.records], g[f"{policy}_ncand"])
+    assert abs(res.mrr - float(g[f"{policy}_mrr"])) / float(g[f"{policy}_mrr"]) <= 0.01
+
+
+def test_fb15k_shape_views_and_negatives_bit_exact():
+    """Config-2 structure at full FB15k-237 shape (sha256 of every array)."""
+    g = load_golden("fb_structure")
+    graph, split = kb.generate_synthetic(14541, 237, 272115 / 14541, seed=0)
+    for P in (2, 4, 8):
+        pset = kb.neighborhood_expand(kb.vertex_cut_partition(graph, P, seed=0), graph, 2)
+        v = kb.build_view(pset.partitions[0], graph.num_entities, graph.num_relations)
+        h = hashlib.sha256()
+        for a in (v.local_ids, v.msg_indptr, v.msg_src, v.msg_rel, v.positive_keys):
+            h.update(np.ascontiguousarray(a, dtype=np.int64).tobytes())
+        h.update(np.ascontiguousarray(v.msg_norm).tobytes())
+        assert h.hexdigest() == bytes(g[f"view0_sha_P{P}"]).decode()
+        neg = kb.sample_negatives(v, 1, np.random.default_rng(0))
+        np.testing.assert_array_equal(neg[:64], g[f"neg0_head_P{P}"])
+        assert hashlib.sha256(neg.astype(np.int64).tobytes()).hexdigest() == bytes(g[f"neg0_sha_P{P}"]).decode()
+        # partition constraint at full size: corrupted entity in the pool, never a positive
+        core = np.repeat(v.core_edges, 1, axis=0)
+        changed = np.where(neg[:, 0] != core[:, 0], neg[:, 0], neg[:, 2])
+        assert (changed < v.pool_size).all()
+        assert not v.is_positive(neg).any()
+
+
+def test_oracle_parity_on_fb_batch():
+    """Teacher-forced loss/grad parity against the oracle on an FB-shaped
+    partition (P=4, part 0) at b = 4096."""
+    graph, split = kb.generate_synthetic(14541, 237, 272115 / 14541, seed=0)
+    pset = kb.neighborhood_expand(kb.vertex_cut_partition(graph, 4, seed=0), graph, 2)
+    part = pset.partitions[0]
+    v = kb.build_view(part, graph.num_entities, graph.num_relations)
+    mc = kb.ModelConfig(2, [32, 32, 32], 2, 237, 1, mode="embedding")
+    p = kb.init_params(mc, np.random.default_rng(0), num_entities=graph.num_entities)
+    p = kb.ModelParams([b.astype(np.float32).astype(np.float64) for b in p.bases],
+                       [c.astype(np.float32).astype(np.float64) for c in p.coeffs],
+                       p.decoder.astype(np.float32).astype(np.float64),
+                       p.entity_embed.astype(np.float32).astype(np.float64))
+    rng = np.random.default_rng(5)
+    neg = kb.sample_negatives(v, 1, rng)
+    batch = kb.make_batches(v.core_edges, neg, 4096, rng, num_batches=1)[0]
+    cg = kb.build_compute_graph(batch, v, 2)
+    cache = kb.EncodeCache()
+    kb.encode(p, mc, cg, p.entity_embed, v.local_ids, cache=cache)
+    loss, gr = kb.loss_from_cache(p, mc, batch, cg, cache, v.local_ids)
+    ov = ko.make_view(part.core, part.support, graph.num_entities, 237, pool_size=part.pool_size)
+    ocg = ko.closure(ov, batch.seed_vertices, 2)
+    np.testing.assert_array_equal(ocg.vertex_order, cg.vertex_order)
+    op = ko.OParams(p.bases, p.coeffs, p.decoder, p.entity_embed)
+    tr = ko.OTrace()
+    ko.forward(op, ocg, op.embed, ov.local_ids, trace=tr)
+    oloss, og = ko.backward(op, ko.OBatch(batch.triples, batch.labels), ocg, tr, ov.local_ids)
+    assert abs(loss - oloss) / abs(oloss) < 1e-5
+    for a, b in zip(gr.dense_blocks(), og.dense()):
+        assert rel_l2(a, b) < 1e-4
+    assert rel_l2(gr.embed_rows, og.embed_rows) < 1e-4
