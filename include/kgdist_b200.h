@@ -89,6 +89,13 @@ typedef struct kg_layer_params {
 /* ---------------------------------------------------------------------- */
 int kg_abi_version(void);
 int kg_last_error(char* buf, int64_t n); /* host buffer */
+/* Number of kernels this library has launched in the process. */
+int64_t kg_launch_count(void);
+/* Bracket every launch of kernels whose name starts with `prefix` (host
+ * string) with CUDA events on the launching stream; _end synchronises and
+ * returns the summed device time and the launch count. */
+kg_status kg_kernel_timer_begin(const char* prefix);
+kg_status kg_kernel_timer_end(double* total_ms, int64_t* launches);
 
 /* ---------------------------------------------------------------------- */
 /* Primitives (stable radix sort / scan) used by every stage below          */

@@ -44,6 +44,9 @@ ST = c_int  # kg_status
 _PROTOS = {
     "kg_abi_version": (c_int, []),
     "kg_last_error": (c_int, [ctypes.c_char_p, c_int64]),
+    "kg_launch_count": (c_int64, []),
+    "kg_kernel_timer_begin": (ST, [ctypes.c_char_p]),
+    "kg_kernel_timer_end": (ST, [POINTER(c_double), POINTER(c_int64)]),
     "kg_sort_workspace_bytes": (c_int64, [c_int64]),
     "kg_sort_pairs_u64": (ST, [P, P, c_int64, c_int, P, c_int64, P]),
     "kg_scan_workspace_bytes": (c_int64, [c_int64]),

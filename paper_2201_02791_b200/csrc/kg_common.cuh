@@ -31,6 +31,26 @@ kg_status from_cuda(cudaError_t e, const char* where);
     if (_e != cudaSuccess) return ::kg::from_cuda(_e, #call);       \
   } while (0)
 
+// Every kernel launch goes through KG_LAUNCH: it counts launches
+// (kg_launch_count) and, while kg_kernel_timer_begin(prefix) is active,
+// brackets matching kernels with CUDA events on their own stream.
+struct LaunchScope {
+  cudaStream_t st;
+  int slot;
+  LaunchScope(const char* name, cudaStream_t s);
+  void done();
+};
+
+#define KG_LAUNCH(name, kern, grid, block, smem, st_, ...)          \
+  do {                                                              \
+    auto _kp = kern;                                                \
+    ::kg::LaunchScope _ls(name, st_);                               \
+    _kp<<<(grid), (block), (smem), (st_)>>>(__VA_ARGS__);           \
+    _ls.done();                                                     \
+    cudaError_t _le = cudaGetLastError();                           \
+    if (_le != cudaSuccess) return ::kg::from_cuda(_le, name);      \
+  } while (0)
+
 #define KG_REQUIRE(cond, status, ...)                               \
   do {                                                              \
     if (!(cond)) { ::kg::set_error(__VA_ARGS__); return status; }   \

@@ -230,14 +230,14 @@ kg_status kg_known_keys(const int32_t* tri, int64_t k, int32_t ca, int32_t cc, i
   char* sws = a.take<char>(sort_workspace(k));
   char* cws = a.take<char>(compact_workspace(k));
   int g = persistent_blocks(k, 256, 8);
-  k_known_keys<<<g, 256, 0, st>>>(tri, k, ca, cc, N, R, keys, vals);
+  KG_LAUNCH("k_known_keys", k_known_keys, g, 256, 0, st, tri, k, ca, cc, N, R, keys, vals);
   uint64_t maxkey = ((uint64_t)(N - 1) * R + (R - 1)) * (uint64_t)N + (N - 1);
   kg_status s = sort_pairs_u64(keys, vals, k, bits_for(maxkey), sws, sort_workspace(k), st);
   if (s != KG_OK) return s;
-  k_key_bounds<<<g, 256, 0, st>>>(keys, k, flags);
+  KG_LAUNCH("k_key_bounds", k_key_bounds, g, 256, 0, st, keys, k, flags);
   s = compact_flags(flags, k, idx, n_out, 0, nullptr, cws, compact_workspace(k), st);
   if (s != KG_OK) return s;
-  k_key_gather<<<g, 256, 0, st>>>(keys, idx, n_out, keys_out);
+  KG_LAUNCH("k_key_gather", k_key_gather, g, 256, 0, st, keys, idx, n_out, keys_out);
   KG_CHECK_LAUNCH("known keys");
   return KG_OK;
 }
@@ -259,10 +259,10 @@ kg_status kg_eval_filtered(const float* H, int32_t d, int32_t N, const float* de
   unsigned long long* gr = a.take<unsigned long long>(2 * nq);
   unsigned long long* eq = a.take<unsigned long long>(2 * nq);
   EvalArgs e{H, d, N, R, dec, qry, nq, ts, gr, eq};
-  k_true_scores<<<persistent_blocks(2 * nq, 256, 8), 256, 0, st>>>(e, ts);
-  k_rank_tiles<<<(unsigned)ceil_div(2 * nq, QB), ET, 0, st>>>(e);
+  KG_LAUNCH("k_true_scores", k_true_scores, persistent_blocks(2 * nq, 256, 8), 256, 0, st, e, ts);
+  KG_LAUNCH("k_rank_tiles", k_rank_tiles, (unsigned)ceil_div(2 * nq, QB), ET, 0, st, e);
   KG_CHECK_LAUNCH("k_rank_tiles");
-  k_rank_finish<<<persistent_blocks(2 * nq, 128, 8), 128, 0, st>>>(e, tkeys, ntk, hkeys, nhk, policy, chunk, ranks,
+  KG_LAUNCH("k_rank_finish", k_rank_finish, persistent_blocks(2 * nq, 128, 8), 128, 0, st, e, tkeys, ntk, hkeys, nhk, policy, chunk, ranks,
                                                                    ncand);
   KG_CHECK_LAUNCH("k_rank_finish");
   return KG_OK;

@@ -123,7 +123,7 @@ __global__ void k_reduce_splits(const float* __restrict__ part, int splits, int6
 kg_status gemm_nn(const GemmArgs& g, cudaStream_t st) {
   if (g.M_max <= 0 || g.N <= 0) return KG_OK;
   dim3 grid((unsigned)ceil_div(g.N, BN), (unsigned)ceil_div(g.M_max, BM), 1);
-  k_gemm<false><<<grid, GT, 0, st>>>(g);
+  KG_LAUNCH("k_gemm", (k_gemm<false>), grid, GT, 0, st, g);
   KG_CHECK_LAUNCH("k_gemm<nn>");
   return KG_OK;
 }
@@ -147,10 +147,10 @@ kg_status gemm_tn(const GemmArgs& g, float* out, void* ws, cudaStream_t st) {
   h.C = static_cast<float*>(ws);
   h.ldc = g.N;
   dim3 grid((unsigned)ceil_div(g.N, BN), (unsigned)ceil_div(g.K, BM), (unsigned)splits);
-  k_gemm<true><<<grid, GT, 0, st>>>(h);
+  KG_LAUNCH("k_gemm", (k_gemm<true>), grid, GT, 0, st, h);
   KG_CHECK_LAUNCH("k_gemm<tn>");
   int64_t cnt = g.K * g.N;
-  k_reduce_splits<<<persistent_blocks(cnt, 256, 4), 256, 0, st>>>(h.C, splits, cnt, out);
+  KG_LAUNCH("k_reduce_splits", k_reduce_splits, persistent_blocks(cnt, 256, 4), 256, 0, st, h.C, splits, cnt, out);
   KG_CHECK_LAUNCH("k_reduce_splits");
   return KG_OK;
 }

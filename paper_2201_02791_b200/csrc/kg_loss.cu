@@ -229,18 +229,18 @@ static kg_status seg_reduce(const LossArgs& la, const uint32_t* keys, const uint
                             const int32_t* ids, const int32_t* ng_dev, int32_t ng_max, float* out, SegWs& w,
                             cudaStream_t st) {
   int gb = persistent_blocks(ng_max, 256, 8);
-  k_group_bounds<<<gb, 256, 0, st>>>(keys, nelem, ids, ng_dev, ng_max, w.lo, w.nsub);
-  k_group_len<<<gb, 256, 0, st>>>(keys, nelem, ids, ng_dev, ng_max, w.hi);
+  KG_LAUNCH("k_group_bounds", k_group_bounds, gb, 256, 0, st, keys, nelem, ids, ng_dev, ng_max, w.lo, w.nsub);
+  KG_LAUNCH("k_group_len", k_group_len, gb, 256, 0, st, keys, nelem, ids, ng_dev, ng_max, w.hi);
   KG_CHECK_LAUNCH("group bounds");
   // with a device-resident group count the caller zeroed nsub[0:ng_max] so the
   // scan sees 0 beyond *ng_dev
   kg_status s = exclusive_scan_u32(w.nsub, w.sub_start, ng_max, w.total, w.scan, scan_workspace(ng_max + 1), st);
   if (s != KG_OK) return s;
   int64_t max_sub = nelem / CH + ng_max + 1;
-  k_sub_partials<KIND><<<persistent_blocks(max_sub * 32, 256, 8), 256, 0, st>>>(la, vals, w.lo, w.hi, w.sub_start,
+  KG_LAUNCH("k_sub_partials", (k_sub_partials<KIND>), persistent_blocks(max_sub * 32, 256, 8), 256, 0, st, la, vals, w.lo, w.hi, w.sub_start,
                                                                                w.total, ng_dev, ng_max, w.partial);
   KG_CHECK_LAUNCH("k_sub_partials");
-  k_group_finish<<<persistent_blocks((int64_t)ng_max * la.d, 256, 8), 256, 0, st>>>(w.partial, w.sub_start, w.nsub,
+  KG_LAUNCH("k_group_finish", k_group_finish, persistent_blocks((int64_t)ng_max * la.d, 256, 8), 256, 0, st, w.partial, w.sub_start, w.nsub,
                                                                                    ids, ng_dev, ng_max, la.d, out);
   KG_CHECK_LAUNCH("k_group_finish");
   return KG_OK;
@@ -270,7 +270,7 @@ int64_t kg_loss_workspace_bytes(int64_t b, int32_t n, int32_t d, int32_t R) {
   a.take<char>(sort32_workspace(2 * b));
   a.take<uint32_t>(n + 1);   // zero fill for nsub tail (memset range)
   seg_ws(b, R, d, nullptr, a);
-  seg_ws(2 * b, n, d, nullptr, a);
+  seg_ws(2 * b, 2 * b < (int64_t)n ? 2 * b : (int64_t)n, d, nullptr, a);
   return (int64_t)a.used + 4096;
 }
 
@@ -282,7 +282,7 @@ kg_status kg_distmult_loss(const float* H, int32_t d, int32_t n_local, const flo
   cudaStream_t st = as_stream(stream);
   KG_REQUIRE(b >= 1 && total >= 1, KG_ERR_VALIDATION, "empty batch");
   // n (local vertices) bound for seed groups: 2b distinct endpoints at most
-  int64_t ngmax = 2 * b;
+  int64_t ngmax = 2 * b < (int64_t)n_local ? 2 * b : (int64_t)n_local;
   Arena a(ws, (size_t)ws_bytes);
   float* dg = a.take<float>(b);
   float* per = a.take<float>(b);
@@ -299,15 +299,15 @@ kg_status kg_distmult_loss(const float* H, int32_t d, int32_t n_local, const flo
   KG_REQUIRE(a.used <= (size_t)ws_bytes && dg != nullptr, KG_ERR_VALIDATION, "loss workspace too small");
 
   LossArgs la{H, d, decoder, tri, labels, total, start, b, dg, per, scores_out, flags};
-  k_score<<<persistent_blocks(b * 32, 256, 8), 256, 0, st>>>(la);
+  KG_LAUNCH("k_score", k_score, persistent_blocks(b * 32, 256, 8), 256, 0, st, la);
   KG_CHECK_LAUNCH("k_score");
   int nb = persistent_blocks(b, 256, 4);
   if (nb > 1024) nb = 1024;
-  k_block_sums<<<nb, 256, 0, st>>>(per, b, part);
-  k_final_mean<<<1, 256, 0, st>>>(part, nb, b, loss_out, flags);
+  KG_LAUNCH("k_block_sums", k_block_sums, nb, 256, 0, st, per, b, part);
+  KG_LAUNCH("k_final_mean", k_final_mean, 1, 256, 0, st, part, nb, b, loss_out, flags);
   KG_CHECK_LAUNCH("loss mean");
 
-  k_loss_keys<<<persistent_blocks(b, 256, 8), 256, 0, st>>>(la, rk, rv, vk, vv);
+  KG_LAUNCH("k_loss_keys", k_loss_keys, persistent_blocks(b, 256, 8), 256, 0, st, la, rk, rv, vk, vv);
   KG_CHECK_LAUNCH("k_loss_keys");
   kg_status s = sort_pairs_u32(rk, rv, b, bits_for((uint64_t)R), sws, sort32_workspace(2 * b), st);
   if (s != KG_OK) return s;

@@ -145,18 +145,18 @@ kg_status kg_dense_step(float* params, float* m, float* v, const float* grads_al
   if (grad_clip > 0.f) {
     const float* g = grads_all;
     if (P > 1) {
-      k_tree_mean<<<blocks, 256, 0, st>>>(grads_all, P, n, gmean);
+      KG_LAUNCH("k_tree_mean", k_tree_mean, blocks, 256, 0, st, grads_all, P, n, gmean);
       g = gmean;
     }
     int nb = persistent_blocks(n, 256, 2);
     if (nb > 1024) nb = 1024;
-    k_sumsq_blocks<<<nb, 256, 0, st>>>(g, n, part);
-    k_clip_scale<<<1, 256, 0, st>>>(part, nb, grad_clip, scale);
+    KG_LAUNCH("k_sumsq_blocks", k_sumsq_blocks, nb, 256, 0, st, g, n, part);
+    KG_LAUNCH("k_clip_scale", k_clip_scale, 1, 256, 0, st, part, nb, grad_clip, scale);
     s.g = g;
     s.P = 1;
     s.scale = scale;
   }
-  k_dense_step<<<blocks, 256, 0, st>>>(s);
+  KG_LAUNCH("k_dense_step", k_dense_step, blocks, 256, 0, st, s);
   KG_CHECK_LAUNCH("k_dense_step");
   return KG_OK;
 }
@@ -164,7 +164,7 @@ kg_status kg_dense_step(float* params, float* m, float* v, const float* grads_al
 kg_status kg_sparse_step(float* table, float* m, float* v, const float* grad, const int32_t* rows,
                          const int32_t* counts, int32_t k, int32_t d, int32_t optimizer, float lr, float beta1,
                          float beta2, float eps, double bc1, double bc2, int32_t n_max, void* stream) {
-  k_sparse_step<<<persistent_blocks((int64_t)n_max * d, 256, 8), 256, 0, as_stream(stream)>>>(
+  KG_LAUNCH("k_sparse_step", k_sparse_step, persistent_blocks((int64_t)n_max * d, 256, 8), 256, 0, as_stream(stream), 
       table, m, v, grad, rows, counts, k, d, optimizer == 1, lr, beta1, beta2, eps, (float)(1.0 / bc1),
       (float)(1.0 / bc2));
   KG_CHECK_LAUNCH("k_sparse_step");

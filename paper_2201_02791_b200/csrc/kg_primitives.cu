@@ -139,7 +139,7 @@ kg_status exclusive_scan_u32(const uint32_t* in, uint32_t* out, int64_t n, uint3
     return KG_OK;
   }
   if (n <= SCAN_TILE) {
-    scan_tiles_apply<<<1, SCAN_THREADS, 0, st>>>(in, out, n, nullptr, total);
+    KG_LAUNCH("scan_tiles_apply", scan_tiles_apply, 1, SCAN_THREADS, 0, st, in, out, n, nullptr, total);
     KG_CHECK_LAUNCH("scan_tiles_apply");
     return KG_OK;
   }
@@ -147,12 +147,12 @@ kg_status exclusive_scan_u32(const uint32_t* in, uint32_t* out, int64_t n, uint3
   int64_t tiles = ceil_div(n, SCAN_TILE);
   uint32_t* sums = static_cast<uint32_t*>(ws);
   char* rest = static_cast<char*>(ws) + align_up(tiles * sizeof(uint32_t));
-  scan_tile_sums<<<(unsigned)tiles, SCAN_THREADS, 0, st>>>(in, n, sums);
+  KG_LAUNCH("scan_tile_sums", scan_tile_sums, (unsigned)tiles, SCAN_THREADS, 0, st, in, n, sums);
   KG_CHECK_LAUNCH("scan_tile_sums");
   kg_status s = exclusive_scan_u32(sums, sums, tiles, nullptr, rest,
                                    ws_bytes - align_up(tiles * sizeof(uint32_t)), st);
   if (s != KG_OK) return s;
-  scan_tiles_apply<<<(unsigned)tiles, SCAN_THREADS, 0, st>>>(in, out, n, sums, total);
+  KG_LAUNCH("scan_tiles_apply", scan_tiles_apply, (unsigned)tiles, SCAN_THREADS, 0, st, in, out, n, sums, total);
   KG_CHECK_LAUNCH("scan_tiles_apply");
   return KG_OK;
 }
@@ -257,11 +257,11 @@ static kg_status sort_pairs(K* keys, uint32_t* vals, int64_t n, int key_bits, vo
   uint32_t* vb = v2;
   for (int p = 0; p < passes; ++p) {
     int shift = 8 * p;
-    radix_hist<K><<<(unsigned)tiles, RS_THREADS, 0, st>>>(ka, n, shift, hist, tiles);
+    KG_LAUNCH("radix_hist", (radix_hist<K>), (unsigned)tiles, RS_THREADS, 0, st, ka, n, shift, hist, tiles);
     KG_CHECK_LAUNCH("radix_hist");
     kg_status s = exclusive_scan_u32(hist, hist, hist_n, nullptr, scan_ws, scan_workspace(hist_n), st);
     if (s != KG_OK) return s;
-    radix_scatter<K><<<(unsigned)tiles, RS_THREADS, 0, st>>>(ka, va, kb, vb, n, shift, hist, tiles);
+    KG_LAUNCH("radix_scatter", (radix_scatter<K>), (unsigned)tiles, RS_THREADS, 0, st, ka, va, kb, vb, n, shift, hist, tiles);
     KG_CHECK_LAUNCH("radix_scatter");
     K* tk = ka; ka = kb; kb = tk;
     uint32_t* tv = va; va = vb; vb = tv;
@@ -308,7 +308,7 @@ kg_status compact_flags(const uint32_t* flags, int64_t n, int32_t* out, int32_t*
   kg_status s = exclusive_scan_u32(flags, pos, n, total, sws, scan_workspace(n), st);
   if (s != KG_OK) return s;
   int blocks = persistent_blocks(n, 256, 8);
-  compact_scatter<<<blocks, 256, 0, st>>>(flags, pos, n, out, off_c, off_d, total, count_out);
+  KG_LAUNCH("compact_scatter", compact_scatter, blocks, 256, 0, st, flags, pos, n, out, off_c, off_d, total, count_out);
   KG_CHECK_LAUNCH("compact_scatter");
   return KG_OK;
 }
@@ -342,6 +342,66 @@ int64_t kg_scan_workspace_bytes(int64_t n) { return (int64_t)kg::scan_workspace(
 kg_status kg_exclusive_scan_u32(const uint32_t* in, uint32_t* out, int64_t n, uint32_t* total, void* ws,
                                 int64_t ws_bytes, void* stream) {
   return kg::exclusive_scan_u32(in, out, n, total, ws, (size_t)ws_bytes, kg::as_stream(stream));
+}
+
+}  // extern "C"
+
+// ---------------------------------------------------------------------------
+// Launch accounting and the live per-kernel event timer (bench.py roofline)
+// ---------------------------------------------------------------------------
+#include <vector>
+
+namespace kg {
+
+static int64_t g_launches = 0;
+static bool g_timer_on = false;
+static char g_timer_prefix[128] = "";
+static std::vector<cudaEvent_t> g_ev_start, g_ev_end;
+static size_t g_ev_used = 0;
+
+LaunchScope::LaunchScope(const char* name, cudaStream_t s) : st(s), slot(-1) {
+  ++g_launches;
+  if (!g_timer_on || strncmp(name, g_timer_prefix, strlen(g_timer_prefix)) != 0) return;
+  if (g_ev_used == g_ev_start.size()) {
+    cudaEvent_t a, b;
+    if (cudaEventCreate(&a) != cudaSuccess || cudaEventCreate(&b) != cudaSuccess) return;
+    g_ev_start.push_back(a);
+    g_ev_end.push_back(b);
+  }
+  slot = (int)g_ev_used++;
+  cudaEventRecord(g_ev_start[slot], st);
+}
+
+void LaunchScope::done() {
+  if (slot >= 0) cudaEventRecord(g_ev_end[slot], st);
+}
+
+}  // namespace kg
+
+extern "C" {
+
+int64_t kg_launch_count(void) { return kg::g_launches; }
+
+kg_status kg_kernel_timer_begin(const char* prefix) {
+  strncpy(kg::g_timer_prefix, prefix ? prefix : "", sizeof(kg::g_timer_prefix) - 1);
+  kg::g_ev_used = 0;
+  kg::g_timer_on = true;
+  return KG_OK;
+}
+
+kg_status kg_kernel_timer_end(double* total_ms, int64_t* launches) {
+  kg::g_timer_on = false;
+  double tot = 0.0;
+  for (size_t i = 0; i < kg::g_ev_used; ++i) {
+    float ms = 0.f;
+    KG_CUDA(cudaEventSynchronize(kg::g_ev_end[i]));
+    KG_CUDA(cudaEventElapsedTime(&ms, kg::g_ev_start[i], kg::g_ev_end[i]));
+    tot += ms;
+  }
+  if (total_ms) *total_ms = tot;
+  if (launches) *launches = (int64_t)kg::g_ev_used;
+  kg::g_ev_used = 0;
+  return KG_OK;
 }
 
 }  // extern "C"

@@ -399,12 +399,14 @@ __global__ void k_dbases_layout(const float* __restrict__ Rm, int B, int di, int
 static bool vec4_ok(int d) { return d % 4 == 0 && d <= 128; }
 
 template <int VEC, int S>
-static void launch_agg(const AggArgs& a, int blocks, size_t smem, cudaStream_t st) {
-  k_aggregate<VEC, S><<<blocks, 256, smem, st>>>(a);
+static kg_status launch_agg(const AggArgs& a, int blocks, size_t smem, cudaStream_t st) {
+  KG_LAUNCH("k_aggregate", (k_aggregate<VEC, S>), blocks, 256, smem, st, a);
+  return KG_OK;
 }
 template <int VEC, int S>
-static void launch_csc(const CscArgs& a, int blocks, size_t smem, cudaStream_t st) {
-  k_csc_backward<VEC, S><<<blocks, 256, smem, st>>>(a);
+static kg_status launch_csc(const CscArgs& a, int blocks, size_t smem, cudaStream_t st) {
+  KG_LAUNCH("k_csc_backward", (k_csc_backward<VEC, S>), blocks, 256, smem, st, a);
+  return KG_OK;
 }
 
 static kg_status run_aggregate(const AggArgs& a, int64_t rows_max, cudaStream_t st) {
@@ -515,8 +517,8 @@ kg_status kg_rgcn_backward(const kg_graph_csr* G, const kg_layer_params* lp, con
   size_t need = layer_ws(G->n, G->e, di, dO, B, &w, ws, (size_t)ws_bytes);
   KG_REQUIRE((size_t)ws_bytes >= need, KG_ERR_VALIDATION, "layer workspace too small");
   const int64_t wn = (int64_t)B * di * dO;
-  k_weight_views<<<persistent_blocks(wn, 256, 2), 256, 0, st>>>(lp->bases, B, di, dO, w.Wy, w.Wb);
-  k_dz<<<persistent_blocks((int64_t)G->n * dO, 256, 8), 256, 0, st>>>(dH_out, H_out, order, counts, t, dO, w.dZ);
+  KG_LAUNCH("k_weight_views", k_weight_views, persistent_blocks(wn, 256, 2), 256, 0, st, lp->bases, B, di, dO, w.Wy, w.Wb);
+  KG_LAUNCH("k_dz", k_dz, persistent_blocks((int64_t)G->n * dO, 256, 8), 256, 0, st, dH_out, H_out, order, counts, t, dO, w.dZ);
   KG_CHECK_LAUNCH("backward prep");
   // Y = X[A_{t+1}] . [V_0 | .. | V_{B-1}]
   GemmArgs gy{};
@@ -539,7 +541,7 @@ kg_status kg_rgcn_backward(const kg_graph_csr* G, const kg_layer_params* lp, con
   gv.K = di; gv.N = (int64_t)B * dO;
   s = gemm_tn(gv, w.Rm, w.tn, st);
   if (s != KG_OK) return s;
-  k_dbases_layout<<<persistent_blocks(wn, 256, 2), 256, 0, st>>>(w.Rm, B, di, dO, d_bases);
+  KG_LAUNCH("k_dbases_layout", k_dbases_layout, persistent_blocks(wn, 256, 2), 256, 0, st, w.Rm, B, di, dO, d_bases);
   if (dH_in) {
     GemmArgs gx{};
     gx.A = w.dS; gx.lda = (int64_t)B * dO;
@@ -550,7 +552,7 @@ kg_status kg_rgcn_backward(const kg_graph_csr* G, const kg_layer_params* lp, con
     s = gemm_nn(gx, st);
     if (s != KG_OK) return s;
   }
-  k_dcoeff_reduce<<<lp->G, 256, 0, st>>>(G->rel_ptr, G->rel_perm, G->c_dst, pos, counts, t, w.ed, w.ed_self, lp->G,
+  KG_LAUNCH("k_dcoeff_reduce", k_dcoeff_reduce, lp->G, 256, 0, st, G->rel_ptr, G->rel_perm, G->c_dst, pos, counts, t, w.ed, w.ed_self, lp->G,
                                          B, d_coeffs);
   KG_CHECK_LAUNCH("k_dcoeff_reduce");
   return KG_OK;

@@ -379,17 +379,16 @@ void kg_pcg64_consume32(kg_pcg64* g, uint64_t count) {
     g->has_uint32 = 0;   // numpy keeps the stale uinteger value
     count -= 1;
   }
-  uint64_t words = count / 2;
-  if (count & 1) {
-    u128 s = apply_jump(pcg_jump(words + 1, inc_of(*g)), state_of(*g));
-    uint64_t x = pcg_output(s);
-    g->state_hi = s.hi;
-    g->state_lo = s.lo;
-    g->has_uint32 = 1;
-    g->uinteger = (uint32_t)(x >> 32);
-  } else if (words) {
-    kg_pcg64_advance(g, words);
-  }
+  if (count == 0) return;
+  // ceil(count/2) fresh words; numpy leaves uinteger = high half of the last
+  // word whether or not that half was consumed (has_uint32 = count odd)
+  uint64_t words = (count + 1) / 2;
+  u128 s = apply_jump(pcg_jump(words, inc_of(*g)), state_of(*g));
+  uint64_t x = pcg_output(s);
+  g->state_hi = s.hi;
+  g->state_lo = s.lo;
+  g->has_uint32 = (count & 1) ? 1 : 0;
+  g->uinteger = (uint32_t)(x >> 32);
 }
 
 void kg_pcg64_peek64(const kg_pcg64* g, uint64_t* out, int64_t count) {
@@ -407,7 +406,7 @@ kg_status kg_neg_init(const int32_t* core, int64_t m, int32_t s, kg_pcg64 g, int
   KG_REQUIRE(m * (int64_t)s < (int64_t(1) << 31), KG_ERR_VALIDATION, "too many negatives");
   int64_t total = m * s;
   int blocks = persistent_blocks(ceil_div(total, COIN_PER_THREAD), 256, 8);
-  k_neg_init<<<blocks, 256, 0, as_stream(stream)>>>(core, m, s, g, neg, col, pending);
+  KG_LAUNCH("k_neg_init", k_neg_init, blocks, 256, 0, as_stream(stream), core, m, s, g, neg, col, pending);
   KG_CHECK_LAUNCH("k_neg_init");
   return KG_OK;
 }
@@ -434,17 +433,17 @@ kg_status kg_neg_round(int32_t* neg, const int8_t* col, const int32_t* core, int
   char* sws = a.take<char>(scan_workspace(W));
   uint32_t n = (uint32_t)pool_size;
   KG_CUDA(cudaMemsetAsync(consumed, 0, sizeof(int64_t), st));
-  k_gen_u32<<<persistent_blocks(ceil_div(W / 2 + 2, GEN_WORDS), 256, 8), 256, 0, st>>>(g, W, U);
-  k_lemire_flags<<<grid_for(W), 256, 0, st>>>(U, W, n, lemire_threshold(n), flags);
+  KG_LAUNCH("k_gen_u32", k_gen_u32, persistent_blocks(ceil_div(W / 2 + 2, GEN_WORDS), 256, 8), 256, 0, st, g, W, U);
+  KG_LAUNCH("k_lemire_flags", k_lemire_flags, grid_for(W), 256, 0, st, U, W, n, lemire_threshold(n), flags);
   KG_CHECK_LAUNCH("neg gen");
   kg_status r = exclusive_scan_u32(flags, rank, W, totals, sws, scan_workspace(W), st);
   if (r != KG_OK) return r;
-  k_neg_assign<<<grid_for(W), 256, 0, st>>>(U, flags, rank, W, n, pending, k, neg, col, core, s, n_local, R,
+  KG_LAUNCH("k_neg_assign", k_neg_assign, grid_for(W), 256, 0, st, U, flags, rank, W, n, pending, k, neg, col, core, s, n_local, R,
                                             pos_keys, n_keys, bad, consumed);
   KG_CHECK_LAUNCH("k_neg_assign");
   r = exclusive_scan_u32(bad, bad_rank, k, totals + 1, sws, scan_workspace(W), st);
   if (r != KG_OK) return r;
-  k_scatter_pending<<<grid_for(k), 256, 0, st>>>(bad, bad_rank, k, pending, next_pending, totals + 1, next_count);
+  KG_LAUNCH("k_scatter_pending", k_scatter_pending, grid_for(k), 256, 0, st, bad, bad_rank, k, pending, next_pending, totals + 1, next_count);
   KG_CHECK_LAUNCH("k_scatter_pending");
   return KG_OK;
 }
@@ -452,7 +451,7 @@ kg_status kg_neg_round(int32_t* neg, const int8_t* col, const int32_t* core, int
 kg_status kg_is_positive(const int32_t* triples, int64_t k, int32_t n_local, int32_t R, const int64_t* pos_keys,
                          const int32_t* n_keys, uint8_t* out, void* stream) {
   if (k <= 0) return KG_OK;
-  k_is_positive<<<grid_for(k), 256, 0, as_stream(stream)>>>(triples, k, n_local, R, pos_keys, n_keys, out);
+  KG_LAUNCH("k_is_positive", k_is_positive, grid_for(k), 256, 0, as_stream(stream), triples, k, n_local, R, pos_keys, n_keys, out);
   KG_CHECK_LAUNCH("k_is_positive");
   return KG_OK;
 }
@@ -472,9 +471,9 @@ kg_status kg_perm_draws_buffered(int64_t n, kg_pcg64 g, uint32_t* U, int64_t W, 
     return KG_OK;
   }
   KG_REQUIRE(W % 4 == 0 && W >= 4096, KG_ERR_VALIDATION, "draw buffer must be a multiple of 4 >= 4096");
-  k_gen_u32<<<persistent_blocks(ceil_div(W / 2 + 2, GEN_WORDS), 256, 8), 256, 0, st>>>(g, W, U);
+  KG_LAUNCH("k_gen_u32", k_gen_u32, persistent_blocks(ceil_div(W / 2 + 2, GEN_WORDS), 256, 8), 256, 0, st, g, W, U);
   KG_CHECK_LAUNCH("perm gen");
-  k_perm_draws<<<1, 32, 0, st>>>(U, W, n, js, consumed32);
+  KG_LAUNCH("k_perm_draws", k_perm_draws, 1, 32, 0, st, U, W, n, js, consumed32);
   KG_CHECK_LAUNCH("k_perm_draws");
   return KG_OK;
 }
@@ -500,15 +499,15 @@ kg_status kg_perm_resolve(const int32_t* js, int64_t n, int32_t* perm, void* ws,
   KG_CUDA(cudaMemsetAsync(cnt, 0, n * 4, st));
   KG_CUDA(cudaMemsetAsync(fill, 0, n * 4, st));
   int gb = grid_for(n);
-  k_group_count<<<gb, 256, 0, st>>>(js, n, cnt);
+  KG_LAUNCH("k_group_count", k_group_count, gb, 256, 0, st, js, n, cnt);
   kg_status r = exclusive_scan_u32(cnt, start, n, nullptr, sws, scan_workspace(n), st);
   if (r != KG_OK) return r;
-  k_group_fill<<<gb, 256, 0, st>>>(js, n, start, fill, members);
-  k_group_sort_T<<<gb, 256, 0, st>>>(members, start, cnt, n, root);
+  KG_LAUNCH("k_group_fill", k_group_fill, gb, 256, 0, st, js, n, start, fill, members);
+  KG_LAUNCH("k_group_sort_T", k_group_sort_T, gb, 256, 0, st, members, start, cnt, n, root);
   int rounds = 1;
   while ((int64_t(1) << rounds) < n) ++rounds;
-  for (int it = 0; it < rounds + 1; ++it) k_pointer_jump<<<gb, 256, 0, st>>>(root, n);
-  k_perm_final<<<gb, 256, 0, st>>>(js, n, members, start, cnt, root, perm);
+  for (int it = 0; it < rounds + 1; ++it) KG_LAUNCH("k_pointer_jump", k_pointer_jump, gb, 256, 0, st, root, n);
+  KG_LAUNCH("k_perm_final", k_perm_final, gb, 256, 0, st, js, n, members, start, cnt, root, perm);
   KG_CHECK_LAUNCH("perm resolve");
   return KG_OK;
 }
@@ -516,7 +515,7 @@ kg_status kg_perm_resolve(const int32_t* js, int64_t n, int32_t* perm, void* ws,
 kg_status kg_stream_gather(const int32_t* pos, int64_t npos, const int32_t* neg, int64_t nneg, const int32_t* perm,
                            int32_t* stream_triples, float* labels, void* stream) {
   if (npos + nneg == 0) return KG_OK;
-  k_stream_gather<<<grid_for(npos + nneg), 256, 0, as_stream(stream)>>>(pos, npos, neg, nneg, perm,
+  KG_LAUNCH("k_stream_gather", k_stream_gather, grid_for(npos + nneg), 256, 0, as_stream(stream), pos, npos, neg, nneg, perm,
                                                                         stream_triples, labels);
   KG_CHECK_LAUNCH("k_stream_gather");
   return KG_OK;
@@ -540,22 +539,22 @@ kg_status kg_closure(const int32_t* tri, int64_t total, int64_t start, int64_t b
   int32_t* bad = a.take<int32_t>(4);
   char* cws = a.take<char>(compact_workspace(n));
   int gn = grid_for(n);
-  k_closure_clear<<<gn, 256, 0, st>>>(pos, flags, n);
+  KG_LAUNCH("k_closure_clear", k_closure_clear, gn, 256, 0, st, pos, flags, n);
   KG_CUDA(cudaMemsetAsync(bad, 0, 4, st));
-  k_mark_batch<<<grid_for(b), 256, 0, st>>>(tri, total, start, b, seed_ids, n, flags, bad);
+  KG_LAUNCH("k_mark_batch", k_mark_batch, grid_for(b), 256, 0, st, tri, total, start, b, seed_ids, n, flags, bad);
   KG_CHECK_LAUNCH("closure mark");
   kg_status r = compact_flags(flags, n, order, counts, 0, nullptr, cws, compact_workspace(n), st);
   if (r != KG_OK) return r;
-  k_set_pos<<<gn, 256, 0, st>>>(order, counts, 0, pos);
+  KG_LAUNCH("k_set_pos", k_set_pos, gn, 256, 0, st, order, counts, 0, pos);
   for (int h = 0; h < hops; ++h) {
-    k_clear_u32<<<gn, 256, 0, st>>>(flags, n);
-    k_mark_sources<<<persistent_blocks((int64_t)n * 32, 256, 8), 256, 0, st>>>(order, counts, h, G->indptr, G->src,
+    KG_LAUNCH("k_clear_u32", k_clear_u32, gn, 256, 0, st, flags, n);
+    KG_LAUNCH("k_mark_sources", k_mark_sources, persistent_blocks((int64_t)n * 32, 256, 8), 256, 0, st, order, counts, h, G->indptr, G->src,
                                                                               pos, flags);
     // append newly reached vertices (ascending) after counts[h]
     r = compact_flags(flags, n, order, bad + 1, 0, counts + h, cws, compact_workspace(n), st);
     if (r != KG_OK) return r;
-    k_counts_next<<<1, 1, 0, st>>>(counts, h, bad + 1);
-    k_set_pos<<<gn, 256, 0, st>>>(order, counts, h + 1, pos);
+    KG_LAUNCH("k_counts_next", k_counts_next, 1, 1, 0, st, counts, h, bad + 1);
+    KG_LAUNCH("k_set_pos", k_set_pos, gn, 256, 0, st, order, counts, h + 1, pos);
     KG_CHECK_LAUNCH("closure hop");
   }
   return KG_OK;

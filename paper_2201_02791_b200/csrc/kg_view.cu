@@ -255,22 +255,22 @@ kg_status kg_view_local_ids(const int32_t* core, int64_t m_core, const int32_t* 
   int32_t* counts = a.take<int32_t>(2);
   char* sws = a.take<char>(sort32_workspace(N));
   int g = grid_for(N);
-  k_fill_u32<<<g, 256, 0, st>>>(first_c, N, NONE32);
-  k_fill_u32<<<g, 256, 0, st>>>(first_s, N, NONE32);
-  k_fill_i32<<<g, 256, 0, st>>>(g2l, N, -1);
+  KG_LAUNCH("k_fill_u32", k_fill_u32, g, 256, 0, st, first_c, N, NONE32);
+  KG_LAUNCH("k_fill_u32", k_fill_u32, g, 256, 0, st, first_s, N, NONE32);
+  KG_LAUNCH("k_fill_i32", k_fill_i32, g, 256, 0, st, g2l, N, -1);
   KG_CUDA(cudaMemsetAsync(counts, 0, 2 * sizeof(int32_t), st));
-  if (m_core) k_first_seen<<<grid_for(2 * m_core), 256, 0, st>>>(core, m_core, first_c, nullptr);
-  if (m_sup) k_first_seen<<<grid_for(2 * m_sup), 256, 0, st>>>(support, m_sup, first_s, first_c);
+  if (m_core) KG_LAUNCH("k_first_seen", k_first_seen, grid_for(2 * m_core), 256, 0, st, core, m_core, first_c, nullptr);
+  if (m_sup) KG_LAUNCH("k_first_seen", k_first_seen, grid_for(2 * m_sup), 256, 0, st, support, m_sup, first_s, first_c);
   KG_CHECK_LAUNCH("k_first_seen");
   uint32_t sent_c = (uint32_t)(2 * m_core), sent_s = (uint32_t)(2 * m_sup);
-  k_first_keys<<<g, 256, 0, st>>>(first_c, N, sent_c, keys, vals, counts + 0);
-  k_first_keys<<<g, 256, 0, st>>>(first_s, N, sent_s, keys2, vals2, counts + 1);
+  KG_LAUNCH("k_first_keys", k_first_keys, g, 256, 0, st, first_c, N, sent_c, keys, vals, counts + 0);
+  KG_LAUNCH("k_first_keys", k_first_keys, g, 256, 0, st, first_s, N, sent_s, keys2, vals2, counts + 1);
   KG_CHECK_LAUNCH("k_first_keys");
   kg_status s = sort_pairs_u32(keys, vals, N, bits_for(sent_c), sws, sort32_workspace(N), st);
   if (s != KG_OK) return s;
   s = sort_pairs_u32(keys2, vals2, N, bits_for(sent_s), sws, sort32_workspace(N), st);
   if (s != KG_OK) return s;
-  k_assemble_local<<<g, 256, 0, st>>>(vals, vals2, counts, N, local_ids, g2l, n_local);
+  KG_LAUNCH("k_assemble_local", k_assemble_local, g, 256, 0, st, vals, vals2, counts, N, local_ids, g2l, n_local);
   KG_CHECK_LAUNCH("k_assemble_local");
   return KG_OK;
 }
@@ -309,67 +309,67 @@ kg_status kg_view_build(const int32_t* edges_global, int64_t m, const int32_t* g
     KG_CUDA(cudaMemsetAsync(n_keys, 0, sizeof(int32_t), st));
     return KG_OK;
   }
-  k_localize<<<grid_for(m), 256, 0, st>>>(edges_global, m, g2l, el);
+  KG_LAUNCH("k_localize", k_localize, grid_for(m), 256, 0, st, edges_global, m, g2l, el);
   KG_CHECK_LAUNCH("k_localize");
 
   // destination CSR indptr (shared by reference order and working CSR)
   KG_CUDA(cudaMemsetAsync(rowcnt, 0, (n + 1) * sizeof(uint32_t), st));
-  k_count_rows<<<g, 256, 0, st>>>(el, m, 0, rowcnt);
+  KG_LAUNCH("k_count_rows", k_count_rows, g, 256, 0, st, el, m, 0, rowcnt);
   s = exclusive_scan_u32(rowcnt, rowcnt, n, nullptr, scws, scan_workspace(big), st);
   if (s != KG_OK) return s;
-  k_u32_to_i32_ptr<<<grid_for(n + 1), 256, 0, st>>>(rowcnt, G->indptr, n, (int32_t)e);
+  KG_LAUNCH("k_u32_to_i32_ptr", k_u32_to_i32_ptr, grid_for(n + 1), 256, 0, st, rowcnt, G->indptr, n, (int32_t)e);
 
   // S2: (dst, rel) runs -> counts c_{dst,rel} per message, working CSR
-  k_msg_keys<<<g, 256, 0, st>>>(el, m, R, 1, keys, perm);
+  KG_LAUNCH("k_msg_keys", k_msg_keys, g, 256, 0, st, el, m, R, 1, keys, perm);
   s = sort_pairs_u64(keys, perm, e, bits_for((uint64_t)n * 2 * R), sws, sort_workspace(big), st);
   if (s != KG_OK) return s;
-  k_boundaries<<<g, 256, 0, st>>>(keys, e, flags);
+  KG_LAUNCH("k_boundaries", k_boundaries, g, 256, 0, st, keys, e, flags);
   s = exclusive_scan_u32(flags, scan, e, nruns, scws, scan_workspace(big), st);
   if (s != KG_OK) return s;
-  k_scatter_run_starts<<<g, 256, 0, st>>>(flags, scan, e, run_start);
-  k_run_lengths<<<g, 256, 0, st>>>(flags, scan, run_start, 0, nruns, perm, e, cnt_by_msg);
-  k_gather_csr<<<g, 256, 0, st>>>(el, m, R, perm, cnt_by_msg, 0, G->src, G->rel, G->norm);
+  KG_LAUNCH("k_scatter_run_starts", k_scatter_run_starts, g, 256, 0, st, flags, scan, e, run_start);
+  KG_LAUNCH("k_run_lengths", k_run_lengths, g, 256, 0, st, flags, scan, run_start, 0, nruns, perm, e, cnt_by_msg);
+  KG_LAUNCH("k_gather_csr", k_gather_csr, g, 256, 0, st, el, m, R, perm, cnt_by_msg, 0, G->src, G->rel, G->norm);
   KG_CHECK_LAUNCH("working csr");
 
   // S1: reference order (stable by destination)
-  k_msg_keys<<<g, 256, 0, st>>>(el, m, R, 0, keys, perm);
+  KG_LAUNCH("k_msg_keys", k_msg_keys, g, 256, 0, st, el, m, R, 0, keys, perm);
   s = sort_pairs_u64(keys, perm, e, bits_for((uint64_t)n), sws, sort_workspace(big), st);
   if (s != KG_OK) return s;
-  k_gather_ref<<<g, 256, 0, st>>>(el, m, R, perm, cnt_by_msg, ref_src, ref_rel, msg_cnt);
+  KG_LAUNCH("k_gather_ref", k_gather_ref, g, 256, 0, st, el, m, R, perm, cnt_by_msg, ref_src, ref_rel, msg_cnt);
   KG_CHECK_LAUNCH("reference order");
 
   // S3: CSC by (src, rel)
   KG_CUDA(cudaMemsetAsync(rowcnt, 0, (n + 1) * sizeof(uint32_t), st));
-  k_count_rows<<<g, 256, 0, st>>>(el, m, 1, rowcnt);
+  KG_LAUNCH("k_count_rows", k_count_rows, g, 256, 0, st, el, m, 1, rowcnt);
   s = exclusive_scan_u32(rowcnt, rowcnt, n, nullptr, scws, scan_workspace(big), st);
   if (s != KG_OK) return s;
-  k_u32_to_i32_ptr<<<grid_for(n + 1), 256, 0, st>>>(rowcnt, G->c_indptr, n, (int32_t)e);
-  k_msg_keys<<<g, 256, 0, st>>>(el, m, R, 2, keys, perm);
+  KG_LAUNCH("k_u32_to_i32_ptr", k_u32_to_i32_ptr, grid_for(n + 1), 256, 0, st, rowcnt, G->c_indptr, n, (int32_t)e);
+  KG_LAUNCH("k_msg_keys", k_msg_keys, g, 256, 0, st, el, m, R, 2, keys, perm);
   s = sort_pairs_u64(keys, perm, e, bits_for((uint64_t)n * 2 * R), sws, sort_workspace(big), st);
   if (s != KG_OK) return s;
-  k_gather_csr<<<g, 256, 0, st>>>(el, m, R, perm, cnt_by_msg, 1, G->c_dst, G->c_rel, G->c_norm);
+  KG_LAUNCH("k_gather_csr", k_gather_csr, g, 256, 0, st, el, m, R, perm, cnt_by_msg, 1, G->c_dst, G->c_rel, G->c_norm);
   KG_CHECK_LAUNCH("csc");
 
   // S4: CSC positions grouped by relation
   KG_CUDA(cudaMemsetAsync(misc, 0, (2 * R + 1) * sizeof(uint32_t), st));
-  k_rel_keys<<<g, 256, 0, st>>>(G->c_rel, e, keys, perm, misc);
+  KG_LAUNCH("k_rel_keys", k_rel_keys, g, 256, 0, st, G->c_rel, e, keys, perm, misc);
   s = sort_pairs_u64(keys, perm, e, bits_for((uint64_t)2 * R), sws, sort_workspace(big), st);
   if (s != KG_OK) return s;
-  k_u32_copy_i32<<<g, 256, 0, st>>>(perm, G->rel_perm, e);
+  KG_LAUNCH("k_u32_copy_i32", k_u32_copy_i32, g, 256, 0, st, perm, G->rel_perm, e);
   s = exclusive_scan_u32(misc, misc, 2 * R, nullptr, scws, scan_workspace(big), st);
   if (s != KG_OK) return s;
-  k_u32_to_i32_ptr<<<1, 256, 0, st>>>(misc, G->rel_ptr, 2 * R, (int32_t)e);
+  KG_LAUNCH("k_u32_to_i32_ptr", k_u32_to_i32_ptr, 1, 256, 0, st, misc, G->rel_ptr, 2 * R, (int32_t)e);
   KG_CHECK_LAUNCH("relation groups");
 
   // S5: sorted unique positive keys
-  k_pos_keys<<<grid_for(m), 256, 0, st>>>(el, m, n, R, keys, perm);
+  KG_LAUNCH("k_pos_keys", k_pos_keys, grid_for(m), 256, 0, st, el, m, n, R, keys, perm);
   uint64_t maxkey = ((uint64_t)(n - 1) * (uint64_t)R + (uint64_t)(R - 1)) * (uint64_t)n + (uint64_t)(n - 1);
   s = sort_pairs_u64(keys, perm, m, bits_for(maxkey), sws, sort_workspace(big), st);
   if (s != KG_OK) return s;
-  k_boundaries<<<grid_for(m), 256, 0, st>>>(keys, m, flags);
+  KG_LAUNCH("k_boundaries", k_boundaries, grid_for(m), 256, 0, st, keys, m, flags);
   s = compact_flags(flags, m, reinterpret_cast<int32_t*>(misc), n_keys, 0, nullptr, cws, compact_workspace(big), st);
   if (s != KG_OK) return s;
-  k_gather_keys<<<grid_for(m), 256, 0, st>>>(keys, reinterpret_cast<int32_t*>(misc), n_keys, m, pos_keys);
+  KG_LAUNCH("k_gather_keys", k_gather_keys, grid_for(m), 256, 0, st, keys, reinterpret_cast<int32_t*>(misc), n_keys, m, pos_keys);
   KG_CHECK_LAUNCH("positive keys");
   return KG_OK;
 }

@@ -145,7 +145,7 @@ class DenseLayout:
         self.shapes += [(G, B)] * L
         self.shapes.append((config.num_relations, config.dims[-1]))
         self.sizes = [int(np.prod(s)) for s in self.shapes]
-        self.offsets = list(np.concatenate([[0], np.cumsum(self.sizes)[:-1]]).astype(int))
+        self.offsets = [int(x) for x in np.concatenate([[0], np.cumsum(self.sizes)[:-1]])]
         self.total = int(sum(self.sizes))
 
     def bases_off(self, l):

@@ -51,3 +51,18 @@ def test_compute_path_fails_loudly_without_cuda():
     from paper_2201_02791_b200 import errors
     with pytest.raises(errors.DeviceError):
         _lib.require_cuda()
+
+
+def test_host_consume32_matches_numpy_for_every_parity():
+    for seed in range(6):
+        for pre in (0, 1):
+            for count in (1, 2, 3, 4, 9, 10):
+                gen = np.random.default_rng(seed)
+                if pre:
+                    gen.integers(0, 2 ** 32, size=1, dtype=np.uint32)   # leave a buffered half
+                st = _lib.pcg_from_numpy(gen)
+                gen.integers(0, 2 ** 32, size=count, dtype=np.uint32)
+                _lib.pcg_consume32(st, count)
+                s = gen.bit_generator.state
+                assert ((st.state_hi << 64) | st.state_lo) == s["state"]["state"]
+                assert (st.has_uint32, st.uinteger) == (s["has_uint32"], s["uinteger"])
