@@ -284,6 +284,7 @@ def run_ours(args, world, rank, local):
                            "graph": {"entities": graph.num_entities, "relations": graph.num_relations,
                                      "train_triples": graph.num_edges}},
                 "e2e": e2e, "gpu_launches": int(launches), "roofline": roofline, "cpu_baseline": cpu,
+                "step_ms": [round(a.elapsed_time(b), 4) for a, b in evs],
                 "clocks": clk.summary()}
         print(json.dumps(line), flush=True)
 

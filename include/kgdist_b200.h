@@ -75,6 +75,24 @@ typedef struct kg_graph_csr {
   float* c_norm;      /* [e]                                              */
   int32_t* rel_perm;  /* [e]   CSC positions grouped by relation          */
   int32_t* rel_ptr;   /* [2R+1] group starts into rel_perm (+ end)        */
+  /* Static work chunks (<= `chunk` messages each) so hub rows are spread
+   * over many warps. For the CSR (ck_*) and the CSC (cc_*):
+   * ptr[n+1] chunk range of row v; row[] owning row of each chunk; slot[]
+   * partial-sum slot of a chunk whose row has > 1 chunk (-1 otherwise);
+   * split[] rows with > 1 chunk; counts[4] = {chunks, split chunks, split
+   * rows, -} (device). Capacities: chunks <= n + e/chunk + 1, split chunks
+   * <= 2e/chunk + 1, split rows <= e/chunk + 1. */
+  int32_t chunk;
+  int32_t* ck_ptr;
+  int32_t* ck_row;
+  int32_t* ck_slot;
+  int32_t* ck_split;
+  int32_t* ck_counts;
+  int32_t* cc_ptr;
+  int32_t* cc_row;
+  int32_t* cc_slot;
+  int32_t* cc_split;
+  int32_t* cc_counts;
 } kg_graph_csr;
 
 /* One RGCN layer's parameters (ref:model.py:64-79). */
@@ -96,6 +114,8 @@ int64_t kg_launch_count(void);
  * returns the summed device time and the launch count. */
 kg_status kg_kernel_timer_begin(const char* prefix);
 kg_status kg_kernel_timer_end(double* total_ms, int64_t* launches);
+/* Ends the timer and writes "name,launches,total_ms" lines (host buffer). */
+kg_status kg_kernel_timer_dump(char* buf, int64_t n);
 
 /* ---------------------------------------------------------------------- */
 /* Primitives (stable radix sort / scan) used by every stage below          */
@@ -193,13 +213,13 @@ kg_status kg_closure(const int32_t* stream_triples, int64_t total, int64_t start
 /* ---------------------------------------------------------------------- */
 /* R13-R17  RGCN layer forward / backward, DistMult + BCE                  */
 /* ---------------------------------------------------------------------- */
-int64_t kg_layer_workspace_bytes(int32_t n, int64_t e, int32_t d_in, int32_t d_out, int32_t B);
+int64_t kg_layer_workspace_bytes(const kg_graph_csr* g, int32_t d_in, int32_t d_out, int32_t B);
 /* ref:model.py:151-164, 216-220: Z[v] = sum_b (sum_{e->v} norm a[r,b] H[src]
  * + a[2R,b] H[v]) V_b for v in A_t = vertex_order[0:counts[t]];
  * H_out[v] = relu(Z) (relu != 0) or Z. H_in/H_out rows indexed by local id. */
 kg_status kg_rgcn_forward(const kg_graph_csr* g, const kg_layer_params* lp, const float* H_in, float* H_out,
-                          const int32_t* vertex_order, const int32_t* counts, int32_t t, int32_t relu,
-                          void* ws, int64_t ws_bytes, void* stream);
+                          const int32_t* vertex_order, const int32_t* pos, const int32_t* counts, int32_t t,
+                          int32_t relu, void* ws, int64_t ws_bytes, void* stream);
 /* ref:model.py:167-185, 286-296: gradients of one layer. dH_out holds
  * dL/dA of the layer output for v in A_t (by local id); H_out (NULL for the
  * last layer) supplies the ReLU mask. Writes d_bases (B,d_in,d_out),
@@ -208,6 +228,14 @@ kg_status kg_rgcn_backward(const kg_graph_csr* g, const kg_layer_params* lp, con
                            const float* H_out, const float* dH_out, float* dH_in, const int32_t* vertex_order,
                            const int32_t* pos, const int32_t* counts, int32_t t, float* d_bases,
                            float* d_coeffs, void* ws, int64_t ws_bytes, void* stream);
+/* Dense GEMM of the factored layer (standalone entry for checks):
+ * trans 0: C[c_rows(p)] = A[a_rows(p), :K] . B[K, N] (+relu), p < M;
+ * trans 1: C[K, N] = sum_{p<M} A[a_rows(p), :K]^T . B[p, :N].
+ * impl 0: tcgen05 3xTF32 tensor cores (product path); 1: CUDA-core fp32. */
+int64_t kg_gemm_workspace_bytes(int64_t M, int64_t K, int64_t N);
+kg_status kg_gemm_f32(const float* A, int64_t lda, const int32_t* a_rows, const float* B, int64_t ldb, float* C,
+                      int64_t ldc, const int32_t* c_rows, int64_t M, int64_t K, int64_t N, int32_t relu,
+                      int32_t trans, int32_t impl, void* ws, int64_t ws_bytes, void* stream);
 int64_t kg_loss_workspace_bytes(int64_t b, int32_t n, int32_t d, int32_t R);
 /* ref:model.py:254-281: DistMult scores of batch rows (start+q) mod total,
  * BCE loss (mean, device scalar), d_decoder (R,d) and dH (rows of the

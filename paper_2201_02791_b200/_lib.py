@@ -29,7 +29,10 @@ class KgGraphCsr(ctypes.Structure):
     _fields_ = [("n", c_int32), ("R", c_int32), ("e", c_int64),
                 ("indptr", c_void_p), ("src", c_void_p), ("rel", c_void_p), ("norm", c_void_p),
                 ("c_indptr", c_void_p), ("c_dst", c_void_p), ("c_rel", c_void_p), ("c_norm", c_void_p),
-                ("rel_perm", c_void_p), ("rel_ptr", c_void_p)]
+                ("rel_perm", c_void_p), ("rel_ptr", c_void_p), ("chunk", c_int32),
+                ("ck_ptr", c_void_p), ("ck_row", c_void_p), ("ck_slot", c_void_p), ("ck_split", c_void_p),
+                ("ck_counts", c_void_p), ("cc_ptr", c_void_p), ("cc_row", c_void_p), ("cc_slot", c_void_p),
+                ("cc_split", c_void_p), ("cc_counts", c_void_p)]
 
 
 class KgLayerParams(ctypes.Structure):
@@ -47,6 +50,7 @@ _PROTOS = {
     "kg_launch_count": (c_int64, []),
     "kg_kernel_timer_begin": (ST, [ctypes.c_char_p]),
     "kg_kernel_timer_end": (ST, [POINTER(c_double), POINTER(c_int64)]),
+    "kg_kernel_timer_dump": (ST, [ctypes.c_char_p, c_int64]),
     "kg_sort_workspace_bytes": (c_int64, [c_int64]),
     "kg_sort_pairs_u64": (ST, [P, P, c_int64, c_int, P, c_int64, P]),
     "kg_scan_workspace_bytes": (c_int64, [c_int64]),
@@ -70,11 +74,14 @@ _PROTOS = {
     "kg_closure_workspace_bytes": (c_int64, [c_int32]),
     "kg_closure": (ST, [P, c_int64, c_int64, c_int64, P, POINTER(KgGraphCsr), c_int32, P, P, P, P,
                         c_int64, P]),
-    "kg_layer_workspace_bytes": (c_int64, [c_int32, c_int64, c_int32, c_int32, c_int32]),
-    "kg_rgcn_forward": (ST, [POINTER(KgGraphCsr), POINTER(KgLayerParams), P, P, P, P, c_int32, c_int32,
+    "kg_layer_workspace_bytes": (c_int64, [POINTER(KgGraphCsr), c_int32, c_int32, c_int32]),
+    "kg_rgcn_forward": (ST, [POINTER(KgGraphCsr), POINTER(KgLayerParams), P, P, P, P, P, c_int32, c_int32,
                              P, c_int64, P]),
     "kg_rgcn_backward": (ST, [POINTER(KgGraphCsr), POINTER(KgLayerParams), P, P, P, P, P, P, P, c_int32,
                               P, P, P, c_int64, P]),
+    "kg_gemm_workspace_bytes": (c_int64, [c_int64, c_int64, c_int64]),
+    "kg_gemm_f32": (ST, [P, c_int64, P, P, c_int64, P, c_int64, P, c_int64, c_int64, c_int64, c_int32, c_int32,
+                         c_int32, P, c_int64, P]),
     "kg_loss_workspace_bytes": (c_int64, [c_int64, c_int32, c_int32, c_int32]),
     "kg_distmult_loss": (ST, [P, c_int32, c_int32, P, c_int32, P, P, c_int64, c_int64, c_int64, P, P, P,
                               P, P, P, P, P, c_int64, P]),
@@ -202,3 +209,20 @@ def pcg_advance(g: KgPcg64, delta: int) -> None:
 
 def pcg_consume32(g: KgPcg64, count: int) -> None:
     load().kg_pcg64_consume32(ctypes.byref(g), c_uint64(count))
+
+
+def kernel_breakdown(fn, *args, **kw):
+    """Run fn with every library launch bracketed by CUDA events (warm, in
+    situ); returns ({kernel: (launches, total_ms)}, fn's result)."""
+    lib = require_cuda()
+    lib.kg_kernel_timer_begin(b"")
+    try:
+        res = fn(*args, **kw)
+    finally:
+        buf = ctypes.create_string_buffer(1 << 16)
+        lib.kg_kernel_timer_dump(buf, 1 << 16)
+    out = {}
+    for line in buf.value.decode().splitlines():
+        name, cnt, ms = line.rsplit(",", 2)
+        out[name] = (int(cnt), float(ms))
+    return out, res

@@ -120,7 +120,7 @@ __global__ void k_reduce_splits(const float* __restrict__ part, int splits, int6
   }
 }
 
-kg_status gemm_nn(const GemmArgs& g, cudaStream_t st) {
+kg_status simt_gemm_nn(const GemmArgs& g, cudaStream_t st) {
   if (g.M_max <= 0 || g.N <= 0) return KG_OK;
   dim3 grid((unsigned)ceil_div(g.N, BN), (unsigned)ceil_div(g.M_max, BM), 1);
   KG_LAUNCH("k_gemm", (k_gemm<false>), grid, GT, 0, st, g);
@@ -136,11 +136,11 @@ int tn_splits(int64_t rows_max) {
   return (int)s;
 }
 
-size_t gemm_tn_workspace(int64_t rows_max, int64_t K, int64_t N) {
+size_t simt_gemm_tn_workspace(int64_t rows_max, int64_t K, int64_t N) {
   return align_up((size_t)tn_splits(rows_max) * K * N * sizeof(float));
 }
 
-kg_status gemm_tn(const GemmArgs& g, float* out, void* ws, cudaStream_t st) {
+kg_status simt_gemm_tn(const GemmArgs& g, float* out, void* ws, cudaStream_t st) {
   // g.K = output rows (features), g.N = output cols, g.M / M_dev = data rows
   int splits = tn_splits(g.M_max);
   GemmArgs h = g;
@@ -155,4 +155,33 @@ kg_status gemm_tn(const GemmArgs& g, float* out, void* ws, cudaStream_t st) {
   return KG_OK;
 }
 
+kg_status reduce_splits(const float* part, int splits, int64_t count, float* out, cudaStream_t st) {
+  KG_LAUNCH("k_reduce_splits", k_reduce_splits, persistent_blocks(count, 256, 4), 256, 0, st, part, splits, count, out);
+  return KG_OK;
+}
+
 }  // namespace kg
+
+using namespace kg;
+
+extern "C" {
+
+// Standalone GEMM entry (test/bench cross-checks). trans = 0: NN
+// C[c_rows(p)] = A[a_rows(p)] . B (M x K . K x N); trans = 1: TN
+// C[K x N] = sum_p A[a_rows(p), 0:K]^T Bm[p, 0:N] over M data rows.
+// impl 0 = tcgen05 3xTF32 (product path), 1 = CUDA-core fp32 reference.
+int64_t kg_gemm_workspace_bytes(int64_t M, int64_t K, int64_t N) { return (int64_t)gemm_tn_workspace(M, K, N) + 256; }
+
+kg_status kg_gemm_f32(const float* A, int64_t lda, const int32_t* a_rows, const float* B, int64_t ldb, float* C,
+                      int64_t ldc, const int32_t* c_rows, int64_t M, int64_t K, int64_t N, int32_t relu,
+                      int32_t trans, int32_t impl, void* ws, int64_t ws_bytes, void* stream) {
+  GemmArgs g{};
+  g.A = A; g.lda = lda; g.a_rows = a_rows; g.B = B; g.ldb = ldb; g.C = C; g.ldc = ldc; g.c_rows = c_rows;
+  g.M = M; g.M_max = M; g.K = K; g.N = N; g.relu = relu;
+  cudaStream_t st = as_stream(stream);
+  if (!trans) return impl ? simt_gemm_nn(g, st) : umma_gemm_nn(g, st);
+  KG_REQUIRE((size_t)ws_bytes >= gemm_tn_workspace(M, K, N), KG_ERR_VALIDATION, "gemm workspace too small");
+  return impl ? simt_gemm_tn(g, C, ws, st) : umma_gemm_tn(g, C, ws, st);
+}
+
+}  // extern "C"

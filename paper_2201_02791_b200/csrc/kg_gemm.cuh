@@ -21,8 +21,25 @@ struct GemmArgs {
   int relu;
 };
 
-kg_status gemm_nn(const GemmArgs& g, cudaStream_t st);
-size_t gemm_tn_workspace(int64_t rows_max, int64_t K, int64_t N);
-kg_status gemm_tn(const GemmArgs& g, float* out, void* ws, cudaStream_t st);
+// CUDA-core reference implementations (kg_gemm.cu): used by tests as a
+// cross-check of the tensor-core kernels.
+kg_status simt_gemm_nn(const GemmArgs& g, cudaStream_t st);
+size_t simt_gemm_tn_workspace(int64_t rows_max, int64_t K, int64_t N);
+kg_status simt_gemm_tn(const GemmArgs& g, float* out, void* ws, cudaStream_t st);
+kg_status reduce_splits(const float* part, int splits, int64_t count, float* out, cudaStream_t st);
+
+// tcgen05 3xTF32 kernels (kg_umma.cu): the product path.
+kg_status umma_gemm_nn(const GemmArgs& g, cudaStream_t st);
+size_t umma_tn_workspace(int64_t rows_max, int64_t K, int64_t N);
+kg_status umma_gemm_tn(const GemmArgs& g, float* out, void* ws, cudaStream_t st);
+
+inline kg_status gemm_nn(const GemmArgs& g, cudaStream_t st) { return umma_gemm_nn(g, st); }
+inline size_t gemm_tn_workspace(int64_t rows_max, int64_t K, int64_t N) {
+  size_t a = umma_tn_workspace(rows_max, K, N), b = simt_gemm_tn_workspace(rows_max, K, N);
+  return a > b ? a : b;
+}
+inline kg_status gemm_tn(const GemmArgs& g, float* out, void* ws, cudaStream_t st) {
+  return umma_gemm_tn(g, out, ws, st);
+}
 
 }  // namespace kg

@@ -137,7 +137,7 @@ __global__ void k_group_len(const uint32_t* __restrict__ keys, int64_t n, const 
 }
 
 // kind 0: d_dec rows (value = triple index); kind 1: dH rows (value = occurrence)
-template <int KIND>
+template <int KIND, int SL>
 __global__ void __launch_bounds__(256) k_sub_partials(LossArgs a, const uint32_t* __restrict__ vals,
                                                       const int32_t* __restrict__ lo, const int32_t* __restrict__ hi,
                                                       const uint32_t* __restrict__ sub_start,
@@ -157,30 +157,58 @@ __global__ void __launch_bounds__(256) k_sub_partials(LossArgs a, const uint32_t
       else h = mid;
     }
     const int32_t g = l;
-    int64_t r0 = lo[g] + (int64_t)(s - sub_start[g]) * CH;
-    int64_t r1 = r0 + CH < hi[g] ? r0 + CH : hi[g];
-    float* out = partial + s * (int64_t)a.d;
-    for (int k0 = 0; k0 < a.d; k0 += 32) {
-      int k = k0 + lane;
-      float acc = 0.f;
-      if (k < a.d) {
-        for (int64_t j = r0; j < r1; ++j) {
-          uint32_t v = vals[j];
-          int64_t ti = (KIND == 1 && v >= a.b) ? v - a.b : v;
-          int64_t row = row_of(a, ti);
-          int32_t hh = a.tri[row * 3], rr = a.tri[row * 3 + 1], tt = a.tri[row * 3 + 2];
-          float dg = a.dg[ti];
-          float x;
-          if (KIND == 0) {
-            x = a.H[(int64_t)hh * a.d + k] * a.H[(int64_t)tt * a.d + k];
-          } else {
-            int32_t other = (v >= a.b) ? hh : tt;
-            x = a.dec[(int64_t)rr * a.d + k] * a.H[(int64_t)other * a.d + k];
-          }
-          acc = fmaf(dg, x, acc);
+    const int64_t r0 = lo[g] + (int64_t)(s - sub_start[g]) * CH;
+    const int64_t r1 = r0 + CH < hi[g] ? r0 + CH : hi[g];
+    float acc[SL];
+#pragma unroll
+    for (int q = 0; q < SL; ++q) acc[q] = 0.f;
+    for (int64_t base = r0; base < r1; base += 32) {
+      const int cnt = (int)min((int64_t)32, r1 - base);
+      // lane i fetches the metadata of row base+i: (row A, row B, dg)
+      int32_t ra = 0, rb = 0;
+      float my_dg = 0.f;
+      if (lane < cnt) {
+        uint32_t v = vals[base + lane];
+        int64_t ti = (KIND == 1 && v >= a.b) ? v - a.b : v;
+        int64_t row = row_of(a, ti);
+        int32_t hh = a.tri[row * 3], rr = a.tri[row * 3 + 1], tt = a.tri[row * 3 + 2];
+        my_dg = a.dg[ti];
+        if (KIND == 0) {            // d m_r += dg * H[h] * H[t]
+          ra = hh;
+          rb = tt;
+        } else {                    // dH_v += dg * m_r * H[other]
+          ra = -1 - rr;             // decoder row, tagged negative
+          rb = (v >= a.b) ? hh : tt;
         }
-        out[k] = acc;
       }
+      for (int j = 0; j < cnt; j += 4) {
+        float xa[4][SL], xb[4][SL], w[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          int32_t A = __shfl_sync(0xffffffffu, ra, (j + u) & 31);
+          int32_t Bv = __shfl_sync(0xffffffffu, rb, (j + u) & 31);
+          w[u] = __shfl_sync(0xffffffffu, my_dg, (j + u) & 31);
+          const float* pa = (KIND == 0) ? a.H + (int64_t)A * a.d : a.dec + (int64_t)(-1 - A) * a.d;
+          const float* pb = a.H + (int64_t)Bv * a.d;
+#pragma unroll
+          for (int q = 0; q < SL; ++q) {
+            int k = q * 32 + lane;
+            bool ok = (j + u < cnt) && k < a.d;
+            xa[u][q] = ok ? __ldg(pa + k) : 0.f;
+            xb[u][q] = ok ? __ldg(pb + k) : 0.f;
+          }
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+#pragma unroll
+          for (int q = 0; q < SL; ++q) acc[q] = fmaf(w[u], xa[u][q] * xb[u][q], acc[q]);
+      }
+    }
+    float* out = partial + s * (int64_t)a.d;
+#pragma unroll
+    for (int q = 0; q < SL; ++q) {
+      int k = q * 32 + lane;
+      if (k < a.d) out[k] = acc[q];
     }
   }
 }
@@ -237,8 +265,12 @@ static kg_status seg_reduce(const LossArgs& la, const uint32_t* keys, const uint
   kg_status s = exclusive_scan_u32(w.nsub, w.sub_start, ng_max, w.total, w.scan, scan_workspace(ng_max + 1), st);
   if (s != KG_OK) return s;
   int64_t max_sub = nelem / CH + ng_max + 1;
-  KG_LAUNCH("k_sub_partials", (k_sub_partials<KIND>), persistent_blocks(max_sub * 32, 256, 8), 256, 0, st, la, vals, w.lo, w.hi, w.sub_start,
-                                                                               w.total, ng_dev, ng_max, w.partial);
+  int pb = persistent_blocks(max_sub * 32, 256, 8);
+  if (la.d <= 32) KG_LAUNCH("k_sub_partials", (k_sub_partials<KIND, 1>), pb, 256, 0, st, la, vals, w.lo, w.hi, w.sub_start, w.total, ng_dev, ng_max, w.partial);
+  else if (la.d <= 64) KG_LAUNCH("k_sub_partials", (k_sub_partials<KIND, 2>), pb, 256, 0, st, la, vals, w.lo, w.hi, w.sub_start, w.total, ng_dev, ng_max, w.partial);
+  else if (la.d <= 128) KG_LAUNCH("k_sub_partials", (k_sub_partials<KIND, 4>), pb, 256, 0, st, la, vals, w.lo, w.hi, w.sub_start, w.total, ng_dev, ng_max, w.partial);
+  else if (la.d <= 256) KG_LAUNCH("k_sub_partials", (k_sub_partials<KIND, 8>), pb, 256, 0, st, la, vals, w.lo, w.hi, w.sub_start, w.total, ng_dev, ng_max, w.partial);
+  else KG_REQUIRE(false, KG_ERR_SHAPE, "embedding width %d > 256 unsupported", la.d);
   KG_CHECK_LAUNCH("k_sub_partials");
   KG_LAUNCH("k_group_finish", k_group_finish, persistent_blocks((int64_t)ng_max * la.d, 256, 8), 256, 0, st, w.partial, w.sub_start, w.nsub,
                                                                                    ids, ng_dev, ng_max, la.d, out);

@@ -357,6 +357,7 @@ static int64_t g_launches = 0;
 static bool g_timer_on = false;
 static char g_timer_prefix[128] = "";
 static std::vector<cudaEvent_t> g_ev_start, g_ev_end;
+static std::vector<const char*> g_ev_name;
 static size_t g_ev_used = 0;
 
 LaunchScope::LaunchScope(const char* name, cudaStream_t s) : st(s), slot(-1) {
@@ -367,8 +368,10 @@ LaunchScope::LaunchScope(const char* name, cudaStream_t s) : st(s), slot(-1) {
     if (cudaEventCreate(&a) != cudaSuccess || cudaEventCreate(&b) != cudaSuccess) return;
     g_ev_start.push_back(a);
     g_ev_end.push_back(b);
+    g_ev_name.push_back(name);
   }
   slot = (int)g_ev_used++;
+  g_ev_name[slot] = name;
   cudaEventRecord(g_ev_start[slot], st);
 }
 
@@ -386,6 +389,33 @@ kg_status kg_kernel_timer_begin(const char* prefix) {
   strncpy(kg::g_timer_prefix, prefix ? prefix : "", sizeof(kg::g_timer_prefix) - 1);
   kg::g_ev_used = 0;
   kg::g_timer_on = true;
+  return KG_OK;
+}
+
+// Per-kernel breakdown of the launches recorded since kg_kernel_timer_begin:
+// writes "name,count,total_ms" lines into buf (host) and ends the timer.
+kg_status kg_kernel_timer_dump(char* buf, int64_t n) {
+  kg::g_timer_on = false;
+  std::vector<std::pair<const char*, std::pair<int64_t, double>>> agg;
+  for (size_t i = 0; i < kg::g_ev_used; ++i) {
+    float ms = 0.f;
+    KG_CUDA(cudaEventSynchronize(kg::g_ev_end[i]));
+    KG_CUDA(cudaEventElapsedTime(&ms, kg::g_ev_start[i], kg::g_ev_end[i]));
+    size_t j = 0;
+    for (; j < agg.size(); ++j)
+      if (strcmp(agg[j].first, kg::g_ev_name[i]) == 0) break;
+    if (j == agg.size()) agg.push_back({kg::g_ev_name[i], {0, 0.0}});
+    agg[j].second.first += 1;
+    agg[j].second.second += ms;
+  }
+  int64_t off = 0;
+  if (buf && n > 0) buf[0] = 0;
+  for (auto& a : agg) {
+    if (!buf || off >= n - 1) break;
+    off += snprintf(buf + off, (size_t)(n - off), "%s,%lld,%.6f\n", a.first, (long long)a.second.first,
+                    a.second.second);
+  }
+  kg::g_ev_used = 0;
   return KG_OK;
 }
 

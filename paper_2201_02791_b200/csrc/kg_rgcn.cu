@@ -9,15 +9,21 @@
 //             dX       = sum_b dS_b V_b^T                   (GEMM)
 //             dV_b     = X^T dS_b                            (split-K GEMM)
 //             d a[r,b] = sum_{e in r} norm_e <(X V_b)[src_e], dZ[dst_e]>
-// The gather/scatter passes are warp-per-row over the relation-sorted CSR
-// (forward) and CSC (backward): no atomics, fixed summation order.
-// Within a (row, relation) run the destination norm is constant, so the
-// forward pass sums the run's source rows first and applies norm*a[r,b] once.
+//
+// Gather/scatter passes run one warp per static work chunk (<= C messages of
+// one row, kg_chunks.cu) so preferential-attachment hubs are spread over many
+// warps; rows cut into several chunks are finished by a combine pass that
+// adds the chunk partials in order (no atomics, deterministic). Lanes cover
+// the feature dimension (float4 per lane for d % 4 == 0, d <= 128); eight
+// gathered rows are in flight per lane. Within a (row, relation) run the
+// forward norm is constant, so the run's rows are summed before applying
+// norm * a[r, b] once.
 #include "kg_gemm.cuh"
 
 namespace kg {
 
 constexpr int MAXB = 4;
+constexpr int UNR = 8;   // gathered rows in flight per lane
 
 template <int VEC>
 struct VecIO;
@@ -37,21 +43,94 @@ struct VecIO<1> {
   __device__ __forceinline__ static void store(float* p, const float* x) { *p = x[0]; }
 };
 
+// Sum x[0..7] over the 32 lanes of a warp, 9 shuffles: on return lane l holds
+// the total of entry ((l>>4)&1)*4 + ((l>>3)&1)*2 + ((l>>2)&1).
+__device__ __forceinline__ float warp_sum8(const float* x) {
+  const unsigned l = lane_id();
+  const bool b4 = l & 16, b3 = l & 8, b2 = l & 4;
+  float y[4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    float send = b4 ? x[i] : x[i + 4];
+    float keep = b4 ? x[i + 4] : x[i];
+    y[i] = keep + __shfl_xor_sync(0xffffffffu, send, 16);
+  }
+  float z[2];
+#pragma unroll
+  for (int i = 0; i < 2; ++i) {
+    float send = b3 ? y[i] : y[i + 2];
+    float keep = b3 ? y[i + 2] : y[i];
+    z[i] = keep + __shfl_xor_sync(0xffffffffu, send, 8);
+  }
+  float send = b2 ? z[0] : z[1];
+  float keep = b2 ? z[1] : z[0];
+  float w = keep + __shfl_xor_sync(0xffffffffu, send, 4);
+  w += __shfl_xor_sync(0xffffffffu, w, 2);
+  w += __shfl_xor_sync(0xffffffffu, w, 1);
+  return w;
+}
+
+__device__ __forceinline__ int sum8_entry(unsigned l) { return ((l >> 4) & 1) * 4 + ((l >> 3) & 1) * 2 + ((l >> 2) & 1); }
+
+// sum[] = sum_{k < n} p[(s0 + k) * stride] in k order, 8 loads in flight
+template <int VEC>
+__device__ __forceinline__ void sum_partials(const float* __restrict__ p, int32_t s0, int32_t n, int64_t stride,
+                                             float* sum) {
+#pragma unroll
+  for (int cc = 0; cc < VEC; ++cc) sum[cc] = 0.f;
+  int32_t k = 0;
+  for (; k + 8 <= n; k += 8) {
+    float x[8][VEC];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) VecIO<VEC>::load(p + (int64_t)(s0 + k + u) * stride, x[u]);
+#pragma unroll
+    for (int u = 0; u < 8; ++u)
+#pragma unroll
+      for (int cc = 0; cc < VEC; ++cc) sum[cc] += x[u][cc];
+  }
+  for (; k < n; ++k) {
+    float x[VEC];
+    VecIO<VEC>::load(p + (int64_t)(s0 + k) * stride, x);
+#pragma unroll
+    for (int cc = 0; cc < VEC; ++cc) sum[cc] += x[cc];
+  }
+}
+
+struct Chunks {
+  const int32_t* ptr;
+  const int32_t* row;
+  const int32_t* slot;
+  const int32_t* split;
+  const int32_t* counts;
+  int C;
+};
+
 struct AggArgs {
   const int32_t* indptr;
   const int32_t* src;
   const int32_t* rel;
   const float* norm;
+  Chunks ck;
   const float* coeffs;   // (G, B)
   int32_t G, B, d;
   const float* H;        // (n, d) by local id
-  const int32_t* order;
+  const int32_t* pos;
   const int32_t* counts;
   int t;
-  float* acc;            // (count, B*d) compact
+  float* acc;            // (count, B*d) compact by position
+  float* partial;        // (split chunks, B*d)
 };
 
-// Slot s of lane l covers features [(s*32 + l)*VEC, +VEC).
+template <int VEC, int S>
+__device__ __forceinline__ void zero3(float (&a)[MAXB][S][VEC]) {
+#pragma unroll
+  for (int b = 0; b < MAXB; ++b)
+#pragma unroll
+    for (int s = 0; s < S; ++s)
+#pragma unroll
+      for (int c = 0; c < VEC; ++c) a[b][s][c] = 0.f;
+}
+
 template <int VEC, int S>
 __global__ void __launch_bounds__(256) k_aggregate(AggArgs a) {
   extern __shared__ float coef[];
@@ -59,28 +138,30 @@ __global__ void __launch_bounds__(256) k_aggregate(AggArgs a) {
   __syncthreads();
   const int lane = lane_id();
   const int32_t T = a.counts[a.t];
+  const int32_t NC = a.ck.counts[0];
   const int d = a.d, B = a.B;
   const int warps = (gridDim.x * blockDim.x) >> 5;
   bool slot_ok[S];
 #pragma unroll
   for (int s = 0; s < S; ++s) slot_ok[s] = (s * 32 + lane) * VEC < d;
-  for (int64_t p = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; p < T; p += warps) {
-    const int32_t v = a.order[p];
+  for (int64_t c = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; c < NC; c += warps) {
+    const int32_t v = a.ck.row[c];
+    const int32_t p = a.pos[v];
+    if (p < 0 || p >= T) continue;
+    const int32_t cbase = a.ck.ptr[v];
+    const int32_t nch = a.ck.ptr[v + 1] - cbase;
+    const int32_t e_row1 = a.indptr[v + 1];
+    const int32_t beg = a.indptr[v] + (int32_t)(c - cbase) * a.ck.C;
+    const int32_t end = min(beg + a.ck.C, e_row1);
     float acc[MAXB][S][VEC];
     float run[S][VEC];
-#pragma unroll
-    for (int b = 0; b < MAXB; ++b)
-#pragma unroll
-      for (int s = 0; s < S; ++s)
-#pragma unroll
-        for (int c = 0; c < VEC; ++c) acc[b][s][c] = 0.f;
+    zero3<VEC, S>(acc);
 #pragma unroll
     for (int s = 0; s < S; ++s)
 #pragma unroll
-      for (int c = 0; c < VEC; ++c) run[s][c] = 0.f;
-    const int32_t e0 = a.indptr[v], e1 = a.indptr[v + 1];
-    for (int32_t base = e0; base < e1; base += 32) {
-      const int cnt = min(32, e1 - base);
+      for (int q = 0; q < VEC; ++q) run[s][q] = 0.f;
+    for (int32_t base = beg; base < end; base += 32) {
+      const int cnt = min(32, end - base);
       int32_t my_src = 0, my_rel = -1;
       float my_norm = 0.f;
       if (lane < cnt) {
@@ -88,11 +169,10 @@ __global__ void __launch_bounds__(256) k_aggregate(AggArgs a) {
         my_rel = a.rel[base + lane];
         my_norm = a.norm[base + lane];
       }
-      const int32_t rel_after = (base + 32 < e1) ? a.rel[base + 32] : -1;
-      for (int j = 0; j < cnt; j += 4) {
-        float xs[4][S][VEC];
+      for (int j = 0; j < cnt; j += UNR) {
+        float xs[UNR][S][VEC];
 #pragma unroll
-        for (int q = 0; q < 4; ++q) {
+        for (int q = 0; q < UNR; ++q) {
           int32_t u = __shfl_sync(0xffffffffu, my_src, (j + q) & 31);
           if (j + q < cnt) {
 #pragma unroll
@@ -101,16 +181,16 @@ __global__ void __launch_bounds__(256) k_aggregate(AggArgs a) {
           }
         }
 #pragma unroll
-        for (int q = 0; q < 4; ++q) {
+        for (int q = 0; q < UNR; ++q) {
           int32_t r = __shfl_sync(0xffffffffu, my_rel, (j + q) & 31);
           int32_t rn = __shfl_sync(0xffffffffu, my_rel, (j + q + 1) & 31);
           float w = __shfl_sync(0xffffffffu, my_norm, (j + q) & 31);
           if (j + q < cnt) {
-            if (j + q + 1 >= cnt) rn = rel_after;
+            if (j + q + 1 >= cnt) rn = -1;   // flush at the end of every 32-edge batch
 #pragma unroll
             for (int s = 0; s < S; ++s)
 #pragma unroll
-              for (int c = 0; c < VEC; ++c) run[s][c] += xs[q][s][c];
+              for (int cc = 0; cc < VEC; ++cc) run[s][cc] += xs[q][s][cc];
             if (rn != r) {
 #pragma unroll
               for (int b = 0; b < MAXB; ++b) {
@@ -119,37 +199,83 @@ __global__ void __launch_bounds__(256) k_aggregate(AggArgs a) {
 #pragma unroll
                   for (int s = 0; s < S; ++s)
 #pragma unroll
-                    for (int c = 0; c < VEC; ++c) acc[b][s][c] = fmaf(cf, run[s][c], acc[b][s][c]);
+                    for (int cc = 0; cc < VEC; ++cc) acc[b][s][cc] = fmaf(cf, run[s][cc], acc[b][s][cc]);
                 }
               }
 #pragma unroll
               for (int s = 0; s < S; ++s)
 #pragma unroll
-                for (int c = 0; c < VEC; ++c) run[s][c] = 0.f;
+                for (int cc = 0; cc < VEC; ++cc) run[s][cc] = 0.f;
             }
           }
         }
       }
     }
-    // self-loop group 2R (norm 1)
+    float* out;
+    if (nch == 1) {
+      // self-loop group 2R (norm 1), then the finished row
+      float xv[S][VEC];
+#pragma unroll
+      for (int s = 0; s < S; ++s)
+        if (slot_ok[s]) VecIO<VEC>::load(a.H + (int64_t)v * d + (s * 32 + lane) * VEC, xv[s]);
+#pragma unroll
+      for (int b = 0; b < MAXB; ++b) {
+        if (b < B) {
+          float cf = coef[(a.G - 1) * B + b];
+#pragma unroll
+          for (int s = 0; s < S; ++s)
+            if (slot_ok[s])
+#pragma unroll
+              for (int cc = 0; cc < VEC; ++cc) acc[b][s][cc] = fmaf(cf, xv[s][cc], acc[b][s][cc]);
+        }
+      }
+      out = a.acc + (int64_t)p * B * d;
+    } else {
+      out = a.partial + (int64_t)a.ck.slot[c] * B * d;
+    }
+#pragma unroll
+    for (int b = 0; b < MAXB; ++b)
+      if (b < B)
+#pragma unroll
+        for (int s = 0; s < S; ++s)
+          if (slot_ok[s]) VecIO<VEC>::store(out + (int64_t)b * d + (s * 32 + lane) * VEC, acc[b][s]);
+  }
+}
+
+// rows cut into several chunks: acc[p] = sum of chunk partials (in order) + self loop
+template <int VEC, int S>
+__global__ void __launch_bounds__(256) k_aggregate_combine(AggArgs a) {
+  const int lane = lane_id();
+  const int32_t T = a.counts[a.t];
+  const int32_t NS = a.ck.counts[2];
+  const int d = a.d, B = a.B;
+  const int warps = (gridDim.x * blockDim.x) >> 5;
+  bool slot_ok[S];
+#pragma unroll
+  for (int s = 0; s < S; ++s) slot_ok[s] = (s * 32 + lane) * VEC < d;
+  for (int64_t r = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; r < NS; r += warps) {
+    const int32_t v = a.ck.split[r];
+    const int32_t p = a.pos[v];
+    if (p < 0 || p >= T) continue;
+    const int32_t c0 = a.ck.ptr[v], c1 = a.ck.ptr[v + 1];
+    const int32_t s0 = a.ck.slot[c0];
     float xv[S][VEC];
 #pragma unroll
     for (int s = 0; s < S; ++s)
       if (slot_ok[s]) VecIO<VEC>::load(a.H + (int64_t)v * d + (s * 32 + lane) * VEC, xv[s]);
-    float* out = a.acc + p * (int64_t)B * d;
+    float* out = a.acc + (int64_t)p * B * d;
+    for (int b = 0; b < B; ++b) {
+      float cf = a.coeffs[(a.G - 1) * B + b];
 #pragma unroll
-    for (int b = 0; b < MAXB; ++b) {
-      if (b < B) {
-        float cf = coef[(a.G - 1) * B + b];
+      for (int s = 0; s < S; ++s) {
+        if (!slot_ok[s]) continue;
+        float sum[VEC];
 #pragma unroll
-        for (int s = 0; s < S; ++s) {
-          if (slot_ok[s]) {
-            float o[VEC];
+        for (int cc = 0; cc < VEC; ++cc) sum[cc] = 0.f;
+        sum_partials<VEC>(a.partial + (int64_t)b * d + (s * 32 + lane) * VEC, s0, c1 - c0, (int64_t)B * d, sum);
 #pragma unroll
-            for (int c = 0; c < VEC; ++c) o[c] = fmaf(cf, xv[s][c], acc[b][s][c]);
-            VecIO<VEC>::store(out + (int64_t)b * d + (s * 32 + lane) * VEC, o);
-          }
-        }
+        for (int cc = 0; cc < VEC; ++cc) sum[cc] = fmaf(cf, xv[s][cc], sum[cc]);
+        VecIO<VEC>::store(out + (int64_t)b * d + (s * 32 + lane) * VEC, sum);
       }
     }
   }
@@ -160,17 +286,18 @@ struct CscArgs {
   const int32_t* c_dst;
   const int32_t* c_rel;
   const float* c_norm;
+  Chunks ck;
   const float* coeffs;   // (G, B)
   int32_t G, B, d;       // d = d_out
-  const float* Y;        // (count_S, B*d) compact: X V_b per source
+  const float* Y;        // (count_S, B*d) compact: X V_b per source position
   const float* dZ;       // (count_T, d) compact
-  const int32_t* order;
   const int32_t* pos;
   const int32_t* counts;
   int t;                 // targets A_t, sources A_{t+1}
   float* dS;             // (count_S, B*d)
   float* ed;             // (e, B) per CSC position
   float* ed_self;        // (count_T, B)
+  float* partial;        // (split chunks, B*d)
 };
 
 template <int VEC, int S>
@@ -178,140 +305,208 @@ __global__ void __launch_bounds__(256) k_csc_backward(CscArgs a) {
   extern __shared__ float coef[];
   for (int i = threadIdx.x; i < a.G * a.B; i += blockDim.x) coef[i] = a.coeffs[i];
   __syncthreads();
-  const int lane = lane_id();
+  const unsigned lane = lane_id();
   const int32_t T = a.counts[a.t];
   const int32_t Sn = a.counts[a.t + 1];
+  const int32_t NC = a.ck.counts[0];
   const int d = a.d, B = a.B;
   const int warps = (gridDim.x * blockDim.x) >> 5;
   bool slot_ok[S];
 #pragma unroll
   for (int s = 0; s < S; ++s) slot_ok[s] = (s * 32 + lane) * VEC < d;
-  for (int64_t q = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; q < Sn; q += warps) {
-    const int32_t u = a.order[q];
+  for (int64_t c = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; c < NC; c += warps) {
+    const int32_t u = a.ck.row[c];
+    const int32_t q = a.pos[u];
+    if (q < 0 || q >= Sn) continue;
+    const int32_t cbase = a.ck.ptr[u];
+    const int32_t nch = a.ck.ptr[u + 1] - cbase;
+    const int32_t e_row1 = a.c_indptr[u + 1];
+    const int32_t beg = a.c_indptr[u] + (int32_t)(c - cbase) * a.ck.C;
+    const int32_t end = min(beg + a.ck.C, e_row1);
     float y[MAXB][S][VEC];
     float acc[MAXB][S][VEC];
     float run[S][VEC];
-#pragma unroll
-    for (int b = 0; b < MAXB; ++b)
-#pragma unroll
-      for (int s = 0; s < S; ++s)
-#pragma unroll
-        for (int c = 0; c < VEC; ++c) { acc[b][s][c] = 0.f; y[b][s][c] = 0.f; }
+    zero3<VEC, S>(acc);
+    zero3<VEC, S>(y);
 #pragma unroll
     for (int b = 0; b < MAXB; ++b)
       if (b < B)
 #pragma unroll
         for (int s = 0; s < S; ++s)
-          if (slot_ok[s]) VecIO<VEC>::load(a.Y + (q * B + b) * (int64_t)d + (s * 32 + lane) * VEC, y[b][s]);
+          if (slot_ok[s]) VecIO<VEC>::load(a.Y + ((int64_t)q * B + b) * d + (s * 32 + lane) * VEC, y[b][s]);
 #pragma unroll
     for (int s = 0; s < S; ++s)
 #pragma unroll
-      for (int c = 0; c < VEC; ++c) run[s][c] = 0.f;
-    const int32_t e0 = a.c_indptr[u], e1 = a.c_indptr[u + 1];
-    for (int32_t base = e0; base < e1; base += 32) {
-      const int cnt = min(32, e1 - base);
-      int32_t my_dst = 0, my_rel = -1, my_pw = -1;
+      for (int cc = 0; cc < VEC; ++cc) run[s][cc] = 0.f;
+    for (int32_t base = beg; base < end; base += 32) {
+      const int cnt = min(32, end - base);
+      int32_t my_rel = -1, my_pw = -1;
       float my_norm = 0.f;
-      if (lane < cnt) {
-        my_dst = a.c_dst[base + lane];
+      if ((int)lane < cnt) {
+        int32_t w = a.c_dst[base + lane];
         my_rel = a.c_rel[base + lane];
         my_norm = a.c_norm[base + lane];
-        int32_t pw = a.pos[my_dst];
+        int32_t pw = a.pos[w];
         my_pw = (pw >= 0 && pw < T) ? pw : -1;
       }
-      const int32_t rel_after = (base + 32 < e1) ? a.c_rel[base + 32] : -1;
-      float my_dot[MAXB];
+      for (int j = 0; j < cnt; j += UNR) {
+        float zs[UNR][S][VEC];
 #pragma unroll
-      for (int b = 0; b < MAXB; ++b) my_dot[b] = 0.f;
-      for (int j = 0; j < cnt; ++j) {
-        int32_t pw = __shfl_sync(0xffffffffu, my_pw, j);
-        int32_t r = __shfl_sync(0xffffffffu, my_rel, j);
-        int32_t rn = __shfl_sync(0xffffffffu, my_rel, (j + 1) & 31);
-        if (j + 1 >= cnt) rn = rel_after;
-        float w = __shfl_sync(0xffffffffu, my_norm, j);
-        if (pw >= 0) {
-          float z[S][VEC];
+        for (int k = 0; k < UNR; ++k) {
+          int32_t pw = __shfl_sync(0xffffffffu, my_pw, (j + k) & 31);
 #pragma unroll
           for (int s = 0; s < S; ++s) {
-            if (slot_ok[s]) VecIO<VEC>::load(a.dZ + (int64_t)pw * d + (s * 32 + lane) * VEC, z[s]);
+            if (j + k < cnt && pw >= 0 && slot_ok[s])
+              VecIO<VEC>::load(a.dZ + (int64_t)pw * d + (s * 32 + lane) * VEC, zs[k][s]);
             else
 #pragma unroll
-              for (int c = 0; c < VEC; ++c) z[s][c] = 0.f;
+              for (int cc = 0; cc < VEC; ++cc) zs[k][s][cc] = 0.f;
           }
+        }
+        // per-edge dots <Y_b[u], dZ[dst]> for the 8 edges, one transposed warp reduction per b
 #pragma unroll
-          for (int s = 0; s < S; ++s)
+        for (int b = 0; b < MAXB; ++b) {
+          if (b < B) {
+            float part[UNR];
 #pragma unroll
-            for (int c = 0; c < VEC; ++c) run[s][c] = fmaf(w, z[s][c], run[s][c]);
-#pragma unroll
-          for (int b = 0; b < MAXB; ++b) {
-            if (b < B) {
+            for (int k = 0; k < UNR; ++k) {
               float dp = 0.f;
 #pragma unroll
               for (int s = 0; s < S; ++s)
 #pragma unroll
-                for (int c = 0; c < VEC; ++c) dp = fmaf(y[b][s][c], z[s][c], dp);
-              dp = warp_sum(dp);
-              if (lane == j) my_dot[b] = w * dp;
+                for (int cc = 0; cc < VEC; ++cc) dp = fmaf(y[b][s][cc], zs[k][s][cc], dp);
+              part[k] = dp;
             }
+            float tot = warp_sum8(part);
+            int k = sum8_entry(lane);
+            float wk = __shfl_sync(0xffffffffu, my_norm, (j + k) & 31);
+            if ((lane & 3) == 0 && j + k < cnt) a.ed[(int64_t)(base + j + k) * B + b] = wk * tot;
           }
         }
-        if (rn != r) {
+        // dS runs
 #pragma unroll
-          for (int b = 0; b < MAXB; ++b) {
-            if (b < B && r >= 0) {
-              float cf = coef[r * B + b];
+        for (int k = 0; k < UNR; ++k) {
+          int32_t r = __shfl_sync(0xffffffffu, my_rel, (j + k) & 31);
+          int32_t rn = __shfl_sync(0xffffffffu, my_rel, (j + k + 1) & 31);
+          float w = __shfl_sync(0xffffffffu, my_norm, (j + k) & 31);
+          if (j + k < cnt) {
+            if (j + k + 1 >= cnt) rn = -1;
+#pragma unroll
+            for (int s = 0; s < S; ++s)
+#pragma unroll
+              for (int cc = 0; cc < VEC; ++cc) run[s][cc] = fmaf(w, zs[k][s][cc], run[s][cc]);
+            if (rn != r) {
+#pragma unroll
+              for (int b = 0; b < MAXB; ++b) {
+                if (b < B) {
+                  float cf = coef[r * B + b];
+#pragma unroll
+                  for (int s = 0; s < S; ++s)
+#pragma unroll
+                    for (int cc = 0; cc < VEC; ++cc) acc[b][s][cc] = fmaf(cf, run[s][cc], acc[b][s][cc]);
+                }
+              }
 #pragma unroll
               for (int s = 0; s < S; ++s)
 #pragma unroll
-                for (int c = 0; c < VEC; ++c) acc[b][s][c] = fmaf(cf, run[s][c], acc[b][s][c]);
+                for (int cc = 0; cc < VEC; ++cc) run[s][cc] = 0.f;
             }
           }
-#pragma unroll
-          for (int s = 0; s < S; ++s)
-#pragma unroll
-            for (int c = 0; c < VEC; ++c) run[s][c] = 0.f;
-        }
-      }
-      if (lane < cnt && my_pw >= 0) {
-#pragma unroll
-        for (int b = 0; b < MAXB; ++b)
-          if (b < B) a.ed[(int64_t)(base + lane) * B + b] = my_dot[b];
-      }
-    }
-    // self-loop (u is a target iff q < T)
-    if (q < T) {
-      float z[S][VEC];
-#pragma unroll
-      for (int s = 0; s < S; ++s) {
-        if (slot_ok[s]) VecIO<VEC>::load(a.dZ + q * (int64_t)d + (s * 32 + lane) * VEC, z[s]);
-        else
-#pragma unroll
-          for (int c = 0; c < VEC; ++c) z[s][c] = 0.f;
-      }
-#pragma unroll
-      for (int b = 0; b < MAXB; ++b) {
-        if (b < B) {
-          float cf = coef[(a.G - 1) * B + b];
-          float dp = 0.f;
-#pragma unroll
-          for (int s = 0; s < S; ++s)
-#pragma unroll
-            for (int c = 0; c < VEC; ++c) {
-              acc[b][s][c] = fmaf(cf, z[s][c], acc[b][s][c]);
-              dp = fmaf(y[b][s][c], z[s][c], dp);
-            }
-          dp = warp_sum(dp);
-          if (lane == 0) a.ed_self[q * B + b] = dp;
         }
       }
     }
-    float* out = a.dS + q * (int64_t)B * d;
+    float* out;
+    if (nch == 1) {
+      if (q < T) {
+        // self-loop (norm 1): dS += a[2R,b] dZ[u]; self dot for d a[2R,b]
+        float z[S][VEC];
+#pragma unroll
+        for (int s = 0; s < S; ++s) {
+          if (slot_ok[s]) VecIO<VEC>::load(a.dZ + (int64_t)q * d + (s * 32 + lane) * VEC, z[s]);
+          else
+#pragma unroll
+            for (int cc = 0; cc < VEC; ++cc) z[s][cc] = 0.f;
+        }
+#pragma unroll
+        for (int b = 0; b < MAXB; ++b) {
+          if (b < B) {
+            float cf = coef[(a.G - 1) * B + b];
+            float dp = 0.f;
+#pragma unroll
+            for (int s = 0; s < S; ++s)
+#pragma unroll
+              for (int cc = 0; cc < VEC; ++cc) {
+                acc[b][s][cc] = fmaf(cf, z[s][cc], acc[b][s][cc]);
+                dp = fmaf(y[b][s][cc], z[s][cc], dp);
+              }
+            dp = warp_sum(dp);
+            if (lane == 0) a.ed_self[(int64_t)q * B + b] = dp;
+          }
+        }
+      }
+      out = a.dS + (int64_t)q * B * d;
+    } else {
+      out = a.partial + (int64_t)a.ck.slot[c] * B * d;
+    }
 #pragma unroll
     for (int b = 0; b < MAXB; ++b)
       if (b < B)
 #pragma unroll
         for (int s = 0; s < S; ++s)
           if (slot_ok[s]) VecIO<VEC>::store(out + (int64_t)b * d + (s * 32 + lane) * VEC, acc[b][s]);
+  }
+}
+
+template <int VEC, int S>
+__global__ void __launch_bounds__(256) k_csc_combine(CscArgs a) {
+  const unsigned lane = lane_id();
+  const int32_t T = a.counts[a.t];
+  const int32_t Sn = a.counts[a.t + 1];
+  const int32_t NS = a.ck.counts[2];
+  const int d = a.d, B = a.B;
+  const int warps = (gridDim.x * blockDim.x) >> 5;
+  bool slot_ok[S];
+#pragma unroll
+  for (int s = 0; s < S; ++s) slot_ok[s] = (s * 32 + lane) * VEC < d;
+  for (int64_t r = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; r < NS; r += warps) {
+    const int32_t u = a.ck.split[r];
+    const int32_t q = a.pos[u];
+    if (q < 0 || q >= Sn) continue;
+    const int32_t c0 = a.ck.ptr[u], c1 = a.ck.ptr[u + 1];
+    const int32_t s0 = a.ck.slot[c0];
+    float z[S][VEC];
+    const bool self = q < T;
+#pragma unroll
+    for (int s = 0; s < S; ++s) {
+      if (self && slot_ok[s]) VecIO<VEC>::load(a.dZ + (int64_t)q * d + (s * 32 + lane) * VEC, z[s]);
+      else
+#pragma unroll
+        for (int cc = 0; cc < VEC; ++cc) z[s][cc] = 0.f;
+    }
+    float* out = a.dS + (int64_t)q * B * d;
+    for (int b = 0; b < B; ++b) {
+      float cf = a.coeffs[(a.G - 1) * B + b];
+      float dp = 0.f;
+#pragma unroll
+      for (int s = 0; s < S; ++s) {
+        float sum[VEC];
+#pragma unroll
+        for (int cc = 0; cc < VEC; ++cc) sum[cc] = 0.f;
+        if (slot_ok[s]) {
+          sum_partials<VEC>(a.partial + (int64_t)b * d + (s * 32 + lane) * VEC, s0, c1 - c0, (int64_t)B * d, sum);
+          float yv[VEC];
+          VecIO<VEC>::load(a.Y + ((int64_t)q * B + b) * d + (s * 32 + lane) * VEC, yv);
+#pragma unroll
+          for (int cc = 0; cc < VEC; ++cc) {
+            sum[cc] = fmaf(cf, z[s][cc], sum[cc]);
+            dp = fmaf(yv[cc], z[s][cc], dp);
+          }
+          VecIO<VEC>::store(out + (int64_t)b * d + (s * 32 + lane) * VEC, sum);
+        }
+      }
+      dp = warp_sum(dp);
+      if (self && lane == 0) a.ed_self[(int64_t)q * B + b] = dp;
+    }
   }
 }
 
@@ -399,46 +594,61 @@ __global__ void k_dbases_layout(const float* __restrict__ Rm, int B, int di, int
 static bool vec4_ok(int d) { return d % 4 == 0 && d <= 128; }
 
 template <int VEC, int S>
-static kg_status launch_agg(const AggArgs& a, int blocks, size_t smem, cudaStream_t st) {
+static kg_status launch_agg(const AggArgs& a, int blocks, int cblocks, size_t smem, cudaStream_t st) {
   KG_LAUNCH("k_aggregate", (k_aggregate<VEC, S>), blocks, 256, smem, st, a);
+  KG_LAUNCH("k_aggregate_combine", (k_aggregate_combine<VEC, S>), cblocks, 256, 0, st, a);
   return KG_OK;
 }
 template <int VEC, int S>
-static kg_status launch_csc(const CscArgs& a, int blocks, size_t smem, cudaStream_t st) {
+static kg_status launch_csc(const CscArgs& a, int blocks, int cblocks, size_t smem, cudaStream_t st) {
   KG_LAUNCH("k_csc_backward", (k_csc_backward<VEC, S>), blocks, 256, smem, st, a);
+  KG_LAUNCH("k_csc_combine", (k_csc_combine<VEC, S>), cblocks, 256, 0, st, a);
   return KG_OK;
 }
 
-static kg_status run_aggregate(const AggArgs& a, int64_t rows_max, cudaStream_t st) {
-  int blocks = persistent_blocks(rows_max * 32, 256, 8);
-  size_t smem = (size_t)a.G * a.B * sizeof(float);
-  int d = a.d;
-  if (vec4_ok(d)) launch_agg<4, 1>(a, blocks, smem, st);
-  else if (d <= 32) launch_agg<1, 1>(a, blocks, smem, st);
-  else if (d <= 64) launch_agg<1, 2>(a, blocks, smem, st);
-  else if (d <= 128) launch_agg<1, 4>(a, blocks, smem, st);
-  else if (d <= 256) launch_agg<1, 8>(a, blocks, smem, st);
-  else KG_REQUIRE(false, KG_ERR_SHAPE, "feature width %d > 256 unsupported", d);
-  KG_CHECK_LAUNCH("k_aggregate");
-  return KG_OK;
+// chunk capacities of kg_graph_csr (see the header)
+static int64_t cap_chunks(const kg_graph_csr* G) { return (int64_t)G->n + G->e / G->chunk + 1; }
+static int64_t cap_split_chunks(const kg_graph_csr* G) { return 2 * G->e / G->chunk + 1; }
+static int64_t cap_split_rows(const kg_graph_csr* G) { return G->e / G->chunk + 1; }
+
+template <typename Args, typename F4, typename F1a, typename F1b, typename F1c, typename F1d>
+static kg_status dispatch_width(int d, F4 f4, F1a f1, F1b f2, F1c f4s, F1d f8) {
+  if (vec4_ok(d)) return f4();
+  if (d <= 32) return f1();
+  if (d <= 64) return f2();
+  if (d <= 128) return f4s();
+  if (d <= 256) return f8();
+  KG_REQUIRE(false, KG_ERR_SHAPE, "feature width %d > 256 unsupported", d);
+  return KG_ERR_SHAPE;
 }
 
-static kg_status run_csc(const CscArgs& a, int64_t rows_max, cudaStream_t st) {
-  int blocks = persistent_blocks(rows_max * 32, 256, 8);
+static kg_status run_aggregate(const AggArgs& a, const kg_graph_csr* G, cudaStream_t st) {
+  int blocks = persistent_blocks(cap_chunks(G) * 32, 256, 8);
+  int cblocks = persistent_blocks(cap_split_rows(G) * 32, 256, 8);
   size_t smem = (size_t)a.G * a.B * sizeof(float);
-  int d = a.d;
-  if (vec4_ok(d)) launch_csc<4, 1>(a, blocks, smem, st);
-  else if (d <= 32) launch_csc<1, 1>(a, blocks, smem, st);
-  else if (d <= 64) launch_csc<1, 2>(a, blocks, smem, st);
-  else if (d <= 128) launch_csc<1, 4>(a, blocks, smem, st);
-  else if (d <= 256) launch_csc<1, 8>(a, blocks, smem, st);
-  else KG_REQUIRE(false, KG_ERR_SHAPE, "feature width %d > 256 unsupported", d);
-  KG_CHECK_LAUNCH("k_csc_backward");
-  return KG_OK;
+  return dispatch_width<AggArgs>(
+      a.d, [&] { return launch_agg<4, 1>(a, blocks, cblocks, smem, st); },
+      [&] { return launch_agg<1, 1>(a, blocks, cblocks, smem, st); },
+      [&] { return launch_agg<1, 2>(a, blocks, cblocks, smem, st); },
+      [&] { return launch_agg<1, 4>(a, blocks, cblocks, smem, st); },
+      [&] { return launch_agg<1, 8>(a, blocks, cblocks, smem, st); });
+}
+
+static kg_status run_csc(const CscArgs& a, const kg_graph_csr* G, cudaStream_t st) {
+  int blocks = persistent_blocks(cap_chunks(G) * 32, 256, 8);
+  int cblocks = persistent_blocks(cap_split_rows(G) * 32, 256, 8);
+  size_t smem = (size_t)a.G * a.B * sizeof(float);
+  return dispatch_width<CscArgs>(
+      a.d, [&] { return launch_csc<4, 1>(a, blocks, cblocks, smem, st); },
+      [&] { return launch_csc<1, 1>(a, blocks, cblocks, smem, st); },
+      [&] { return launch_csc<1, 2>(a, blocks, cblocks, smem, st); },
+      [&] { return launch_csc<1, 4>(a, blocks, cblocks, smem, st); },
+      [&] { return launch_csc<1, 8>(a, blocks, cblocks, smem, st); });
 }
 
 struct LayerWs {
   float* acc;     // forward (n, B*d_in)
+  float* partial; // (split chunks, B*max(d_in, d_out))
   float* Wy;      // (d_in, B*d_out)
   float* Wb;      // (B*d_out, d_in)
   float* dZ;      // (n, d_out)
@@ -450,10 +660,12 @@ struct LayerWs {
   char* tn;       // split-K partials
 };
 
-static size_t layer_ws(int64_t n, int64_t e, int di, int dO, int B, LayerWs* w, void* base, size_t cap) {
+static size_t layer_ws(int64_t n, int64_t e, int64_t split_chunks, int di, int dO, int B, LayerWs* w, void* base,
+                       size_t cap) {
   Arena a(base, cap);
   LayerWs l;
   l.acc = a.take<float>((size_t)n * B * di);
+  l.partial = a.take<float>((size_t)split_chunks * B * (di > dO ? di : dO));
   l.Wy = a.take<float>((size_t)B * di * dO);
   l.Wb = a.take<float>((size_t)B * di * dO);
   l.dZ = a.take<float>((size_t)n * dO);
@@ -467,27 +679,35 @@ static size_t layer_ws(int64_t n, int64_t e, int di, int dO, int B, LayerWs* w, 
   return a.used + 256;
 }
 
+static Chunks csr_chunks(const kg_graph_csr* G) {
+  return Chunks{G->ck_ptr, G->ck_row, G->ck_slot, G->ck_split, G->ck_counts, G->chunk};
+}
+static Chunks csc_chunks(const kg_graph_csr* G) {
+  return Chunks{G->cc_ptr, G->cc_row, G->cc_slot, G->cc_split, G->cc_counts, G->chunk};
+}
+
 }  // namespace kg
 
 using namespace kg;
 
 extern "C" {
 
-int64_t kg_layer_workspace_bytes(int32_t n, int64_t e, int32_t d_in, int32_t d_out, int32_t B) {
-  return (int64_t)layer_ws(n, e, d_in, d_out, B, nullptr, nullptr, 0);
+int64_t kg_layer_workspace_bytes(const kg_graph_csr* G, int32_t d_in, int32_t d_out, int32_t B) {
+  return (int64_t)layer_ws(G->n, G->e, cap_split_chunks(G), d_in, d_out, B, nullptr, nullptr, 0);
 }
 
 kg_status kg_rgcn_forward(const kg_graph_csr* G, const kg_layer_params* lp, const float* H_in, float* H_out,
-                          const int32_t* order, const int32_t* counts, int32_t t, int32_t relu, void* ws,
-                          int64_t ws_bytes, void* stream) {
+                          const int32_t* order, const int32_t* pos, const int32_t* counts, int32_t t, int32_t relu,
+                          void* ws, int64_t ws_bytes, void* stream) {
   cudaStream_t st = as_stream(stream);
   KG_REQUIRE(lp->B >= 1 && lp->B <= MAXB, KG_ERR_VALIDATION, "num_bases must be in [1, %d]", MAXB);
   KG_REQUIRE(lp->G == 2 * G->R + 1, KG_ERR_SHAPE, "coeff groups %d != 2R+1", lp->G);
   LayerWs w;
-  size_t need = layer_ws(G->n, G->e, lp->d_in, lp->d_out, lp->B, &w, ws, (size_t)ws_bytes);
+  size_t need = layer_ws(G->n, G->e, cap_split_chunks(G), lp->d_in, lp->d_out, lp->B, &w, ws, (size_t)ws_bytes);
   KG_REQUIRE((size_t)ws_bytes >= need, KG_ERR_VALIDATION, "layer workspace too small");
-  AggArgs a{G->indptr, G->src, G->rel, G->norm, lp->coeffs, lp->G, lp->B, lp->d_in, H_in, order, counts, t, w.acc};
-  kg_status s = run_aggregate(a, G->n, st);
+  AggArgs a{G->indptr, G->src, G->rel, G->norm, csr_chunks(G), lp->coeffs, lp->G, lp->B, lp->d_in, H_in, pos,
+            counts, t, w.acc, w.partial};
+  kg_status s = run_aggregate(a, G, st);
   if (s != KG_OK) return s;
   GemmArgs g{};
   g.A = w.acc;
@@ -514,12 +734,13 @@ kg_status kg_rgcn_backward(const kg_graph_csr* G, const kg_layer_params* lp, con
   const int B = lp->B, di = lp->d_in, dO = lp->d_out;
   KG_REQUIRE(B >= 1 && B <= MAXB, KG_ERR_VALIDATION, "num_bases must be in [1, %d]", MAXB);
   LayerWs w;
-  size_t need = layer_ws(G->n, G->e, di, dO, B, &w, ws, (size_t)ws_bytes);
+  size_t need = layer_ws(G->n, G->e, cap_split_chunks(G), di, dO, B, &w, ws, (size_t)ws_bytes);
   KG_REQUIRE((size_t)ws_bytes >= need, KG_ERR_VALIDATION, "layer workspace too small");
   const int64_t wn = (int64_t)B * di * dO;
-  KG_LAUNCH("k_weight_views", k_weight_views, persistent_blocks(wn, 256, 2), 256, 0, st, lp->bases, B, di, dO, w.Wy, w.Wb);
-  KG_LAUNCH("k_dz", k_dz, persistent_blocks((int64_t)G->n * dO, 256, 8), 256, 0, st, dH_out, H_out, order, counts, t, dO, w.dZ);
-  KG_CHECK_LAUNCH("backward prep");
+  KG_LAUNCH("k_weight_views", k_weight_views, persistent_blocks(wn, 256, 2), 256, 0, st, lp->bases, B, di, dO, w.Wy,
+            w.Wb);
+  KG_LAUNCH("k_dz", k_dz, persistent_blocks((int64_t)G->n * dO, 256, 8), 256, 0, st, dH_out, H_out, order, counts, t,
+            dO, w.dZ);
   // Y = X[A_{t+1}] . [V_0 | .. | V_{B-1}]
   GemmArgs gy{};
   gy.A = H_in; gy.lda = di; gy.a_rows = order;
@@ -529,9 +750,9 @@ kg_status kg_rgcn_backward(const kg_graph_csr* G, const kg_layer_params* lp, con
   gy.K = di; gy.N = (int64_t)B * dO;
   kg_status s = gemm_nn(gy, st);
   if (s != KG_OK) return s;
-  CscArgs c{G->c_indptr, G->c_dst, G->c_rel, G->c_norm, lp->coeffs, lp->G, B, dO, w.Y, w.dZ, order, pos, counts,
-            t, w.dS, w.ed, w.ed_self};
-  s = run_csc(c, G->n, st);
+  CscArgs c{G->c_indptr, G->c_dst, G->c_rel, G->c_norm, csc_chunks(G), lp->coeffs, lp->G, B, dO, w.Y, w.dZ, pos,
+            counts, t, w.dS, w.ed, w.ed_self, w.partial};
+  s = run_csc(c, G, st);
   if (s != KG_OK) return s;
   // dV = X^T dS  (reduction over the source rows)
   GemmArgs gv{};
@@ -552,9 +773,8 @@ kg_status kg_rgcn_backward(const kg_graph_csr* G, const kg_layer_params* lp, con
     s = gemm_nn(gx, st);
     if (s != KG_OK) return s;
   }
-  KG_LAUNCH("k_dcoeff_reduce", k_dcoeff_reduce, lp->G, 256, 0, st, G->rel_ptr, G->rel_perm, G->c_dst, pos, counts, t, w.ed, w.ed_self, lp->G,
-                                         B, d_coeffs);
-  KG_CHECK_LAUNCH("k_dcoeff_reduce");
+  KG_LAUNCH("k_dcoeff_reduce", k_dcoeff_reduce, lp->G, 256, 0, st, G->rel_ptr, G->rel_perm, G->c_dst, pos, counts, t,
+            w.ed, w.ed_self, lp->G, B, d_coeffs);
   return KG_OK;
 }
 

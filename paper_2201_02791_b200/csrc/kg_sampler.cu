@@ -142,20 +142,23 @@ __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commi
 template <int N>
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
 
-// One warp walks i = n-1 .. 1. For a 32-position window of the uint32 stream
-// every lane's acceptance is decided unless its masked value lies in
-// (i - lane, i]; the first such ambiguous lane is resolved exactly and the
-// window restarts after it. Positions stream through a 4-quarter smem ring
-// filled by cp.async two quarters ahead.
+// One warp walks i = n-1 .. 1 over a speculative window of 128 uint32 stream
+// positions (4 per lane, position p + 32r + lane). With a uniform mask over
+// the window, offset o is certainly accepted when (U & mask) <= i - o and
+// certainly rejected when (U & mask) > i; the first ambiguous offset is
+// resolved exactly and the window restarts after it. Positions stream through
+// a 4-quarter shared-memory ring filled by cp.async two quarters ahead.
+constexpr int PR = 4;            // positions per lane per window
+constexpr int PW = 32 * PR;      // window
+
 __global__ void __launch_bounds__(32) k_perm_draws(const uint32_t* __restrict__ U, int64_t W, int64_t n,
                                                    int32_t* __restrict__ js, int64_t* __restrict__ consumed) {
   __shared__ __align__(16) uint32_t ring[RING];
   const unsigned lane = lane_id();
-  int64_t issued = 0;   // quarters issued
+  int64_t issued = 0;
   auto issue = [&](int64_t q) {
     int64_t base = q * RING_Q;
     uint32_t* dst = ring + (q & 3) * RING_Q;
-    // 1024 uint32 = 256 x 16B; 8 per lane
 #pragma unroll
     for (int j = 0; j < 8; ++j) {
       int64_t e = base + (int64_t)(j * 32 + lane) * 4;
@@ -164,31 +167,31 @@ __global__ void __launch_bounds__(32) k_perm_draws(const uint32_t* __restrict__ 
     cp_async_commit();
   };
   int64_t i = n - 1, p = 0;
+  int64_t waited_q = -1;
   bool ok = true;
   while (i >= 1) {
-    int64_t need_q = (p + 31) / RING_Q;
-    while (issued <= need_q + 2) {
-      if (issued * RING_Q < W) issue(issued);
-      else cp_async_commit();   // keep group accounting uniform
-      ++issued;
+    const int64_t need_q = (p + PW - 1) / RING_Q;
+    if (need_q > waited_q) {
+      while (issued <= need_q + 2) {
+        if (issued * RING_Q < W) issue(issued);
+        else cp_async_commit();
+        ++issued;
+      }
+      cp_async_wait<2>();
+      __syncwarp();
+      waited_q = need_q;
     }
-    if (p + 32 > W) { ok = false; break; }
-    // quarters issued after need_q: issued - 1 - need_q (>= 2); wait for need_q
-    cp_async_wait<2>();
-    __syncwarp();
-    uint32_t ii = (uint32_t)i;
-    uint32_t mask = smear(ii);
-    bool serial = ii < 64 || smear(ii - 31) != mask;
-    if (serial) {
+    if (p + PW > W) { ok = false; break; }
+    const uint32_t ii = (uint32_t)i;
+    const uint32_t mask = smear(ii);
+    if (ii < 2 * PW || smear(ii - (PW - 1)) != mask) {
       // one exact draw for this i (lane 0), broadcast
       int64_t pp = p;
       uint32_t v = 0;
       if (lane == 0) {
         while (true) {
           if (pp >= W) { pp = -1; break; }
-          // ring residency: pp stays within need_q window for this draw (<32 apart typical);
-          // fall back to global for safety beyond it
-          uint32_t u = (pp < (int64_t)(need_q + 1) * RING_Q) ? ring[pp & (RING - 1)] : U[pp];
+          uint32_t u = (pp < (waited_q + 1) * RING_Q) ? ring[pp & (RING - 1)] : U[pp];
           ++pp;
           v = u & mask;
           if (v <= ii) break;
@@ -202,29 +205,49 @@ __global__ void __launch_bounds__(32) k_perm_draws(const uint32_t* __restrict__ 
       i -= 1;
       continue;
     }
-    uint32_t v = ring[(p + lane) & (RING - 1)] & mask;
-    bool acc_sure = v + lane <= ii;            // v <= i - lane
-    bool rej_sure = v > ii;
-    unsigned amb = __ballot_sync(0xffffffffu, !acc_sure && !rej_sure);
-    int f = amb ? __ffs(amb) - 1 : 32;
-    unsigned before = (f == 32) ? 0xffffffffu : ((1u << f) - 1u);
-    unsigned accm = __ballot_sync(0xffffffffu, acc_sure) & before;
-    if ((int)lane < f && acc_sure) {
-      uint32_t il = ii - __popc(accm & lanemask_lt());
-      js[il] = (int32_t)v;
+    uint32_t v[PR];
+    unsigned acc_b[PR], amb_b[PR];
+#pragma unroll
+    for (int r = 0; r < PR; ++r) {
+      v[r] = ring[(p + r * 32 + lane) & (RING - 1)] & mask;
+      const uint32_t o = r * 32 + lane;
+      const bool acc_sure = v[r] + o <= ii;
+      const bool rej_sure = v[r] > ii;
+      acc_b[r] = __ballot_sync(0xffffffffu, acc_sure);
+      amb_b[r] = __ballot_sync(0xffffffffu, !acc_sure && !rej_sure);
     }
-    int taken = f == 32 ? 32 : f + 1;
-    int accepts = __popc(accm);
-    if (f < 32) {
-      uint32_t il_f = ii - accepts;
-      uint32_t vf = __shfl_sync(0xffffffffu, v, f);
+    int f = PW;
+#pragma unroll
+    for (int r = PR - 1; r >= 0; --r)
+      if (amb_b[r]) f = r * 32 + __ffs(amb_b[r]) - 1;
+    int before = 0;   // accepts at offsets < 32r (running over r)
+#pragma unroll
+    for (int r = 0; r < PR; ++r) {
+      unsigned lim = (f >= (r + 1) * 32) ? 0xffffffffu : (f <= r * 32 ? 0u : ((1u << (f - r * 32)) - 1u));
+      unsigned am = acc_b[r] & lim;
+      if ((am >> lane) & 1u) {
+        uint32_t il = ii - before - __popc(am & lanemask_lt());
+        js[il] = (int32_t)v[r];
+      }
+      before += __popc(am);
+    }
+    int taken = PW;
+    if (f < PW) {
+      uint32_t il_f = ii - before;
+      uint32_t vf = 0;
+#pragma unroll
+      for (int r = 0; r < PR; ++r) {
+        uint32_t x = __shfl_sync(0xffffffffu, v[r], f & 31);
+        if ((f >> 5) == r) vf = x;
+      }
       if (vf <= il_f) {
         if (lane == 0) js[il_f] = (int32_t)vf;
-        accepts += 1;
+        before += 1;
       }
+      taken = f + 1;
     }
     p += taken;
-    i -= accepts;
+    i -= before;
   }
   cp_async_wait<0>();
   if (lane == 0) *consumed = ok ? p : -1;
@@ -338,14 +361,21 @@ __global__ void k_set_pos(const int32_t* __restrict__ order, const int32_t* __re
 }
 
 // warp per active vertex: flag unplaced sources of its messages
-__global__ void k_mark_sources(const int32_t* __restrict__ order, const int32_t* __restrict__ counts, int hop,
-                               const int32_t* __restrict__ indptr, const int32_t* __restrict__ src,
+// warp per static CSR chunk of an active vertex: flag unplaced sources
+__global__ void k_mark_sources(const int32_t* __restrict__ ck_ptr, const int32_t* __restrict__ ck_row,
+                               const int32_t* __restrict__ ck_counts, int C, const int32_t* __restrict__ counts,
+                               int hop, const int32_t* __restrict__ indptr, const int32_t* __restrict__ src,
                                const int32_t* __restrict__ pos, uint32_t* __restrict__ flags) {
   const int32_t active = counts[hop];
+  const int32_t NC = ck_counts[0];
   const int warps = (gridDim.x * blockDim.x) >> 5;
-  for (int64_t w = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; w < active; w += warps) {
-    int32_t v = order[w];
-    for (int32_t e = indptr[v] + (int32_t)lane_id(); e < indptr[v + 1]; e += 32) {
+  for (int64_t c = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; c < NC; c += warps) {
+    int32_t v = ck_row[c];
+    int32_t p = pos[v];
+    if (p < 0 || p >= active) continue;
+    int32_t beg = indptr[v] + (int32_t)(c - ck_ptr[v]) * C;
+    int32_t end = min(beg + C, indptr[v + 1]);
+    for (int32_t e = beg + (int32_t)lane_id(); e < end; e += 32) {
       int32_t u = src[e];
       if (pos[u] < 0) flags[u] = 1u;
     }
@@ -548,8 +578,8 @@ kg_status kg_closure(const int32_t* tri, int64_t total, int64_t start, int64_t b
   KG_LAUNCH("k_set_pos", k_set_pos, gn, 256, 0, st, order, counts, 0, pos);
   for (int h = 0; h < hops; ++h) {
     KG_LAUNCH("k_clear_u32", k_clear_u32, gn, 256, 0, st, flags, n);
-    KG_LAUNCH("k_mark_sources", k_mark_sources, persistent_blocks((int64_t)n * 32, 256, 8), 256, 0, st, order, counts, h, G->indptr, G->src,
-                                                                              pos, flags);
+    KG_LAUNCH("k_mark_sources", k_mark_sources, persistent_blocks(((int64_t)n + G->e / G->chunk + 1) * 32, 256, 8), 256,
+              0, st, G->ck_ptr, G->ck_row, G->ck_counts, G->chunk, counts, h, G->indptr, G->src, pos, flags);
     // append newly reached vertices (ascending) after counts[h]
     r = compact_flags(flags, n, order, bad + 1, 0, counts + h, cws, compact_workspace(n), st);
     if (r != KG_OK) return r;

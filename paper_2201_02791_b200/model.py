@@ -229,7 +229,7 @@ class ViewBuffers:
         self.flags = torch.zeros(1, dtype=torch.int32, device=dev)
         self.ws = _lib.Workspace(dev)
         lib = _lib.require_cuda()
-        self.layer_ws_bytes = max(lib.kg_layer_workspace_bytes(n, 2 * view.m + 1, config.dims[l],
+        self.layer_ws_bytes = max(lib.kg_layer_workspace_bytes(ctypes.byref(view.csr()), config.dims[l],
                                                                config.dims[l + 1], config.num_bases)
                                   for l in range(L))
         self.loss_ws_bytes = lib.kg_loss_workspace_bytes(max(b_max, 1), n, config.dims[-1],
@@ -255,8 +255,8 @@ def device_forward(model: DeviceModel, bufs: ViewBuffers) -> None:
     st = _lib.stream_handle()
     for l in range(L):
         _lib.call("kg_rgcn_forward", csr, ctypes.byref(model.layer(l)), bufs.H[l].data_ptr(),
-                  bufs.H[l + 1].data_ptr(), bufs.order.data_ptr(), bufs.counts.data_ptr(), L - 1 - l,
-                  1 if l < L - 1 else 0, ws.data_ptr(), ws.numel(), st)
+                  bufs.H[l + 1].data_ptr(), bufs.order.data_ptr(), bufs.pos.data_ptr(), bufs.counts.data_ptr(),
+                  L - 1 - l, 1 if l < L - 1 else 0, ws.data_ptr(), ws.numel(), st)
 
 
 def device_loss(model: DeviceModel, bufs: ViewBuffers, stream, start: int, b: int, grad_flat, loss_out,

@@ -22,6 +22,7 @@ from .errors import IntegrityError, SamplingError, ValidationError
 from .partition import Partition
 
 MAX_RESAMPLE_ROUNDS = 100
+CHUNK_EDGES = 64          # messages per warp work chunk (hub rows are split)
 
 
 def _torch():
@@ -199,9 +200,19 @@ def build_view(partition: Partition, num_entities: int, num_relations: int) -> P
     v.d_rel_ptr = torch.empty(2 * num_relations + 1, **i32)
     v.d_pos_keys = torch.empty(max(m, 1), dtype=torch.int64, device=dev)
     v.d_n_keys = torch.zeros(1, **i32)
+    C = CHUNK_EDGES
+    cap_chunks, cap_split_chunks, cap_split_rows = n_local + e // C + 1, 2 * e // C + 1, e // C + 1
+    for pre in ("ck", "cc"):
+        setattr(v, f"d_{pre}_ptr", torch.empty(n_local + 1, **i32))
+        setattr(v, f"d_{pre}_row", torch.empty(cap_chunks, **i32))
+        setattr(v, f"d_{pre}_slot", torch.empty(cap_chunks, **i32))
+        setattr(v, f"d_{pre}_split", torch.empty(cap_split_rows, **i32))
+        setattr(v, f"d_{pre}_counts", torch.zeros(4, **i32))
     c = _lib.KgGraphCsr()
-    c.n, c.R, c.e = n_local, num_relations, e
-    for f in ("indptr", "src", "rel", "norm", "c_indptr", "c_dst", "c_rel", "c_norm", "rel_perm", "rel_ptr"):
+    c.n, c.R, c.e, c.chunk = n_local, num_relations, e, C
+    for f in ("indptr", "src", "rel", "norm", "c_indptr", "c_dst", "c_rel", "c_norm", "rel_perm", "rel_ptr",
+              "ck_ptr", "ck_row", "ck_slot", "ck_split", "ck_counts",
+              "cc_ptr", "cc_row", "cc_slot", "cc_split", "cc_counts"):
         setattr(c, f, getattr(v, "d_" + f).data_ptr())
     v._csr = c
     ws_bytes2 = lib.kg_view_workspace_bytes(max(m, 1), n_local)
