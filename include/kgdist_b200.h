@@ -161,20 +161,24 @@ kg_status kg_view_build(const int32_t* edges_global, int64_t m, const int32_t* g
 /* ---------------------------------------------------------------------- */
 /* R3/R4  Constraint-based negatives (ref:sampler.py:60-70, 144-182)        */
 /* ---------------------------------------------------------------------- */
-/* neg = repeat(core, s); col[i] = 0 (head) if random() < 0.5 else 2;
- * pending = 0..s*m-1. Consumes s*m next64 draws (host advances g). */
-kg_status kg_neg_init(const int32_t* core, int64_t m, int32_t s, kg_pcg64 g, int32_t* neg, int8_t* col,
+/* The sampler's PCG64 state lives in device memory (`g`, a kg_pcg64 in
+ * HBM): every entry below reads it and advances it on the device, so an
+ * epoch of sampling is one asynchronous kernel chain (no host syncs).
+ *
+ * neg = repeat(core, s); col[i] = 0 (head) if random() < 0.5 else 2;
+ * pending = 0..s*m-1; advances g by s*m next64 draws. */
+kg_status kg_neg_init(const int32_t* core, int64_t m, int32_t s, kg_pcg64* g, int32_t* neg, int8_t* col,
                       int32_t* pending, void* stream);
 int64_t kg_neg_round_workspace_bytes(int64_t window);
-/* One resampling round over the k pending rows (ascending): draws
- * integers(pool_size, size=k) from a window of `window` uint32 positions,
- * writes the corrupted entity, rejects originals and local positives.
- * Outputs next_pending[*next_count] and *consumed32 (uint32 draws used;
- * 0 => window too small, retry larger). */
+/* One resampling round over the *k_dev pending rows (ascending, <= k_max):
+ * draws integers(pool_size, size=k) from `window` uint32 stream positions,
+ * writes the corrupted entity, rejects originals and local positives,
+ * advances g. Outputs next_pending[*next_count] and *consumed32 (uint32
+ * draws used; -1 => window too small, g untouched: retry larger). */
 kg_status kg_neg_round(int32_t* neg, const int8_t* col, const int32_t* core, int32_t s,
-                       const int32_t* pending, int64_t k, int64_t pool_size, int32_t n_local, int32_t R,
-                       const int64_t* pos_keys, const int32_t* n_keys, kg_pcg64 g, int64_t window,
-                       int32_t* next_pending, int32_t* next_count, int64_t* consumed32, void* ws,
+                       const int32_t* pending, const int32_t* k_dev, int64_t k_max, int64_t pool_size,
+                       int32_t n_local, int32_t R, const int64_t* pos_keys, const int32_t* n_keys, kg_pcg64* g,
+                       int64_t window, int32_t* next_pending, int32_t* next_count, int64_t* consumed32, void* ws,
                        int64_t ws_bytes, void* stream);
 /* is_positive over (k,3) local triples -> out[k] (0/1). */
 kg_status kg_is_positive(const int32_t* triples, int64_t k, int32_t n_local, int32_t R, const int64_t* pos_keys,
@@ -188,7 +192,7 @@ kg_status kg_is_positive(const int32_t* triples, int64_t k, int32_t n_local, int
  * positions (W = kg_perm_draws_buffer_len(n)); *consumed32 = uint32 draws
  * used, or -1 if W was too small (retry with a larger buffer). */
 int64_t kg_perm_draws_buffer_len(int64_t n);
-kg_status kg_perm_draws_buffered(int64_t n, kg_pcg64 g, uint32_t* U, int64_t W, int32_t* js, int64_t* consumed32,
+kg_status kg_perm_draws_buffered(int64_t n, kg_pcg64* g, uint32_t* U, int64_t W, int32_t* js, int64_t* consumed32,
                                  void* stream);
 int64_t kg_perm_resolve_workspace_bytes(int64_t n);
 /* Final permutation from the swap targets without replaying the swaps. */

@@ -61,13 +61,13 @@ _PROTOS = {
     "kg_view_workspace_bytes": (c_int64, [c_int64, c_int64]),
     "kg_view_local_ids": (ST, [P, c_int64, P, c_int64, c_int64, P, P, P, P, c_int64, P]),
     "kg_view_build": (ST, [P, c_int64, P, P, P, P, P, POINTER(KgGraphCsr), P, P, P, c_int64, P]),
-    "kg_neg_init": (ST, [P, c_int64, c_int32, KgPcg64, P, P, P, P]),
+    "kg_neg_init": (ST, [P, c_int64, c_int32, P, P, P, P, P]),
     "kg_neg_round_workspace_bytes": (c_int64, [c_int64]),
-    "kg_neg_round": (ST, [P, P, P, c_int32, P, c_int64, c_int64, c_int32, c_int32, P, P, KgPcg64,
+    "kg_neg_round": (ST, [P, P, P, c_int32, P, P, c_int64, c_int64, c_int32, c_int32, P, P, P,
                           c_int64, P, P, P, P, c_int64, P]),
     "kg_is_positive": (ST, [P, c_int64, c_int32, c_int32, P, P, P, P]),
     "kg_perm_draws_buffer_len": (c_int64, [c_int64]),
-    "kg_perm_draws_buffered": (ST, [c_int64, KgPcg64, P, c_int64, P, P, P]),
+    "kg_perm_draws_buffered": (ST, [c_int64, P, P, c_int64, P, P, P]),
     "kg_perm_resolve_workspace_bytes": (c_int64, [c_int64]),
     "kg_perm_resolve": (ST, [P, c_int64, P, P, c_int64, P]),
     "kg_stream_gather": (ST, [P, c_int64, P, c_int64, P, P, P, P]),
@@ -226,3 +226,17 @@ def kernel_breakdown(fn, *args, **kw):
         name, cnt, ms = line.rsplit(",", 2)
         out[name] = (int(cnt), float(ms))
     return out, res
+
+
+# ---------------------------------------------------------------------------
+# device-resident PCG64 state (40-byte kg_pcg64 in HBM)
+# ---------------------------------------------------------------------------
+def pcg_to_device(g: KgPcg64, device):
+    import torch
+    raw = np.frombuffer(bytes(g), dtype=np.uint8).copy()
+    return torch.as_tensor(raw).to(device)
+
+
+def pcg_from_device(t) -> KgPcg64:
+    raw = t.cpu().numpy().tobytes()
+    return KgPcg64.from_buffer_copy(raw[: ctypes.sizeof(KgPcg64)])

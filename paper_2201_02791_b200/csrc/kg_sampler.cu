@@ -13,7 +13,8 @@ static int grid_for(int64_t n) { return persistent_blocks(n, 256, 8); }
 // ---------------------------------------------------------------------------
 constexpr int GEN_WORDS = 16;   // next64 words per thread
 
-__global__ void k_gen_u32(kg_pcg64 g, int64_t W, uint32_t* __restrict__ U) {
+__global__ void k_gen_u32(const kg_pcg64* __restrict__ gp, int64_t W, uint32_t* __restrict__ U) {
+  const kg_pcg64 g = *gp;
   const u128 s0 = state_of(g), inc = inc_of(g);
   const int64_t off = g.has_uint32 ? 1 : 0;
   const int64_t nwords = (W - off + 1) / 2 + 1;
@@ -38,8 +39,9 @@ __global__ void k_gen_u32(kg_pcg64 g, int64_t W, uint32_t* __restrict__ U) {
 // ---------------------------------------------------------------------------
 constexpr int COIN_PER_THREAD = 16;
 
-__global__ void k_neg_init(const int32_t* __restrict__ core, int64_t m, int32_t s, kg_pcg64 g,
+__global__ void k_neg_init(const int32_t* __restrict__ core, int64_t m, int32_t s, const kg_pcg64* __restrict__ gp,
                            int32_t* __restrict__ neg, int8_t* __restrict__ col, int32_t* __restrict__ pending) {
+  const kg_pcg64 g = *gp;
   const u128 s0 = state_of(g), inc = inc_of(g);
   const int64_t total = m * s;
   for (int64_t i0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) * COIN_PER_THREAD; i0 < total;
@@ -85,12 +87,14 @@ __global__ void k_lemire_flags(const uint32_t* __restrict__ U, int64_t W, uint32
 
 __global__ void k_neg_assign(const uint32_t* __restrict__ U, const uint32_t* __restrict__ flags,
                              const uint32_t* __restrict__ rank, int64_t W, uint32_t n_pool,
-                             const int32_t* __restrict__ pending, int64_t k, int32_t* __restrict__ neg,
+                             const int32_t* __restrict__ pending, const int32_t* __restrict__ kp,
+                             int32_t* __restrict__ neg,
                              const int8_t* __restrict__ col, const int32_t* __restrict__ core, int32_t s,
                              int32_t n_local, int32_t R, const int64_t* __restrict__ keys,
                              const int32_t* __restrict__ n_keys, uint32_t* __restrict__ bad,
                              int64_t* __restrict__ consumed) {
   const int32_t nk = *n_keys;
+  const int64_t k = *kp;
   for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < W; p += (int64_t)gridDim.x * blockDim.x) {
     if (!flags[p]) continue;
     uint32_t q = rank[p];
@@ -107,12 +111,48 @@ __global__ void k_neg_assign(const uint32_t* __restrict__ U, const uint32_t* __r
   }
 }
 
-__global__ void k_scatter_pending(const uint32_t* __restrict__ bad, const uint32_t* __restrict__ rank, int64_t k,
-                                  const int32_t* __restrict__ pending, int32_t* __restrict__ next,
-                                  const uint32_t* __restrict__ total, int32_t* __restrict__ next_count) {
+__global__ void k_scatter_pending(const uint32_t* __restrict__ bad, const uint32_t* __restrict__ rank,
+                                  const int32_t* __restrict__ kp, const int32_t* __restrict__ pending,
+                                  int32_t* __restrict__ next, const uint32_t* __restrict__ total,
+                                  int32_t* __restrict__ next_count) {
+  const int64_t k = *kp;
   for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < k; q += (int64_t)gridDim.x * blockDim.x)
     if (bad[q]) next[rank[q]] = pending[q];
   if (blockIdx.x == 0 && threadIdx.x == 0) *next_count = (int32_t)*total;
+}
+
+// Device-resident PCG64 bookkeeping (one thread): the sampler's RNG state
+// lives in HBM so an epoch's sampling is a sync-free chain of kernels.
+__global__ void k_pcg_advance(kg_pcg64* __restrict__ g, uint64_t delta) {
+  u128 s = apply_jump(pcg_jump(delta, inc_of(*g)), state_of(*g));
+  g->state_hi = s.hi;
+  g->state_lo = s.lo;
+}
+
+// consume `*count` next_uint32 draws; *count < 0 (failed draw) leaves g as is.
+// With `need` set, a zero count while need[0] > 0 means the window was too
+// small: it is flagged as -1 so the host retries with a larger window.
+__global__ void k_pcg_consume32(kg_pcg64* __restrict__ g, int64_t* __restrict__ count,
+                                const int32_t* __restrict__ need) {
+  int64_t c = *count;
+  if (need && *need > 0 && c == 0) {
+    *count = -1;
+    return;
+  }
+  if (c <= 0) return;
+  uint64_t cnt = (uint64_t)c;
+  if (g->has_uint32) {
+    g->has_uint32 = 0;
+    cnt -= 1;
+  }
+  if (cnt == 0) return;
+  uint64_t words = (cnt + 1) / 2;
+  u128 s = apply_jump(pcg_jump(words, inc_of(*g)), state_of(*g));
+  uint64_t x = pcg_output(s);
+  g->state_hi = s.hi;
+  g->state_lo = s.lo;
+  g->has_uint32 = (cnt & 1) ? 1u : 0u;
+  g->uinteger = (uint32_t)(x >> 32);
 }
 
 __global__ void k_is_positive(const int32_t* __restrict__ tri, int64_t k, int32_t n, int32_t R,
@@ -430,14 +470,15 @@ void kg_pcg64_peek64(const kg_pcg64* g, uint64_t* out, int64_t count) {
 }
 
 // --- negatives -------------------------------------------------------------
-kg_status kg_neg_init(const int32_t* core, int64_t m, int32_t s, kg_pcg64 g, int32_t* neg, int8_t* col,
+kg_status kg_neg_init(const int32_t* core, int64_t m, int32_t s, kg_pcg64* g, int32_t* neg, int8_t* col,
                       int32_t* pending, void* stream) {
+  cudaStream_t st = as_stream(stream);
   KG_REQUIRE(s >= 1 && m >= 1, KG_ERR_VALIDATION, "neg_init needs s >= 1 and m >= 1");
   KG_REQUIRE(m * (int64_t)s < (int64_t(1) << 31), KG_ERR_VALIDATION, "too many negatives");
   int64_t total = m * s;
   int blocks = persistent_blocks(ceil_div(total, COIN_PER_THREAD), 256, 8);
-  KG_LAUNCH("k_neg_init", k_neg_init, blocks, 256, 0, as_stream(stream), core, m, s, g, neg, col, pending);
-  KG_CHECK_LAUNCH("k_neg_init");
+  KG_LAUNCH("k_neg_init", k_neg_init, blocks, 256, 0, st, core, m, s, g, neg, col, pending);
+  KG_LAUNCH("k_pcg_advance", k_pcg_advance, 1, 1, 0, st, g, (uint64_t)total);   // one next64 per coin
   return KG_OK;
 }
 
@@ -446,12 +487,13 @@ int64_t kg_neg_round_workspace_bytes(int64_t W) {
 }
 
 kg_status kg_neg_round(int32_t* neg, const int8_t* col, const int32_t* core, int32_t s, const int32_t* pending,
-                       int64_t k, int64_t pool_size, int32_t n_local, int32_t R, const int64_t* pos_keys,
-                       const int32_t* n_keys, kg_pcg64 g, int64_t W, int32_t* next_pending,
-                       int32_t* next_count, int64_t* consumed, void* ws, int64_t ws_bytes, void* stream) {
+                       const int32_t* k_dev, int64_t k_max, int64_t pool_size, int32_t n_local, int32_t R,
+                       const int64_t* pos_keys, const int32_t* n_keys, kg_pcg64* g, int64_t W,
+                       int32_t* next_pending, int32_t* next_count, int64_t* consumed, void* ws, int64_t ws_bytes,
+                       void* stream) {
   cudaStream_t st = as_stream(stream);
   KG_REQUIRE(pool_size >= 2 && pool_size <= 0xFFFFFFFFLL, KG_ERR_SAMPLING, "pool size out of range");
-  KG_REQUIRE(W >= k && k >= 1, KG_ERR_VALIDATION, "bad resampling window");
+  KG_REQUIRE(W >= k_max && k_max >= 1, KG_ERR_VALIDATION, "bad resampling window");
   KG_REQUIRE(ws_bytes >= kg_neg_round_workspace_bytes(W), KG_ERR_VALIDATION, "neg workspace too small");
   Arena a(ws, (size_t)ws_bytes);
   uint32_t* U = a.take<uint32_t>(W);
@@ -463,18 +505,19 @@ kg_status kg_neg_round(int32_t* neg, const int8_t* col, const int32_t* core, int
   char* sws = a.take<char>(scan_workspace(W));
   uint32_t n = (uint32_t)pool_size;
   KG_CUDA(cudaMemsetAsync(consumed, 0, sizeof(int64_t), st));
+  KG_CUDA(cudaMemsetAsync(bad, 0, k_max * sizeof(uint32_t), st));
   KG_LAUNCH("k_gen_u32", k_gen_u32, persistent_blocks(ceil_div(W / 2 + 2, GEN_WORDS), 256, 8), 256, 0, st, g, W, U);
   KG_LAUNCH("k_lemire_flags", k_lemire_flags, grid_for(W), 256, 0, st, U, W, n, lemire_threshold(n), flags);
-  KG_CHECK_LAUNCH("neg gen");
   kg_status r = exclusive_scan_u32(flags, rank, W, totals, sws, scan_workspace(W), st);
   if (r != KG_OK) return r;
-  KG_LAUNCH("k_neg_assign", k_neg_assign, grid_for(W), 256, 0, st, U, flags, rank, W, n, pending, k, neg, col, core, s, n_local, R,
-                                            pos_keys, n_keys, bad, consumed);
-  KG_CHECK_LAUNCH("k_neg_assign");
-  r = exclusive_scan_u32(bad, bad_rank, k, totals + 1, sws, scan_workspace(W), st);
+  KG_LAUNCH("k_neg_assign", k_neg_assign, grid_for(W), 256, 0, st, U, flags, rank, W, n, pending, k_dev, neg, col,
+            core, s, n_local, R, pos_keys, n_keys, bad, consumed);
+  r = exclusive_scan_u32(bad, bad_rank, k_max, totals + 1, sws, scan_workspace(W), st);
   if (r != KG_OK) return r;
-  KG_LAUNCH("k_scatter_pending", k_scatter_pending, grid_for(k), 256, 0, st, bad, bad_rank, k, pending, next_pending, totals + 1, next_count);
-  KG_CHECK_LAUNCH("k_scatter_pending");
+  KG_LAUNCH("k_scatter_pending", k_scatter_pending, grid_for(k_max), 256, 0, st, bad, bad_rank, k_dev, pending,
+            next_pending, totals + 1, next_count);
+  // advance the device state by the draws used (-1 flags a too-small window)
+  KG_LAUNCH("k_pcg_consume32", k_pcg_consume32, 1, 1, 0, st, g, consumed, k_dev);
   return KG_OK;
 }
 
@@ -492,7 +535,7 @@ int64_t kg_perm_draws_buffer_len(int64_t n) {
   return ((2 * n + 8192 + 4 * 1024) / 1024 + 4) * 1024;
 }
 
-kg_status kg_perm_draws_buffered(int64_t n, kg_pcg64 g, uint32_t* U, int64_t W, int32_t* js, int64_t* consumed32,
+kg_status kg_perm_draws_buffered(int64_t n, kg_pcg64* g, uint32_t* U, int64_t W, int32_t* js, int64_t* consumed32,
                                  void* stream) {
   cudaStream_t st = as_stream(stream);
   KG_REQUIRE(n >= 1 && n < (int64_t(1) << 31), KG_ERR_VALIDATION, "permutation size out of range");
@@ -502,9 +545,8 @@ kg_status kg_perm_draws_buffered(int64_t n, kg_pcg64 g, uint32_t* U, int64_t W, 
   }
   KG_REQUIRE(W % 4 == 0 && W >= 4096, KG_ERR_VALIDATION, "draw buffer must be a multiple of 4 >= 4096");
   KG_LAUNCH("k_gen_u32", k_gen_u32, persistent_blocks(ceil_div(W / 2 + 2, GEN_WORDS), 256, 8), 256, 0, st, g, W, U);
-  KG_CHECK_LAUNCH("perm gen");
   KG_LAUNCH("k_perm_draws", k_perm_draws, 1, 32, 0, st, U, W, n, js, consumed32);
-  KG_CHECK_LAUNCH("k_perm_draws");
+  KG_LAUNCH("k_pcg_consume32", k_pcg_consume32, 1, 1, 0, st, g, consumed32, (const int32_t*)nullptr);
   return KG_OK;
 }
 

@@ -251,68 +251,87 @@ def _round_window(k: int, pool: int) -> int:
     return int(k + 2 * mean + 8 * math.sqrt(mean + 1.0) + 64)
 
 
-def sample_negatives_device(view: PartitionView, s: int, pcg, ws: Optional["_lib.Workspace"] = None):
-    """Device-resident negatives: returns ((s*m,3) int32 tensor, advanced pcg).
-    Bit-exact with the reference's draws from the same PCG64 state."""
+def _neg_round(view, s, neg, col, pend_in, k_in, k_max, g_dev, W, pend_out, k_out, consumed, ws):
+    lib = _lib.require_cuda()
+    buf = ws.get("neg_round", lib.kg_neg_round_workspace_bytes(W))
+    _lib.call("kg_neg_round", neg.data_ptr(), col.data_ptr(), view.d_edges.data_ptr(), s, pend_in.data_ptr(),
+              k_in.data_ptr(), k_max, view.pool_size, view.n, view.num_relations, view.d_pos_keys.data_ptr(),
+              view.d_n_keys.data_ptr(), g_dev.data_ptr(), W, pend_out.data_ptr(), k_out.data_ptr(),
+              consumed.data_ptr(), buf.data_ptr(), buf.numel(), _lib.stream_handle())
+
+
+def _neg_buffers(view, s, dev):
+    torch = _torch()
+    total = view.num_core * s
+    return dict(neg=torch.empty((total, 3), dtype=torch.int32, device=dev),
+                col=torch.empty(total, dtype=torch.int8, device=dev),
+                pend=[torch.empty(total, dtype=torch.int32, device=dev) for _ in range(2)],
+                k=[torch.zeros(1, dtype=torch.int32, device=dev) for _ in range(2)],
+                consumed=torch.zeros(MAX_RESAMPLE_ROUNDS, dtype=torch.int64, device=dev))
+
+
+def sample_negatives_device(view: PartitionView, s: int, g_dev, ws: Optional["_lib.Workspace"] = None,
+                            bufs: Optional[dict] = None, async_rounds: int = 0):
+    """Constraint negatives on the device from the device-resident PCG64
+    state g_dev (advanced in place). With async_rounds > 0 only that many
+    resampling rounds are enqueued, without any host synchronisation; the
+    caller validates with `negatives_pending()`. Otherwise rounds run until
+    every row is accepted (host-checked). Returns the (s*m, 3) tensor."""
     torch = _torch()
     if s < 0:
         raise ValidationError("negatives_per_positive must be >= 0")
     m = view.num_core
     dev = view.device
     if s == 0 or m == 0:
-        return torch.zeros((0, 3), dtype=torch.int32, device=dev), pcg
+        return torch.zeros((0, 3), dtype=torch.int32, device=dev)
     if view.pool_size < 2:
         raise SamplingError("partition has fewer than 2 core vertices")
-    lib = _lib.require_cuda()
-    st = _lib.stream_handle()
     ws = ws or _lib.Workspace(dev)
+    b = bufs or _neg_buffers(view, s, dev)
     total = m * s
-    neg = torch.empty((total, 3), dtype=torch.int32, device=dev)
-    col = torch.empty(total, dtype=torch.int8, device=dev)
-    pend = [torch.empty(total, dtype=torch.int32, device=dev), torch.empty(total, dtype=torch.int32, device=dev)]
-    g = _lib.pcg_copy(pcg)
-    _lib.call("kg_neg_init", view.d_edges.data_ptr(), m, s, g, neg.data_ptr(), col.data_ptr(),
-              pend[0].data_ptr(), st)
-    _lib.pcg_advance(g, total)
-    counters = torch.zeros(4, dtype=torch.int64, device=dev)   # [consumed, next_count (int32)]
-    k = total
+    st = _lib.stream_handle()
+    _lib.call("kg_neg_init", view.d_edges.data_ptr(), m, s, g_dev.data_ptr(), b["neg"].data_ptr(), b["col"].data_ptr(),
+              b["pend"][0].data_ptr(), st)
+    b["k"][0].fill_(total)
+    b["consumed"].zero_()
+    W = _round_window(total, view.pool_size)
     cur = 0
-    for _ in range(MAX_RESAMPLE_ROUNDS):
+    if async_rounds:
+        for r in range(async_rounds):
+            _neg_round(view, s, b["neg"], b["col"], b["pend"][cur], b["k"][cur], total, g_dev, W, b["pend"][1 - cur],
+                       b["k"][1 - cur], b["consumed"][r:r + 1], ws)
+            cur = 1 - cur
+        b["cur"] = cur
+        return b["neg"]
+    k = total
+    for r in range(MAX_RESAMPLE_ROUNDS):
         if k == 0:
             break
-        W = _round_window(k, view.pool_size)
         while True:
-            nbytes = lib.kg_neg_round_workspace_bytes(W)
-            buf = ws.get("neg_round", nbytes)
-            _lib.call("kg_neg_round", neg.data_ptr(), col.data_ptr(), view.d_edges.data_ptr(), s,
-                      pend[cur].data_ptr(), k, view.pool_size, view.n, view.num_relations,
-                      view.d_pos_keys.data_ptr(), view.d_n_keys.data_ptr(), g, W,
-                      pend[1 - cur].data_ptr(), counters.data_ptr() + 8, counters.data_ptr(),
-                      buf.data_ptr(), buf.numel(), st)
-            host = counters.cpu()
-            consumed = int(host[0])
-            if consumed > 0:
+            _neg_round(view, s, b["neg"], b["col"], b["pend"][cur], b["k"][cur], total, g_dev, W, b["pend"][1 - cur],
+                       b["k"][1 - cur], b["consumed"][r:r + 1], ws)
+            if int(b["consumed"][r].item()) >= 0:
                 break
-            W *= 2
-        next_k = int(host[1]) & 0xFFFFFFFF       # int32 next_count written at byte offset 8
-        _lib.pcg_consume32(g, consumed)
+            W *= 2                      # window too small: state untouched, retry wider
         cur = 1 - cur
-        k = next_k
+        k = int(b["k"][cur].item())
+    b["cur"] = cur
     if k > 0:
-        row = int(pend[cur][0].item())
+        row = int(b["pend"][cur][0].item())
         e = view.core_edges[row // s]
         raise SamplingError(f"could not corrupt edge {tuple(int(x) for x in e)} after "
                             f"{MAX_RESAMPLE_ROUNDS} rounds")
-    return neg, g
+    return b["neg"]
 
 
 def sample_negatives(view: PartitionView, negatives_per_positive: int,
                      rng: np.random.Generator) -> np.ndarray:
     """Corrupt every core edge s times inside the partition's core-vertex pool
-    (ref:sampler.py:144-182); returns (s*num_core, 3) int64 local triples."""
-    pcg = _lib.pcg_from_numpy(rng)
-    neg, g = sample_negatives_device(view, negatives_per_positive, pcg)
-    _lib.pcg_to_numpy(g, rng)
+    (ref:sampler.py:144-182); returns (s*num_core, 3) int64 local triples and
+    advances `rng` exactly as the reference's draws would."""
+    g_dev = _lib.pcg_to_device(_lib.pcg_from_numpy(rng), view.device)
+    neg = sample_negatives_device(view, negatives_per_positive, g_dev)
+    _lib.pcg_to_numpy(_lib.pcg_from_device(g_dev), rng)
     return neg.cpu().numpy().astype(np.int64).reshape(-1, 3)
 
 
@@ -320,31 +339,36 @@ def sample_negatives(view: PartitionView, negatives_per_positive: int,
 # Batching (ref:sampler.py:189-232)
 # ---------------------------------------------------------------------------
 
-def permutation_device(n: int, pcg, device, ws: Optional["_lib.Workspace"] = None):
-    """rng.permutation(n) on the GPU, bit-exact; returns (int32 tensor, pcg)."""
+def permutation_device(n: int, g_dev, device, ws: Optional["_lib.Workspace"] = None, check: bool = True,
+                       out=None):
+    """rng.permutation(n) on the GPU, bit-exact, from the device-resident
+    PCG64 state g_dev (advanced in place). Returns (perm int32 tensor,
+    consumed-count tensor; -1 there means the draw buffer was too small)."""
     torch = _torch()
     lib = _lib.require_cuda()
     st = _lib.stream_handle()
     ws = ws or _lib.Workspace(device)
-    g = _lib.pcg_copy(pcg)
+    perm = out if out is not None else torch.empty(n, dtype=torch.int32, device=device)
+    consumed = ws.get("perm_consumed", 8)[:8].view(torch.int64)
     if n <= 1:
-        return torch.zeros(n, dtype=torch.int32, device=device), g
+        perm.zero_()
+        consumed.zero_()
+        return perm, consumed
     js = ws.get("perm_js", 4 * n)
     W = lib.kg_perm_draws_buffer_len(n)
-    consumed_t = torch.zeros(1, dtype=torch.int64, device=device)
     while True:
         U = ws.get("perm_U", 4 * W)
-        _lib.call("kg_perm_draws_buffered", n, g, U.data_ptr(), W, js.data_ptr(), consumed_t.data_ptr(), st)
-        consumed = int(consumed_t.item())
-        if consumed >= 0:
+        snap = g_dev.clone() if check else None
+        _lib.call("kg_perm_draws_buffered", n, g_dev.data_ptr(), U.data_ptr(), W, js.data_ptr(), consumed.data_ptr(),
+                  st)
+        if not check or int(consumed.item()) >= 0:
             break
+        g_dev.copy_(snap)
         W = ((2 * W) // 1024 + 1) * 1024
-    perm = torch.empty(n, dtype=torch.int32, device=device)
     rb = lib.kg_perm_resolve_workspace_bytes(n)
     buf = ws.get("perm_resolve", rb)
     _lib.call("kg_perm_resolve", js.data_ptr(), n, perm.data_ptr(), buf.data_ptr(), buf.numel(), st)
-    _lib.pcg_consume32(g, consumed)
-    return perm, g
+    return perm, consumed
 
 
 @dataclass
@@ -376,18 +400,22 @@ class DeviceStream:
         return EdgeMiniBatch(t, y)
 
 
-def stream_device(pos, neg, pcg, device, ws=None):
+def stream_device(pos, neg, g_dev, device, ws=None, check=True, out=None):
     """concat(pos, neg)[perm] with labels, perm = rng.permutation(total)."""
     torch = _torch()
     npos, nneg = int(pos.shape[0]), int(neg.shape[0])
     total = npos + nneg
-    perm, g = permutation_device(total, pcg, device, ws)
-    tri = torch.empty((total, 3), dtype=torch.int32, device=device)
-    lab = torch.empty(total, dtype=torch.float32, device=device)
+    perm_out = out["perm"] if out is not None else None
+    perm, consumed = permutation_device(total, g_dev, device, ws, check=check, out=perm_out)
+    if out is not None:
+        tri, lab = out["tri"], out["lab"]
+    else:
+        tri = torch.empty((total, 3), dtype=torch.int32, device=device)
+        lab = torch.empty(total, dtype=torch.float32, device=device)
     if total:
         _lib.call("kg_stream_gather", pos.data_ptr(), npos, neg.data_ptr(), nneg, perm.data_ptr(),
                   tri.data_ptr(), lab.data_ptr(), _lib.stream_handle())
-    return DeviceStream(tri, lab, total), g
+    return DeviceStream(tri, lab, total), consumed
 
 
 def make_batches(positives: np.ndarray, negatives: np.ndarray, batch_size: int,
@@ -402,9 +430,9 @@ def make_batches(positives: np.ndarray, negatives: np.ndarray, batch_size: int,
     if total == 0:
         return []
     dev = _device()
-    ds, g = stream_device(_dev_i32(pos, dev).reshape(-1, 3), _dev_i32(neg, dev).reshape(-1, 3),
-                          _lib.pcg_from_numpy(rng), dev)
-    _lib.pcg_to_numpy(g, rng)
+    g_dev = _lib.pcg_to_device(_lib.pcg_from_numpy(rng), dev)
+    ds, _ = stream_device(_dev_i32(pos, dev).reshape(-1, 3), _dev_i32(neg, dev).reshape(-1, 3), g_dev, dev)
+    _lib.pcg_to_numpy(_lib.pcg_from_device(g_dev), rng)
     tri = ds.triples.cpu().numpy().astype(np.int64)
     lab = ds.labels.cpu().numpy().astype(np.float64)
     if num_batches is None:
@@ -521,3 +549,96 @@ def compute_graph_for_seeds(seeds: np.ndarray, view: PartitionView, hops: int) -
 def build_compute_graph(batch: EdgeMiniBatch, view: PartitionView, hops: int) -> ComputeGraph:
     """Layered n-hop closure of the batch endpoints (ref:sampler.py:310-317)."""
     return compute_graph_for_seeds(batch.triples[:, [0, 2]].reshape(-1), view, hops)
+
+
+# ---------------------------------------------------------------------------
+# Asynchronous epoch sampling (negatives + shuffle) on a side stream
+# ---------------------------------------------------------------------------
+
+class EpochSampler:
+    """Per-partition epoch pipeline: the negatives and the shuffled stream of
+    epoch e+1 are produced on a side CUDA stream while epoch e trains. The
+    PCG64 state lives on the device, so the whole chain is enqueued without
+    host synchronisation; at the epoch boundary `next()` checks the few
+    device status words (all negatives accepted, draw windows large enough)
+    and, in the rare case they are not, redoes that epoch synchronously from
+    a snapshot of the epoch's starting RNG state. Bit-exact either way."""
+
+    ASYNC_ROUNDS = 3
+
+    def __init__(self, view: PartitionView, s: int, g_dev):
+        torch = _torch()
+        self.view, self.s, self.g = view, s, g_dev
+        self.dev = view.device
+        self.side = torch.cuda.Stream(self.dev)
+        self.ws = _lib.Workspace(self.dev)
+        core = view.num_core
+        total = core * (s + 1)
+        self.total = total
+        self.core = view.d_edges[:core]
+        self.slots = []
+        for _ in range(2):
+            self.slots.append(dict(
+                neg=_neg_buffers(view, s, self.dev) if s > 0 and core > 0 else None,
+                out=dict(perm=torch.empty(max(total, 1), dtype=torch.int32, device=self.dev),
+                         tri=torch.empty((max(total, 1), 3), dtype=torch.int32, device=self.dev),
+                         lab=torch.empty(max(total, 1), dtype=torch.float32, device=self.dev)),
+                g_start=torch.empty_like(g_dev), ready=torch.cuda.Event(), released=None,
+                status=torch.zeros(3, dtype=torch.int64, device=self.dev),
+                host=torch.zeros(3, dtype=torch.int64, pin_memory=True), stream=None))
+        self.parity = 0
+        self._enqueue(0)
+
+    def _enqueue(self, parity):
+        torch = _torch()
+        slot = self.slots[parity]
+        with torch.cuda.stream(self.side):
+            if slot["released"] is not None:
+                self.side.wait_event(slot["released"])
+            slot["g_start"].copy_(self.g)
+            if slot["neg"] is not None:
+                neg = sample_negatives_device(self.view, self.s, self.g, self.ws, bufs=slot["neg"],
+                                              async_rounds=self.ASYNC_ROUNDS)
+                b = slot["neg"]
+                slot["status"][0:1].copy_(b["k"][b["cur"]])
+                slot["status"][1:2].copy_(b["consumed"].min().view(1))
+            else:
+                neg = torch.zeros((0, 3), dtype=torch.int32, device=self.dev)
+                slot["status"][:2].zero_()
+            ds, consumed = stream_device(self.core, neg, self.g, self.dev, self.ws, check=False, out=slot["out"])
+            slot["status"][2:3].copy_(consumed)
+            slot["host"].copy_(slot["status"], non_blocking=True)
+            slot["ready"].record(self.side)
+            slot["stream"] = DeviceStream(slot["out"]["tri"], slot["out"]["lab"], ds.total)
+
+    def next(self) -> DeviceStream:
+        """Stream of the next epoch (main stream ordered after it); enqueues
+        the epoch after that."""
+        torch = _torch()
+        slot = self.slots[self.parity]
+        slot["ready"].synchronize()
+        k_left, min_consumed, perm_consumed = (int(x) for x in slot["host"].tolist())
+        if k_left > 0 or min_consumed < 0 or perm_consumed < 0:
+            self._redo(slot)
+        torch.cuda.current_stream().wait_event(slot["ready"])
+        out = slot["stream"]
+        # the next epoch's buffers may be rewritten only after this epoch's compute
+        other = self.slots[1 - self.parity]
+        other["released"] = torch.cuda.Event()
+        other["released"].record(torch.cuda.current_stream())
+        self.parity = 1 - self.parity
+        self._enqueue(self.parity)
+        return out
+
+    def _redo(self, slot):
+        """Synchronous, host-checked re-run of one epoch from its start state."""
+        torch = _torch()
+        with torch.cuda.stream(self.side):
+            self.g.copy_(slot["g_start"])
+            if slot["neg"] is not None:
+                neg = sample_negatives_device(self.view, self.s, self.g, self.ws, bufs=slot["neg"])
+            else:
+                neg = torch.zeros((0, 3), dtype=torch.int32, device=self.dev)
+            stream_device(self.core, neg, self.g, self.dev, self.ws, check=True, out=slot["out"])
+            slot["ready"].record(self.side)
+        slot["ready"].synchronize()

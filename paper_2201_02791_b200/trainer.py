@@ -30,7 +30,7 @@ from .errors import KGError, NumericError, ProtocolError, ValidationError
 from .model import (MODE_EMBEDDING, MODE_FEATURE, DeviceModel, ModelConfig, ModelParams, ViewBuffers,
                     check_flags, device_backward, device_forward, device_loss, init_params)
 from .partition import PartitionSet
-from .sampler import build_view, sample_negatives_device, stream_device
+from .sampler import EpochSampler, build_view
 
 _DROPOUT_STREAM_OFFSET = 0x9E3779B9
 
@@ -241,7 +241,9 @@ class _Worker:
         self.b = b
         self.config = config
         dev = self.view.device
-        self.pcg = _lib.pcg_from_numpy(np.random.default_rng(tc.seed ^ self.view.partition_id))
+        # the worker's RNG stream (ref:trainer.py:185) lives on the device
+        self.g_dev = _lib.pcg_to_device(
+            _lib.pcg_from_numpy(np.random.default_rng(tc.seed ^ self.view.partition_id)), dev)
         local = self.view.local_ids
         if config.mode == MODE_EMBEDDING:
             rows = params.entity_embed[local]
@@ -256,12 +258,12 @@ class _Worker:
         else:
             self.em = self.ev = None
         self.ws = _lib.Workspace(dev)
-        self.core = self.view.d_edges[: self.view.num_core]
         self.stream = None
+        # epoch e+1's negatives + shuffle are produced on a side stream while epoch e trains
+        self.sampler = EpochSampler(self.view, config.negatives_per_positive, self.g_dev)
 
     def begin_epoch(self):
-        neg, self.pcg = sample_negatives_device(self.view, self.config.negatives_per_positive, self.pcg, self.ws)
-        self.stream, self.pcg = stream_device(self.core, neg, self.pcg, self.view.device, self.ws)
+        self.stream = self.sampler.next()
 
     def closure(self, rnd: int):
         from .sampler import closure_device

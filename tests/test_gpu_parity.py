@@ -105,10 +105,34 @@ def test_permutation_bit_exact(n, seed):
     ref.bit_generator.state = gen.bit_generator.state
     want = ref.permutation(n)
     dev = torch.device("cuda")
-    perm, g2 = permutation_device(n, _lib.pcg_from_numpy(gen), dev)
+    g_dev = _lib.pcg_to_device(_lib.pcg_from_numpy(gen), dev)
+    perm, consumed = permutation_device(n, g_dev, dev)
     np.testing.assert_array_equal(perm.cpu().numpy(), want)
-    _lib.pcg_to_numpy(g2, gen)
+    assert int(consumed.item()) >= 0
+    _lib.pcg_to_numpy(_lib.pcg_from_device(g_dev), gen)
     assert gen.bit_generator.state == ref.bit_generator.state
+
+
+def test_epoch_sampler_matches_reference_streams():
+    """The async side-stream epoch pipeline reproduces the reference's
+    per-epoch draws (negatives, then permutation) epoch after epoch."""
+    g = load_golden("synth_p4")
+    graph, pset, cfg = golden_pset(g)
+    v = kb.build_view(pset.partitions[0], graph.num_entities, graph.num_relations)
+    from paper_2201_02791_b200.sampler import EpochSampler
+    seed = 1234
+    g_dev = _lib.pcg_to_device(_lib.pcg_from_numpy(np.random.default_rng(seed)), v.device)
+    es = EpochSampler(v, 1, g_dev)
+    rng = np.random.default_rng(seed)
+    ov = ko.make_view(pset.partitions[0].core, pset.partitions[0].support, graph.num_entities,
+                      graph.num_relations, pool_size=pset.partitions[0].pool_size)
+    for epoch in range(4):
+        ds = es.next()
+        neg = ko.corrupt(ov, 1, rng)
+        want = ko.batch_stream(ov.core_edges, neg, ds.total, rng)[0]
+        torch.cuda.synchronize()
+        np.testing.assert_array_equal(ds.triples.cpu().numpy()[: ds.total], want.triples)
+        np.testing.assert_array_equal(ds.labels.cpu().numpy()[: ds.total], want.labels)
 
 
 @pytest.mark.parametrize("name", SCEN)
