@@ -318,6 +318,9 @@ class Trainer:
         self.grads_local = torch.zeros((nloc, D), dtype=torch.float32, device=self.dev)
         self.grads_all = (torch.zeros((self.P, D), dtype=torch.float32, device=self.dev) if self.dist
                           else self.grads_local)
+        if self.dist:
+            self._recv = torch.empty((self.world * nloc, D), dtype=torch.float32, device=self.dev)
+            self._gidx = payload_order(self.P, self.world, self.dev)
         self.m = torch.zeros(D, dtype=torch.float32, device=self.dev)
         self.v = torch.zeros(D, dtype=torch.float32, device=self.dev)
         self.flags = torch.zeros(1, dtype=torch.int32, device=self.dev)
@@ -364,14 +367,7 @@ class Trainer:
         self.round_in_epoch += 1
 
     def _gather(self):
-        torch = _torch()
-        dist = torch.distributed
-        W, nloc = self.world, len(self.workers)
-        recv = torch.empty((W * nloc, self.D), dtype=torch.float32, device=self.dev)
-        dist.all_gather_into_tensor(recv, self.grads_local)
-        # rank r slot j holds partition r + j*W -> reorder into partition order
-        idx = torch.tensor([(p % W) * nloc + p // W for p in range(self.P)], device=self.dev)
-        torch.index_select(recv, 0, idx, out=self.grads_all)
+        gather_partition_payloads(self.grads_local, self.P, self.world, self.grads_all, self._recv, self._gidx)
 
     def check(self):
         for w in self.workers:
@@ -422,6 +418,34 @@ class Trainer:
         for r in range(1, self.world):
             if not torch.equal(allr[0], allr[r]):
                 raise ProtocolError(f"replica divergence: rank {r} dense blocks differ from rank 0")
+
+
+def payload_order(P: int, world: int, device):
+    """Rank r owns partitions r, r+W, ...: slot j of rank r is partition
+    r + j*W. Index that reorders the all-gathered slots into partition order
+    (the payload order of ref:trainer.py:430-438)."""
+    torch = _torch()
+    nloc = P // world
+    return torch.tensor([(p % world) * nloc + p // world for p in range(P)], dtype=torch.long, device=device)
+
+
+def gather_partition_payloads(local, P: int, world: int, out, recv=None, order=None):
+    """All-gather every rank's (P/W, D) gradient payloads into `out` (P, D)
+    in partition order; the fused tree-mean then runs on identical inputs on
+    every rank. NCCL on device tensors (gloo for CPU tests)."""
+    torch = _torch()
+    dist = torch.distributed
+    nloc, D = local.shape
+    if recv is None:
+        recv = torch.empty((world * nloc, D), dtype=local.dtype, device=local.device)
+    if order is None:
+        order = payload_order(P, world, local.device)
+    if local.is_cuda:
+        dist.all_gather_into_tensor(recv, local)
+    else:
+        dist.all_gather(list(recv.chunk(world)), local)
+    torch.index_select(recv, 0, order, out=out)
+    return out
 
 
 def train(pset: PartitionSet, graph, model_config: ModelConfig, train_config: TrainConfig,
