@@ -206,13 +206,16 @@ kg_status kg_stream_gather(const int32_t* pos, int64_t npos, const int32_t* neg,
 /* R7/R8  Layered closure (ref:sampler.py:310-376)                          */
 /* ---------------------------------------------------------------------- */
 int64_t kg_closure_workspace_bytes(int32_t n);
-/* Seeds = endpoints of batch rows (start+q) mod total, q < b, of the
+/* start_dev (optional, device int64) overrides `start` so a captured CUDA
+ * graph can be replayed for every round. Seeds = endpoints of batch rows
+ * (start+q) mod total, q < b, of the
  * (total,3) stream; or, when stream_triples == NULL, the ids seed_ids[b].
  * Writes vertex_order (seeds ascending, then each hop's new sources
  * ascending), pos[n] (-1 if absent) and counts[hops+1] (device). */
-kg_status kg_closure(const int32_t* stream_triples, int64_t total, int64_t start, int64_t b,
-                     const int32_t* seed_ids, const kg_graph_csr* g, int32_t hops, int32_t* vertex_order,
-                     int32_t* pos, int32_t* counts, void* ws, int64_t ws_bytes, void* stream);
+kg_status kg_closure(const int32_t* stream_triples, int64_t total, int64_t start, const int64_t* start_dev,
+                     int64_t b, const int32_t* seed_ids, const kg_graph_csr* g, int32_t hops,
+                     int32_t* vertex_order, int32_t* pos, int32_t* counts, void* ws, int64_t ws_bytes,
+                     void* stream);
 
 /* ---------------------------------------------------------------------- */
 /* R13-R17  RGCN layer forward / backward, DistMult + BCE                  */
@@ -246,7 +249,8 @@ int64_t kg_loss_workspace_bytes(int64_t b, int32_t n, int32_t d, int32_t R);
  * seeds, by local id). Non-finite score/loss sets bits in *flags. */
 kg_status kg_distmult_loss(const float* H, int32_t d, int32_t n_local, const float* decoder, int32_t R,
                            const int32_t* stream_triples, const float* labels, int64_t total, int64_t start,
-                           int64_t b, const int32_t* vertex_order, const int32_t* counts, float* dH,
+                           const int64_t* start_dev, int64_t b, const int32_t* vertex_order, const int32_t* counts,
+                           float* dH,
                            float* d_decoder, float* loss_out, float* scores_out, uint32_t* flags, void* ws,
                            int64_t ws_bytes, void* stream);
 
@@ -254,20 +258,21 @@ kg_status kg_distmult_loss(const float* H, int32_t d, int32_t n_local, const flo
 /* R19/R20  Reduction + optimizer (ref:trainer.py:63-151)                  */
 /* ---------------------------------------------------------------------- */
 int64_t kg_optim_workspace_bytes(int64_t n);
-/* Dense step on the flat block buffer. grads_all holds P payloads
+/* step_dev (optional, device int64 Adam step t) overrides bc1/bc2 for
+ * graph replay. Dense step on the flat block buffer. grads_all holds P payloads
  * back to back (P*n); they are combined in the reference's pairwise-tree
  * order and divided by P (ref:trainer.py:77-86) inside the same kernel.
  * optimizer: 0 = sgd, 1 = adam. grad_clip <= 0 disables clipping. */
 kg_status kg_dense_step(float* params, float* m, float* v, const float* grads_all, int32_t P, int64_t n,
                         int32_t optimizer, float lr, float beta1, float beta2, float eps, double bc1,
-                        double bc2, float grad_clip, uint32_t* flags, void* ws, int64_t ws_bytes,
-                        void* stream);
+                        double bc2, const int64_t* step_dev, float grad_clip, uint32_t* flags, void* ws,
+                        int64_t ws_bytes, void* stream);
 /* Lazy sparse rows (ref:trainer.py:136-147): rows = vertex_order[0:counts[k]]
  * of the (n,d) table; grad rows by local id. */
 kg_status kg_sparse_step(float* table, float* m, float* v, const float* grad, const int32_t* rows,
                          const int32_t* counts, int32_t k, int32_t d, int32_t optimizer, float lr,
-                         float beta1, float beta2, float eps, double bc1, double bc2, int32_t n_max,
-                         void* stream);
+                         float beta1, float beta2, float eps, double bc1, double bc2, const int64_t* step_dev,
+                         int32_t n_max, void* stream);
 
 /* ---------------------------------------------------------------------- */
 /* R24-R26  Filtered evaluation (ref:evaluate.py:93-225)                   */

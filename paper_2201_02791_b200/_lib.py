@@ -72,7 +72,7 @@ _PROTOS = {
     "kg_perm_resolve": (ST, [P, c_int64, P, P, c_int64, P]),
     "kg_stream_gather": (ST, [P, c_int64, P, c_int64, P, P, P, P]),
     "kg_closure_workspace_bytes": (c_int64, [c_int32]),
-    "kg_closure": (ST, [P, c_int64, c_int64, c_int64, P, POINTER(KgGraphCsr), c_int32, P, P, P, P,
+    "kg_closure": (ST, [P, c_int64, c_int64, P, c_int64, P, POINTER(KgGraphCsr), c_int32, P, P, P, P,
                         c_int64, P]),
     "kg_layer_workspace_bytes": (c_int64, [POINTER(KgGraphCsr), c_int32, c_int32, c_int32]),
     "kg_rgcn_forward": (ST, [POINTER(KgGraphCsr), POINTER(KgLayerParams), P, P, P, P, P, c_int32, c_int32,
@@ -83,13 +83,13 @@ _PROTOS = {
     "kg_gemm_f32": (ST, [P, c_int64, P, P, c_int64, P, c_int64, P, c_int64, c_int64, c_int64, c_int32, c_int32,
                          c_int32, P, c_int64, P]),
     "kg_loss_workspace_bytes": (c_int64, [c_int64, c_int32, c_int32, c_int32]),
-    "kg_distmult_loss": (ST, [P, c_int32, c_int32, P, c_int32, P, P, c_int64, c_int64, c_int64, P, P, P,
+    "kg_distmult_loss": (ST, [P, c_int32, c_int32, P, c_int32, P, P, c_int64, c_int64, P, c_int64, P, P, P,
                               P, P, P, P, P, c_int64, P]),
     "kg_optim_workspace_bytes": (c_int64, [c_int64]),
     "kg_dense_step": (ST, [P, P, P, P, c_int32, c_int64, c_int32, c_float, c_float, c_float, c_float,
-                           c_double, c_double, c_float, P, P, c_int64, P]),
+                           c_double, c_double, P, c_float, P, P, c_int64, P]),
     "kg_sparse_step": (ST, [P, P, P, P, P, P, c_int32, c_int32, c_int32, c_float, c_float, c_float,
-                            c_float, c_double, c_double, c_int32, P]),
+                            c_float, c_double, c_double, P, c_int32, P]),
     "kg_eval_workspace_bytes": (c_int64, [c_int64]),
     "kg_eval_filtered": (ST, [P, c_int32, c_int32, P, c_int32, P, c_int64, P, c_int64, P, c_int64,
                               c_int32, c_int32, P, P, P, c_int64, P]),

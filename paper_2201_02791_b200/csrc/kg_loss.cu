@@ -25,13 +25,16 @@ struct LossArgs {
   const int32_t* tri;
   const float* labels;
   int64_t total, start, b;
+  const int64_t* start_dev;   // when set, the batch offset is read on the device (graph replay)
   float* dg;
   float* per;
   float* scores;
   uint32_t* flags;
 };
 
-__device__ __forceinline__ int64_t row_of(const LossArgs& a, int64_t i) { return (a.start + i) % a.total; }
+__device__ __forceinline__ int64_t row_of(const LossArgs& a, int64_t i) {
+  return ((a.start_dev ? __ldg(a.start_dev) : a.start) + i) % a.total;
+}
 
 __global__ void __launch_bounds__(256) k_score(LossArgs a) {
   const int lane = lane_id();
@@ -308,7 +311,8 @@ int64_t kg_loss_workspace_bytes(int64_t b, int32_t n, int32_t d, int32_t R) {
 
 kg_status kg_distmult_loss(const float* H, int32_t d, int32_t n_local, const float* decoder, int32_t R,
                            const int32_t* tri,
-                           const float* labels, int64_t total, int64_t start, int64_t b, const int32_t* order,
+                           const float* labels, int64_t total, int64_t start, const int64_t* start_dev, int64_t b,
+                           const int32_t* order,
                            const int32_t* counts, float* dH, float* d_decoder, float* loss_out, float* scores_out,
                            uint32_t* flags, void* ws, int64_t ws_bytes, void* stream) {
   cudaStream_t st = as_stream(stream);
@@ -330,7 +334,7 @@ kg_status kg_distmult_loss(const float* H, int32_t d, int32_t n_local, const flo
   seg_ws(2 * b, ngmax, d, &wv, a);
   KG_REQUIRE(a.used <= (size_t)ws_bytes && dg != nullptr, KG_ERR_VALIDATION, "loss workspace too small");
 
-  LossArgs la{H, d, decoder, tri, labels, total, start, b, dg, per, scores_out, flags};
+  LossArgs la{H, d, decoder, tri, labels, total, start, b, start_dev, dg, per, scores_out, flags};
   KG_LAUNCH("k_score", k_score, persistent_blocks(b * 32, 256, 8), 256, 0, st, la);
   KG_CHECK_LAUNCH("k_score");
   int nb = persistent_blocks(b, 256, 4);

@@ -70,12 +70,21 @@ struct StepArgs {
   int adam;
   float lr, b1, b2, eps;
   float inv_bc1, inv_bc2;
+  const int64_t* step_dev;  // when set: Adam step t read on the device (graph replay)
   const float* scale;    // optional clip scale (device)
   uint32_t* flags;
 };
 
+__device__ __forceinline__ void bias_corrections(const int64_t* step_dev, float b1, float b2, float& i1, float& i2) {
+  if (!step_dev) return;
+  const double t = (double)*step_dev;
+  i1 = (float)(1.0 / (1.0 - pow((double)b1, t)));
+  i2 = (float)(1.0 / (1.0 - pow((double)b2, t)));
+}
+
 __global__ void k_dense_step(StepArgs a) {
   const float sc = a.scale ? *a.scale : 1.f;
+  bias_corrections(a.step_dev, a.b1, a.b2, a.inv_bc1, a.inv_bc2);
   bool bad = false;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < a.n; i += (int64_t)gridDim.x * blockDim.x) {
     float g = (a.P == 1) ? a.g[i] : tree_mean_at(a.g, a.P, a.n, i);
@@ -99,7 +108,8 @@ __global__ void k_dense_step(StepArgs a) {
 __global__ void k_sparse_step(float* __restrict__ table, float* __restrict__ m, float* __restrict__ v,
                               const float* __restrict__ grad, const int32_t* __restrict__ rows,
                               const int32_t* __restrict__ counts, int k, int d, int adam, float lr, float b1, float b2,
-                              float eps, float inv_bc1, float inv_bc2) {
+                              float eps, float inv_bc1, float inv_bc2, const int64_t* __restrict__ step_dev) {
+  bias_corrections(step_dev, b1, b2, inv_bc1, inv_bc2);
   const int32_t nrows = counts[k];
   const int64_t total = (int64_t)nrows * d;
   for (int64_t x = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; x < total; x += (int64_t)gridDim.x * blockDim.x) {
@@ -131,7 +141,8 @@ int64_t kg_optim_workspace_bytes(int64_t n) {
 
 kg_status kg_dense_step(float* params, float* m, float* v, const float* grads_all, int32_t P, int64_t n,
                         int32_t optimizer, float lr, float beta1, float beta2, float eps, double bc1, double bc2,
-                        float grad_clip, uint32_t* flags, void* ws, int64_t ws_bytes, void* stream) {
+                        const int64_t* step_dev, float grad_clip, uint32_t* flags, void* ws, int64_t ws_bytes,
+                        void* stream) {
   cudaStream_t st = as_stream(stream);
   KG_REQUIRE(P >= 1 && P <= MAXP, KG_ERR_PROTOCOL, "payload count %d out of range", P);
   KG_REQUIRE(ws_bytes >= kg_optim_workspace_bytes(n), KG_ERR_VALIDATION, "optim workspace too small");
@@ -140,7 +151,7 @@ kg_status kg_dense_step(float* params, float* m, float* v, const float* grads_al
   double* part = a.take<double>(1024);
   float* scale = a.take<float>(1);
   StepArgs s{params, m, v, grads_all, P, n, optimizer == 1, lr, beta1, beta2, eps,
-             (float)(1.0 / bc1), (float)(1.0 / bc2), nullptr, flags};
+             (float)(1.0 / bc1), (float)(1.0 / bc2), step_dev, nullptr, flags};
   int blocks = persistent_blocks(n, 256, 4);
   if (grad_clip > 0.f) {
     const float* g = grads_all;
@@ -163,10 +174,11 @@ kg_status kg_dense_step(float* params, float* m, float* v, const float* grads_al
 
 kg_status kg_sparse_step(float* table, float* m, float* v, const float* grad, const int32_t* rows,
                          const int32_t* counts, int32_t k, int32_t d, int32_t optimizer, float lr, float beta1,
-                         float beta2, float eps, double bc1, double bc2, int32_t n_max, void* stream) {
+                         float beta2, float eps, double bc1, double bc2, const int64_t* step_dev, int32_t n_max,
+                         void* stream) {
   KG_LAUNCH("k_sparse_step", k_sparse_step, persistent_blocks((int64_t)n_max * d, 256, 8), 256, 0, as_stream(stream), 
       table, m, v, grad, rows, counts, k, d, optimizer == 1, lr, beta1, beta2, eps, (float)(1.0 / bc1),
-      (float)(1.0 / bc2));
+      (float)(1.0 / bc2), step_dev);
   KG_CHECK_LAUNCH("k_sparse_step");
   return KG_OK;
 }

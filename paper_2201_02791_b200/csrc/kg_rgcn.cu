@@ -10,20 +10,22 @@
 //             dV_b     = X^T dS_b                            (split-K GEMM)
 //             d a[r,b] = sum_{e in r} norm_e <(X V_b)[src_e], dZ[dst_e]>
 //
-// Gather/scatter passes run one warp per static work chunk (<= C messages of
+// Gather/scatter passes run one warp per static work chunk (<= 64 messages of
 // one row, kg_chunks.cu) so preferential-attachment hubs are spread over many
-// warps; rows cut into several chunks are finished by a combine pass that
-// adds the chunk partials in order (no atomics, deterministic). Lanes cover
-// the feature dimension (float4 per lane for d % 4 == 0, d <= 128); eight
-// gathered rows are in flight per lane. Within a (row, relation) run the
-// forward norm is constant, so the run's rows are summed before applying
-// norm * a[r, b] once.
+// warps; rows cut into several chunks are finished by a combine pass (one
+// block per row) that adds the chunk partials in a fixed order (no atomics,
+// deterministic). Lanes cover the feature dimension (float4 per lane for
+// d % 4 == 0, d <= 128). A chunk's metadata (2 messages per lane) is fetched
+// in one shot and each message carries its own coefficients norm_e*a[r_e,b],
+// so gathered rows stream with UNR loads in flight per lane and no serial
+// dependency between messages.
 #include "kg_gemm.cuh"
 
 namespace kg {
 
 constexpr int MAXB = 4;
-constexpr int UNR = 8;   // gathered rows in flight per lane
+constexpr int UNR = 8;     // gathered rows in flight per lane
+constexpr int MAXC = 64;   // messages per chunk handled by one warp (2 per lane)
 
 template <int VEC>
 struct VecIO;
@@ -72,30 +74,6 @@ __device__ __forceinline__ float warp_sum8(const float* x) {
 
 __device__ __forceinline__ int sum8_entry(unsigned l) { return ((l >> 4) & 1) * 4 + ((l >> 3) & 1) * 2 + ((l >> 2) & 1); }
 
-// sum[] = sum_{k < n} p[(s0 + k) * stride] in k order, 8 loads in flight
-template <int VEC>
-__device__ __forceinline__ void sum_partials(const float* __restrict__ p, int32_t s0, int32_t n, int64_t stride,
-                                             float* sum) {
-#pragma unroll
-  for (int cc = 0; cc < VEC; ++cc) sum[cc] = 0.f;
-  int32_t k = 0;
-  for (; k + 8 <= n; k += 8) {
-    float x[8][VEC];
-#pragma unroll
-    for (int u = 0; u < 8; ++u) VecIO<VEC>::load(p + (int64_t)(s0 + k + u) * stride, x[u]);
-#pragma unroll
-    for (int u = 0; u < 8; ++u)
-#pragma unroll
-      for (int cc = 0; cc < VEC; ++cc) sum[cc] += x[u][cc];
-  }
-  for (; k < n; ++k) {
-    float x[VEC];
-    VecIO<VEC>::load(p + (int64_t)(s0 + k) * stride, x);
-#pragma unroll
-    for (int cc = 0; cc < VEC; ++cc) sum[cc] += x[cc];
-  }
-}
-
 struct Chunks {
   const int32_t* ptr;
   const int32_t* row;
@@ -121,25 +99,33 @@ struct AggArgs {
   float* partial;        // (split chunks, B*d)
 };
 
-template <int VEC, int S>
-__device__ __forceinline__ void zero3(float (&a)[MAXB][S][VEC]) {
+template <int NB, int VEC, int S>
+__device__ __forceinline__ void zero3(float (&a)[NB][S][VEC]) {
 #pragma unroll
-  for (int b = 0; b < MAXB; ++b)
+  for (int b = 0; b < NB; ++b)
 #pragma unroll
     for (int s = 0; s < S; ++s)
 #pragma unroll
       for (int c = 0; c < VEC; ++c) a[b][s][c] = 0.f;
 }
 
-template <int VEC, int S>
-__global__ void __launch_bounds__(256) k_aggregate(AggArgs a) {
+// metadata of message `lane + 32*h` of the chunk, coefficient c_b = norm * a[rel, b]
+template <int NB>
+struct EdgeMeta {
+  int32_t other[2];        // src (forward) / destination position (backward)
+  float cf[2][NB];
+};
+
+template <int NB, int VEC, int S>
+__global__ void __launch_bounds__(256, 3) k_aggregate(AggArgs a) {
   extern __shared__ float coef[];
   for (int i = threadIdx.x; i < a.G * a.B; i += blockDim.x) coef[i] = a.coeffs[i];
   __syncthreads();
   const int lane = lane_id();
   const int32_t T = a.counts[a.t];
   const int32_t NC = a.ck.counts[0];
-  const int d = a.d, B = a.B;
+  const int d = a.d;
+  constexpr int B = NB;
   const int warps = (gridDim.x * blockDim.x) >> 5;
   bool slot_ok[S];
 #pragma unroll
@@ -150,62 +136,52 @@ __global__ void __launch_bounds__(256) k_aggregate(AggArgs a) {
     if (p < 0 || p >= T) continue;
     const int32_t cbase = a.ck.ptr[v];
     const int32_t nch = a.ck.ptr[v + 1] - cbase;
-    const int32_t e_row1 = a.indptr[v + 1];
     const int32_t beg = a.indptr[v] + (int32_t)(c - cbase) * a.ck.C;
-    const int32_t end = min(beg + a.ck.C, e_row1);
-    float acc[MAXB][S][VEC];
-    float run[S][VEC];
-    zero3<VEC, S>(acc);
+    const int32_t cnt = min(beg + a.ck.C, a.indptr[v + 1]) - beg;
+    EdgeMeta<NB> m;
 #pragma unroll
-    for (int s = 0; s < S; ++s)
+    for (int h = 0; h < 2; ++h) {
+      const int e = lane + 32 * h;
+      m.other[h] = 0;
 #pragma unroll
-      for (int q = 0; q < VEC; ++q) run[s][q] = 0.f;
-    for (int32_t base = beg; base < end; base += 32) {
-      const int cnt = min(32, end - base);
-      int32_t my_src = 0, my_rel = -1;
-      float my_norm = 0.f;
-      if (lane < cnt) {
-        my_src = a.src[base + lane];
-        my_rel = a.rel[base + lane];
-        my_norm = a.norm[base + lane];
+      for (int b = 0; b < NB; ++b) m.cf[h][b] = 0.f;
+      if (e < cnt) {
+        m.other[h] = a.src[beg + e];
+        const int32_t r = a.rel[beg + e];
+        const float w = a.norm[beg + e];
+#pragma unroll
+        for (int b = 0; b < NB; ++b)
+          if (b < B) m.cf[h][b] = w * coef[r * B + b];
       }
-      for (int j = 0; j < cnt; j += UNR) {
+    }
+    float acc[NB][S][VEC];
+    zero3<NB, VEC, S>(acc);
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int nh = min(32, cnt - 32 * h);
+      for (int j = 0; j < nh; j += UNR) {
         float xs[UNR][S][VEC];
 #pragma unroll
         for (int q = 0; q < UNR; ++q) {
-          int32_t u = __shfl_sync(0xffffffffu, my_src, (j + q) & 31);
-          if (j + q < cnt) {
+          const int32_t u = __shfl_sync(0xffffffffu, m.other[h], (j + q) & 31);
 #pragma unroll
-            for (int s = 0; s < S; ++s)
-              if (slot_ok[s]) VecIO<VEC>::load(a.H + (int64_t)u * d + (s * 32 + lane) * VEC, xs[q][s]);
+          for (int s = 0; s < S; ++s) {
+            if (j + q < nh && slot_ok[s]) VecIO<VEC>::load(a.H + (int64_t)u * d + (s * 32 + lane) * VEC, xs[q][s]);
+            else
+#pragma unroll
+              for (int cc = 0; cc < VEC; ++cc) xs[q][s][cc] = 0.f;
           }
         }
 #pragma unroll
         for (int q = 0; q < UNR; ++q) {
-          int32_t r = __shfl_sync(0xffffffffu, my_rel, (j + q) & 31);
-          int32_t rn = __shfl_sync(0xffffffffu, my_rel, (j + q + 1) & 31);
-          float w = __shfl_sync(0xffffffffu, my_norm, (j + q) & 31);
-          if (j + q < cnt) {
-            if (j + q + 1 >= cnt) rn = -1;   // flush at the end of every 32-edge batch
 #pragma unroll
-            for (int s = 0; s < S; ++s)
-#pragma unroll
-              for (int cc = 0; cc < VEC; ++cc) run[s][cc] += xs[q][s][cc];
-            if (rn != r) {
-#pragma unroll
-              for (int b = 0; b < MAXB; ++b) {
-                if (b < B) {
-                  float cf = w * coef[r * B + b];
-#pragma unroll
-                  for (int s = 0; s < S; ++s)
-#pragma unroll
-                    for (int cc = 0; cc < VEC; ++cc) acc[b][s][cc] = fmaf(cf, run[s][cc], acc[b][s][cc]);
-                }
-              }
+          for (int b = 0; b < NB; ++b) {
+            if (b < B) {
+              const float cf = __shfl_sync(0xffffffffu, m.cf[h][b], (j + q) & 31);
 #pragma unroll
               for (int s = 0; s < S; ++s)
 #pragma unroll
-                for (int cc = 0; cc < VEC; ++cc) run[s][cc] = 0.f;
+                for (int cc = 0; cc < VEC; ++cc) acc[b][s][cc] = fmaf(cf, xs[q][s][cc], acc[b][s][cc]);
             }
           }
         }
@@ -219,7 +195,7 @@ __global__ void __launch_bounds__(256) k_aggregate(AggArgs a) {
       for (int s = 0; s < S; ++s)
         if (slot_ok[s]) VecIO<VEC>::load(a.H + (int64_t)v * d + (s * 32 + lane) * VEC, xv[s]);
 #pragma unroll
-      for (int b = 0; b < MAXB; ++b) {
+      for (int b = 0; b < NB; ++b) {
         if (b < B) {
           float cf = coef[(a.G - 1) * B + b];
 #pragma unroll
@@ -234,7 +210,7 @@ __global__ void __launch_bounds__(256) k_aggregate(AggArgs a) {
       out = a.partial + (int64_t)a.ck.slot[c] * B * d;
     }
 #pragma unroll
-    for (int b = 0; b < MAXB; ++b)
+    for (int b = 0; b < NB; ++b)
       if (b < B)
 #pragma unroll
         for (int s = 0; s < S; ++s)
@@ -242,40 +218,60 @@ __global__ void __launch_bounds__(256) k_aggregate(AggArgs a) {
   }
 }
 
-// rows cut into several chunks: acc[p] = sum of chunk partials (in order) + self loop
-template <int VEC, int S>
-__global__ void __launch_bounds__(256) k_aggregate_combine(AggArgs a) {
-  const int lane = lane_id();
+// Rows cut into several chunks: one block (8 warps) per row. Warp w adds the
+// partials of chunks w, w+8, ... in order; the 8 warp sums are added in warp
+// order (fixed summation order), plus the self-loop term. width = B*d floats.
+constexpr int CB_THREADS = 256;
+constexpr int CB_WARPS = CB_THREADS / 32;
+
+__device__ __forceinline__ void block_sum_partials(const float* __restrict__ partial, int32_t s0, int32_t nparts,
+                                                   int width, int col, float* red /* smem [8][32] */,
+                                                   float& out) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  float sum = 0.f;
+  if (col < width) {
+    int32_t k = warp;
+    for (; k + 3 * CB_WARPS < nparts; k += 4 * CB_WARPS) {
+      float x0 = __ldg(partial + (int64_t)(s0 + k) * width + col);
+      float x1 = __ldg(partial + (int64_t)(s0 + k + CB_WARPS) * width + col);
+      float x2 = __ldg(partial + (int64_t)(s0 + k + 2 * CB_WARPS) * width + col);
+      float x3 = __ldg(partial + (int64_t)(s0 + k + 3 * CB_WARPS) * width + col);
+      sum += x0;
+      sum += x1;
+      sum += x2;
+      sum += x3;
+    }
+    for (; k < nparts; k += CB_WARPS) sum += __ldg(partial + (int64_t)(s0 + k) * width + col);
+  }
+  red[warp * 32 + lane] = sum;
+  __syncthreads();
+  float tot = 0.f;
+  if (warp == 0)
+#pragma unroll
+    for (int w = 0; w < CB_WARPS; ++w) tot += red[w * 32 + lane];
+  __syncthreads();
+  out = tot;
+}
+
+__global__ void __launch_bounds__(CB_THREADS) k_aggregate_combine(AggArgs a) {
+  __shared__ float red[CB_WARPS * 32];
   const int32_t T = a.counts[a.t];
   const int32_t NS = a.ck.counts[2];
-  const int d = a.d, B = a.B;
-  const int warps = (gridDim.x * blockDim.x) >> 5;
-  bool slot_ok[S];
-#pragma unroll
-  for (int s = 0; s < S; ++s) slot_ok[s] = (s * 32 + lane) * VEC < d;
-  for (int64_t r = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; r < NS; r += warps) {
+  const int width = a.B * a.d;
+  for (int64_t r = blockIdx.x; r < NS; r += gridDim.x) {
     const int32_t v = a.ck.split[r];
     const int32_t p = a.pos[v];
     if (p < 0 || p >= T) continue;
     const int32_t c0 = a.ck.ptr[v], c1 = a.ck.ptr[v + 1];
     const int32_t s0 = a.ck.slot[c0];
-    float xv[S][VEC];
-#pragma unroll
-    for (int s = 0; s < S; ++s)
-      if (slot_ok[s]) VecIO<VEC>::load(a.H + (int64_t)v * d + (s * 32 + lane) * VEC, xv[s]);
-    float* out = a.acc + (int64_t)p * B * d;
-    for (int b = 0; b < B; ++b) {
-      float cf = a.coeffs[(a.G - 1) * B + b];
-#pragma unroll
-      for (int s = 0; s < S; ++s) {
-        if (!slot_ok[s]) continue;
-        float sum[VEC];
-#pragma unroll
-        for (int cc = 0; cc < VEC; ++cc) sum[cc] = 0.f;
-        sum_partials<VEC>(a.partial + (int64_t)b * d + (s * 32 + lane) * VEC, s0, c1 - c0, (int64_t)B * d, sum);
-#pragma unroll
-        for (int cc = 0; cc < VEC; ++cc) sum[cc] = fmaf(cf, xv[s][cc], sum[cc]);
-        VecIO<VEC>::store(out + (int64_t)b * d + (s * 32 + lane) * VEC, sum);
+    for (int col0 = 0; col0 < width; col0 += 32) {
+      const int col = col0 + (threadIdx.x & 31);
+      float tot;
+      block_sum_partials(a.partial, s0, c1 - c0, width, col, red, tot);
+      if ((threadIdx.x >> 5) == 0 && col < width) {
+        const int b = col / a.d, k = col % a.d;
+        const float self = a.coeffs[(a.G - 1) * a.B + b] * a.H[(int64_t)v * a.d + k];
+        a.acc[(int64_t)p * width + col] = tot + self;
       }
     }
   }
@@ -300,8 +296,8 @@ struct CscArgs {
   float* partial;        // (split chunks, B*d)
 };
 
-template <int VEC, int S>
-__global__ void __launch_bounds__(256) k_csc_backward(CscArgs a) {
+template <int NB, int VEC, int S>
+__global__ void __launch_bounds__(256, 3) k_csc_backward(CscArgs a) {
   extern __shared__ float coef[];
   for (int i = threadIdx.x; i < a.G * a.B; i += blockDim.x) coef[i] = a.coeffs[i];
   __syncthreads();
@@ -309,7 +305,8 @@ __global__ void __launch_bounds__(256) k_csc_backward(CscArgs a) {
   const int32_t T = a.counts[a.t];
   const int32_t Sn = a.counts[a.t + 1];
   const int32_t NC = a.ck.counts[0];
-  const int d = a.d, B = a.B;
+  const int d = a.d;
+  constexpr int B = NB;
   const int warps = (gridDim.x * blockDim.x) >> 5;
   bool slot_ok[S];
 #pragma unroll
@@ -320,52 +317,76 @@ __global__ void __launch_bounds__(256) k_csc_backward(CscArgs a) {
     if (q < 0 || q >= Sn) continue;
     const int32_t cbase = a.ck.ptr[u];
     const int32_t nch = a.ck.ptr[u + 1] - cbase;
-    const int32_t e_row1 = a.c_indptr[u + 1];
     const int32_t beg = a.c_indptr[u] + (int32_t)(c - cbase) * a.ck.C;
-    const int32_t end = min(beg + a.ck.C, e_row1);
-    float y[MAXB][S][VEC];
-    float acc[MAXB][S][VEC];
-    float run[S][VEC];
-    zero3<VEC, S>(acc);
-    zero3<VEC, S>(y);
+    const int32_t cnt = min(beg + a.ck.C, a.c_indptr[u + 1]) - beg;
+    // metadata: destination position (-1 if not a target) and coefficients
+    EdgeMeta<NB> m;
+    float nrm[2];
 #pragma unroll
-    for (int b = 0; b < MAXB; ++b)
+    for (int h = 0; h < 2; ++h) {
+      const int e = (int)lane + 32 * h;
+      m.other[h] = -1;
+      nrm[h] = 0.f;
+#pragma unroll
+      for (int b = 0; b < NB; ++b) m.cf[h][b] = 0.f;
+      if (e < cnt) {
+        const int32_t w = a.c_dst[beg + e];
+        const int32_t r = a.c_rel[beg + e];
+        const float nw = a.c_norm[beg + e];
+        const int32_t pw = a.pos[w];
+        if (pw >= 0 && pw < T) {
+          m.other[h] = pw;
+          nrm[h] = nw;
+#pragma unroll
+          for (int b = 0; b < NB; ++b)
+            if (b < B) m.cf[h][b] = nw * coef[r * B + b];
+        }
+      }
+    }
+    float y[NB][S][VEC];
+    float acc[NB][S][VEC];
+    zero3<NB, VEC, S>(acc);
+    zero3<NB, VEC, S>(y);
+#pragma unroll
+    for (int b = 0; b < NB; ++b)
       if (b < B)
 #pragma unroll
         for (int s = 0; s < S; ++s)
           if (slot_ok[s]) VecIO<VEC>::load(a.Y + ((int64_t)q * B + b) * d + (s * 32 + lane) * VEC, y[b][s]);
 #pragma unroll
-    for (int s = 0; s < S; ++s)
-#pragma unroll
-      for (int cc = 0; cc < VEC; ++cc) run[s][cc] = 0.f;
-    for (int32_t base = beg; base < end; base += 32) {
-      const int cnt = min(32, end - base);
-      int32_t my_rel = -1, my_pw = -1;
-      float my_norm = 0.f;
-      if ((int)lane < cnt) {
-        int32_t w = a.c_dst[base + lane];
-        my_rel = a.c_rel[base + lane];
-        my_norm = a.c_norm[base + lane];
-        int32_t pw = a.pos[w];
-        my_pw = (pw >= 0 && pw < T) ? pw : -1;
-      }
-      for (int j = 0; j < cnt; j += UNR) {
+    for (int h = 0; h < 2; ++h) {
+      const int nh = min(32, cnt - 32 * h);
+      for (int j = 0; j < nh; j += UNR) {
         float zs[UNR][S][VEC];
 #pragma unroll
         for (int k = 0; k < UNR; ++k) {
-          int32_t pw = __shfl_sync(0xffffffffu, my_pw, (j + k) & 31);
+          const int32_t pw = __shfl_sync(0xffffffffu, m.other[h], (j + k) & 31);
 #pragma unroll
           for (int s = 0; s < S; ++s) {
-            if (j + k < cnt && pw >= 0 && slot_ok[s])
+            if (j + k < nh && pw >= 0 && slot_ok[s])
               VecIO<VEC>::load(a.dZ + (int64_t)pw * d + (s * 32 + lane) * VEC, zs[k][s]);
             else
 #pragma unroll
               for (int cc = 0; cc < VEC; ++cc) zs[k][s][cc] = 0.f;
           }
         }
-        // per-edge dots <Y_b[u], dZ[dst]> for the 8 edges, one transposed warp reduction per b
+        // dS_b += c_eb * dZ[dst]
 #pragma unroll
-        for (int b = 0; b < MAXB; ++b) {
+        for (int k = 0; k < UNR; ++k) {
+#pragma unroll
+          for (int b = 0; b < NB; ++b) {
+            if (b < B) {
+              const float cf = __shfl_sync(0xffffffffu, m.cf[h][b], (j + k) & 31);
+#pragma unroll
+              for (int s = 0; s < S; ++s)
+#pragma unroll
+                for (int cc = 0; cc < VEC; ++cc) acc[b][s][cc] = fmaf(cf, zs[k][s][cc], acc[b][s][cc]);
+            }
+          }
+        }
+        // per-edge dots <Y_b[u], dZ[dst]>: one transposed warp reduction per b
+#pragma unroll
+        for (int b = 0; b < NB; ++b) {
           if (b < B) {
             float part[UNR];
 #pragma unroll
@@ -377,40 +398,10 @@ __global__ void __launch_bounds__(256) k_csc_backward(CscArgs a) {
                 for (int cc = 0; cc < VEC; ++cc) dp = fmaf(y[b][s][cc], zs[k][s][cc], dp);
               part[k] = dp;
             }
-            float tot = warp_sum8(part);
-            int k = sum8_entry(lane);
-            float wk = __shfl_sync(0xffffffffu, my_norm, (j + k) & 31);
-            if ((lane & 3) == 0 && j + k < cnt) a.ed[(int64_t)(base + j + k) * B + b] = wk * tot;
-          }
-        }
-        // dS runs
-#pragma unroll
-        for (int k = 0; k < UNR; ++k) {
-          int32_t r = __shfl_sync(0xffffffffu, my_rel, (j + k) & 31);
-          int32_t rn = __shfl_sync(0xffffffffu, my_rel, (j + k + 1) & 31);
-          float w = __shfl_sync(0xffffffffu, my_norm, (j + k) & 31);
-          if (j + k < cnt) {
-            if (j + k + 1 >= cnt) rn = -1;
-#pragma unroll
-            for (int s = 0; s < S; ++s)
-#pragma unroll
-              for (int cc = 0; cc < VEC; ++cc) run[s][cc] = fmaf(w, zs[k][s][cc], run[s][cc]);
-            if (rn != r) {
-#pragma unroll
-              for (int b = 0; b < MAXB; ++b) {
-                if (b < B) {
-                  float cf = coef[r * B + b];
-#pragma unroll
-                  for (int s = 0; s < S; ++s)
-#pragma unroll
-                    for (int cc = 0; cc < VEC; ++cc) acc[b][s][cc] = fmaf(cf, run[s][cc], acc[b][s][cc]);
-                }
-              }
-#pragma unroll
-              for (int s = 0; s < S; ++s)
-#pragma unroll
-                for (int cc = 0; cc < VEC; ++cc) run[s][cc] = 0.f;
-            }
+            const float tot = warp_sum8(part);
+            const int k = sum8_entry(lane);
+            const float wk = __shfl_sync(0xffffffffu, nrm[h], (j + k) & 31);
+            if ((lane & 3) == 0 && j + k < nh) a.ed[(int64_t)(beg + 32 * h + j + k) * B + b] = wk * tot;
           }
         }
       }
@@ -428,7 +419,7 @@ __global__ void __launch_bounds__(256) k_csc_backward(CscArgs a) {
             for (int cc = 0; cc < VEC; ++cc) z[s][cc] = 0.f;
         }
 #pragma unroll
-        for (int b = 0; b < MAXB; ++b) {
+        for (int b = 0; b < NB; ++b) {
           if (b < B) {
             float cf = coef[(a.G - 1) * B + b];
             float dp = 0.f;
@@ -449,7 +440,7 @@ __global__ void __launch_bounds__(256) k_csc_backward(CscArgs a) {
       out = a.partial + (int64_t)a.ck.slot[c] * B * d;
     }
 #pragma unroll
-    for (int b = 0; b < MAXB; ++b)
+    for (int b = 0; b < NB; ++b)
       if (b < B)
 #pragma unroll
         for (int s = 0; s < S; ++s)
@@ -457,55 +448,47 @@ __global__ void __launch_bounds__(256) k_csc_backward(CscArgs a) {
   }
 }
 
-template <int VEC, int S>
-__global__ void __launch_bounds__(256) k_csc_combine(CscArgs a) {
-  const unsigned lane = lane_id();
+__global__ void __launch_bounds__(CB_THREADS) k_csc_combine(CscArgs a) {
+  __shared__ float red[CB_WARPS * 32];
+  __shared__ float dots[MAXB][CB_WARPS];
   const int32_t T = a.counts[a.t];
   const int32_t Sn = a.counts[a.t + 1];
   const int32_t NS = a.ck.counts[2];
-  const int d = a.d, B = a.B;
-  const int warps = (gridDim.x * blockDim.x) >> 5;
-  bool slot_ok[S];
-#pragma unroll
-  for (int s = 0; s < S; ++s) slot_ok[s] = (s * 32 + lane) * VEC < d;
-  for (int64_t r = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; r < NS; r += warps) {
+  const int width = a.B * a.d;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (int64_t r = blockIdx.x; r < NS; r += gridDim.x) {
     const int32_t u = a.ck.split[r];
     const int32_t q = a.pos[u];
     if (q < 0 || q >= Sn) continue;
     const int32_t c0 = a.ck.ptr[u], c1 = a.ck.ptr[u + 1];
     const int32_t s0 = a.ck.slot[c0];
-    float z[S][VEC];
     const bool self = q < T;
-#pragma unroll
-    for (int s = 0; s < S; ++s) {
-      if (self && slot_ok[s]) VecIO<VEC>::load(a.dZ + (int64_t)q * d + (s * 32 + lane) * VEC, z[s]);
-      else
-#pragma unroll
-        for (int cc = 0; cc < VEC; ++cc) z[s][cc] = 0.f;
-    }
-    float* out = a.dS + (int64_t)q * B * d;
-    for (int b = 0; b < B; ++b) {
-      float cf = a.coeffs[(a.G - 1) * B + b];
-      float dp = 0.f;
-#pragma unroll
-      for (int s = 0; s < S; ++s) {
-        float sum[VEC];
-#pragma unroll
-        for (int cc = 0; cc < VEC; ++cc) sum[cc] = 0.f;
-        if (slot_ok[s]) {
-          sum_partials<VEC>(a.partial + (int64_t)b * d + (s * 32 + lane) * VEC, s0, c1 - c0, (int64_t)B * d, sum);
-          float yv[VEC];
-          VecIO<VEC>::load(a.Y + ((int64_t)q * B + b) * d + (s * 32 + lane) * VEC, yv);
-#pragma unroll
-          for (int cc = 0; cc < VEC; ++cc) {
-            sum[cc] = fmaf(cf, z[s][cc], sum[cc]);
-            dp = fmaf(yv[cc], z[s][cc], dp);
-          }
-          VecIO<VEC>::store(out + (int64_t)b * d + (s * 32 + lane) * VEC, sum);
-        }
+    for (int col0 = 0; col0 < width; col0 += 32) {
+      const int col = col0 + lane;
+      float tot;
+      block_sum_partials(a.partial, s0, c1 - c0, width, col, red, tot);
+      if (warp == 0 && col < width) {
+        const int b = col / a.d, k = col % a.d;
+        const float z = self ? a.dZ[(int64_t)q * a.d + k] : 0.f;
+        a.dS[(int64_t)q * width + col] = tot + a.coeffs[(a.G - 1) * a.B + b] * z;
       }
-      dp = warp_sum(dp);
-      if (self && lane == 0) a.ed_self[(int64_t)q * B + b] = dp;
+    }
+    // self dots <Y_b[u], dZ[u]> (fixed order: lanes over k, then warp tree)
+    if (self) {
+      for (int b = 0; b < a.B; ++b) {
+        float dp = 0.f;
+        for (int k = threadIdx.x; k < a.d; k += CB_THREADS)
+          dp = fmaf(a.Y[((int64_t)q * a.B + b) * a.d + k], a.dZ[(int64_t)q * a.d + k], dp);
+        dp = warp_sum(dp);
+        if (lane == 0) dots[b][warp] = dp;
+      }
+      __syncthreads();
+      if (threadIdx.x < a.B) {
+        float s = 0.f;
+        for (int w = 0; w < CB_WARPS; ++w) s += dots[threadIdx.x][w];
+        a.ed_self[(int64_t)q * a.B + threadIdx.x] = s;
+      }
+      __syncthreads();
     }
   }
 }
@@ -593,25 +576,35 @@ __global__ void k_dbases_layout(const float* __restrict__ Rm, int B, int di, int
 
 static bool vec4_ok(int d) { return d % 4 == 0 && d <= 128; }
 
-template <int VEC, int S>
-static kg_status launch_agg(const AggArgs& a, int blocks, int cblocks, size_t smem, cudaStream_t st) {
-  KG_LAUNCH("k_aggregate", (k_aggregate<VEC, S>), blocks, 256, smem, st, a);
-  KG_LAUNCH("k_aggregate_combine", (k_aggregate_combine<VEC, S>), cblocks, 256, 0, st, a);
-  return KG_OK;
-}
-template <int VEC, int S>
-static kg_status launch_csc(const CscArgs& a, int blocks, int cblocks, size_t smem, cudaStream_t st) {
-  KG_LAUNCH("k_csc_backward", (k_csc_backward<VEC, S>), blocks, 256, smem, st, a);
-  KG_LAUNCH("k_csc_combine", (k_csc_combine<VEC, S>), cblocks, 256, 0, st, a);
-  return KG_OK;
-}
-
 // chunk capacities of kg_graph_csr (see the header)
 static int64_t cap_chunks(const kg_graph_csr* G) { return (int64_t)G->n + G->e / G->chunk + 1; }
 static int64_t cap_split_chunks(const kg_graph_csr* G) { return 2 * G->e / G->chunk + 1; }
 static int64_t cap_split_rows(const kg_graph_csr* G) { return G->e / G->chunk + 1; }
 
-template <typename Args, typename F4, typename F1a, typename F1b, typename F1c, typename F1d>
+template <int VEC, int S>
+static kg_status launch_agg(const AggArgs& a, int blocks, int cblocks, size_t smem, cudaStream_t st) {
+  switch (a.B) {
+    case 1: KG_LAUNCH("k_aggregate", (k_aggregate<1, VEC, S>), blocks, 256, smem, st, a); break;
+    case 2: KG_LAUNCH("k_aggregate", (k_aggregate<2, VEC, S>), blocks, 256, smem, st, a); break;
+    case 3: KG_LAUNCH("k_aggregate", (k_aggregate<3, VEC, S>), blocks, 256, smem, st, a); break;
+    default: KG_LAUNCH("k_aggregate", (k_aggregate<4, VEC, S>), blocks, 256, smem, st, a); break;
+  }
+  KG_LAUNCH("k_aggregate_combine", k_aggregate_combine, cblocks, CB_THREADS, 0, st, a);
+  return KG_OK;
+}
+template <int VEC, int S>
+static kg_status launch_csc(const CscArgs& a, int blocks, int cblocks, size_t smem, cudaStream_t st) {
+  switch (a.B) {
+    case 1: KG_LAUNCH("k_csc_backward", (k_csc_backward<1, VEC, S>), blocks, 256, smem, st, a); break;
+    case 2: KG_LAUNCH("k_csc_backward", (k_csc_backward<2, VEC, S>), blocks, 256, smem, st, a); break;
+    case 3: KG_LAUNCH("k_csc_backward", (k_csc_backward<3, VEC, S>), blocks, 256, smem, st, a); break;
+    default: KG_LAUNCH("k_csc_backward", (k_csc_backward<4, VEC, S>), blocks, 256, smem, st, a); break;
+  }
+  KG_LAUNCH("k_csc_combine", k_csc_combine, cblocks, CB_THREADS, 0, st, a);
+  return KG_OK;
+}
+
+template <typename F4, typename F1a, typename F1b, typename F1c, typename F1d>
 static kg_status dispatch_width(int d, F4 f4, F1a f1, F1b f2, F1c f4s, F1d f8) {
   if (vec4_ok(d)) return f4();
   if (d <= 32) return f1();
@@ -623,10 +616,11 @@ static kg_status dispatch_width(int d, F4 f4, F1a f1, F1b f2, F1c f4s, F1d f8) {
 }
 
 static kg_status run_aggregate(const AggArgs& a, const kg_graph_csr* G, cudaStream_t st) {
-  int blocks = persistent_blocks(cap_chunks(G) * 32, 256, 8);
-  int cblocks = persistent_blocks(cap_split_rows(G) * 32, 256, 8);
+  KG_REQUIRE(G->chunk <= MAXC, KG_ERR_VALIDATION, "chunk size %d > %d", G->chunk, MAXC);
+  int blocks = persistent_blocks(cap_chunks(G) * 32, 256, 3);
+  int cblocks = (int)(cap_split_rows(G) < num_sms() * 8 ? cap_split_rows(G) : num_sms() * 8);
   size_t smem = (size_t)a.G * a.B * sizeof(float);
-  return dispatch_width<AggArgs>(
+  return dispatch_width(
       a.d, [&] { return launch_agg<4, 1>(a, blocks, cblocks, smem, st); },
       [&] { return launch_agg<1, 1>(a, blocks, cblocks, smem, st); },
       [&] { return launch_agg<1, 2>(a, blocks, cblocks, smem, st); },
@@ -635,10 +629,11 @@ static kg_status run_aggregate(const AggArgs& a, const kg_graph_csr* G, cudaStre
 }
 
 static kg_status run_csc(const CscArgs& a, const kg_graph_csr* G, cudaStream_t st) {
-  int blocks = persistent_blocks(cap_chunks(G) * 32, 256, 8);
-  int cblocks = persistent_blocks(cap_split_rows(G) * 32, 256, 8);
+  KG_REQUIRE(G->chunk <= MAXC, KG_ERR_VALIDATION, "chunk size %d > %d", G->chunk, MAXC);
+  int blocks = persistent_blocks(cap_chunks(G) * 32, 256, 3);
+  int cblocks = (int)(cap_split_rows(G) < num_sms() * 8 ? cap_split_rows(G) : num_sms() * 8);
   size_t smem = (size_t)a.G * a.B * sizeof(float);
-  return dispatch_width<CscArgs>(
+  return dispatch_width(
       a.d, [&] { return launch_csc<4, 1>(a, blocks, cblocks, smem, st); },
       [&] { return launch_csc<1, 1>(a, blocks, cblocks, smem, st); },
       [&] { return launch_csc<1, 2>(a, blocks, cblocks, smem, st); },

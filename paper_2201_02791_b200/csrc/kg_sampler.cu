@@ -374,9 +374,10 @@ __global__ void k_closure_clear(int32_t* __restrict__ pos, uint32_t* __restrict_
   }
 }
 
-__global__ void k_mark_batch(const int32_t* __restrict__ tri, int64_t total, int64_t start, int64_t b,
-                             const int32_t* __restrict__ ids, int32_t n, uint32_t* __restrict__ flags,
-                             int32_t* __restrict__ bad) {
+__global__ void k_mark_batch(const int32_t* __restrict__ tri, int64_t total, int64_t start,
+                             const int64_t* __restrict__ start_dev, int64_t b, const int32_t* __restrict__ ids,
+                             int32_t n, uint32_t* __restrict__ flags, int32_t* __restrict__ bad) {
+  if (start_dev) start = *start_dev;
   for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < b; q += (int64_t)gridDim.x * blockDim.x) {
     if (tri) {
       int64_t row = (start + q) % total;
@@ -598,9 +599,9 @@ int64_t kg_closure_workspace_bytes(int32_t n) {
   return (int64_t)(align_up((int64_t)n * 4) + compact_workspace(n) + 4096);
 }
 
-kg_status kg_closure(const int32_t* tri, int64_t total, int64_t start, int64_t b, const int32_t* seed_ids,
-                     const kg_graph_csr* G, int32_t hops, int32_t* order, int32_t* pos, int32_t* counts,
-                     void* ws, int64_t ws_bytes, void* stream) {
+kg_status kg_closure(const int32_t* tri, int64_t total, int64_t start, const int64_t* start_dev, int64_t b,
+                     const int32_t* seed_ids, const kg_graph_csr* G, int32_t hops, int32_t* order, int32_t* pos,
+                     int32_t* counts, void* ws, int64_t ws_bytes, void* stream) {
   cudaStream_t st = as_stream(stream);
   const int32_t n = G->n;
   KG_REQUIRE(hops >= 0, KG_ERR_VALIDATION, "hops must be >= 0");
@@ -613,7 +614,8 @@ kg_status kg_closure(const int32_t* tri, int64_t total, int64_t start, int64_t b
   int gn = grid_for(n);
   KG_LAUNCH("k_closure_clear", k_closure_clear, gn, 256, 0, st, pos, flags, n);
   KG_CUDA(cudaMemsetAsync(bad, 0, 4, st));
-  KG_LAUNCH("k_mark_batch", k_mark_batch, grid_for(b), 256, 0, st, tri, total, start, b, seed_ids, n, flags, bad);
+  KG_LAUNCH("k_mark_batch", k_mark_batch, grid_for(b), 256, 0, st, tri, total, start, start_dev, b, seed_ids, n,
+            flags, bad);
   KG_CHECK_LAUNCH("closure mark");
   kg_status r = compact_flags(flags, n, order, counts, 0, nullptr, cws, compact_workspace(n), st);
   if (r != KG_OK) return r;

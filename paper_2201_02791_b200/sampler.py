@@ -508,8 +508,9 @@ class ComputeGraph:
 
 
 def closure_device(view: PartitionView, hops: int, *, stream: Optional[DeviceStream] = None, start: int = 0,
-                   size: int = 0, seed_ids=None, out=None, ws=None) -> ComputeGraph:
-    """Run kg_closure for a stream window or an explicit seed id tensor."""
+                   size: int = 0, seed_ids=None, out=None, ws=None, start_dev=None) -> ComputeGraph:
+    """Run kg_closure for a stream window (batch offset `start`, or the
+    device int64 `start_dev` for graph replay) or an explicit seed tensor."""
     torch = _torch()
     lib = _lib.require_cuda()
     dev = view.device
@@ -523,11 +524,11 @@ def closure_device(view: PartitionView, hops: int, *, stream: Optional[DeviceStr
     buf = ws.get("closure", nb)
     import ctypes
     if stream is not None:
-        _lib.call("kg_closure", stream.triples.data_ptr(), stream.total, start, size, 0,
+        _lib.call("kg_closure", stream.triples.data_ptr(), stream.total, start, _lib.ptr(start_dev), size, 0,
                   ctypes.byref(view.csr()), hops, order.data_ptr(), pos.data_ptr(), counts.data_ptr(),
                   buf.data_ptr(), buf.numel(), _lib.stream_handle())
     else:
-        _lib.call("kg_closure", 0, 0, 0, int(seed_ids.numel()), seed_ids.data_ptr(),
+        _lib.call("kg_closure", 0, 0, 0, 0, int(seed_ids.numel()), seed_ids.data_ptr(),
                   ctypes.byref(view.csr()), hops, order.data_ptr(), pos.data_ptr(), counts.data_ptr(),
                   buf.data_ptr(), buf.numel(), _lib.stream_handle())
     return ComputeGraph(view, hops, order, pos, counts)

@@ -19,6 +19,7 @@ partition-local and updated with lazy sparse Adam.
 from __future__ import annotations
 
 import math
+import os
 import time
 from dataclasses import dataclass, field
 from typing import Optional
@@ -91,7 +92,7 @@ def allreduce_mean(payloads: list) -> list:
     ws = torch.empty(lib.kg_optim_workspace_bytes(n), dtype=torch.uint8, device=dev)
     # p = 0 - 1 * mean  ->  -mean
     _lib.call("kg_dense_step", out.data_ptr(), 0, 0, g.data_ptr(), len(payloads), n, 0, 1.0, 0.9, 0.999,
-              1e-8, 1.0, 1.0, 0.0, flags.data_ptr(), ws.data_ptr(), ws.numel(), _lib.stream_handle())
+              1e-8, 1.0, 1.0, 0, 0.0, flags.data_ptr(), ws.data_ptr(), ws.numel(), _lib.stream_handle())
     res = (-out).double().cpu().numpy()
     outs, o = [], 0
     for s in shapes:
@@ -140,7 +141,7 @@ class Optimizer:
         bc1 = 1.0 - cfg.beta1 ** self.t
         bc2 = 1.0 - cfg.beta2 ** self.t
         _lib.call("kg_dense_step", p.data_ptr(), self.m.data_ptr(), self.v.data_ptr(), g.data_ptr(), 1, p.numel(),
-                  1 if self._adam else 0, cfg.learning_rate, cfg.beta1, cfg.beta2, cfg.adam_eps, bc1, bc2,
+                  1 if self._adam else 0, cfg.learning_rate, cfg.beta1, cfg.beta2, cfg.adam_eps, bc1, bc2, 0,
                   float(cfg.grad_clip) if cfg.grad_clip is not None else 0.0, flags.data_ptr(), ws.data_ptr(),
                   ws.numel(), _lib.stream_handle())
         flat = p.double().cpu().numpy()
@@ -157,7 +158,7 @@ class Optimizer:
             cnt = torch.tensor([len(embed_ids)], dtype=torch.int32, device=self.dev)
             _lib.call("kg_sparse_step", table.data_ptr(), self.em.data_ptr(), self.ev.data_ptr(), grad.data_ptr(),
                       rows.data_ptr(), cnt.data_ptr(), 0, table.shape[1], 1 if self._adam else 0,
-                      cfg.learning_rate, cfg.beta1, cfg.beta2, cfg.adam_eps, bc1, bc2, len(embed_ids),
+                      cfg.learning_rate, cfg.beta1, cfg.beta2, cfg.adam_eps, bc1, bc2, 0, len(embed_ids),
                       _lib.stream_handle())
             params.entity_embed[...] = table.double().cpu().numpy()
         if int(flags.item()):
@@ -265,10 +266,10 @@ class _Worker:
     def begin_epoch(self):
         self.stream = self.sampler.next()
 
-    def closure(self, rnd: int):
+    def closure(self, start_dev):
         from .sampler import closure_device
-        closure_device(self.view, self.config.num_layers, stream=self.stream, start=rnd * self.b, size=self.b,
-                       out=(self.bufs.order, self.bufs.pos, self.bufs.counts), ws=self.ws)
+        closure_device(self.view, self.config.num_layers, stream=self.stream, start=0, size=self.b,
+                       out=(self.bufs.order, self.bufs.pos, self.bufs.counts), ws=self.ws, start_dev=start_dev)
 
 
 class Trainer:
@@ -327,6 +328,17 @@ class Trainer:
         self.optim_ws = torch.empty(_lib.require_cuda().kg_optim_workspace_bytes(D), dtype=torch.uint8,
                                     device=self.dev)
         self.losses = torch.zeros((nloc, max(self.rounds, 1)), dtype=torch.float32, device=self.dev)
+        self.loss_scratch = torch.zeros(nloc, dtype=torch.float32, device=self.dev)
+        # per-round scalars live on the device so a captured round replays for every round
+        self.step_dev = torch.zeros(1, dtype=torch.int64, device=self.dev)        # Adam step t
+        self.start_dev = torch.zeros(nloc, dtype=torch.int64, device=self.dev)    # batch offsets r*b_w
+        self.round_dev = torch.zeros(1, dtype=torch.int64, device=self.dev)
+        self.scalars_host = torch.zeros(nloc + 1, dtype=torch.int64, pin_memory=True)
+        self.scalars_dev = torch.zeros(nloc + 1, dtype=torch.int64, device=self.dev)
+        self.use_graphs = os.environ.get("KG_CUDA_GRAPHS", "1") != "0"
+        self._graphs = {}
+        self._graph_pool = None
+        self._eager_rounds = 0
         self.t = 0
         self.round_in_epoch = 0
         self.epoch = 0
@@ -337,33 +349,72 @@ class Trainer:
             w.begin_epoch()
         self.round_in_epoch = 0
 
-    def run_round(self):
-        tc = self.tc
-        r = self.round_in_epoch
+    def _compute_body(self):
+        """closure -> forward -> DistMult+BCE -> backward of every local worker
+        (all per-round scalars read from device memory)."""
         for i, w in enumerate(self.workers):
-            w.closure(r)
+            w.closure(self.start_dev[i:i + 1])
             device_forward(self.model, w.bufs)
             gslot = self.grads_local[i]
-            device_loss(self.model, w.bufs, w.stream, r * w.b, w.b, gslot, self.losses[i, r:r + 1])
+            device_loss(self.model, w.bufs, w.stream, 0, w.b, gslot, self.loss_scratch[i:i + 1],
+                        start_dev=self.start_dev[i:i + 1])
+            self.losses[i].index_copy_(0, self.round_dev, self.loss_scratch[i:i + 1])
             device_backward(self.model, w.bufs, gslot, input_grad=w.emb)
-        if self.dist:
-            self._gather()
-        self.t += 1
-        bc1 = 1.0 - tc.beta1 ** self.t
-        bc2 = 1.0 - tc.beta2 ** self.t
+
+    def _update_body(self):
+        """Fused tree-mean + dense Adam/SGD, then lazy sparse rows."""
+        tc = self.tc
+        self.step_dev.add_(1)
         adam = 1 if tc.optimizer == "adam" else 0
         st = _lib.stream_handle()
         _lib.call("kg_dense_step", self.model.flat.data_ptr(), self.m.data_ptr(), self.v.data_ptr(),
                   self.grads_all.data_ptr(), self.P, self.D, adam, tc.learning_rate, tc.beta1, tc.beta2,
-                  tc.adam_eps, bc1, bc2, float(tc.grad_clip) if tc.grad_clip is not None else 0.0,
+                  tc.adam_eps, 1.0, 1.0, self.step_dev.data_ptr(),
+                  float(tc.grad_clip) if tc.grad_clip is not None else 0.0,
                   self.flags.data_ptr(), self.optim_ws.data_ptr(), self.optim_ws.numel(), st)
         L = self.mc.num_layers
         for w in self.workers:
             if w.emb:
                 _lib.call("kg_sparse_step", w.input_rows.data_ptr(), _lib.ptr(w.em), _lib.ptr(w.ev),
                           w.bufs.dH[0].data_ptr(), w.bufs.order.data_ptr(), w.bufs.counts.data_ptr(), L,
-                          self.mc.dims[0], adam, tc.learning_rate, tc.beta1, tc.beta2, tc.adam_eps, bc1, bc2,
-                          w.view.n, st)
+                          self.mc.dims[0], adam, tc.learning_rate, tc.beta1, tc.beta2, tc.adam_eps, 1.0, 1.0,
+                          self.step_dev.data_ptr(), w.view.n, st)
+
+    def run_round(self):
+        """One synchronized round. After two eager warm-up rounds the compute
+        and update halves are captured as CUDA graphs (one pair per epoch
+        buffer slot) and replayed; the NCCL gather runs between them."""
+        torch = _torch()
+        r = self.round_in_epoch
+        for i, w in enumerate(self.workers):
+            self.scalars_host[i] = r * w.b
+        self.scalars_host[len(self.workers)] = r
+        self.scalars_dev.copy_(self.scalars_host, non_blocking=True)
+        self.start_dev.copy_(self.scalars_dev[: len(self.workers)])
+        self.round_dev.copy_(self.scalars_dev[len(self.workers):])
+        key = tuple(w.stream.triples.data_ptr() for w in self.workers)
+        if not self.use_graphs or self._eager_rounds < 2:
+            self._compute_body()
+            if self.dist:
+                self._gather()
+            self._update_body()
+            self._eager_rounds += 1
+        else:
+            if key not in self._graphs:
+                if self._graph_pool is None:
+                    self._graph_pool = torch.cuda.graph_pool_handle()
+                gc, gu = torch.cuda.CUDAGraph(), torch.cuda.CUDAGraph()
+                with torch.cuda.graph(gc, pool=self._graph_pool):
+                    self._compute_body()
+                with torch.cuda.graph(gu, pool=self._graph_pool):
+                    self._update_body()
+                self._graphs[key] = (gc, gu)
+            gc, gu = self._graphs[key]
+            gc.replay()
+            if self.dist:
+                self._gather()
+            gu.replay()
+        self.t += 1
         self.round_in_epoch += 1
 
     def _gather(self):
