@@ -109,13 +109,19 @@ int kg_abi_version(void);
 int kg_last_error(char* buf, int64_t n); /* host buffer */
 /* Number of kernels this library has launched in the process. */
 int64_t kg_launch_count(void);
-/* Bracket every launch of kernels whose name starts with `prefix` (host
+/* Bracket every launch of the kernel named `prefix` ("" = all kernels; host
  * string) with CUDA events on the launching stream; _end synchronises and
  * returns the summed device time and the launch count. */
 kg_status kg_kernel_timer_begin(const char* prefix);
 kg_status kg_kernel_timer_end(double* total_ms, int64_t* launches);
 /* Ends the timer and writes "name,launches,total_ms" lines (host buffer). */
 kg_status kg_kernel_timer_dump(char* buf, int64_t n);
+/* While a stream is being captured into a CUDA graph the timer's event
+ * records become graph nodes: _detach ends the timer and keeps those events
+ * as a group (handle) that every replay re-records; _read sums the group's
+ * elapsed time after a replay (synchronises on its events). */
+kg_status kg_kernel_timer_detach(int64_t* handle);
+kg_status kg_kernel_timer_read(int64_t handle, double* total_ms, int64_t* launches);
 
 /* ---------------------------------------------------------------------- */
 /* Primitives (stable radix sort / scan) used by every stage below          */

@@ -51,6 +51,8 @@ _PROTOS = {
     "kg_kernel_timer_begin": (ST, [ctypes.c_char_p]),
     "kg_kernel_timer_end": (ST, [POINTER(c_double), POINTER(c_int64)]),
     "kg_kernel_timer_dump": (ST, [ctypes.c_char_p, c_int64]),
+    "kg_kernel_timer_detach": (ST, [POINTER(c_int64)]),
+    "kg_kernel_timer_read": (ST, [c_int64, POINTER(c_double), POINTER(c_int64)]),
     "kg_sort_workspace_bytes": (c_int64, [c_int64]),
     "kg_sort_pairs_u64": (ST, [P, P, c_int64, c_int, P, c_int64, P]),
     "kg_scan_workspace_bytes": (c_int64, [c_int64]),

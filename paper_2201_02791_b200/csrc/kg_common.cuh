@@ -34,6 +34,10 @@ kg_status from_cuda(cudaError_t e, const char* where);
 // Every kernel launch goes through KG_LAUNCH: it counts launches
 // (kg_launch_count) and, while kg_kernel_timer_begin(prefix) is active,
 // brackets matching kernels with CUDA events on their own stream.
+// Clears (and remembers) a runtime error left by an earlier call whose
+// status was not consumed, so it is not misattributed to the next launch.
+void check_stale(const char* before);
+
 struct LaunchScope {
   cudaStream_t st;
   int slot;
@@ -44,6 +48,7 @@ struct LaunchScope {
 #define KG_LAUNCH(name, kern, grid, block, smem, st_, ...)          \
   do {                                                              \
     auto _kp = kern;                                                \
+    ::kg::check_stale(name);                                        \
     ::kg::LaunchScope _ls(name, st_);                               \
     _kp<<<(grid), (block), (smem), (st_)>>>(__VA_ARGS__);           \
     _ls.done();                                                     \

@@ -23,8 +23,16 @@ void set_error(const char* fmt, ...) {
   va_end(ap);
 }
 
+static thread_local char g_stale[256] = "";
+
+void check_stale(const char* before) {
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess)
+    snprintf(g_stale, sizeof(g_stale), "stale %s cleared before %s", cudaGetErrorString(e), before);
+}
+
 kg_status from_cuda(cudaError_t e, const char* where) {
-  set_error("CUDA error %s at %s", cudaGetErrorString(e), where);
+  set_error("CUDA error %s at %s%s%s", cudaGetErrorString(e), where, g_stale[0] ? " | " : "", g_stale);
   return KG_ERR_CUDA;
 }
 
@@ -362,7 +370,7 @@ static size_t g_ev_used = 0;
 
 LaunchScope::LaunchScope(const char* name, cudaStream_t s) : st(s), slot(-1) {
   ++g_launches;
-  if (!g_timer_on || strncmp(name, g_timer_prefix, strlen(g_timer_prefix)) != 0) return;
+  if (!g_timer_on || (g_timer_prefix[0] && strcmp(name, g_timer_prefix) != 0)) return;   // exact kernel name, "" = all
   if (g_ev_used == g_ev_start.size()) {
     cudaEvent_t a, b;
     if (cudaEventCreate(&a) != cudaSuccess || cudaEventCreate(&b) != cudaSuccess) return;
@@ -372,11 +380,11 @@ LaunchScope::LaunchScope(const char* name, cudaStream_t s) : st(s), slot(-1) {
   }
   slot = (int)g_ev_used++;
   g_ev_name[slot] = name;
-  cudaEventRecord(g_ev_start[slot], st);
+  cudaEventRecordWithFlags(g_ev_start[slot], st, cudaEventRecordExternal);   // graph node when captured
 }
 
 void LaunchScope::done() {
-  if (slot >= 0) cudaEventRecord(g_ev_end[slot], st);
+  if (slot >= 0) cudaEventRecordWithFlags(g_ev_end[slot], st, cudaEventRecordExternal);
 }
 
 }  // namespace kg
@@ -416,6 +424,39 @@ kg_status kg_kernel_timer_dump(char* buf, int64_t n) {
                     a.second.second);
   }
   kg::g_ev_used = 0;
+  return KG_OK;
+}
+
+// Graph capture support: the event pairs recorded while a stream was being
+// captured became event-record nodes of that graph; detaching keeps them out
+// of the reuse pool so every replay re-records them.
+static std::vector<std::vector<std::pair<cudaEvent_t, cudaEvent_t>>> g_detached;
+
+kg_status kg_kernel_timer_detach(int64_t* handle) {
+  kg::g_timer_on = false;
+  std::vector<std::pair<cudaEvent_t, cudaEvent_t>> grp;
+  for (size_t i = 0; i < kg::g_ev_used; ++i) grp.push_back({kg::g_ev_start[i], kg::g_ev_end[i]});
+  // hand the events over: the pool forgets them
+  kg::g_ev_start.erase(kg::g_ev_start.begin(), kg::g_ev_start.begin() + kg::g_ev_used);
+  kg::g_ev_end.erase(kg::g_ev_end.begin(), kg::g_ev_end.begin() + kg::g_ev_used);
+  kg::g_ev_name.erase(kg::g_ev_name.begin(), kg::g_ev_name.begin() + kg::g_ev_used);
+  kg::g_ev_used = 0;
+  g_detached.push_back(grp);
+  *handle = (int64_t)g_detached.size() - 1;
+  return KG_OK;
+}
+
+kg_status kg_kernel_timer_read(int64_t handle, double* total_ms, int64_t* launches) {
+  KG_REQUIRE(handle >= 0 && handle < (int64_t)g_detached.size(), KG_ERR_VALIDATION, "bad timer handle");
+  double tot = 0.0;
+  for (auto& pr : g_detached[handle]) {
+    float ms = 0.f;
+    KG_CUDA(cudaEventSynchronize(pr.second));
+    KG_CUDA(cudaEventElapsedTime(&ms, pr.first, pr.second));
+    tot += ms;
+  }
+  *total_ms = tot;
+  *launches = (int64_t)g_detached[handle].size();
   return KG_OK;
 }
 

@@ -612,6 +612,11 @@ class EpochSampler:
             slot["ready"].record(self.side)
             slot["stream"] = DeviceStream(slot["out"]["tri"], slot["out"]["lab"], ds.total)
 
+    def slot_stream(self, slot: int) -> DeviceStream:
+        """The (fixed-address) stream buffers of a slot, for graph capture."""
+        o = self.slots[slot]["out"]
+        return DeviceStream(o["tri"], o["lab"], self.total)
+
     def next(self) -> DeviceStream:
         """Stream of the next epoch (main stream ordered after it); enqueues
         the epoch after that."""

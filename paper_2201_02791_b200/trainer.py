@@ -18,6 +18,7 @@ partition-local and updated with lazy sparse Adam.
 
 from __future__ import annotations
 
+import ctypes
 import math
 import os
 import time
@@ -332,10 +333,16 @@ class Trainer:
         # per-round scalars live on the device so a captured round replays for every round
         self.step_dev = torch.zeros(1, dtype=torch.int64, device=self.dev)        # Adam step t
         self.start_dev = torch.zeros(nloc, dtype=torch.int64, device=self.dev)    # batch offsets r*b_w
-        self.round_dev = torch.zeros(1, dtype=torch.int64, device=self.dev)
-        self.scalars_host = torch.zeros(nloc + 1, dtype=torch.int64, pin_memory=True)
-        self.scalars_dev = torch.zeros(nloc + 1, dtype=torch.int64, device=self.dev)
-        self.use_graphs = os.environ.get("KG_CUDA_GRAPHS", "1") != "0"
+        self.round_dev = torch.zeros(1, dtype=torch.int64, device=self.dev)       # r, advanced on device
+        self.b_dev = torch.tensor([w.b for w in self.workers], dtype=torch.int64, device=self.dev)
+        # CUDA graphs pay off over many rounds; short runs stay eager
+        env = os.environ.get("KG_CUDA_GRAPHS", "auto")
+        self.use_graphs = env == "1" or (env == "auto" and train_config.epochs * self.rounds >= 64)
+        self.graph_kernel_launches = 0
+        # optional: CUDA events around one kernel family, captured into the graphs
+        self.timer_prefix = None
+        self._timer_handles = {}
+        self.last_timer_handle = None
         self._graphs = {}
         self._graph_pool = None
         self._eager_rounds = 0
@@ -348,10 +355,13 @@ class Trainer:
         for w in self.workers:
             w.begin_epoch()
         self.round_in_epoch = 0
+        self.round_dev.zero_()
 
     def _compute_body(self):
         """closure -> forward -> DistMult+BCE -> backward of every local worker
         (all per-round scalars read from device memory)."""
+        torch = _torch()
+        torch.mul(self.b_dev, self.round_dev, out=self.start_dev)
         for i, w in enumerate(self.workers):
             w.closure(self.start_dev[i:i + 1])
             device_forward(self.model, w.bufs)
@@ -379,20 +389,13 @@ class Trainer:
                           w.bufs.dH[0].data_ptr(), w.bufs.order.data_ptr(), w.bufs.counts.data_ptr(), L,
                           self.mc.dims[0], adam, tc.learning_rate, tc.beta1, tc.beta2, tc.adam_eps, 1.0, 1.0,
                           self.step_dev.data_ptr(), w.view.n, st)
+        self.round_dev.add_(1)
 
     def run_round(self):
         """One synchronized round. After two eager warm-up rounds the compute
         and update halves are captured as CUDA graphs (one pair per epoch
         buffer slot) and replayed; the NCCL gather runs between them."""
         torch = _torch()
-        r = self.round_in_epoch
-        for i, w in enumerate(self.workers):
-            self.scalars_host[i] = r * w.b
-        self.scalars_host[len(self.workers)] = r
-        self.scalars_dev.copy_(self.scalars_host, non_blocking=True)
-        self.start_dev.copy_(self.scalars_dev[: len(self.workers)])
-        self.round_dev.copy_(self.scalars_dev[len(self.workers):])
-        key = tuple(w.stream.triples.data_ptr() for w in self.workers)
         if not self.use_graphs or self._eager_rounds < 2:
             self._compute_body()
             if self.dist:
@@ -400,22 +403,54 @@ class Trainer:
             self._update_body()
             self._eager_rounds += 1
         else:
-            if key not in self._graphs:
-                if self._graph_pool is None:
-                    self._graph_pool = torch.cuda.graph_pool_handle()
-                gc, gu = torch.cuda.CUDAGraph(), torch.cuda.CUDAGraph()
-                with torch.cuda.graph(gc, pool=self._graph_pool):
-                    self._compute_body()
-                with torch.cuda.graph(gu, pool=self._graph_pool):
-                    self._update_body()
-                self._graphs[key] = (gc, gu)
-            gc, gu = self._graphs[key]
+            if not self._graphs:
+                self._capture_all()
+            key = tuple(w.stream.triples.data_ptr() for w in self.workers)
+            gc, gu, nk = self._graphs[key]
+            self.last_timer_handle = self._timer_handles.get(key)
             gc.replay()
             if self.dist:
                 self._gather()
             gu.replay()
+            self.graph_kernel_launches += nk
         self.t += 1
         self.round_in_epoch += 1
+
+    def _capture(self, body, graph):
+        torch = _torch()
+        side = torch.cuda.Stream(self.dev)
+        side.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(side):
+            graph.capture_begin(pool=self._graph_pool)
+            body()
+            graph.capture_end()
+        torch.cuda.current_stream().wait_stream(side)
+
+    def _capture_all(self):
+        """Capture the compute and update halves of a round for both epoch
+        buffer slots of the samplers (pointers are fixed per slot)."""
+        torch = _torch()
+        lib = _lib.require_cuda()
+        if self._graph_pool is None:
+            self._graph_pool = torch.cuda.graph_pool_handle()
+        current = [w.stream for w in self.workers]
+        for slot in range(2):
+            for w in self.workers:
+                w.stream = w.sampler.slot_stream(slot)
+            key = tuple(w.stream.triples.data_ptr() for w in self.workers)
+            gc, gu = torch.cuda.CUDAGraph(), torch.cuda.CUDAGraph()
+            n0 = lib.kg_launch_count()
+            if self.timer_prefix:
+                lib.kg_kernel_timer_begin(self.timer_prefix.encode())
+            self._capture(self._compute_body, gc)
+            if self.timer_prefix:
+                h = ctypes.c_int64(-1)
+                lib.kg_kernel_timer_detach(ctypes.byref(h))
+                self._timer_handles[key] = h.value
+            self._capture(self._update_body, gu)
+            self._graphs[key] = (gc, gu, lib.kg_launch_count() - n0)
+        for w, st in zip(self.workers, current):
+            w.stream = st
 
     def _gather(self):
         gather_partition_payloads(self.grads_local, self.P, self.world, self.grads_all, self._recv, self._gidx)

@@ -253,3 +253,34 @@ def test_oracle_parity_on_fb_batch():
     for a, b in zip(gr.dense_blocks(), og.dense()):
         assert rel_l2(a, b) < 1e-4
     assert rel_l2(gr.embed_rows, og.embed_rows) < 1e-4
+
+
+def test_cuda_graph_replay_is_bitwise_identical_to_eager():
+    """Rounds replayed from captured CUDA graphs (both epoch slots, device
+    round scalars) produce exactly the eager parameters and losses."""
+    g = load_golden("synth_p4")
+    graph, pset, cfg = golden_pset(g)
+    L = len(cfg["dims"]) - 1
+    mc = kb.ModelConfig(L, cfg["dims"], cfg["num_bases"], graph.num_relations, 1, mode="embedding")
+    tc = kb.TrainConfig(epochs=1, batch_size=96, seed=2)
+    p0 = golden_params(g, "init_", L)
+    results = []
+    for graphs in (False, True):
+        tr = kb.Trainer(pset, graph, mc, tc, initial_params=p0)
+        tr.use_graphs = graphs
+        losses = []
+        for _ in range(3 * tr.rounds + 1):
+            if tr.round_in_epoch == 0 or tr.round_in_epoch >= tr.rounds:
+                if tr.round_in_epoch:
+                    losses.append(tr.epoch_losses())
+                tr.begin_epoch()
+            tr.run_round()
+        torch.cuda.synchronize()
+        if graphs:
+            assert tr.graph_kernel_launches > 0
+        results.append((tr.snapshot(), losses))
+    (a, la), (b, lb) = results
+    assert la == lb
+    for x, y in zip(a.dense_blocks(), b.dense_blocks()):
+        np.testing.assert_array_equal(x, y)
+    np.testing.assert_array_equal(a.entity_embed, b.entity_embed)
