@@ -368,6 +368,13 @@ static std::vector<cudaEvent_t> g_ev_start, g_ev_end;
 static std::vector<const char*> g_ev_name;
 static size_t g_ev_used = 0;
 
+// inside stream capture the records must become external event nodes of the graph
+static unsigned record_flags(cudaStream_t st) {
+  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+  cudaStreamIsCapturing(st, &cs);
+  return cs == cudaStreamCaptureStatusActive ? cudaEventRecordExternal : cudaEventRecordDefault;
+}
+
 LaunchScope::LaunchScope(const char* name, cudaStream_t s) : st(s), slot(-1) {
   ++g_launches;
   if (!g_timer_on || (g_timer_prefix[0] && strcmp(name, g_timer_prefix) != 0)) return;   // exact kernel name, "" = all
@@ -380,11 +387,11 @@ LaunchScope::LaunchScope(const char* name, cudaStream_t s) : st(s), slot(-1) {
   }
   slot = (int)g_ev_used++;
   g_ev_name[slot] = name;
-  cudaEventRecordWithFlags(g_ev_start[slot], st, cudaEventRecordExternal);   // graph node when captured
+  cudaEventRecordWithFlags(g_ev_start[slot], st, record_flags(st));
 }
 
 void LaunchScope::done() {
-  if (slot >= 0) cudaEventRecordWithFlags(g_ev_end[slot], st, cudaEventRecordExternal);
+  if (slot >= 0) cudaEventRecordWithFlags(g_ev_end[slot], st, record_flags(st));
 }
 
 }  // namespace kg

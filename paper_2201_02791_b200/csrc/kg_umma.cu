@@ -3,28 +3,35 @@
 //   NN  C[row(p), :] (+relu) = A[arow(p), 0:K] . B[0:K, 0:N]
 //   TN  P_z[0:Mf, 0:N]       = sum_{p in split z} A[arow(p), 0:Mf]^T . Bm[p, 0:N]
 //
-// tcgen05.mma kind::tf32 with 3xTF32 split (x = hi + lo, D += Ahi Bhi +
-// Ahi Blo + Alo Bhi, ~fp32 accuracy: plain TF32 would break the 1e-4
-// gradient tolerance). One CTA per SM (persistent), 128
-// threads; the accumulator (128 lanes x N_pad fp32 columns) lives in TMEM.
-// Operand chunks of 32 K-values are staged by all threads into shared memory
-// in the K-major no-swizzle canonical UMMA layout (core matrices of 8 rows x
-// 16 B), split into hi/lo on the way, double-buffered; one elected thread
-// issues the MMAs and commits them to per-stage mbarriers, so staging of
-// chunk k+1 overlaps the tensor-core work of chunk k. The epilogue reads
-// TMEM with tcgen05.ld (32x32b.x16) and applies ReLU / the row scatter.
+// tcgen05.mma kind::tf32 with a 3xTF32 split (x = hi + lo, D += Ahi Bhi +
+// Ahi Blo + Alo Bhi, ~fp32 accuracy; plain TF32 would break the 1e-4
+// gradient tolerance). One persistent CTA per SM, 256
+// threads; the fp32 accumulator (128 lanes x N_pad columns) lives in TMEM.
+//
+// Pipeline per K-chunk of 16 values:
+//   cp.async   raw fp32 rows (gathered by a_rows, zero-filled at the edges)
+//              into a 4-deep shared-memory ring, issued 3 chunks ahead
+//   convert    all threads split the arrived chunk into hi/lo tf32 operands
+//              in the K-major no-swizzle canonical UMMA layout (core matrices
+//              of 8 rows x 16 B), double-buffered
+//   mma        one elected thread issues 2 K-steps x 3 MMAs and commits them
+//              to the operand buffer's mbarrier (reuse guard)
+// so global-memory latency overlaps conversion and tensor-core work. The
+// epilogue reads TMEM with tcgen05.ld (32x32b.x16; warps w and w+4 share
+// lanes 32(w%4).. and split the columns) and applies ReLU / the row scatter.
 #include "kg_gemm.cuh"
 
 namespace kg {
 
 constexpr int UM = 128;        // MMA M (rows per tile)
-constexpr int UKC = 32;        // K values staged per chunk
+constexpr int UKC = 16;        // K values per chunk
 constexpr int UKG = UKC / 4;   // 16-byte k-groups per chunk
-constexpr int UTHREADS = 128;
+constexpr int UNS = 4;         // raw ring depth
+constexpr int UTHREADS = 256;
 
 __host__ __device__ inline int pad16(int n) { return (n + 15) / 16 * 16; }
 
-// byte offset of element (r, k) inside an R-row chunk tile (k < UKC)
+// byte offset of element (r, k) inside an R-row operand chunk (k < UKC)
 __device__ __forceinline__ uint32_t tile_off(int r, int k, int R) {
   return (uint32_t)(((k >> 2) * (R >> 3) + (r >> 3)) * 128 + (r & 7) * 16 + (k & 3) * 4);
 }
@@ -98,116 +105,82 @@ __device__ __forceinline__ void split_tf32(float x, float& hi, float& lo) {
   lo = x - hi;
 }
 
-// no "memory" clobber: ordering against the MMA is established by
-// fence.proxy.async + __syncthreads, and global loads must stay free to be
-// hoisted above earlier stores
 __device__ __forceinline__ void sts128(uint32_t addr, float a, float b, float c, float d) {
   asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "f"(a), "f"(b), "f"(c), "f"(d));
 }
 
-__device__ __forceinline__ void store_split(uint32_t hi_base, uint32_t lo_base, uint32_t off, const float* v) {
-  float h[4], l[4];
-#pragma unroll
-  for (int i = 0; i < 4; ++i) split_tf32(v[i], h[i], l[i]);
-  sts128(hi_base + off, h[0], h[1], h[2], h[3]);
-  sts128(lo_base + off, l[0], l[1], l[2], l[3]);
+// cp.async with zero fill: copies `bytes` (0 => all zeros) of a 16 B / 4 B slot
+__device__ __forceinline__ void cp16(uint32_t dst, const void* src, int bytes) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(dst), "l"(src), "r"(bytes) : "memory");
 }
-
-// Stage rows-by-K operand: element (r, k) = X[rowid(r0 + r)][kb + k], k contiguous.
-// Warp instruction covers 8 rows x 4 k-groups (16 B each); all of a thread's
-// loads are issued before any split/store (8 x 16 B in flight per thread).
-__device__ __forceinline__ void stage_rowsK(uint32_t hi_base, uint32_t lo_base, const float* __restrict__ X, int64_t ldx,
-                                            const int32_t* __restrict__ rowid, int64_t r0, int64_t rows, int64_t kb,
-                                            int64_t K, int R) {
-  const int tid = threadIdx.x;
-  const int lane = tid & 31, warp = tid >> 5;
-  const int rr = lane & 7, gg = lane >> 3;
-  const bool vec = ((ldx & 3) == 0) && ((kb & 3) == 0);
-  constexpr int IT = (UM / 8) * (UKG / 4) / (UTHREADS / 32);   // 8 items per thread for R = 128
-  float v[IT][4];
-#pragma unroll
-  for (int q = 0; q < IT; ++q) {
-    const int it = warp + q * (UTHREADS / 32);
-    const int rg = it % (R / 8);
-    const int g = (it / (R / 8)) * 4 + gg;
-    const int r = rg * 8 + rr;
-    v[q][0] = v[q][1] = v[q][2] = v[q][3] = 0.f;
-    const int64_t row = r0 + r;
-    if (row < rows) {
-      const int64_t grow = rowid ? (int64_t)__ldg(rowid + row) : row;
-      const float* p = X + grow * ldx + kb + g * 4;
-      const int64_t k0 = kb + g * 4;
-      if (vec && k0 + 4 <= K) {
-        float4 t = __ldg(reinterpret_cast<const float4*>(p));
-        v[q][0] = t.x; v[q][1] = t.y; v[q][2] = t.z; v[q][3] = t.w;
-      } else {
-#pragma unroll
-        for (int i = 0; i < 4; ++i)
-          if (k0 + i < K) v[q][i] = __ldg(p + i);
-      }
-    }
-  }
-#pragma unroll
-  for (int q = 0; q < IT; ++q) {
-    const int it = warp + q * (UTHREADS / 32);
-    const int rg = it % (R / 8);
-    const int g = (it / (R / 8)) * 4 + gg;
-    store_split(hi_base, lo_base, tile_off(rg * 8 + rr, g * 4, R), v[q]);
-  }
+__device__ __forceinline__ void cp4(uint32_t dst, const void* src, int bytes) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;" ::"r"(dst), "l"(src), "r"(bytes) : "memory");
 }
+__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
 
-// Stage cols-by-K operand: element (r, k) = X[rowid(kb + k)][r], r contiguous;
-// batches of 8 items (32 loads) in flight per thread.
-__device__ __forceinline__ void stage_colsK(uint32_t hi_base, uint32_t lo_base, const float* __restrict__ X, int64_t ldx,
-                                            const int32_t* __restrict__ rowid, int64_t kb, int64_t kend, int ncols, int R) {
-  constexpr int BATCH = 8;
-  const int total = R * UKG;
-  for (int base = threadIdx.x; base < total; base += BATCH * UTHREADS) {
-    float v[BATCH][4];
-#pragma unroll
-    for (int q = 0; q < BATCH; ++q) {
-      const int idx = base + q * UTHREADS;
-      const int r = idx % R, g = idx / R;
-#pragma unroll
-      for (int i = 0; i < 4; ++i) {
-        const int64_t kk = kb + g * 4 + i;
-        float x = 0.f;
-        if (idx < total && r < ncols && kk < kend) {
-          const int64_t grow = rowid ? (int64_t)__ldg(rowid + kk) : kk;
-          x = __ldg(X + grow * ldx + r);
-        }
-        v[q][i] = x;
+// Raw copy of a rows x cols fp32 block: row i = X + rowid(r0 + i) * ld + c0 (cols contiguous).
+// Rows >= nrows / cols >= ncols are zero-filled. dst row stride = dcols floats.
+__device__ __forceinline__ void copy_block(uint32_t dst, int dcols, const float* __restrict__ X, int64_t ld,
+                                           const int32_t* __restrict__ rowid, int64_t r0, int64_t nrows, int rows,
+                                           int64_t c0, int64_t ncols, int cols, bool vec) {
+  if (vec) {
+    const int per_row = cols / 4;
+    for (int idx = threadIdx.x; idx < rows * per_row; idx += UTHREADS) {
+      const int i = idx / per_row, q = idx % per_row;
+      const int64_t row = r0 + i, col = c0 + 4 * q;
+      int bytes = 0;
+      const float* src = X;
+      if (row < nrows && col < ncols) {
+        const int64_t g = rowid ? (int64_t)__ldg(rowid + row) : row;
+        src = X + g * ld + col;
+        bytes = (int)((ncols - col) >= 4 ? 16 : (ncols - col) * 4);
       }
+      cp16(dst + (uint32_t)((i * dcols + 4 * q) * 4), src, bytes);
     }
-#pragma unroll
-    for (int q = 0; q < BATCH; ++q) {
-      const int idx = base + q * UTHREADS;
-      if (idx < total) store_split(hi_base, lo_base, tile_off(idx % R, (idx / R) * 4, R), v[q]);
+  } else {
+    for (int idx = threadIdx.x; idx < rows * cols; idx += UTHREADS) {
+      const int i = idx / cols, q = idx % cols;
+      const int64_t row = r0 + i, col = c0 + q;
+      int bytes = 0;
+      const float* src = X;
+      if (row < nrows && col < ncols) {
+        const int64_t g = rowid ? (int64_t)__ldg(rowid + row) : row;
+        src = X + g * ld + col;
+        bytes = 4;
+      }
+      cp4(dst + (uint32_t)((i * dcols + q) * 4), src, bytes);
     }
   }
 }
 
 struct UmmaSmem {
-  // per stage: A hi, A lo (UM x UKC), B hi, B lo (NP x UKC)
-  __host__ __device__ static size_t a_bytes() { return (size_t)UM * UKC * 4; }
-  __host__ __device__ static size_t b_bytes(int np) { return (size_t)np * UKC * 4; }
-  __host__ __device__ static size_t stage_bytes(int np) { return 2 * a_bytes() + 2 * b_bytes(np); }
-  __host__ __device__ static size_t total(int np) { return 2 * stage_bytes(np) + 128; }
+  __host__ __device__ static size_t rawA() { return (size_t)UM * UKC * 4; }        // one raw A chunk
+  __host__ __device__ static size_t rawB(int np) { return (size_t)np * UKC * 4; }  // one raw B chunk
+  __host__ __device__ static size_t opA() { return (size_t)UM * UKC * 4; }
+  __host__ __device__ static size_t opB(int np) { return (size_t)np * UKC * 4; }
+  __host__ __device__ static size_t raw_stage(int np) { return rawA() + rawB(np); }
+  __host__ __device__ static size_t op_buf(int np) { return 2 * opA() + 2 * opB(np); }
+  __host__ __device__ static size_t total(int np) { return UNS * raw_stage(np) + 2 * op_buf(np) + 128; }
 };
 
 template <bool TN>
 __global__ void __launch_bounds__(UTHREADS, 1) k_umma_gemm(GemmArgs g, int np, uint32_t tmem_cols) {
   extern __shared__ __align__(1024) uint8_t smem[];
-  __shared__ uint64_t bar_stage[2];
+  __shared__ uint64_t bar_op[2];
   __shared__ uint64_t bar_done;
   __shared__ uint32_t tmem_base_s;
   const int tid = threadIdx.x, warp = tid >> 5;
   const uint32_t sbase = smem_u32(smem);
-  const size_t SB = UmmaSmem::stage_bytes(np);
-  auto a_hi = [&](int s) { return sbase + (uint32_t)(s * SB); };
-  auto a_lo = [&](int s) { return sbase + (uint32_t)(s * SB + UmmaSmem::a_bytes()); };
-  auto b_hi = [&](int s) { return sbase + (uint32_t)(s * SB + 2 * UmmaSmem::a_bytes()); };
-  auto b_lo = [&](int s) { return sbase + (uint32_t)(s * SB + 2 * UmmaSmem::a_bytes() + UmmaSmem::b_bytes(np)); };
+  auto raw_a = [&](int s) { return sbase + (uint32_t)(s * UmmaSmem::raw_stage(np)); };
+  auto raw_b = [&](int s) { return sbase + (uint32_t)(s * UmmaSmem::raw_stage(np) + UmmaSmem::rawA()); };
+  const uint32_t opbase = sbase + (uint32_t)(UNS * UmmaSmem::raw_stage(np));
+  auto a_hi = [&](int b) { return opbase + (uint32_t)(b * UmmaSmem::op_buf(np)); };
+  auto a_lo = [&](int b) { return a_hi(b) + (uint32_t)UmmaSmem::opA(); };
+  auto b_hi = [&](int b) { return a_hi(b) + (uint32_t)(2 * UmmaSmem::opA()); };
+  auto b_lo = [&](int b) { return b_hi(b) + (uint32_t)UmmaSmem::opB(np); };
+  const float* rawf = reinterpret_cast<const float*>(smem);
 
   if (warp == 0) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&tmem_base_s)),
@@ -215,8 +188,8 @@ __global__ void __launch_bounds__(UTHREADS, 1) k_umma_gemm(GemmArgs g, int np, u
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
   if (tid == 0) {
-    mbar_init(&bar_stage[0], 1);
-    mbar_init(&bar_stage[1], 1);
+    mbar_init(&bar_op[0], 1);
+    mbar_init(&bar_op[1], 1);
     mbar_init(&bar_done, 1);
     fence_async_smem();
   }
@@ -227,7 +200,6 @@ __global__ void __launch_bounds__(UTHREADS, 1) k_umma_gemm(GemmArgs g, int np, u
   const uint32_t idesc = make_idesc(np);
 
   const int64_t M = g.M_dev ? (int64_t)g.M_dev[g.M_dev_index] : g.M;
-  // NN: tiles over data rows, reduce over g.K. TN: one tile of features (blockIdx.y), reduce over this CTA's rows.
   int64_t ntiles, k_lo = 0, k_hi;
   if (!TN) {
     ntiles = (M + UM - 1) / UM;
@@ -239,50 +211,104 @@ __global__ void __launch_bounds__(UTHREADS, 1) k_umma_gemm(GemmArgs g, int np, u
     k_lo = (int64_t)blockIdx.x * per;
     k_hi = k_lo + per < M ? k_lo + per : M;
   }
-  uint32_t ph_stage[2] = {0, 0}, ph_done = 0;
-  int64_t gc = 0;   // global chunk counter (stage = gc & 1)
+  const int64_t mf0 = TN ? (int64_t)blockIdx.y * UM : 0;            // TN feature tile
+  const int64_t mf_n = TN ? (g.K - mf0 < UM ? g.K - mf0 : UM) : 0;
+  // 16-byte cp.async needs 16-byte aligned rows; otherwise 4-byte copies
+  const bool a16 = ((uintptr_t)g.A & 15) == 0, b16 = ((uintptr_t)g.B & 15) == 0;
+  const bool vecA = a16 && (g.lda & 3) == 0 && (!TN || (mf0 & 3) == 0);
+  const bool vecB = b16 && (g.ldb & 3) == 0;
+  uint32_t ph_op[2] = {0, 0}, ph_done = 0;
+  int64_t gop = 0;   // operand-buffer uses (buffer = gop & 1)
+
   for (int64_t tile = TN ? 0 : blockIdx.x; tile < ntiles; tile += TN ? 1 : gridDim.x) {
-    const int64_t m0 = TN ? (int64_t)blockIdx.y * UM : tile * UM;
-    int kc = 0;
-    for (int64_t kb = k_lo; kb < k_hi; kb += UKC, ++kc, ++gc) {
-      const int s = (int)(gc & 1);
-      if (gc >= 2) {
-        mbar_wait(&bar_stage[s], ph_stage[s]);
-        ph_stage[s] ^= 1;
+    const int64_t m0 = TN ? mf0 : tile * UM;
+    const int nk = (int)((k_hi - k_lo + UKC - 1) / UKC);
+    if (nk == 0) continue;
+    // issue raw chunk kc into ring slot kc % UNS (one commit group per chunk)
+    auto issue = [&](int kc) {
+      if (kc < nk) {
+        const int s = kc % UNS;
+        const int64_t kb = k_lo + (int64_t)kc * UKC;
+        if (!TN) {
+          // A rows m0.. (gathered), K columns kb..kb+UKC; raw[r][k]
+          copy_block(raw_a(s), UKC, g.A, g.lda, g.a_rows, m0, M, UM, kb, g.K, UKC, vecA && (kb & 3) == 0);
+          // B rows kb.. (K x N row-major); raw[k][n]
+          copy_block(raw_b(s), np, g.B, g.ldb, nullptr, kb, g.K, UKC, 0, g.N, np, vecB);
+        } else {
+          // A^T: data rows kb.. (gathered), feature columns mf0..; raw[k][m]
+          copy_block(raw_a(s), UM, g.A, g.lda, g.a_rows, kb, k_hi, UKC, mf0, g.K, UM, vecA);
+          copy_block(raw_b(s), np, g.B, g.ldb, nullptr, kb, k_hi, UKC, 0, g.N, np, vecB);
+        }
       }
-      if (!TN) {
-        stage_rowsK(a_hi(s), a_lo(s), g.A, g.lda, g.a_rows, m0, M, kb, g.K, UM);
-        stage_colsK(b_hi(s), b_lo(s), g.B, g.ldb, nullptr, kb, g.K, (int)g.N, np);
-      } else {
-        // A^T: element (feature m, data row k) = A[arow(k)][m0 + m]
-        stage_colsK(a_hi(s), a_lo(s), g.A + m0, g.lda, g.a_rows, kb, k_hi, (int)(g.K - m0 < UM ? g.K - m0 : UM), UM);
-        stage_colsK(b_hi(s), b_lo(s), g.B, g.ldb, nullptr, kb, k_hi, (int)g.N, np);
+      cp_commit();   // uniform group accounting (empty groups past the end)
+    };
+#pragma unroll
+    for (int j = 0; j < UNS - 1; ++j) issue(j);
+    for (int kc = 0; kc < nk; ++kc) {
+      issue(kc + UNS - 1);
+      cp_wait<UNS - 1>();   // this thread's copies of chunk kc have landed
+      const int ob = (int)(gop & 1);
+      if (gop >= 2) {
+        mbar_wait(&bar_op[ob], ph_op[ob]);   // MMAs that read this operand buffer are done
+        ph_op[ob] ^= 1;
+      }
+      __syncthreads();                       // every thread's copies of chunk kc are visible
+      const int s = kc % UNS;
+      const float* ra = rawf + (size_t)s * UmmaSmem::raw_stage(np) / 4;
+      const float* rb = ra + UmmaSmem::rawA() / 4;
+      // convert: A (UM x UKC) and B (np x UKC) into hi/lo operands
+      for (int idx = tid; idx < (UM + np) * UKG; idx += UTHREADS) {
+        float v[4];
+        uint32_t hib, lob, off;
+        if (idx < UM * UKG) {
+          const int r = idx % UM, gq = idx / UM;
+#pragma unroll
+          for (int i = 0; i < 4; ++i) v[i] = TN ? ra[(gq * 4 + i) * UM + r] : ra[r * UKC + gq * 4 + i];
+          hib = a_hi(ob);
+          lob = a_lo(ob);
+          off = tile_off(r, gq * 4, UM);
+        } else {
+          const int j = idx - UM * UKG;
+          const int n = j % np, gq = j / np;
+#pragma unroll
+          for (int i = 0; i < 4; ++i) v[i] = rb[(gq * 4 + i) * np + n];
+          hib = b_hi(ob);
+          lob = b_lo(ob);
+          off = tile_off(n, gq * 4, np);
+        }
+        float h[4], l[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) split_tf32(v[i], h[i], l[i]);
+        sts128(hib + off, h[0], h[1], h[2], h[3]);
+        sts128(lob + off, l[0], l[1], l[2], l[3]);
       }
       fence_async_smem();
       __syncthreads();
       if (tid == 0) {
         tc_fence_after();
+        const uint32_t lbo_a = (UM / 8) * 128, lbo_b = (uint32_t)(np / 8) * 128;
 #pragma unroll
         for (int j = 0; j < UKC / 8; ++j) {
-          const uint32_t lbo_a = (UM / 8) * 128, lbo_b = (uint32_t)(np / 8) * 128;
-          const uint32_t koff_a = (uint32_t)(2 * j) * lbo_a, koff_b = (uint32_t)(2 * j) * lbo_b;
-          uint64_t dah = make_desc(a_hi(s) + koff_a, lbo_a, 128), dal = make_desc(a_lo(s) + koff_a, lbo_a, 128);
-          uint64_t dbh = make_desc(b_hi(s) + koff_b, lbo_b, 128), dbl = make_desc(b_lo(s) + koff_b, lbo_b, 128);
+          const uint32_t ka = (uint32_t)(2 * j) * lbo_a, kbb = (uint32_t)(2 * j) * lbo_b;
+          uint64_t dah = make_desc(a_hi(ob) + ka, lbo_a, 128), dal = make_desc(a_lo(ob) + ka, lbo_a, 128);
+          uint64_t dbh = make_desc(b_hi(ob) + kbb, lbo_b, 128), dbl = make_desc(b_lo(ob) + kbb, lbo_b, 128);
           const uint32_t acc = (kc > 0 || j > 0) ? 1u : 0u;
           mma_tf32(tmem, dah, dbh, idesc, acc);
           mma_tf32(tmem, dah, dbl, idesc, 1u);
           mma_tf32(tmem, dal, dbh, idesc, 1u);
         }
-        mma_commit(&bar_stage[s]);
+        mma_commit(&bar_op[ob]);
       }
+      ++gop;
     }
-    if (kc == 0) continue;   // empty reduction range (TN split with no rows)
+    cp_wait<0>();
     if (tid == 0) mma_commit(&bar_done);
     mbar_wait(&bar_done, ph_done);
     ph_done ^= 1;
     tc_fence_after();
-    // epilogue: warp w owns TMEM lanes / tile rows [32w, 32w+32)
-    const int r = warp * 32 + (tid & 31);
+    // epilogue: warps w and w+4 read TMEM lanes [32(w%4), +32) and split the columns
+    const int lanegrp = warp & 3;
+    const int r = lanegrp * 32 + (tid & 31);
     const int64_t m = m0 + r;
     const int64_t out_rows = TN ? g.K : M;
     float* crow = nullptr;
@@ -290,9 +316,11 @@ __global__ void __launch_bounds__(UTHREADS, 1) k_umma_gemm(GemmArgs g, int np, u
       if (!TN) crow = g.C + (g.c_rows ? (int64_t)g.c_rows[m] : m) * g.ldc;
       else crow = g.C + ((int64_t)blockIdx.x * g.K + m) * g.ldc;
     }
-    for (int c0 = 0; c0 < np; c0 += 16) {
+    const int nchunks = np / 16;
+    for (int cidx = (warp >> 2); cidx < nchunks; cidx += 2) {
+      const int c0 = cidx * 16;
       float v[16];
-      tmem_ld16(tmem + ((uint32_t)(warp * 32) << 16) + (uint32_t)c0, v);
+      tmem_ld16(tmem + ((uint32_t)(lanegrp * 32) << 16) + (uint32_t)c0, v);
       if (crow) {
 #pragma unroll
         for (int i = 0; i < 16; ++i) {
@@ -304,10 +332,10 @@ __global__ void __launch_bounds__(UTHREADS, 1) k_umma_gemm(GemmArgs g, int np, u
     tc_fence_before();
     __syncthreads();
   }
-  // TN CTAs with an empty range still own a partial slot: zero it
+  // TN CTAs with an empty row range still own a partial slot: zero it
   if (TN && k_lo >= k_hi) {
     for (int idx = tid; idx < UM * g.N; idx += UTHREADS) {
-      int64_t m = (int64_t)blockIdx.y * UM + idx / g.N;
+      int64_t m = mf0 + idx / g.N;
       if (m < g.K) g.C[((int64_t)blockIdx.x * g.K + m) * g.ldc + idx % g.N] = 0.f;
     }
   }
@@ -326,10 +354,10 @@ static kg_status launch_umma(const GemmArgs& g, int np, dim3 grid, cudaStream_t 
   size_t smem = UmmaSmem::total(np);
   static bool attr_set[2] = {false, false};
   if (!attr_set[TN]) {
-    KG_CUDA(cudaFuncSetAttribute(k_umma_gemm<TN>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+    KG_CUDA(cudaFuncSetAttribute(k_umma_gemm<TN>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
     attr_set[TN] = true;
   }
-  KG_REQUIRE(smem <= 200 * 1024, KG_ERR_SHAPE, "umma tile too large (N_pad %d)", np);
+  KG_REQUIRE(smem <= 220 * 1024, KG_ERR_SHAPE, "umma tile too large (N_pad %d)", np);
   KG_LAUNCH(TN ? "k_umma_gemm_tn" : "k_umma_gemm_nn", k_umma_gemm<TN>, grid, UTHREADS, smem, st, g, np,
             tmem_cols_for(np));
   return KG_OK;
@@ -345,7 +373,7 @@ kg_status umma_gemm_nn(const GemmArgs& g, cudaStream_t st) {
 }
 
 int umma_tn_splits(int64_t rows_max) {
-  // >= 64 data rows (2 chunks) per split, at most one CTA per SM
+  // >= 64 data rows (4 chunks) per split, at most one CTA per SM
   int64_t s = ceil_div(rows_max, 64);
   if (s > num_sms()) s = num_sms();
   return (int)(s < 1 ? 1 : s);
