@@ -170,7 +170,10 @@ extern "C" {
 // C[c_rows(p)] = A[a_rows(p)] . B (M x K . K x N); trans = 1: TN
 // C[K x N] = sum_p A[a_rows(p), 0:K]^T Bm[p, 0:N] over M data rows.
 // impl 0 = tcgen05 3xTF32 (product path), 1 = CUDA-core fp32 reference.
-int64_t kg_gemm_workspace_bytes(int64_t M, int64_t K, int64_t N) { return (int64_t)gemm_tn_workspace(M, K, N) + 256; }
+int64_t kg_gemm_workspace_bytes(int64_t M, int64_t K, int64_t N) {
+  size_t a = gemm_tn_workspace(M, K, N), b = gemm_nn_workspace(M, K, N);
+  return (int64_t)(a > b ? a : b) + 256;
+}
 
 kg_status kg_gemm_f32(const float* A, int64_t lda, const int32_t* a_rows, const float* B, int64_t ldb, float* C,
                       int64_t ldc, const int32_t* c_rows, int64_t M, int64_t K, int64_t N, int32_t relu,
@@ -179,8 +182,8 @@ kg_status kg_gemm_f32(const float* A, int64_t lda, const int32_t* a_rows, const 
   g.A = A; g.lda = lda; g.a_rows = a_rows; g.B = B; g.ldb = ldb; g.C = C; g.ldc = ldc; g.c_rows = c_rows;
   g.M = M; g.M_max = M; g.K = K; g.N = N; g.relu = relu;
   cudaStream_t st = as_stream(stream);
-  if (!trans) return impl ? simt_gemm_nn(g, st) : umma_gemm_nn(g, st);
-  KG_REQUIRE((size_t)ws_bytes >= gemm_tn_workspace(M, K, N), KG_ERR_VALIDATION, "gemm workspace too small");
+  KG_REQUIRE(ws_bytes >= kg_gemm_workspace_bytes(M, K, N) - 256, KG_ERR_VALIDATION, "gemm workspace too small");
+  if (!trans) return impl ? simt_gemm_nn(g, st) : umma_gemm_nn(g, ws, st);
   return impl ? simt_gemm_tn(g, C, ws, st) : umma_gemm_tn(g, C, ws, st);
 }
 

@@ -652,7 +652,7 @@ struct LayerWs {
   float* ed;      // (e, B)
   float* ed_self; // (n, B)
   float* Rm;      // (d_in, B*d_out)
-  char* tn;       // split-K partials
+  char* gemm;     // packed GEMM operands / split-K partials (GEMMs run back to back)
 };
 
 static size_t layer_ws(int64_t n, int64_t e, int64_t split_chunks, int di, int dO, int B, LayerWs* w, void* base,
@@ -669,7 +669,11 @@ static size_t layer_ws(int64_t n, int64_t e, int64_t split_chunks, int di, int d
   l.ed = a.take<float>((size_t)e * B);
   l.ed_self = a.take<float>((size_t)n * B);
   l.Rm = a.take<float>((size_t)di * B * dO);
-  l.tn = a.take<char>(gemm_tn_workspace(n, di, (int64_t)B * dO));
+  size_t gw = gemm_tn_workspace(n, di, (int64_t)B * dO);
+  const size_t nn[3] = {gemm_nn_workspace(n, (int64_t)B * di, dO), gemm_nn_workspace(n, di, (int64_t)B * dO),
+                        gemm_nn_workspace(n, (int64_t)B * dO, di)};
+  for (size_t x : nn) gw = x > gw ? x : gw;
+  l.gemm = a.take<char>(gw);
   if (w) *w = l;
   return a.used + 256;
 }
@@ -718,7 +722,7 @@ kg_status kg_rgcn_forward(const kg_graph_csr* G, const kg_layer_params* lp, cons
   g.K = (int64_t)lp->B * lp->d_in;
   g.N = lp->d_out;
   g.relu = relu;
-  return gemm_nn(g, st);
+  return gemm_nn(g, w.gemm, st);
 }
 
 kg_status kg_rgcn_backward(const kg_graph_csr* G, const kg_layer_params* lp, const float* H_in, const float* H_out,
@@ -743,7 +747,7 @@ kg_status kg_rgcn_backward(const kg_graph_csr* G, const kg_layer_params* lp, con
   gy.C = w.Y; gy.ldc = (int64_t)B * dO;
   gy.M_dev = counts; gy.M_dev_index = t + 1; gy.M_max = G->n;
   gy.K = di; gy.N = (int64_t)B * dO;
-  kg_status s = gemm_nn(gy, st);
+  kg_status s = gemm_nn(gy, w.gemm, st);
   if (s != KG_OK) return s;
   CscArgs c{G->c_indptr, G->c_dst, G->c_rel, G->c_norm, csc_chunks(G), lp->coeffs, lp->G, B, dO, w.Y, w.dZ, pos,
             counts, t, w.dS, w.ed, w.ed_self, w.partial};
@@ -755,7 +759,7 @@ kg_status kg_rgcn_backward(const kg_graph_csr* G, const kg_layer_params* lp, con
   gv.B = w.dS; gv.ldb = (int64_t)B * dO;
   gv.M_dev = counts; gv.M_dev_index = t + 1; gv.M_max = G->n;
   gv.K = di; gv.N = (int64_t)B * dO;
-  s = gemm_tn(gv, w.Rm, w.tn, st);
+  s = gemm_tn(gv, w.Rm, w.gemm, st);
   if (s != KG_OK) return s;
   KG_LAUNCH("k_dbases_layout", k_dbases_layout, persistent_blocks(wn, 256, 2), 256, 0, st, w.Rm, B, di, dO, d_bases);
   if (dH_in) {
@@ -765,7 +769,7 @@ kg_status kg_rgcn_backward(const kg_graph_csr* G, const kg_layer_params* lp, con
     gx.C = dH_in; gx.ldc = di; gx.c_rows = order;
     gx.M_dev = counts; gx.M_dev_index = t + 1; gx.M_max = G->n;
     gx.K = (int64_t)B * dO; gx.N = di;
-    s = gemm_nn(gx, st);
+    s = gemm_nn(gx, w.gemm, st);
     if (s != KG_OK) return s;
   }
   KG_LAUNCH("k_dcoeff_reduce", k_dcoeff_reduce, lp->G, 256, 0, st, G->rel_ptr, G->rel_perm, G->c_dst, pos, counts, t,

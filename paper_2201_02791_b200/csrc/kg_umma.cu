@@ -5,36 +5,42 @@
 //
 // tcgen05.mma kind::tf32 with a 3xTF32 split (x = hi + lo, D += Ahi Bhi +
 // Ahi Blo + Alo Bhi, ~fp32 accuracy; plain TF32 would break the 1e-4
-// gradient tolerance). One persistent CTA per SM, 256
-// threads; the fp32 accumulator (128 lanes x N_pad columns) lives in TMEM.
+// gradient tolerance).
 //
-// Pipeline per K-chunk of 16 values:
-//   cp.async   raw fp32 rows (gathered by a_rows, zero-filled at the edges)
-//              into a 4-deep shared-memory ring, issued 3 chunks ahead
-//   convert    all threads split the arrived chunk into hi/lo tf32 operands
-//              in the K-major no-swizzle canonical UMMA layout (core matrices
-//              of 8 rows x 16 B), double-buffered
-//   mma        one elected thread issues 2 K-steps x 3 MMAs and commits them
-//              to the operand buffer's mbarrier (reuse guard)
-// so global-memory latency overlaps conversion and tensor-core work. The
-// epilogue reads TMEM with tcgen05.ld (32x32b.x16; warps w and w+4 share
-// lanes 32(w%4).. and split the columns) and applies ReLU / the row scatter.
+// Two kernels per GEMM:
+//   k_umma_pack    high-occupancy elementwise pass: gathers the operand rows,
+//                  splits fp32 into tf32 hi/lo and writes both in the K-major
+//                  no-swizzle canonical UMMA layout (core matrices of 8 rows x
+//                  16 B), one contiguous "record" per (row block, 16-wide K
+//                  chunk). Both operands of a GEMM are packed by one launch.
+//   k_umma_packed  warp-specialised tensor-core loop: warp 0 lane 0 streams
+//                  records into a shared-memory ring with cp.async.bulk
+//                  (mbarrier transaction counting), warp 1 lane 0 issues the
+//                  2 K-steps x 3 MMAs per record and commits them to the
+//                  slot's "empty" barrier, warps 2..5 drain the fp32
+//                  accumulator from TMEM (tcgen05.ld 32x32b) and apply ReLU /
+//                  the row scatter. Two TMEM accumulators let the epilogue of
+//                  tile i overlap the MMAs of tile i+1.
+// The earlier single-kernel variant converted in the GEMM itself and was
+// issue-latency bound at one CTA per SM (profiles/r1_v11_umma_stalls.txt).
 #include "kg_gemm.cuh"
 
 namespace kg {
 
 constexpr int UM = 128;        // MMA M (rows per tile)
-constexpr int UKC = 16;        // K values per chunk
-constexpr int UKG = UKC / 4;   // 16-byte k-groups per chunk
-constexpr int UNS = 4;         // raw ring depth
-constexpr int UTHREADS = 256;
+constexpr int UKC = 16;        // K values per record
+constexpr int UMAXS = 8;       // max ring stages
+constexpr int UTHREADS = 192;  // producer warp, MMA warp, 4 epilogue warps
+constexpr size_t USMEM_CAP = 200 * 1024;
 
 __host__ __device__ inline int pad16(int n) { return (n + 15) / 16 * 16; }
 
-// byte offset of element (r, k) inside an R-row operand chunk (k < UKC)
-__device__ __forceinline__ uint32_t tile_off(int r, int k, int R) {
+// byte offset of element (r, k) inside an R-row record half (k < UKC)
+__host__ __device__ __forceinline__ uint32_t tile_off(int r, int k, int R) {
   return (uint32_t)(((k >> 2) * (R >> 3) + (r >> 3)) * 128 + (r & 7) * 16 + (k & 3) * 4);
 }
+// floats per record (hi + lo halves)
+__host__ __device__ inline int64_t rec_floats(int R) { return (int64_t)2 * R * UKC; }
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
 
@@ -63,26 +69,40 @@ __device__ __forceinline__ void mma_tf32(uint32_t tmem_d, uint64_t da, uint64_t 
       "l"(da), "l"(db), "r"(idesc), "r"(acc));
 }
 
-__device__ __forceinline__ void mma_commit(uint64_t* bar) {
-  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
-               : "memory");
+__device__ __forceinline__ void mma_commit(uint32_t bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(bar) : "memory");
 }
 
-__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+__device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count) : "memory");
 }
 
-__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
   asm volatile(
       "{\n\t.reg .pred P1;\n"
       "WAIT_%=:\n\t"
       "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
-      "@!P1 bra WAIT_%=;\n\t}\n" ::"r"(smem_u32(bar)),
+      "@!P1 bra WAIT_%=;\n\t}\n" ::"r"(bar),
       "r"(parity)
       : "memory");
 }
 
-__device__ __forceinline__ void fence_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+__device__ __forceinline__ void mbar_arrive(uint32_t bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
+}
+
+__device__ __forceinline__ void mbar_expect_tx(uint32_t bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
+}
+
+// 1-D bulk copy global -> shared, completion counted on an mbarrier
+__device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t bytes, uint32_t bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
+               "l"(src), "r"(bytes), "r"(bar)
+               : "memory");
+}
+
+__device__ __forceinline__ void fence_barrier_init() { asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory"); }
 __device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
 __device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
 
@@ -105,295 +125,384 @@ __device__ __forceinline__ void split_tf32(float x, float& hi, float& lo) {
   lo = x - hi;
 }
 
-__device__ __forceinline__ void sts128(uint32_t addr, float a, float b, float c, float d) {
-  asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "f"(a), "f"(b), "f"(c), "f"(d));
+// ---------------------------------------------------------------------------
+// Operand packing.
+//   rows mode (cols_mode = 0): MMA row = source row (gathered by rowid, count
+//     nrows, possibly on the device), k = source column (static, ncols).
+//   cols mode (cols_mode = 1): MMA row = source column (static), k = source
+//     row (gathered, count possibly on the device).
+// Record (blk, kc) lives at out + (blk * nk_alloc + kc) * rec_floats(R);
+// entries past the valid rows / columns are written as zeros.
+struct PackJob {
+  const float* src;
+  int64_t ld;
+  const int32_t* rowid;
+  const int32_t* nrows_dev;
+  int nrows_idx;
+  int64_t nrows;      // if nrows_dev == nullptr
+  int64_t ncols;
+  int R;              // record rows (128 for A, N_pad for B)
+  int cols_mode;
+  int64_t nk_alloc;   // records per block in the layout
+  float* out;
+};
+
+__device__ __forceinline__ void pack_store(float* rec, int R, int r, int q, const float* v) {
+  float h[4], l[4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i) split_tf32(v[i], h[i], l[i]);
+  const uint32_t off = tile_off(r, 4 * q, R) >> 2;
+  *reinterpret_cast<float4*>(rec + off) = make_float4(h[0], h[1], h[2], h[3]);
+  *reinterpret_cast<float4*>(rec + (int64_t)R * UKC + off) = make_float4(l[0], l[1], l[2], l[3]);
 }
 
-// cp.async with zero fill: copies `bytes` (0 => all zeros) of a 16 B / 4 B slot
-__device__ __forceinline__ void cp16(uint32_t dst, const void* src, int bytes) {
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(dst), "l"(src), "r"(bytes) : "memory");
-}
-__device__ __forceinline__ void cp4(uint32_t dst, const void* src, int bytes) {
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;" ::"r"(dst), "l"(src), "r"(bytes) : "memory");
-}
-__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
-template <int N>
-__device__ __forceinline__ void cp_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
-
-// Raw copy of a rows x cols fp32 block: row i = X + rowid(r0 + i) * ld + c0 (cols contiguous).
-// Rows >= nrows / cols >= ncols are zero-filled. dst row stride = dcols floats.
-__device__ __forceinline__ void copy_block(uint32_t dst, int dcols, const float* __restrict__ X, int64_t ld,
-                                           const int32_t* __restrict__ rowid, int64_t r0, int64_t nrows, int rows,
-                                           int64_t c0, int64_t ncols, int cols, bool vec) {
-  if (vec) {
-    const int per_row = cols / 4;
-    for (int idx = threadIdx.x; idx < rows * per_row; idx += UTHREADS) {
-      const int i = idx / per_row, q = idx % per_row;
-      const int64_t row = r0 + i, col = c0 + 4 * q;
-      int bytes = 0;
-      const float* src = X;
-      if (row < nrows && col < ncols) {
-        const int64_t g = rowid ? (int64_t)__ldg(rowid + row) : row;
-        src = X + g * ld + col;
-        bytes = (int)((ncols - col) >= 4 ? 16 : (ncols - col) * 4);
+__global__ void __launch_bounds__(256) k_umma_pack(PackJob j0, PackJob j1) {
+  const PackJob& j = blockIdx.y == 0 ? j0 : j1;
+  if (!j.src) return;
+  const int64_t nrows = j.nrows_dev ? (int64_t)j.nrows_dev[j.nrows_idx] : j.nrows;
+  const int R = j.R;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  if (!j.cols_mode) {
+    // items (blk, kc, r, q), q fastest: 4 consecutive lanes read 64 B of one row
+    const int64_t nk = j.nk_alloc, nblk = (nrows + R - 1) / R;
+    const int64_t items = nblk * nk * R * 4;
+    const bool vec = ((uintptr_t)j.src & 15) == 0 && (j.ld & 3) == 0;
+    for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < items; idx += stride) {
+      const int q = (int)(idx & 3);
+      const int64_t t = idx >> 2;
+      const int r = (int)(t % R);
+      const int64_t u = t / R;
+      const int64_t kc = u % nk, blk = u / nk;
+      const int64_t row = blk * R + r, c0 = kc * UKC + 4 * q;
+      float v[4] = {0.f, 0.f, 0.f, 0.f};
+      if (row < nrows) {
+        const float* s = j.src + (j.rowid ? (int64_t)__ldg(j.rowid + row) : row) * j.ld;
+        if (vec && c0 + 3 < j.ncols) {
+          const float4 x = __ldg(reinterpret_cast<const float4*>(s + c0));
+          v[0] = x.x; v[1] = x.y; v[2] = x.z; v[3] = x.w;
+        } else {
+#pragma unroll
+          for (int i = 0; i < 4; ++i)
+            if (c0 + i < j.ncols) v[i] = __ldg(s + c0 + i);
+        }
       }
-      cp16(dst + (uint32_t)((i * dcols + 4 * q) * 4), src, bytes);
+      pack_store(j.out + (blk * nk + kc) * rec_floats(R), R, r, q, v);
     }
   } else {
-    for (int idx = threadIdx.x; idx < rows * cols; idx += UTHREADS) {
-      const int i = idx / cols, q = idx % cols;
-      const int64_t row = r0 + i, col = c0 + q;
-      int bytes = 0;
-      const float* src = X;
-      if (row < nrows && col < ncols) {
-        const int64_t g = rowid ? (int64_t)__ldg(rowid + row) : row;
-        src = X + g * ld + col;
-        bytes = 4;
+    // items (blk, kc, q, m), m fastest: a warp reads 32 consecutive columns
+    const int64_t nkd = (nrows + UKC - 1) / UKC, nblk = (j.ncols + R - 1) / R;
+    const int64_t items = nblk * nkd * 4 * R;
+    for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < items; idx += stride) {
+      const int m = (int)(idx % R);
+      const int64_t t = idx / R;
+      const int q = (int)(t & 3);
+      const int64_t u = t >> 2;
+      const int64_t kc = u % nkd, blk = u / nkd;
+      const int64_t col = blk * R + m, k0 = kc * UKC + 4 * q;
+      float v[4] = {0.f, 0.f, 0.f, 0.f};
+      if (col < j.ncols) {
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          const int64_t k = k0 + i;
+          if (k < nrows) v[i] = __ldg(j.src + (j.rowid ? (int64_t)__ldg(j.rowid + k) : k) * j.ld + col);
+        }
       }
-      cp4(dst + (uint32_t)((i * dcols + q) * 4), src, bytes);
+      pack_store(j.out + (blk * j.nk_alloc + kc) * rec_floats(R), R, m, q, v);
     }
   }
 }
 
-struct UmmaSmem {
-  __host__ __device__ static size_t rawA() { return (size_t)UM * UKC * 4; }        // one raw A chunk
-  __host__ __device__ static size_t rawB(int np) { return (size_t)np * UKC * 4; }  // one raw B chunk
-  __host__ __device__ static size_t opA() { return (size_t)UM * UKC * 4; }
-  __host__ __device__ static size_t opB(int np) { return (size_t)np * UKC * 4; }
-  __host__ __device__ static size_t raw_stage(int np) { return rawA() + rawB(np); }
-  __host__ __device__ static size_t op_buf(int np) { return 2 * opA() + 2 * opB(np); }
-  __host__ __device__ static size_t total(int np) { return UNS * raw_stage(np) + 2 * op_buf(np) + 128; }
+// ---------------------------------------------------------------------------
+struct PackedArgs {
+  const float* Ap;        // A records, R = UM
+  const float* Bp;        // B records, R = np (single block)
+  int64_t a_nk_alloc;     // records per A block
+  int np;
+  // NN: tiles = ceil(M / UM), every tile uses records kc in [0, nk)
+  // TN: CTA (x, y) uses A block y and records [x*per, ...) of nk_dyn
+  int tn;
+  int64_t M;              // NN rows / TN data rows (if M_dev == nullptr)
+  const int32_t* M_dev;
+  int M_dev_index;
+  int64_t nk;             // NN: static record count
+  float* C;
+  int64_t ldc;
+  const int32_t* c_rows;
+  int64_t N;
+  int64_t out_rows;       // TN: feature rows (g.K)
+  int relu;
 };
 
-template <bool TN>
-__global__ void __launch_bounds__(UTHREADS, 1) k_umma_gemm(GemmArgs g, int np, uint32_t tmem_cols) {
+__device__ __forceinline__ uint32_t stage_bytes(int np) { return (uint32_t)((UM + np) * UKC * 2 * 4); }
+
+__global__ void __launch_bounds__(UTHREADS, 1) k_umma_packed(PackedArgs g, int nstages, uint32_t acc_cols) {
   extern __shared__ __align__(1024) uint8_t smem[];
-  __shared__ uint64_t bar_op[2];
-  __shared__ uint64_t bar_done;
+  __shared__ __align__(8) uint64_t bar_full[UMAXS], bar_empty[UMAXS], bar_tfull[2], bar_tempty[2];
   __shared__ uint32_t tmem_base_s;
-  const int tid = threadIdx.x, warp = tid >> 5;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int np = g.np;
+
+  // work assignment
+  const int64_t M = g.M_dev ? (int64_t)g.M_dev[g.M_dev_index] : g.M;
+  int64_t ntiles, c_lo = 0, c_hi;
+  if (!g.tn) {
+    ntiles = (M + UM - 1) / UM;
+    c_hi = g.nk;
+  } else {
+    ntiles = 1;
+    const int64_t nkd = (M + UKC - 1) / UKC;
+    const int64_t per = (nkd + gridDim.x - 1) / gridDim.x;
+    c_lo = (int64_t)blockIdx.x * per;
+    c_hi = c_lo + per < nkd ? c_lo + per : nkd;
+    if (c_lo >= c_hi) {   // empty split: its partial slot is zero
+      const int64_t mf0 = (int64_t)blockIdx.y * UM;
+      for (int idx = tid; idx < UM * g.N; idx += UTHREADS) {
+        const int64_t m = mf0 + idx / g.N;
+        if (m < g.out_rows) g.C[((int64_t)blockIdx.x * g.out_rows + m) * g.ldc + idx % g.N] = 0.f;
+      }
+      return;
+    }
+  }
+  const int64_t tile0 = g.tn ? 0 : blockIdx.x, tstep = g.tn ? 1 : gridDim.x;
+  const int nk = (int)(c_hi - c_lo);
+  if (tile0 >= ntiles) return;
+
   const uint32_t sbase = smem_u32(smem);
-  auto raw_a = [&](int s) { return sbase + (uint32_t)(s * UmmaSmem::raw_stage(np)); };
-  auto raw_b = [&](int s) { return sbase + (uint32_t)(s * UmmaSmem::raw_stage(np) + UmmaSmem::rawA()); };
-  const uint32_t opbase = sbase + (uint32_t)(UNS * UmmaSmem::raw_stage(np));
-  auto a_hi = [&](int b) { return opbase + (uint32_t)(b * UmmaSmem::op_buf(np)); };
-  auto a_lo = [&](int b) { return a_hi(b) + (uint32_t)UmmaSmem::opA(); };
-  auto b_hi = [&](int b) { return a_hi(b) + (uint32_t)(2 * UmmaSmem::opA()); };
-  auto b_lo = [&](int b) { return b_hi(b) + (uint32_t)UmmaSmem::opB(np); };
-  const float* rawf = reinterpret_cast<const float*>(smem);
+  const uint32_t sb = stage_bytes(np), a_bytes = (uint32_t)(UM * UKC * 8), b_half = (uint32_t)(np * UKC * 4);
+  auto full = [&](int s) { return smem_u32(&bar_full[s]); };
+  auto empty = [&](int s) { return smem_u32(&bar_empty[s]); };
 
   if (warp == 0) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&tmem_base_s)),
-                 "r"(tmem_cols));
+                 "r"(2 * acc_cols));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
-  if (tid == 0) {
-    mbar_init(&bar_op[0], 1);
-    mbar_init(&bar_op[1], 1);
-    mbar_init(&bar_done, 1);
-    fence_async_smem();
+  if (tid == 32) {
+    for (int s = 0; s < nstages; ++s) {
+      mbar_init(full(s), 1);
+      mbar_init(empty(s), 1);
+    }
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(smem_u32(&bar_tfull[a]), 1);
+      mbar_init(smem_u32(&bar_tempty[a]), 4);
+    }
+    fence_barrier_init();
   }
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = tmem_base_s;
-  const uint32_t idesc = make_idesc(np);
 
-  const int64_t M = g.M_dev ? (int64_t)g.M_dev[g.M_dev_index] : g.M;
-  int64_t ntiles, k_lo = 0, k_hi;
-  if (!TN) {
-    ntiles = (M + UM - 1) / UM;
-    k_hi = g.K;
-  } else {
-    ntiles = 1;
-    int64_t per = (M + gridDim.x - 1) / gridDim.x;
-    per = (per + UKC - 1) / UKC * UKC;
-    k_lo = (int64_t)blockIdx.x * per;
-    k_hi = k_lo + per < M ? k_lo + per : M;
-  }
-  const int64_t mf0 = TN ? (int64_t)blockIdx.y * UM : 0;            // TN feature tile
-  const int64_t mf_n = TN ? (g.K - mf0 < UM ? g.K - mf0 : UM) : 0;
-  // 16-byte cp.async needs 16-byte aligned rows; otherwise 4-byte copies
-  const bool a16 = ((uintptr_t)g.A & 15) == 0, b16 = ((uintptr_t)g.B & 15) == 0;
-  const bool vecA = a16 && (g.lda & 3) == 0 && (!TN || (mf0 & 3) == 0);
-  const bool vecB = b16 && (g.ldb & 3) == 0;
-  uint32_t ph_op[2] = {0, 0}, ph_done = 0;
-  int64_t gop = 0;   // operand-buffer uses (buffer = gop & 1)
-
-  for (int64_t tile = TN ? 0 : blockIdx.x; tile < ntiles; tile += TN ? 1 : gridDim.x) {
-    const int64_t m0 = TN ? mf0 : tile * UM;
-    const int nk = (int)((k_hi - k_lo + UKC - 1) / UKC);
-    if (nk == 0) continue;
-    // issue raw chunk kc into ring slot kc % UNS (one commit group per chunk)
-    auto issue = [&](int kc) {
-      if (kc < nk) {
-        const int s = kc % UNS;
-        const int64_t kb = k_lo + (int64_t)kc * UKC;
-        if (!TN) {
-          // A rows m0.. (gathered), K columns kb..kb+UKC; raw[r][k]
-          copy_block(raw_a(s), UKC, g.A, g.lda, g.a_rows, m0, M, UM, kb, g.K, UKC, vecA && (kb & 3) == 0);
-          // B rows kb.. (K x N row-major); raw[k][n]
-          copy_block(raw_b(s), np, g.B, g.ldb, nullptr, kb, g.K, UKC, 0, g.N, np, vecB);
-        } else {
-          // A^T: data rows kb.. (gathered), feature columns mf0..; raw[k][m]
-          copy_block(raw_a(s), UM, g.A, g.lda, g.a_rows, kb, k_hi, UKC, mf0, g.K, UM, vecA);
-          copy_block(raw_b(s), np, g.B, g.ldb, nullptr, kb, k_hi, UKC, 0, g.N, np, vecB);
+  if (warp == 0) {
+    if (lane == 0) {
+      // producer: stream (A record, B record) pairs through the ring
+      int64_t it = 0;
+      for (int64_t tile = tile0; tile < ntiles; tile += tstep) {
+        const int64_t ablk = g.tn ? blockIdx.y : tile;
+        const float* arec = g.Ap + (ablk * g.a_nk_alloc + c_lo) * rec_floats(UM);
+        const float* brec = g.Bp + c_lo * rec_floats(np);
+        for (int kc = 0; kc < nk; ++kc, ++it) {
+          const int s = (int)(it % nstages);
+          if (it >= nstages) mbar_wait(empty(s), (uint32_t)((it / nstages - 1) & 1));
+          const uint32_t dst = sbase + (uint32_t)s * sb;
+          mbar_expect_tx(full(s), sb);
+          bulk_g2s(dst, arec + (int64_t)kc * rec_floats(UM), a_bytes, full(s));
+          bulk_g2s(dst + a_bytes, brec + (int64_t)kc * rec_floats(np), 2 * b_half, full(s));
         }
       }
-      cp_commit();   // uniform group accounting (empty groups past the end)
-    };
-#pragma unroll
-    for (int j = 0; j < UNS - 1; ++j) issue(j);
-    for (int kc = 0; kc < nk; ++kc) {
-      issue(kc + UNS - 1);
-      cp_wait<UNS - 1>();   // this thread's copies of chunk kc have landed
-      const int ob = (int)(gop & 1);
-      if (gop >= 2) {
-        mbar_wait(&bar_op[ob], ph_op[ob]);   // MMAs that read this operand buffer are done
-        ph_op[ob] ^= 1;
-      }
-      __syncthreads();                       // every thread's copies of chunk kc are visible
-      const int s = kc % UNS;
-      const float* ra = rawf + (size_t)s * UmmaSmem::raw_stage(np) / 4;
-      const float* rb = ra + UmmaSmem::rawA() / 4;
-      // convert: A (UM x UKC) and B (np x UKC) into hi/lo operands
-      for (int idx = tid; idx < (UM + np) * UKG; idx += UTHREADS) {
-        float v[4];
-        uint32_t hib, lob, off;
-        if (idx < UM * UKG) {
-          const int r = idx % UM, gq = idx / UM;
-#pragma unroll
-          for (int i = 0; i < 4; ++i) v[i] = TN ? ra[(gq * 4 + i) * UM + r] : ra[r * UKC + gq * 4 + i];
-          hib = a_hi(ob);
-          lob = a_lo(ob);
-          off = tile_off(r, gq * 4, UM);
-        } else {
-          const int j = idx - UM * UKG;
-          const int n = j % np, gq = j / np;
-#pragma unroll
-          for (int i = 0; i < 4; ++i) v[i] = rb[(gq * 4 + i) * np + n];
-          hib = b_hi(ob);
-          lob = b_lo(ob);
-          off = tile_off(n, gq * 4, np);
-        }
-        float h[4], l[4];
-#pragma unroll
-        for (int i = 0; i < 4; ++i) split_tf32(v[i], h[i], l[i]);
-        sts128(hib + off, h[0], h[1], h[2], h[3]);
-        sts128(lob + off, l[0], l[1], l[2], l[3]);
-      }
-      fence_async_smem();
-      __syncthreads();
-      if (tid == 0) {
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      // MMA issuer
+      const uint32_t idesc = make_idesc(np);
+      const uint32_t lbo_a = (UM / 8) * 128, lbo_b = (uint32_t)(np / 8) * 128;
+      int64_t it = 0, tcount = 0;
+      for (int64_t tile = tile0; tile < ntiles; tile += tstep, ++tcount) {
+        const int acc = (int)(tcount & 1);
+        if (tcount >= 2) mbar_wait(smem_u32(&bar_tempty[acc]), (uint32_t)((tcount / 2 - 1) & 1));
         tc_fence_after();
-        const uint32_t lbo_a = (UM / 8) * 128, lbo_b = (uint32_t)(np / 8) * 128;
+        const uint32_t d = tmem + (uint32_t)acc * acc_cols;
+        for (int kc = 0; kc < nk; ++kc, ++it) {
+          const int s = (int)(it % nstages);
+          mbar_wait(full(s), (uint32_t)((it / nstages) & 1));
+          tc_fence_after();
+          const uint32_t a_hi = sbase + (uint32_t)s * sb, a_lo = a_hi + (uint32_t)(UM * UKC * 4);
+          const uint32_t b_hi = a_hi + a_bytes, b_lo = b_hi + b_half;
 #pragma unroll
-        for (int j = 0; j < UKC / 8; ++j) {
-          const uint32_t ka = (uint32_t)(2 * j) * lbo_a, kbb = (uint32_t)(2 * j) * lbo_b;
-          uint64_t dah = make_desc(a_hi(ob) + ka, lbo_a, 128), dal = make_desc(a_lo(ob) + ka, lbo_a, 128);
-          uint64_t dbh = make_desc(b_hi(ob) + kbb, lbo_b, 128), dbl = make_desc(b_lo(ob) + kbb, lbo_b, 128);
-          const uint32_t acc = (kc > 0 || j > 0) ? 1u : 0u;
-          mma_tf32(tmem, dah, dbh, idesc, acc);
-          mma_tf32(tmem, dah, dbl, idesc, 1u);
-          mma_tf32(tmem, dal, dbh, idesc, 1u);
+          for (int j = 0; j < UKC / 8; ++j) {
+            const uint32_t ka = (uint32_t)(2 * j) * lbo_a, kb = (uint32_t)(2 * j) * lbo_b;
+            const uint64_t dah = make_desc(a_hi + ka, lbo_a, 128), dal = make_desc(a_lo + ka, lbo_a, 128);
+            const uint64_t dbh = make_desc(b_hi + kb, lbo_b, 128), dbl = make_desc(b_lo + kb, lbo_b, 128);
+            mma_tf32(d, dah, dbh, idesc, (kc > 0 || j > 0) ? 1u : 0u);
+            mma_tf32(d, dah, dbl, idesc, 1u);
+            mma_tf32(d, dal, dbh, idesc, 1u);
+          }
+          mma_commit(empty(s));   // slot reusable once these MMAs have read it
         }
-        mma_commit(&bar_op[ob]);
+        mma_commit(smem_u32(&bar_tfull[acc]));
       }
-      ++gop;
     }
-    cp_wait<0>();
-    if (tid == 0) mma_commit(&bar_done);
-    mbar_wait(&bar_done, ph_done);
-    ph_done ^= 1;
-    tc_fence_after();
-    // epilogue: warps w and w+4 read TMEM lanes [32(w%4), +32) and split the columns
+  } else {
+    // epilogue warps 2..5: TMEM lanes 32 * (warp % 4) ..
     const int lanegrp = warp & 3;
-    const int r = lanegrp * 32 + (tid & 31);
-    const int64_t m = m0 + r;
-    const int64_t out_rows = TN ? g.K : M;
-    float* crow = nullptr;
-    if (m < out_rows) {
-      if (!TN) crow = g.C + (g.c_rows ? (int64_t)g.c_rows[m] : m) * g.ldc;
-      else crow = g.C + ((int64_t)blockIdx.x * g.K + m) * g.ldc;
-    }
-    const int nchunks = np / 16;
-    for (int cidx = (warp >> 2); cidx < nchunks; cidx += 2) {
-      const int c0 = cidx * 16;
-      float v[16];
-      tmem_ld16(tmem + ((uint32_t)(lanegrp * 32) << 16) + (uint32_t)c0, v);
-      if (crow) {
+    const int r = lanegrp * 32 + lane;
+    const bool vec = ((uintptr_t)g.C & 15) == 0 && (g.ldc & 3) == 0;
+    int64_t tcount = 0;
+    for (int64_t tile = tile0; tile < ntiles; tile += tstep, ++tcount) {
+      const int acc = (int)(tcount & 1);
+      mbar_wait(smem_u32(&bar_tfull[acc]), (uint32_t)((tcount / 2) & 1));
+      tc_fence_after();
+      float* crow = nullptr;
+      if (!g.tn) {
+        const int64_t m = tile * UM + r;
+        if (m < M) crow = g.C + (g.c_rows ? (int64_t)__ldg(g.c_rows + m) : m) * g.ldc;
+      } else {
+        const int64_t m = (int64_t)blockIdx.y * UM + r;
+        if (m < g.out_rows) crow = g.C + ((int64_t)blockIdx.x * g.out_rows + m) * g.ldc;
+      }
+      const uint32_t taddr = tmem + (uint32_t)acc * acc_cols + ((uint32_t)(lanegrp * 32) << 16);
+      for (int c0 = 0; c0 < np; c0 += 16) {
+        float v[16];
+        tmem_ld16(taddr + (uint32_t)c0, v);
+        if (crow) {
+          if (g.relu) {
 #pragma unroll
-        for (int i = 0; i < 16; ++i) {
-          const int64_t n = c0 + i;
-          if (n < g.N) crow[n] = g.relu ? fmaxf(v[i], 0.f) : v[i];
+            for (int i = 0; i < 16; ++i) v[i] = fmaxf(v[i], 0.f);
+          }
+          if (vec && c0 + 16 <= g.N) {
+#pragma unroll
+            for (int i = 0; i < 16; i += 4)
+              *reinterpret_cast<float4*>(crow + c0 + i) = make_float4(v[i], v[i + 1], v[i + 2], v[i + 3]);
+          } else {
+#pragma unroll
+            for (int i = 0; i < 16; ++i)
+              if (c0 + i < g.N) crow[c0 + i] = v[i];
+          }
         }
       }
-    }
-    tc_fence_before();
-    __syncthreads();
-  }
-  // TN CTAs with an empty row range still own a partial slot: zero it
-  if (TN && k_lo >= k_hi) {
-    for (int idx = tid; idx < UM * g.N; idx += UTHREADS) {
-      int64_t m = mf0 + idx / g.N;
-      if (m < g.K) g.C[((int64_t)blockIdx.x * g.K + m) * g.ldc + idx % g.N] = 0.f;
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(smem_u32(&bar_tempty[acc]));
     }
   }
+  tc_fence_before();
   __syncthreads();
-  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(tmem_cols));
+  tc_fence_after();
+  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(2 * acc_cols));
 }
 
-static uint32_t tmem_cols_for(int np) {
+static uint32_t acc_cols_for(int np) {
   uint32_t c = 32;
   while ((int)c < np) c <<= 1;
   return c;
 }
 
-template <bool TN>
-static kg_status launch_umma(const GemmArgs& g, int np, dim3 grid, cudaStream_t st) {
-  size_t smem = UmmaSmem::total(np);
-  static bool attr_set[2] = {false, false};
-  if (!attr_set[TN]) {
-    KG_CUDA(cudaFuncSetAttribute(k_umma_gemm<TN>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
-    attr_set[TN] = true;
-  }
-  KG_REQUIRE(smem <= 220 * 1024, KG_ERR_SHAPE, "umma tile too large (N_pad %d)", np);
-  KG_LAUNCH(TN ? "k_umma_gemm_tn" : "k_umma_gemm_nn", k_umma_gemm<TN>, grid, UTHREADS, smem, st, g, np,
-            tmem_cols_for(np));
+static int stages_for(int np) {
+  int s = (int)(USMEM_CAP / ((size_t)(UM + np) * UKC * 8));
+  return s > UMAXS ? UMAXS : s;
+}
+
+static kg_status launch_pack(const PackJob& a, const PackJob& b, int64_t items_max, cudaStream_t st) {
+  dim3 grid((unsigned)persistent_blocks(items_max, 256, 8), 2, 1);
+  KG_LAUNCH("k_umma_pack", k_umma_pack, grid, 256, 0, st, a, b);
   return KG_OK;
 }
 
-kg_status umma_gemm_nn(const GemmArgs& g, cudaStream_t st) {
-  if (g.M_max <= 0 || g.N <= 0) return KG_OK;
-  KG_REQUIRE(g.N <= 256, KG_ERR_SHAPE, "umma NN supports N <= 256 (got %lld)", (long long)g.N);
-  int np = pad16((int)g.N);
-  int64_t tiles = ceil_div(g.M_max, UM);
-  int ctas = (int)(tiles < num_sms() ? tiles : num_sms());
-  return launch_umma<false>(g, np, dim3(ctas, 1, 1), st);
+static kg_status launch_packed(const PackedArgs& p, dim3 grid, cudaStream_t st) {
+  static bool attr_set = false;
+  if (!attr_set) {
+    KG_CUDA(cudaFuncSetAttribute(k_umma_packed, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)USMEM_CAP));
+    attr_set = true;
+  }
+  const int ns = stages_for(p.np);
+  const size_t smem = (size_t)ns * (UM + p.np) * UKC * 8;
+  KG_LAUNCH(p.tn ? "k_umma_gemm_tn" : "k_umma_gemm_nn", k_umma_packed, grid, UTHREADS, smem, st, p, ns,
+            acc_cols_for(p.np));
+  return KG_OK;
 }
 
-int umma_tn_splits(int64_t rows_max) {
-  // >= 64 data rows (4 chunks) per split, at most one CTA per SM
-  int64_t s = ceil_div(rows_max, 64);
-  if (s > num_sms()) s = num_sms();
+// NN workspace: A records (tiles x nk) + B records (nk)
+static size_t nn_pack_sizes(int64_t M_max, int64_t K, int64_t N, size_t* a_bytes) {
+  const int np = pad16((int)N);
+  const int64_t nk = ceil_div(K, UKC), tiles = ceil_div(M_max > 0 ? M_max : 1, UM);
+  size_t a = align_up((size_t)(tiles * nk * rec_floats(UM)) * 4);
+  size_t b = align_up((size_t)(nk * rec_floats(np)) * 4);
+  if (a_bytes) *a_bytes = a;
+  return a + b;
+}
+
+size_t umma_nn_workspace(int64_t M_max, int64_t K, int64_t N) { return nn_pack_sizes(M_max, K, N, nullptr); }
+
+kg_status umma_gemm_nn(const GemmArgs& g, void* ws, cudaStream_t st) {
+  if (g.M_max <= 0 || g.N <= 0) return KG_OK;
+  KG_REQUIRE(g.N <= 256, KG_ERR_SHAPE, "umma NN supports N <= 256 (got %lld)", (long long)g.N);
+  const int np = pad16((int)g.N);
+  const int64_t nk = ceil_div(g.K, UKC), tiles = ceil_div(g.M_max, UM);
+  size_t a_bytes = 0;
+  nn_pack_sizes(g.M_max, g.K, g.N, &a_bytes);
+  float* Ap = static_cast<float*>(ws);
+  float* Bp = reinterpret_cast<float*>(static_cast<char*>(ws) + a_bytes);
+  PackJob ja{g.A, g.lda, g.a_rows, g.M_dev, g.M_dev_index, g.M, g.K, UM, 0, nk, Ap};
+  PackJob jb{g.B, g.ldb, nullptr, nullptr, 0, g.K, g.N, np, 1, nk, Bp};
+  const int64_t items = tiles * nk * UM * 4;
+  kg_status s = launch_pack(ja, jb, items, st);
+  if (s != KG_OK) return s;
+  PackedArgs p{};
+  p.Ap = Ap; p.Bp = Bp; p.a_nk_alloc = nk; p.np = np; p.tn = 0;
+  p.M = g.M; p.M_dev = g.M_dev; p.M_dev_index = g.M_dev_index; p.nk = nk;
+  p.C = g.C; p.ldc = g.ldc; p.c_rows = g.c_rows; p.N = g.N; p.out_rows = 0; p.relu = g.relu;
+  const int ctas = (int)(tiles < num_sms() ? tiles : num_sms());
+  return launch_packed(p, dim3((unsigned)ctas, 1, 1), st);
+}
+
+int umma_tn_splits(int64_t rows_max, int64_t K) {
+  // >= 12 records (192 data rows) per split, one CTA per SM over all feature blocks
+  const int64_t blocks = ceil_div(K, UM);
+  int64_t s = ceil_div(ceil_div(rows_max, UKC), 12);
+  const int64_t cap = num_sms() / blocks > 0 ? num_sms() / blocks : 1;
+  if (s > cap) s = cap;
   return (int)(s < 1 ? 1 : s);
 }
 
-kg_status umma_gemm_tn(const GemmArgs& g, float* out, void* ws, cudaStream_t st) {
-  KG_REQUIRE(g.N <= 256, KG_ERR_SHAPE, "umma TN supports N <= 256");
-  int np = pad16((int)g.N);
-  int splits = umma_tn_splits(g.M_max);
-  GemmArgs h = g;
-  h.C = static_cast<float*>(ws);
-  h.ldc = g.N;
-  dim3 grid((unsigned)splits, (unsigned)ceil_div(g.K, UM), 1);
-  kg_status s = launch_umma<true>(h, np, grid, st);
-  if (s != KG_OK) return s;
-  return reduce_splits(h.C, splits, g.K * g.N, out, st);
+// TN workspace: A^T records (feature blocks x nk_alloc) + B^T records + split partials
+static size_t tn_sizes(int64_t rows_max, int64_t K, int64_t N, size_t* a_bytes, size_t* b_bytes) {
+  const int np = pad16((int)N);
+  const int64_t nk = ceil_div(rows_max > 0 ? rows_max : 1, UKC), blocks = ceil_div(K, UM);
+  size_t a = align_up((size_t)(blocks * nk * rec_floats(UM)) * 4);
+  size_t b = align_up((size_t)(nk * rec_floats(np)) * 4);
+  if (a_bytes) *a_bytes = a;
+  if (b_bytes) *b_bytes = b;
+  return a + b + align_up((size_t)umma_tn_splits(rows_max, K) * K * N * sizeof(float));
 }
 
-size_t umma_tn_workspace(int64_t rows_max, int64_t K, int64_t N) {
-  return align_up((size_t)umma_tn_splits(rows_max) * K * N * sizeof(float));
+size_t umma_tn_workspace(int64_t rows_max, int64_t K, int64_t N) { return tn_sizes(rows_max, K, N, nullptr, nullptr); }
+
+kg_status umma_gemm_tn(const GemmArgs& g, float* out, void* ws, cudaStream_t st) {
+  KG_REQUIRE(g.N <= 256, KG_ERR_SHAPE, "umma TN supports N <= 256");
+  if (g.K <= 0 || g.N <= 0) return KG_OK;
+  const int np = pad16((int)g.N);
+  const int64_t rows_max = g.M_max > 0 ? g.M_max : 1;
+  const int64_t nk_alloc = ceil_div(rows_max, UKC), blocks = ceil_div(g.K, UM);
+  size_t a_bytes = 0, b_bytes = 0;
+  tn_sizes(rows_max, g.K, g.N, &a_bytes, &b_bytes);
+  float* Ap = static_cast<float*>(ws);
+  float* Bp = reinterpret_cast<float*>(static_cast<char*>(ws) + a_bytes);
+  float* part = reinterpret_cast<float*>(static_cast<char*>(ws) + a_bytes + b_bytes);
+  // A^T: MMA rows = feature columns of A, k = data rows (gathered)
+  PackJob ja{g.A, g.lda, g.a_rows, g.M_dev, g.M_dev_index, g.M, g.K, UM, 1, nk_alloc, Ap};
+  // Bm^T: MMA rows = output columns, k = data rows
+  PackJob jb{g.B, g.ldb, nullptr, g.M_dev, g.M_dev_index, g.M, g.N, np, 1, nk_alloc, Bp};
+  const int64_t items = (blocks * UM > np ? blocks * UM : np) * nk_alloc * 4;
+  kg_status s = launch_pack(ja, jb, items, st);
+  if (s != KG_OK) return s;
+  const int splits = umma_tn_splits(rows_max, g.K);
+  PackedArgs p{};
+  p.Ap = Ap; p.Bp = Bp; p.a_nk_alloc = nk_alloc; p.np = np; p.tn = 1;
+  p.M = g.M; p.M_dev = g.M_dev; p.M_dev_index = g.M_dev_index; p.nk = 0;
+  p.C = part; p.ldc = g.N; p.c_rows = nullptr; p.N = g.N; p.out_rows = g.K; p.relu = 0;
+  s = launch_packed(p, dim3((unsigned)splits, (unsigned)blocks, 1), st);
+  if (s != KG_OK) return s;
+  return reduce_splits(part, splits, g.K * g.N, out, st);
 }
 
 }  // namespace kg
