@@ -100,6 +100,15 @@ __device__ __forceinline__ double warp_sum_d(double v) {
 
 __device__ __forceinline__ unsigned lane_id() { return threadIdx.x & 31u; }
 
+// Broadcast from lane 0: tells the compiler the value is warp-uniform, so loops
+// and loads derived from it stay convergent (no collective fallback around the
+// __shfl_sync calls inside per-warp work loops).
+__device__ __forceinline__ int64_t warp_uniform(int64_t v) {
+  const int lo = __shfl_sync(0xffffffffu, (int)(v & 0xffffffff), 0);
+  const int hi = __shfl_sync(0xffffffffu, (int)(v >> 32), 0);
+  return ((int64_t)hi << 32) | (uint32_t)lo;
+}
+
 __device__ __forceinline__ unsigned lanemask_lt() {
   unsigned m;
   asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));

@@ -19,7 +19,67 @@ struct GemmArgs {
   int64_t K;               // NN: reduction length; TN: output rows
   int64_t N;
   int relu;
+  const float* a_packed;   // NN only: A already in hi/lo records (see packed_store), a_rows ignored
 };
+
+// --- packed tensor-core operand records (kg_umma.cu) -----------------------
+// An operand with 128-row blocks is stored as records (block, kc) of 16 K
+// values: [hi | lo] halves of 128 x 16 fp32 (tf32-valued) in the K-major
+// no-swizzle canonical layout. Producers that can emit this layout directly
+// (k_aggregate) save the separate pack pass.
+constexpr int PK_ROWS = 128;
+constexpr int PK_K = 16;
+constexpr int64_t PK_REC = 2 * PK_ROWS * PK_K;   // floats per record
+
+inline int64_t packed_records(int64_t K) { return (K + PK_K - 1) / PK_K; }
+inline size_t packed_bytes(int64_t rows, int64_t K) {
+  return (size_t)((rows + PK_ROWS - 1) / PK_ROWS) * (size_t)packed_records(K) * PK_REC * sizeof(float);
+}
+
+#ifdef __CUDACC__
+__device__ __forceinline__ void split_tf32(float x, float& hi, float& lo) {
+  uint32_t h;
+  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(h) : "f"(x));   // nearest tf32: |lo| <= 2^-12 |x|
+  hi = __uint_as_float(h);
+  lo = x - hi;
+}
+
+// hi-half float pointer of element (row, k); the lo half is at +PK_ROWS*PK_K
+__device__ __forceinline__ float* packed_at(float* P, int64_t nk, int64_t row, int k) {
+  const int r = (int)(row & (PK_ROWS - 1)), kk = k & (PK_K - 1);
+  const int64_t rec = (row / PK_ROWS) * nk + (k / PK_K);
+  return P + rec * PK_REC + ((kk >> 2) * (PK_ROWS / 8) + (r >> 3)) * 32 + (r & 7) * 4 + (kk & 3);
+}
+
+// V consecutive values starting at k (k % V == 0, V in {1, 2, 4})
+template <int V>
+__device__ __forceinline__ void packed_store(float* P, int64_t nk, int64_t row, int k, const float* v) {
+  float h[V], l[V];
+#pragma unroll
+  for (int i = 0; i < V; ++i) split_tf32(v[i], h[i], l[i]);
+  float* ph = packed_at(P, nk, row, k);
+  float* pl = ph + PK_ROWS * PK_K;
+  if constexpr (V == 4) {
+    *reinterpret_cast<float4*>(ph) = make_float4(h[0], h[1], h[2], h[3]);
+    *reinterpret_cast<float4*>(pl) = make_float4(l[0], l[1], l[2], l[3]);
+  } else if constexpr (V == 2) {
+    *reinterpret_cast<float2*>(ph) = make_float2(h[0], h[1]);
+    *reinterpret_cast<float2*>(pl) = make_float2(l[0], l[1]);
+  } else {
+    *ph = h[0];
+    *pl = l[0];
+  }
+}
+
+// zero the K padding [K, 16*nk) of one row (lanes of a warp share the work)
+__device__ __forceinline__ void packed_zero_pad(float* P, int64_t nk, int64_t row, int K, int lane, int nlanes) {
+  for (int k = K + lane; k < nk * PK_K; k += nlanes) {
+    float* ph = packed_at(P, nk, row, k);
+    ph[0] = 0.f;
+    ph[PK_ROWS * PK_K] = 0.f;
+  }
+}
+#endif
 
 // CUDA-core reference implementations (kg_gemm.cu): used by tests as a
 // cross-check of the tensor-core kernels.

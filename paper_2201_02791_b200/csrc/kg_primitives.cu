@@ -129,6 +129,46 @@ __global__ void scan_tiles_apply(const uint32_t* __restrict__ in, uint32_t* __re
   if (total && blockIdx.x == gridDim.x - 1 && threadIdx.x == 0) *total = off + tot;
 }
 
+// Small inputs: one CTA walks the tiles with a running carry (1 launch instead
+// of tile sums + recursive scan + apply). With `cout` set it also performs the
+// flag compaction cout[off + rank(i)] = i (flags = in) in the same pass.
+constexpr int64_t SCAN_SINGLE_MAX = 8 * SCAN_TILE;
+
+__global__ void __launch_bounds__(SCAN_THREADS) scan_single(const uint32_t* __restrict__ in, uint32_t* out,
+                                                            int64_t n, uint32_t* total, int32_t* __restrict__ cout,
+                                                            int32_t off_c, const int32_t* __restrict__ off_d,
+                                                            int32_t* __restrict__ count_out) {
+  __shared__ uint32_t s[SCAN_TILE];
+  const int32_t off = cout ? off_c + (off_d ? *off_d : 0) : 0;
+  uint32_t carry = 0;
+  for (int64_t base = 0; base < n; base += SCAN_TILE) {
+    uint32_t f[SCAN_ITEMS];
+#pragma unroll
+    for (int j = 0; j < SCAN_ITEMS; ++j) {
+      const int64_t i = base + j * SCAN_THREADS + threadIdx.x;
+      f[j] = i < n ? in[i] : 0u;
+      s[j * SCAN_THREADS + threadIdx.x] = f[j];
+    }
+    __syncthreads();
+    const uint32_t tot = block_scan_tile(s);
+#pragma unroll
+    for (int j = 0; j < SCAN_ITEMS; ++j) {
+      const int64_t i = base + j * SCAN_THREADS + threadIdx.x;
+      if (i < n) {
+        const uint32_t v = s[j * SCAN_THREADS + threadIdx.x] + carry;
+        if (out) out[i] = v;
+        if (cout && f[j]) cout[off + (int64_t)v] = (int32_t)i;
+      }
+    }
+    carry += tot;
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    if (total) *total = carry;
+    if (count_out) *count_out = (int32_t)carry;
+  }
+}
+
 size_t scan_workspace(int64_t n) {
   size_t bytes = 0;
   int64_t m = n;
@@ -146,9 +186,9 @@ kg_status exclusive_scan_u32(const uint32_t* in, uint32_t* out, int64_t n, uint3
     if (total) KG_CUDA(cudaMemsetAsync(total, 0, sizeof(uint32_t), st));
     return KG_OK;
   }
-  if (n <= SCAN_TILE) {
-    KG_LAUNCH("scan_tiles_apply", scan_tiles_apply, 1, SCAN_THREADS, 0, st, in, out, n, nullptr, total);
-    KG_CHECK_LAUNCH("scan_tiles_apply");
+  if (n <= SCAN_SINGLE_MAX) {
+    KG_LAUNCH("scan_single", scan_single, 1, SCAN_THREADS, 0, st, in, out, n, total, (int32_t*)nullptr, 0,
+              (const int32_t*)nullptr, (int32_t*)nullptr);
     return KG_OK;
   }
   KG_REQUIRE(ws_bytes >= scan_workspace(n), KG_ERR_VALIDATION, "scan workspace too small");
@@ -172,10 +212,13 @@ constexpr int RS_THREADS = 256;
 constexpr int RS_ROUNDS = 16;
 constexpr int RS_TILE = RS_THREADS * RS_ROUNDS;
 constexpr int RS_WARPS = RS_THREADS / 32;
+constexpr int64_t RS_SELF_OFFSET_TILES = 64;   // up to 256 K keys: offsets computed in the scatter
 
+// tile_major = 0: hist[d * tiles + tile] (scanned as one array);
+// tile_major = 1: hist[tile * 256 + d] (read back by radix_scatter's own offsets)
 template <typename K>
 __global__ void __launch_bounds__(RS_THREADS) radix_hist(const K* __restrict__ keys, int64_t n, int shift,
-                                                          uint32_t* __restrict__ hist, int64_t tiles) {
+                                                          uint32_t* __restrict__ hist, int64_t tiles, int tile_major) {
   __shared__ uint32_t cnt[256];
   cnt[threadIdx.x] = 0;
   __syncthreads();
@@ -186,19 +229,53 @@ __global__ void __launch_bounds__(RS_THREADS) radix_hist(const K* __restrict__ k
     if (i < n) atomicAdd(&cnt[(unsigned)(keys[i] >> shift) & 255u], 1u);
   }
   __syncthreads();
-  hist[(int64_t)threadIdx.x * tiles + blockIdx.x] = cnt[threadIdx.x];
+  if (tile_major) hist[(int64_t)blockIdx.x * 256 + threadIdx.x] = cnt[threadIdx.x];
+  else hist[(int64_t)threadIdx.x * tiles + blockIdx.x] = cnt[threadIdx.x];
 }
 
+// Exclusive scan of one value per thread over a 256-thread block.
+__device__ __forceinline__ uint32_t block_excl_scan256(uint32_t x, uint32_t* wsum /* smem [8] */) {
+  const int t = threadIdx.x, lane = t & 31, w = t >> 5;
+  uint32_t inc = x;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t y = __shfl_up_sync(0xffffffffu, inc, o);
+    if (lane >= o) inc += y;
+  }
+  if (lane == 31) wsum[w] = inc;
+  __syncthreads();
+  uint32_t before = 0;
+#pragma unroll
+  for (int q = 0; q < RS_WARPS; ++q)
+    if (q < w) before += wsum[q];
+  return before + inc - x;
+}
+
+// offs == nullptr: the digit offsets of this tile are derived here from the
+// tile-major histogram (sum over all tiles per digit, exclusive scan over
+// digits, plus the same digit's counts in earlier tiles) — no scan launches.
 template <typename K>
 __global__ void __launch_bounds__(RS_THREADS) radix_scatter(const K* __restrict__ kin, const uint32_t* __restrict__ vin,
                                                              K* __restrict__ kout, uint32_t* __restrict__ vout,
                                                              int64_t n, int shift,
-                                                             const uint32_t* __restrict__ offs, int64_t tiles) {
+                                                             const uint32_t* __restrict__ offs, int64_t tiles,
+                                                             const uint32_t* __restrict__ hist_tm) {
   __shared__ uint32_t base[256];
   __shared__ uint32_t wcnt[RS_WARPS][256];
   __shared__ uint32_t woff[RS_WARPS][256];
   const int t = threadIdx.x, w = t >> 5;
-  base[t] = offs[(int64_t)t * tiles + blockIdx.x];
+  if (offs) {
+    base[t] = offs[(int64_t)t * tiles + blockIdx.x];
+  } else {
+    uint32_t tot = 0, pre = 0;
+    for (int64_t q = 0; q < tiles; ++q) {
+      const uint32_t h = __ldg(hist_tm + q * 256 + t);
+      tot += h;
+      if (q < (int64_t)blockIdx.x) pre += h;
+    }
+    base[t] = block_excl_scan256(tot, &woff[0][0]) + pre;
+    __syncthreads();
+  }
 #pragma unroll
   for (int q = 0; q < RS_WARPS; ++q) wcnt[q][t] = 0;
   __syncthreads();
@@ -263,14 +340,20 @@ static kg_status sort_pairs(K* keys, uint32_t* vals, int64_t n, int key_bits, vo
   uint32_t* va = vals;
   K* kb = k2;
   uint32_t* vb = v2;
+  const bool self_offsets = tiles <= RS_SELF_OFFSET_TILES;
   for (int p = 0; p < passes; ++p) {
     int shift = 8 * p;
-    KG_LAUNCH("radix_hist", (radix_hist<K>), (unsigned)tiles, RS_THREADS, 0, st, ka, n, shift, hist, tiles);
-    KG_CHECK_LAUNCH("radix_hist");
-    kg_status s = exclusive_scan_u32(hist, hist, hist_n, nullptr, scan_ws, scan_workspace(hist_n), st);
-    if (s != KG_OK) return s;
-    KG_LAUNCH("radix_scatter", (radix_scatter<K>), (unsigned)tiles, RS_THREADS, 0, st, ka, va, kb, vb, n, shift, hist, tiles);
-    KG_CHECK_LAUNCH("radix_scatter");
+    KG_LAUNCH("radix_hist", (radix_hist<K>), (unsigned)tiles, RS_THREADS, 0, st, ka, n, shift, hist, tiles,
+              self_offsets ? 1 : 0);
+    if (self_offsets) {
+      KG_LAUNCH("radix_scatter", (radix_scatter<K>), (unsigned)tiles, RS_THREADS, 0, st, ka, va, kb, vb, n, shift,
+                (const uint32_t*)nullptr, tiles, (const uint32_t*)hist);
+    } else {
+      kg_status s = exclusive_scan_u32(hist, hist, hist_n, nullptr, scan_ws, scan_workspace(hist_n), st);
+      if (s != KG_OK) return s;
+      KG_LAUNCH("radix_scatter", (radix_scatter<K>), (unsigned)tiles, RS_THREADS, 0, st, ka, va, kb, vb, n, shift,
+                (const uint32_t*)hist, tiles, (const uint32_t*)nullptr);
+    }
     K* tk = ka; ka = kb; kb = tk;
     uint32_t* tv = va; va = vb; vb = tv;
   }
@@ -309,6 +392,11 @@ size_t compact_workspace(int64_t n) { return align_up(n * sizeof(uint32_t)) + 25
 kg_status compact_flags(const uint32_t* flags, int64_t n, int32_t* out, int32_t* count_out, int32_t off_c,
                         const int32_t* off_d, void* ws, size_t ws_bytes, cudaStream_t st) {
   KG_REQUIRE(ws_bytes >= compact_workspace(n), KG_ERR_VALIDATION, "compact workspace too small");
+  if (n > 0 && n <= SCAN_SINGLE_MAX) {
+    KG_LAUNCH("scan_single", scan_single, 1, SCAN_THREADS, 0, st, flags, (uint32_t*)nullptr, n, (uint32_t*)nullptr,
+              out, off_c, off_d, count_out);
+    return KG_OK;
+  }
   Arena a(ws, ws_bytes);
   uint32_t* pos = a.take<uint32_t>(n);
   uint32_t* total = a.take<uint32_t>(1);

@@ -95,7 +95,8 @@ struct AggArgs {
   const int32_t* pos;
   const int32_t* counts;
   int t;
-  float* acc;            // (count, B*d) compact by position
+  float* acc;            // packed hi/lo GEMM records of the (count, B*d) rows, by position
+  int64_t acc_nk;        // records per 128-row block (packed_records(B*d))
   float* partial;        // (split chunks, B*d)
 };
 
@@ -130,7 +131,7 @@ __global__ void __launch_bounds__(256, 3) k_aggregate(AggArgs a) {
   bool slot_ok[S];
 #pragma unroll
   for (int s = 0; s < S; ++s) slot_ok[s] = (s * 32 + lane) * VEC < d;
-  for (int64_t c = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; c < NC; c += warps) {
+  for (int64_t c = warp_uniform((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5); c < NC; c += warps) {
     const int32_t v = a.ck.row[c];
     const int32_t p = a.pos[v];
     if (p < 0 || p >= T) continue;
@@ -205,10 +206,17 @@ __global__ void __launch_bounds__(256, 3) k_aggregate(AggArgs a) {
               for (int cc = 0; cc < VEC; ++cc) acc[b][s][cc] = fmaf(cf, xv[s][cc], acc[b][s][cc]);
         }
       }
-      out = a.acc + (int64_t)p * B * d;
-    } else {
-      out = a.partial + (int64_t)a.ck.slot[c] * B * d;
+      // finished row: straight into the GEMM's packed hi/lo A records
+#pragma unroll
+      for (int b = 0; b < NB; ++b)
+        if (b < B)
+#pragma unroll
+          for (int s = 0; s < S; ++s)
+            if (slot_ok[s]) packed_store<VEC>(a.acc, a.acc_nk, p, b * d + (s * 32 + lane) * VEC, acc[b][s]);
+      packed_zero_pad(a.acc, a.acc_nk, p, B * d, lane, 32);
+      continue;
     }
+    out = a.partial + (int64_t)a.ck.slot[c] * B * d;
 #pragma unroll
     for (int b = 0; b < NB; ++b)
       if (b < B)
@@ -271,9 +279,11 @@ __global__ void __launch_bounds__(CB_THREADS) k_aggregate_combine(AggArgs a) {
       if ((threadIdx.x >> 5) == 0 && col < width) {
         const int b = col / a.d, k = col % a.d;
         const float self = a.coeffs[(a.G - 1) * a.B + b] * a.H[(int64_t)v * a.d + k];
-        a.acc[(int64_t)p * width + col] = tot + self;
+        const float x = tot + self;
+        packed_store<1>(a.acc, a.acc_nk, p, col, &x);
       }
     }
+    if ((threadIdx.x >> 5) == 0) packed_zero_pad(a.acc, a.acc_nk, p, width, threadIdx.x & 31, 32);
   }
 }
 
@@ -311,7 +321,7 @@ __global__ void __launch_bounds__(256, 3) k_csc_backward(CscArgs a) {
   bool slot_ok[S];
 #pragma unroll
   for (int s = 0; s < S; ++s) slot_ok[s] = (s * 32 + lane) * VEC < d;
-  for (int64_t c = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; c < NC; c += warps) {
+  for (int64_t c = warp_uniform((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5); c < NC; c += warps) {
     const int32_t u = a.ck.row[c];
     const int32_t q = a.pos[u];
     if (q < 0 || q >= Sn) continue;
@@ -642,7 +652,7 @@ static kg_status run_csc(const CscArgs& a, const kg_graph_csr* G, cudaStream_t s
 }
 
 struct LayerWs {
-  float* acc;     // forward (n, B*d_in)
+  float* acc;     // forward (n, B*d_in) as packed GEMM records
   float* partial; // (split chunks, B*max(d_in, d_out))
   float* Wy;      // (d_in, B*d_out)
   float* Wb;      // (B*d_out, d_in)
@@ -659,7 +669,7 @@ static size_t layer_ws(int64_t n, int64_t e, int64_t split_chunks, int di, int d
                        size_t cap) {
   Arena a(base, cap);
   LayerWs l;
-  l.acc = a.take<float>((size_t)n * B * di);
+  l.acc = a.take<float>(packed_bytes(n, (int64_t)B * di) / sizeof(float));
   l.partial = a.take<float>((size_t)split_chunks * B * (di > dO ? di : dO));
   l.Wy = a.take<float>((size_t)B * di * dO);
   l.Wb = a.take<float>((size_t)B * di * dO);
@@ -705,11 +715,11 @@ kg_status kg_rgcn_forward(const kg_graph_csr* G, const kg_layer_params* lp, cons
   size_t need = layer_ws(G->n, G->e, cap_split_chunks(G), lp->d_in, lp->d_out, lp->B, &w, ws, (size_t)ws_bytes);
   KG_REQUIRE((size_t)ws_bytes >= need, KG_ERR_VALIDATION, "layer workspace too small");
   AggArgs a{G->indptr, G->src, G->rel, G->norm, csr_chunks(G), lp->coeffs, lp->G, lp->B, lp->d_in, H_in, pos,
-            counts, t, w.acc, w.partial};
+            counts, t, w.acc, packed_records((int64_t)lp->B * lp->d_in), w.partial};
   kg_status s = run_aggregate(a, G, st);
   if (s != KG_OK) return s;
   GemmArgs g{};
-  g.A = w.acc;
+  g.a_packed = w.acc;
   g.lda = (int64_t)lp->B * lp->d_in;
   g.B = lp->bases;   // (B*d_in, d_out)
   g.ldb = lp->d_out;

@@ -410,7 +410,7 @@ __global__ void k_mark_sources(const int32_t* __restrict__ ck_ptr, const int32_t
   const int32_t active = counts[hop];
   const int32_t NC = ck_counts[0];
   const int warps = (gridDim.x * blockDim.x) >> 5;
-  for (int64_t c = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; c < NC; c += warps) {
+  for (int64_t c = warp_uniform((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5); c < NC; c += warps) {
     int32_t v = ck_row[c];
     int32_t p = pos[v];
     if (p < 0 || p >= active) continue;

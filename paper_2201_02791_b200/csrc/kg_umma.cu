@@ -27,8 +27,8 @@
 
 namespace kg {
 
-constexpr int UM = 128;        // MMA M (rows per tile)
-constexpr int UKC = 16;        // K values per record
+constexpr int UM = PK_ROWS;    // MMA M (rows per tile)
+constexpr int UKC = PK_K;      // K values per record
 constexpr int UMAXS = 8;       // max ring stages
 constexpr int UTHREADS = 192;  // producer warp, MMA warp, 4 epilogue warps
 constexpr size_t USMEM_CAP = 200 * 1024;
@@ -116,13 +116,6 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, float* v) {
   asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 #pragma unroll
   for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
-}
-
-__device__ __forceinline__ void split_tf32(float x, float& hi, float& lo) {
-  uint32_t h;
-  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(h) : "f"(x));   // nearest tf32: |lo| <= 2^-12 |x|
-  hi = __uint_as_float(h);
-  lo = x - hi;
 }
 
 // ---------------------------------------------------------------------------
@@ -443,8 +436,12 @@ kg_status umma_gemm_nn(const GemmArgs& g, void* ws, cudaStream_t st) {
   float* Ap = static_cast<float*>(ws);
   float* Bp = reinterpret_cast<float*>(static_cast<char*>(ws) + a_bytes);
   PackJob ja{g.A, g.lda, g.a_rows, g.M_dev, g.M_dev_index, g.M, g.K, UM, 0, nk, Ap};
+  if (g.a_packed) {   // producer already wrote the A records
+    ja.src = nullptr;
+    Ap = const_cast<float*>(g.a_packed);
+  }
   PackJob jb{g.B, g.ldb, nullptr, nullptr, 0, g.K, g.N, np, 1, nk, Bp};
-  const int64_t items = tiles * nk * UM * 4;
+  const int64_t items = g.a_packed ? nk * np * 4 : tiles * nk * UM * 4;
   kg_status s = launch_pack(ja, jb, items, st);
   if (s != KG_OK) return s;
   PackedArgs p{};
