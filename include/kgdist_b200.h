@@ -259,6 +259,21 @@ kg_status kg_distmult_loss(const float* H, int32_t d, int32_t n_local, const flo
                            float* dH,
                            float* d_decoder, float* loss_out, float* scores_out, uint32_t* flags, void* ws,
                            int64_t ws_bytes, void* stream);
+/* kg_distmult_loss in two halves with identical arguments and workspace:
+ * kg_loss_groups only sorts the batch keys and builds the segment bounds
+ * (needs the closure's seed order, not H), so a trainer can run it on a
+ * second stream concurrently with the layers; kg_loss_compute (ordered after
+ * it) scores, reduces the loss and scatters d_decoder / dH. */
+kg_status kg_loss_groups(const float* H, int32_t d, int32_t n_local, const float* decoder, int32_t R,
+                         const int32_t* stream_triples, const float* labels, int64_t total, int64_t start,
+                         const int64_t* start_dev, int64_t b, const int32_t* vertex_order, const int32_t* counts,
+                         float* dH, float* d_decoder, float* loss_out, float* scores_out, uint32_t* flags, void* ws,
+                         int64_t ws_bytes, void* stream);
+kg_status kg_loss_compute(const float* H, int32_t d, int32_t n_local, const float* decoder, int32_t R,
+                          const int32_t* stream_triples, const float* labels, int64_t total, int64_t start,
+                          const int64_t* start_dev, int64_t b, const int32_t* vertex_order, const int32_t* counts,
+                          float* dH, float* d_decoder, float* loss_out, float* scores_out, uint32_t* flags,
+                          void* ws, int64_t ws_bytes, void* stream);
 
 /* ---------------------------------------------------------------------- */
 /* R19/R20  Reduction + optimizer (ref:trainer.py:63-151)                  */

@@ -87,6 +87,10 @@ _PROTOS = {
     "kg_loss_workspace_bytes": (c_int64, [c_int64, c_int32, c_int32, c_int32]),
     "kg_distmult_loss": (ST, [P, c_int32, c_int32, P, c_int32, P, P, c_int64, c_int64, P, c_int64, P, P, P,
                               P, P, P, P, P, c_int64, P]),
+    "kg_loss_groups": (ST, [P, c_int32, c_int32, P, c_int32, P, P, c_int64, c_int64, P, c_int64, P, P, P,
+                            P, P, P, P, P, c_int64, P]),
+    "kg_loss_compute": (ST, [P, c_int32, c_int32, P, c_int32, P, P, c_int64, c_int64, P, c_int64, P, P, P,
+                             P, P, P, P, P, c_int64, P]),
     "kg_optim_workspace_bytes": (c_int64, [c_int64]),
     "kg_dense_step": (ST, [P, P, P, P, c_int32, c_int64, c_int32, c_float, c_float, c_float, c_float,
                            c_double, c_double, P, c_float, P, P, c_int64, P]),

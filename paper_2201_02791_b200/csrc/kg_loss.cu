@@ -39,7 +39,7 @@ __device__ __forceinline__ int64_t row_of(const LossArgs& a, int64_t i) {
 __global__ void __launch_bounds__(256) k_score(LossArgs a) {
   const int lane = lane_id();
   const int warps = (gridDim.x * blockDim.x) >> 5;
-  for (int64_t i = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; i < a.b; i += warps) {
+  for (int64_t i = warp_uniform((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5); i < a.b; i += warps) {
     int64_t row = row_of(a, i);
     int32_t h = a.tri[row * 3], r = a.tri[row * 3 + 1], t = a.tri[row * 3 + 2];
     const float* Hh = a.H + (int64_t)h * a.d;
@@ -151,7 +151,7 @@ __global__ void __launch_bounds__(256) k_sub_partials(LossArgs a, const uint32_t
   const uint32_t S = *total_sub;
   const int lane = lane_id();
   const int warps = (gridDim.x * blockDim.x) >> 5;
-  for (int64_t s = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; s < S; s += warps) {
+  for (int64_t s = warp_uniform((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5); s < S; s += warps) {
     // group = last g with sub_start[g] <= s
     int32_t l = 0, h = ng;
     while (h - l > 1) {
@@ -255,18 +255,19 @@ static size_t seg_ws(int64_t nelem, int64_t ngroups, int d, SegWs* w, Arena& a) 
   return a.used;
 }
 
-template <int KIND>
-static kg_status seg_reduce(const LossArgs& la, const uint32_t* keys, const uint32_t* vals, int64_t nelem,
-                            const int32_t* ids, const int32_t* ng_dev, int32_t ng_max, float* out, SegWs& w,
-                            cudaStream_t st) {
+static kg_status seg_bounds(const uint32_t* keys, int64_t nelem, const int32_t* ids, const int32_t* ng_dev,
+                            int32_t ng_max, SegWs& w, cudaStream_t st) {
   int gb = persistent_blocks(ng_max, 256, 8);
   KG_LAUNCH("k_group_bounds", k_group_bounds, gb, 256, 0, st, keys, nelem, ids, ng_dev, ng_max, w.lo, w.nsub);
   KG_LAUNCH("k_group_len", k_group_len, gb, 256, 0, st, keys, nelem, ids, ng_dev, ng_max, w.hi);
-  KG_CHECK_LAUNCH("group bounds");
   // with a device-resident group count the caller zeroed nsub[0:ng_max] so the
   // scan sees 0 beyond *ng_dev
-  kg_status s = exclusive_scan_u32(w.nsub, w.sub_start, ng_max, w.total, w.scan, scan_workspace(ng_max + 1), st);
-  if (s != KG_OK) return s;
+  return exclusive_scan_u32(w.nsub, w.sub_start, ng_max, w.total, w.scan, scan_workspace(ng_max + 1), st);
+}
+
+template <int KIND>
+static kg_status seg_sums(const LossArgs& la, const uint32_t* vals, int64_t nelem, const int32_t* ids,
+                          const int32_t* ng_dev, int32_t ng_max, float* out, SegWs& w, cudaStream_t st) {
   int64_t max_sub = nelem / CH + ng_max + 1;
   int pb = persistent_blocks(max_sub * 32, 256, 8);
   if (la.d <= 32) KG_LAUNCH("k_sub_partials", (k_sub_partials<KIND, 1>), pb, 256, 0, st, la, vals, w.lo, w.hi, w.sub_start, w.total, ng_dev, ng_max, w.partial);
@@ -274,10 +275,8 @@ static kg_status seg_reduce(const LossArgs& la, const uint32_t* keys, const uint
   else if (la.d <= 128) KG_LAUNCH("k_sub_partials", (k_sub_partials<KIND, 4>), pb, 256, 0, st, la, vals, w.lo, w.hi, w.sub_start, w.total, ng_dev, ng_max, w.partial);
   else if (la.d <= 256) KG_LAUNCH("k_sub_partials", (k_sub_partials<KIND, 8>), pb, 256, 0, st, la, vals, w.lo, w.hi, w.sub_start, w.total, ng_dev, ng_max, w.partial);
   else KG_REQUIRE(false, KG_ERR_SHAPE, "embedding width %d > 256 unsupported", la.d);
-  KG_CHECK_LAUNCH("k_sub_partials");
   KG_LAUNCH("k_group_finish", k_group_finish, persistent_blocks((int64_t)ng_max * la.d, 256, 8), 256, 0, st, w.partial, w.sub_start, w.nsub,
                                                                                    ids, ng_dev, ng_max, la.d, out);
-  KG_CHECK_LAUNCH("k_group_finish");
   return KG_OK;
 }
 
@@ -293,21 +292,78 @@ using namespace kg;
 
 extern "C" {
 
-int64_t kg_loss_workspace_bytes(int64_t b, int32_t n, int32_t d, int32_t R) {
-  Arena a(nullptr, 0);
-  a.take<float>(b);          // dg
-  a.take<float>(b);          // per
-  a.take<double>(1024);      // block partials
-  a.take<uint32_t>(b);       // rk
-  a.take<uint32_t>(b);       // rv
-  a.take<uint32_t>(2 * b);   // vk
-  a.take<uint32_t>(2 * b);   // vv
-  a.take<char>(sort32_workspace(2 * b));
-  a.take<uint32_t>(n + 1);   // zero fill for nsub tail (memset range)
-  seg_ws(b, R, d, nullptr, a);
-  seg_ws(2 * b, 2 * b < (int64_t)n ? 2 * b : (int64_t)n, d, nullptr, a);
-  return (int64_t)a.used + 4096;
+// One arena layout shared by the grouping and the compute halves (they may run
+// on different streams: the grouping touches keys/sort/segment-bound regions,
+// the compute half dg/per/partials).
+struct LossWs {
+  float* dg;
+  float* per;
+  double* part;
+  uint32_t *rk, *rv, *vk, *vv;
+  char* sws;
+  SegWs wr, wv;
+  int64_t ngmax;
+};
+
+static size_t loss_arena(void* ws, size_t bytes, int64_t b, int32_t n_local, int32_t d, int32_t R, LossWs* L) {
+  Arena a(ws, bytes);
+  LossWs w;
+  w.ngmax = 2 * b < (int64_t)n_local ? 2 * b : (int64_t)n_local;
+  w.dg = a.take<float>(b);
+  w.per = a.take<float>(b);
+  w.part = a.take<double>(1024);
+  w.rk = a.take<uint32_t>(b);
+  w.rv = a.take<uint32_t>(b);
+  w.vk = a.take<uint32_t>(2 * b);
+  w.vv = a.take<uint32_t>(2 * b);
+  w.sws = a.take<char>(sort32_workspace(2 * b));
+  seg_ws(b, R, d, &w.wr, a);
+  seg_ws(2 * b, w.ngmax, d, &w.wv, a);
+  if (L) *L = w;
+  return a.used + 4096;
 }
+
+static kg_status loss_groups(const LossArgs& la, int32_t n_local, int32_t R, const int32_t* order,
+                             const int32_t* counts, LossWs& w, cudaStream_t st) {
+  const int64_t b = la.b;
+  KG_LAUNCH("k_loss_keys", k_loss_keys, persistent_blocks(b, 256, 8), 256, 0, st, la, w.rk, w.rv, w.vk, w.vv);
+  kg_status s = sort_pairs_u32(w.rk, w.rv, b, bits_for((uint64_t)R), w.sws, sort32_workspace(2 * b), st);
+  if (s != KG_OK) return s;
+  s = sort_pairs_u32(w.vk, w.vv, 2 * b, bits_for((uint64_t)n_local), w.sws, sort32_workspace(2 * b), st);
+  if (s != KG_OK) return s;
+  KG_CUDA(cudaMemsetAsync(w.wr.nsub, 0, (R + 1) * sizeof(uint32_t), st));
+  KG_CUDA(cudaMemsetAsync(w.wv.nsub, 0, (w.ngmax + 1) * sizeof(uint32_t), st));
+  s = seg_bounds(w.rk, b, nullptr, nullptr, R, w.wr, st);
+  if (s != KG_OK) return s;
+  // seed groups: A_0 = order[0:counts[0]] (ascending, exactly the distinct endpoints)
+  return seg_bounds(w.vk, 2 * b, order, counts, (int32_t)w.ngmax, w.wv, st);
+}
+
+static kg_status loss_compute(const LossArgs& la, int32_t R, const int32_t* order, const int32_t* counts,
+                              float* dH, float* d_decoder, float* loss_out, uint32_t* flags, LossWs& w,
+                              cudaStream_t st) {
+  const int64_t b = la.b;
+  KG_LAUNCH("k_score", k_score, persistent_blocks(b * 32, 256, 8), 256, 0, st, la);
+  int nb = persistent_blocks(b, 256, 4);
+  if (nb > 1024) nb = 1024;
+  KG_LAUNCH("k_block_sums", k_block_sums, nb, 256, 0, st, w.per, b, w.part);
+  KG_LAUNCH("k_final_mean", k_final_mean, 1, 256, 0, st, w.part, nb, b, loss_out, flags);
+  kg_status s = seg_sums<0>(la, w.rv, b, nullptr, nullptr, R, d_decoder, w.wr, st);
+  if (s != KG_OK) return s;
+  return seg_sums<1>(la, w.vv, 2 * b, order, counts, (int32_t)w.ngmax, dH, w.wv, st);
+}
+
+int64_t kg_loss_workspace_bytes(int64_t b, int32_t n, int32_t d, int32_t R) {
+  return (int64_t)loss_arena(nullptr, 0, b, n, d, R, nullptr);
+}
+
+#define KG_LOSS_SETUP()                                                                                     \
+  cudaStream_t st = as_stream(stream);                                                                      \
+  KG_REQUIRE(b >= 1 && total >= 1, KG_ERR_VALIDATION, "empty batch");                                       \
+  LossWs w;                                                                                                 \
+  KG_REQUIRE(loss_arena(ws, (size_t)ws_bytes, b, n_local, d, R, &w) <= (size_t)ws_bytes, KG_ERR_VALIDATION, \
+             "loss workspace too small");                                                                   \
+  LossArgs la{H, d, decoder, tri, labels, total, start, b, start_dev, w.dg, w.per, scores_out, flags}
 
 kg_status kg_distmult_loss(const float* H, int32_t d, int32_t n_local, const float* decoder, int32_t R,
                            const int32_t* tri,
@@ -315,47 +371,31 @@ kg_status kg_distmult_loss(const float* H, int32_t d, int32_t n_local, const flo
                            const int32_t* order,
                            const int32_t* counts, float* dH, float* d_decoder, float* loss_out, float* scores_out,
                            uint32_t* flags, void* ws, int64_t ws_bytes, void* stream) {
-  cudaStream_t st = as_stream(stream);
-  KG_REQUIRE(b >= 1 && total >= 1, KG_ERR_VALIDATION, "empty batch");
-  // n (local vertices) bound for seed groups: 2b distinct endpoints at most
-  int64_t ngmax = 2 * b < (int64_t)n_local ? 2 * b : (int64_t)n_local;
-  Arena a(ws, (size_t)ws_bytes);
-  float* dg = a.take<float>(b);
-  float* per = a.take<float>(b);
-  double* part = a.take<double>(1024);
-  uint32_t* rk = a.take<uint32_t>(b);
-  uint32_t* rv = a.take<uint32_t>(b);
-  uint32_t* vk = a.take<uint32_t>(2 * b);
-  uint32_t* vv = a.take<uint32_t>(2 * b);
-  char* sws = a.take<char>(sort32_workspace(2 * b));
-  a.take<uint32_t>(ngmax + 1);
-  SegWs wr, wv;
-  seg_ws(b, R, d, &wr, a);
-  seg_ws(2 * b, ngmax, d, &wv, a);
-  KG_REQUIRE(a.used <= (size_t)ws_bytes && dg != nullptr, KG_ERR_VALIDATION, "loss workspace too small");
+  KG_LOSS_SETUP();
+  kg_status s = loss_groups(la, n_local, R, order, counts, w, st);
+  if (s != KG_OK) return s;
+  return loss_compute(la, R, order, counts, dH, d_decoder, loss_out, flags, w, st);
+}
 
-  LossArgs la{H, d, decoder, tri, labels, total, start, b, start_dev, dg, per, scores_out, flags};
-  KG_LAUNCH("k_score", k_score, persistent_blocks(b * 32, 256, 8), 256, 0, st, la);
-  KG_CHECK_LAUNCH("k_score");
-  int nb = persistent_blocks(b, 256, 4);
-  if (nb > 1024) nb = 1024;
-  KG_LAUNCH("k_block_sums", k_block_sums, nb, 256, 0, st, per, b, part);
-  KG_LAUNCH("k_final_mean", k_final_mean, 1, 256, 0, st, part, nb, b, loss_out, flags);
-  KG_CHECK_LAUNCH("loss mean");
+// The batch-only half of kg_distmult_loss (sort keys, group bounds). It needs
+// the closure's seed order but not H, so it can run on a second stream while
+// the layers run; kg_loss_compute must follow it (same ws) on any stream.
+kg_status kg_loss_groups(const float* H, int32_t d, int32_t n_local, const float* decoder, int32_t R,
+                         const int32_t* tri, const float* labels, int64_t total, int64_t start,
+                         const int64_t* start_dev, int64_t b, const int32_t* order, const int32_t* counts,
+                         float* dH, float* d_decoder, float* loss_out, float* scores_out, uint32_t* flags, void* ws,
+                         int64_t ws_bytes, void* stream) {
+  KG_LOSS_SETUP();
+  return loss_groups(la, n_local, R, order, counts, w, st);
+}
 
-  KG_LAUNCH("k_loss_keys", k_loss_keys, persistent_blocks(b, 256, 8), 256, 0, st, la, rk, rv, vk, vv);
-  KG_CHECK_LAUNCH("k_loss_keys");
-  kg_status s = sort_pairs_u32(rk, rv, b, bits_for((uint64_t)R), sws, sort32_workspace(2 * b), st);
-  if (s != KG_OK) return s;
-  s = sort_pairs_u32(vk, vv, 2 * b, bits_for((uint64_t)n_local), sws, sort32_workspace(2 * b), st);
-  if (s != KG_OK) return s;
-  KG_CUDA(cudaMemsetAsync(wr.nsub, 0, (R + 1) * sizeof(uint32_t), st));
-  KG_CUDA(cudaMemsetAsync(wv.nsub, 0, (ngmax + 1) * sizeof(uint32_t), st));
-  s = seg_reduce<0>(la, rk, rv, b, nullptr, nullptr, R, d_decoder, wr, st);
-  if (s != KG_OK) return s;
-  // seed groups: A_0 = order[0:counts[0]] (ascending, exactly the distinct endpoints)
-  s = seg_reduce<1>(la, vk, vv, 2 * b, order, counts, (int32_t)ngmax, dH, wv, st);
-  return s;
+kg_status kg_loss_compute(const float* H, int32_t d, int32_t n_local, const float* decoder, int32_t R,
+                          const int32_t* tri, const float* labels, int64_t total, int64_t start,
+                          const int64_t* start_dev, int64_t b, const int32_t* order, const int32_t* counts,
+                          float* dH, float* d_decoder, float* loss_out, float* scores_out, uint32_t* flags,
+                          void* ws, int64_t ws_bytes, void* stream) {
+  KG_LOSS_SETUP();
+  return loss_compute(la, R, order, counts, dH, d_decoder, loss_out, flags, w, st);
 }
 
 }  // extern "C"

@@ -260,13 +260,16 @@ def device_forward(model: DeviceModel, bufs: ViewBuffers) -> None:
 
 
 def device_loss(model: DeviceModel, bufs: ViewBuffers, stream, start: int, b: int, grad_flat, loss_out,
-                scores_out=None, start_dev=None) -> None:
+                scores_out=None, start_dev=None, part: str = "all") -> None:
     """DistMult + BCE (ref:model.py:254-281): loss -> loss_out (device scalar),
-    d_decoder -> grad_flat's decoder block, dH_L -> bufs.dH[L] seed rows."""
+    d_decoder -> grad_flat's decoder block, dH_L -> bufs.dH[L] seed rows.
+    part "groups" / "compute" run the two halves separately (the batch-only
+    grouping can overlap the layers on another stream); "all" runs both."""
     cfg = model.config
     L = cfg.num_layers
     ws = bufs.loss_ws(b)
-    _lib.call("kg_distmult_loss", bufs.H[L].data_ptr(), cfg.dims[-1], bufs.n, model.decoder_ptr(),
+    fn = {"all": "kg_distmult_loss", "groups": "kg_loss_groups", "compute": "kg_loss_compute"}[part]
+    _lib.call(fn, bufs.H[L].data_ptr(), cfg.dims[-1], bufs.n, model.decoder_ptr(),
               cfg.num_relations, stream.triples.data_ptr(), stream.labels.data_ptr(), stream.total, start,
               _lib.ptr(start_dev), b,
               bufs.order.data_ptr(), bufs.counts.data_ptr(), bufs.dH[L].data_ptr(),

@@ -345,6 +345,7 @@ class Trainer:
         self.last_timer_handle = None
         self._graphs = {}
         self._graph_pool = None
+        self._loss_stream = torch.cuda.Stream(self.dev)   # batch-only loss grouping, overlaps the layers
         self._eager_rounds = 0
         self.t = 0
         self.round_in_epoch = 0
@@ -362,12 +363,20 @@ class Trainer:
         (all per-round scalars read from device memory)."""
         torch = _torch()
         torch.mul(self.b_dev, self.round_dev, out=self.start_dev)
+        main = torch.cuda.current_stream()
         for i, w in enumerate(self.workers):
             w.closure(self.start_dev[i:i + 1])
-            device_forward(self.model, w.bufs)
             gslot = self.grads_local[i]
+            # fork: key sorts + segment bounds of the loss need only the batch
+            # and the seed order, so they run beside the layers
+            self._loss_stream.wait_stream(main)
+            with torch.cuda.stream(self._loss_stream):
+                device_loss(self.model, w.bufs, w.stream, 0, w.b, gslot, self.loss_scratch[i:i + 1],
+                            start_dev=self.start_dev[i:i + 1], part="groups")
+            device_forward(self.model, w.bufs)
+            main.wait_stream(self._loss_stream)
             device_loss(self.model, w.bufs, w.stream, 0, w.b, gslot, self.loss_scratch[i:i + 1],
-                        start_dev=self.start_dev[i:i + 1])
+                        start_dev=self.start_dev[i:i + 1], part="compute")
             self.losses[i].index_copy_(0, self.round_dev, self.loss_scratch[i:i + 1])
             device_backward(self.model, w.bufs, gslot, input_grad=w.emb)
 
