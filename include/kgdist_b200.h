@@ -236,11 +236,14 @@ kg_status kg_rgcn_forward(const kg_graph_csr* g, const kg_layer_params* lp, cons
 /* ref:model.py:167-185, 286-296: gradients of one layer. dH_out holds
  * dL/dA of the layer output for v in A_t (by local id); H_out (NULL for the
  * last layer) supplies the ReLU mask. Writes d_bases (B,d_in,d_out),
- * d_coeffs (G,B) and, if dH_in != NULL, dL/dH_in for v in A_{t+1}. */
+ * d_coeffs (G,B) and, if dH_in != NULL, dL/dH_in for v in A_{t+1}.
+ * side_stream (optional): d_bases / d_coeffs are then produced on it, off the
+ * dH_in critical path; the caller must order side_stream before reading them
+ * and before reusing ws (one ws per layer). */
 kg_status kg_rgcn_backward(const kg_graph_csr* g, const kg_layer_params* lp, const float* H_in,
                            const float* H_out, const float* dH_out, float* dH_in, const int32_t* vertex_order,
                            const int32_t* pos, const int32_t* counts, int32_t t, float* d_bases,
-                           float* d_coeffs, void* ws, int64_t ws_bytes, void* stream);
+                           float* d_coeffs, void* ws, int64_t ws_bytes, void* stream, void* side_stream);
 /* Dense GEMM of the factored layer (standalone entry for checks):
  * trans 0: C[c_rows(p)] = A[a_rows(p), :K] . B[K, N] (+relu), p < M;
  * trans 1: C[K, N] = sum_{p<M} A[a_rows(p), :K]^T . B[p, :N].

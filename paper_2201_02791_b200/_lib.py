@@ -80,7 +80,7 @@ _PROTOS = {
     "kg_rgcn_forward": (ST, [POINTER(KgGraphCsr), POINTER(KgLayerParams), P, P, P, P, P, c_int32, c_int32,
                              P, c_int64, P]),
     "kg_rgcn_backward": (ST, [POINTER(KgGraphCsr), POINTER(KgLayerParams), P, P, P, P, P, P, P, c_int32,
-                              P, P, P, c_int64, P]),
+                              P, P, P, c_int64, P, P]),
     "kg_gemm_workspace_bytes": (c_int64, [c_int64, c_int64, c_int64]),
     "kg_gemm_f32": (ST, [P, c_int64, P, P, c_int64, P, c_int64, P, c_int64, c_int64, c_int64, c_int32, c_int32,
                          c_int32, P, c_int64, P]),

@@ -662,7 +662,8 @@ struct LayerWs {
   float* ed;      // (e, B)
   float* ed_self; // (n, B)
   float* Rm;      // (d_in, B*d_out)
-  char* gemm;     // packed GEMM operands / split-K partials (GEMMs run back to back)
+  char* gemm;     // packed GEMM operands (main-stream GEMMs run back to back)
+  char* gemm_tn;  // packed operands + split-K partials of dV (may run on the side stream)
 };
 
 static size_t layer_ws(int64_t n, int64_t e, int64_t split_chunks, int di, int dO, int B, LayerWs* w, void* base,
@@ -679,13 +680,22 @@ static size_t layer_ws(int64_t n, int64_t e, int64_t split_chunks, int di, int d
   l.ed = a.take<float>((size_t)e * B);
   l.ed_self = a.take<float>((size_t)n * B);
   l.Rm = a.take<float>((size_t)di * B * dO);
-  size_t gw = gemm_tn_workspace(n, di, (int64_t)B * dO);
+  size_t gw = 0;
   const size_t nn[3] = {gemm_nn_workspace(n, (int64_t)B * di, dO), gemm_nn_workspace(n, di, (int64_t)B * dO),
                         gemm_nn_workspace(n, (int64_t)B * dO, di)};
   for (size_t x : nn) gw = x > gw ? x : gw;
   l.gemm = a.take<char>(gw);
+  l.gemm_tn = a.take<char>(gemm_tn_workspace(n, di, (int64_t)B * dO));
   if (w) *w = l;
   return a.used + 256;
+}
+
+// fork point main -> side stream (record + wait are capture-safe; one event is
+// enough since each wait binds to the most recent record)
+static cudaEvent_t fork_event() {
+  static cudaEvent_t ev = nullptr;
+  if (!ev) cudaEventCreateWithFlags(&ev, cudaEventDisableTiming);
+  return ev;
 }
 
 static Chunks csr_chunks(const kg_graph_csr* G) {
@@ -738,7 +748,7 @@ kg_status kg_rgcn_forward(const kg_graph_csr* G, const kg_layer_params* lp, cons
 kg_status kg_rgcn_backward(const kg_graph_csr* G, const kg_layer_params* lp, const float* H_in, const float* H_out,
                            const float* dH_out, float* dH_in, const int32_t* order, const int32_t* pos,
                            const int32_t* counts, int32_t t, float* d_bases, float* d_coeffs, void* ws,
-                           int64_t ws_bytes, void* stream) {
+                           int64_t ws_bytes, void* stream, void* side_stream) {
   cudaStream_t st = as_stream(stream);
   const int B = lp->B, di = lp->d_in, dO = lp->d_out;
   KG_REQUIRE(B >= 1 && B <= MAXB, KG_ERR_VALIDATION, "num_bases must be in [1, %d]", MAXB);
@@ -763,15 +773,25 @@ kg_status kg_rgcn_backward(const kg_graph_csr* G, const kg_layer_params* lp, con
             counts, t, w.dS, w.ed, w.ed_self, w.partial};
   s = run_csc(c, G, st);
   if (s != KG_OK) return s;
+  // The parameter gradients (dV, d coeffs) feed only the optimizer: with a side
+  // stream they leave the critical path (the caller joins it before the update).
+  cudaStream_t sd = st;
+  if (side_stream) {
+    sd = as_stream(side_stream);
+    KG_CUDA(cudaEventRecord(fork_event(), st));
+    KG_CUDA(cudaStreamWaitEvent(sd, fork_event(), 0));
+  }
   // dV = X^T dS  (reduction over the source rows)
   GemmArgs gv{};
   gv.A = H_in; gv.lda = di; gv.a_rows = order;
   gv.B = w.dS; gv.ldb = (int64_t)B * dO;
   gv.M_dev = counts; gv.M_dev_index = t + 1; gv.M_max = G->n;
   gv.K = di; gv.N = (int64_t)B * dO;
-  s = gemm_tn(gv, w.Rm, w.gemm, st);
+  s = gemm_tn(gv, w.Rm, w.gemm_tn, sd);
   if (s != KG_OK) return s;
-  KG_LAUNCH("k_dbases_layout", k_dbases_layout, persistent_blocks(wn, 256, 2), 256, 0, st, w.Rm, B, di, dO, d_bases);
+  KG_LAUNCH("k_dbases_layout", k_dbases_layout, persistent_blocks(wn, 256, 2), 256, 0, sd, w.Rm, B, di, dO, d_bases);
+  KG_LAUNCH("k_dcoeff_reduce", k_dcoeff_reduce, lp->G, 256, 0, sd, G->rel_ptr, G->rel_perm, G->c_dst, pos, counts, t,
+            w.ed, w.ed_self, lp->G, B, d_coeffs);
   if (dH_in) {
     GemmArgs gx{};
     gx.A = w.dS; gx.lda = (int64_t)B * dO;
@@ -782,8 +802,6 @@ kg_status kg_rgcn_backward(const kg_graph_csr* G, const kg_layer_params* lp, con
     s = gemm_nn(gx, w.gemm, st);
     if (s != KG_OK) return s;
   }
-  KG_LAUNCH("k_dcoeff_reduce", k_dcoeff_reduce, lp->G, 256, 0, st, G->rel_ptr, G->rel_perm, G->c_dst, pos, counts, t,
-            w.ed, w.ed_self, lp->G, B, d_coeffs);
   return KG_OK;
 }
 

@@ -236,8 +236,10 @@ class ViewBuffers:
                                                          config.num_relations)
         self.b_max = b_max
 
-    def layer_ws(self):
-        return self.ws.get("layer", self.layer_ws_bytes)
+    def layer_ws(self, l: int = 0):
+        """Per-layer scratch: a layer's side-stream gradient work may still read
+        its workspace while the next (lower) layer runs."""
+        return self.ws.get(f"layer{l}", self.layer_ws_bytes)
 
     def loss_ws(self, b):
         if b > self.b_max:
@@ -251,9 +253,9 @@ def device_forward(model: DeviceModel, bufs: ViewBuffers) -> None:
     """All layers over the closure in bufs.order/counts (ref:model.py:196-235)."""
     L = model.config.num_layers
     csr = ctypes.byref(bufs.view.csr())
-    ws = bufs.layer_ws()
     st = _lib.stream_handle()
     for l in range(L):
+        ws = bufs.layer_ws(l)
         _lib.call("kg_rgcn_forward", csr, ctypes.byref(model.layer(l)), bufs.H[l].data_ptr(),
                   bufs.H[l + 1].data_ptr(), bufs.order.data_ptr(), bufs.pos.data_ptr(), bufs.counts.data_ptr(),
                   L - 1 - l, 1 if l < L - 1 else 0, ws.data_ptr(), ws.numel(), st)
@@ -278,21 +280,26 @@ def device_loss(model: DeviceModel, bufs: ViewBuffers, stream, start: int, b: in
               ws.numel(), _lib.stream_handle())
 
 
-def device_backward(model: DeviceModel, bufs: ViewBuffers, grad_flat, input_grad: bool) -> None:
+def device_backward(model: DeviceModel, bufs: ViewBuffers, grad_flat, input_grad: bool, side=None) -> None:
     """Layer gradients in reverse (ref:model.py:283-296): d bases / d coeffs
-    into grad_flat, dL/dH_0 rows into bufs.dH[0] when input_grad."""
+    into grad_flat, dL/dH_0 rows into bufs.dH[0] when input_grad. With a side
+    stream (torch.cuda.Stream) the parameter-gradient branch of every layer
+    runs on it; it is joined back into the current stream before returning."""
+    torch = _torch()
     L = model.config.num_layers
     csr = ctypes.byref(bufs.view.csr())
-    ws = bufs.layer_ws()
     st = _lib.stream_handle()
     lay = model.layout
     for l in range(L - 1, -1, -1):
+        ws = bufs.layer_ws(l)
         dh_in = bufs.dH[l].data_ptr() if (l > 0 or input_grad) else 0
         _lib.call("kg_rgcn_backward", csr, ctypes.byref(model.layer(l)), bufs.H[l].data_ptr(),
                   bufs.H[l + 1].data_ptr() if l < L - 1 else 0, bufs.dH[l + 1].data_ptr(), dh_in,
                   bufs.order.data_ptr(), bufs.pos.data_ptr(), bufs.counts.data_ptr(), L - 1 - l,
                   grad_flat.data_ptr() + 4 * lay.bases_off(l), grad_flat.data_ptr() + 4 * lay.coeffs_off(l),
-                  ws.data_ptr(), ws.numel(), st)
+                  ws.data_ptr(), ws.numel(), st, None if side is None else side.cuda_stream)
+    if side is not None:
+        torch.cuda.current_stream().wait_stream(side)
 
 
 def check_flags(bufs: ViewBuffers, what: str = "") -> None:

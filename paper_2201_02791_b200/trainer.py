@@ -378,7 +378,7 @@ class Trainer:
             device_loss(self.model, w.bufs, w.stream, 0, w.b, gslot, self.loss_scratch[i:i + 1],
                         start_dev=self.start_dev[i:i + 1], part="compute")
             self.losses[i].index_copy_(0, self.round_dev, self.loss_scratch[i:i + 1])
-            device_backward(self.model, w.bufs, gslot, input_grad=w.emb)
+            device_backward(self.model, w.bufs, gslot, input_grad=w.emb, side=self._loss_stream)
 
     def _update_body(self):
         """Fused tree-mean + dense Adam/SGD, then lazy sparse rows."""
