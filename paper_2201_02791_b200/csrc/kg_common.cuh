@@ -144,6 +144,11 @@ size_t compact_workspace(int64_t n);
 kg_status compact_flags(const uint32_t* flags, int64_t n, int32_t* out, int32_t* count_out,
                         int32_t out_offset_const, const int32_t* out_offset_dev, void* ws,
                         size_t ws_bytes, cudaStream_t st);
+// Closure-style compaction: out[off + rank(i)] = i for flagged i with off =
+// *off_d (0 if null), pos_out[i] = off + rank(i), *count_abs = off + total,
+// and the flags are cleared for the next use.
+kg_status compact_flags_ex(uint32_t* flags, int64_t n, int32_t* out, const int32_t* off_d, int32_t* count_abs,
+                           int32_t* pos_out, void* ws, size_t ws_bytes, cudaStream_t st);
 
 // Static work-chunk table of a CSR (kg_chunks.cu).
 size_t chunk_workspace(int64_t n);

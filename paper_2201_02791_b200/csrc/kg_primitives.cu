@@ -129,43 +129,96 @@ __global__ void scan_tiles_apply(const uint32_t* __restrict__ in, uint32_t* __re
   if (total && blockIdx.x == gridDim.x - 1 && threadIdx.x == 0) *total = off + tot;
 }
 
-// Small inputs: one CTA walks the tiles with a running carry (1 launch instead
-// of tile sums + recursive scan + apply). With `cout` set it also performs the
-// flag compaction cout[off + rank(i)] = i (flags = in) in the same pass.
-constexpr int64_t SCAN_SINGLE_MAX = 8 * SCAN_TILE;
+// Small inputs: one 1024-thread CTA walks tiles of 8192 values with a running
+// carry (1 launch instead of tile sums + recursive scan + apply). Values are
+// staged through padded shared memory so each thread scans 8 consecutive
+// values in registers. With `c.out` set it also performs the flag compaction
+// c.out[off + rank(i)] = i (flags = in), optionally writing pos_out[i] =
+// off + rank(i), the absolute count off + total, and clearing the flags.
+struct CompactSpec {
+  int32_t* out;              // compaction target (nullptr: plain scan)
+  int32_t off_c;
+  const int32_t* off_d;      // device offset added to off_c (optional)
+  int32_t* count_out;        // total (or off + total when count_abs)
+  int count_abs;
+  int32_t* pos_out;          // inverse map (optional)
+  int clear_flags;           // zero in[] after reading it
+};
 
-__global__ void __launch_bounds__(SCAN_THREADS) scan_single(const uint32_t* __restrict__ in, uint32_t* out,
-                                                            int64_t n, uint32_t* total, int32_t* __restrict__ cout,
-                                                            int32_t off_c, const int32_t* __restrict__ off_d,
-                                                            int32_t* __restrict__ count_out) {
-  __shared__ uint32_t s[SCAN_TILE];
-  const int32_t off = cout ? off_c + (off_d ? *off_d : 0) : 0;
+constexpr int SS_THREADS = 1024;
+constexpr int SS_ITEMS = 8;
+constexpr int SS_TILE = SS_THREADS * SS_ITEMS;
+constexpr int64_t SCAN_SINGLE_MAX = 4 * SS_TILE;
+
+__device__ __forceinline__ int ss_pad(int i) { return i + (i >> 5); }
+
+__global__ void __launch_bounds__(SS_THREADS) scan_single(uint32_t* in, uint32_t* out, int64_t n, uint32_t* total,
+                                                          CompactSpec c) {
+  __shared__ uint32_t s[SS_TILE + SS_TILE / 32 + 1];
+  __shared__ uint32_t wsum[SS_THREADS / 32];
+  const int t = threadIdx.x, lane = t & 31, w = t >> 5;
+  const int32_t off = c.out ? c.off_c + (c.off_d ? *c.off_d : 0) : 0;
   uint32_t carry = 0;
-  for (int64_t base = 0; base < n; base += SCAN_TILE) {
-    uint32_t f[SCAN_ITEMS];
+  for (int64_t base = 0; base < n; base += SS_TILE) {
+    uint32_t f[SS_ITEMS];
 #pragma unroll
-    for (int j = 0; j < SCAN_ITEMS; ++j) {
-      const int64_t i = base + j * SCAN_THREADS + threadIdx.x;
+    for (int j = 0; j < SS_ITEMS; ++j) {
+      const int64_t i = base + j * SS_THREADS + t;
       f[j] = i < n ? in[i] : 0u;
-      s[j * SCAN_THREADS + threadIdx.x] = f[j];
+      if (c.clear_flags && i < n) in[i] = 0u;
+      s[ss_pad(j * SS_THREADS + t)] = f[j];
     }
     __syncthreads();
-    const uint32_t tot = block_scan_tile(s);
+    uint32_t x[SS_ITEMS], run = 0;
 #pragma unroll
-    for (int j = 0; j < SCAN_ITEMS; ++j) {
-      const int64_t i = base + j * SCAN_THREADS + threadIdx.x;
+    for (int j = 0; j < SS_ITEMS; ++j) {
+      x[j] = run;
+      run += s[ss_pad(t * SS_ITEMS + j)];
+    }
+    uint32_t inc = run;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t y = __shfl_up_sync(0xffffffffu, inc, o);
+      if (lane >= o) inc += y;
+    }
+    if (lane == 31) wsum[w] = inc;
+    __syncthreads();
+    if (w == 0) {
+      const uint32_t v = wsum[lane];
+      uint32_t vi = v;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xffffffffu, vi, o);
+        if (lane >= o) vi += y;
+      }
+      wsum[lane] = vi - v;   // exclusive warp offsets; vi of lane 31 = tile total
+      if (lane == 31) s[ss_pad(SS_TILE - 1) + 1] = vi;   // spare slot past the padded tile
+    }
+    __syncthreads();
+    const uint32_t tbase = carry + wsum[w] + inc - run;
+    const uint32_t tile_total = s[ss_pad(SS_TILE - 1) + 1];
+    __syncthreads();
+#pragma unroll
+    for (int j = 0; j < SS_ITEMS; ++j) s[ss_pad(t * SS_ITEMS + j)] = tbase + x[j];
+    __syncthreads();
+#pragma unroll
+    for (int j = 0; j < SS_ITEMS; ++j) {
+      const int64_t i = base + j * SS_THREADS + t;
       if (i < n) {
-        const uint32_t v = s[j * SCAN_THREADS + threadIdx.x] + carry;
+        const uint32_t v = s[ss_pad(j * SS_THREADS + t)];
         if (out) out[i] = v;
-        if (cout && f[j]) cout[off + (int64_t)v] = (int32_t)i;
+        if (c.out && f[j]) {
+          c.out[off + (int64_t)v] = (int32_t)i;
+          if (c.pos_out) c.pos_out[i] = off + (int32_t)v;
+        }
       }
     }
-    carry += tot;
+    carry += tile_total;
     __syncthreads();
   }
-  if (threadIdx.x == 0) {
+  if (t == 0) {
     if (total) *total = carry;
-    if (count_out) *count_out = (int32_t)carry;
+    if (c.count_out) *c.count_out = (c.count_abs ? off : 0) + (int32_t)carry;
   }
 }
 
@@ -187,8 +240,8 @@ kg_status exclusive_scan_u32(const uint32_t* in, uint32_t* out, int64_t n, uint3
     return KG_OK;
   }
   if (n <= SCAN_SINGLE_MAX) {
-    KG_LAUNCH("scan_single", scan_single, 1, SCAN_THREADS, 0, st, in, out, n, total, (int32_t*)nullptr, 0,
-              (const int32_t*)nullptr, (int32_t*)nullptr);
+    KG_LAUNCH("scan_single", scan_single, 1, SS_THREADS, 0, st, const_cast<uint32_t*>(in), out, n, total,
+              CompactSpec{});
     return KG_OK;
   }
   KG_REQUIRE(ws_bytes >= scan_workspace(n), KG_ERR_VALIDATION, "scan workspace too small");
@@ -377,24 +430,26 @@ kg_status sort_pairs_u32(uint32_t* keys, uint32_t* vals, int64_t n, int key_bits
 // ---------------------------------------------------------------------------
 // Flag compaction: out[off + rank(i)] = i for flagged i, ascending.
 // ---------------------------------------------------------------------------
-__global__ void compact_scatter(const uint32_t* __restrict__ flags, const uint32_t* __restrict__ pos, int64_t n,
-                                int32_t* __restrict__ out, int32_t off_c, const int32_t* __restrict__ off_d,
-                                const uint32_t* __restrict__ total, int32_t* __restrict__ count_out) {
-  int32_t off = off_c + (off_d ? *off_d : 0);
+__global__ void compact_scatter(uint32_t* flags, const uint32_t* __restrict__ pos, int64_t n,
+                                const uint32_t* __restrict__ total, CompactSpec c) {
+  const int32_t off = c.off_c + (c.off_d ? *c.off_d : 0);
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
-    if (flags[i]) out[off + pos[i]] = (int32_t)i;
+    if (flags[i]) {
+      c.out[off + pos[i]] = (int32_t)i;
+      if (c.pos_out) c.pos_out[i] = off + (int32_t)pos[i];
+      if (c.clear_flags) flags[i] = 0u;
+    }
   }
-  if (count_out && blockIdx.x == 0 && threadIdx.x == 0) *count_out = (int32_t)*total;
+  if (c.count_out && blockIdx.x == 0 && threadIdx.x == 0) *c.count_out = (c.count_abs ? off : 0) + (int32_t)*total;
 }
 
 size_t compact_workspace(int64_t n) { return align_up(n * sizeof(uint32_t)) + 256 + scan_workspace(n) + 256; }
 
-kg_status compact_flags(const uint32_t* flags, int64_t n, int32_t* out, int32_t* count_out, int32_t off_c,
-                        const int32_t* off_d, void* ws, size_t ws_bytes, cudaStream_t st) {
+static kg_status compact_run(uint32_t* flags, int64_t n, const CompactSpec& c, void* ws, size_t ws_bytes,
+                             cudaStream_t st) {
   KG_REQUIRE(ws_bytes >= compact_workspace(n), KG_ERR_VALIDATION, "compact workspace too small");
   if (n > 0 && n <= SCAN_SINGLE_MAX) {
-    KG_LAUNCH("scan_single", scan_single, 1, SCAN_THREADS, 0, st, flags, (uint32_t*)nullptr, n, (uint32_t*)nullptr,
-              out, off_c, off_d, count_out);
+    KG_LAUNCH("scan_single", scan_single, 1, SS_THREADS, 0, st, flags, (uint32_t*)nullptr, n, (uint32_t*)nullptr, c);
     return KG_OK;
   }
   Arena a(ws, ws_bytes);
@@ -404,9 +459,20 @@ kg_status compact_flags(const uint32_t* flags, int64_t n, int32_t* out, int32_t*
   kg_status s = exclusive_scan_u32(flags, pos, n, total, sws, scan_workspace(n), st);
   if (s != KG_OK) return s;
   int blocks = persistent_blocks(n, 256, 8);
-  KG_LAUNCH("compact_scatter", compact_scatter, blocks, 256, 0, st, flags, pos, n, out, off_c, off_d, total, count_out);
-  KG_CHECK_LAUNCH("compact_scatter");
+  KG_LAUNCH("compact_scatter", compact_scatter, blocks, 256, 0, st, flags, pos, n, total, c);
   return KG_OK;
+}
+
+kg_status compact_flags(const uint32_t* flags, int64_t n, int32_t* out, int32_t* count_out, int32_t off_c,
+                        const int32_t* off_d, void* ws, size_t ws_bytes, cudaStream_t st) {
+  CompactSpec c{out, off_c, off_d, count_out, 0, nullptr, 0};
+  return compact_run(const_cast<uint32_t*>(flags), n, c, ws, ws_bytes, st);
+}
+
+kg_status compact_flags_ex(uint32_t* flags, int64_t n, int32_t* out, const int32_t* off_d, int32_t* count_abs,
+                           int32_t* pos_out, void* ws, size_t ws_bytes, cudaStream_t st) {
+  CompactSpec c{out, 0, off_d, count_abs, 1, pos_out, 1};
+  return compact_run(flags, n, c, ws, ws_bytes, st);
 }
 
 }  // namespace kg

@@ -367,7 +367,9 @@ __global__ void k_stream_gather(const int32_t* __restrict__ pos, int64_t npos, c
 // ---------------------------------------------------------------------------
 // closure
 // ---------------------------------------------------------------------------
-__global__ void k_closure_clear(int32_t* __restrict__ pos, uint32_t* __restrict__ flags, int64_t n) {
+__global__ void k_closure_clear(int32_t* __restrict__ pos, uint32_t* __restrict__ flags, int64_t n,
+                                int32_t* __restrict__ bad) {
+  if (blockIdx.x == 0 && threadIdx.x < 4) bad[threadIdx.x] = 0;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
     pos[i] = -1;
     flags[i] = 0;
@@ -393,14 +395,6 @@ __global__ void k_mark_batch(const int32_t* __restrict__ tri, int64_t total, int
   }
 }
 
-__global__ void k_set_pos(const int32_t* __restrict__ order, const int32_t* __restrict__ counts, int hop,
-                          int32_t* __restrict__ pos) {
-  int32_t lo = hop == 0 ? 0 : counts[hop - 1];
-  int32_t hi = counts[hop];
-  for (int64_t i = lo + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < hi; i += (int64_t)gridDim.x * blockDim.x)
-    pos[order[i]] = (int32_t)i;
-}
-
 // warp per active vertex: flag unplaced sources of its messages
 // warp per static CSR chunk of an active vertex: flag unplaced sources
 __global__ void k_mark_sources(const int32_t* __restrict__ ck_ptr, const int32_t* __restrict__ ck_row,
@@ -421,14 +415,6 @@ __global__ void k_mark_sources(const int32_t* __restrict__ ck_ptr, const int32_t
       if (pos[u] < 0) flags[u] = 1u;
     }
   }
-}
-
-__global__ void k_clear_u32(uint32_t* __restrict__ a, int64_t n) {
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) a[i] = 0;
-}
-
-__global__ void k_counts_next(int32_t* __restrict__ counts, int hop, const int32_t* __restrict__ added) {
-  counts[hop + 1] = counts[hop] + *added;
 }
 
 }  // namespace kg
@@ -611,25 +597,19 @@ kg_status kg_closure(const int32_t* tri, int64_t total, int64_t start, const int
   uint32_t* flags = a.take<uint32_t>(n);
   int32_t* bad = a.take<int32_t>(4);
   char* cws = a.take<char>(compact_workspace(n));
-  int gn = grid_for(n);
-  KG_LAUNCH("k_closure_clear", k_closure_clear, gn, 256, 0, st, pos, flags, n);
-  KG_CUDA(cudaMemsetAsync(bad, 0, 4, st));
+  // pos = -1, flags = 0, bad = 0; every compaction below clears the flags it read
+  KG_LAUNCH("k_closure_clear", k_closure_clear, grid_for(n), 256, 0, st, pos, flags, n, bad);
   KG_LAUNCH("k_mark_batch", k_mark_batch, grid_for(b), 256, 0, st, tri, total, start, start_dev, b, seed_ids, n,
             flags, bad);
-  KG_CHECK_LAUNCH("closure mark");
-  kg_status r = compact_flags(flags, n, order, counts, 0, nullptr, cws, compact_workspace(n), st);
+  // A_0 in ascending id order; pos and counts[0] written by the same pass
+  kg_status r = compact_flags_ex(flags, n, order, nullptr, counts, pos, cws, compact_workspace(n), st);
   if (r != KG_OK) return r;
-  KG_LAUNCH("k_set_pos", k_set_pos, gn, 256, 0, st, order, counts, 0, pos);
   for (int h = 0; h < hops; ++h) {
-    KG_LAUNCH("k_clear_u32", k_clear_u32, gn, 256, 0, st, flags, n);
     KG_LAUNCH("k_mark_sources", k_mark_sources, persistent_blocks(((int64_t)n + G->e / G->chunk + 1) * 32, 256, 8), 256,
               0, st, G->ck_ptr, G->ck_row, G->ck_counts, G->chunk, counts, h, G->indptr, G->src, pos, flags);
-    // append newly reached vertices (ascending) after counts[h]
-    r = compact_flags(flags, n, order, bad + 1, 0, counts + h, cws, compact_workspace(n), st);
+    // append newly reached vertices (ascending) after counts[h]; counts[h+1] = counts[h] + new
+    r = compact_flags_ex(flags, n, order, counts + h, counts + h + 1, pos, cws, compact_workspace(n), st);
     if (r != KG_OK) return r;
-    KG_LAUNCH("k_counts_next", k_counts_next, 1, 1, 0, st, counts, h, bad + 1);
-    KG_LAUNCH("k_set_pos", k_set_pos, gn, 256, 0, st, order, counts, h + 1, pos);
-    KG_CHECK_LAUNCH("closure hop");
   }
   return KG_OK;
 }
