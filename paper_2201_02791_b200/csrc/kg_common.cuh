@@ -100,6 +100,25 @@ __device__ __forceinline__ double warp_sum_d(double v) {
 
 __device__ __forceinline__ unsigned lane_id() { return threadIdx.x & 31u; }
 
+// V consecutive floats (V = 4: 16-byte aligned float4; V = 1: scalar)
+template <int VEC>
+struct VecIO;
+template <>
+struct VecIO<4> {
+  __device__ __forceinline__ static void load(const float* p, float* x) {
+    float4 v = __ldg(reinterpret_cast<const float4*>(p));
+    x[0] = v.x; x[1] = v.y; x[2] = v.z; x[3] = v.w;
+  }
+  __device__ __forceinline__ static void store(float* p, const float* x) {
+    *reinterpret_cast<float4*>(p) = make_float4(x[0], x[1], x[2], x[3]);
+  }
+};
+template <>
+struct VecIO<1> {
+  __device__ __forceinline__ static void load(const float* p, float* x) { x[0] = __ldg(p); }
+  __device__ __forceinline__ static void store(float* p, const float* x) { *p = x[0]; }
+};
+
 // Broadcast from lane 0: tells the compiler the value is warp-uniform, so loops
 // and loads derived from it stay convergent (no collective fallback around the
 // __shfl_sync calls inside per-warp work loops).

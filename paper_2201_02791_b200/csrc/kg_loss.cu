@@ -36,6 +36,7 @@ __device__ __forceinline__ int64_t row_of(const LossArgs& a, int64_t i) {
   return ((a.start_dev ? __ldg(a.start_dev) : a.start) + i) % a.total;
 }
 
+template <bool V4>
 __global__ void __launch_bounds__(256) k_score(LossArgs a) {
   const int lane = lane_id();
   const int warps = (gridDim.x * blockDim.x) >> 5;
@@ -46,7 +47,18 @@ __global__ void __launch_bounds__(256) k_score(LossArgs a) {
     const float* Ht = a.H + (int64_t)t * a.d;
     const float* M = a.dec + (int64_t)r * a.d;
     float s = 0.f;
-    for (int k = lane; k < a.d; k += 32) s = fmaf(Hh[k] * M[k], Ht[k], s);
+    if (V4) {
+      for (int k = 4 * lane; k < a.d; k += 128) {
+        float x[4], m[4], y[4];
+        VecIO<4>::load(Hh + k, x);
+        VecIO<4>::load(M + k, m);
+        VecIO<4>::load(Ht + k, y);
+#pragma unroll
+        for (int c = 0; c < 4; ++c) s = fmaf(x[c] * m[c], y[c], s);
+      }
+    } else {
+      for (int k = lane; k < a.d; k += 32) s = fmaf(Hh[k] * M[k], Ht[k], s);
+    }
     s = warp_sum(s);
     if (lane == 0) {
       float y = a.labels[row];
@@ -216,6 +228,77 @@ __global__ void __launch_bounds__(256) k_sub_partials(LossArgs a, const uint32_t
   }
 }
 
+// float4 lanes (d % 4 == 0, d <= 128): lane l owns features 4l..4l+3; 8 rows
+// of each operand in flight per lane.
+template <int KIND>
+__global__ void __launch_bounds__(256) k_sub_partials_v4(LossArgs a, const uint32_t* __restrict__ vals,
+                                                         const int32_t* __restrict__ lo,
+                                                         const int32_t* __restrict__ hi,
+                                                         const uint32_t* __restrict__ sub_start,
+                                                         const uint32_t* __restrict__ total_sub,
+                                                         const int32_t* __restrict__ ng_dev, int32_t ng_host,
+                                                         float* __restrict__ partial) {
+  const int32_t ng = ng_dev ? *ng_dev : ng_host;
+  const uint32_t S = *total_sub;
+  const int lane = lane_id();
+  const bool on = 4 * lane < a.d;
+  const int warps = (gridDim.x * blockDim.x) >> 5;
+  for (int64_t s = warp_uniform((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5); s < S; s += warps) {
+    int32_t l = 0, h = ng;
+    while (h - l > 1) {
+      int32_t mid = (l + h) >> 1;
+      if (sub_start[mid] <= s) l = mid;
+      else h = mid;
+    }
+    const int32_t g = l;
+    const int64_t r0 = lo[g] + (int64_t)(s - sub_start[g]) * CH;
+    const int64_t r1 = r0 + CH < hi[g] ? r0 + CH : hi[g];
+    float acc[4] = {0.f, 0.f, 0.f, 0.f};
+    for (int64_t base = r0; base < r1; base += 32) {
+      const int cnt = (int)min((int64_t)32, r1 - base);
+      int32_t ra = 0, rb = 0;
+      float my_dg = 0.f;
+      if (lane < cnt) {
+        uint32_t v = vals[base + lane];
+        int64_t ti = (KIND == 1 && v >= a.b) ? v - a.b : v;
+        int64_t row = row_of(a, ti);
+        int32_t hh = a.tri[row * 3], rr = a.tri[row * 3 + 1], tt = a.tri[row * 3 + 2];
+        my_dg = a.dg[ti];
+        if (KIND == 0) {
+          ra = hh;
+          rb = tt;
+        } else {
+          ra = -1 - rr;
+          rb = (v >= a.b) ? hh : tt;
+        }
+      }
+      for (int j = 0; j < cnt; j += 8) {
+        float xa[8][4], xb[8][4], w[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          const int32_t A = __shfl_sync(0xffffffffu, ra, (j + u) & 31);
+          const int32_t Bv = __shfl_sync(0xffffffffu, rb, (j + u) & 31);
+          w[u] = __shfl_sync(0xffffffffu, my_dg, (j + u) & 31);
+          const float* pa = (KIND == 0) ? a.H + (int64_t)A * a.d : a.dec + (int64_t)(-1 - A) * a.d;
+          const float* pb = a.H + (int64_t)Bv * a.d;
+          if (on && j + u < cnt) {
+            VecIO<4>::load(pa + 4 * lane, xa[u]);
+            VecIO<4>::load(pb + 4 * lane, xb[u]);
+          } else {
+#pragma unroll
+            for (int i = 0; i < 4; ++i) xa[u][i] = xb[u][i] = 0.f;
+          }
+        }
+#pragma unroll
+        for (int u = 0; u < 8; ++u)
+#pragma unroll
+          for (int i = 0; i < 4; ++i) acc[i] = fmaf(w[u], xa[u][i] * xb[u][i], acc[i]);
+      }
+    }
+    if (on) VecIO<4>::store(partial + s * (int64_t)a.d + 4 * lane, acc);
+  }
+}
+
 __global__ void k_group_finish(const float* __restrict__ partial, const uint32_t* __restrict__ sub_start,
                                const uint32_t* __restrict__ nsub, const int32_t* __restrict__ ids,
                                const int32_t* __restrict__ ng_dev, int32_t ng_host, int d, float* __restrict__ out) {
@@ -270,7 +353,9 @@ static kg_status seg_sums(const LossArgs& la, const uint32_t* vals, int64_t nele
                           const int32_t* ng_dev, int32_t ng_max, float* out, SegWs& w, cudaStream_t st) {
   int64_t max_sub = nelem / CH + ng_max + 1;
   int pb = persistent_blocks(max_sub * 32, 256, 8);
-  if (la.d <= 32) KG_LAUNCH("k_sub_partials", (k_sub_partials<KIND, 1>), pb, 256, 0, st, la, vals, w.lo, w.hi, w.sub_start, w.total, ng_dev, ng_max, w.partial);
+  const bool v4 = la.d % 4 == 0 && la.d <= 128 && (((uintptr_t)la.H | (uintptr_t)la.dec) & 15) == 0;
+  if (v4) KG_LAUNCH("k_sub_partials", (k_sub_partials_v4<KIND>), pb, 256, 0, st, la, vals, w.lo, w.hi, w.sub_start, w.total, ng_dev, ng_max, w.partial);
+  else if (la.d <= 32) KG_LAUNCH("k_sub_partials", (k_sub_partials<KIND, 1>), pb, 256, 0, st, la, vals, w.lo, w.hi, w.sub_start, w.total, ng_dev, ng_max, w.partial);
   else if (la.d <= 64) KG_LAUNCH("k_sub_partials", (k_sub_partials<KIND, 2>), pb, 256, 0, st, la, vals, w.lo, w.hi, w.sub_start, w.total, ng_dev, ng_max, w.partial);
   else if (la.d <= 128) KG_LAUNCH("k_sub_partials", (k_sub_partials<KIND, 4>), pb, 256, 0, st, la, vals, w.lo, w.hi, w.sub_start, w.total, ng_dev, ng_max, w.partial);
   else if (la.d <= 256) KG_LAUNCH("k_sub_partials", (k_sub_partials<KIND, 8>), pb, 256, 0, st, la, vals, w.lo, w.hi, w.sub_start, w.total, ng_dev, ng_max, w.partial);
@@ -343,7 +428,8 @@ static kg_status loss_compute(const LossArgs& la, int32_t R, const int32_t* orde
                               float* dH, float* d_decoder, float* loss_out, uint32_t* flags, LossWs& w,
                               cudaStream_t st) {
   const int64_t b = la.b;
-  KG_LAUNCH("k_score", k_score, persistent_blocks(b * 32, 256, 8), 256, 0, st, la);
+  const bool v4 = la.d % 4 == 0 && (((uintptr_t)la.H | (uintptr_t)la.dec) & 15) == 0;
+  KG_LAUNCH("k_score", v4 ? k_score<true> : k_score<false>, persistent_blocks(b * 32, 256, 8), 256, 0, st, la);
   int nb = persistent_blocks(b, 256, 4);
   if (nb > 1024) nb = 1024;
   KG_LAUNCH("k_block_sums", k_block_sums, nb, 256, 0, st, w.per, b, w.part);

@@ -105,26 +105,43 @@ __global__ void k_dense_step(StepArgs a) {
   if (__any_sync(0xffffffffu, bad) && lane_id() == 0) atomicOr(a.flags, KG_FLAG_NONFINITE_PARAM);
 }
 
-__global__ void k_sparse_step(float* __restrict__ table, float* __restrict__ m, float* __restrict__ v,
-                              const float* __restrict__ grad, const int32_t* __restrict__ rows,
-                              const int32_t* __restrict__ counts, int k, int d, int adam, float lr, float b1, float b2,
-                              float eps, float inv_bc1, float inv_bc2, const int64_t* __restrict__ step_dev) {
+// Lazy (row-wise) step on the rows of A_k: one warp per row, float4 lanes
+// when the row width allows it.
+template <bool V4>
+__global__ void __launch_bounds__(256) k_sparse_step(float* __restrict__ table, float* __restrict__ m,
+                                                     float* __restrict__ v, const float* __restrict__ grad,
+                                                     const int32_t* __restrict__ rows,
+                                                     const int32_t* __restrict__ counts, int k, int d, int adam,
+                                                     float lr, float b1, float b2, float eps, float inv_bc1,
+                                                     float inv_bc2, const int64_t* __restrict__ step_dev) {
   bias_corrections(step_dev, b1, b2, inv_bc1, inv_bc2);
   const int32_t nrows = counts[k];
-  const int64_t total = (int64_t)nrows * d;
-  for (int64_t x = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; x < total; x += (int64_t)gridDim.x * blockDim.x) {
-    int64_t p = x / d;
-    int j = (int)(x - p * d);
-    int64_t idx = (int64_t)rows[p] * d + j;
-    float g = grad[idx];
-    if (!adam) {
-      table[idx] -= lr * g;
-    } else {
-      float mm = m[idx] * b1 + (1.f - b1) * g;
-      float vv = v[idx] * b2 + (1.f - b2) * g * g;
-      m[idx] = mm;
-      v[idx] = vv;
-      table[idx] -= lr * (mm * inv_bc1) / (sqrtf(vv * inv_bc2) + eps);
+  const int lane = lane_id(), nw = (gridDim.x * blockDim.x) >> 5;
+  constexpr int V = V4 ? 4 : 1;
+  for (int64_t p = warp_uniform((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5); p < nrows; p += nw) {
+    const int64_t base = (int64_t)rows[p] * d;
+    for (int j = lane * V; j < d; j += 32 * V) {
+      const int64_t idx = base + j;
+      float g[V], t[V];
+      VecIO<V>::load(grad + idx, g);
+      VecIO<V>::load(table + idx, t);
+      if (!adam) {
+#pragma unroll
+        for (int i = 0; i < V; ++i) t[i] -= lr * g[i];
+      } else {
+        float mm[V], vv[V];
+        VecIO<V>::load(m + idx, mm);
+        VecIO<V>::load(v + idx, vv);
+#pragma unroll
+        for (int i = 0; i < V; ++i) {
+          mm[i] = mm[i] * b1 + (1.f - b1) * g[i];
+          vv[i] = vv[i] * b2 + (1.f - b2) * g[i] * g[i];
+          t[i] -= lr * (mm[i] * inv_bc1) / (sqrtf(vv[i] * inv_bc2) + eps);
+        }
+        VecIO<V>::store(m + idx, mm);
+        VecIO<V>::store(v + idx, vv);
+      }
+      VecIO<V>::store(table + idx, t);
     }
   }
 }
@@ -176,9 +193,11 @@ kg_status kg_sparse_step(float* table, float* m, float* v, const float* grad, co
                          const int32_t* counts, int32_t k, int32_t d, int32_t optimizer, float lr, float beta1,
                          float beta2, float eps, double bc1, double bc2, const int64_t* step_dev, int32_t n_max,
                          void* stream) {
-  KG_LAUNCH("k_sparse_step", k_sparse_step, persistent_blocks((int64_t)n_max * d, 256, 8), 256, 0, as_stream(stream), 
-      table, m, v, grad, rows, counts, k, d, optimizer == 1, lr, beta1, beta2, eps, (float)(1.0 / bc1),
-      (float)(1.0 / bc2), step_dev);
+  const bool v4 = d % 4 == 0 && (((uintptr_t)table | (uintptr_t)grad | (uintptr_t)m | (uintptr_t)v) & 15) == 0;
+  auto kern = v4 ? k_sparse_step<true> : k_sparse_step<false>;
+  KG_LAUNCH("k_sparse_step", kern, persistent_blocks((int64_t)n_max * 32, 256, 8), 256, 0, as_stream(stream), table,
+            m, v, grad, rows, counts, k, d, optimizer == 1, lr, beta1, beta2, eps, (float)(1.0 / bc1),
+            (float)(1.0 / bc2), step_dev);
   KG_CHECK_LAUNCH("k_sparse_step");
   return KG_OK;
 }

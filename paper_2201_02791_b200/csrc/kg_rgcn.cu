@@ -27,24 +27,6 @@ constexpr int MAXB = 4;
 constexpr int UNR = 8;     // gathered rows in flight per lane
 constexpr int MAXC = 64;   // messages per chunk handled by one warp (2 per lane)
 
-template <int VEC>
-struct VecIO;
-template <>
-struct VecIO<4> {
-  __device__ __forceinline__ static void load(const float* p, float* x) {
-    float4 v = __ldg(reinterpret_cast<const float4*>(p));
-    x[0] = v.x; x[1] = v.y; x[2] = v.z; x[3] = v.w;
-  }
-  __device__ __forceinline__ static void store(float* p, const float* x) {
-    *reinterpret_cast<float4*>(p) = make_float4(x[0], x[1], x[2], x[3]);
-  }
-};
-template <>
-struct VecIO<1> {
-  __device__ __forceinline__ static void load(const float* p, float* x) { x[0] = __ldg(p); }
-  __device__ __forceinline__ static void store(float* p, const float* x) { *p = x[0]; }
-};
-
 // Sum x[0..7] over the 32 lanes of a warp, 9 shuffles: on return lane l holds
 // the total of entry ((l>>4)&1)*4 + ((l>>3)&1)*2 + ((l>>2)&1).
 __device__ __forceinline__ float warp_sum8(const float* x) {
@@ -226,64 +208,92 @@ __global__ void __launch_bounds__(256, 3) k_aggregate(AggArgs a) {
   }
 }
 
-// Rows cut into several chunks: one block (8 warps) per row. Warp w adds the
-// partials of chunks w, w+8, ... in order; the 8 warp sums are added in warp
-// order (fixed summation order), plus the self-loop term. width = B*d floats.
+// Rows cut into several chunks (hubs): one 256-thread block per row. Thread
+// (g, c) sums the partials of chunks g, g + G, ... of V-wide column c (in chunk
+// order); the G group sums are then added in group order — a fixed summation
+// order (deterministic, no atomics) with G-fold parallelism over the chunks.
 constexpr int CB_THREADS = 256;
-constexpr int CB_WARPS = CB_THREADS / 32;
 
-__device__ __forceinline__ void block_sum_partials(const float* __restrict__ partial, int32_t s0, int32_t nparts,
-                                                   int width, int col, float* red /* smem [8][32] */,
-                                                   float& out) {
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  float sum = 0.f;
-  if (col < width) {
-    int32_t k = warp;
-    for (; k + 3 * CB_WARPS < nparts; k += 4 * CB_WARPS) {
-      float x0 = __ldg(partial + (int64_t)(s0 + k) * width + col);
-      float x1 = __ldg(partial + (int64_t)(s0 + k + CB_WARPS) * width + col);
-      float x2 = __ldg(partial + (int64_t)(s0 + k + 2 * CB_WARPS) * width + col);
-      float x3 = __ldg(partial + (int64_t)(s0 + k + 3 * CB_WARPS) * width + col);
-      sum += x0;
-      sum += x1;
-      sum += x2;
-      sum += x3;
-    }
-    for (; k < nparts; k += CB_WARPS) sum += __ldg(partial + (int64_t)(s0 + k) * width + col);
-  }
-  red[warp * 32 + lane] = sum;
-  __syncthreads();
-  float tot = 0.f;
-  if (warp == 0)
+template <int V>
+struct BlockPartialSum {
+  float red[V][CB_THREADS];
+  // returns, for threads with g == 0 and c < ncols, the column total of
+  // V-wide column c0 + c; `valid` tells the caller whether it holds one
+  __device__ __forceinline__ void run(const float* __restrict__ part, int width, int np, int c0, int ncols,
+                                      float* tot, bool& valid) {
+    const int groups = CB_THREADS / ncols;
+    const int g = threadIdx.x / ncols, c = threadIdx.x - g * ncols;
+    float acc[V];
 #pragma unroll
-    for (int w = 0; w < CB_WARPS; ++w) tot += red[w * 32 + lane];
-  __syncthreads();
-  out = tot;
-}
+    for (int i = 0; i < V; ++i) acc[i] = 0.f;
+    if (g < groups) {
+      const float* src = part + (int64_t)(c0 + c) * V;
+      int k = g;
+      for (; k + 3 * groups < np; k += 4 * groups) {
+        float y[4][V];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) VecIO<V>::load(src + (int64_t)(k + u * groups) * width, y[u]);
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+#pragma unroll
+          for (int i = 0; i < V; ++i) acc[i] += y[u][i];
+      }
+      for (; k < np; k += groups) {
+        float y[V];
+        VecIO<V>::load(src + (int64_t)k * width, y);
+#pragma unroll
+        for (int i = 0; i < V; ++i) acc[i] += y[i];
+      }
+    }
+#pragma unroll
+    for (int i = 0; i < V; ++i) red[i][threadIdx.x] = acc[i];
+    __syncthreads();
+    valid = g == 0 && c < ncols;
+    if (valid) {
+#pragma unroll
+      for (int i = 0; i < V; ++i) {
+        float t = red[i][c];
+        for (int q = 1; q < groups; ++q) t += red[i][q * ncols + c];
+        tot[i] = t;
+      }
+    }
+    __syncthreads();
+  }
+};
 
+template <bool V4>
 __global__ void __launch_bounds__(CB_THREADS) k_aggregate_combine(AggArgs a) {
-  __shared__ float red[CB_WARPS * 32];
+  constexpr int V = V4 ? 4 : 1;
+  __shared__ BlockPartialSum<V> bs;
   const int32_t T = a.counts[a.t];
   const int32_t NS = a.ck.counts[2];
-  const int width = a.B * a.d;
+  const int width = a.B * a.d, cols = width / V;
   for (int64_t r = blockIdx.x; r < NS; r += gridDim.x) {
     const int32_t v = a.ck.split[r];
     const int32_t p = a.pos[v];
     if (p < 0 || p >= T) continue;
-    const int32_t c0 = a.ck.ptr[v], c1 = a.ck.ptr[v + 1];
-    const int32_t s0 = a.ck.slot[c0];
-    for (int col0 = 0; col0 < width; col0 += 32) {
-      const int col = col0 + (threadIdx.x & 31);
-      float tot;
-      block_sum_partials(a.partial, s0, c1 - c0, width, col, red, tot);
-      if ((threadIdx.x >> 5) == 0 && col < width) {
-        const int b = col / a.d, k = col % a.d;
-        const float self = a.coeffs[(a.G - 1) * a.B + b] * a.H[(int64_t)v * a.d + k];
-        const float x = tot + self;
-        packed_store<1>(a.acc, a.acc_nk, p, col, &x);
+    const int32_t c0 = a.ck.ptr[v], np = a.ck.ptr[v + 1] - c0;
+    const float* part = a.partial + (int64_t)a.ck.slot[c0] * width;
+    for (int cb = 0; cb < cols; cb += CB_THREADS) {
+      const int ncols = min(CB_THREADS, cols - cb);
+      float tot[V];
+      bool valid;
+      bs.run(part, width, np, cb, ncols, tot, valid);
+      if (valid) {
+        const int col = (cb + (int)threadIdx.x) * V;
+        const int b = col / a.d, kk = col - b * a.d;
+        const float cf = a.coeffs[(a.G - 1) * a.B + b];
+        float h[V], x[V];
+        VecIO<V>::load(a.H + (int64_t)v * a.d + kk, h);
+#pragma unroll
+        for (int i = 0; i < V; ++i) {
+          const float self = cf * h[i];
+          x[i] = tot[i] + self;
+        }
+        packed_store<V>(a.acc, a.acc_nk, p, col, x);
       }
     }
-    if ((threadIdx.x >> 5) == 0) packed_zero_pad(a.acc, a.acc_nk, p, width, threadIdx.x & 31, 32);
+    if (threadIdx.x < 32) packed_zero_pad(a.acc, a.acc_nk, p, width, threadIdx.x, 32);
   }
 }
 
@@ -458,47 +468,57 @@ __global__ void __launch_bounds__(256, 3) k_csc_backward(CscArgs a) {
   }
 }
 
+// Split source rows: one block per row (chunk-order partial sums as in
+// k_aggregate_combine, plus the self-loop term into dS), then the self dots
+// <Y_b[u], dZ[u]> for d a[2R, b] by warp 0.
+template <bool V4>
 __global__ void __launch_bounds__(CB_THREADS) k_csc_combine(CscArgs a) {
-  __shared__ float red[CB_WARPS * 32];
-  __shared__ float dots[MAXB][CB_WARPS];
+  constexpr int V = V4 ? 4 : 1;
+  __shared__ BlockPartialSum<V> bs;
   const int32_t T = a.counts[a.t];
   const int32_t Sn = a.counts[a.t + 1];
   const int32_t NS = a.ck.counts[2];
-  const int width = a.B * a.d;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int width = a.B * a.d, cols = width / V;
   for (int64_t r = blockIdx.x; r < NS; r += gridDim.x) {
     const int32_t u = a.ck.split[r];
     const int32_t q = a.pos[u];
     if (q < 0 || q >= Sn) continue;
-    const int32_t c0 = a.ck.ptr[u], c1 = a.ck.ptr[u + 1];
-    const int32_t s0 = a.ck.slot[c0];
+    const int32_t c0 = a.ck.ptr[u], np = a.ck.ptr[u + 1] - c0;
+    const float* part = a.partial + (int64_t)a.ck.slot[c0] * width;
     const bool self = q < T;
-    for (int col0 = 0; col0 < width; col0 += 32) {
-      const int col = col0 + lane;
-      float tot;
-      block_sum_partials(a.partial, s0, c1 - c0, width, col, red, tot);
-      if (warp == 0 && col < width) {
-        const int b = col / a.d, k = col % a.d;
-        const float z = self ? a.dZ[(int64_t)q * a.d + k] : 0.f;
-        a.dS[(int64_t)q * width + col] = tot + a.coeffs[(a.G - 1) * a.B + b] * z;
+    for (int cb = 0; cb < cols; cb += CB_THREADS) {
+      const int ncols = min(CB_THREADS, cols - cb);
+      float tot[V];
+      bool valid;
+      bs.run(part, width, np, cb, ncols, tot, valid);
+      if (valid) {
+        const int col = (cb + (int)threadIdx.x) * V;
+        const int b = col / a.d, kk = col - b * a.d;
+        float z[V], x[V];
+        if (self) VecIO<V>::load(a.dZ + (int64_t)q * a.d + kk, z);
+        else
+#pragma unroll
+          for (int i = 0; i < V; ++i) z[i] = 0.f;
+        const float cf = a.coeffs[(a.G - 1) * a.B + b];
+#pragma unroll
+        for (int i = 0; i < V; ++i) x[i] = tot[i] + cf * z[i];
+        VecIO<V>::store(a.dS + (int64_t)q * width + col, x);
       }
     }
-    // self dots <Y_b[u], dZ[u]> (fixed order: lanes over k, then warp tree)
-    if (self) {
+    if (self && threadIdx.x < 32) {
+      const int lane = threadIdx.x;
       for (int b = 0; b < a.B; ++b) {
         float dp = 0.f;
-        for (int k = threadIdx.x; k < a.d; k += CB_THREADS)
-          dp = fmaf(a.Y[((int64_t)q * a.B + b) * a.d + k], a.dZ[(int64_t)q * a.d + k], dp);
+        for (int k = lane * V; k < a.d; k += 32 * V) {
+          float y[V], z[V];
+          VecIO<V>::load(a.Y + ((int64_t)q * a.B + b) * a.d + k, y);
+          VecIO<V>::load(a.dZ + (int64_t)q * a.d + k, z);
+#pragma unroll
+          for (int i = 0; i < V; ++i) dp = fmaf(y[i], z[i], dp);
+        }
         dp = warp_sum(dp);
-        if (lane == 0) dots[b][warp] = dp;
+        if (lane == 0) a.ed_self[(int64_t)q * a.B + b] = dp;
       }
-      __syncthreads();
-      if (threadIdx.x < a.B) {
-        float s = 0.f;
-        for (int w = 0; w < CB_WARPS; ++w) s += dots[threadIdx.x][w];
-        a.ed_self[(int64_t)q * a.B + threadIdx.x] = s;
-      }
-      __syncthreads();
     }
   }
 }
@@ -544,18 +564,27 @@ __global__ void __launch_bounds__(256) k_dcoeff_reduce(const int32_t* __restrict
   if (threadIdx.x < B) d_coeffs[g * B + threadIdx.x] = red[threadIdx.x][0];
 }
 
-// dZ[p] = dH[v_p] * (H_out[v_p] > 0) (mask skipped when H_out == nullptr)
-__global__ void k_dz(const float* __restrict__ dH, const float* __restrict__ Hout, const int32_t* __restrict__ order,
-                     const int32_t* __restrict__ counts, int t, int d, float* __restrict__ dZ) {
+// dZ[p] = dH[v_p] * (H_out[v_p] > 0) (mask skipped when H_out == nullptr); warp per row
+template <bool V4>
+__global__ void __launch_bounds__(256) k_dz(const float* __restrict__ dH, const float* __restrict__ Hout,
+                                            const int32_t* __restrict__ order, const int32_t* __restrict__ counts,
+                                            int t, int d, float* __restrict__ dZ) {
   const int32_t T = counts[t];
-  const int64_t total = (int64_t)T * d;
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
-    int64_t p = i / d;
-    int k = (int)(i - p * d);
-    int64_t src = (int64_t)order[p] * d + k;
-    float g = dH[src];
-    if (Hout && !(Hout[src] > 0.f)) g = 0.f;
-    dZ[i] = g;
+  const int lane = lane_id(), nw = (gridDim.x * blockDim.x) >> 5;
+  constexpr int V = V4 ? 4 : 1;
+  for (int64_t p = warp_uniform((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5); p < T; p += nw) {
+    const int64_t src = (int64_t)order[p] * d;
+    for (int k = lane * V; k < d; k += 32 * V) {
+      float g[V], h[V];
+      VecIO<V>::load(dH + src + k, g);
+      if (Hout) {
+        VecIO<V>::load(Hout + src + k, h);
+#pragma unroll
+        for (int i = 0; i < V; ++i)
+          if (!(h[i] > 0.f)) g[i] = 0.f;
+      }
+      VecIO<V>::store(dZ + p * d + k, g);
+    }
   }
 }
 
@@ -599,7 +628,8 @@ static kg_status launch_agg(const AggArgs& a, int blocks, int cblocks, size_t sm
     case 3: KG_LAUNCH("k_aggregate", (k_aggregate<3, VEC, S>), blocks, 256, smem, st, a); break;
     default: KG_LAUNCH("k_aggregate", (k_aggregate<4, VEC, S>), blocks, 256, smem, st, a); break;
   }
-  KG_LAUNCH("k_aggregate_combine", k_aggregate_combine, cblocks, CB_THREADS, 0, st, a);
+  if (a.d % 4 == 0) KG_LAUNCH("k_aggregate_combine", k_aggregate_combine<true>, cblocks, CB_THREADS, 0, st, a);
+  else KG_LAUNCH("k_aggregate_combine", k_aggregate_combine<false>, cblocks, CB_THREADS, 0, st, a);
   return KG_OK;
 }
 template <int VEC, int S>
@@ -610,7 +640,8 @@ static kg_status launch_csc(const CscArgs& a, int blocks, int cblocks, size_t sm
     case 3: KG_LAUNCH("k_csc_backward", (k_csc_backward<3, VEC, S>), blocks, 256, smem, st, a); break;
     default: KG_LAUNCH("k_csc_backward", (k_csc_backward<4, VEC, S>), blocks, 256, smem, st, a); break;
   }
-  KG_LAUNCH("k_csc_combine", k_csc_combine, cblocks, CB_THREADS, 0, st, a);
+  if (a.d % 4 == 0) KG_LAUNCH("k_csc_combine", k_csc_combine<true>, cblocks, CB_THREADS, 0, st, a);
+  else KG_LAUNCH("k_csc_combine", k_csc_combine<false>, cblocks, CB_THREADS, 0, st, a);
   return KG_OK;
 }
 
@@ -628,7 +659,7 @@ static kg_status dispatch_width(int d, F4 f4, F1a f1, F1b f2, F1c f4s, F1d f8) {
 static kg_status run_aggregate(const AggArgs& a, const kg_graph_csr* G, cudaStream_t st) {
   KG_REQUIRE(G->chunk <= MAXC, KG_ERR_VALIDATION, "chunk size %d > %d", G->chunk, MAXC);
   int blocks = persistent_blocks(cap_chunks(G) * 32, 256, 3);
-  int cblocks = (int)(cap_split_rows(G) < num_sms() * 8 ? cap_split_rows(G) : num_sms() * 8);
+  int cblocks = persistent_blocks(cap_split_rows(G) * CB_THREADS, CB_THREADS, 8);   // one block per split row
   size_t smem = (size_t)a.G * a.B * sizeof(float);
   return dispatch_width(
       a.d, [&] { return launch_agg<4, 1>(a, blocks, cblocks, smem, st); },
@@ -641,7 +672,7 @@ static kg_status run_aggregate(const AggArgs& a, const kg_graph_csr* G, cudaStre
 static kg_status run_csc(const CscArgs& a, const kg_graph_csr* G, cudaStream_t st) {
   KG_REQUIRE(G->chunk <= MAXC, KG_ERR_VALIDATION, "chunk size %d > %d", G->chunk, MAXC);
   int blocks = persistent_blocks(cap_chunks(G) * 32, 256, 3);
-  int cblocks = (int)(cap_split_rows(G) < num_sms() * 8 ? cap_split_rows(G) : num_sms() * 8);
+  int cblocks = persistent_blocks(cap_split_rows(G) * CB_THREADS, CB_THREADS, 8);   // one block per split row
   size_t smem = (size_t)a.G * a.B * sizeof(float);
   return dispatch_width(
       a.d, [&] { return launch_csc<4, 1>(a, blocks, cblocks, smem, st); },
@@ -758,8 +789,12 @@ kg_status kg_rgcn_backward(const kg_graph_csr* G, const kg_layer_params* lp, con
   const int64_t wn = (int64_t)B * di * dO;
   KG_LAUNCH("k_weight_views", k_weight_views, persistent_blocks(wn, 256, 2), 256, 0, st, lp->bases, B, di, dO, w.Wy,
             w.Wb);
-  KG_LAUNCH("k_dz", k_dz, persistent_blocks((int64_t)G->n * dO, 256, 8), 256, 0, st, dH_out, H_out, order, counts, t,
-            dO, w.dZ);
+  if (dO % 4 == 0)
+    KG_LAUNCH("k_dz", k_dz<true>, persistent_blocks((int64_t)G->n * 32, 256, 8), 256, 0, st, dH_out, H_out, order,
+              counts, t, dO, w.dZ);
+  else
+    KG_LAUNCH("k_dz", k_dz<false>, persistent_blocks((int64_t)G->n * 32, 256, 8), 256, 0, st, dH_out, H_out, order,
+              counts, t, dO, w.dZ);
   // Y = X[A_{t+1}] . [V_0 | .. | V_{B-1}]
   GemmArgs gy{};
   gy.A = H_in; gy.lda = di; gy.a_rows = order;
