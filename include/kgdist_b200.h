@@ -100,6 +100,10 @@ typedef struct kg_layer_params {
   int32_t d_in, d_out, B, G; /* G = 2R + 1 relation groups                 */
   const float* bases;        /* (B, d_in, d_out)                           */
   const float* coeffs;       /* (G, B)                                     */
+  /* Optional: the bases as tensor-core operand records written by
+   * kg_rgcn_pack_weights from the CURRENT bases (repack after every update);
+   * NULL = forward/backward pack them on the fly. */
+  const float* packed;
 } kg_layer_params;
 
 /* ---------------------------------------------------------------------- */
@@ -129,6 +133,18 @@ kg_status kg_kernel_timer_read(int64_t handle, double* total_ms, int64_t* launch
 int64_t kg_sort_workspace_bytes(int64_t n);
 kg_status kg_sort_pairs_u64(uint64_t* keys, uint32_t* vals, int64_t n, int key_bits, void* ws,
                             int64_t ws_bytes, void* stream);
+/* Round-indexed copies (<= 16 segments, one launch): segment i copies
+ * `bytes` from src + r*src_round_stride to dst + r*dst_round_stride with
+ * r = *round_dev (device int64, e.g. inside a CUDA graph) or round_host. */
+typedef struct kg_copy_seg {
+  void* dst;
+  const void* src;
+  int64_t bytes;
+  int64_t dst_round_stride;
+  int64_t src_round_stride;
+} kg_copy_seg;
+kg_status kg_copy_segments(const kg_copy_seg* segs, int32_t n, const int64_t* round_dev, int64_t round_host,
+                           void* stream);
 int64_t kg_scan_workspace_bytes(int64_t n);
 kg_status kg_exclusive_scan_u32(const uint32_t* in, uint32_t* out, int64_t n, uint32_t* total, void* ws,
                                 int64_t ws_bytes, void* stream);
@@ -232,7 +248,10 @@ int64_t kg_layer_workspace_bytes(const kg_graph_csr* g, int32_t d_in, int32_t d_
  * H_out[v] = relu(Z) (relu != 0) or Z. H_in/H_out rows indexed by local id. */
 kg_status kg_rgcn_forward(const kg_graph_csr* g, const kg_layer_params* lp, const float* H_in, float* H_out,
                           const int32_t* vertex_order, const int32_t* pos, const int32_t* counts, int32_t t,
-                          int32_t relu, void* ws, int64_t ws_bytes, void* stream);
+                          int32_t relu, float* H_out_packed, void* ws, int64_t ws_bytes, void* stream);
+/* H_out_packed (optional, kg_pack_rows_bytes(n, d_out)): the output rows by
+ * position p < counts[t] also as tensor-core operand records — exactly what
+ * the next layer's kg_rgcn_backward takes as H_in_packed. */
 /* ref:model.py:167-185, 286-296: gradients of one layer. dH_out holds
  * dL/dA of the layer output for v in A_t (by local id); H_out (NULL for the
  * last layer) supplies the ReLU mask. Writes d_bases (B,d_in,d_out),
@@ -243,7 +262,18 @@ kg_status kg_rgcn_forward(const kg_graph_csr* g, const kg_layer_params* lp, cons
 kg_status kg_rgcn_backward(const kg_graph_csr* g, const kg_layer_params* lp, const float* H_in,
                            const float* H_out, const float* dH_out, float* dH_in, const int32_t* vertex_order,
                            const int32_t* pos, const int32_t* counts, int32_t t, float* d_bases,
-                           float* d_coeffs, void* ws, int64_t ws_bytes, void* stream, void* side_stream);
+                           float* d_coeffs, const float* H_in_packed, void* ws, int64_t ws_bytes, void* stream,
+                           void* side_stream);
+/* H_in_packed (optional): H_in[vertex_order[p]], p < counts[t+1], as operand
+ * records (the previous layer's H_out_packed, or kg_pack_rows). */
+int64_t kg_pack_rows_bytes(int64_t rows, int64_t cols);
+kg_status kg_pack_rows(const float* src, int64_t ld, const int32_t* rowid, const int32_t* counts,
+                       int32_t count_index, int64_t n_max, int64_t cols, float* out, void* stream);
+/* Pre-pack the three tensor-core weight operands of one layer (forward
+ * Z = acc.V, backward Y = X.[V_b] and dX = dS.[V_b]^T) into `out`
+ * (kg_rgcn_weights_bytes); set lp->packed = out for the calls that follow. */
+int64_t kg_rgcn_weights_bytes(int32_t d_in, int32_t d_out, int32_t B);
+kg_status kg_rgcn_pack_weights(const kg_layer_params* lp, float* out, void* stream);
 /* Dense GEMM of the factored layer (standalone entry for checks):
  * trans 0: C[c_rows(p)] = A[a_rows(p), :K] . B[K, N] (+relu), p < M;
  * trans 1: C[K, N] = sum_{p<M} A[a_rows(p), :K]^T . B[p, :N].
@@ -262,6 +292,11 @@ kg_status kg_distmult_loss(const float* H, int32_t d, int32_t n_local, const flo
                            float* dH,
                            float* d_decoder, float* loss_out, float* scores_out, uint32_t* flags, void* ws,
                            int64_t ws_bytes, void* stream);
+/* The batch-derived fields kg_loss_groups leaves in ws (sorted values and
+ * segment bounds), as (pointer, bytes) pairs; returns their count (<= max).
+ * A trainer may precompute them for every round and copy them back in. */
+int32_t kg_loss_group_fields(void* ws, int64_t ws_bytes, int64_t b, int32_t n_local, int32_t d, int32_t R,
+                             void** ptrs, int64_t* bytes, int32_t max);
 /* kg_distmult_loss in two halves with identical arguments and workspace:
  * kg_loss_groups only sorts the batch keys and builds the segment bounds
  * (needs the closure's seed order, not H), so a trainer can run it on a

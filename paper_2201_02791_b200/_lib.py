@@ -37,7 +37,12 @@ class KgGraphCsr(ctypes.Structure):
 
 class KgLayerParams(ctypes.Structure):
     _fields_ = [("d_in", c_int32), ("d_out", c_int32), ("B", c_int32), ("G", c_int32),
-                ("bases", c_void_p), ("coeffs", c_void_p)]
+                ("bases", c_void_p), ("coeffs", c_void_p), ("packed", c_void_p)]
+
+
+class KgCopySeg(ctypes.Structure):
+    _fields_ = [("dst", c_void_p), ("src", c_void_p), ("bytes", c_int64), ("dst_round_stride", c_int64),
+                ("src_round_stride", c_int64)]
 
 
 P = c_void_p
@@ -53,6 +58,9 @@ _PROTOS = {
     "kg_kernel_timer_dump": (ST, [ctypes.c_char_p, c_int64]),
     "kg_kernel_timer_detach": (ST, [POINTER(c_int64)]),
     "kg_kernel_timer_read": (ST, [c_int64, POINTER(c_double), POINTER(c_int64)]),
+    "kg_copy_segments": (ST, [POINTER(KgCopySeg), c_int32, P, c_int64, P]),
+    "kg_loss_group_fields": (c_int32, [P, c_int64, c_int64, c_int32, c_int32, c_int32, POINTER(c_void_p),
+                                       POINTER(c_int64), c_int32]),
     "kg_sort_workspace_bytes": (c_int64, [c_int64]),
     "kg_sort_pairs_u64": (ST, [P, P, c_int64, c_int, P, c_int64, P]),
     "kg_scan_workspace_bytes": (c_int64, [c_int64]),
@@ -78,9 +86,13 @@ _PROTOS = {
                         c_int64, P]),
     "kg_layer_workspace_bytes": (c_int64, [POINTER(KgGraphCsr), c_int32, c_int32, c_int32]),
     "kg_rgcn_forward": (ST, [POINTER(KgGraphCsr), POINTER(KgLayerParams), P, P, P, P, P, c_int32, c_int32,
-                             P, c_int64, P]),
+                             P, P, c_int64, P]),
     "kg_rgcn_backward": (ST, [POINTER(KgGraphCsr), POINTER(KgLayerParams), P, P, P, P, P, P, P, c_int32,
-                              P, P, P, c_int64, P, P]),
+                              P, P, P, P, c_int64, P, P]),
+    "kg_pack_rows_bytes": (c_int64, [c_int64, c_int64]),
+    "kg_pack_rows": (ST, [P, c_int64, P, P, c_int32, c_int64, c_int64, P, P]),
+    "kg_rgcn_weights_bytes": (c_int64, [c_int32, c_int32, c_int32]),
+    "kg_rgcn_pack_weights": (ST, [POINTER(KgLayerParams), P, P]),
     "kg_gemm_workspace_bytes": (c_int64, [c_int64, c_int64, c_int64]),
     "kg_gemm_f32": (ST, [P, c_int64, P, P, c_int64, P, c_int64, P, c_int64, c_int64, c_int64, c_int32, c_int32,
                          c_int32, P, c_int64, P]),

@@ -20,6 +20,8 @@ struct GemmArgs {
   int64_t N;
   int relu;
   const float* a_packed;   // NN only: A already in hi/lo records (see packed_store), a_rows ignored
+  const float* b_packed;   // NN only: B already in records (N_pad rows, one block; kg_rgcn_pack_weights)
+  float* c_packed;         // NN only, optional: the output also as A records by MMA row (K = N)
 };
 
 // --- packed tensor-core operand records (kg_umma.cu) -----------------------

@@ -439,6 +439,23 @@ static kg_status loss_compute(const LossArgs& la, int32_t R, const int32_t* orde
   return seg_sums<1>(la, w.vv, 2 * b, order, counts, (int32_t)w.ngmax, dH, w.wv, st);
 }
 
+int32_t kg_loss_group_fields(void* ws, int64_t ws_bytes, int64_t b, int32_t n_local, int32_t d, int32_t R,
+                             void** ptrs, int64_t* bytes, int32_t max) {
+  LossWs w;
+  if (loss_arena(ws, (size_t)ws_bytes, b, n_local, d, R, &w) > (size_t)ws_bytes) return -1;
+  const int64_t nr = (int64_t)R + 1, nv = w.ngmax + 1;
+  void* p[] = {w.rv, w.vv, w.wr.lo, w.wr.hi, w.wr.nsub, w.wr.sub_start, w.wr.total,
+               w.wv.lo, w.wv.hi, w.wv.nsub, w.wv.sub_start, w.wv.total};
+  const int64_t sz[] = {4 * b, 8 * b, 4 * nr, 4 * nr, 4 * nr, 4 * nr, 16, 4 * nv, 4 * nv, 4 * nv, 4 * nv, 16};
+  const int32_t n = (int32_t)(sizeof(sz) / sizeof(sz[0]));
+  if (n > max) return -1;
+  for (int32_t i = 0; i < n; ++i) {
+    ptrs[i] = p[i];
+    bytes[i] = sz[i];
+  }
+  return n;
+}
+
 int64_t kg_loss_workspace_bytes(int64_t b, int32_t n, int32_t d, int32_t R) {
   return (int64_t)loss_arena(nullptr, 0, b, n, d, R, nullptr);
 }

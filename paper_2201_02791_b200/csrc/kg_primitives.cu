@@ -475,6 +475,35 @@ kg_status compact_flags_ex(uint32_t* flags, int64_t n, int32_t* out, const int32
   return compact_run(flags, n, c, ws, ws_bytes, st);
 }
 
+// Round-indexed segment copy: seg i copies bytes from src + r*src_stride to
+// dst + r*dst_stride, r = *round_dev (device) or round_host. One launch moves
+// a round's precomputed closure / grouping into the fixed working buffers.
+constexpr int KG_MAX_SEGS = 16;
+struct SegList {
+  kg_copy_seg seg[KG_MAX_SEGS];
+  int n;
+};
+
+__global__ void __launch_bounds__(256) k_copy_segments(SegList L, const int64_t* __restrict__ round_dev,
+                                                       int64_t round_host) {
+  const int64_t r = round_dev ? *round_dev : round_host;
+  for (int i = 0; i < L.n; ++i) {
+    const kg_copy_seg& g = L.seg[i];
+    const char* src = static_cast<const char*>(g.src) + r * g.src_round_stride;
+    char* dst = static_cast<char*>(g.dst) + r * g.dst_round_stride;
+    const bool v16 = (((uintptr_t)src | (uintptr_t)dst | (uintptr_t)g.bytes) & 15) == 0;
+    if (v16) {
+      const int64_t n = g.bytes / 16;
+      for (int64_t x = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; x < n; x += (int64_t)gridDim.x * blockDim.x)
+        reinterpret_cast<int4*>(dst)[x] = reinterpret_cast<const int4*>(src)[x];
+    } else {
+      for (int64_t x = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; x < g.bytes;
+           x += (int64_t)gridDim.x * blockDim.x)
+        dst[x] = src[x];
+    }
+  }
+}
+
 }  // namespace kg
 
 // ---------------------------------------------------------------------------
@@ -483,6 +512,22 @@ kg_status compact_flags_ex(uint32_t* flags, int64_t n, int32_t* out, const int32
 extern "C" {
 
 int kg_abi_version(void) { return KG_ABI_VERSION; }
+
+kg_status kg_copy_segments(const kg_copy_seg* segs, int32_t n, const int64_t* round_dev, int64_t round_host,
+                           void* stream) {
+  KG_REQUIRE(n >= 0 && n <= kg::KG_MAX_SEGS, KG_ERR_VALIDATION, "at most %d segments", kg::KG_MAX_SEGS);
+  if (n == 0) return KG_OK;
+  kg::SegList L{};
+  int64_t most = 0;
+  for (int i = 0; i < n; ++i) {
+    L.seg[i] = segs[i];
+    most = segs[i].bytes > most ? segs[i].bytes : most;
+  }
+  L.n = n;
+  KG_LAUNCH("k_copy_segments", kg::k_copy_segments, kg::persistent_blocks(most / 16 + 1, 256, 2), 256, 0,
+            kg::as_stream(stream), L, round_dev, round_host);
+  return KG_OK;
+}
 
 int kg_last_error(char* buf, int64_t n) {
   if (buf && n > 0) {

@@ -314,6 +314,8 @@ struct CscArgs {
   float* ed;             // (e, B) per CSC position
   float* ed_self;        // (count_T, B)
   float* partial;        // (split chunks, B*d)
+  float* dS_pk;          // optional: dS also as packed GEMM A records (dX = dS . Wb)
+  int64_t dS_nk;
 };
 
 template <int NB, int VEC, int S>
@@ -456,6 +458,15 @@ __global__ void __launch_bounds__(256, 3) k_csc_backward(CscArgs a) {
         }
       }
       out = a.dS + (int64_t)q * B * d;
+      if (a.dS_pk) {
+#pragma unroll
+        for (int b = 0; b < NB; ++b)
+          if (b < B)
+#pragma unroll
+            for (int s = 0; s < S; ++s)
+              if (slot_ok[s]) packed_store<VEC>(a.dS_pk, a.dS_nk, q, b * d + (s * 32 + lane) * VEC, acc[b][s]);
+        packed_zero_pad(a.dS_pk, a.dS_nk, q, B * d, lane, 32);
+      }
     } else {
       out = a.partial + (int64_t)a.ck.slot[c] * B * d;
     }
@@ -503,8 +514,10 @@ __global__ void __launch_bounds__(CB_THREADS) k_csc_combine(CscArgs a) {
 #pragma unroll
         for (int i = 0; i < V; ++i) x[i] = tot[i] + cf * z[i];
         VecIO<V>::store(a.dS + (int64_t)q * width + col, x);
+        if (a.dS_pk) packed_store<V>(a.dS_pk, a.dS_nk, q, col, x);
       }
     }
+    if (a.dS_pk && threadIdx.x < 32) packed_zero_pad(a.dS_pk, a.dS_nk, q, width, threadIdx.x, 32);
     if (self && threadIdx.x < 32) {
       const int lane = threadIdx.x;
       for (int b = 0; b < a.B; ++b) {
@@ -613,6 +626,61 @@ __global__ void k_dbases_layout(const float* __restrict__ Rm, int B, int di, int
   }
 }
 
+// Tensor-core B operands of one layer, packed once per optimizer step:
+//   fwd  (B*d_in x d_out)  Z = acc . [V_b]      element (o, b*d_in+i)
+//   y    (d_in x B*d_out)  Y = X . [V_0|..]     element (b*d_out+o, i)
+//   dx   (B*d_out x d_in)  dX = dS . [V_b]^T    element (i, b*d_out+o)
+// each as records of R = pad16(N) rows x 16 K values (pads zero).
+struct WeightsLayout {
+  int64_t off[3], rows[3], nk[3], total;
+};
+
+static WeightsLayout weights_layout(int di, int dO, int B) {
+  WeightsLayout w;
+  const int64_t N[3] = {dO, (int64_t)B * dO, di}, K[3] = {(int64_t)B * di, di, (int64_t)B * dO};
+  int64_t o = 0;
+  for (int j = 0; j < 3; ++j) {
+    w.rows[j] = (N[j] + 15) / 16 * 16;
+    w.nk[j] = packed_records(K[j]);
+    w.off[j] = o;
+    o += (w.rows[j] * w.nk[j] * 2 * PK_K + 63) / 64 * 64;   // 256-byte aligned sections
+  }
+  w.total = o;
+  return w;
+}
+
+__global__ void k_pack_weights(const float* __restrict__ V, int B, int di, int dO, WeightsLayout L,
+                               float* __restrict__ out) {
+  const int j = blockIdx.y;
+  const int64_t R = L.rows[j], nk = L.nk[j], count = R * nk * PK_K;
+  for (int64_t x = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; x < count; x += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t kc = x / (R * PK_K);
+    const int rem = (int)(x - kc * R * PK_K);
+    const int n = rem / PK_K, kk = rem - n * PK_K;
+    const int64_t k = kc * PK_K + kk;
+    float val = 0.f;
+    if (j == 0) {          // (o = n, b*di + i = k)
+      if (n < dO && k < (int64_t)B * di) val = V[k * dO + n];
+    } else if (j == 1) {   // (b*dO + o = n, i = k)
+      if (n < B * dO && k < di) {
+        const int b = n / dO, o = n - b * dO;
+        val = V[((int64_t)b * di + k) * dO + o];
+      }
+    } else {               // (i = n, b*dO + o = k)
+      if (n < di && k < (int64_t)B * dO) {
+        const int b = (int)(k / dO), o = (int)(k - (int64_t)b * dO);
+        val = V[((int64_t)b * di + n) * dO + o];
+      }
+    }
+    float hi, lo;
+    split_tf32(val, hi, lo);
+    float* rec = out + L.off[j] + kc * 2 * R * PK_K;
+    const int64_t off = ((kk >> 2) * (R >> 3) + (n >> 3)) * 32 + (n & 7) * 4 + (kk & 3);
+    rec[off] = hi;
+    rec[R * PK_K + off] = lo;
+  }
+}
+
 static bool vec4_ok(int d) { return d % 4 == 0 && d <= 128; }
 
 // chunk capacities of kg_graph_csr (see the header)
@@ -690,6 +758,7 @@ struct LayerWs {
   float* dZ;      // (n, d_out)
   float* Y;       // (n, B*d_out)
   float* dS;      // (n, B*d_out)
+  float* dS_pk;   // dS as packed GEMM A records
   float* ed;      // (e, B)
   float* ed_self; // (n, B)
   float* Rm;      // (d_in, B*d_out)
@@ -708,6 +777,7 @@ static size_t layer_ws(int64_t n, int64_t e, int64_t split_chunks, int di, int d
   l.dZ = a.take<float>((size_t)n * dO);
   l.Y = a.take<float>((size_t)n * B * dO);
   l.dS = a.take<float>((size_t)n * B * dO);
+  l.dS_pk = a.take<float>(packed_bytes(n, (int64_t)B * dO) / sizeof(float));
   l.ed = a.take<float>((size_t)e * B);
   l.ed_self = a.take<float>((size_t)n * B);
   l.Rm = a.take<float>((size_t)di * B * dO);
@@ -748,7 +818,7 @@ int64_t kg_layer_workspace_bytes(const kg_graph_csr* G, int32_t d_in, int32_t d_
 
 kg_status kg_rgcn_forward(const kg_graph_csr* G, const kg_layer_params* lp, const float* H_in, float* H_out,
                           const int32_t* order, const int32_t* pos, const int32_t* counts, int32_t t, int32_t relu,
-                          void* ws, int64_t ws_bytes, void* stream) {
+                          float* H_out_packed, void* ws, int64_t ws_bytes, void* stream) {
   cudaStream_t st = as_stream(stream);
   KG_REQUIRE(lp->B >= 1 && lp->B <= MAXB, KG_ERR_VALIDATION, "num_bases must be in [1, %d]", MAXB);
   KG_REQUIRE(lp->G == 2 * G->R + 1, KG_ERR_SHAPE, "coeff groups %d != 2R+1", lp->G);
@@ -773,13 +843,15 @@ kg_status kg_rgcn_forward(const kg_graph_csr* G, const kg_layer_params* lp, cons
   g.K = (int64_t)lp->B * lp->d_in;
   g.N = lp->d_out;
   g.relu = relu;
+  if (lp->packed) g.b_packed = lp->packed + weights_layout(lp->d_in, lp->d_out, lp->B).off[0];
+  g.c_packed = H_out_packed;   // next layer's backward Y = H . [V_b] operand, by position
   return gemm_nn(g, w.gemm, st);
 }
 
 kg_status kg_rgcn_backward(const kg_graph_csr* G, const kg_layer_params* lp, const float* H_in, const float* H_out,
                            const float* dH_out, float* dH_in, const int32_t* order, const int32_t* pos,
-                           const int32_t* counts, int32_t t, float* d_bases, float* d_coeffs, void* ws,
-                           int64_t ws_bytes, void* stream, void* side_stream) {
+                           const int32_t* counts, int32_t t, float* d_bases, float* d_coeffs,
+                           const float* H_in_packed, void* ws, int64_t ws_bytes, void* stream, void* side_stream) {
   cudaStream_t st = as_stream(stream);
   const int B = lp->B, di = lp->d_in, dO = lp->d_out;
   KG_REQUIRE(B >= 1 && B <= MAXB, KG_ERR_VALIDATION, "num_bases must be in [1, %d]", MAXB);
@@ -787,8 +859,10 @@ kg_status kg_rgcn_backward(const kg_graph_csr* G, const kg_layer_params* lp, con
   size_t need = layer_ws(G->n, G->e, cap_split_chunks(G), di, dO, B, &w, ws, (size_t)ws_bytes);
   KG_REQUIRE((size_t)ws_bytes >= need, KG_ERR_VALIDATION, "layer workspace too small");
   const int64_t wn = (int64_t)B * di * dO;
-  KG_LAUNCH("k_weight_views", k_weight_views, persistent_blocks(wn, 256, 2), 256, 0, st, lp->bases, B, di, dO, w.Wy,
-            w.Wb);
+  const WeightsLayout wl = weights_layout(di, dO, B);
+  if (!lp->packed)
+    KG_LAUNCH("k_weight_views", k_weight_views, persistent_blocks(wn, 256, 2), 256, 0, st, lp->bases, B, di, dO, w.Wy,
+              w.Wb);
   if (dO % 4 == 0)
     KG_LAUNCH("k_dz", k_dz<true>, persistent_blocks((int64_t)G->n * 32, 256, 8), 256, 0, st, dH_out, H_out, order,
               counts, t, dO, w.dZ);
@@ -798,14 +872,16 @@ kg_status kg_rgcn_backward(const kg_graph_csr* G, const kg_layer_params* lp, con
   // Y = X[A_{t+1}] . [V_0 | .. | V_{B-1}]
   GemmArgs gy{};
   gy.A = H_in; gy.lda = di; gy.a_rows = order;
+  gy.a_packed = H_in_packed;
   gy.B = w.Wy; gy.ldb = (int64_t)B * dO;
   gy.C = w.Y; gy.ldc = (int64_t)B * dO;
   gy.M_dev = counts; gy.M_dev_index = t + 1; gy.M_max = G->n;
   gy.K = di; gy.N = (int64_t)B * dO;
+  if (lp->packed) gy.b_packed = lp->packed + wl.off[1];
   kg_status s = gemm_nn(gy, w.gemm, st);
   if (s != KG_OK) return s;
   CscArgs c{G->c_indptr, G->c_dst, G->c_rel, G->c_norm, csc_chunks(G), lp->coeffs, lp->G, B, dO, w.Y, w.dZ, pos,
-            counts, t, w.dS, w.ed, w.ed_self, w.partial};
+            counts, t, w.dS, w.ed, w.ed_self, w.partial, w.dS_pk, packed_records((int64_t)B * dO)};
   s = run_csc(c, G, st);
   if (s != KG_OK) return s;
   // The parameter gradients (dV, d coeffs) feed only the optimizer: with a side
@@ -830,13 +906,32 @@ kg_status kg_rgcn_backward(const kg_graph_csr* G, const kg_layer_params* lp, con
   if (dH_in) {
     GemmArgs gx{};
     gx.A = w.dS; gx.lda = (int64_t)B * dO;
+    gx.a_packed = w.dS_pk;
     gx.B = w.Wb; gx.ldb = di;
     gx.C = dH_in; gx.ldc = di; gx.c_rows = order;
     gx.M_dev = counts; gx.M_dev_index = t + 1; gx.M_max = G->n;
     gx.K = (int64_t)B * dO; gx.N = di;
+    if (lp->packed) gx.b_packed = lp->packed + wl.off[2];
     s = gemm_nn(gx, w.gemm, st);
     if (s != KG_OK) return s;
   }
+  return KG_OK;
+}
+
+int64_t kg_rgcn_weights_bytes(int32_t d_in, int32_t d_out, int32_t B) {
+  return weights_layout(d_in, d_out, B).total * (int64_t)sizeof(float);
+}
+
+kg_status kg_rgcn_pack_weights(const kg_layer_params* lp, float* out, void* stream) {
+  KG_REQUIRE(lp->B >= 1 && lp->B <= MAXB, KG_ERR_VALIDATION, "num_bases must be in [1, %d]", MAXB);
+  KG_REQUIRE(lp->d_out <= 256 && (int64_t)lp->B * lp->d_out <= 256 && lp->d_in <= 256, KG_ERR_SHAPE,
+             "packed weights need d_in, d_out, B*d_out <= 256");
+  const WeightsLayout L = weights_layout(lp->d_in, lp->d_out, lp->B);
+  int64_t most = 0;
+  for (int j = 0; j < 3; ++j) most = L.rows[j] * L.nk[j] * PK_K > most ? L.rows[j] * L.nk[j] * PK_K : most;
+  dim3 grid((unsigned)persistent_blocks(most, 256, 2), 3, 1);
+  KG_LAUNCH("k_pack_weights", k_pack_weights, grid, 256, 0, as_stream(stream), lp->bases, lp->B, lp->d_in, lp->d_out,
+            L, out);
   return KG_OK;
 }
 

@@ -224,6 +224,8 @@ struct PackedArgs {
   int64_t N;
   int64_t out_rows;       // TN: feature rows (g.K)
   int relu;
+  float* c_packed;        // NN: optional packed copy of the output (records by MMA row, K = np)
+  int64_t c_nk;
 };
 
 __device__ __forceinline__ uint32_t stage_bytes(int np) { return (uint32_t)((UM + np) * UKC * 2 * 4); }
@@ -362,6 +364,11 @@ __global__ void __launch_bounds__(UTHREADS, 1) k_umma_packed(PackedArgs g, int n
 #pragma unroll
             for (int i = 0; i < 16; ++i) v[i] = fmaxf(v[i], 0.f);
           }
+          if (g.c_packed) {   // pad columns hold exact zeros (zero B rows)
+            const int64_t m = tile * UM + r;
+#pragma unroll
+            for (int i = 0; i < 16; i += 4) packed_store<4>(g.c_packed, g.c_nk, m, c0 + i, v + i);
+          }
           if (vec && c0 + 16 <= g.N) {
 #pragma unroll
             for (int i = 0; i < 16; i += 4)
@@ -441,13 +448,20 @@ kg_status umma_gemm_nn(const GemmArgs& g, void* ws, cudaStream_t st) {
     Ap = const_cast<float*>(g.a_packed);
   }
   PackJob jb{g.B, g.ldb, nullptr, nullptr, 0, g.K, g.N, np, 1, nk, Bp};
-  const int64_t items = g.a_packed ? nk * np * 4 : tiles * nk * UM * 4;
-  kg_status s = launch_pack(ja, jb, items, st);
-  if (s != KG_OK) return s;
+  if (g.b_packed) {   // weights packed once per optimizer step
+    jb.src = nullptr;
+    Bp = const_cast<float*>(g.b_packed);
+  }
+  if (ja.src || jb.src) {
+    const int64_t items = ja.src ? tiles * nk * UM * 4 : nk * np * 4;
+    kg_status s = launch_pack(ja, jb, items, st);
+    if (s != KG_OK) return s;
+  }
   PackedArgs p{};
   p.Ap = Ap; p.Bp = Bp; p.a_nk_alloc = nk; p.np = np; p.tn = 0;
   p.M = g.M; p.M_dev = g.M_dev; p.M_dev_index = g.M_dev_index; p.nk = nk;
   p.C = g.C; p.ldc = g.ldc; p.c_rows = g.c_rows; p.N = g.N; p.out_rows = 0; p.relu = g.relu;
+  p.c_packed = g.c_packed; p.c_nk = ceil_div(g.N, UKC);
   const int ctas = (int)(tiles < num_sms() ? tiles : num_sms());
   return launch_packed(p, dim3((unsigned)ctas, 1, 1), st);
 }
@@ -503,3 +517,21 @@ kg_status umma_gemm_tn(const GemmArgs& g, float* out, void* ws, cudaStream_t st)
 }
 
 }  // namespace kg
+
+using namespace kg;
+
+extern "C" {
+
+int64_t kg_pack_rows_bytes(int64_t rows, int64_t cols) { return (int64_t)packed_bytes(rows, cols); }
+
+kg_status kg_pack_rows(const float* src, int64_t ld, const int32_t* rowid, const int32_t* counts,
+                       int32_t count_index, int64_t n_max, int64_t cols, float* out, void* stream) {
+  KG_REQUIRE(n_max >= 0 && cols >= 1, KG_ERR_VALIDATION, "bad pack shape");
+  if (n_max == 0) return KG_OK;
+  const int64_t nk = ceil_div(cols, UKC), tiles = ceil_div(n_max, UM);
+  PackJob ja{src, ld, rowid, counts, count_index, n_max, cols, UM, 0, nk, out};
+  PackJob none{};
+  return launch_pack(ja, none, tiles * nk * UM * 4, as_stream(stream));
+}
+
+}  // extern "C"

@@ -190,7 +190,30 @@ class DeviceModel:
             lp.B, lp.G = config.num_bases, config.num_rel_groups
             lp.bases = self.flat.data_ptr() + 4 * self.layout.bases_off(l)
             lp.coeffs = self.flat.data_ptr() + 4 * self.layout.coeffs_off(l)
+            lp.packed = None
             self._lp.append(lp)
+        self._lp_packed = None   # copies pointing at pre-packed weights (see repack)
+        self.wpack = None
+
+    def repack(self) -> None:
+        """Re-pack every layer's tensor-core weight operands from the current
+        bases (enqueued on the current stream). Callers that use
+        layer(l, packed=True) must repack after every parameter update."""
+        torch = _torch()
+        lib = _lib.require_cuda()
+        if self._lp_packed is None:
+            sizes = [lib.kg_rgcn_weights_bytes(lp.d_in, lp.d_out, lp.B) for lp in self._lp]
+            offs = [sum(sizes[:l]) for l in range(len(sizes))]
+            self.wpack = torch.empty(max(sum(sizes), 4) // 4, dtype=torch.float32, device=self.device)
+            self._lp_packed = []
+            for lp, off in zip(self._lp, offs):
+                q = _lib.KgLayerParams()
+                ctypes.memmove(ctypes.byref(q), ctypes.byref(lp), ctypes.sizeof(lp))
+                q.packed = self.wpack.data_ptr() + off
+                self._lp_packed.append(q)
+        st = _lib.stream_handle()
+        for q in self._lp_packed:
+            _lib.call("kg_rgcn_pack_weights", ctypes.byref(q), q.packed, st)
 
     @classmethod
     def from_params(cls, config: ModelConfig, params: ModelParams, device) -> "DeviceModel":
@@ -198,7 +221,11 @@ class DeviceModel:
         flat = torch.as_tensor(DenseLayout(config).pack(params.dense_blocks())).to(device)
         return cls(config, device, flat)
 
-    def layer(self, l) -> "_lib.KgLayerParams":
+    def layer(self, l, packed: bool = False) -> "_lib.KgLayerParams":
+        if packed:
+            if self._lp_packed is None:
+                raise RuntimeError("repack() must run before packed layers are used")
+            return self._lp_packed[l]
         return self._lp[l]
 
     def decoder_ptr(self) -> int:
@@ -236,6 +263,14 @@ class ViewBuffers:
                                                          config.num_relations)
         self.b_max = b_max
 
+    def hpk(self, l: int):
+        """Layer l's input rows (by closure position) as tensor-core operand
+        records for the backward Y GEMM (written by layer l-1's forward, or by
+        device_pack_inputs for l = 0)."""
+        key = f"hpk{l}"
+        nbytes = _lib.require_cuda().kg_pack_rows_bytes(self.n, self.config.dims[l])
+        return self.ws.get(key, nbytes)
+
     def layer_ws(self, l: int = 0):
         """Per-layer scratch: a layer's side-stream gradient work may still read
         its workspace while the next (lower) layer runs."""
@@ -249,16 +284,29 @@ class ViewBuffers:
         return self.ws.get("loss", self.loss_ws_bytes)
 
 
-def device_forward(model: DeviceModel, bufs: ViewBuffers) -> None:
-    """All layers over the closure in bufs.order/counts (ref:model.py:196-235)."""
+def device_pack_inputs(bufs: ViewBuffers) -> None:
+    """Layer 0's input rows H_0[order[p]], p < counts[L], as operand records
+    (bufs.hpk(0)); only needs the closure, so it can run on a side stream."""
+    L = bufs.config.num_layers
+    out = bufs.hpk(0)
+    _lib.call("kg_pack_rows", bufs.H[0].data_ptr(), bufs.config.dims[0], bufs.order.data_ptr(),
+              bufs.counts.data_ptr(), L, bufs.n, bufs.config.dims[0], out.data_ptr(), _lib.stream_handle())
+
+
+def device_forward(model: DeviceModel, bufs: ViewBuffers, packed: bool = False, hpk: bool = False) -> None:
+    """All layers over the closure in bufs.order/counts (ref:model.py:196-235).
+    packed: use the model's pre-packed weight operands (DeviceModel.repack);
+    hpk: also emit each hidden layer's output as the next layer's packed
+    backward operand (bufs.hpk)."""
     L = model.config.num_layers
     csr = ctypes.byref(bufs.view.csr())
     st = _lib.stream_handle()
     for l in range(L):
         ws = bufs.layer_ws(l)
-        _lib.call("kg_rgcn_forward", csr, ctypes.byref(model.layer(l)), bufs.H[l].data_ptr(),
+        _lib.call("kg_rgcn_forward", csr, ctypes.byref(model.layer(l, packed)), bufs.H[l].data_ptr(),
                   bufs.H[l + 1].data_ptr(), bufs.order.data_ptr(), bufs.pos.data_ptr(), bufs.counts.data_ptr(),
-                  L - 1 - l, 1 if l < L - 1 else 0, ws.data_ptr(), ws.numel(), st)
+                  L - 1 - l, 1 if l < L - 1 else 0, bufs.hpk(l + 1).data_ptr() if (hpk and l < L - 1) else None,
+                  ws.data_ptr(), ws.numel(), st)
 
 
 def device_loss(model: DeviceModel, bufs: ViewBuffers, stream, start: int, b: int, grad_flat, loss_out,
@@ -280,7 +328,8 @@ def device_loss(model: DeviceModel, bufs: ViewBuffers, stream, start: int, b: in
               ws.numel(), _lib.stream_handle())
 
 
-def device_backward(model: DeviceModel, bufs: ViewBuffers, grad_flat, input_grad: bool, side=None) -> None:
+def device_backward(model: DeviceModel, bufs: ViewBuffers, grad_flat, input_grad: bool, side=None,
+                    packed: bool = False, hpk: bool = False) -> None:
     """Layer gradients in reverse (ref:model.py:283-296): d bases / d coeffs
     into grad_flat, dL/dH_0 rows into bufs.dH[0] when input_grad. With a side
     stream (torch.cuda.Stream) the parameter-gradient branch of every layer
@@ -293,10 +342,11 @@ def device_backward(model: DeviceModel, bufs: ViewBuffers, grad_flat, input_grad
     for l in range(L - 1, -1, -1):
         ws = bufs.layer_ws(l)
         dh_in = bufs.dH[l].data_ptr() if (l > 0 or input_grad) else 0
-        _lib.call("kg_rgcn_backward", csr, ctypes.byref(model.layer(l)), bufs.H[l].data_ptr(),
+        _lib.call("kg_rgcn_backward", csr, ctypes.byref(model.layer(l, packed)), bufs.H[l].data_ptr(),
                   bufs.H[l + 1].data_ptr() if l < L - 1 else 0, bufs.dH[l + 1].data_ptr(), dh_in,
                   bufs.order.data_ptr(), bufs.pos.data_ptr(), bufs.counts.data_ptr(), L - 1 - l,
                   grad_flat.data_ptr() + 4 * lay.bases_off(l), grad_flat.data_ptr() + 4 * lay.coeffs_off(l),
+                  bufs.hpk(l).data_ptr() if hpk else None,
                   ws.data_ptr(), ws.numel(), st, None if side is None else side.cuda_stream)
     if side is not None:
         torch.cuda.current_stream().wait_stream(side)

@@ -566,6 +566,7 @@ class EpochSampler:
     a snapshot of the epoch's starting RNG state. Bit-exact either way."""
 
     ASYNC_ROUNDS = 3
+    NSLOTS = 3   # epochs e+1 and e+2 are sampled (and round-prepped) while e trains
 
     def __init__(self, view: PartitionView, s: int, g_dev):
         torch = _torch()
@@ -578,7 +579,7 @@ class EpochSampler:
         self.total = total
         self.core = view.d_edges[:core]
         self.slots = []
-        for _ in range(2):
+        for _ in range(self.NSLOTS):
             self.slots.append(dict(
                 neg=_neg_buffers(view, s, self.dev) if s > 0 and core > 0 else None,
                 out=dict(perm=torch.empty(max(total, 1), dtype=torch.int32, device=self.dev),
@@ -587,8 +588,28 @@ class EpochSampler:
                 g_start=torch.empty_like(g_dev), ready=torch.cuda.Event(), released=None,
                 status=torch.zeros(3, dtype=torch.int64, device=self.dev),
                 host=torch.zeros(3, dtype=torch.int64, pin_memory=True), stream=None))
-        self.parity = 0
-        self._enqueue(0)
+        self.parity = 0   # slot of the next epoch handed out
+        self._prep = None
+        for k in range(self.NSLOTS - 1):
+            self._enqueue(k)
+
+    def set_round_prep(self, fn) -> None:
+        """fn(slot, DeviceStream) enqueues per-round precomputation for an
+        epoch's stream; it runs on the side stream right after sampling (and
+        now for an epoch already enqueued)."""
+        torch = _torch()
+        self._prep = fn
+        for i, slot in enumerate(self.slots):
+            if slot["stream"] is not None:
+                with torch.cuda.stream(self.side):
+                    fn(i, slot["stream"])
+                    slot["ready"].record(self.side)
+
+    def slot_of(self, ds) -> int:
+        for i, slot in enumerate(self.slots):
+            if slot["out"]["tri"].data_ptr() == ds.triples.data_ptr():
+                return i
+        raise ValueError("stream does not belong to this sampler")
 
     def _enqueue(self, parity):
         torch = _torch()
@@ -609,8 +630,10 @@ class EpochSampler:
             ds, consumed = stream_device(self.core, neg, self.g, self.dev, self.ws, check=False, out=slot["out"])
             slot["status"][2:3].copy_(consumed)
             slot["host"].copy_(slot["status"], non_blocking=True)
-            slot["ready"].record(self.side)
             slot["stream"] = DeviceStream(slot["out"]["tri"], slot["out"]["lab"], ds.total)
+            if self._prep is not None:
+                self._prep(parity, slot["stream"])
+            slot["ready"].record(self.side)
 
     def slot_stream(self, slot: int) -> DeviceStream:
         """The (fixed-address) stream buffers of a slot, for graph capture."""
@@ -628,12 +651,14 @@ class EpochSampler:
             self._redo(slot)
         torch.cuda.current_stream().wait_event(slot["ready"])
         out = slot["stream"]
-        # the next epoch's buffers may be rewritten only after this epoch's compute
-        other = self.slots[1 - self.parity]
+        # the previous epoch's slot (all its compute is enqueued by now) is
+        # refilled with epoch e + NSLOTS - 1 once that compute has run
+        free = (self.parity + self.NSLOTS - 1) % self.NSLOTS
+        other = self.slots[free]
         other["released"] = torch.cuda.Event()
         other["released"].record(torch.cuda.current_stream())
-        self.parity = 1 - self.parity
-        self._enqueue(self.parity)
+        self.parity = (self.parity + 1) % self.NSLOTS
+        self._enqueue(free)
         return out
 
     def _redo(self, slot):
@@ -646,5 +671,7 @@ class EpochSampler:
             else:
                 neg = torch.zeros((0, 3), dtype=torch.int32, device=self.dev)
             stream_device(self.core, neg, self.g, self.dev, self.ws, check=True, out=slot["out"])
+            if self._prep is not None:
+                self._prep(next(i for i, x in enumerate(self.slots) if x is slot), slot["stream"])
             slot["ready"].record(self.side)
         slot["ready"].synchronize()

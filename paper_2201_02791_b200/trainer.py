@@ -30,7 +30,8 @@ import numpy as np
 from . import _lib
 from .errors import KGError, NumericError, ProtocolError, ValidationError
 from .model import (MODE_EMBEDDING, MODE_FEATURE, DeviceModel, ModelConfig, ModelParams, ViewBuffers,
-                    check_flags, device_backward, device_forward, device_loss, init_params)
+                    check_flags, device_backward, device_forward, device_loss, device_pack_inputs,
+                    init_params)
 from .partition import PartitionSet
 from .sampler import EpochSampler, build_view
 
@@ -231,12 +232,102 @@ def _assemble_embed(pset: PartitionSet, tables: dict, base: np.ndarray) -> np.nd
 # Device engine
 # ---------------------------------------------------------------------------
 
+class _RoundPrep:
+    """Batch-only per-round work of a whole epoch — the closure (order, pos,
+    counts) and the loss grouping (sorted values, segment bounds) of every
+    round — computed on the epoch sampler's side stream while the previous
+    epoch trains, into per-slot slabs. A training round then starts with one
+    kg_copy_segments launch indexed by the device round counter."""
+
+    def __init__(self, worker, rounds: int):
+        torch = _torch()
+        lib = _lib.require_cuda()
+        self.w = worker
+        v, cfg, b = worker.view, worker.config, worker.b
+        self.rounds, self.n, self.L1 = max(rounds, 1), v.n, cfg.num_layers + 1
+        dev = v.device
+        i32 = dict(dtype=torch.int32, device=dev)
+        self.slabs = [dict(order=torch.empty((self.rounds, self.n), **i32), pos=torch.empty((self.rounds, self.n), **i32),
+                           counts=torch.zeros((self.rounds, self.L1), **i32))
+                      for _ in range(EpochSampler.NSLOTS)]
+        self.ws = _lib.Workspace(dev)
+        self.flags = torch.zeros(1, **i32)
+        self.loss_args = (cfg.dims[-1], v.n, cfg.num_relations)
+        nbytes = lib.kg_loss_workspace_bytes(b, v.n, cfg.dims[-1], cfg.num_relations)
+        self.prep_ws = torch.empty(nbytes, dtype=torch.uint8, device=dev)
+        self.prep_fields = self._fields(self.prep_ws)
+        self.offs, o = [], 0
+        for _, nb in self.prep_fields:
+            self.offs.append(o)
+            o += (nb + 255) // 256 * 256
+        self.blob = o
+        for sl in self.slabs:
+            sl["groups"] = torch.empty(self.rounds * self.blob, dtype=torch.uint8, device=dev)
+        self.graphs = [None] * EpochSampler.NSLOTS
+
+    def _fields(self, ws):
+        d, n, R = self.loss_args
+        ptrs = (ctypes.c_void_p * 16)()
+        nbytes = (ctypes.c_int64 * 16)()
+        k = _lib.require_cuda().kg_loss_group_fields(ws.data_ptr(), ws.numel(), self.w.b, n, d, R, ptrs, nbytes, 16)
+        if k < 0:
+            raise KGError("loss workspace layout mismatch")
+        return [(int(ptrs[i] or 0), int(nbytes[i])) for i in range(k)]
+
+    def run(self, slot: int, ds) -> None:
+        """Enqueue every round of the epoch in `ds` (current stream = the
+        sampler's side stream): captured once per slot as a CUDA graph (the
+        slot's buffers are fixed), then replayed — one launch per epoch."""
+        torch = _torch()
+        if self.graphs[slot] is None:
+            g = torch.cuda.CUDAGraph()
+            g.capture_begin()
+            self._rounds(slot, ds)
+            g.capture_end()
+            self.graphs[slot] = g
+        self.graphs[slot].replay()
+
+    def _rounds(self, slot: int, ds) -> None:
+        from .sampler import closure_device
+        sl = self.slabs[slot]
+        w = self.w
+        d, n, R = self.loss_args
+        st = _lib.stream_handle()
+        for r in range(self.rounds):
+            start = r * w.b
+            closure_device(w.view, w.config.num_layers, stream=ds, start=start, size=w.b,
+                           out=(sl["order"][r], sl["pos"][r], sl["counts"][r]), ws=self.ws)
+            _lib.call("kg_loss_groups", 0, d, n, 0, R, ds.triples.data_ptr(), ds.labels.data_ptr(), ds.total,
+                      start, None, w.b, sl["order"][r].data_ptr(), sl["counts"][r].data_ptr(), 0, 0, 0, 0,
+                      self.flags.data_ptr(), self.prep_ws.data_ptr(), self.prep_ws.numel(), st)
+            base = sl["groups"].data_ptr() + r * self.blob
+            segs = (_lib.KgCopySeg * len(self.prep_fields))()
+            for i, ((ptr, nb), off) in enumerate(zip(self.prep_fields, self.offs)):
+                segs[i].dst, segs[i].src, segs[i].bytes = base + off, ptr, nb
+            _lib.call("kg_copy_segments", segs, len(segs), None, 0, st)
+
+    def import_round(self, slot: int, round_dev, loss_ws) -> None:
+        """Copy round *round_dev of `slot` into the worker's working buffers."""
+        sl, bufs = self.slabs[slot], self.w.bufs
+        fields = self._fields(loss_ws)
+        segs = (_lib.KgCopySeg * (3 + len(fields)))()
+        n, L1 = self.n, self.L1
+        for i, (dst, src, nb) in enumerate(((bufs.order, sl["order"], 4 * n), (bufs.pos, sl["pos"], 4 * n),
+                                            (bufs.counts, sl["counts"], 4 * L1))):
+            segs[i].dst, segs[i].src, segs[i].bytes, segs[i].src_round_stride = dst.data_ptr(), src.data_ptr(), nb, nb
+        gbase = sl["groups"].data_ptr()
+        for j, ((ptr, nb), off) in enumerate(zip(fields, self.offs)):
+            g = segs[3 + j]
+            g.dst, g.src, g.bytes, g.src_round_stride = ptr, gbase + off, nb, self.blob
+        _lib.call("kg_copy_segments", segs, len(segs), round_dev.data_ptr(), 0, _lib.stream_handle())
+
+
 class _Worker:
     """Device state of one partition: view, buffers, RNG stream, local
     embedding rows and their Adam moments."""
 
     def __init__(self, wid, partition, pset, config: ModelConfig, tc: TrainConfig, b: int, params: ModelParams,
-                 features):
+                 features, rounds: int = 1):
         torch = _torch()
         self.wid = wid
         self.view = build_view(partition, pset.num_entities, pset.num_relations)
@@ -263,9 +354,14 @@ class _Worker:
         self.stream = None
         # epoch e+1's negatives + shuffle are produced on a side stream while epoch e trains
         self.sampler = EpochSampler(self.view, config.negatives_per_positive, self.g_dev)
+        self.prep = _RoundPrep(self, rounds)
+        self.sampler.set_round_prep(self.prep.run)
 
     def begin_epoch(self):
         self.stream = self.sampler.next()
+
+    def slot(self) -> int:
+        return self.sampler.slot_of(self.stream)
 
     def closure(self, start_dev):
         from .sampler import closure_device
@@ -315,7 +411,7 @@ class Trainer:
         D = self.model.layout.total
         self.D = D
         self.workers = [_Worker(w, pset.partitions[w], pset, model_config, train_config, self.sizes[w], params,
-                                features) for w in self.local_wids]
+                                features, self.rounds) for w in self.local_wids]
         nloc = len(self.workers)
         self.grads_local = torch.zeros((nloc, D), dtype=torch.float32, device=self.dev)
         self.grads_all = (torch.zeros((self.P, D), dtype=torch.float32, device=self.dev) if self.dist
@@ -346,6 +442,7 @@ class Trainer:
         self._graphs = {}
         self._graph_pool = None
         self._loss_stream = torch.cuda.Stream(self.dev)   # batch-only loss grouping, overlaps the layers
+        self.model.repack()
         self._eager_rounds = 0
         self.t = 0
         self.round_in_epoch = 0
@@ -365,20 +462,20 @@ class Trainer:
         torch.mul(self.b_dev, self.round_dev, out=self.start_dev)
         main = torch.cuda.current_stream()
         for i, w in enumerate(self.workers):
-            w.closure(self.start_dev[i:i + 1])
+            # closure + loss grouping of this round were precomputed with the
+            # epoch (_RoundPrep); one copy brings them into the working buffers
+            w.prep.import_round(w.slot(), self.round_dev, w.bufs.loss_ws(w.b))
             gslot = self.grads_local[i]
-            # fork: key sorts + segment bounds of the loss need only the batch
-            # and the seed order, so they run beside the layers
             self._loss_stream.wait_stream(main)
             with torch.cuda.stream(self._loss_stream):
-                device_loss(self.model, w.bufs, w.stream, 0, w.b, gslot, self.loss_scratch[i:i + 1],
-                            start_dev=self.start_dev[i:i + 1], part="groups")
-            device_forward(self.model, w.bufs)
+                device_pack_inputs(w.bufs)   # layer-0 backward operand, beside the forward
+            device_forward(self.model, w.bufs, packed=True, hpk=True)
             main.wait_stream(self._loss_stream)
             device_loss(self.model, w.bufs, w.stream, 0, w.b, gslot, self.loss_scratch[i:i + 1],
                         start_dev=self.start_dev[i:i + 1], part="compute")
             self.losses[i].index_copy_(0, self.round_dev, self.loss_scratch[i:i + 1])
-            device_backward(self.model, w.bufs, gslot, input_grad=w.emb, side=self._loss_stream)
+            device_backward(self.model, w.bufs, gslot, input_grad=w.emb, side=self._loss_stream, packed=True,
+                            hpk=True)
 
     def _update_body(self):
         """Fused tree-mean + dense Adam/SGD, then lazy sparse rows."""
@@ -391,6 +488,7 @@ class Trainer:
                   tc.adam_eps, 1.0, 1.0, self.step_dev.data_ptr(),
                   float(tc.grad_clip) if tc.grad_clip is not None else 0.0,
                   self.flags.data_ptr(), self.optim_ws.data_ptr(), self.optim_ws.numel(), st)
+        self.model.repack()   # tensor-core weight operands of the updated bases
         L = self.mc.num_layers
         for w in self.workers:
             if w.emb:
@@ -443,7 +541,7 @@ class Trainer:
         if self._graph_pool is None:
             self._graph_pool = torch.cuda.graph_pool_handle()
         current = [w.stream for w in self.workers]
-        for slot in range(2):
+        for slot in range(EpochSampler.NSLOTS):
             for w in self.workers:
                 w.stream = w.sampler.slot_stream(slot)
             key = tuple(w.stream.triples.data_ptr() for w in self.workers)

@@ -284,3 +284,39 @@ def test_cuda_graph_replay_is_bitwise_identical_to_eager():
     for x, y in zip(a.dense_blocks(), b.dense_blocks()):
         np.testing.assert_array_equal(x, y)
     np.testing.assert_array_equal(a.entity_embed, b.entity_embed)
+
+
+def test_prepacked_weights_are_bitwise_identical():
+    """Forward/backward with the once-per-step packed weight operands
+    (DeviceModel.repack) and the producer-packed activations (hpk, dS
+    records) equal on-the-fly packing bit for bit."""
+    from paper_2201_02791_b200.model import device_backward, device_forward, device_loss, device_pack_inputs
+    graph, split = kb.generate_synthetic(3000, 40, 12.0, seed=3)
+    pset = kb.neighborhood_expand(kb.vertex_cut_partition(graph, 2, seed=0), graph, 2)
+    v = kb.build_view(pset.partitions[0], graph.num_entities, graph.num_relations)
+    mc = kb.ModelConfig(2, [48, 64, 40], 3, 40, 1, mode="embedding")
+    p = kb.init_params(mc, np.random.default_rng(1), num_entities=graph.num_entities)
+    rng = np.random.default_rng(2)
+    batch = kb.make_batches(v.core_edges, kb.sample_negatives(v, 1, rng), 1024, rng, num_batches=1)[0]
+    cg = kb.build_compute_graph(batch, v, 2)
+    cache = kb.EncodeCache()
+    kb.encode(p, mc, cg, p.entity_embed, v.local_ids, cache=cache)
+    model, bufs = cache.model, cache.bufs
+    from paper_2201_02791_b200.sampler import DeviceStream
+    tri = torch.as_tensor(batch.triples.astype(np.int32)).cuda()
+    lab = torch.as_tensor(batch.labels.astype(np.float32)).cuda()
+    ds = DeviceStream(tri, lab, len(batch.triples))
+    model.repack()
+    out = []
+    for packed in (False, True):
+        if packed:
+            device_pack_inputs(bufs)
+        device_forward(model, bufs, packed=packed, hpk=packed)
+        grad = torch.zeros(model.layout.total, dtype=torch.float32, device="cuda")
+        loss = torch.zeros(1, dtype=torch.float32, device="cuda")
+        device_loss(model, bufs, ds, 0, len(batch.triples), grad, loss)
+        device_backward(model, bufs, grad, input_grad=True, packed=packed, hpk=packed)
+        torch.cuda.synchronize()
+        out.append((bufs.H[2].clone(), grad.clone(), bufs.dH[0].clone(), loss.clone()))
+    for a, b in zip(*out):
+        assert torch.equal(a, b)
