@@ -568,7 +568,10 @@ class EpochSampler:
     ASYNC_ROUNDS = 3
     NSLOTS = 3   # epochs e+1 and e+2 are sampled (and round-prepped) while e trains
 
-    def __init__(self, view: PartitionView, s: int, g_dev):
+    def __init__(self, view: PartitionView, s: int, g_dev, prep=None):
+        """prep(slot, DeviceStream), optional: enqueues per-round
+        precomputation for an epoch's stream; it becomes part of the slot's
+        captured epoch graph, right after the sampling."""
         torch = _torch()
         self.view, self.s, self.g = view, s, g_dev
         self.dev = view.device
@@ -587,23 +590,15 @@ class EpochSampler:
                          lab=torch.empty(max(total, 1), dtype=torch.float32, device=self.dev)),
                 g_start=torch.empty_like(g_dev), ready=torch.cuda.Event(), released=None,
                 status=torch.zeros(3, dtype=torch.int64, device=self.dev),
-                host=torch.zeros(3, dtype=torch.int64, pin_memory=True), stream=None))
+                host=torch.zeros(3, dtype=torch.int64, pin_memory=True), stream=None, graph=None))
         self.parity = 0   # slot of the next epoch handed out
-        self._prep = None
+        self._prep = prep
+        # one CUDA graph per slot holds the whole epoch pipeline (negatives,
+        # shuffle, gather, round prep): an epoch boundary costs one replay
+        for k in range(self.NSLOTS):
+            self._capture(k)
         for k in range(self.NSLOTS - 1):
             self._enqueue(k)
-
-    def set_round_prep(self, fn) -> None:
-        """fn(slot, DeviceStream) enqueues per-round precomputation for an
-        epoch's stream; it runs on the side stream right after sampling (and
-        now for an epoch already enqueued)."""
-        torch = _torch()
-        self._prep = fn
-        for i, slot in enumerate(self.slots):
-            if slot["stream"] is not None:
-                with torch.cuda.stream(self.side):
-                    fn(i, slot["stream"])
-                    slot["ready"].record(self.side)
 
     def slot_of(self, ds) -> int:
         for i, slot in enumerate(self.slots):
@@ -611,28 +606,45 @@ class EpochSampler:
                 return i
         raise ValueError("stream does not belong to this sampler")
 
+    def _body(self, parity):
+        """The epoch's kernels (current stream = side stream)."""
+        torch = _torch()
+        slot = self.slots[parity]
+        slot["g_start"].copy_(self.g)
+        if slot["neg"] is not None:
+            neg = sample_negatives_device(self.view, self.s, self.g, self.ws, bufs=slot["neg"],
+                                          async_rounds=self.ASYNC_ROUNDS)
+            b = slot["neg"]
+            slot["status"][0:1].copy_(b["k"][b["cur"]])
+            slot["status"][1:2].copy_(b["consumed"].min().view(1))
+        else:
+            neg = slot.setdefault("empty_neg", torch.zeros((0, 3), dtype=torch.int32, device=self.dev))
+            slot["status"][:2].zero_()
+        ds, consumed = stream_device(self.core, neg, self.g, self.dev, self.ws, check=False, out=slot["out"])
+        slot["status"][2:3].copy_(consumed)
+        slot["host"].copy_(slot["status"], non_blocking=True)
+        if self._prep is not None:
+            self._prep(parity, self.slot_stream(parity))
+
+    def _capture(self, parity):
+        torch = _torch()
+        slot = self.slots[parity]
+        g = torch.cuda.CUDAGraph()
+        self.side.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(self.side):
+            g.capture_begin()
+            self._body(parity)
+            g.capture_end()
+        slot["graph"] = g
+        slot["stream"] = self.slot_stream(parity)
+
     def _enqueue(self, parity):
         torch = _torch()
         slot = self.slots[parity]
         with torch.cuda.stream(self.side):
             if slot["released"] is not None:
                 self.side.wait_event(slot["released"])
-            slot["g_start"].copy_(self.g)
-            if slot["neg"] is not None:
-                neg = sample_negatives_device(self.view, self.s, self.g, self.ws, bufs=slot["neg"],
-                                              async_rounds=self.ASYNC_ROUNDS)
-                b = slot["neg"]
-                slot["status"][0:1].copy_(b["k"][b["cur"]])
-                slot["status"][1:2].copy_(b["consumed"].min().view(1))
-            else:
-                neg = torch.zeros((0, 3), dtype=torch.int32, device=self.dev)
-                slot["status"][:2].zero_()
-            ds, consumed = stream_device(self.core, neg, self.g, self.dev, self.ws, check=False, out=slot["out"])
-            slot["status"][2:3].copy_(consumed)
-            slot["host"].copy_(slot["status"], non_blocking=True)
-            slot["stream"] = DeviceStream(slot["out"]["tri"], slot["out"]["lab"], ds.total)
-            if self._prep is not None:
-                self._prep(parity, slot["stream"])
+            slot["graph"].replay()
             slot["ready"].record(self.side)
 
     def slot_stream(self, slot: int) -> DeviceStream:

@@ -263,7 +263,6 @@ class _RoundPrep:
         self.blob = o
         for sl in self.slabs:
             sl["groups"] = torch.empty(self.rounds * self.blob, dtype=torch.uint8, device=dev)
-        self.graphs = [None] * EpochSampler.NSLOTS
 
     def _fields(self, ws):
         d, n, R = self.loss_args
@@ -276,18 +275,7 @@ class _RoundPrep:
 
     def run(self, slot: int, ds) -> None:
         """Enqueue every round of the epoch in `ds` (current stream = the
-        sampler's side stream): captured once per slot as a CUDA graph (the
-        slot's buffers are fixed), then replayed — one launch per epoch."""
-        torch = _torch()
-        if self.graphs[slot] is None:
-            g = torch.cuda.CUDAGraph()
-            g.capture_begin()
-            self._rounds(slot, ds)
-            g.capture_end()
-            self.graphs[slot] = g
-        self.graphs[slot].replay()
-
-    def _rounds(self, slot: int, ds) -> None:
+        sampler's side stream; captured into the sampler's epoch graph)."""
         from .sampler import closure_device
         sl = self.slabs[slot]
         w = self.w
@@ -353,9 +341,8 @@ class _Worker:
         self.ws = _lib.Workspace(dev)
         self.stream = None
         # epoch e+1's negatives + shuffle are produced on a side stream while epoch e trains
-        self.sampler = EpochSampler(self.view, config.negatives_per_positive, self.g_dev)
         self.prep = _RoundPrep(self, rounds)
-        self.sampler.set_round_prep(self.prep.run)
+        self.sampler = EpochSampler(self.view, config.negatives_per_positive, self.g_dev, prep=self.prep.run)
 
     def begin_epoch(self):
         self.stream = self.sampler.next()
