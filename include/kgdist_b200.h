@@ -341,11 +341,19 @@ kg_status kg_sparse_step(float* table, float* m, float* v, const float* grad, co
  * train+valid+test, head_keys = sorted unique (t*R+r)*N+h. Records are
  * written in the reference order (per chunk: tail records, head records).
  * policy: 0 mean, 1 optimistic, 2 pessimistic. */
-int64_t kg_eval_workspace_bytes(int64_t nq);
+/* impl 0: all-entity scores on the tcgen05 tensor cores (3xTF32, d <= 128;
+ * true score and candidate scores come from the same MMA arithmetic), known
+ * candidates skipped in the fused compare/count epilogue; impl 1 (or d > 128):
+ * CUDA-core tiles with an exact sequential fmaf chain per score. */
+/* known_pairs: an upper bound on sum over (query, side) of the known
+ * candidates other than the true entity (impl 0 scores them in a separate
+ * pass); *overflow (device uint32, optional) is set when it was too small. */
+int64_t kg_eval_workspace_bytes(int64_t nq, int32_t N, int32_t d, int64_t known_pairs);
 kg_status kg_eval_filtered(const float* H, int32_t d, int32_t N, const float* decoder, int32_t R,
                            const int32_t* queries, int64_t nq, const int64_t* tail_keys, int64_t n_tail,
                            const int64_t* head_keys, int64_t n_head, int32_t policy, int32_t chunk,
-                           double* ranks, int32_t* ncand, void* ws, int64_t ws_bytes, void* stream);
+                           int32_t impl, int64_t known_pairs, double* ranks, int32_t* ncand, uint32_t* overflow,
+                           void* ws, int64_t ws_bytes, void* stream);
 /* Sorted unique keys (a*R + r)*N + c of (k,3) triples with (a,c) = (col_a, col_c). */
 int64_t kg_known_keys_workspace_bytes(int64_t k);
 kg_status kg_known_keys(const int32_t* triples, int64_t k, int32_t col_a, int32_t col_c, int32_t N, int32_t R,

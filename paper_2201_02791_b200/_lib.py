@@ -108,9 +108,9 @@ _PROTOS = {
                            c_double, c_double, P, c_float, P, P, c_int64, P]),
     "kg_sparse_step": (ST, [P, P, P, P, P, P, c_int32, c_int32, c_int32, c_float, c_float, c_float,
                             c_float, c_double, c_double, P, c_int32, P]),
-    "kg_eval_workspace_bytes": (c_int64, [c_int64]),
+    "kg_eval_workspace_bytes": (c_int64, [c_int64, c_int32, c_int32, c_int64]),
     "kg_eval_filtered": (ST, [P, c_int32, c_int32, P, c_int32, P, c_int64, P, c_int64, P, c_int64,
-                              c_int32, c_int32, P, P, P, c_int64, P]),
+                              c_int32, c_int32, c_int32, c_int64, P, P, P, P, c_int64, P]),
     "kg_known_keys_workspace_bytes": (c_int64, [c_int64]),
     "kg_known_keys": (ST, [P, c_int64, c_int32, c_int32, c_int32, c_int32, P, P, P, c_int64, P]),
     "kg_generate_synthetic": (c_int64, [c_int64, c_int32, c_int64, POINTER(KgPcg64), P, c_int64]),

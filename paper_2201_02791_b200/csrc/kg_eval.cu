@@ -12,7 +12,7 @@
 // Every score -- bulk tile, true score, filtered candidate -- is the same
 // sequential fmaf chain over k = 0..d-1 starting from 0, so the comparisons
 // are exact (the reference compares entries of one matrix, evaluate.py:200).
-#include "kg_common.cuh"
+#include "kg_gemm.cuh"
 
 namespace kg {
 
@@ -242,18 +242,25 @@ kg_status kg_known_keys(const int32_t* tri, int64_t k, int32_t ca, int32_t cc, i
   return KG_OK;
 }
 
-int64_t kg_eval_workspace_bytes(int64_t nq) {
-  return (int64_t)(align_up(2 * nq * 4) + align_up(2 * nq * 8) * 2 + 1024);
+int64_t kg_eval_workspace_bytes(int64_t nq, int32_t N, int32_t d, int64_t known_pairs) {
+  const size_t simt = align_up(2 * nq * 4) + align_up(2 * nq * 8) * 2 + 1024;
+  const size_t tc = d <= 128 ? umma_rank_workspace(nq, N, d, known_pairs) + 1024 : 0;
+  return (int64_t)(simt > tc ? simt : tc);
 }
 
 kg_status kg_eval_filtered(const float* H, int32_t d, int32_t N, const float* dec, int32_t R, const int32_t* qry,
                            int64_t nq, const int64_t* tkeys, int64_t ntk, const int64_t* hkeys, int64_t nhk,
-                           int32_t policy, int32_t chunk, double* ranks, int32_t* ncand, void* ws,
-                           int64_t ws_bytes, void* stream) {
+                           int32_t policy, int32_t chunk, int32_t impl, int64_t known_pairs, double* ranks,
+                           int32_t* ncand, uint32_t* overflow, void* ws, int64_t ws_bytes, void* stream) {
   cudaStream_t st = as_stream(stream);
   KG_REQUIRE(policy >= 0 && policy <= 2, KG_ERR_VALIDATION, "unknown tie policy");
   KG_REQUIRE(chunk >= 1 && nq >= 1, KG_ERR_VALIDATION, "bad chunk / empty split");
-  KG_REQUIRE(ws_bytes >= kg_eval_workspace_bytes(nq), KG_ERR_VALIDATION, "eval workspace too small");
+  KG_REQUIRE(ws_bytes >= kg_eval_workspace_bytes(nq, N, d, known_pairs), KG_ERR_VALIDATION,
+             "eval workspace too small");
+  if (impl == 0 && d <= 128)
+    return umma_rank_filtered(H, d, N, dec, R, qry, nq, tkeys, ntk, hkeys, nhk, policy, chunk, known_pairs, ranks,
+                              ncand, overflow, ws, (size_t)ws_bytes, st);
+  if (overflow) KG_CUDA(cudaMemsetAsync(overflow, 0, 4, st));
   Arena a(ws, (size_t)ws_bytes);
   float* ts = a.take<float>(2 * nq);
   unsigned long long* gr = a.take<unsigned long long>(2 * nq);

@@ -516,6 +516,430 @@ kg_status umma_gemm_tn(const GemmArgs& g, float* out, void* ws, cudaStream_t st)
   return reduce_splits(part, splits, g.K * g.N, out, st);
 }
 
+// ---------------------------------------------------------------------------
+// Filtered ranking on the tensor cores (R25/R26, ref:evaluate.py:192-217).
+//
+// Rows x = side*nq + q are the (query, side) pairs; q_x = H[anchor] * dec[r]
+// (fp32 product). k_rank_umma keeps a 128-row query tile resident in shared
+// memory and streams record tiles through a ring: first the tile's "diagonal"
+// B rows (the true entity of each row), then every candidate block; D = Q.C^T
+// on tcgen05 (3xTF32, 128 x 128 per virtual tile, TMEM double buffer). The
+// epilogue never writes a score: virtual tile 0 yields the true score as the
+// diagonal D[x][x] (a tcgen05 element depends only on its A and B rows, so it
+// is bit-identical to the bulk element of the true column —
+// tools/check_mma_position.py), then 8 epilogue warps count candidates
+// scoring greater / equal, branch-free. Known (train+valid+test) candidates
+// are a short pair list per query: their scores come from the same kernel in
+// diagonal-only mode (A rows = the pair's query, B rows = the candidate) and
+// are subtracted from the counts before the tie policy of
+// ref:evaluate.py:93-100 is applied.
+struct RankArgs {
+  const float* Qp;    // A records, 128-row blocks over rows
+  const float* Tp;    // diagonal B records, same blocking
+  const float* Cp;    // candidate records (ncols columns), may be null
+  int nk;
+  int64_t rows;
+  int32_t ncols;      // 0: diagonal only
+  float* ts;          // out: diagonal per row
+  uint32_t* greater;  // out (accumulated): candidates scoring > ts
+  uint32_t* equal;    // out (accumulated): candidates scoring == ts
+};
+
+constexpr int RK_EPI_WARPS = 8;
+constexpr int RK_THREADS = 64 + 32 * RK_EPI_WARPS;
+constexpr int RK_MAXS = 8;
+constexpr uint32_t RK_REC = 128 * UKC * 8;   // bytes per 128-row record (hi + lo)
+constexpr size_t RK_SMEM_CAP = 220 * 1024;
+
+__device__ __forceinline__ int64_t rk_lower_bound(const int64_t* __restrict__ k, int64_t n, int64_t x) {
+  int64_t lo = 0, hi = n;
+  while (lo < hi) {
+    const int64_t mid = (lo + hi) >> 1;
+    if (k[mid] < x) lo = mid + 1;
+    else hi = mid;
+  }
+  return lo;
+}
+
+__device__ __forceinline__ void rk_query(const int32_t* __restrict__ qry, int64_t nq, int64_t x, int& side,
+                                         int64_t& q, int32_t& anc, int32_t& rel, int32_t& tru) {
+  side = (int)(x / nq);
+  q = x - side * nq;
+  const int32_t h = qry[q * 3], tl = qry[q * 3 + 2];
+  rel = qry[q * 3 + 1];
+  anc = side == 0 ? h : tl;
+  tru = side == 0 ? tl : h;
+}
+
+// A rows: q_x (or, for the known-pair pass, q of the pair's row); diagonal B
+// rows: H[tru(x)] (or H[c] of the pair).
+__global__ void __launch_bounds__(256) k_eval_pack(const float* __restrict__ H, const float* __restrict__ dec,
+                                                   const int32_t* __restrict__ qry, int64_t nq,
+                                                   const int32_t* __restrict__ pair_x,
+                                                   const int32_t* __restrict__ pair_c,
+                                                   const int32_t* __restrict__ rows_dev, int64_t rows_host, int d,
+                                                   int nk, float* __restrict__ Qp, float* __restrict__ Tp) {
+  const int64_t rows = rows_dev ? (int64_t)*rows_dev : rows_host, tiles = (rows + 127) / 128;
+  const int64_t items = tiles * nk * 128 * 4;
+  for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < items;
+       idx += (int64_t)gridDim.x * blockDim.x) {
+    const int q4 = (int)(idx & 3);
+    const int64_t t = idx >> 2;
+    const int r = (int)(t & 127);
+    const int64_t u = t >> 7;
+    const int64_t kc = u % nk, blk = u / nk;
+    const int64_t i = blk * 128 + r;
+    const int k0 = (int)kc * UKC + 4 * q4;
+    float vq[4] = {0.f, 0.f, 0.f, 0.f}, vt[4] = {0.f, 0.f, 0.f, 0.f};
+    if (i < rows) {
+      const int64_t x = pair_x ? pair_x[i] : i;
+      int side;
+      int64_t q;
+      int32_t anc, rel, tru;
+      rk_query(qry, nq, x, side, q, anc, rel, tru);
+      const int32_t c = pair_c ? pair_c[i] : tru;
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const int k = k0 + j;
+        if (k < d) {
+          vq[j] = H[(int64_t)anc * d + k] * dec[(int64_t)rel * d + k];
+          vt[j] = H[(int64_t)c * d + k];
+        }
+      }
+    }
+    pack_store(Qp + (blk * nk + kc) * rec_floats(128), 128, r, q4, vq);
+    pack_store(Tp + (blk * nk + kc) * rec_floats(128), 128, r, q4, vt);
+  }
+}
+
+__global__ void __launch_bounds__(RK_THREADS, 1) k_rank_umma(RankArgs a, const int32_t* __restrict__ rows_dev,
+                                                             int nstages) {
+  extern __shared__ __align__(1024) uint8_t smem[];
+  __shared__ __align__(8) uint64_t bar_full[RK_MAXS], bar_empty[RK_MAXS], bar_tfull[2], bar_tempty[2];
+  __shared__ __align__(8) uint64_t bar_afull, bar_aempty;
+  __shared__ uint32_t tmem_base_s;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int64_t rows = rows_dev ? (int64_t)*rows_dev : a.rows, qtiles = (rows + 127) / 128;
+  const int nblk = (a.ncols + 127) / 128, nj = nblk + 1, nk = a.nk;
+  if ((int64_t)blockIdx.x >= qtiles) return;
+  const uint32_t sbase = smem_u32(smem), ring = sbase + (uint32_t)nk * RK_REC;
+  auto full = [&](int s) { return smem_u32(&bar_full[s]); };
+  auto empty = [&](int s) { return smem_u32(&bar_empty[s]); };
+  const int64_t RF = rec_floats(128);
+
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&tmem_base_s)),
+                 "r"(256));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  if (tid == 32) {
+    for (int s = 0; s < nstages; ++s) {
+      mbar_init(full(s), 1);
+      mbar_init(empty(s), 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(smem_u32(&bar_tfull[i]), 1);
+      mbar_init(smem_u32(&bar_tempty[i]), RK_EPI_WARPS);
+    }
+    mbar_init(smem_u32(&bar_afull), 1);
+    mbar_init(smem_u32(&bar_aempty), 1);
+    fence_barrier_init();
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = tmem_base_s;
+
+  if (warp == 0) {
+    if (lane == 0) {   // producer
+      int64_t it = 0, tc = 0;
+      for (int64_t tile = blockIdx.x; tile < qtiles; tile += gridDim.x, ++tc) {
+        if (tc > 0) mbar_wait(smem_u32(&bar_aempty), (uint32_t)((tc - 1) & 1));
+        mbar_expect_tx(smem_u32(&bar_afull), (uint32_t)nk * RK_REC);
+        for (int kc = 0; kc < nk; ++kc)
+          bulk_g2s(sbase + (uint32_t)kc * RK_REC, a.Qp + (tile * nk + kc) * RF, RK_REC, smem_u32(&bar_afull));
+        for (int j = 0; j < nj; ++j)
+          for (int kc = 0; kc < nk; ++kc, ++it) {
+            const int s = (int)(it % nstages);
+            if (it >= nstages) mbar_wait(empty(s), (uint32_t)((it / nstages - 1) & 1));
+            mbar_expect_tx(full(s), RK_REC);
+            const float* src = j == 0 ? a.Tp + (tile * nk + kc) * RF : a.Cp + ((int64_t)(j - 1) * nk + kc) * RF;
+            bulk_g2s(ring + (uint32_t)s * RK_REC, src, RK_REC, full(s));
+          }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {   // MMA issuer
+      const uint32_t idesc = make_idesc(128);
+      const uint32_t lbo = (128 / 8) * 128, half = 128 * UKC * 4;
+      int64_t it = 0, jc = 0, tc = 0;
+      for (int64_t tile = blockIdx.x; tile < qtiles; tile += gridDim.x, ++tc) {
+        mbar_wait(smem_u32(&bar_afull), (uint32_t)(tc & 1));
+        tc_fence_after();
+        for (int j = 0; j < nj; ++j, ++jc) {
+          const int acc = (int)(jc & 1);
+          if (jc >= 2) mbar_wait(smem_u32(&bar_tempty[acc]), (uint32_t)((jc / 2 - 1) & 1));
+          tc_fence_after();
+          const uint32_t dt = tmem + (uint32_t)acc * 128;
+          for (int kc = 0; kc < nk; ++kc, ++it) {
+            const int s = (int)(it % nstages);
+            mbar_wait(full(s), (uint32_t)((it / nstages) & 1));
+            tc_fence_after();
+            const uint32_t a_hi = sbase + (uint32_t)kc * RK_REC, a_lo = a_hi + half;
+            const uint32_t b_hi = ring + (uint32_t)s * RK_REC, b_lo = b_hi + half;
+#pragma unroll
+            for (int jj = 0; jj < UKC / 8; ++jj) {
+              const uint32_t ko = (uint32_t)(2 * jj) * lbo;
+              const uint64_t dah = make_desc(a_hi + ko, lbo, 128), dal = make_desc(a_lo + ko, lbo, 128);
+              const uint64_t dbh = make_desc(b_hi + ko, lbo, 128), dbl = make_desc(b_lo + ko, lbo, 128);
+              mma_tf32(dt, dah, dbh, idesc, (kc > 0 || jj > 0) ? 1u : 0u);
+              mma_tf32(dt, dah, dbl, idesc, 1u);
+              mma_tf32(dt, dal, dbh, idesc, 1u);
+            }
+            mma_commit(empty(s));
+          }
+          mma_commit(smem_u32(&bar_tfull[acc]));
+        }
+        mma_commit(smem_u32(&bar_aempty));
+      }
+    }
+  } else {   // epilogue warps: TMEM lanes 32*(warp%4).., column half (warp-2)/4
+    const int lanegrp = warp & 3, r = lanegrp * 32 + lane, colh = (warp - 2) >> 2;
+    int64_t jc = 0;
+    for (int64_t tile = blockIdx.x; tile < qtiles; tile += gridDim.x) {
+      const int64_t x = tile * 128 + r;
+      float ts = 0.f;
+      uint32_t g = 0, e = 0;
+      for (int j = 0; j < nj; ++j, ++jc) {
+        const int acc = (int)(jc & 1);
+        mbar_wait(smem_u32(&bar_tfull[acc]), (uint32_t)((jc / 2) & 1));
+        tc_fence_after();
+        const uint32_t taddr = tmem + (uint32_t)acc * 128 + ((uint32_t)(lanegrp * 32) << 16);
+        if (j == 0) {
+          float v[32];
+          tmem_ld16(taddr + (uint32_t)(lanegrp * 32), v);
+          tmem_ld16(taddr + (uint32_t)(lanegrp * 32 + 16), v + 16);
+#pragma unroll
+          for (int i = 0; i < 32; ++i)
+            if (i == lane) ts = v[i];
+        } else {
+          const int32_t c0 = (j - 1) * 128 + colh * 64;
+          const int nvalid = a.ncols - c0;   // columns of this half that exist
+#pragma unroll
+          for (int ch = 0; ch < 4; ++ch) {
+            float v[16];
+            tmem_ld16(taddr + (uint32_t)(colh * 64 + ch * 16), v);
+            if (nvalid >= (ch + 1) * 16) {
+#pragma unroll
+              for (int i = 0; i < 16; ++i) {
+                g += v[i] > ts ? 1u : 0u;
+                e += v[i] == ts ? 1u : 0u;
+              }
+            } else {
+#pragma unroll
+              for (int i = 0; i < 16; ++i) {
+                const bool ok = ch * 16 + i < nvalid;
+                g += (ok && v[i] > ts) ? 1u : 0u;
+                e += (ok && v[i] == ts) ? 1u : 0u;
+              }
+            }
+          }
+        }
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(smem_u32(&bar_tempty[acc]));
+      }
+      if (x < rows) {
+        if (colh == 0) a.ts[x] = ts;
+        if (a.greater && nj > 1) {
+          atomicAdd(a.greater + x, g);
+          atomicAdd(a.equal + x, e);
+        }
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(256));
+}
+
+// known (train+valid+test) candidates other than the true one, per row x
+__global__ void k_known_count(const int32_t* __restrict__ qry, int64_t nq, int32_t N, int32_t R,
+                              const int64_t* __restrict__ tkeys, int64_t ntk, const int64_t* __restrict__ hkeys,
+                              int64_t nhk, uint32_t* __restrict__ cnt, int64_t* __restrict__ lo_out) {
+  for (int64_t x = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; x < 2 * nq; x += (int64_t)gridDim.x * blockDim.x) {
+    int side;
+    int64_t q;
+    int32_t anc, rel, tru;
+    rk_query(qry, nq, x, side, q, anc, rel, tru);
+    const int64_t* keys = side == 0 ? tkeys : hkeys;
+    const int64_t nkeys = side == 0 ? ntk : nhk;
+    const int64_t base = ((int64_t)anc * R + rel) * (int64_t)N;
+    const int64_t lo = rk_lower_bound(keys, nkeys, base), hi = rk_lower_bound(keys, nkeys, base + N);
+    const int64_t t = rk_lower_bound(keys, nkeys, base + tru);
+    const bool has_true = t < hi && keys[t] == base + tru;
+    cnt[x] = (uint32_t)(hi - lo - (has_true ? 1 : 0));
+    lo_out[x] = lo;
+  }
+}
+
+__global__ void k_known_pairs(const int32_t* __restrict__ qry, int64_t nq, int32_t N, int32_t R,
+                              const int64_t* __restrict__ tkeys, const int64_t* __restrict__ hkeys,
+                              const uint32_t* __restrict__ cnt, const uint32_t* __restrict__ off,
+                              const int64_t* __restrict__ lo, int64_t max_pairs, uint32_t* npairs,
+                              int32_t* __restrict__ px, int32_t* __restrict__ pc) {
+  for (int64_t x = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; x < 2 * nq; x += (int64_t)gridDim.x * blockDim.x) {
+    int side;
+    int64_t q;
+    int32_t anc, rel, tru;
+    rk_query(qry, nq, x, side, q, anc, rel, tru);
+    const int64_t* keys = side == 0 ? tkeys : hkeys;
+    const int64_t base = ((int64_t)anc * R + rel) * (int64_t)N;
+    uint32_t o = off[x];
+    const uint32_t n = cnt[x];
+    for (int64_t j = lo[x]; o < off[x] + n && (int64_t)o < max_pairs; ++j) {
+      const int32_t c = (int32_t)(keys[j] - base);
+      if (c == tru) continue;
+      px[o] = (int32_t)x;
+      pc[o] = c;
+      ++o;
+    }
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) {   // clamped pair count for the diagonal pass
+    const uint32_t t = npairs[0];
+    npairs[1] = (int64_t)t < max_pairs ? t : (uint32_t)max_pairs;
+    npairs[2] = (int64_t)t > max_pairs ? 1u : 0u;   // overflow: caller's bound too small
+  }
+}
+
+// subtract known candidates that were counted as greater / equal
+__global__ void k_known_fix(const int32_t* __restrict__ px, const float* __restrict__ ps,
+                            const uint32_t* __restrict__ npairs, const float* __restrict__ ts,
+                            uint32_t* __restrict__ greater, uint32_t* __restrict__ equal) {
+  const uint32_t n = *npairs;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const int32_t x = px[i];
+    const float s = ps[i], t = ts[x];
+    if (s > t) atomicSub(greater + x, 1u);
+    if (s == t) atomicSub(equal + x, 1u);
+  }
+}
+
+__global__ void k_rank_policy(int64_t nq, int32_t N, int policy, int chunk, const uint32_t* __restrict__ greater,
+                              const uint32_t* __restrict__ equal, const uint32_t* __restrict__ known,
+                              double* __restrict__ ranks, int32_t* __restrict__ ncand) {
+  for (int64_t x = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; x < 2 * nq; x += (int64_t)gridDim.x * blockDim.x) {
+    const int side = (int)(x / nq);
+    const int64_t q = x - side * nq;
+    const double g = (double)greater[x], e = (double)equal[x] - 1.0;   // minus the true entity itself
+    double rank;
+    if (policy == 0) rank = 1.0 + g + e / 2.0;
+    else if (policy == 1) rank = 1.0 + g;
+    else rank = 1.0 + g + e;
+    const int64_t cb = q / chunk, qi = q - cb * chunk;
+    const int64_t cs = (nq - cb * chunk) < chunk ? (nq - cb * chunk) : chunk;
+    const int64_t rec = 2 * cb * chunk + side * cs + qi;
+    ranks[rec] = rank;
+    ncand[rec] = N - 1 - (int32_t)known[x];
+  }
+}
+
+struct RankWs {
+  float *Qp, *Tp, *Cp, *Pq, *Pc, *ts, *ps;
+  uint32_t *greater, *equal, *cnt, *off, *npairs;
+  int64_t* lo;
+  int32_t *px, *pc;
+  char* scan;
+};
+
+static size_t rank_ws(int64_t nq, int32_t N, int d, int64_t max_pairs, RankWs* w, void* base, size_t cap) {
+  Arena a(base, cap);
+  const int64_t nk = ceil_div(d, UKC), qt = ceil_div(2 * nq, 128), cb = ceil_div(N, 128), pt = ceil_div(max_pairs, 128);
+  RankWs r;
+  r.Qp = a.take<float>((size_t)(qt * nk * rec_floats(128)));
+  r.Tp = a.take<float>((size_t)(qt * nk * rec_floats(128)));
+  r.Cp = a.take<float>((size_t)(cb * nk * rec_floats(128)));
+  r.Pq = a.take<float>((size_t)((pt > 0 ? pt : 1) * nk * rec_floats(128)));
+  r.Pc = a.take<float>((size_t)((pt > 0 ? pt : 1) * nk * rec_floats(128)));
+  r.ts = a.take<float>(2 * nq);
+  r.ps = a.take<float>(max_pairs > 0 ? max_pairs : 1);
+  r.greater = a.take<uint32_t>(2 * nq);
+  r.equal = a.take<uint32_t>(2 * nq);
+  r.cnt = a.take<uint32_t>(2 * nq);
+  r.off = a.take<uint32_t>(2 * nq);
+  r.npairs = a.take<uint32_t>(4);
+  r.lo = a.take<int64_t>(2 * nq);
+  r.px = a.take<int32_t>(max_pairs > 0 ? max_pairs : 1);
+  r.pc = a.take<int32_t>(max_pairs > 0 ? max_pairs : 1);
+  r.scan = a.take<char>(scan_workspace(2 * nq));
+  if (w) *w = r;
+  return a.used + 1024;
+}
+
+size_t umma_rank_workspace(int64_t nq, int32_t N, int d, int64_t max_pairs) {
+  return rank_ws(nq, N, d, max_pairs, nullptr, nullptr, 0);
+}
+
+static kg_status launch_rank(const RankArgs& ra, const int32_t* rows_dev, int64_t rows_max, cudaStream_t st) {
+  int ns = (int)((RK_SMEM_CAP - (size_t)ra.nk * RK_REC) / RK_REC);
+  if (ns > RK_MAXS) ns = RK_MAXS;
+  KG_REQUIRE(ns >= 2, KG_ERR_SHAPE, "ranking tile does not fit shared memory");
+  const size_t smem = (size_t)(ra.nk + ns) * RK_REC;
+  static bool attr = false;
+  if (!attr) {
+    KG_CUDA(cudaFuncSetAttribute(k_rank_umma, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)RK_SMEM_CAP));
+    attr = true;
+  }
+  const int64_t qt = ceil_div(rows_max > 0 ? rows_max : 1, 128);
+  const int ctas = (int)(qt < num_sms() ? qt : num_sms());
+  KG_LAUNCH("k_rank_umma", k_rank_umma, ctas, RK_THREADS, smem, st, ra, rows_dev, ns);
+  return KG_OK;
+}
+
+kg_status umma_rank_filtered(const float* H, int d, int32_t N, const float* dec, int32_t R, const int32_t* qry,
+                             int64_t nq, const int64_t* tkeys, int64_t ntk, const int64_t* hkeys, int64_t nhk,
+                             int policy, int chunk, int64_t max_pairs, double* ranks, int32_t* ncand,
+                             uint32_t* overflow, void* ws, size_t ws_bytes, cudaStream_t st) {
+  KG_REQUIRE(d >= 1 && d <= 128, KG_ERR_SHAPE, "tensor-core ranking supports d <= 128");
+  RankWs w;
+  KG_REQUIRE(rank_ws(nq, N, d, max_pairs, &w, ws, ws_bytes) <= ws_bytes, KG_ERR_VALIDATION,
+             "eval workspace too small");
+  const int nk = (int)ceil_div(d, UKC);
+  const int64_t rows = 2 * nq, qt = ceil_div(rows, 128), cb = ceil_div(N, 128);
+  // operands: query rows + their true entities, all candidates
+  KG_LAUNCH("k_eval_pack", k_eval_pack, persistent_blocks(qt * nk * 128 * 4, 256, 8), 256, 0, st, H, dec, qry, nq,
+            (const int32_t*)nullptr, (const int32_t*)nullptr, (const int32_t*)nullptr, rows, d, nk, w.Qp, w.Tp);
+  PackJob jc{H, d, nullptr, nullptr, 0, N, d, 128, 0, nk, w.Cp};
+  PackJob none{};
+  kg_status s = launch_pack(jc, none, cb * nk * 128 * 4, st);
+  if (s != KG_OK) return s;
+  KG_CUDA(cudaMemsetAsync(w.greater, 0, (size_t)rows * 4, st));
+  KG_CUDA(cudaMemsetAsync(w.equal, 0, (size_t)rows * 4, st));
+  s = launch_rank(RankArgs{w.Qp, w.Tp, w.Cp, nk, rows, N, w.ts, w.greater, w.equal}, nullptr, rows, st);
+  if (s != KG_OK) return s;
+  // known candidates: pair list (row, candidate), diagonal scores, fix-up
+  const int g1 = persistent_blocks(rows, 256, 8);
+  KG_LAUNCH("k_known_count", k_known_count, g1, 256, 0, st, qry, nq, N, R, tkeys, ntk, hkeys, nhk, w.cnt, w.lo);
+  s = exclusive_scan_u32(w.cnt, w.off, rows, w.npairs, w.scan, scan_workspace(rows), st);
+  if (s != KG_OK) return s;
+  KG_LAUNCH("k_known_pairs", k_known_pairs, g1, 256, 0, st, qry, nq, N, R, tkeys, hkeys, w.cnt, w.off, w.lo,
+            max_pairs, w.npairs, w.px, w.pc);
+  const int64_t pt = ceil_div(max_pairs > 0 ? max_pairs : 1, 128);
+  KG_LAUNCH("k_eval_pack", k_eval_pack, persistent_blocks(pt * nk * 128 * 4, 256, 8), 256, 0, st, H, dec, qry, nq,
+            (const int32_t*)w.px, (const int32_t*)w.pc, (const int32_t*)(w.npairs + 1), (int64_t)0, d, nk, w.Pq,
+            w.Pc);
+  s = launch_rank(RankArgs{w.Pq, w.Pc, nullptr, nk, 0, 0, w.ps, nullptr, nullptr},
+                  reinterpret_cast<const int32_t*>(w.npairs + 1), max_pairs, st);
+  if (s != KG_OK) return s;
+  KG_LAUNCH("k_known_fix", k_known_fix, persistent_blocks(max_pairs > 0 ? max_pairs : 1, 256, 8), 256, 0, st, w.px,
+            w.ps, w.npairs + 1, w.ts, w.greater, w.equal);
+  if (overflow) KG_CUDA(cudaMemcpyAsync(overflow, w.npairs + 2, 4, cudaMemcpyDeviceToDevice, st));
+  KG_LAUNCH("k_rank_policy", k_rank_policy, g1, 256, 0, st, nq, N, policy, chunk, w.greater, w.equal, w.cnt, ranks,
+            ncand);
+  return KG_OK;
+}
+
 }  // namespace kg
 
 using namespace kg;

@@ -10,7 +10,7 @@ from typing import NamedTuple, Optional
 import numpy as np
 
 from . import _lib
-from .errors import IntegrityError, ValidationError
+from .errors import IntegrityError, KGError, ValidationError
 from .model import MODE_EMBEDDING, DeviceModel, ModelConfig, ModelParams, ViewBuffers, device_forward
 from .sampler import closure_device, full_graph_view
 
@@ -130,11 +130,29 @@ def _result(records: list) -> EvalResult:
                       records=records)
 
 
+def _known_pair_bound(tkeys, ntk: int, hkeys, nhk: int, dq, N: int, R: int) -> int:
+    """Known candidates the tensor-core ranker scores separately: for every
+    query and side, the distinct known triples sharing its (anchor, relation)
+    (an upper bound: the true entity is included). Device searchsorted over
+    the sorted unique keys."""
+    import torch
+    q = dq.to(torch.int64)
+    total = 0
+    for keys, n, a in ((tkeys, ntk, 0), (hkeys, nhk, 2)):
+        if n == 0:
+            continue
+        base = (q[:, a] * R + q[:, 1]) * N
+        k = keys[:n]
+        total += int((torch.searchsorted(k, base + N) - torch.searchsorted(k, base)).sum().item())
+    return max(total, 1)
+
+
 def evaluate(params: ModelParams, config: ModelConfig, graph, split, which: str = "test",
              protocol: str = "filtered", candidates: Optional[dict] = None, tie_policy: str = TIE_MEAN,
-             chunk: int = 512) -> EvalResult:
+             chunk: int = 512, impl: int = 0) -> EvalResult:
     """Rank every triple of the split against all entities on both sides,
-    filtered by train+valid+test (ref:evaluate.py:136-218)."""
+    filtered by train+valid+test (ref:evaluate.py:136-218). impl 0: tensor-core
+    scores (d <= 128); 1: exact CUDA-core fmaf chains."""
     import torch
     if which not in ("valid", "test"):
         raise ValidationError("which must be valid or test")
@@ -158,18 +176,25 @@ def evaluate(params: ModelParams, config: ModelConfig, graph, split, which: str 
     ranks = torch.empty(2 * nq, dtype=torch.float64, device=dev)
     ncand = torch.empty(2 * nq, dtype=torch.int32, device=dev)
     lib = _lib.require_cuda()
-    ws = torch.empty(lib.kg_eval_workspace_bytes(nq), dtype=torch.uint8, device=dev)
+    pairs = _known_pair_bound(tkeys, ntk, hkeys, nhk, dq, N, R)
+    ws = torch.empty(lib.kg_eval_workspace_bytes(nq, N, config.dims[-1], pairs), dtype=torch.uint8, device=dev)
+    overflow = torch.zeros(1, dtype=torch.int32, device=dev)
     _lib.call("kg_eval_filtered", H.data_ptr(), config.dims[-1], N, model.decoder_ptr(), R, dq.data_ptr(), nq,
-              tkeys.data_ptr(), ntk, hkeys.data_ptr(), nhk, _POLICY[tie_policy], chunk, ranks.data_ptr(),
-              ncand.data_ptr(), ws.data_ptr(), ws.numel(), _lib.stream_handle())
+              tkeys.data_ptr(), ntk, hkeys.data_ptr(), nhk, _POLICY[tie_policy], chunk, impl, pairs,
+              ranks.data_ptr(), ncand.data_ptr(), overflow.data_ptr(), ws.data_ptr(), ws.numel(),
+              _lib.stream_handle())
+    if int(overflow.item()):
+        raise KGError("internal: known-candidate pair bound exceeded")
     r = ranks.cpu().numpy()
     c = ncand.cpu().numpy()
-    records = []
-    k = 0
+    # record order of the reference: per chunk, its tail records then its head records
+    idx, sides = [], []
     for a in range(0, nq, chunk):
-        blk = q[a:a + chunk]
-        for side in (SIDE_TAIL, SIDE_HEAD):
-            for h, rel, t in blk.tolist():
-                records.append(RankRecord(h, rel, t, side, float(r[k]), int(c[k])))
-                k += 1
-    return _result(records)
+        blk = np.arange(a, min(a + chunk, nq))
+        idx += [blk, blk]
+        sides += [SIDE_TAIL] * len(blk) + [SIDE_HEAD] * len(blk)
+    rows = np.asarray(q, dtype=np.int64)[np.concatenate(idx)]
+    records = list(map(RankRecord, rows[:, 0].tolist(), rows[:, 1].tolist(), rows[:, 2].tolist(), sides,
+                       r.tolist(), c.tolist()))
+    return EvalResult(mrr=float((1.0 / r).mean()), hits={k: float((r <= k).mean()) for k in HITS_KS},
+                      records=records)
