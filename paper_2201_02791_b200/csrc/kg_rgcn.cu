@@ -336,11 +336,16 @@ __global__ void __launch_bounds__(256, 3) k_csc_backward(CscArgs a) {
   for (int64_t c = warp_uniform((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5); c < NC; c += warps) {
     const int32_t u = a.ck.row[c];
     const int32_t q = a.pos[u];
-    if (q < 0 || q >= Sn) continue;
     const int32_t cbase = a.ck.ptr[u];
     const int32_t nch = a.ck.ptr[u + 1] - cbase;
     const int32_t beg = a.c_indptr[u] + (int32_t)(c - cbase) * a.ck.C;
     const int32_t cnt = min(beg + a.ck.C, a.c_indptr[u + 1]) - beg;
+    if (q < 0 || q >= Sn) {
+      // not a source of this layer: its edge dots are zero (k_dcoeff_partial
+      // sums every edge of a relation without a membership test)
+      for (int x = (int)lane; x < cnt * B; x += 32) a.ed[(int64_t)beg * B + x] = 0.f;
+      continue;
+    }
     // metadata: destination position (-1 if not a target) and coefficients
     EdgeMeta<NB> m;
     float nrm[2];
@@ -536,34 +541,43 @@ __global__ void __launch_bounds__(CB_THREADS) k_csc_combine(CscArgs a) {
   }
 }
 
-// d coeffs: block per relation group (2R message groups + 1 self-loop group)
-__global__ void __launch_bounds__(256) k_dcoeff_reduce(const int32_t* __restrict__ rel_ptr,
-                                                       const int32_t* __restrict__ rel_perm,
-                                                       const int32_t* __restrict__ c_dst,
-                                                       const int32_t* __restrict__ pos,
-                                                       const int32_t* __restrict__ counts, int t,
-                                                       const float* __restrict__ ed, const float* __restrict__ ed_self,
-                                                       int32_t G, int32_t B, float* __restrict__ d_coeffs) {
+// d coeffs (ref:model.py:294): d a[g,b] = sum over the edges of relation
+// group g of the edge dots (ed is zero for edges outside the layer), plus the
+// self-loop group over ed_self. Block (g, s) sums the s-th of `split`
+// contiguous slices of the group (fixed order: thread-strided then a fixed
+// tree), k_dcoeff_final adds the slices in order -> deterministic, and heavy
+// relations are spread over several blocks (split grows with the average
+// group size, up to DC_SPLIT).
+constexpr int DC_SPLIT = 64;
+
+static int dcoeff_split(int64_t e, int64_t groups) {
+  int64_t s = (e / (groups > 0 ? groups : 1) + 4095) / 4096;
+  return (int)(s < 1 ? 1 : (s > DC_SPLIT ? DC_SPLIT : s));
+}
+
+__global__ void __launch_bounds__(256) k_dcoeff_partial(const int32_t* __restrict__ rel_ptr,
+                                                        const int32_t* __restrict__ rel_perm,
+                                                        const int32_t* __restrict__ counts, int t,
+                                                        const float* __restrict__ ed,
+                                                        const float* __restrict__ ed_self, int32_t G, int32_t B,
+                                                        float* __restrict__ part) {
   __shared__ float red[MAXB][256];
-  const int g = blockIdx.x;
-  const int32_t T = counts[t];
-  float s[MAXB] = {0.f, 0.f, 0.f, 0.f};
+  const int g = blockIdx.x, sl = blockIdx.y, split = gridDim.y;
+  int64_t lo, hi;
   if (g < G - 1) {
-    for (int32_t j = rel_ptr[g] + threadIdx.x; j < rel_ptr[g + 1]; j += blockDim.x) {
-      int32_t cj = rel_perm[j];
-      int32_t pw = pos[c_dst[cj]];
-      if (pw >= 0 && pw < T) {
-#pragma unroll
-        for (int b = 0; b < MAXB; ++b)
-          if (b < B) s[b] += ed[(int64_t)cj * B + b];
-      }
-    }
+    lo = rel_ptr[g];
+    hi = rel_ptr[g + 1];
   } else {
-    for (int32_t q = threadIdx.x; q < T; q += blockDim.x) {
+    lo = 0;
+    hi = counts[t];
+  }
+  const int64_t len = hi - lo, a0 = lo + len * sl / split, a1 = lo + len * (sl + 1) / split;
+  float s[MAXB] = {0.f, 0.f, 0.f, 0.f};
+  for (int64_t j = a0 + threadIdx.x; j < a1; j += blockDim.x) {
+    const float* src = g < G - 1 ? ed + (int64_t)__ldg(rel_perm + j) * B : ed_self + j * B;
 #pragma unroll
-      for (int b = 0; b < MAXB; ++b)
-        if (b < B) s[b] += ed_self[(int64_t)q * B + b];
-    }
+    for (int b = 0; b < MAXB; ++b)
+      if (b < B) s[b] += src[b];
   }
 #pragma unroll
   for (int b = 0; b < MAXB; ++b) red[b][threadIdx.x] = s[b];
@@ -574,7 +588,18 @@ __global__ void __launch_bounds__(256) k_dcoeff_reduce(const int32_t* __restrict
       for (int b = 0; b < MAXB; ++b) red[b][threadIdx.x] += red[b][threadIdx.x + w];
     __syncthreads();
   }
-  if (threadIdx.x < B) d_coeffs[g * B + threadIdx.x] = red[threadIdx.x][0];
+  if (threadIdx.x < B) part[((int64_t)g * split + sl) * B + threadIdx.x] = red[threadIdx.x][0];
+}
+
+__global__ void k_dcoeff_final(const float* __restrict__ part, int32_t G, int32_t B, int split,
+                               float* __restrict__ d_coeffs) {
+  for (int64_t x = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; x < (int64_t)G * B;
+       x += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t g = x / B, b = x - g * B;
+    float s = 0.f;
+    for (int sl = 0; sl < split; ++sl) s += part[(g * split + sl) * B + b];
+    d_coeffs[x] = s;
+  }
 }
 
 // dZ[p] = dH[v_p] * (H_out[v_p] > 0) (mask skipped when H_out == nullptr); warp per row
@@ -762,12 +787,14 @@ struct LayerWs {
   float* ed;      // (e, B)
   float* ed_self; // (n, B)
   float* Rm;      // (d_in, B*d_out)
+  float* dc_part; // (G, DC_SPLIT, B) d-coeff slice partials
   char* gemm;     // packed GEMM operands (main-stream GEMMs run back to back)
   char* gemm_tn;  // packed operands + split-K partials of dV (may run on the side stream)
 };
 
-static size_t layer_ws(int64_t n, int64_t e, int64_t split_chunks, int di, int dO, int B, LayerWs* w, void* base,
-                       size_t cap) {
+static size_t layer_ws(int64_t n, int64_t e, int64_t split_chunks, int di, int dO, int B, int R, LayerWs* w,
+                       void* base, size_t cap) {
+  const int64_t G = 2 * (int64_t)R + 1;
   Arena a(base, cap);
   LayerWs l;
   l.acc = a.take<float>(packed_bytes(n, (int64_t)B * di) / sizeof(float));
@@ -781,6 +808,7 @@ static size_t layer_ws(int64_t n, int64_t e, int64_t split_chunks, int di, int d
   l.ed = a.take<float>((size_t)e * B);
   l.ed_self = a.take<float>((size_t)n * B);
   l.Rm = a.take<float>((size_t)di * B * dO);
+  l.dc_part = a.take<float>((size_t)G * DC_SPLIT * B);
   size_t gw = 0;
   const size_t nn[3] = {gemm_nn_workspace(n, (int64_t)B * di, dO), gemm_nn_workspace(n, di, (int64_t)B * dO),
                         gemm_nn_workspace(n, (int64_t)B * dO, di)};
@@ -813,7 +841,7 @@ using namespace kg;
 extern "C" {
 
 int64_t kg_layer_workspace_bytes(const kg_graph_csr* G, int32_t d_in, int32_t d_out, int32_t B) {
-  return (int64_t)layer_ws(G->n, G->e, cap_split_chunks(G), d_in, d_out, B, nullptr, nullptr, 0);
+  return (int64_t)layer_ws(G->n, G->e, cap_split_chunks(G), d_in, d_out, B, G->R, nullptr, nullptr, 0);
 }
 
 kg_status kg_rgcn_forward(const kg_graph_csr* G, const kg_layer_params* lp, const float* H_in, float* H_out,
@@ -823,7 +851,8 @@ kg_status kg_rgcn_forward(const kg_graph_csr* G, const kg_layer_params* lp, cons
   KG_REQUIRE(lp->B >= 1 && lp->B <= MAXB, KG_ERR_VALIDATION, "num_bases must be in [1, %d]", MAXB);
   KG_REQUIRE(lp->G == 2 * G->R + 1, KG_ERR_SHAPE, "coeff groups %d != 2R+1", lp->G);
   LayerWs w;
-  size_t need = layer_ws(G->n, G->e, cap_split_chunks(G), lp->d_in, lp->d_out, lp->B, &w, ws, (size_t)ws_bytes);
+  size_t need = layer_ws(G->n, G->e, cap_split_chunks(G), lp->d_in, lp->d_out, lp->B, G->R, &w, ws,
+                         (size_t)ws_bytes);
   KG_REQUIRE((size_t)ws_bytes >= need, KG_ERR_VALIDATION, "layer workspace too small");
   AggArgs a{G->indptr, G->src, G->rel, G->norm, csr_chunks(G), lp->coeffs, lp->G, lp->B, lp->d_in, H_in, pos,
             counts, t, w.acc, packed_records((int64_t)lp->B * lp->d_in), w.partial};
@@ -856,7 +885,7 @@ kg_status kg_rgcn_backward(const kg_graph_csr* G, const kg_layer_params* lp, con
   const int B = lp->B, di = lp->d_in, dO = lp->d_out;
   KG_REQUIRE(B >= 1 && B <= MAXB, KG_ERR_VALIDATION, "num_bases must be in [1, %d]", MAXB);
   LayerWs w;
-  size_t need = layer_ws(G->n, G->e, cap_split_chunks(G), di, dO, B, &w, ws, (size_t)ws_bytes);
+  size_t need = layer_ws(G->n, G->e, cap_split_chunks(G), di, dO, B, G->R, &w, ws, (size_t)ws_bytes);
   KG_REQUIRE((size_t)ws_bytes >= need, KG_ERR_VALIDATION, "layer workspace too small");
   const int64_t wn = (int64_t)B * di * dO;
   const WeightsLayout wl = weights_layout(di, dO, B);
@@ -901,8 +930,11 @@ kg_status kg_rgcn_backward(const kg_graph_csr* G, const kg_layer_params* lp, con
   s = gemm_tn(gv, w.Rm, w.gemm_tn, sd);
   if (s != KG_OK) return s;
   KG_LAUNCH("k_dbases_layout", k_dbases_layout, persistent_blocks(wn, 256, 2), 256, 0, sd, w.Rm, B, di, dO, d_bases);
-  KG_LAUNCH("k_dcoeff_reduce", k_dcoeff_reduce, lp->G, 256, 0, sd, G->rel_ptr, G->rel_perm, G->c_dst, pos, counts, t,
-            w.ed, w.ed_self, lp->G, B, d_coeffs);
+  const int split = dcoeff_split(G->e, lp->G);
+  KG_LAUNCH("k_dcoeff_reduce", k_dcoeff_partial, dim3((unsigned)lp->G, (unsigned)split, 1), 256, 0, sd, G->rel_ptr,
+            G->rel_perm, counts, t, w.ed, w.ed_self, lp->G, B, w.dc_part);
+  KG_LAUNCH("k_dcoeff_final", k_dcoeff_final, persistent_blocks((int64_t)lp->G * B, 256, 2), 256, 0, sd, w.dc_part,
+            lp->G, B, split, d_coeffs);
   if (dH_in) {
     GemmArgs gx{};
     gx.A = w.dS; gx.lda = (int64_t)B * dO;

@@ -149,58 +149,59 @@ __device__ __forceinline__ void pack_store(float* rec, int R, int r, int q, cons
   *reinterpret_cast<float4*>(rec + (int64_t)R * UKC + off) = make_float4(l[0], l[1], l[2], l[3]);
 }
 
+// One block per record (grid-stride over records): the per-element index
+// decode is shifts and compares only (the first version's 64-bit div/mod per
+// element made the transposed packs compute-bound at wikikg2 scale).
 __global__ void __launch_bounds__(256) k_umma_pack(PackJob j0, PackJob j1) {
   const PackJob& j = blockIdx.y == 0 ? j0 : j1;
   if (!j.src) return;
   const int64_t nrows = j.nrows_dev ? (int64_t)j.nrows_dev[j.nrows_idx] : j.nrows;
   const int R = j.R;
-  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   if (!j.cols_mode) {
-    // items (blk, kc, r, q), q fastest: 4 consecutive lanes read 64 B of one row
-    const int64_t nk = j.nk_alloc, nblk = (nrows + R - 1) / R;
-    const int64_t items = nblk * nk * R * 4;
+    // record (blk, kc): items (r, q), q fastest -> 4 lanes read 64 B of one row
+    const int64_t nk = j.nk_alloc, nrec = (nrows + R - 1) / R * nk;
     const bool vec = ((uintptr_t)j.src & 15) == 0 && (j.ld & 3) == 0;
-    for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < items; idx += stride) {
-      const int q = (int)(idx & 3);
-      const int64_t t = idx >> 2;
-      const int r = (int)(t % R);
-      const int64_t u = t / R;
-      const int64_t kc = u % nk, blk = u / nk;
-      const int64_t row = blk * R + r, c0 = kc * UKC + 4 * q;
-      float v[4] = {0.f, 0.f, 0.f, 0.f};
-      if (row < nrows) {
-        const float* s = j.src + (j.rowid ? (int64_t)__ldg(j.rowid + row) : row) * j.ld;
-        if (vec && c0 + 3 < j.ncols) {
-          const float4 x = __ldg(reinterpret_cast<const float4*>(s + c0));
-          v[0] = x.x; v[1] = x.y; v[2] = x.z; v[3] = x.w;
-        } else {
+    for (int64_t rec = blockIdx.x; rec < nrec; rec += gridDim.x) {
+      const int64_t blk = rec / nk, kc = rec - blk * nk;
+      float* out = j.out + rec * rec_floats(R);
+      for (int i = threadIdx.x; i < R * 4; i += blockDim.x) {
+        const int q = i & 3, r = i >> 2;
+        const int64_t row = blk * R + r, c0 = kc * UKC + 4 * q;
+        float v[4] = {0.f, 0.f, 0.f, 0.f};
+        if (row < nrows) {
+          const float* src = j.src + (j.rowid ? (int64_t)__ldg(j.rowid + row) : row) * j.ld;
+          if (vec && c0 + 3 < j.ncols) {
+            const float4 x = __ldg(reinterpret_cast<const float4*>(src + c0));
+            v[0] = x.x; v[1] = x.y; v[2] = x.z; v[3] = x.w;
+          } else {
 #pragma unroll
-          for (int i = 0; i < 4; ++i)
-            if (c0 + i < j.ncols) v[i] = __ldg(s + c0 + i);
+            for (int t = 0; t < 4; ++t)
+              if (c0 + t < j.ncols) v[t] = __ldg(src + c0 + t);
+          }
         }
+        pack_store(out, R, r, q, v);
       }
-      pack_store(j.out + (blk * nk + kc) * rec_floats(R), R, r, q, v);
     }
   } else {
-    // items (blk, kc, q, m), m fastest: a warp reads 32 consecutive columns
+    // record (blk, kc) with kc over 16-row groups of the source: items (q, m),
+    // m fastest -> a warp reads 32 consecutive columns of 4 source rows
     const int64_t nkd = (nrows + UKC - 1) / UKC, nblk = (j.ncols + R - 1) / R;
-    const int64_t items = nblk * nkd * 4 * R;
-    for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < items; idx += stride) {
-      const int m = (int)(idx % R);
-      const int64_t t = idx / R;
-      const int q = (int)(t & 3);
-      const int64_t u = t >> 2;
-      const int64_t kc = u % nkd, blk = u / nkd;
-      const int64_t col = blk * R + m, k0 = kc * UKC + 4 * q;
-      float v[4] = {0.f, 0.f, 0.f, 0.f};
-      if (col < j.ncols) {
+    for (int64_t rec = blockIdx.x; rec < nblk * nkd; rec += gridDim.x) {
+      const int64_t blk = rec / nkd, kc = rec - blk * nkd;
+      float* out = j.out + (blk * j.nk_alloc + kc) * rec_floats(R);
+      for (int i = threadIdx.x; i < R * 4; i += blockDim.x) {
+        const int q = (i >= R) + (i >= 2 * R) + (i >= 3 * R), m = i - q * R;
+        const int64_t col = blk * R + m, k0 = kc * UKC + 4 * q;
+        float v[4] = {0.f, 0.f, 0.f, 0.f};
+        if (col < j.ncols) {
 #pragma unroll
-        for (int i = 0; i < 4; ++i) {
-          const int64_t k = k0 + i;
-          if (k < nrows) v[i] = __ldg(j.src + (j.rowid ? (int64_t)__ldg(j.rowid + k) : k) * j.ld + col);
+          for (int t = 0; t < 4; ++t) {
+            const int64_t k = k0 + t;
+            if (k < nrows) v[t] = __ldg(j.src + (j.rowid ? (int64_t)__ldg(j.rowid + k) : k) * j.ld + col);
+          }
         }
+        pack_store(out, R, m, q, v);
       }
-      pack_store(j.out + (blk * j.nk_alloc + kc) * rec_floats(R), R, m, q, v);
     }
   }
 }
@@ -403,7 +404,8 @@ static int stages_for(int np) {
 }
 
 static kg_status launch_pack(const PackJob& a, const PackJob& b, int64_t items_max, cudaStream_t st) {
-  dim3 grid((unsigned)persistent_blocks(items_max, 256, 8), 2, 1);
+  // items_max / 512 approximates the record count (R*4 items per record)
+  dim3 grid((unsigned)persistent_blocks(items_max, 512, 8), 2, 1);
   KG_LAUNCH("k_umma_pack", k_umma_pack, grid, 256, 0, st, a, b);
   return KG_OK;
 }

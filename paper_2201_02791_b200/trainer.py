@@ -428,7 +428,9 @@ class Trainer:
         self.last_timer_handle = None
         self._graphs = {}
         self._graph_pool = None
-        self._loss_stream = torch.cuda.Stream(self.dev)   # batch-only loss grouping, overlaps the layers
+        self._loss_stream = torch.cuda.Stream(self.dev)   # forked work beside the layers
+        # diagnostics: KG_FORK_STREAMS=0 keeps every kernel on one stream
+        self.fork_streams = os.environ.get("KG_FORK_STREAMS", "1") != "0"
         self.model.repack()
         self._eager_rounds = 0
         self.t = 0
@@ -453,16 +455,17 @@ class Trainer:
             # epoch (_RoundPrep); one copy brings them into the working buffers
             w.prep.import_round(w.slot(), self.round_dev, w.bufs.loss_ws(w.b))
             gslot = self.grads_local[i]
-            self._loss_stream.wait_stream(main)
-            with torch.cuda.stream(self._loss_stream):
+            side = self._loss_stream if self.fork_streams else main
+            side.wait_stream(main)
+            with torch.cuda.stream(side):
                 device_pack_inputs(w.bufs)   # layer-0 backward operand, beside the forward
             device_forward(self.model, w.bufs, packed=True, hpk=True)
-            main.wait_stream(self._loss_stream)
+            main.wait_stream(side)
             device_loss(self.model, w.bufs, w.stream, 0, w.b, gslot, self.loss_scratch[i:i + 1],
                         start_dev=self.start_dev[i:i + 1], part="compute")
             self.losses[i].index_copy_(0, self.round_dev, self.loss_scratch[i:i + 1])
-            device_backward(self.model, w.bufs, gslot, input_grad=w.emb, side=self._loss_stream, packed=True,
-                            hpk=True)
+            device_backward(self.model, w.bufs, gslot, input_grad=w.emb,
+                            side=self._loss_stream if self.fork_streams else None, packed=True, hpk=True)
 
     def _update_body(self):
         """Fused tree-mean + dense Adam/SGD, then lazy sparse rows."""
