@@ -21,6 +21,8 @@
 // dependency between messages.
 #include "kg_gemm.cuh"
 
+#include <stdlib.h>
+
 namespace kg {
 
 constexpr int MAXB = 4;
@@ -188,17 +190,21 @@ __global__ void __launch_bounds__(256, 3) k_aggregate(AggArgs a) {
               for (int cc = 0; cc < VEC; ++cc) acc[b][s][cc] = fmaf(cf, xv[s][cc], acc[b][s][cc]);
         }
       }
-      // finished row: straight into the GEMM's packed hi/lo A records
+      if (a.acc_nk) {
+        // finished row: straight into the GEMM's packed hi/lo A records
 #pragma unroll
-      for (int b = 0; b < NB; ++b)
-        if (b < B)
+        for (int b = 0; b < NB; ++b)
+          if (b < B)
 #pragma unroll
-          for (int s = 0; s < S; ++s)
-            if (slot_ok[s]) packed_store<VEC>(a.acc, a.acc_nk, p, b * d + (s * 32 + lane) * VEC, acc[b][s]);
-      packed_zero_pad(a.acc, a.acc_nk, p, B * d, lane, 32);
-      continue;
+            for (int s = 0; s < S; ++s)
+              if (slot_ok[s]) packed_store<VEC>(a.acc, a.acc_nk, p, b * d + (s * 32 + lane) * VEC, acc[b][s]);
+        packed_zero_pad(a.acc, a.acc_nk, p, B * d, lane, 32);
+        continue;
+      }
+      out = a.acc + (int64_t)p * B * d;   // row-major (the GEMM packs it)
+    } else {
+      out = a.partial + (int64_t)a.ck.slot[c] * B * d;
     }
-    out = a.partial + (int64_t)a.ck.slot[c] * B * d;
 #pragma unroll
     for (int b = 0; b < NB; ++b)
       if (b < B)
@@ -290,10 +296,11 @@ __global__ void __launch_bounds__(CB_THREADS) k_aggregate_combine(AggArgs a) {
           const float self = cf * h[i];
           x[i] = tot[i] + self;
         }
-        packed_store<V>(a.acc, a.acc_nk, p, col, x);
+        if (a.acc_nk) packed_store<V>(a.acc, a.acc_nk, p, col, x);
+        else VecIO<V>::store(a.acc + (int64_t)p * width + col, x);
       }
     }
-    if (threadIdx.x < 32) packed_zero_pad(a.acc, a.acc_nk, p, width, threadIdx.x, 32);
+    if (a.acc_nk && threadIdx.x < 32) packed_zero_pad(a.acc, a.acc_nk, p, width, threadIdx.x, 32);
   }
 }
 
@@ -827,6 +834,17 @@ static cudaEvent_t fork_event() {
   return ev;
 }
 
+// Producers write packed GEMM records only while they stay L2-resident: a
+// row-at-a-time producer fills each 128-byte core-matrix line 16 bytes at a
+// time, which costs DRAM read-modify-writes once the operand spills to HBM
+// (then the row-major output + one coalesced pack pass is cheaper).
+// KG_DIRECT_PACK_MAX_MB overrides the 48 MB limit (tests exercise both paths).
+static bool direct_pack(int64_t rows, int64_t K) {
+  const char* env = getenv("KG_DIRECT_PACK_MAX_MB");
+  const size_t limit = (env ? (size_t)atoll(env) : size_t(48)) << 20;
+  return packed_bytes(rows, K) <= limit;
+}
+
 static Chunks csr_chunks(const kg_graph_csr* G) {
   return Chunks{G->ck_ptr, G->ck_row, G->ck_slot, G->ck_split, G->ck_counts, G->chunk};
 }
@@ -855,11 +873,13 @@ kg_status kg_rgcn_forward(const kg_graph_csr* G, const kg_layer_params* lp, cons
                          (size_t)ws_bytes);
   KG_REQUIRE((size_t)ws_bytes >= need, KG_ERR_VALIDATION, "layer workspace too small");
   AggArgs a{G->indptr, G->src, G->rel, G->norm, csr_chunks(G), lp->coeffs, lp->G, lp->B, lp->d_in, H_in, pos,
-            counts, t, w.acc, packed_records((int64_t)lp->B * lp->d_in), w.partial};
+            counts, t, w.acc, direct_pack(G->n, (int64_t)lp->B * lp->d_in) ? packed_records((int64_t)lp->B * lp->d_in) : 0,
+            w.partial};
   kg_status s = run_aggregate(a, G, st);
   if (s != KG_OK) return s;
   GemmArgs g{};
-  g.a_packed = w.acc;
+  if (a.acc_nk) g.a_packed = w.acc;
+  else g.A = w.acc;
   g.lda = (int64_t)lp->B * lp->d_in;
   g.B = lp->bases;   // (B*d_in, d_out)
   g.ldb = lp->d_out;
@@ -910,7 +930,8 @@ kg_status kg_rgcn_backward(const kg_graph_csr* G, const kg_layer_params* lp, con
   kg_status s = gemm_nn(gy, w.gemm, st);
   if (s != KG_OK) return s;
   CscArgs c{G->c_indptr, G->c_dst, G->c_rel, G->c_norm, csc_chunks(G), lp->coeffs, lp->G, B, dO, w.Y, w.dZ, pos,
-            counts, t, w.dS, w.ed, w.ed_self, w.partial, w.dS_pk, packed_records((int64_t)B * dO)};
+            counts, t, w.dS, w.ed, w.ed_self, w.partial,
+            direct_pack(G->n, (int64_t)B * dO) ? w.dS_pk : nullptr, packed_records((int64_t)B * dO)};
   s = run_csc(c, G, st);
   if (s != KG_OK) return s;
   // The parameter gradients (dV, d coeffs) feed only the optimizer: with a side
@@ -938,7 +959,7 @@ kg_status kg_rgcn_backward(const kg_graph_csr* G, const kg_layer_params* lp, con
   if (dH_in) {
     GemmArgs gx{};
     gx.A = w.dS; gx.lda = (int64_t)B * dO;
-    gx.a_packed = w.dS_pk;
+    gx.a_packed = c.dS_pk;   // nullptr: the GEMM packs dS itself
     gx.B = w.Wb; gx.ldb = di;
     gx.C = dH_in; gx.ldc = di; gx.c_rows = order;
     gx.M_dev = counts; gx.M_dev_index = t + 1; gx.M_max = G->n;

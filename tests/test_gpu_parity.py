@@ -286,10 +286,12 @@ def test_cuda_graph_replay_is_bitwise_identical_to_eager():
     np.testing.assert_array_equal(a.entity_embed, b.entity_embed)
 
 
-def test_prepacked_weights_are_bitwise_identical():
+def test_prepacked_weights_are_bitwise_identical(monkeypatch):
     """Forward/backward with the once-per-step packed weight operands
     (DeviceModel.repack) and the producer-packed activations (hpk, dS
-    records) equal on-the-fly packing bit for bit."""
+    records) equal on-the-fly packing bit for bit — with producers writing
+    packed records directly (small operands) or row-major + a pack pass
+    (KG_DIRECT_PACK_MAX_MB=0, the path large graphs take)."""
     from paper_2201_02791_b200.model import device_backward, device_forward, device_loss, device_pack_inputs
     graph, split = kb.generate_synthetic(3000, 40, 12.0, seed=3)
     pset = kb.neighborhood_expand(kb.vertex_cut_partition(graph, 2, seed=0), graph, 2)
@@ -308,7 +310,8 @@ def test_prepacked_weights_are_bitwise_identical():
     ds = DeviceStream(tri, lab, len(batch.triples))
     model.repack()
     out = []
-    for packed in (False, True):
+    for direct_mb, packed in (("48", False), ("48", True), ("0", False), ("0", True)):
+        monkeypatch.setenv("KG_DIRECT_PACK_MAX_MB", direct_mb)
         if packed:
             device_pack_inputs(bufs)
         device_forward(model, bufs, packed=packed, hpk=packed)
@@ -318,8 +321,9 @@ def test_prepacked_weights_are_bitwise_identical():
         device_backward(model, bufs, grad, input_grad=True, packed=packed, hpk=packed)
         torch.cuda.synchronize()
         out.append((bufs.H[2].clone(), grad.clone(), bufs.dH[0].clone(), loss.clone()))
-    for a, b in zip(*out):
-        assert torch.equal(a, b)
+    for other in out[1:]:
+        for a, b in zip(out[0], other):
+            assert torch.equal(a, b)
 
 
 @pytest.mark.parametrize("policy", ["mean", "pessimistic"])
