@@ -188,7 +188,7 @@ __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_gr
 // certainly rejected when (U & mask) > i; the first ambiguous offset is
 // resolved exactly and the window restarts after it. Positions stream through
 // a 4-quarter shared-memory ring filled by cp.async two quarters ahead.
-constexpr int PR = 4;            // positions per lane per window
+constexpr int PR = 8;            // positions per lane per window
 constexpr int PW = 32 * PR;      // window
 
 __global__ void __launch_bounds__(32) k_perm_draws(const uint32_t* __restrict__ U, int64_t W, int64_t n,
@@ -224,7 +224,7 @@ __global__ void __launch_bounds__(32) k_perm_draws(const uint32_t* __restrict__ 
     if (p + PW > W) { ok = false; break; }
     const uint32_t ii = (uint32_t)i;
     const uint32_t mask = smear(ii);
-    if (ii < 2 * PW || smear(ii - (PW - 1)) != mask) {
+    if (ii < 32) {
       // one exact draw for this i (lane 0), broadcast
       int64_t pp = p;
       uint32_t v = 0;
@@ -245,25 +245,30 @@ __global__ void __launch_bounds__(32) k_perm_draws(const uint32_t* __restrict__ 
       i -= 1;
       continue;
     }
+    // draws at offsets < Wl all have indices in [2^k, ii] (one mask): the
+    // window shrinks near a power of two instead of drawing one at a time
+    const int Wl = (int)min((uint32_t)PW, ii - (mask >> 1));
     uint32_t v[PR];
     unsigned acc_b[PR], amb_b[PR];
 #pragma unroll
     for (int r = 0; r < PR; ++r) {
       v[r] = ring[(p + r * 32 + lane) & (RING - 1)] & mask;
       const uint32_t o = r * 32 + lane;
-      const bool acc_sure = v[r] + o <= ii;
+      const bool in = (int)o < Wl;
+      const bool acc_sure = in && v[r] + o <= ii;
       const bool rej_sure = v[r] > ii;
       acc_b[r] = __ballot_sync(0xffffffffu, acc_sure);
-      amb_b[r] = __ballot_sync(0xffffffffu, !acc_sure && !rej_sure);
+      amb_b[r] = __ballot_sync(0xffffffffu, in && !acc_sure && !rej_sure);
     }
     int f = PW;
 #pragma unroll
     for (int r = PR - 1; r >= 0; --r)
       if (amb_b[r]) f = r * 32 + __ffs(amb_b[r]) - 1;
+    const int stop = f < Wl ? f : Wl;   // first position not decided by this window
     int before = 0;   // accepts at offsets < 32r (running over r)
 #pragma unroll
     for (int r = 0; r < PR; ++r) {
-      unsigned lim = (f >= (r + 1) * 32) ? 0xffffffffu : (f <= r * 32 ? 0u : ((1u << (f - r * 32)) - 1u));
+      unsigned lim = (stop >= (r + 1) * 32) ? 0xffffffffu : (stop <= r * 32 ? 0u : ((1u << (stop - r * 32)) - 1u));
       unsigned am = acc_b[r] & lim;
       if ((am >> lane) & 1u) {
         uint32_t il = ii - before - __popc(am & lanemask_lt());
@@ -271,8 +276,8 @@ __global__ void __launch_bounds__(32) k_perm_draws(const uint32_t* __restrict__ 
       }
       before += __popc(am);
     }
-    int taken = PW;
-    if (f < PW) {
+    int taken = Wl;
+    if (f < Wl) {
       uint32_t il_f = ii - before;
       uint32_t vf = 0;
 #pragma unroll
