@@ -246,10 +246,17 @@ def run_ours(args, world, rank, local):
         peaks = json.load(open(pk_path))
     peak = float(peaks.get("hbm_gbs", 6650.0))
     achieved = per_launch_alg / (avg_launch_ms / 1e3) / 1e9 if avg_launch_ms > 0 else None
+    # DRAM bytes per launch of this kernel from one ncu --set full capture of
+    # the same command (tools/ncu_traffic.sh -> profiles/r1_roofline_traffic.json)
+    traffic, traffic_src = None, None
+    tpath = os.path.join(ROOT, "profiles", "r1_roofline_traffic.json")
+    if args.roofline_kernel == "k_aggregate" and os.path.isfile(tpath):
+        tj = json.load(open(tpath))
+        traffic, traffic_src = tj.get("traffic_bytes_per_launch"), tj.get("source")
     roofline = {"bound": "hbm", "kernel": args.roofline_kernel, "achieved": achieved, "peak": peak,
                 "peak_source": "MEASURED_PEAKS.json hbm_gbs" if peaks else "fallback 6650 GB/s",
                 "unit": "GB/s", "frac": (achieved / peak) if achieved else None,
-                "traffic": None, "alg_bytes_per_launch": per_launch_alg,
+                "traffic": traffic, "traffic_source": traffic_src, "alg_bytes_per_launch": per_launch_alg,
                 "avg_launch_ms": avg_launch_ms, "launches_timed": kt_n.value,
                 "kernel_share_of_step": (kt_ms.value / (step_ms)) if step_ms > 0 else None,
                 "note": "FB15k-237 working set is L2-resident (H7): effective bandwidth vs HBM peak"}
