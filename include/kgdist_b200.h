@@ -248,10 +248,13 @@ int64_t kg_layer_workspace_bytes(const kg_graph_csr* g, int32_t d_in, int32_t d_
  * H_out[v] = relu(Z) (relu != 0) or Z. H_in/H_out rows indexed by local id. */
 kg_status kg_rgcn_forward(const kg_graph_csr* g, const kg_layer_params* lp, const float* H_in, float* H_out,
                           const int32_t* vertex_order, const int32_t* pos, const int32_t* counts, int32_t t,
-                          int32_t relu, float* H_out_packed, void* ws, int64_t ws_bytes, void* stream);
-/* H_out_packed (optional, kg_pack_rows_bytes(n, d_out)): the output rows by
- * position p < counts[t] also as tensor-core operand records — exactly what
- * the next layer's kg_rgcn_backward takes as H_in_packed. */
+                          int32_t relu, const float* dropout_mask, float* H_out_packed, void* ws,
+                          int64_t ws_bytes, void* stream);
+/* dropout_mask (optional, kg_dropout_mask, (counts[t], d_out) by position):
+ * H_out = relu(Z) * mask. H_out_packed (optional, kg_pack_rows_bytes(n,
+ * d_out)): the output rows by position p < counts[t] also as tensor-core
+ * operand records — exactly what the next layer's kg_rgcn_backward takes as
+ * H_in_packed. */
 /* ref:model.py:167-185, 286-296: gradients of one layer. dH_out holds
  * dL/dA of the layer output for v in A_t (by local id); H_out (NULL for the
  * last layer) supplies the ReLU mask. Writes d_bases (B,d_in,d_out),
@@ -262,10 +265,11 @@ kg_status kg_rgcn_forward(const kg_graph_csr* g, const kg_layer_params* lp, cons
 kg_status kg_rgcn_backward(const kg_graph_csr* g, const kg_layer_params* lp, const float* H_in,
                            const float* H_out, const float* dH_out, float* dH_in, const int32_t* vertex_order,
                            const int32_t* pos, const int32_t* counts, int32_t t, float* d_bases,
-                           float* d_coeffs, const float* H_in_packed, void* ws, int64_t ws_bytes, void* stream,
-                           void* side_stream);
+                           float* d_coeffs, const float* H_in_packed, const float* dropout_mask, void* ws,
+                           int64_t ws_bytes, void* stream, void* side_stream);
 /* H_in_packed (optional): H_in[vertex_order[p]], p < counts[t+1], as operand
- * records (the previous layer's H_out_packed, or kg_pack_rows). */
+ * records (the previous layer's H_out_packed, or kg_pack_rows).
+ * dropout_mask (optional): the mask this layer's forward applied to H_out. */
 int64_t kg_pack_rows_bytes(int64_t rows, int64_t cols);
 kg_status kg_pack_rows(const float* src, int64_t ld, const int32_t* rowid, const int32_t* counts,
                        int32_t count_index, int64_t n_max, int64_t cols, float* out, void* stream);
@@ -332,6 +336,15 @@ kg_status kg_sparse_step(float* table, float* m, float* v, const float* grad, co
                          const int32_t* counts, int32_t k, int32_t d, int32_t optimizer, float lr,
                          float beta1, float beta2, float eps, double bc1, double bc2, const int64_t* step_dev,
                          int32_t n_max, void* stream);
+
+/* ---------------------------------------------------------------------- */
+/* Dropout (ref:model.py:221-227)                                          */
+/* ---------------------------------------------------------------------- */
+/* mask[j] = (rng.random() >= p) / (1 - p) for j < counts[t] * d (row-major
+ * (T, d) as numpy draws it), then advances g by counts[t] * d next64 draws.
+ * n_max bounds counts[t] for the launch size. */
+kg_status kg_dropout_mask(kg_pcg64* g, const int32_t* counts, int32_t t, int32_t d, double p, int64_t n_max,
+                          float* mask, void* stream);
 
 /* ---------------------------------------------------------------------- */
 /* R24-R26  Filtered evaluation (ref:evaluate.py:93-225)                   */

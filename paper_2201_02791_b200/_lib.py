@@ -86,9 +86,10 @@ _PROTOS = {
                         c_int64, P]),
     "kg_layer_workspace_bytes": (c_int64, [POINTER(KgGraphCsr), c_int32, c_int32, c_int32]),
     "kg_rgcn_forward": (ST, [POINTER(KgGraphCsr), POINTER(KgLayerParams), P, P, P, P, P, c_int32, c_int32,
-                             P, P, c_int64, P]),
+                             P, P, P, c_int64, P]),
     "kg_rgcn_backward": (ST, [POINTER(KgGraphCsr), POINTER(KgLayerParams), P, P, P, P, P, P, P, c_int32,
-                              P, P, P, P, c_int64, P, P]),
+                              P, P, P, P, P, c_int64, P, P]),
+    "kg_dropout_mask": (ST, [P, P, c_int32, c_int32, c_double, c_int64, P, P]),
     "kg_pack_rows_bytes": (c_int64, [c_int64, c_int64]),
     "kg_pack_rows": (ST, [P, c_int64, P, P, c_int32, c_int64, c_int64, P, P]),
     "kg_rgcn_weights_bytes": (c_int64, [c_int32, c_int32, c_int32]),

@@ -22,6 +22,7 @@ struct GemmArgs {
   const float* a_packed;   // NN only: A already in hi/lo records (see packed_store), a_rows ignored
   const float* b_packed;   // NN only: B already in records (N_pad rows, one block; kg_rgcn_pack_weights)
   float* c_packed;         // NN only, optional: the output also as A records by MMA row (K = N)
+  const float* mul;        // NN only, optional: output row m scaled by mul[m*N + n] after ReLU (dropout)
 };
 
 // --- packed tensor-core operand records (kg_umma.cu) -----------------------

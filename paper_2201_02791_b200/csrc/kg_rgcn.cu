@@ -613,7 +613,7 @@ __global__ void k_dcoeff_final(const float* __restrict__ part, int32_t G, int32_
 template <bool V4>
 __global__ void __launch_bounds__(256) k_dz(const float* __restrict__ dH, const float* __restrict__ Hout,
                                             const int32_t* __restrict__ order, const int32_t* __restrict__ counts,
-                                            int t, int d, float* __restrict__ dZ) {
+                                            int t, int d, const float* __restrict__ mask, float* __restrict__ dZ) {
   const int32_t T = counts[t];
   const int lane = lane_id(), nw = (gridDim.x * blockDim.x) >> 5;
   constexpr int V = V4 ? 4 : 1;
@@ -627,6 +627,12 @@ __global__ void __launch_bounds__(256) k_dz(const float* __restrict__ dH, const 
 #pragma unroll
         for (int i = 0; i < V; ++i)
           if (!(h[i] > 0.f)) g[i] = 0.f;
+      }
+      if (mask) {   // dropout on this output: dA/dZ' = mask (then the ReLU test above)
+        float mk[V];
+        VecIO<V>::load(mask + p * d + k, mk);
+#pragma unroll
+        for (int i = 0; i < V; ++i) g[i] *= mk[i];
       }
       VecIO<V>::store(dZ + p * d + k, g);
     }
@@ -864,7 +870,7 @@ int64_t kg_layer_workspace_bytes(const kg_graph_csr* G, int32_t d_in, int32_t d_
 
 kg_status kg_rgcn_forward(const kg_graph_csr* G, const kg_layer_params* lp, const float* H_in, float* H_out,
                           const int32_t* order, const int32_t* pos, const int32_t* counts, int32_t t, int32_t relu,
-                          float* H_out_packed, void* ws, int64_t ws_bytes, void* stream) {
+                          const float* dropout_mask, float* H_out_packed, void* ws, int64_t ws_bytes, void* stream) {
   cudaStream_t st = as_stream(stream);
   KG_REQUIRE(lp->B >= 1 && lp->B <= MAXB, KG_ERR_VALIDATION, "num_bases must be in [1, %d]", MAXB);
   KG_REQUIRE(lp->G == 2 * G->R + 1, KG_ERR_SHAPE, "coeff groups %d != 2R+1", lp->G);
@@ -894,13 +900,15 @@ kg_status kg_rgcn_forward(const kg_graph_csr* G, const kg_layer_params* lp, cons
   g.relu = relu;
   if (lp->packed) g.b_packed = lp->packed + weights_layout(lp->d_in, lp->d_out, lp->B).off[0];
   g.c_packed = H_out_packed;   // next layer's backward Y = H . [V_b] operand, by position
+  g.mul = dropout_mask;        // by position, (counts[t], d_out)
   return gemm_nn(g, w.gemm, st);
 }
 
 kg_status kg_rgcn_backward(const kg_graph_csr* G, const kg_layer_params* lp, const float* H_in, const float* H_out,
                            const float* dH_out, float* dH_in, const int32_t* order, const int32_t* pos,
                            const int32_t* counts, int32_t t, float* d_bases, float* d_coeffs,
-                           const float* H_in_packed, void* ws, int64_t ws_bytes, void* stream, void* side_stream) {
+                           const float* H_in_packed, const float* dropout_mask, void* ws, int64_t ws_bytes,
+                           void* stream, void* side_stream) {
   cudaStream_t st = as_stream(stream);
   const int B = lp->B, di = lp->d_in, dO = lp->d_out;
   KG_REQUIRE(B >= 1 && B <= MAXB, KG_ERR_VALIDATION, "num_bases must be in [1, %d]", MAXB);
@@ -914,10 +922,10 @@ kg_status kg_rgcn_backward(const kg_graph_csr* G, const kg_layer_params* lp, con
               w.Wb);
   if (dO % 4 == 0)
     KG_LAUNCH("k_dz", k_dz<true>, persistent_blocks((int64_t)G->n * 32, 256, 8), 256, 0, st, dH_out, H_out, order,
-              counts, t, dO, w.dZ);
+              counts, t, dO, dropout_mask, w.dZ);
   else
     KG_LAUNCH("k_dz", k_dz<false>, persistent_blocks((int64_t)G->n * 32, 256, 8), 256, 0, st, dH_out, H_out, order,
-              counts, t, dO, w.dZ);
+              counts, t, dO, dropout_mask, w.dZ);
   // Y = X[A_{t+1}] . [V_0 | .. | V_{B-1}]
   GemmArgs gy{};
   gy.A = H_in; gy.lda = di; gy.a_rows = order;

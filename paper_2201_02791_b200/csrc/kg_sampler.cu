@@ -129,6 +129,36 @@ __global__ void k_pcg_advance(kg_pcg64* __restrict__ g, uint64_t delta) {
   g->state_lo = s.lo;
 }
 
+// Inverted dropout (ref:model.py:221-227): keep = rng.random((T, d)) >= p,
+// mask = keep / (1 - p). random() is (next64 >> 11) * 2^-53, one next64 per
+// value in row-major order, so value j sits at stream position j: each thread
+// jumps to its first position and steps. T = counts[t] lives on the device.
+constexpr int DROP_PER_THREAD = 32;
+
+__global__ void k_dropout_mask(const kg_pcg64* __restrict__ gp, const int32_t* __restrict__ counts, int t, int d,
+                               double p, float scale, float* __restrict__ mask) {
+  const kg_pcg64 g = *gp;
+  const u128 s0 = state_of(g), inc = inc_of(g);
+  const int64_t total = (int64_t)counts[t] * d;
+  for (int64_t j0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) * DROP_PER_THREAD; j0 < total;
+       j0 += (int64_t)gridDim.x * blockDim.x * DROP_PER_THREAD) {
+    u128 st = apply_jump(pcg_jump((uint64_t)j0, inc), s0);
+    for (int k = 0; k < DROP_PER_THREAD && j0 + k < total; ++k) {
+      st = pcg_step(st, inc);
+      const double u = (double)(pcg_output(st) >> 11) * (1.0 / 9007199254740992.0);
+      mask[j0 + k] = u >= p ? scale : 0.f;
+    }
+  }
+}
+
+// advance by counts[t] * d next64 draws (after k_dropout_mask)
+__global__ void k_pcg_advance_count(kg_pcg64* __restrict__ g, const int32_t* __restrict__ counts, int t, int d) {
+  const uint64_t delta = (uint64_t)counts[t] * (uint64_t)d;
+  u128 s = apply_jump(pcg_jump(delta, inc_of(*g)), state_of(*g));
+  g->state_hi = s.hi;
+  g->state_lo = s.lo;
+}
+
 // consume `*count` next_uint32 draws; *count < 0 (failed draw) leaves g as is.
 // With `need` set, a zero count while need[0] > 0 means the window was too
 // small: it is flagged as -1 so the host retries with a larger window.
@@ -582,6 +612,17 @@ kg_status kg_stream_gather(const int32_t* pos, int64_t npos, const int32_t* neg,
   KG_LAUNCH("k_stream_gather", k_stream_gather, grid_for(npos + nneg), 256, 0, as_stream(stream), pos, npos, neg, nneg, perm,
                                                                         stream_triples, labels);
   KG_CHECK_LAUNCH("k_stream_gather");
+  return KG_OK;
+}
+
+// --- dropout -------------------------------------------------------------------
+kg_status kg_dropout_mask(kg_pcg64* g, const int32_t* counts, int32_t t, int32_t d, double p, int64_t n_max,
+                          float* mask, void* stream) {
+  KG_REQUIRE(p > 0.0 && p < 1.0, KG_ERR_VALIDATION, "dropout must be in (0, 1)");
+  cudaStream_t st = as_stream(stream);
+  KG_LAUNCH("k_dropout_mask", k_dropout_mask, persistent_blocks(ceil_div(n_max * d, DROP_PER_THREAD), 256, 8), 256, 0,
+            st, g, counts, t, d, p, (float)(1.0 / (1.0 - p)), mask);
+  KG_LAUNCH("k_pcg_advance", k_pcg_advance_count, 1, 1, 0, st, g, counts, t, d);
   return KG_OK;
 }
 

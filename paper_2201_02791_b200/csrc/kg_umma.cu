@@ -227,6 +227,7 @@ struct PackedArgs {
   int relu;
   float* c_packed;        // NN: optional packed copy of the output (records by MMA row, K = np)
   int64_t c_nk;
+  const float* mul;       // NN: optional per-element output scale by MMA row (ld N)
 };
 
 __device__ __forceinline__ uint32_t stage_bytes(int np) { return (uint32_t)((UM + np) * UKC * 2 * 4); }
@@ -365,6 +366,12 @@ __global__ void __launch_bounds__(UTHREADS, 1) k_umma_packed(PackedArgs g, int n
 #pragma unroll
             for (int i = 0; i < 16; ++i) v[i] = fmaxf(v[i], 0.f);
           }
+          if (g.mul) {   // inverted-dropout mask of this output row
+            const float* mr = g.mul + (tile * UM + r) * g.N;
+#pragma unroll
+            for (int i = 0; i < 16; ++i)
+              if (c0 + i < g.N) v[i] *= __ldg(mr + c0 + i);
+          }
           if (g.c_packed) {   // pad columns hold exact zeros (zero B rows)
             const int64_t m = tile * UM + r;
 #pragma unroll
@@ -463,7 +470,7 @@ kg_status umma_gemm_nn(const GemmArgs& g, void* ws, cudaStream_t st) {
   p.Ap = Ap; p.Bp = Bp; p.a_nk_alloc = nk; p.np = np; p.tn = 0;
   p.M = g.M; p.M_dev = g.M_dev; p.M_dev_index = g.M_dev_index; p.nk = nk;
   p.C = g.C; p.ldc = g.ldc; p.c_rows = g.c_rows; p.N = g.N; p.out_rows = 0; p.relu = g.relu;
-  p.c_packed = g.c_packed; p.c_nk = ceil_div(g.N, UKC);
+  p.c_packed = g.c_packed; p.c_nk = ceil_div(g.N, UKC); p.mul = g.mul;
   const int ctas = (int)(tiles < num_sms() ? tiles : num_sms());
   return launch_packed(p, dim3((unsigned)ctas, 1, 1), st);
 }

@@ -263,6 +263,16 @@ class ViewBuffers:
                                                          config.num_relations)
         self.b_max = b_max
 
+    def drop_masks(self) -> list:
+        """Inverted-dropout masks of the non-last layers' outputs, (n, d_{l+1})
+        by closure position (allocated on first use)."""
+        if getattr(self, "_masks", None) is None:
+            torch = _torch()
+            L = self.config.num_layers
+            self._masks = [torch.empty((self.n, self.config.dims[l + 1]), dtype=torch.float32,
+                                       device=self.view.device) for l in range(L - 1)]
+        return self._masks
+
     def hpk(self, l: int):
         """Layer l's input rows (by closure position) as tensor-core operand
         records for the backward Y GEMM (written by layer l-1's forward, or by
@@ -293,7 +303,21 @@ def device_pack_inputs(bufs: ViewBuffers) -> None:
               bufs.counts.data_ptr(), L, bufs.n, bufs.config.dims[0], out.data_ptr(), _lib.stream_handle())
 
 
-def device_forward(model: DeviceModel, bufs: ViewBuffers, packed: bool = False, hpk: bool = False) -> None:
+def device_dropout(bufs: ViewBuffers, g_dev, p: float) -> list:
+    """Masks of every non-last layer, in forward order (the reference's draw
+    order, ref:model.py:221-227), from the device PCG64 state g_dev (advanced
+    in place)."""
+    L = bufs.config.num_layers
+    masks = bufs.drop_masks()
+    st = _lib.stream_handle()
+    for l in range(L - 1):
+        _lib.call("kg_dropout_mask", g_dev.data_ptr(), bufs.counts.data_ptr(), L - 1 - l, bufs.config.dims[l + 1],
+                  float(p), bufs.n, masks[l].data_ptr(), st)
+    return masks
+
+
+def device_forward(model: DeviceModel, bufs: ViewBuffers, packed: bool = False, hpk: bool = False,
+                   masks: Optional[list] = None) -> None:
     """All layers over the closure in bufs.order/counts (ref:model.py:196-235).
     packed: use the model's pre-packed weight operands (DeviceModel.repack);
     hpk: also emit each hidden layer's output as the next layer's packed
@@ -305,8 +329,8 @@ def device_forward(model: DeviceModel, bufs: ViewBuffers, packed: bool = False, 
         ws = bufs.layer_ws(l)
         _lib.call("kg_rgcn_forward", csr, ctypes.byref(model.layer(l, packed)), bufs.H[l].data_ptr(),
                   bufs.H[l + 1].data_ptr(), bufs.order.data_ptr(), bufs.pos.data_ptr(), bufs.counts.data_ptr(),
-                  L - 1 - l, 1 if l < L - 1 else 0, bufs.hpk(l + 1).data_ptr() if (hpk and l < L - 1) else None,
-                  ws.data_ptr(), ws.numel(), st)
+                  L - 1 - l, 1 if l < L - 1 else 0, masks[l].data_ptr() if (masks and l < L - 1) else None,
+                  bufs.hpk(l + 1).data_ptr() if (hpk and l < L - 1) else None, ws.data_ptr(), ws.numel(), st)
 
 
 def device_loss(model: DeviceModel, bufs: ViewBuffers, stream, start: int, b: int, grad_flat, loss_out,
@@ -329,7 +353,7 @@ def device_loss(model: DeviceModel, bufs: ViewBuffers, stream, start: int, b: in
 
 
 def device_backward(model: DeviceModel, bufs: ViewBuffers, grad_flat, input_grad: bool, side=None,
-                    packed: bool = False, hpk: bool = False) -> None:
+                    packed: bool = False, hpk: bool = False, masks: Optional[list] = None) -> None:
     """Layer gradients in reverse (ref:model.py:283-296): d bases / d coeffs
     into grad_flat, dL/dH_0 rows into bufs.dH[0] when input_grad. With a side
     stream (torch.cuda.Stream) the parameter-gradient branch of every layer
@@ -346,7 +370,7 @@ def device_backward(model: DeviceModel, bufs: ViewBuffers, grad_flat, input_grad
                   bufs.H[l + 1].data_ptr() if l < L - 1 else 0, bufs.dH[l + 1].data_ptr(), dh_in,
                   bufs.order.data_ptr(), bufs.pos.data_ptr(), bufs.counts.data_ptr(), L - 1 - l,
                   grad_flat.data_ptr() + 4 * lay.bases_off(l), grad_flat.data_ptr() + 4 * lay.coeffs_off(l),
-                  bufs.hpk(l).data_ptr() if hpk else None,
+                  bufs.hpk(l).data_ptr() if hpk else None, masks[l].data_ptr() if (masks and l < L - 1) else None,
                   ws.data_ptr(), ws.numel(), st, None if side is None else side.cuda_stream)
     if side is not None:
         torch.cuda.current_stream().wait_stream(side)
@@ -396,10 +420,9 @@ def encode(params: ModelParams, config: ModelConfig, cg, input_table: np.ndarray
     embeddings in cg.seed_vertices order (ref:model.py:196-235)."""
     if cg.num_layers != config.num_layers:
         raise ShapeError(f"compute graph has {cg.num_layers} layers, model has {config.num_layers}")
-    if training and config.dropout > 0.0:
-        if dropout_rng is None:
-            raise ValidationError("training with dropout needs a dropout rng")
-        raise ValidationError("dropout > 0 is not supported by the device path yet")
+    drop = training and config.dropout > 0.0
+    if drop and dropout_rng is None:
+        raise ValidationError("training with dropout needs a dropout rng")
     view = cg.view
     dev = view.device
     model = DeviceModel.from_params(config, params, dev)
@@ -408,7 +431,17 @@ def encode(params: ModelParams, config: ModelConfig, cg, input_table: np.ndarray
     bufs.order.copy_(cg.d_order)
     bufs.pos.copy_(cg.d_pos)
     bufs.counts.copy_(cg.d_counts)
-    device_forward(model, bufs)
+    masks = None
+    if drop:
+        # the Generator's stream drives the device masks; afterwards the
+        # Generator is advanced exactly as numpy's random((T, d)) calls would
+        g_dev = _lib.pcg_to_device(_lib.pcg_from_numpy(dropout_rng), dev)
+        masks = device_dropout(bufs, g_dev, config.dropout)
+        counts = cg.d_counts.cpu().tolist()
+        L = config.num_layers
+        dropout_rng.bit_generator.advance(sum(int(counts[L - 1 - l]) * config.dims[l + 1] for l in range(L - 1)))
+    bufs.masks = masks
+    device_forward(model, bufs, masks=masks)
     seeds = cg.seed_vertices
     import torch
     out = bufs.H[-1][torch.as_tensor(seeds, device=dev)].double().cpu().numpy()
@@ -452,7 +485,7 @@ def loss_from_cache(params: ModelParams, config: ModelConfig, batch, cg, cache: 
     device_loss(model, bufs, stream, 0, len(batch.triples), grad, loss_t)
     check_flags(bufs)
     emb = config.mode == MODE_EMBEDDING
-    device_backward(model, bufs, grad, input_grad=emb)
+    device_backward(model, bufs, grad, input_grad=emb, masks=getattr(bufs, "masks", None))
     blocks = model.layout.unpack(grad.cpu().numpy())
     L = config.num_layers
     g = Gradients(blocks[:L], blocks[L:2 * L], blocks[2 * L])

@@ -30,8 +30,8 @@ import numpy as np
 from . import _lib
 from .errors import KGError, NumericError, ProtocolError, ValidationError
 from .model import (MODE_EMBEDDING, MODE_FEATURE, DeviceModel, ModelConfig, ModelParams, ViewBuffers,
-                    check_flags, device_backward, device_forward, device_loss, device_pack_inputs,
-                    init_params)
+                    check_flags, device_backward, device_dropout, device_forward, device_loss,
+                    device_pack_inputs, init_params)
 from .partition import PartitionSet
 from .sampler import EpochSampler, build_view
 
@@ -325,6 +325,10 @@ class _Worker:
         # the worker's RNG stream (ref:trainer.py:185) lives on the device
         self.g_dev = _lib.pcg_to_device(
             _lib.pcg_from_numpy(np.random.default_rng(tc.seed ^ self.view.partition_id)), dev)
+        # dropout stream (ref:trainer.py:186-187)
+        self.g_drop = (_lib.pcg_to_device(_lib.pcg_from_numpy(
+            np.random.default_rng((tc.seed ^ self.view.partition_id) + 0x9E3779B9)), dev)
+            if config.dropout > 0.0 else None)
         local = self.view.local_ids
         if config.mode == MODE_EMBEDDING:
             rows = params.entity_embed[local]
@@ -369,8 +373,6 @@ class Trainer:
                                   f"{model_config.num_layers} layers")
         if model_config.num_relations != pset.num_relations:
             raise ValidationError("model num_relations != partition set num_relations")
-        if model_config.dropout > 0.0:
-            raise ValidationError("dropout > 0 is not supported by the device path yet")
         self.pset, self.mc, self.tc = pset, model_config, train_config
         self.P = pset.num_parts
         dist = torch.distributed
@@ -459,13 +461,15 @@ class Trainer:
             side.wait_stream(main)
             with torch.cuda.stream(side):
                 device_pack_inputs(w.bufs)   # layer-0 backward operand, beside the forward
-            device_forward(self.model, w.bufs, packed=True, hpk=True)
+            masks = device_dropout(w.bufs, w.g_drop, self.mc.dropout) if w.g_drop is not None else None
+            device_forward(self.model, w.bufs, packed=True, hpk=True, masks=masks)
             main.wait_stream(side)
             device_loss(self.model, w.bufs, w.stream, 0, w.b, gslot, self.loss_scratch[i:i + 1],
                         start_dev=self.start_dev[i:i + 1], part="compute")
             self.losses[i].index_copy_(0, self.round_dev, self.loss_scratch[i:i + 1])
             device_backward(self.model, w.bufs, gslot, input_grad=w.emb,
-                            side=self._loss_stream if self.fork_streams else None, packed=True, hpk=True)
+                            side=self._loss_stream if self.fork_streams else None, packed=True, hpk=True,
+                            masks=masks)
 
     def _update_body(self):
         """Fused tree-mean + dense Adam/SGD, then lazy sparse rows."""

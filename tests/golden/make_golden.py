@@ -264,7 +264,62 @@ def scenario_fb_structure(name):
     print(f"wrote {name}.npz")
 
 
+def scenario_dropout(name):
+    """Inverted dropout (ref:model.py:221-227): one teacher-forced training
+    step with a seeded dropout Generator (masks, loss, gradients, Generator
+    state after) and a 2-partition training run with dropout 0.25."""
+    out = {}
+    graph = multigraph(60, 4, 260, seed=21)
+    dims, hops = (6, 8, 8, 5), 3
+    out["triples"] = graph.triples
+    out["num_entities"] = np.int64(graph.num_entities)
+    out["num_relations"] = np.int64(graph.num_relations)
+    pset = kpart.neighborhood_expand(kpart.vertex_cut_partition(graph, 2, 3), graph, hops)
+    dump_partitions("", pset, out)
+    out["hops"] = np.int64(hops)
+    mc = kmodel.ModelConfig(num_layers=3, dims=list(dims), num_bases=2,
+                            num_relations=graph.num_relations, negatives_per_positive=1,
+                            dropout=0.25, mode="embedding")
+    params = fp32_params(kmodel.init_params(mc, np.random.default_rng(8),
+                                            num_entities=graph.num_entities))
+    dump_params("init_", params, out)
+    view = ksamp.build_view(pset.partitions[0], graph.num_entities, graph.num_relations)
+    rng = np.random.default_rng(99)
+    neg = ksamp.sample_negatives(view, 1, rng)
+    b0 = ksamp.make_batches(view.core_edges, neg, 40, rng, num_batches=2)[0]
+    out["batch0_triples"] = b0.triples
+    out["batch0_labels"] = b0.labels
+    cg0 = ksamp.build_compute_graph(b0, view, hops)
+    drng = np.random.default_rng(1234)
+    out["drng_init"] = rng_state(drng)
+    cache = kmodel.EncodeCache()
+    emb = kmodel.encode(params, mc, cg0, params.entity_embed, view.local_ids, training=True,
+                        dropout_rng=drng, cache=cache)
+    loss, grads = kmodel.loss_from_cache(params, mc, b0, cg0, cache, view.local_ids)
+    out["drng_after"] = rng_state(drng)
+    out["b0_seed_emb"] = emb
+    out["b0_loss"] = np.float64(loss)
+    for l in range(mc.num_layers):
+        out[f"b0_dbases_{l}"] = grads.bases[l]
+        out[f"b0_dcoeffs_{l}"] = grads.coeffs[l]
+    out["b0_ddecoder"] = grads.decoder
+    out["b0_embed_ids"] = grads.embed_ids
+    out["b0_embed_rows"] = grads.embed_rows
+    tc = ktrain.TrainConfig(epochs=2, batch_size=48, optimizer="adam", learning_rate=0.01, seed=3)
+    got, report = ktrain.train(pset, graph, mc, tc, initial_params=params)
+    dump_params("trained_", got, out)
+    out["loss_curve"] = np.asarray(report.loss_curve)
+    out["config_json"] = np.frombuffer(json.dumps({
+        "dims": list(dims), "hops": hops, "dropout": 0.25, "parts": 2, "part_seed": 3,
+        "batch": 48, "epochs": 2, "train_seed": 3}).encode(), dtype=np.uint8)
+    np.savez_compressed(os.path.join(OUT, f"{name}.npz"), **out)
+    print(f"wrote {name}.npz ({len(out)} arrays)")
+
+
 if __name__ == "__main__":
+    if "--dropout-only" in sys.argv:
+        scenario_dropout("dropout_small")
+        sys.exit(0)
     scenario_small("small_embed", multigraph(40, 5, 160, seed=11), parts=2, hops=2,
                    part_seed=1, dims=(5, 6, 4), s=2, batch=32, rounds=4,
                    train_seed=9, epochs=2)
@@ -275,5 +330,6 @@ if __name__ == "__main__":
                    part_seed=0, dims=(16, 16, 8), s=1, batch=128, rounds=5,
                    train_seed=1, epochs=2)
     scenario_eval("eval_small", 200, 6, 5.0, seed=5, dims=(8, 8, 8))
+    scenario_dropout("dropout_small")
     if "--fb" in sys.argv:
         scenario_fb_structure("fb_structure")

@@ -255,13 +255,16 @@ def test_oracle_parity_on_fb_batch():
     assert rel_l2(gr.embed_rows, og.embed_rows) < 1e-4
 
 
-def test_cuda_graph_replay_is_bitwise_identical_to_eager():
-    """Rounds replayed from captured CUDA graphs (both epoch slots, device
-    round scalars) produce exactly the eager parameters and losses."""
+@pytest.mark.parametrize("dropout", [0.0, 0.2])
+def test_cuda_graph_replay_is_bitwise_identical_to_eager(dropout):
+    """Rounds replayed from captured CUDA graphs (every epoch slot, device
+    round scalars, device dropout stream) produce exactly the eager
+    parameters and losses."""
     g = load_golden("synth_p4")
     graph, pset, cfg = golden_pset(g)
     L = len(cfg["dims"]) - 1
-    mc = kb.ModelConfig(L, cfg["dims"], cfg["num_bases"], graph.num_relations, 1, mode="embedding")
+    mc = kb.ModelConfig(L, cfg["dims"], cfg["num_bases"], graph.num_relations, 1, dropout=dropout,
+                        mode="embedding")
     tc = kb.TrainConfig(epochs=1, batch_size=96, seed=2)
     p0 = golden_params(g, "init_", L)
     results = []
@@ -341,3 +344,36 @@ def test_tensor_core_ranking_matches_exact_fma_ranking(policy):
     rb = np.array([r.rank for r in b.records])
     assert np.mean(ra == rb) >= 0.999
     assert abs(a.mrr - b.mrr) / b.mrr <= 1e-3
+
+
+def test_dropout_step_and_training_match_reference():
+    """Inverted dropout on the device: masks from the caller's Generator
+    (state advanced exactly as numpy's), teacher-forced loss/gradients, and a
+    2-partition training run with dropout 0.25 against the reference."""
+    from conftest import rng_from_state, state_tuple
+    g = load_golden("dropout_small")
+    graph, pset, cfg = golden_pset(g)
+    L = len(cfg["dims"]) - 1
+    mc = kb.ModelConfig(L, cfg["dims"], 2, graph.num_relations, 1, dropout=cfg["dropout"], mode="embedding")
+    params = golden_params(g, "init_", L)
+    v = kb.build_view(pset.partitions[0], graph.num_entities, graph.num_relations)
+    b = kb.EdgeMiniBatch(g["batch0_triples"], g["batch0_labels"])
+    cg = kb.build_compute_graph(b, v, L)
+    drng = rng_from_state(g["drng_init"])
+    cache = kb.EncodeCache()
+    emb = kb.encode(params, mc, cg, params.entity_embed, v.local_ids, training=True, dropout_rng=drng, cache=cache)
+    assert state_tuple(drng) == state_tuple(rng_from_state(g["drng_after"]))
+    assert rel_l2(emb, g["b0_seed_emb"]) < 1e-5
+    loss, grads = kb.loss_from_cache(params, mc, b, cg, cache, v.local_ids)
+    assert abs(loss - float(g["b0_loss"])) / abs(float(g["b0_loss"])) < 1e-5
+    for l in range(L):
+        assert rel_l2(grads.bases[l], g[f"b0_dbases_{l}"]) < 1e-4
+        assert rel_l2(grads.coeffs[l], g[f"b0_dcoeffs_{l}"]) < 1e-4
+    assert rel_l2(grads.embed_rows, g["b0_embed_rows"]) < 1e-4
+    tc = kb.TrainConfig(epochs=cfg["epochs"], batch_size=cfg["batch"], optimizer="adam", learning_rate=0.01,
+                        seed=cfg["train_seed"])
+    got, report = kb.train(pset, graph, mc, tc, initial_params=golden_params(g, "init_", L))
+    np.testing.assert_allclose(report.loss_curve, g["loss_curve"], rtol=1e-4)
+    want = golden_params(g, "trained_", L)
+    for a, c in zip(got.dense_blocks(), want.dense_blocks()):
+        assert rel_l2(a, c) < 1e-3

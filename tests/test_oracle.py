@@ -196,3 +196,34 @@ def em_perm_replay(js, n):
         i = n - 1 - k
         a[i], a[j] = a[j], a[i]
     return a
+
+
+def test_dropout_step_and_training_match_reference():
+    """Inverted dropout (ref:model.py:221-227): teacher-forced step with a
+    seeded dropout Generator (masks drawn in forward order, Generator state
+    after) and a 2-partition training run with dropout 0.25."""
+    g = load_golden("dropout_small")
+    cfg = golden_json(g)
+    views, ends = oracle_views(g)
+    v = views[0]
+    L = len(cfg["dims"]) - 1
+    p = oracle_params(g, "init_", L)
+    b = ko.OBatch(g["batch0_triples"], g["batch0_labels"])
+    cg = ko.closure(v, b.seed_vertices, cfg["hops"])
+    drng = rng_from_state(g["drng_init"])
+    tr = ko.OTrace()
+    out = ko.forward(p, cg, p.embed, v.local_ids, cfg["dropout"], drng, tr)
+    assert state_tuple(drng) == state_tuple(rng_from_state(g["drng_after"]))
+    assert rel_err(out, g["b0_seed_emb"][: len(out)]) < 1e-12
+    loss, gr = ko.backward(p, b, cg, tr, v.local_ids, True)
+    assert abs(loss - float(g["b0_loss"])) < 1e-12
+    for l in range(L):
+        assert rel_err(gr.bases[l], g[f"b0_dbases_{l}"]) < 1e-10
+        assert rel_err(gr.coeffs[l], g[f"b0_dcoeffs_{l}"]) < 1e-10
+    assert rel_err(gr.embed_rows, g["b0_embed_rows"]) < 1e-10
+    got, curve, _, _ = ko.train(views, ends, oracle_params(g, "init_", L), 1, cfg["epochs"],
+                                batch_size=cfg["batch"], seed=cfg["train_seed"], dropout=cfg["dropout"])
+    np.testing.assert_allclose(curve, g["loss_curve"], rtol=1e-10)
+    want = oracle_params(g, "trained_", L)
+    for a, c in zip(got.dense(), want.dense()):
+        assert rel_err(a, c) < 1e-9
