@@ -337,6 +337,14 @@ kg_status kg_sparse_step(float* table, float* m, float* v, const float* grad, co
                          float beta1, float beta2, float eps, double bc1, double bc2, const int64_t* step_dev,
                          int32_t n_max, void* stream);
 
+/* Given-candidates protocol (ref:evaluate.py:168-180), tail side only:
+ * query i ranks candidate cand[cand_ptr[i] + true_pos[i]] (its true tail;
+ * the caller appends it when absent) against cand[cand_ptr[i]..cand_ptr[i+1]).
+ * ranks / ncand (= list length - 1) per query. d <= 256. */
+kg_status kg_eval_candidates(const float* H, int32_t d, const float* decoder, const int32_t* queries, int64_t nq,
+                             const int64_t* cand_ptr, const int32_t* cand, const int32_t* true_pos, int32_t policy,
+                             double* ranks, int32_t* ncand, void* stream);
+
 /* ---------------------------------------------------------------------- */
 /* Dropout (ref:model.py:221-227)                                          */
 /* ---------------------------------------------------------------------- */

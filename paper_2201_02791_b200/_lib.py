@@ -90,6 +90,7 @@ _PROTOS = {
     "kg_rgcn_backward": (ST, [POINTER(KgGraphCsr), POINTER(KgLayerParams), P, P, P, P, P, P, P, c_int32,
                               P, P, P, P, P, c_int64, P, P]),
     "kg_dropout_mask": (ST, [P, P, c_int32, c_int32, c_double, c_int64, P, P]),
+    "kg_eval_candidates": (ST, [P, c_int32, P, P, c_int64, P, P, P, c_int32, P, P, P]),
     "kg_pack_rows_bytes": (c_int64, [c_int64, c_int64]),
     "kg_pack_rows": (ST, [P, c_int64, P, P, c_int32, c_int64, c_int64, P, P]),
     "kg_rgcn_weights_bytes": (c_int64, [c_int32, c_int32, c_int32]),

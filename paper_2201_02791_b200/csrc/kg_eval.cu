@@ -177,6 +177,59 @@ __global__ void k_rank_finish(EvalArgs a, const int64_t* __restrict__ tkeys, int
   }
 }
 
+// --- given-candidates protocol (ref:evaluate.py:168-180) ----------------------
+// One warp per query: q = H[h] * dec[r] held in the lanes (feature f = lane +
+// 32 j), every score — the true candidate's included — is the same per-lane
+// fmaf chain plus the same xor-tree warp sum, so the comparisons are exact.
+constexpr int CQ_J = 8;   // d <= 256
+
+__device__ __forceinline__ float cand_dot(const float (&q)[CQ_J], const float* __restrict__ Hc, int d) {
+  const int lane = (int)lane_id();
+  float s = 0.f;
+#pragma unroll
+  for (int j = 0; j < CQ_J; ++j) {
+    const int f = lane + 32 * j;
+    if (f < d) s = fmaf(q[j], __ldg(Hc + f), s);
+  }
+  return warp_sum(s);
+}
+
+__global__ void __launch_bounds__(256) k_rank_candidates(const float* __restrict__ H, int d,
+                                                         const float* __restrict__ dec,
+                                                         const int32_t* __restrict__ qry, int64_t nq,
+                                                         const int64_t* __restrict__ cptr,
+                                                         const int32_t* __restrict__ cand,
+                                                         const int32_t* __restrict__ tpos, int policy,
+                                                         double* __restrict__ ranks, int32_t* __restrict__ ncand) {
+  const int lane = (int)lane_id(), nw = (gridDim.x * blockDim.x) >> 5;
+  for (int64_t i = warp_uniform((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5); i < nq; i += nw) {
+    const int32_t h = qry[i * 3], r = qry[i * 3 + 1];
+    float q[CQ_J];
+#pragma unroll
+    for (int j = 0; j < CQ_J; ++j) {
+      const int f = lane + 32 * j;
+      q[j] = f < d ? H[(int64_t)h * d + f] * dec[(int64_t)r * d + f] : 0.f;
+    }
+    const int64_t lo = cptr[i], hi = cptr[i + 1];
+    const float ts = cand_dot(q, H + (int64_t)cand[lo + tpos[i]] * d, d);
+    long long g = 0, e = 0;
+    for (int64_t c = lo; c < hi; ++c) {
+      const float sc = cand_dot(q, H + (int64_t)cand[c] * d, d);
+      g += sc > ts;
+      e += sc == ts;
+    }
+    e -= 1;   // the true candidate itself
+    if (lane == 0) {
+      double rank;
+      if (policy == 0) rank = 1.0 + (double)g + (double)e / 2.0;
+      else if (policy == 1) rank = 1.0 + (double)g;
+      else rank = 1.0 + (double)g + (double)e;
+      ranks[i] = rank;
+      ncand[i] = (int32_t)(hi - lo - 1);
+    }
+  }
+}
+
 // --- known keys --------------------------------------------------------------
 __global__ void k_known_keys(const int32_t* __restrict__ tri, int64_t k, int ca, int cc, int32_t N, int32_t R,
                              uint64_t* __restrict__ keys, uint32_t* __restrict__ vals) {
@@ -272,6 +325,17 @@ kg_status kg_eval_filtered(const float* H, int32_t d, int32_t N, const float* de
   KG_LAUNCH("k_rank_finish", k_rank_finish, persistent_blocks(2 * nq, 128, 8), 128, 0, st, e, tkeys, ntk, hkeys, nhk, policy, chunk, ranks,
                                                                    ncand);
   KG_CHECK_LAUNCH("k_rank_finish");
+  return KG_OK;
+}
+
+kg_status kg_eval_candidates(const float* H, int32_t d, const float* dec, const int32_t* qry, int64_t nq,
+                             const int64_t* cand_ptr, const int32_t* cand, const int32_t* true_pos, int32_t policy,
+                             double* ranks, int32_t* ncand, void* stream) {
+  KG_REQUIRE(policy >= 0 && policy <= 2, KG_ERR_VALIDATION, "unknown tie policy");
+  KG_REQUIRE(d >= 1 && d <= 32 * CQ_J, KG_ERR_SHAPE, "candidates protocol supports d <= %d", 32 * CQ_J);
+  if (nq <= 0) return KG_OK;
+  KG_LAUNCH("k_rank_candidates", k_rank_candidates, persistent_blocks(nq * 32, 256, 8), 256, 0, as_stream(stream), H,
+            d, dec, qry, nq, cand_ptr, cand, true_pos, policy, ranks, ncand);
   return KG_OK;
 }
 

@@ -147,6 +147,44 @@ def _known_pair_bound(tkeys, ntk: int, hkeys, nhk: int, dq, N: int, R: int) -> i
     return max(total, 1)
 
 
+def _evaluate_candidates(params, config, graph, q, candidates: dict, tie_policy: str) -> EvalResult:
+    """Given-candidates protocol (ref:evaluate.py:168-180): the tail of every
+    query against its candidate list (the true tail appended when absent)."""
+    import torch
+    nq = len(q)
+    lists, tpos = [], np.empty(nq, dtype=np.int32)
+    for i, t in enumerate(np.asarray(q)[:, 2].tolist()):
+        cand = np.asarray(candidates.get(i, []), dtype=np.int64)
+        if len(cand) == 0:
+            raise ValidationError(f"no candidates for test index {i}")
+        pos = np.flatnonzero(cand == t)
+        if len(pos) == 0:
+            cand = np.concatenate([cand, [t]])
+            pos = [len(cand) - 1]
+        lists.append(cand)
+        tpos[i] = int(pos[0])
+    ptr = np.zeros(nq + 1, dtype=np.int64)
+    ptr[1:] = np.cumsum([len(c) for c in lists])
+    flat = np.concatenate(lists)
+    if flat.min() < 0 or flat.max() >= graph.num_entities:
+        raise IntegrityError("candidate entity id out of range")
+    H, model, view = _device_encode_all(params, config, graph)
+    dev = view.device
+    t = lambda a, dt: torch.as_tensor(np.ascontiguousarray(a, dtype=dt)).to(dev)
+    dq, dptr, dc, dt_ = t(q, np.int32), t(ptr, np.int64), t(flat, np.int32), t(tpos, np.int32)
+    ranks = torch.empty(nq, dtype=torch.float64, device=dev)
+    ncand = torch.empty(nq, dtype=torch.int32, device=dev)
+    _lib.call("kg_eval_candidates", H.data_ptr(), config.dims[-1], model.decoder_ptr(), dq.data_ptr(), nq,
+              dptr.data_ptr(), dc.data_ptr(), dt_.data_ptr(), _POLICY[tie_policy], ranks.data_ptr(),
+              ncand.data_ptr(), _lib.stream_handle())
+    r, c = ranks.cpu().numpy(), ncand.cpu().numpy()
+    rows = np.asarray(q, dtype=np.int64)
+    records = list(map(RankRecord, rows[:, 0].tolist(), rows[:, 1].tolist(), rows[:, 2].tolist(),
+                       [SIDE_TAIL] * nq, r.tolist(), c.tolist()))
+    return EvalResult(mrr=float((1.0 / r).mean()), hits={k: float((r <= k).mean()) for k in HITS_KS},
+                      records=records)
+
+
 def evaluate(params: ModelParams, config: ModelConfig, graph, split, which: str = "test",
              protocol: str = "filtered", candidates: Optional[dict] = None, tie_policy: str = TIE_MEAN,
              chunk: int = 512, impl: int = 0) -> EvalResult:
@@ -161,10 +199,12 @@ def evaluate(params: ModelParams, config: ModelConfig, graph, split, which: str 
         raise ValidationError(f"{which} split is empty")
     if protocol not in ("filtered", "candidates"):
         raise ValidationError(f"unknown protocol {protocol!r}")
-    if protocol == "candidates":
-        raise ValidationError("the candidates protocol is not part of the device path yet")
+    if protocol == "candidates" and candidates is None:
+        raise ValidationError("candidates protocol requires a candidate map")
     if tie_policy not in _POLICY:
         raise ValidationError(f"unknown tie policy {tie_policy!r}")
+    if protocol == "candidates":
+        return _evaluate_candidates(params, config, graph, q, candidates, tie_policy)
     H, model, view = _device_encode_all(params, config, graph)
     dev = view.device
     N, R = graph.num_entities, graph.num_relations

@@ -264,6 +264,40 @@ def scenario_fb_structure(name):
     print(f"wrote {name}.npz")
 
 
+def scenario_candidates(name):
+    """Given-candidates protocol (ref:evaluate.py:168-180): per test index a
+    candidate list (some without the true tail -> appended, some with
+    duplicates of it), all tie policies."""
+    n, R, dims = 200, 6, (8, 8, 8)
+    graph, split = generate_synthetic(n, R, 5.0, seed=5)
+    mc = kmodel.ModelConfig(num_layers=2, dims=list(dims), num_bases=2, num_relations=R, mode="embedding")
+    params = fp32_params(kmodel.init_params(mc, np.random.default_rng(6), num_entities=n))
+    rng = np.random.default_rng(17)
+    cmap, flat, ptr = {}, [], [0]
+    for i, (h, r, t) in enumerate(split.test.tolist()):
+        c = rng.integers(0, n, int(rng.integers(5, 40)))
+        if i % 3 == 0:
+            c = np.concatenate([c, [t]])
+        if i % 7 == 0:
+            c = np.concatenate([c, [t, t]])
+        cmap[i] = c.tolist()
+        flat += cmap[i]
+        ptr.append(len(flat))
+    out = {"train": split.train, "valid": split.valid, "test": split.test,
+           "num_entities": np.int64(n), "num_relations": np.int64(R), "dims": np.asarray(dims, dtype=np.int64),
+           "cand": np.asarray(flat, dtype=np.int64), "cand_ptr": np.asarray(ptr, dtype=np.int64)}
+    dump_params("p_", params, out)
+    out["H"] = kev.encode_all_entities(params, mc, graph)
+    for pol in (kev.TIE_MEAN, kev.TIE_OPTIMISTIC, kev.TIE_PESSIMISTIC):
+        res = kev.evaluate(params, mc, graph, split, which="test", protocol="candidates", candidates=cmap,
+                           tie_policy=pol)
+        out[f"{pol}_mrr"] = np.float64(res.mrr)
+        out[f"{pol}_ranks"] = np.asarray([r.rank for r in res.records])
+        out[f"{pol}_ncand"] = np.asarray([r.num_candidates for r in res.records])
+    np.savez_compressed(os.path.join(OUT, f"{name}.npz"), **out)
+    print(f"wrote {name}.npz")
+
+
 def scenario_dropout(name):
     """Inverted dropout (ref:model.py:221-227): one teacher-forced training
     step with a seeded dropout Generator (masks, loss, gradients, Generator
@@ -320,6 +354,9 @@ if __name__ == "__main__":
     if "--dropout-only" in sys.argv:
         scenario_dropout("dropout_small")
         sys.exit(0)
+    if "--candidates-only" in sys.argv:
+        scenario_candidates("eval_candidates")
+        sys.exit(0)
     scenario_small("small_embed", multigraph(40, 5, 160, seed=11), parts=2, hops=2,
                    part_seed=1, dims=(5, 6, 4), s=2, batch=32, rounds=4,
                    train_seed=9, epochs=2)
@@ -331,5 +368,6 @@ if __name__ == "__main__":
                    train_seed=1, epochs=2)
     scenario_eval("eval_small", 200, 6, 5.0, seed=5, dims=(8, 8, 8))
     scenario_dropout("dropout_small")
+    scenario_candidates("eval_candidates")
     if "--fb" in sys.argv:
         scenario_fb_structure("fb_structure")

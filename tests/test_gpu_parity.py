@@ -377,3 +377,22 @@ def test_dropout_step_and_training_match_reference():
     want = golden_params(g, "trained_", L)
     for a, c in zip(got.dense_blocks(), want.dense_blocks()):
         assert rel_l2(a, c) < 1e-3
+
+
+@pytest.mark.parametrize("policy", ["mean", "optimistic", "pessimistic"])
+def test_candidates_protocol_matches_reference(policy):
+    g = load_golden("eval_candidates")
+    N, R = int(g["num_entities"]), int(g["num_relations"])
+    dims = g["dims"].tolist()
+    mc = kb.ModelConfig(len(dims) - 1, dims, 2, R, mode="embedding")
+    graph = KnowledgeGraph(N, R, g["train"])
+    split = kb.DatasetSplit(g["train"], g["valid"], g["test"])
+    ptr, cand = g["cand_ptr"], g["cand"]
+    cmap = {i: cand[ptr[i]:ptr[i + 1]].tolist() for i in range(len(ptr) - 1)}
+    res = kb.evaluate(golden_params(g, "p_", len(dims) - 1), mc, graph, split, which="test",
+                      protocol="candidates", candidates=cmap, tie_policy=policy)
+    ranks = np.array([r.rank for r in res.records])
+    np.testing.assert_array_equal([r.num_candidates for r in res.records], g[f"{policy}_ncand"])
+    assert np.mean(ranks == g[f"{policy}_ranks"]) >= 0.999
+    assert all(r.corrupted_side == "tail" for r in res.records)
+    assert abs(res.mrr - float(g[f"{policy}_mrr"])) / float(g[f"{policy}_mrr"]) <= 0.01

@@ -227,3 +227,15 @@ def test_dropout_step_and_training_match_reference():
     want = oracle_params(g, "trained_", L)
     for a, c in zip(got.dense(), want.dense()):
         assert rel_err(a, c) < 1e-9
+
+
+@pytest.mark.parametrize("policy", ["mean", "optimistic", "pessimistic"])
+def test_candidates_protocol_matches_reference(policy):
+    g = load_golden("eval_candidates")
+    L = len(g["dims"]) - 1
+    p = oracle_params(g, "p_", L)
+    ptr, cand = g["cand_ptr"], g["cand"]
+    cmap = {i: cand[ptr[i]:ptr[i + 1]].tolist() for i in range(len(ptr) - 1)}
+    ranks, ncand = ko.candidate_ranks(g["H"], p.decoder, g["test"], cmap, policy)
+    np.testing.assert_array_equal(ranks, g[f"{policy}_ranks"])
+    np.testing.assert_array_equal(ncand, g[f"{policy}_ncand"])
