@@ -265,8 +265,15 @@ kg_status kg_rgcn_forward(const kg_graph_csr* g, const kg_layer_params* lp, cons
 kg_status kg_rgcn_backward(const kg_graph_csr* g, const kg_layer_params* lp, const float* H_in,
                            const float* H_out, const float* dH_out, float* dH_in, const int32_t* vertex_order,
                            const int32_t* pos, const int32_t* counts, int32_t t, float* d_bases,
-                           float* d_coeffs, const float* H_in_packed, const float* dropout_mask, void* ws,
-                           int64_t ws_bytes, void* stream, void* side_stream);
+                           float* d_coeffs, const float* H_in_packed, const float* dropout_mask,
+                           int32_t y_ready, void* ws, int64_t ws_bytes, void* stream, void* side_stream);
+/* The backward's first GEMM, Y = H_in[vertex_order[p]] . [V_0 | .. | V_{B-1}]
+ * for p < counts[t+1], ahead of time (it needs only forward outputs): call it
+ * on any stream ordered before kg_rgcn_backward(..., y_ready = 1, ...) with
+ * the same ws. Needs lp->packed. */
+kg_status kg_rgcn_backward_y(const kg_graph_csr* g, const kg_layer_params* lp, const float* H_in,
+                             const float* H_in_packed, const int32_t* vertex_order, const int32_t* counts, int32_t t,
+                             void* ws, int64_t ws_bytes, void* stream);
 /* H_in_packed (optional): H_in[vertex_order[p]], p < counts[t+1], as operand
  * records (the previous layer's H_out_packed, or kg_pack_rows).
  * dropout_mask (optional): the mask this layer's forward applied to H_out. */
@@ -311,11 +318,13 @@ kg_status kg_loss_groups(const float* H, int32_t d, int32_t n_local, const float
                          const int64_t* start_dev, int64_t b, const int32_t* vertex_order, const int32_t* counts,
                          float* dH, float* d_decoder, float* loss_out, float* scores_out, uint32_t* flags, void* ws,
                          int64_t ws_bytes, void* stream);
+/* side_stream (optional): the loss mean and d_decoder are produced on it
+ * (only dH stays on `stream`); order it before reading them. */
 kg_status kg_loss_compute(const float* H, int32_t d, int32_t n_local, const float* decoder, int32_t R,
                           const int32_t* stream_triples, const float* labels, int64_t total, int64_t start,
                           const int64_t* start_dev, int64_t b, const int32_t* vertex_order, const int32_t* counts,
                           float* dH, float* d_decoder, float* loss_out, float* scores_out, uint32_t* flags,
-                          void* ws, int64_t ws_bytes, void* stream);
+                          void* ws, int64_t ws_bytes, void* stream, void* side_stream);
 
 /* ---------------------------------------------------------------------- */
 /* R19/R20  Reduction + optimizer (ref:trainer.py:63-151)                  */

@@ -88,7 +88,8 @@ _PROTOS = {
     "kg_rgcn_forward": (ST, [POINTER(KgGraphCsr), POINTER(KgLayerParams), P, P, P, P, P, c_int32, c_int32,
                              P, P, P, c_int64, P]),
     "kg_rgcn_backward": (ST, [POINTER(KgGraphCsr), POINTER(KgLayerParams), P, P, P, P, P, P, P, c_int32,
-                              P, P, P, P, P, c_int64, P, P]),
+                              P, P, P, P, c_int32, P, c_int64, P, P]),
+    "kg_rgcn_backward_y": (ST, [POINTER(KgGraphCsr), POINTER(KgLayerParams), P, P, P, P, c_int32, P, c_int64, P]),
     "kg_dropout_mask": (ST, [P, P, c_int32, c_int32, c_double, c_int64, P, P]),
     "kg_eval_candidates": (ST, [P, c_int32, P, P, c_int64, P, P, P, c_int32, P, P, P]),
     "kg_pack_rows_bytes": (c_int64, [c_int64, c_int64]),
@@ -104,7 +105,7 @@ _PROTOS = {
     "kg_loss_groups": (ST, [P, c_int32, c_int32, P, c_int32, P, P, c_int64, c_int64, P, c_int64, P, P, P,
                             P, P, P, P, P, c_int64, P]),
     "kg_loss_compute": (ST, [P, c_int32, c_int32, P, c_int32, P, P, c_int64, c_int64, P, c_int64, P, P, P,
-                             P, P, P, P, P, c_int64, P]),
+                             P, P, P, P, P, c_int64, P, P]),
     "kg_optim_workspace_bytes": (c_int64, [c_int64]),
     "kg_dense_step": (ST, [P, P, P, P, c_int32, c_int64, c_int32, c_float, c_float, c_float, c_float,
                            c_double, c_double, P, c_float, P, P, c_int64, P]),

@@ -424,17 +424,31 @@ static kg_status loss_groups(const LossArgs& la, int32_t n_local, int32_t R, con
   return seg_bounds(w.vk, 2 * b, order, counts, (int32_t)w.ngmax, w.wv, st);
 }
 
+static cudaEvent_t loss_fork_event() {
+  static cudaEvent_t ev = nullptr;
+  if (!ev) cudaEventCreateWithFlags(&ev, cudaEventDisableTiming);
+  return ev;
+}
+
+// With a side stream only the dH reduction (which the backward needs) stays on
+// `st`; the loss mean and d_decoder (optimizer inputs) run on `side`.
 static kg_status loss_compute(const LossArgs& la, int32_t R, const int32_t* order, const int32_t* counts,
                               float* dH, float* d_decoder, float* loss_out, uint32_t* flags, LossWs& w,
-                              cudaStream_t st) {
+                              cudaStream_t st, cudaStream_t side = nullptr) {
   const int64_t b = la.b;
   const bool v4 = la.d % 4 == 0 && (((uintptr_t)la.H | (uintptr_t)la.dec) & 15) == 0;
   KG_LAUNCH("k_score", v4 ? k_score<true> : k_score<false>, persistent_blocks(b * 32, 256, 8), 256, 0, st, la);
+  cudaStream_t sd = st;
+  if (side) {
+    sd = side;
+    KG_CUDA(cudaEventRecord(loss_fork_event(), st));
+    KG_CUDA(cudaStreamWaitEvent(sd, loss_fork_event(), 0));
+  }
   int nb = persistent_blocks(b, 256, 4);
   if (nb > 1024) nb = 1024;
-  KG_LAUNCH("k_block_sums", k_block_sums, nb, 256, 0, st, w.per, b, w.part);
-  KG_LAUNCH("k_final_mean", k_final_mean, 1, 256, 0, st, w.part, nb, b, loss_out, flags);
-  kg_status s = seg_sums<0>(la, w.rv, b, nullptr, nullptr, R, d_decoder, w.wr, st);
+  KG_LAUNCH("k_block_sums", k_block_sums, nb, 256, 0, sd, w.per, b, w.part);
+  KG_LAUNCH("k_final_mean", k_final_mean, 1, 256, 0, sd, w.part, nb, b, loss_out, flags);
+  kg_status s = seg_sums<0>(la, w.rv, b, nullptr, nullptr, R, d_decoder, w.wr, sd);
   if (s != KG_OK) return s;
   return seg_sums<1>(la, w.vv, 2 * b, order, counts, (int32_t)w.ngmax, dH, w.wv, st);
 }
@@ -496,9 +510,10 @@ kg_status kg_loss_compute(const float* H, int32_t d, int32_t n_local, const floa
                           const int32_t* tri, const float* labels, int64_t total, int64_t start,
                           const int64_t* start_dev, int64_t b, const int32_t* order, const int32_t* counts,
                           float* dH, float* d_decoder, float* loss_out, float* scores_out, uint32_t* flags,
-                          void* ws, int64_t ws_bytes, void* stream) {
+                          void* ws, int64_t ws_bytes, void* stream, void* side_stream) {
   KG_LOSS_SETUP();
-  return loss_compute(la, R, order, counts, dH, d_decoder, loss_out, flags, w, st);
+  return loss_compute(la, R, order, counts, dH, d_decoder, loss_out, flags, w, st,
+                      side_stream ? as_stream(side_stream) : nullptr);
 }
 
 }  // extern "C"

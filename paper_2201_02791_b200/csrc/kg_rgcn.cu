@@ -860,9 +860,40 @@ static Chunks csc_chunks(const kg_graph_csr* G) {
 
 }  // namespace kg
 
+namespace kg {
+// Y = X[A_{t+1}] . [V_0 | .. | V_{B-1}], rows by closure position
+static kg_status y_gemm(const kg_graph_csr* G, const kg_layer_params* lp, const float* H_in,
+                        const float* H_in_packed, const float* Wy, const int32_t* order, const int32_t* counts,
+                        int32_t t, float* Y, void* gemm_ws, cudaStream_t st) {
+  const int B = lp->B, di = lp->d_in, dO = lp->d_out;
+  GemmArgs gy{};
+  gy.A = H_in; gy.lda = di; gy.a_rows = order;
+  gy.a_packed = H_in_packed;
+  gy.B = Wy; gy.ldb = (int64_t)B * dO;
+  gy.C = Y; gy.ldc = (int64_t)B * dO;
+  gy.M_dev = counts; gy.M_dev_index = t + 1; gy.M_max = G->n;
+  gy.K = di; gy.N = (int64_t)B * dO;
+  if (lp->packed) gy.b_packed = lp->packed + weights_layout(di, dO, B).off[1];
+  return gemm_nn(gy, gemm_ws, st);
+}
+}  // namespace kg
+
 using namespace kg;
 
 extern "C" {
+
+kg_status kg_rgcn_backward_y(const kg_graph_csr* G, const kg_layer_params* lp, const float* H_in,
+                             const float* H_in_packed, const int32_t* order, const int32_t* counts, int32_t t,
+                             void* ws, int64_t ws_bytes, void* stream) {
+  KG_REQUIRE(lp->packed != nullptr, KG_ERR_VALIDATION, "kg_rgcn_backward_y needs packed weights");
+  LayerWs w;
+  size_t need = layer_ws(G->n, G->e, cap_split_chunks(G), lp->d_in, lp->d_out, lp->B, G->R, &w, ws,
+                         (size_t)ws_bytes);
+  KG_REQUIRE((size_t)ws_bytes >= need, KG_ERR_VALIDATION, "layer workspace too small");
+  // gemm_tn is the side-stream region (the forward of the same layer may be
+  // using w.gemm concurrently)
+  return y_gemm(G, lp, H_in, H_in_packed, nullptr, order, counts, t, w.Y, w.gemm_tn, as_stream(stream));
+}
 
 int64_t kg_layer_workspace_bytes(const kg_graph_csr* G, int32_t d_in, int32_t d_out, int32_t B) {
   return (int64_t)layer_ws(G->n, G->e, cap_split_chunks(G), d_in, d_out, B, G->R, nullptr, nullptr, 0);
@@ -907,8 +938,8 @@ kg_status kg_rgcn_forward(const kg_graph_csr* G, const kg_layer_params* lp, cons
 kg_status kg_rgcn_backward(const kg_graph_csr* G, const kg_layer_params* lp, const float* H_in, const float* H_out,
                            const float* dH_out, float* dH_in, const int32_t* order, const int32_t* pos,
                            const int32_t* counts, int32_t t, float* d_bases, float* d_coeffs,
-                           const float* H_in_packed, const float* dropout_mask, void* ws, int64_t ws_bytes,
-                           void* stream, void* side_stream) {
+                           const float* H_in_packed, const float* dropout_mask, int32_t y_ready, void* ws,
+                           int64_t ws_bytes, void* stream, void* side_stream) {
   cudaStream_t st = as_stream(stream);
   const int B = lp->B, di = lp->d_in, dO = lp->d_out;
   KG_REQUIRE(B >= 1 && B <= MAXB, KG_ERR_VALIDATION, "num_bases must be in [1, %d]", MAXB);
@@ -926,17 +957,12 @@ kg_status kg_rgcn_backward(const kg_graph_csr* G, const kg_layer_params* lp, con
   else
     KG_LAUNCH("k_dz", k_dz<false>, persistent_blocks((int64_t)G->n * 32, 256, 8), 256, 0, st, dH_out, H_out, order,
               counts, t, dO, dropout_mask, w.dZ);
-  // Y = X[A_{t+1}] . [V_0 | .. | V_{B-1}]
-  GemmArgs gy{};
-  gy.A = H_in; gy.lda = di; gy.a_rows = order;
-  gy.a_packed = H_in_packed;
-  gy.B = w.Wy; gy.ldb = (int64_t)B * dO;
-  gy.C = w.Y; gy.ldc = (int64_t)B * dO;
-  gy.M_dev = counts; gy.M_dev_index = t + 1; gy.M_max = G->n;
-  gy.K = di; gy.N = (int64_t)B * dO;
-  if (lp->packed) gy.b_packed = lp->packed + wl.off[1];
-  kg_status s = gemm_nn(gy, w.gemm, st);
-  if (s != KG_OK) return s;
+  // Y = X[A_{t+1}] . [V_0 | .. | V_{B-1}]  (unless kg_rgcn_backward_y made it)
+  kg_status s = KG_OK;
+  if (!y_ready) {
+    s = y_gemm(G, lp, H_in, H_in_packed, w.Wy, order, counts, t, w.Y, w.gemm, st);
+    if (s != KG_OK) return s;
+  }
   CscArgs c{G->c_indptr, G->c_dst, G->c_rel, G->c_norm, csc_chunks(G), lp->coeffs, lp->G, B, dO, w.Y, w.dZ, pos,
             counts, t, w.dS, w.ed, w.ed_self, w.partial,
             direct_pack(G->n, (int64_t)B * dO) ? w.dS_pk : nullptr, packed_records((int64_t)B * dO)};

@@ -316,8 +316,19 @@ def device_dropout(bufs: ViewBuffers, g_dev, p: float) -> list:
     return masks
 
 
+def device_backward_y(model: DeviceModel, bufs: ViewBuffers, l: int) -> None:
+    """Layer l's backward operand Y = H_l[A_{t+1}] . [V_0 | .. | V_{B-1}]
+    ahead of time (needs packed weights and bufs.hpk(l)); kg_rgcn_backward
+    then runs with y_ready."""
+    L = model.config.num_layers
+    ws = bufs.layer_ws(l)
+    _lib.call("kg_rgcn_backward_y", ctypes.byref(bufs.view.csr()), ctypes.byref(model.layer(l, True)),
+              bufs.H[l].data_ptr(), bufs.hpk(l).data_ptr(), bufs.order.data_ptr(), bufs.counts.data_ptr(),
+              L - 1 - l, ws.data_ptr(), ws.numel(), _lib.stream_handle())
+
+
 def device_forward(model: DeviceModel, bufs: ViewBuffers, packed: bool = False, hpk: bool = False,
-                   masks: Optional[list] = None) -> None:
+                   masks: Optional[list] = None, after_layer=None) -> None:
     """All layers over the closure in bufs.order/counts (ref:model.py:196-235).
     packed: use the model's pre-packed weight operands (DeviceModel.repack);
     hpk: also emit each hidden layer's output as the next layer's packed
@@ -331,10 +342,12 @@ def device_forward(model: DeviceModel, bufs: ViewBuffers, packed: bool = False, 
                   bufs.H[l + 1].data_ptr(), bufs.order.data_ptr(), bufs.pos.data_ptr(), bufs.counts.data_ptr(),
                   L - 1 - l, 1 if l < L - 1 else 0, masks[l].data_ptr() if (masks and l < L - 1) else None,
                   bufs.hpk(l + 1).data_ptr() if (hpk and l < L - 1) else None, ws.data_ptr(), ws.numel(), st)
+        if after_layer is not None:
+            after_layer(l)
 
 
 def device_loss(model: DeviceModel, bufs: ViewBuffers, stream, start: int, b: int, grad_flat, loss_out,
-                scores_out=None, start_dev=None, part: str = "all") -> None:
+                scores_out=None, start_dev=None, part: str = "all", side=None) -> None:
     """DistMult + BCE (ref:model.py:254-281): loss -> loss_out (device scalar),
     d_decoder -> grad_flat's decoder block, dH_L -> bufs.dH[L] seed rows.
     part "groups" / "compute" run the two halves separately (the batch-only
@@ -343,17 +356,21 @@ def device_loss(model: DeviceModel, bufs: ViewBuffers, stream, start: int, b: in
     L = cfg.num_layers
     ws = bufs.loss_ws(b)
     fn = {"all": "kg_distmult_loss", "groups": "kg_loss_groups", "compute": "kg_loss_compute"}[part]
-    _lib.call(fn, bufs.H[L].data_ptr(), cfg.dims[-1], bufs.n, model.decoder_ptr(),
-              cfg.num_relations, stream.triples.data_ptr(), stream.labels.data_ptr(), stream.total, start,
-              _lib.ptr(start_dev), b,
-              bufs.order.data_ptr(), bufs.counts.data_ptr(), bufs.dH[L].data_ptr(),
-              grad_flat.data_ptr() + 4 * model.layout.decoder_off(), loss_out.data_ptr(),
-              0 if scores_out is None else scores_out.data_ptr(), bufs.flags.data_ptr(), ws.data_ptr(),
-              ws.numel(), _lib.stream_handle())
+    args = [bufs.H[L].data_ptr(), cfg.dims[-1], bufs.n, model.decoder_ptr(),
+            cfg.num_relations, stream.triples.data_ptr(), stream.labels.data_ptr(), stream.total, start,
+            _lib.ptr(start_dev), b,
+            bufs.order.data_ptr(), bufs.counts.data_ptr(), bufs.dH[L].data_ptr(),
+            grad_flat.data_ptr() + 4 * model.layout.decoder_off(), loss_out.data_ptr(),
+            0 if scores_out is None else scores_out.data_ptr(), bufs.flags.data_ptr(), ws.data_ptr(),
+            ws.numel(), _lib.stream_handle()]
+    if part == "compute":
+        args.append(None if side is None else side.cuda_stream)
+    _lib.call(fn, *args)
 
 
 def device_backward(model: DeviceModel, bufs: ViewBuffers, grad_flat, input_grad: bool, side=None,
-                    packed: bool = False, hpk: bool = False, masks: Optional[list] = None) -> None:
+                    packed: bool = False, hpk: bool = False, masks: Optional[list] = None,
+                    y_ready: bool = False) -> None:
     """Layer gradients in reverse (ref:model.py:283-296): d bases / d coeffs
     into grad_flat, dL/dH_0 rows into bufs.dH[0] when input_grad. With a side
     stream (torch.cuda.Stream) the parameter-gradient branch of every layer
@@ -371,7 +388,7 @@ def device_backward(model: DeviceModel, bufs: ViewBuffers, grad_flat, input_grad
                   bufs.order.data_ptr(), bufs.pos.data_ptr(), bufs.counts.data_ptr(), L - 1 - l,
                   grad_flat.data_ptr() + 4 * lay.bases_off(l), grad_flat.data_ptr() + 4 * lay.coeffs_off(l),
                   bufs.hpk(l).data_ptr() if hpk else None, masks[l].data_ptr() if (masks and l < L - 1) else None,
-                  ws.data_ptr(), ws.numel(), st, None if side is None else side.cuda_stream)
+                  1 if y_ready else 0, ws.data_ptr(), ws.numel(), st, None if side is None else side.cuda_stream)
     if side is not None:
         torch.cuda.current_stream().wait_stream(side)
 

@@ -30,8 +30,8 @@ import numpy as np
 from . import _lib
 from .errors import KGError, NumericError, ProtocolError, ValidationError
 from .model import (MODE_EMBEDDING, MODE_FEATURE, DeviceModel, ModelConfig, ModelParams, ViewBuffers,
-                    check_flags, device_backward, device_dropout, device_forward, device_loss,
-                    device_pack_inputs, init_params)
+                    check_flags, device_backward, device_backward_y, device_dropout, device_forward,
+                    device_loss, device_pack_inputs, init_params)
 from .partition import PartitionSet
 from .sampler import EpochSampler, build_view
 
@@ -458,18 +458,30 @@ class Trainer:
             w.prep.import_round(w.slot(), self.round_dev, w.bufs.loss_ws(w.b))
             gslot = self.grads_local[i]
             side = self._loss_stream if self.fork_streams else main
+            masks = device_dropout(w.bufs, w.g_drop, self.mc.dropout) if w.g_drop is not None else None
             side.wait_stream(main)
             with torch.cuda.stream(side):
-                device_pack_inputs(w.bufs)   # layer-0 backward operand, beside the forward
-            masks = device_dropout(w.bufs, w.g_drop, self.mc.dropout) if w.g_drop is not None else None
-            device_forward(self.model, w.bufs, packed=True, hpk=True, masks=masks)
+                # backward operands that only need forward outputs, beside the forward:
+                # layer 0's packed input rows and Y_0 = H_0 . [V_b]
+                device_pack_inputs(w.bufs)
+                device_backward_y(self.model, w.bufs, 0)
+
+            def after_layer(l, w=w):   # H_{l+1} is ready: Y_{l+1} on the forked stream
+                if l + 1 < self.mc.num_layers:
+                    side.wait_stream(main)
+                    with torch.cuda.stream(side):
+                        device_backward_y(self.model, w.bufs, l + 1)
+
+            device_forward(self.model, w.bufs, packed=True, hpk=True, masks=masks, after_layer=after_layer)
             main.wait_stream(side)
             device_loss(self.model, w.bufs, w.stream, 0, w.b, gslot, self.loss_scratch[i:i + 1],
-                        start_dev=self.start_dev[i:i + 1], part="compute")
-            self.losses[i].index_copy_(0, self.round_dev, self.loss_scratch[i:i + 1])
+                        start_dev=self.start_dev[i:i + 1], part="compute",
+                        side=self._loss_stream if self.fork_streams else None)
             device_backward(self.model, w.bufs, gslot, input_grad=w.emb,
                             side=self._loss_stream if self.fork_streams else None, packed=True, hpk=True,
-                            masks=masks)
+                            masks=masks, y_ready=True)
+            # the loss value comes from the forked stream, joined by device_backward
+            self.losses[i].index_copy_(0, self.round_dev, self.loss_scratch[i:i + 1])
 
     def _update_body(self):
         """Fused tree-mean + dense Adam/SGD, then lazy sparse rows."""
