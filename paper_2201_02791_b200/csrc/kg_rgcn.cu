@@ -323,9 +323,13 @@ struct CscArgs {
   float* partial;        // (split chunks, B*d)
   float* dS_pk;          // optional: dS also as packed GEMM A records (dX = dS . Wb)
   int64_t dS_nk;
+  int self_dots;         // k_csc_combine: also the split rows' self dots (MODE 0 runs)
 };
 
-template <int NB, int VEC, int S>
+// MODE 0: dS and edge dots in one pass. MODE 1: dS only (the critical path:
+// dX = dS . Wb feeds the next layer). MODE 2: edge dots + self dots only (they
+// feed only d coeffs, so this pass runs on the forked stream).
+template <int NB, int VEC, int S, int MODE>
 __global__ void __launch_bounds__(256, 3) k_csc_backward(CscArgs a) {
   extern __shared__ float coef[];
   for (int i = threadIdx.x; i < a.G * a.B; i += blockDim.x) coef[i] = a.coeffs[i];
@@ -350,7 +354,8 @@ __global__ void __launch_bounds__(256, 3) k_csc_backward(CscArgs a) {
     if (q < 0 || q >= Sn) {
       // not a source of this layer: its edge dots are zero (k_dcoeff_partial
       // sums every edge of a relation without a membership test)
-      for (int x = (int)lane; x < cnt * B; x += 32) a.ed[(int64_t)beg * B + x] = 0.f;
+      if (MODE != 1)
+        for (int x = (int)lane; x < cnt * B; x += 32) a.ed[(int64_t)beg * B + x] = 0.f;
       continue;
     }
     // metadata: destination position (-1 if not a target) and coefficients
@@ -371,9 +376,10 @@ __global__ void __launch_bounds__(256, 3) k_csc_backward(CscArgs a) {
         if (pw >= 0 && pw < T) {
           m.other[h] = pw;
           nrm[h] = nw;
+          if (MODE != 2)
 #pragma unroll
-          for (int b = 0; b < NB; ++b)
-            if (b < B) m.cf[h][b] = nw * coef[r * B + b];
+            for (int b = 0; b < NB; ++b)
+              if (b < B) m.cf[h][b] = nw * coef[r * B + b];
         }
       }
     }
@@ -381,12 +387,13 @@ __global__ void __launch_bounds__(256, 3) k_csc_backward(CscArgs a) {
     float acc[NB][S][VEC];
     zero3<NB, VEC, S>(acc);
     zero3<NB, VEC, S>(y);
+    if (MODE != 1)
 #pragma unroll
-    for (int b = 0; b < NB; ++b)
-      if (b < B)
+      for (int b = 0; b < NB; ++b)
+        if (b < B)
 #pragma unroll
-        for (int s = 0; s < S; ++s)
-          if (slot_ok[s]) VecIO<VEC>::load(a.Y + ((int64_t)q * B + b) * d + (s * 32 + lane) * VEC, y[b][s]);
+          for (int s = 0; s < S; ++s)
+            if (slot_ok[s]) VecIO<VEC>::load(a.Y + ((int64_t)q * B + b) * d + (s * 32 + lane) * VEC, y[b][s]);
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
       const int nh = min(32, cnt - 32 * h);
@@ -405,6 +412,7 @@ __global__ void __launch_bounds__(256, 3) k_csc_backward(CscArgs a) {
           }
         }
         // dS_b += c_eb * dZ[dst]
+        if (MODE != 2)
 #pragma unroll
         for (int k = 0; k < UNR; ++k) {
 #pragma unroll
@@ -419,6 +427,7 @@ __global__ void __launch_bounds__(256, 3) k_csc_backward(CscArgs a) {
           }
         }
         // per-edge dots <Y_b[u], dZ[dst]>: one transposed warp reduction per b
+        if (MODE != 1)
 #pragma unroll
         for (int b = 0; b < NB; ++b) {
           if (b < B) {
@@ -439,6 +448,32 @@ __global__ void __launch_bounds__(256, 3) k_csc_backward(CscArgs a) {
           }
         }
       }
+    }
+    if (MODE == 2) {
+      // self dot for d a[2R,b], by the row's first chunk (split rows too)
+      if (c == cbase && q < T) {
+        float z[S][VEC];
+#pragma unroll
+        for (int s = 0; s < S; ++s) {
+          if (slot_ok[s]) VecIO<VEC>::load(a.dZ + (int64_t)q * d + (s * 32 + lane) * VEC, z[s]);
+          else
+#pragma unroll
+            for (int cc = 0; cc < VEC; ++cc) z[s][cc] = 0.f;
+        }
+#pragma unroll
+        for (int b = 0; b < NB; ++b) {
+          if (b < B) {
+            float dp = 0.f;
+#pragma unroll
+            for (int s = 0; s < S; ++s)
+#pragma unroll
+              for (int cc = 0; cc < VEC; ++cc) dp = fmaf(y[b][s][cc], z[s][cc], dp);
+            dp = warp_sum(dp);
+            if (lane == 0) a.ed_self[(int64_t)q * B + b] = dp;
+          }
+        }
+      }
+      continue;
     }
     float* out;
     if (nch == 1) {
@@ -464,8 +499,10 @@ __global__ void __launch_bounds__(256, 3) k_csc_backward(CscArgs a) {
                 acc[b][s][cc] = fmaf(cf, z[s][cc], acc[b][s][cc]);
                 dp = fmaf(y[b][s][cc], z[s][cc], dp);
               }
-            dp = warp_sum(dp);
-            if (lane == 0) a.ed_self[(int64_t)q * B + b] = dp;
+            if (MODE == 0) {
+              dp = warp_sum(dp);
+              if (lane == 0) a.ed_self[(int64_t)q * B + b] = dp;
+            }
           }
         }
       }
@@ -530,7 +567,7 @@ __global__ void __launch_bounds__(CB_THREADS) k_csc_combine(CscArgs a) {
       }
     }
     if (a.dS_pk && threadIdx.x < 32) packed_zero_pad(a.dS_pk, a.dS_nk, q, width, threadIdx.x, 32);
-    if (self && threadIdx.x < 32) {
+    if (a.self_dots && self && threadIdx.x < 32) {
       const int lane = threadIdx.x;
       for (int b = 0; b < a.B; ++b) {
         float dp = 0.f;
@@ -738,14 +775,27 @@ static kg_status launch_agg(const AggArgs& a, int blocks, int cblocks, size_t sm
   else KG_LAUNCH("k_aggregate_combine", k_aggregate_combine<false>, cblocks, CB_THREADS, 0, st, a);
   return KG_OK;
 }
-template <int VEC, int S>
-static kg_status launch_csc(const CscArgs& a, int blocks, int cblocks, size_t smem, cudaStream_t st) {
+template <int VEC, int S, int MODE>
+static kg_status launch_csc_mode(const CscArgs& a, int blocks, size_t smem, cudaStream_t st) {
+  const char* name = MODE == 2 ? "k_csc_dots" : "k_csc_backward";
   switch (a.B) {
-    case 1: KG_LAUNCH("k_csc_backward", (k_csc_backward<1, VEC, S>), blocks, 256, smem, st, a); break;
-    case 2: KG_LAUNCH("k_csc_backward", (k_csc_backward<2, VEC, S>), blocks, 256, smem, st, a); break;
-    case 3: KG_LAUNCH("k_csc_backward", (k_csc_backward<3, VEC, S>), blocks, 256, smem, st, a); break;
-    default: KG_LAUNCH("k_csc_backward", (k_csc_backward<4, VEC, S>), blocks, 256, smem, st, a); break;
+    case 1: KG_LAUNCH(name, (k_csc_backward<1, VEC, S, MODE>), blocks, 256, smem, st, a); break;
+    case 2: KG_LAUNCH(name, (k_csc_backward<2, VEC, S, MODE>), blocks, 256, smem, st, a); break;
+    case 3: KG_LAUNCH(name, (k_csc_backward<3, VEC, S, MODE>), blocks, 256, smem, st, a); break;
+    default: KG_LAUNCH(name, (k_csc_backward<4, VEC, S, MODE>), blocks, 256, smem, st, a); break;
   }
+  return KG_OK;
+}
+
+// mode 0: dS + dots (+ combine); 1: dS (+ combine without self dots); 2: dots only
+template <int VEC, int S>
+static kg_status launch_csc(const CscArgs& a0, int blocks, int cblocks, size_t smem, cudaStream_t st, int mode) {
+  CscArgs a = a0;
+  a.self_dots = mode == 0;
+  kg_status s = mode == 0 ? launch_csc_mode<VEC, S, 0>(a, blocks, smem, st)
+              : mode == 1 ? launch_csc_mode<VEC, S, 1>(a, blocks, smem, st)
+                          : launch_csc_mode<VEC, S, 2>(a, blocks, smem, st);
+  if (s != KG_OK || mode == 2) return s;
   if (a.d % 4 == 0) KG_LAUNCH("k_csc_combine", k_csc_combine<true>, cblocks, CB_THREADS, 0, st, a);
   else KG_LAUNCH("k_csc_combine", k_csc_combine<false>, cblocks, CB_THREADS, 0, st, a);
   return KG_OK;
@@ -775,17 +825,17 @@ static kg_status run_aggregate(const AggArgs& a, const kg_graph_csr* G, cudaStre
       [&] { return launch_agg<1, 8>(a, blocks, cblocks, smem, st); });
 }
 
-static kg_status run_csc(const CscArgs& a, const kg_graph_csr* G, cudaStream_t st) {
+static kg_status run_csc(const CscArgs& a, const kg_graph_csr* G, cudaStream_t st, int mode = 0) {
   KG_REQUIRE(G->chunk <= MAXC, KG_ERR_VALIDATION, "chunk size %d > %d", G->chunk, MAXC);
   int blocks = persistent_blocks(cap_chunks(G) * 32, 256, 3);
   int cblocks = persistent_blocks(cap_split_rows(G) * CB_THREADS, CB_THREADS, 8);   // one block per split row
   size_t smem = (size_t)a.G * a.B * sizeof(float);
   return dispatch_width(
-      a.d, [&] { return launch_csc<4, 1>(a, blocks, cblocks, smem, st); },
-      [&] { return launch_csc<1, 1>(a, blocks, cblocks, smem, st); },
-      [&] { return launch_csc<1, 2>(a, blocks, cblocks, smem, st); },
-      [&] { return launch_csc<1, 4>(a, blocks, cblocks, smem, st); },
-      [&] { return launch_csc<1, 8>(a, blocks, cblocks, smem, st); });
+      a.d, [&] { return launch_csc<4, 1>(a, blocks, cblocks, smem, st, mode); },
+      [&] { return launch_csc<1, 1>(a, blocks, cblocks, smem, st, mode); },
+      [&] { return launch_csc<1, 2>(a, blocks, cblocks, smem, st, mode); },
+      [&] { return launch_csc<1, 4>(a, blocks, cblocks, smem, st, mode); },
+      [&] { return launch_csc<1, 8>(a, blocks, cblocks, smem, st, mode); });
 }
 
 struct LayerWs {
@@ -965,16 +1015,30 @@ kg_status kg_rgcn_backward(const kg_graph_csr* G, const kg_layer_params* lp, con
   }
   CscArgs c{G->c_indptr, G->c_dst, G->c_rel, G->c_norm, csc_chunks(G), lp->coeffs, lp->G, B, dO, w.Y, w.dZ, pos,
             counts, t, w.dS, w.ed, w.ed_self, w.partial,
-            direct_pack(G->n, (int64_t)B * dO) ? w.dS_pk : nullptr, packed_records((int64_t)B * dO)};
-  s = run_csc(c, G, st);
-  if (s != KG_OK) return s;
+            direct_pack(G->n, (int64_t)B * dO) ? w.dS_pk : nullptr, packed_records((int64_t)B * dO), 1};
   // The parameter gradients (dV, d coeffs) feed only the optimizer: with a side
   // stream they leave the critical path (the caller joins it before the update).
+  // There the CSC pass splits: dS on `st`, the edge/self dots (d coeffs) on the
+  // side stream concurrently; dV follows dS on the side stream.
   cudaStream_t sd = st;
+  const int split = dcoeff_split(G->e, lp->G);
   if (side_stream) {
     sd = as_stream(side_stream);
     KG_CUDA(cudaEventRecord(fork_event(), st));
     KG_CUDA(cudaStreamWaitEvent(sd, fork_event(), 0));
+    s = run_csc(c, G, sd, 2);
+    if (s != KG_OK) return s;
+    KG_LAUNCH("k_dcoeff_reduce", k_dcoeff_partial, dim3((unsigned)lp->G, (unsigned)split, 1), 256, 0, sd,
+              G->rel_ptr, G->rel_perm, counts, t, w.ed, w.ed_self, lp->G, B, w.dc_part);
+    KG_LAUNCH("k_dcoeff_final", k_dcoeff_final, persistent_blocks((int64_t)lp->G * B, 256, 2), 256, 0, sd,
+              w.dc_part, lp->G, B, split, d_coeffs);
+    s = run_csc(c, G, st, 1);
+    if (s != KG_OK) return s;
+    KG_CUDA(cudaEventRecord(fork_event(), st));
+    KG_CUDA(cudaStreamWaitEvent(sd, fork_event(), 0));
+  } else {
+    s = run_csc(c, G, st, 0);
+    if (s != KG_OK) return s;
   }
   // dV = X^T dS  (reduction over the source rows)
   GemmArgs gv{};
@@ -985,11 +1049,12 @@ kg_status kg_rgcn_backward(const kg_graph_csr* G, const kg_layer_params* lp, con
   s = gemm_tn(gv, w.Rm, w.gemm_tn, sd);
   if (s != KG_OK) return s;
   KG_LAUNCH("k_dbases_layout", k_dbases_layout, persistent_blocks(wn, 256, 2), 256, 0, sd, w.Rm, B, di, dO, d_bases);
-  const int split = dcoeff_split(G->e, lp->G);
-  KG_LAUNCH("k_dcoeff_reduce", k_dcoeff_partial, dim3((unsigned)lp->G, (unsigned)split, 1), 256, 0, sd, G->rel_ptr,
-            G->rel_perm, counts, t, w.ed, w.ed_self, lp->G, B, w.dc_part);
-  KG_LAUNCH("k_dcoeff_final", k_dcoeff_final, persistent_blocks((int64_t)lp->G * B, 256, 2), 256, 0, sd, w.dc_part,
-            lp->G, B, split, d_coeffs);
+  if (!side_stream) {
+    KG_LAUNCH("k_dcoeff_reduce", k_dcoeff_partial, dim3((unsigned)lp->G, (unsigned)split, 1), 256, 0, sd,
+              G->rel_ptr, G->rel_perm, counts, t, w.ed, w.ed_self, lp->G, B, w.dc_part);
+    KG_LAUNCH("k_dcoeff_final", k_dcoeff_final, persistent_blocks((int64_t)lp->G * B, 256, 2), 256, 0, sd,
+              w.dc_part, lp->G, B, split, d_coeffs);
+  }
   if (dH_in) {
     GemmArgs gx{};
     gx.A = w.dS; gx.lda = (int64_t)B * dO;
