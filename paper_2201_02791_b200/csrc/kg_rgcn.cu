@@ -756,7 +756,9 @@ __global__ void k_pack_weights(const float* __restrict__ V, int B, int di, int d
   }
 }
 
-static bool vec4_ok(int d) { return d % 4 == 0 && d <= 128; }
+// float4 lanes only when they fill most of the warp (d > 64); narrower rows use
+// one float per lane so all 32 lanes gather
+static bool vec4_ok(int d) { return d % 4 == 0 && d > 64 && d <= 128; }
 
 // chunk capacities of kg_graph_csr (see the header)
 static int64_t cap_chunks(const kg_graph_csr* G) { return (int64_t)G->n + G->e / G->chunk + 1; }

@@ -1,8 +1,13 @@
-"""Config 4: ogbl-wikikg2-shaped synthetic KG (2.5M entities,
-535 relations, ~16M train triples), RGCN dims [128,128,128], 2 bases, P = 8
-vertex-cut partitions with 2-hop halos, b = 1,048,576 per GPU. One GPU runs
-partition `--part` exactly as it would in the 8-GPU job (its per-round work
-does not depend on the other ranks apart from the 553 KB gradient exchange).
+"""Configs 4 and 5 on one GPU:
+  4: ogbl-wikikg2-shaped synthetic KG (2.5M entities, 535 relations, ~16M
+     train triples), RGCN dims [128,128,128], 2 bases, P = 8 vertex-cut
+     partitions with 2-hop halos, b = 1,048,576 per GPU;
+  5: ogbl-citation2-shaped graph (2.93M nodes, 1 relation, ~30.4M edges),
+     3-layer RGCN dims [32,32,32,32], 3-hop halos, P = 8, 256/P batches per
+     epoch (b ~ 237k per GPU).
+One GPU runs partition `--part` exactly as it would in the 8-GPU job (its
+per-round work does not depend on the other ranks apart from the small dense
+gradient exchange).
 
 Prints one JSON line: triples/s of the partition, and for the message-passing
 kernels the algorithmic bytes per launch / measured launch time
@@ -24,6 +29,7 @@ from paper_2201_02791_b200 import _lib
 from paper_2201_02791_b200.partition import PartitionSet
 
 ap = argparse.ArgumentParser()
+ap.add_argument("--config", type=int, default=4, choices=[4, 5])
 ap.add_argument("--scale", type=float, default=1.0)
 ap.add_argument("--parts", type=int, default=8)
 ap.add_argument("--part", type=int, default=0)
@@ -32,16 +38,23 @@ ap.add_argument("--rounds", type=int, default=8)
 args = ap.parse_args()
 
 t0 = time.perf_counter()
-n_ent = int(2_500_000 * args.scale)
-graph, split = kb.generate_synthetic(n_ent, 535, 6.4, seed=0)
+if args.config == 4:
+    n_ent, R, deg, dims, hops = int(2_500_000 * args.scale), 535, 6.4, [128, 128, 128], 2
+else:
+    n_ent, R, dims, hops = int(2_927_963 * args.scale), 1, [32, 32, 32, 32], 3
+    deg = 30_387_995 / 2_927_963
+graph, split = kb.generate_synthetic(n_ent, R, deg, seed=0)
 t_gen = time.perf_counter() - t0
 t0 = time.perf_counter()
-pset = kb.neighborhood_expand(kb.vertex_cut_partition(graph, args.parts, seed=0), graph, 2)
+pset = kb.neighborhood_expand(kb.vertex_cut_partition(graph, args.parts, seed=0), graph, hops)
 t_part = time.perf_counter() - t0
 one = PartitionSet([pset.partitions[args.part]], pset.num_entities, pset.num_relations, pset.hops, pset.seed,
                    pset.method, pset.graph_checksum)
-mc = kb.ModelConfig(2, [128, 128, 128], 2, 535, 1, mode="embedding")
-tc = kb.TrainConfig(batch_size=args.batch, seed=0)
+mc = kb.ModelConfig(len(dims) - 1, dims, 2, R, 1, mode="embedding")
+if args.config == 4:
+    tc = kb.TrainConfig(batch_size=args.batch, seed=0)
+else:   # 256 / P batches per epoch
+    tc = kb.TrainConfig(fixed_num_batches=max(1, 256 // args.parts), seed=0)
 t0 = time.perf_counter()
 tr = kb.Trainer(one, graph, mc, tc)
 t_setup = time.perf_counter() - t0
@@ -88,11 +101,12 @@ for name in ("k_aggregate", "k_csc_backward"):
 shapes = bench.layer_shapes(tr, w)
 top = sorted(bd.items(), key=lambda x: -x[1][1])[:12]
 print(json.dumps({
-    "workload": f"wikikg2-shape synthetic KG scale {args.scale}: {graph.num_entities} entities, 535 relations, "
-                f"{len(graph.triples)} train triples; partition {args.part} of {args.parts} (2-hop halo)",
+    "workload": f"config {args.config} synthetic KG scale {args.scale}: {graph.num_entities} entities, {R} relations, "
+                f"{len(graph.triples)} train triples; dims {dims}; partition {args.part} of {args.parts} "
+                f"({hops}-hop halo)",
     "n_local": w.view.n, "messages": int(w.view.e) if hasattr(w.view, "e") else None,
-    "batch": args.batch, "rounds_per_epoch": tr.rounds, "layer_shapes_T_S_E": shapes,
-    "ms_per_round": ms, "triples_per_s": args.batch / (ms * 1e-3),
+    "batch": w.b, "rounds_per_epoch": tr.rounds, "layer_shapes_T_S_E": shapes,
+    "ms_per_round": ms, "triples_per_s": w.b / (ms * 1e-3),
     "kernels": kern, "peak_hbm_gbs": peak,
     "eager_breakdown_ms": {k: round(v[1], 3) for k, v in top},
     "host_s": {"generate": round(t_gen, 1), "partition_expand": round(t_part, 1), "trainer_setup": round(t_setup, 1)},
