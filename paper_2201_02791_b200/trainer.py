@@ -430,7 +430,10 @@ class Trainer:
         self.last_timer_handle = None
         self._graphs = {}
         self._graph_pool = None
-        self._loss_stream = torch.cuda.Stream(self.dev)   # forked work beside the layers
+        # Training runs on high-priority streams: the sampler's epoch graphs
+        # (default, low priority) then fill SM slots training leaves idle.
+        self._prio = torch.cuda.Stream(self.dev, priority=-2)
+        self._loss_stream = torch.cuda.Stream(self.dev, priority=-2)   # forked work beside the layers
         # diagnostics: KG_FORK_STREAMS=0 keeps every kernel on one stream
         self.fork_streams = os.environ.get("KG_FORK_STREAMS", "1") != "0"
         self.model.repack()
@@ -509,29 +512,33 @@ class Trainer:
         and update halves are captured as CUDA graphs (one pair per epoch
         buffer slot) and replayed; the NCCL gather runs between them."""
         torch = _torch()
-        if not self.use_graphs or self._eager_rounds < 2:
-            self._compute_body()
-            if self.dist:
-                self._gather()
-            self._update_body()
-            self._eager_rounds += 1
-        else:
-            if not self._graphs:
-                self._capture_all()
-            key = tuple(w.stream.triples.data_ptr() for w in self.workers)
-            gc, gu, nk = self._graphs[key]
-            self.last_timer_handle = self._timer_handles.get(key)
-            gc.replay()
-            if self.dist:
-                self._gather()
-            gu.replay()
-            self.graph_kernel_launches += nk
+        cur = torch.cuda.current_stream()
+        self._prio.wait_stream(cur)
+        with torch.cuda.stream(self._prio):
+            if not self.use_graphs or self._eager_rounds < 2:
+                self._compute_body()
+                if self.dist:
+                    self._gather()
+                self._update_body()
+                self._eager_rounds += 1
+            else:
+                if not self._graphs:
+                    self._capture_all()
+                key = tuple(w.stream.triples.data_ptr() for w in self.workers)
+                gc, gu, nk = self._graphs[key]
+                self.last_timer_handle = self._timer_handles.get(key)
+                gc.replay()
+                if self.dist:
+                    self._gather()
+                gu.replay()
+                self.graph_kernel_launches += nk
+        cur.wait_stream(self._prio)
         self.t += 1
         self.round_in_epoch += 1
 
     def _capture(self, body, graph):
         torch = _torch()
-        side = torch.cuda.Stream(self.dev)
+        side = torch.cuda.Stream(self.dev, priority=-2)
         side.wait_stream(torch.cuda.current_stream())
         with torch.cuda.stream(side):
             graph.capture_begin(pool=self._graph_pool)
