@@ -20,5 +20,8 @@ from .model import (MODE_EMBEDDING, MODE_FEATURE, Gradients, ModelConfig, ModelP
 from .trainer import Optimizer, TrainConfig, TrainReport, Trainer, allreduce_mean, train
 from .evaluate import (TIE_MEAN, TIE_OPTIMISTIC, TIE_PESSIMISTIC, EvalResult, RankRecord,
                        encode_all_entities, evaluate, filtered_candidates, rank_triplet)
+from .io import (PartitionStats, bench_components, load_dataset_dir, load_features, load_triples,
+                 partition_stats, read_candidates, read_dictionary, read_partitions, write_dataset_dir,
+                 write_dictionary, write_partitions, write_results, write_triples)
 
 __version__ = "0.1.0"
