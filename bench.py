@@ -206,30 +206,40 @@ def run_ours(args, world, rank, local):
     kt_ms, kt_n = ctypes.c_double(0), ctypes.c_int64(0)
     lib.kg_kernel_timer_begin(args.roofline_kernel.encode())   # eager launches (graphs off)
     with ClockSampler(local) as clk:
+        # the K timed steps: no host synchronisation inside the loop (the host
+        # runs ahead, as in a training loop), events on the launch stream
         for k in range(args.steps):
             flush.zero_()                      # L2 flush between timed steps (outside the events)
             evs[k][0].record()
             step()
             evs[k][1].record()
-            if tr.use_graphs and tr.last_timer_handle is not None:
-                # the kernel's events were captured into the replayed graph: read this replay's time
-                # (synchronises between steps, outside the step events)
-                ms, n = ctypes.c_double(0), ctypes.c_int64(0)
-                lib.kg_kernel_timer_read(tr.last_timer_handle, ctypes.byref(ms), ctypes.byref(n))
-                kt_ms.value += ms.value
-                kt_n.value += n.value
         torch.cuda.synchronize()
-    e_ms, e_n = ctypes.c_double(0), ctypes.c_int64(0)
-    lib.kg_kernel_timer_end(ctypes.byref(e_ms), ctypes.byref(e_n))
-    kt_ms.value += e_ms.value
-    kt_n.value += e_n.value
     launches = lib.kg_launch_count() - launches0 + tr.graph_kernel_launches - g0
     if tr.dist:
         torch.distributed.barrier()
     step_ms = sum(a.elapsed_time(b) for a, b in evs)
+    # roofline kernel: its events are captured into the replayed graphs; read
+    # them over a few extra steps (each read synchronises, so not in the loop above)
+    for _ in range(min(args.steps, 6)):
+        flush.zero_()
+        step()
+        if tr.use_graphs and tr.last_timer_handle is not None:
+            ms, n = ctypes.c_double(0), ctypes.c_int64(0)
+            lib.kg_kernel_timer_read(tr.last_timer_handle, ctypes.byref(ms), ctypes.byref(n))
+            kt_ms.value += ms.value
+            kt_n.value += n.value
+    torch.cuda.synchronize()
+    e_ms, e_n = ctypes.c_double(0), ctypes.c_int64(0)
+    lib.kg_kernel_timer_end(ctypes.byref(e_ms), ctypes.byref(e_n))
+    kt_ms.value += e_ms.value
+    kt_n.value += e_n.value
     tr.check()
     t_max = torch.tensor([step_ms], dtype=torch.float64, device=dev)
+    rank_ms = [step_ms]
     if tr.dist:
+        every = [torch.zeros_like(t_max) for _ in range(world)]
+        torch.distributed.all_gather(every, t_max)
+        rank_ms = [float(x.item()) for x in every]
         torch.distributed.all_reduce(t_max, op=torch.distributed.ReduceOp.MAX)
     total_ms = float(t_max.item())
     triples_per_step = sum(tr.sizes)          # every partition's batch, all ranks
@@ -310,6 +320,7 @@ def run_ours(args, world, rank, local):
                            "graph": {"entities": graph.num_entities, "relations": graph.num_relations,
                                      "train_triples": graph.num_edges}},
                 "e2e": e2e, "gpu_launches": int(launches), "roofline": roofline, "cpu_baseline": cpu,
+                "rank_ms": [round(x, 3) for x in rank_ms],
                 "step_ms": [round(a.elapsed_time(b), 4) for a, b in evs],
                 "clocks": clk.summary()}
         print(json.dumps(line), flush=True)

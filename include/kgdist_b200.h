@@ -110,6 +110,9 @@ typedef struct kg_layer_params {
 /* Library                                                                 */
 /* ---------------------------------------------------------------------- */
 int kg_abi_version(void);
+/* cudaGraphUpload of an instantiated graph (e.g. torch CUDAGraph
+ * .raw_cuda_graph_exec()), so its first replay does not pay the upload. */
+kg_status kg_graph_upload(void* graph_exec, void* stream);
 int kg_last_error(char* buf, int64_t n); /* host buffer */
 /* Number of kernels this library has launched in the process. */
 int64_t kg_launch_count(void);

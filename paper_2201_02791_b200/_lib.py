@@ -51,6 +51,7 @@ ST = c_int  # kg_status
 # name -> (restype, argtypes)
 _PROTOS = {
     "kg_abi_version": (c_int, []),
+    "kg_graph_upload": (ST, [P, P]),
     "kg_last_error": (c_int, [ctypes.c_char_p, c_int64]),
     "kg_launch_count": (c_int64, []),
     "kg_kernel_timer_begin": (ST, [ctypes.c_char_p]),
@@ -175,6 +176,12 @@ def call(name: str, *args):
 
 def ptr(t) -> int:
     return 0 if t is None else t.data_ptr()
+
+
+def graph_upload(graph) -> None:
+    """Upload a just-instantiated torch CUDAGraph to the device now (the
+    first replay would otherwise pay for it inside the timed loop)."""
+    call("kg_graph_upload", graph.raw_cuda_graph_exec(), stream_handle())
 
 
 def stream_handle() -> int:

@@ -513,6 +513,11 @@ extern "C" {
 
 int kg_abi_version(void) { return KG_ABI_VERSION; }
 
+kg_status kg_graph_upload(void* graph_exec, void* stream) {
+  KG_CUDA(cudaGraphUpload(reinterpret_cast<cudaGraphExec_t>(graph_exec), kg::as_stream(stream)));
+  return KG_OK;
+}
+
 kg_status kg_copy_segments(const kg_copy_seg* segs, int32_t n, const int64_t* round_dev, int64_t round_host,
                            void* stream) {
   KG_REQUIRE(n >= 0 && n <= kg::KG_MAX_SEGS, KG_ERR_VALIDATION, "at most %d segments", kg::KG_MAX_SEGS);

@@ -635,6 +635,7 @@ class EpochSampler:
             g.capture_begin()
             self._body(parity)
             g.capture_end()
+            _lib.graph_upload(g)
         slot["graph"] = g
         slot["stream"] = self.slot_stream(parity)
 

@@ -544,6 +544,7 @@ class Trainer:
             graph.capture_begin(pool=self._graph_pool)
             body()
             graph.capture_end()
+            _lib.graph_upload(graph)
         torch.cuda.current_stream().wait_stream(side)
 
     def _capture_all(self):
