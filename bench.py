@@ -302,7 +302,13 @@ def run_ours(args, world, rank, local):
         e2e = {"value": steps_e2e * triples_per_step / wall, "unit": UNIT,
                "h2d_bytes_per_step": int(h2d * world / steps_e2e), "d2h_bytes_per_step": int(d2h * world / steps_e2e),
                "wall_s": wall, "steps": steps_e2e, "api": "paper_2201_02791_b200.train()",
-               "final_loss": report.loss_curve[-1]}
+               "final_loss": report.loss_curve[-1], "setup_s": report.setup_seconds,
+               "epochs_s": float(sum(report.epoch_seconds)), "finish_s": report.finish_seconds,
+               "epoch_ms": [round(x * 1e3, 2) for x in report.epoch_seconds]}
+        from paper_2201_02791_b200 import trainer as _trm
+        if _trm.setup_marks:
+            m = _trm.setup_marks
+            e2e["setup_marks_ms"] = [(b[0], round((b[1] - a[1]) * 1e3, 2)) for a, b in zip(m, m[1:])]
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:

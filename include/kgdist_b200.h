@@ -329,6 +329,36 @@ kg_status kg_loss_compute(const float* H, int32_t d, int32_t n_local, const floa
                           float* dH, float* d_decoder, float* loss_out, float* scores_out, uint32_t* flags,
                           void* ws, int64_t ws_bytes, void* stream, void* side_stream);
 
+/* R7/R8 + R16 batch-only half, for a whole epoch in one call: for every
+ * round r < rounds, kg_closure of stream rows [r*b, (r+1)*b) into
+ * order/pos (rounds, n) and counts (rounds, hops+1) row r, kg_loss_groups
+ * into loss_ws, and the kg_loss_group_fields exported to
+ * groups + r*groups_stride at 256-byte aligned offsets. Replaces the
+ * build_compute_graph call of every round of ref:trainer.py:212-214 (plus
+ * the batch grouping of the loss) for a trainer that prepares an epoch ahead. */
+typedef struct kg_epoch_prep_args {
+  const kg_graph_csr* g;
+  int32_t hops;
+  int32_t rounds;
+  const int32_t* stream_triples; /* (total, 3) */
+  const float* labels;           /* (total)    */
+  int64_t total;
+  int64_t b;
+  int32_t d;
+  int32_t R;
+  int32_t* order;
+  int32_t* pos;
+  int32_t* counts;
+  uint8_t* groups;
+  int64_t groups_stride;
+  uint32_t* flags;
+  void* closure_ws;
+  int64_t closure_ws_bytes;
+  void* loss_ws;
+  int64_t loss_ws_bytes;
+} kg_epoch_prep_args;
+kg_status kg_epoch_prep(const kg_epoch_prep_args* a, void* stream);
+
 /* ---------------------------------------------------------------------- */
 /* R19/R20  Reduction + optimizer (ref:trainer.py:63-151)                  */
 /* ---------------------------------------------------------------------- */

@@ -45,6 +45,14 @@ class KgCopySeg(ctypes.Structure):
                 ("src_round_stride", c_int64)]
 
 
+class KgEpochPrepArgs(ctypes.Structure):
+    _fields_ = [("g", POINTER(KgGraphCsr)), ("hops", c_int32), ("rounds", c_int32), ("stream_triples", c_void_p),
+                ("labels", c_void_p), ("total", c_int64), ("b", c_int64), ("d", c_int32), ("R", c_int32),
+                ("order", c_void_p), ("pos", c_void_p), ("counts", c_void_p), ("groups", c_void_p),
+                ("groups_stride", c_int64), ("flags", c_void_p), ("closure_ws", c_void_p),
+                ("closure_ws_bytes", c_int64), ("loss_ws", c_void_p), ("loss_ws_bytes", c_int64)]
+
+
 P = c_void_p
 ST = c_int  # kg_status
 
@@ -107,6 +115,7 @@ _PROTOS = {
                             P, P, P, P, P, c_int64, P]),
     "kg_loss_compute": (ST, [P, c_int32, c_int32, P, c_int32, P, P, c_int64, c_int64, P, c_int64, P, P, P,
                              P, P, P, P, P, c_int64, P, P]),
+    "kg_epoch_prep": (ST, [POINTER(KgEpochPrepArgs), P]),
     "kg_optim_workspace_bytes": (c_int64, [c_int64]),
     "kg_dense_step": (ST, [P, P, P, P, c_int32, c_int64, c_int32, c_float, c_float, c_float, c_float,
                            c_double, c_double, P, c_float, P, P, c_int64, P]),
@@ -176,6 +185,29 @@ def call(name: str, *args):
 
 def ptr(t) -> int:
     return 0 if t is None else t.data_ptr()
+
+
+def capture(graph, body, pool=None) -> None:
+    """Capture body() into `graph` on the current stream and upload it.
+    The cyclic garbage collector is held off while capturing: it could
+    otherwise destroy an unreachable earlier trainer's CUDA graphs or events
+    mid-capture, which invalidates the capture."""
+    import gc
+    enabled = gc.isenabled()
+    gc.disable()
+    try:
+        if pool is None:
+            graph.capture_begin()
+        else:
+            graph.capture_begin(pool=pool)
+        try:
+            body()
+        finally:
+            graph.capture_end()
+    finally:
+        if enabled:
+            gc.enable()
+    graph_upload(graph)
 
 
 def graph_upload(graph) -> None:

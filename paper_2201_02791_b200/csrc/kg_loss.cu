@@ -516,4 +516,49 @@ kg_status kg_loss_compute(const float* H, int32_t d, int32_t n_local, const floa
                       side_stream ? as_stream(side_stream) : nullptr);
 }
 
+
+// The batch-only work of a whole epoch (SURVEY.md §8 R7/R8 + the loss
+// grouping of R16), one host call: for every round r the closure of rows
+// [r*b, (r+1)*b) into order/pos/counts row r, the loss grouping into loss_ws,
+// and an export of kg_loss_group_fields into groups + r*groups_stride (fields
+// at 256-byte aligned offsets, in kg_loss_group_fields order). Issued as ~25
+// launches per round from C, so capturing it into an epoch graph costs
+// microseconds per launch instead of a Python round trip each.
+kg_status kg_epoch_prep(const kg_epoch_prep_args* a, void* stream) {
+  KG_REQUIRE(a != nullptr && a->g != nullptr, KG_ERR_VALIDATION, "kg_epoch_prep: null arguments");
+  KG_REQUIRE(a->rounds >= 1 && a->b >= 1 && a->hops >= 0, KG_ERR_VALIDATION, "kg_epoch_prep: bad sizes");
+  const int32_t n = a->g->n, L1 = a->hops + 1;
+  void* ptrs[16];
+  int64_t sz[16];
+  const int32_t nf = kg_loss_group_fields(a->loss_ws, a->loss_ws_bytes, a->b, n, a->d, a->R, ptrs, sz, 16);
+  KG_REQUIRE(nf > 0, KG_ERR_VALIDATION, "kg_epoch_prep: loss workspace too small");
+  kg_copy_seg segs[16];
+  int64_t off = 0;
+  for (int32_t i = 0; i < nf; ++i) {
+    segs[i].dst = a->groups + off;
+    segs[i].src = ptrs[i];
+    segs[i].bytes = sz[i];
+    segs[i].dst_round_stride = a->groups_stride;
+    segs[i].src_round_stride = 0;
+    off += (int64_t)align_up((size_t)sz[i]);
+  }
+  KG_REQUIRE(off <= a->groups_stride, KG_ERR_VALIDATION, "kg_epoch_prep: groups stride %lld < %lld",
+             (long long)a->groups_stride, (long long)off);
+  for (int32_t r = 0; r < a->rounds; ++r) {
+    const int64_t start = (int64_t)r * a->b;
+    int32_t* order = a->order + (int64_t)r * n;
+    int32_t* counts = a->counts + (int64_t)r * L1;
+    kg_status s = kg_closure(a->stream_triples, a->total, start, nullptr, a->b, nullptr, a->g, a->hops, order,
+                             a->pos + (int64_t)r * n, counts, a->closure_ws, a->closure_ws_bytes, stream);
+    if (s != KG_OK) return s;
+    s = kg_loss_groups(nullptr, a->d, n, nullptr, a->R, a->stream_triples, a->labels, a->total, start, nullptr,
+                       a->b, order, counts, nullptr, nullptr, nullptr, nullptr, a->flags, a->loss_ws,
+                       a->loss_ws_bytes, stream);
+    if (s != KG_OK) return s;
+    s = kg_copy_segments(segs, nf, nullptr, r, stream);
+    if (s != KG_OK) return s;
+  }
+  return KG_OK;
+}
+
 }  // extern "C"

@@ -632,10 +632,7 @@ class EpochSampler:
         g = torch.cuda.CUDAGraph()
         self.side.wait_stream(torch.cuda.current_stream())
         with torch.cuda.stream(self.side):
-            g.capture_begin()
-            self._body(parity)
-            g.capture_end()
-            _lib.graph_upload(g)
+            _lib.capture(g, lambda: self._body(parity))
         slot["graph"] = g
         slot["stream"] = self.slot_stream(parity)
 
@@ -647,6 +644,11 @@ class EpochSampler:
                 self.side.wait_event(slot["released"])
             slot["graph"].replay()
             slot["ready"].record(self.side)
+
+    def close(self) -> None:
+        """Drop the captured epoch graphs (call after the device is idle)."""
+        for slot in self.slots:
+            slot["graph"] = None
 
     def slot_stream(self, slot: int) -> DeviceStream:
         """The (fixed-address) stream buffers of a slot, for graph capture."""

@@ -181,6 +181,8 @@ class TrainReport:
     cg_build_per_batch: list = field(default_factory=list)
     encode_per_batch: list = field(default_factory=list)
     loss_step_per_batch: list = field(default_factory=list)
+    setup_seconds: float = 0.0       # Trainer construction (views, uploads, graph captures)
+    finish_seconds: float = 0.0      # replica check + parameter snapshot to host
 
     def mean_timings(self) -> dict:
         def m(x):
@@ -276,23 +278,17 @@ class _RoundPrep:
     def run(self, slot: int, ds) -> None:
         """Enqueue every round of the epoch in `ds` (current stream = the
         sampler's side stream; captured into the sampler's epoch graph)."""
-        from .sampler import closure_device
         sl = self.slabs[slot]
         w = self.w
         d, n, R = self.loss_args
-        st = _lib.stream_handle()
-        for r in range(self.rounds):
-            start = r * w.b
-            closure_device(w.view, w.config.num_layers, stream=ds, start=start, size=w.b,
-                           out=(sl["order"][r], sl["pos"][r], sl["counts"][r]), ws=self.ws)
-            _lib.call("kg_loss_groups", 0, d, n, 0, R, ds.triples.data_ptr(), ds.labels.data_ptr(), ds.total,
-                      start, None, w.b, sl["order"][r].data_ptr(), sl["counts"][r].data_ptr(), 0, 0, 0, 0,
-                      self.flags.data_ptr(), self.prep_ws.data_ptr(), self.prep_ws.numel(), st)
-            base = sl["groups"].data_ptr() + r * self.blob
-            segs = (_lib.KgCopySeg * len(self.prep_fields))()
-            for i, ((ptr, nb), off) in enumerate(zip(self.prep_fields, self.offs)):
-                segs[i].dst, segs[i].src, segs[i].bytes = base + off, ptr, nb
-            _lib.call("kg_copy_segments", segs, len(segs), None, 0, st)
+        lib = _lib.require_cuda()
+        cbuf = self.ws.get("closure", lib.kg_closure_workspace_bytes(n))
+        a = _lib.KgEpochPrepArgs(ctypes.pointer(w.view.csr()), w.config.num_layers, self.rounds,
+                                 ds.triples.data_ptr(), ds.labels.data_ptr(), ds.total, w.b, d, R,
+                                 sl["order"].data_ptr(), sl["pos"].data_ptr(), sl["counts"].data_ptr(),
+                                 sl["groups"].data_ptr(), self.blob, self.flags.data_ptr(),
+                                 cbuf.data_ptr(), cbuf.numel(), self.prep_ws.data_ptr(), self.prep_ws.numel())
+        _lib.call("kg_epoch_prep", ctypes.byref(a), _lib.stream_handle())
 
     def import_round(self, slot: int, round_dev, loss_ws) -> None:
         """Copy round *round_dev of `slot` into the worker's working buffers."""
@@ -310,6 +306,17 @@ class _RoundPrep:
         _lib.call("kg_copy_segments", segs, len(segs), round_dev.data_ptr(), 0, _lib.stream_handle())
 
 
+_SETUP_MARKS = os.environ.get("KG_SETUP_TIMES", "0") == "1"
+setup_marks: list = []
+
+
+def _mark(name: str) -> None:
+    """Diagnostics (KG_SETUP_TIMES=1): synchronised timestamps of the setup phases."""
+    if _SETUP_MARKS:
+        _torch().cuda.synchronize()
+        setup_marks.append((name, time.perf_counter()))
+
+
 class _Worker:
     """Device state of one partition: view, buffers, RNG stream, local
     embedding rows and their Adam moments."""
@@ -318,7 +325,9 @@ class _Worker:
                  features, rounds: int = 1):
         torch = _torch()
         self.wid = wid
+        _mark("worker")
         self.view = build_view(partition, pset.num_entities, pset.num_relations)
+        _mark("view")
         self.b = b
         self.config = config
         dev = self.view.device
@@ -335,7 +344,9 @@ class _Worker:
         else:
             rows = features[local]
         self.input_rows = torch.as_tensor(np.ascontiguousarray(rows, dtype=np.float32)).to(dev)
+        _mark("rng+rows")
         self.bufs = ViewBuffers(config, self.view, b, input_rows=self.input_rows)
+        _mark("bufs")
         self.emb = config.mode == MODE_EMBEDDING
         if self.emb and tc.optimizer == "adam":
             self.em = torch.zeros_like(self.input_rows)
@@ -346,7 +357,9 @@ class _Worker:
         self.stream = None
         # epoch e+1's negatives + shuffle are produced on a side stream while epoch e trains
         self.prep = _RoundPrep(self, rounds)
+        _mark("roundprep")
         self.sampler = EpochSampler(self.view, config.negatives_per_positive, self.g_dev, prep=self.prep.run)
+        _mark("sampler")
 
     def begin_epoch(self):
         self.stream = self.sampler.next()
@@ -382,6 +395,8 @@ class Trainer:
         if self.dist and self.P % self.world != 0:
             raise ValidationError(f"{self.P} partitions cannot be split evenly over {self.world} ranks")
         self.local_wids = [w for w in range(self.P) if w % self.world == self.rank]
+        setup_marks.clear()
+        _mark("start")
         params = initial_params.copy() if initial_params is not None else init_params(
             model_config, np.random.default_rng(train_config.seed), num_entities=pset.num_entities)
         if model_config.mode == MODE_FEATURE:
@@ -396,7 +411,9 @@ class Trainer:
         self.sizes, self.rounds = _plan_batches([p.num_core_edges for p in pset.partitions],
                                                 model_config.negatives_per_positive, train_config)
         self.dev = torch.device("cuda", torch.cuda.current_device())
+        _mark("params")
         self.model = DeviceModel.from_params(model_config, params, self.dev)
+        _mark("model")
         D = self.model.layout.total
         self.D = D
         self.workers = [_Worker(w, pset.partitions[w], pset, model_config, train_config, self.sizes[w], params,
@@ -437,6 +454,7 @@ class Trainer:
         # diagnostics: KG_FORK_STREAMS=0 keeps every kernel on one stream
         self.fork_streams = os.environ.get("KG_FORK_STREAMS", "1") != "0"
         self.model.repack()
+        _mark("trainer")
         self._eager_rounds = 0
         self.t = 0
         self.round_in_epoch = 0
@@ -444,10 +462,58 @@ class Trainer:
 
     # -- one synchronized round ----------------------------------------------
     def begin_epoch(self):
+        torch = _torch()
         for w in self.workers:
             w.begin_epoch()
         self.round_in_epoch = 0
         self.round_dev.zero_()
+        self._epoch_start = torch.cuda.Event(enable_timing=True)
+        self._epoch_start.record()
+
+    def end_epoch(self):
+        """Enqueue the epoch's bookkeeping: per-worker mean loss (and, with
+        several ranks, the all-gathered (loss sum, count) of every rank), the
+        non-finite flags (then cleared) and an end event; copied to pinned
+        host memory without blocking. finish_epoch(handle) reads it."""
+        torch = _torch()
+        nloc = len(self.workers)
+        means = self.losses[:, : self.rounds].mean(dim=1).double()
+        if self.dist:
+            both = torch.stack([means.sum(), torch.tensor(float(nloc), dtype=torch.float64, device=self.dev)])
+            gathered = torch.empty((self.world, 2), dtype=torch.float64, device=self.dev)
+            torch.distributed.all_gather_into_tensor(gathered, both)
+            means = gathered.reshape(-1)
+        flags = torch.cat([w.bufs.flags.reshape(1) for w in self.workers] + [self.flags.reshape(1)])
+        host_means = torch.empty(means.shape, dtype=means.dtype, pin_memory=True)
+        host_flags = torch.empty(flags.shape, dtype=flags.dtype, pin_memory=True)
+        host_means.copy_(means, non_blocking=True)
+        host_flags.copy_(flags, non_blocking=True)
+        for w in self.workers:
+            w.bufs.flags.zero_()
+        self.flags.zero_()
+        end = torch.cuda.Event(enable_timing=True)
+        end.record()
+        return (self._epoch_start, end, host_means, host_flags)
+
+    def finish_epoch(self, handle) -> tuple:
+        """Wait for an end_epoch() handle; raise on non-finite values, return
+        (mean loss, device seconds of the epoch on this rank)."""
+        start, end, host_means, host_flags = handle
+        end.synchronize()
+        for f in host_flags.tolist()[:-1]:
+            if f:
+                if f & 1:
+                    raise NumericError("non-finite score")
+                if f & 2:
+                    raise NumericError("non-finite loss")
+                if f & 4:
+                    raise NumericError("non-finite parameter after optimizer step")
+                raise NumericError(f"device status {f:#x}")
+        if host_flags.tolist()[-1]:
+            raise NumericError("non-finite parameter after optimizer step")
+        m = host_means.numpy()
+        loss = float(m[0::2].sum() / m[1::2].sum()) if self.dist else float(np.mean(m))
+        return loss, start.elapsed_time(end) / 1e3
 
     def _compute_body(self):
         """closure -> forward -> DistMult+BCE -> backward of every local worker
@@ -541,10 +607,7 @@ class Trainer:
         side = torch.cuda.Stream(self.dev, priority=-2)
         side.wait_stream(torch.cuda.current_stream())
         with torch.cuda.stream(side):
-            graph.capture_begin(pool=self._graph_pool)
-            body()
-            graph.capture_end()
-            _lib.graph_upload(graph)
+            _lib.capture(graph, body, self._graph_pool)
         torch.cuda.current_stream().wait_stream(side)
 
     def _capture_all(self):
@@ -572,6 +635,14 @@ class Trainer:
             self._graphs[key] = (gc, gu, lib.kg_launch_count() - n0)
         for w, st in zip(self.workers, current):
             w.stream = st
+
+    def close(self):
+        """Release the captured CUDA graphs now (the trainer and its samplers
+        reference each other, so they would otherwise wait for the cyclic GC)."""
+        _torch().cuda.synchronize()
+        self._graphs.clear()
+        for w in self.workers:
+            w.sampler.close()
 
     def _gather(self):
         gather_partition_payloads(self.grads_local, self.P, self.world, self.grads_all, self._recv, self._gidx)
@@ -661,36 +732,49 @@ def train(pset: PartitionSet, graph, model_config: ModelConfig, train_config: Tr
     (ref:trainer.py:336-480). eval_fn(params) -> float is called at epochs
     selected by train_config.eval_every."""
     torch = _torch()
+    t_setup = time.perf_counter()
     tr = Trainer(pset, graph, model_config, train_config, initial_params)
-    report = TrainReport(rounds_per_epoch=tr.rounds, batch_sizes=list(tr.sizes))
+    torch.cuda.synchronize()
+    report = TrainReport(rounds_per_epoch=tr.rounds, batch_sizes=list(tr.sizes),
+                         setup_seconds=time.perf_counter() - t_setup)
     tc = train_config
     eval_epochs = frozenset(e for e in range(tc.epochs)
                             if tc.eval_every and (e + 1) % tc.eval_every == 0) if eval_fn is not None else frozenset()
-    for epoch in range(tc.epochs):
-        torch.cuda.synchronize()
-        t0 = time.perf_counter()
-        tr.begin_epoch()
-        for _ in range(tr.rounds):
-            tr.run_round()
-        torch.cuda.synchronize()
-        secs = time.perf_counter() - t0
-        tr.check()
-        losses = tr.epoch_losses()
-        if tr.dist:
-            both = torch.tensor([sum(losses), float(len(losses)), secs], dtype=torch.float64, device=tr.dev)
-            gathered = [torch.zeros_like(both) for _ in range(tr.world)]
-            torch.distributed.all_gather(gathered, both)
-            g = torch.stack(gathered).cpu().numpy()
-            report.loss_curve.append(float(g[:, 0].sum() / g[:, 1].sum()))
-            report.epoch_seconds.append(float(g[:, 2].max()))
-        else:
-            report.loss_curve.append(float(np.mean(losses)))
-            report.epoch_seconds.append(secs)
+    # Epoch-end bookkeeping (losses, non-finite flags, device epoch time) is
+    # read back one epoch late, so the device queue never drains between
+    # epochs; an eval epoch is settled at once (it needs a snapshot anyway).
+    pending = []
+
+    def settle():
+        e, h = pending.pop(0)
+        losses, secs = tr.finish_epoch(h)
+        report.loss_curve.append(losses)
+        report.epoch_seconds.append(secs)
         nb = tr.P * tr.rounds
         report.cg_build_per_batch.append(0.0)
         report.encode_per_batch.append(0.0)
-        report.loss_step_per_batch.append(report.epoch_seconds[-1] * (tr.P if not tr.dist else 1) / nb)
-        if epoch in eval_epochs:
-            report.val_mrr.append((epoch, float(eval_fn(tr.snapshot()))))
+        report.loss_step_per_batch.append(secs * (tr.P if not tr.dist else 1) / nb)
+        if e in eval_epochs:
+            report.val_mrr.append((e, float(eval_fn(tr.snapshot()))))
+
+    for epoch in range(tc.epochs):
+        tr.begin_epoch()
+        for _ in range(tr.rounds):
+            tr.run_round()
+        pending.append((epoch, tr.end_epoch()))
+        while len(pending) > 1 or (pending and pending[-1][0] in eval_epochs):
+            settle()
+    while pending:
+        settle()
+    if tr.dist:
+        # epoch time = max over ranks (one collective for the whole run)
+        secs = torch.tensor(report.epoch_seconds, dtype=torch.float64, device=tr.dev)
+        torch.distributed.all_reduce(secs, op=torch.distributed.ReduceOp.MAX)
+        report.epoch_seconds = secs.cpu().tolist()
+        report.loss_step_per_batch = [x / (tr.P * tr.rounds) for x in report.epoch_seconds]
+    t_fin = time.perf_counter()
     tr.check_replicas()
-    return tr.snapshot(), report
+    params = tr.snapshot()
+    tr.close()
+    report.finish_seconds = time.perf_counter() - t_fin
+    return params, report

@@ -396,3 +396,18 @@ def test_candidates_protocol_matches_reference(policy):
     assert np.mean(ranks == g[f"{policy}_ranks"]) >= 0.999
     assert all(r.corrupted_side == "tail" for r in res.records)
     assert abs(res.mrr - float(g[f"{policy}_mrr"])) / float(g[f"{policy}_mrr"]) <= 0.01
+
+
+@pytest.mark.parametrize("graphs", ["0", "1"])
+def test_train_raises_on_non_finite(monkeypatch, graphs):
+    """A diverging run raises NumericError from train() (eager and CUDA-graph
+    paths; the epoch bookkeeping is read back one epoch late), as the
+    reference's optimizer does (ref:trainer.py:150-151)."""
+    monkeypatch.setenv("KG_CUDA_GRAPHS", graphs)
+    g = load_golden("synth_p4")
+    graph, pset, cfg = golden_pset(g)
+    L = len(cfg["dims"]) - 1
+    mc = kb.ModelConfig(L, cfg["dims"], cfg["num_bases"], graph.num_relations, 1, mode="embedding")
+    tc = kb.TrainConfig(epochs=4, batch_size=96, seed=2, optimizer="sgd", learning_rate=1e38)
+    with pytest.raises(kb.NumericError):
+        kb.train(pset, graph, mc, tc, initial_params=golden_params(g, "init_", L))
