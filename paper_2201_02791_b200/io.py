@@ -10,6 +10,8 @@ package load in the other):
   partition dir      meta (key=value + sha256 over the keys), p<i>/
                      core_edges.tsv, support_edges.tsv, vertices.tsv
                      (global id, role, local id)               ref:partition.py:336-482
+                     or (fmt="npy", memory-mapped) core_edges.npy,
+                     support_edges.npy, vertices.npy, roles.npy
   candidates file    `test_index<TAB>c1,c2,...`                 ref:evaluate.py:232-242
   results file       one rank record per line + `# mrr=` / `# hits@k=` ref:evaluate.py:245-253
 """
@@ -247,14 +249,25 @@ def partition_stats(pset: PartitionSet) -> PartitionStats:
 
 _META = ("version", "num_parts", "hops", "seed", "partitioner", "num_entities", "num_relations",
          "graph_checksum")
+_ROLE_CODE = {ROLE_CORE: 0, ROLE_REPLICATED: 1, ROLE_SUPPORT: 2}
+PARTITION_FORMATS = ("tsv", "npy")
 
 
 def _meta_sha(fields: dict) -> str:
     return hashlib.sha256("\n".join(f"{k}={fields[k]}" for k in _META).encode()).hexdigest()
 
 
-def write_partitions(pset: PartitionSet, out_dir: str) -> None:
-    """Partition directory (ref:partition.py:362-384)."""
+def write_partitions(pset: PartitionSet, out_dir: str, fmt: str = "tsv") -> None:
+    """Partition directory (ref:partition.py:362-384).
+
+    fmt="tsv" writes the reference's text layout (readable by either package);
+    fmt="npy" writes per partition core_edges.npy /
+    support_edges.npy (int64 (m,3)) and vertices.npy / roles.npy (global id
+    and role code 0 core / 1 replicated / 2 support, in local-id order), which
+    read_partitions memory-maps instead of parsing. The manifest is the same
+    (its checksum covers the same keys)."""
+    if fmt not in PARTITION_FORMATS:
+        raise FormatError(f"unknown partition format {fmt!r}")
     os.makedirs(out_dir, exist_ok=True)
     fields = dict(version=1, num_parts=pset.num_parts, hops=pset.hops, seed=pset.seed, partitioner=pset.method,
                   num_entities=pset.num_entities, num_relations=pset.num_relations,
@@ -265,43 +278,88 @@ def write_partitions(pset: PartitionSet, out_dir: str) -> None:
     for p in pset.partitions:
         d = os.path.join(out_dir, f"p{p.id}")
         os.makedirs(d, exist_ok=True)
+        local = p.local_vertices()
+        if fmt == "npy":
+            np.save(os.path.join(d, "core_edges.npy"), np.ascontiguousarray(p.core, dtype=np.int64))
+            np.save(os.path.join(d, "support_edges.npy"), np.ascontiguousarray(p.support, dtype=np.int64))
+            roles = np.full(len(local), -1, dtype=np.int8)
+            pos = np.argsort(local, kind="stable")
+            for role, verts in p.vertex_roles().items():
+                roles[pos[np.searchsorted(local[pos], verts)]] = _ROLE_CODE[role]
+            np.save(os.path.join(d, "vertices.npy"), np.ascontiguousarray(local, dtype=np.int64))
+            np.save(os.path.join(d, "roles.npy"), roles)
+            continue
         np.savetxt(os.path.join(d, "core_edges.tsv"), p.core, fmt="%d", delimiter="\t")
         np.savetxt(os.path.join(d, "support_edges.tsv"), p.support, fmt="%d", delimiter="\t")
-        local = {int(g): i for i, g in enumerate(p.local_vertices())}
+        lid = {int(g): i for i, g in enumerate(local)}
         with open(os.path.join(d, "vertices.tsv"), "w", encoding="utf-8") as fh:
             for role, verts in p.vertex_roles().items():
-                fh.writelines(f"{int(g)}\t{role}\t{local[int(g)]}\n" for g in verts)
+                fh.writelines(f"{int(g)}\t{role}\t{lid[int(g)]}\n" for g in verts)
 
 
-def _tsv_triples(path: str) -> np.ndarray:
-    if not os.path.isfile(path):
-        raise FormatError(f"missing partition file {path}")
-    return np.loadtxt(path, dtype=np.int64, delimiter="\t", ndmin=2).reshape(-1, 3)
+class _EdgeIndex:
+    """Graph triples sorted by key (h*R + r)*N + t, built once per read."""
+
+    def __init__(self, graph: KnowledgeGraph):
+        tri = np.asarray(graph.triples, dtype=np.int64).reshape(-1, 3)
+        self.N, self.R = int(graph.num_entities), max(int(graph.num_relations), 1)
+        keys = self.keys(tri)
+        self.order = np.argsort(keys, kind="stable")
+        self.sorted = keys[self.order]
+        # end of each sorted position's run of equal keys
+        n = len(keys)
+        last = np.r_[self.sorted[1:] != self.sorted[:-1], True] if n else np.zeros(0, bool)
+        ends = np.where(last, np.arange(1, n + 1), 0)
+        self.run_end = np.minimum.accumulate(np.where(last, ends, n)[::-1])[::-1] if n else ends
+
+    def keys(self, t: np.ndarray) -> np.ndarray:
+        return (t[:, 0] * self.R + t[:, 1]) * self.N + t[:, 2]
 
 
-def _edge_ids(graph: KnowledgeGraph, triples: np.ndarray, taken: dict) -> np.ndarray:
-    """Graph edge index of every triple; duplicates consume occurrences in order."""
-    occ = taken.get("_occ")
-    if occ is None:
-        occ = {}
-        for eid, key in enumerate(map(tuple, graph.triples.tolist())):
-            occ.setdefault(key, []).append(eid)
-        taken["_occ"] = occ
-    out = np.empty(len(triples), dtype=np.int64)
-    for i, key in enumerate(map(tuple, triples.tolist())):
-        ids, k = occ.get(key), taken.get(key, 0)
-        if not ids:
-            raise ProvenanceError(f"partition edge {key} not found in graph")
-        if k >= len(ids):
+class _EdgeIdResolver:
+    """Graph edge index of partition triples, vectorised: duplicates of a
+    triple consume its graph occurrences in order, across every batch passed
+    to the same resolver (ref:partition.py:398-417 keeps a dict of lists and
+    a per-key use count; here the graph is key-sorted once and use counts
+    live in an array). Raises at the first offending triple, as the
+    reference's loop does."""
+
+    def __init__(self, graph_or_index):
+        self.ix = graph_or_index if isinstance(graph_or_index, _EdgeIndex) else _EdgeIndex(graph_or_index)
+        self.used = np.zeros(len(self.ix.sorted), dtype=np.int64)   # at the first sorted position of a key
+
+    def __call__(self, triples: np.ndarray) -> np.ndarray:
+        ix = self.ix
+        t = np.asarray(triples, dtype=np.int64).reshape(-1, 3)
+        if len(t) == 0:
+            return np.zeros(0, dtype=np.int64)
+        ok = ((t[:, 0] >= 0) & (t[:, 0] < ix.N) & (t[:, 2] >= 0) & (t[:, 2] < ix.N)
+              & (t[:, 1] >= 0) & (t[:, 1] < ix.R))
+        keys = np.where(ok, ix.keys(np.where(ok[:, None], t, 0)), -1)
+        # work in key order: sorted needles make searchsorted cache-friendly
+        srt = np.argsort(keys, kind="stable")
+        ks = keys[srt]
+        lo_s = np.searchsorted(ix.sorted, ks, "left")
+        inb = lo_s < len(ix.sorted)
+        found_s = inb & (ix.sorted[np.where(inb, lo_s, 0)] == ks) & (ks >= 0)
+        cnt_s = np.where(found_s, ix.run_end[np.where(inb, lo_s, 0)] - lo_s, 0)
+        first = np.r_[True, ks[1:] != ks[:-1]]
+        grp_start = np.maximum.accumulate(np.where(first, np.arange(len(ks)), 0))
+        k_s = np.arange(len(ks)) - grp_start + np.where(found_s, self.used[np.where(found_s, lo_s, 0)], 0)
+        lo, found, cnt, k = (np.empty_like(a) for a in (lo_s, found_s, cnt_s, k_s))
+        lo[srt], found[srt], cnt[srt], k[srt] = lo_s, found_s, cnt_s, k_s
+        bad = ~found | (k >= cnt)
+        if bad.any():
+            i = int(np.argmax(bad))
+            key = tuple(int(x) for x in t[i])
+            if not found[i]:
+                raise ProvenanceError(f"partition edge {key} not found in graph")
             raise ProvenanceError(f"partition edge {key} occurs more often than in the graph")
-        out[i] = ids[k]
-        taken[key] = k + 1
-    return out
+        np.add.at(self.used, lo, 1)
+        return ix.order[lo + k]
 
 
-def read_partitions(in_dir: str, graph: Optional[KnowledgeGraph] = None) -> PartitionSet:
-    """Load a partition directory; with `graph`, check provenance and map
-    every edge back to its graph index (ref:partition.py:420-482)."""
+def _read_manifest(in_dir: str) -> dict:
     meta = os.path.join(in_dir, "meta")
     if not os.path.isfile(meta):
         raise FormatError(f"missing manifest {meta}")
@@ -320,35 +378,71 @@ def read_partitions(in_dir: str, graph: Optional[KnowledgeGraph] = None) -> Part
         raise FormatError(f"manifest missing key {missing[0]!r}")
     if _meta_sha(fields) != fields["meta_checksum"]:
         raise ProvenanceError("manifest checksum mismatch (tampered or corrupt meta file)")
+    return fields
+
+
+def _need(path: str) -> str:
+    if not os.path.isfile(path):
+        raise FormatError(f"missing partition file {path}")
+    return path
+
+
+def _part_tsv(d: str) -> tuple:
+    """(core, support, local ids, role per local id) of a text partition."""
+    def triples(name):
+        return np.loadtxt(_need(os.path.join(d, name)), dtype=np.int64, delimiter="\t", ndmin=2).reshape(-1, 3)
+    core, support = triples("core_edges.tsv"), triples("support_edges.tsv")
+    rows = []
+    with open(_need(os.path.join(d, "vertices.tsv")), "r", encoding="utf-8") as fh:
+        for raw in fh:
+            g, role, li = raw.strip().split("\t")
+            if role not in _ROLE_CODE:
+                raise FormatError(f"unknown vertex role {role!r}")
+            rows.append((int(li), int(g), _ROLE_CODE[role]))
+    rows.sort()
+    local = np.asarray([g for _, g, _ in rows], dtype=np.int64)
+    roles = np.asarray([c for _, _, c in rows], dtype=np.int8)
+    return core, support, local, roles
+
+
+def _part_npy(d: str) -> tuple:
+    """Memory-mapped (no parse, no copy) binary partition."""
+    def arr(name, dtype, ndim):
+        a = np.load(_need(os.path.join(d, name)), mmap_mode="r", allow_pickle=False)
+        if a.dtype != dtype or a.ndim != ndim or (ndim == 2 and a.shape[1] != 3):
+            raise FormatError(f"{os.path.join(d, name)}: expected {np.dtype(dtype).name} with {ndim} dims")
+        return a
+    core, support = arr("core_edges.npy", np.int64, 2), arr("support_edges.npy", np.int64, 2)
+    local, roles = arr("vertices.npy", np.int64, 1), arr("roles.npy", np.int8, 1)
+    if len(local) != len(roles):
+        raise FormatError(f"{d}: vertices.npy and roles.npy differ in length")
+    if len(roles) and (roles.min() < 0 or roles.max() > 2):
+        raise FormatError(f"{d}: unknown vertex role code")
+    return core, support, local, roles
+
+
+def read_partitions(in_dir: str, graph: Optional[KnowledgeGraph] = None) -> PartitionSet:
+    """Load a partition directory (text or binary layout, detected per
+    partition); with `graph`, check provenance and map every edge back to its
+    graph index (ref:partition.py:420-482)."""
+    fields = _read_manifest(in_dir)
     if graph is not None and graph.checksum() != fields["graph_checksum"]:
         raise ProvenanceError("partition directory was built from a different graph")
     hops = int(fields["hops"])
-    core_taken: dict = {}
+    index = _EdgeIndex(graph) if graph is not None else None
+    core_ids = _EdgeIdResolver(index) if graph is not None else None
     parts = []
     for pid in range(int(fields["num_parts"])):
         d = os.path.join(in_dir, f"p{pid}")
-        core, support = _tsv_triples(os.path.join(d, "core_edges.tsv")), _tsv_triples(os.path.join(d, "support_edges.tsv"))
-        vfile = os.path.join(d, "vertices.tsv")
-        if not os.path.isfile(vfile):
-            raise FormatError(f"missing partition file {vfile}")
-        roles = {ROLE_CORE: [], ROLE_REPLICATED: [], ROLE_SUPPORT: []}
-        loc = []
-        with open(vfile, "r", encoding="utf-8") as fh:
-            for raw in fh:
-                g, role, li = raw.strip().split("\t")
-                if role not in roles:
-                    raise FormatError(f"unknown vertex role {role!r}")
-                roles[role].append(int(g))
-                loc.append((int(li), int(g)))
-        part = Partition(id=pid, core=core, support=support,
-                         core_vertices=np.sort(np.asarray(roles[ROLE_CORE], dtype=np.int64)),
-                         replicated_vertices=np.sort(np.asarray(roles[ROLE_REPLICATED], dtype=np.int64)),
-                         support_vertices=np.sort(np.asarray(roles[ROLE_SUPPORT], dtype=np.int64)),
-                         hop_count=hops)
-        part._local = np.asarray([g for _, g in sorted(loc)], dtype=np.int64)
+        binary = os.path.isfile(os.path.join(d, "core_edges.npy"))
+        core, support, local, roles = _part_npy(d) if binary else _part_tsv(d)
+        by_role = [np.sort(np.asarray(local[roles == c], dtype=np.int64)) for c in range(3)]
+        part = Partition(id=pid, core=core, support=support, core_vertices=by_role[0],
+                         replicated_vertices=by_role[1], support_vertices=by_role[2], hop_count=hops)
+        part._local = np.asarray(local, dtype=np.int64)
         if graph is not None:
-            part.core_edge_ids = _edge_ids(graph, core, core_taken)
-            part.support_edge_ids = _edge_ids(graph, support, {})
+            part.core_edge_ids = core_ids(core)
+            part.support_edge_ids = _EdgeIdResolver(index)(support)
         parts.append(part)
     return PartitionSet(parts, int(fields["num_entities"]), int(fields["num_relations"]), hops,
                         int(fields["seed"]), fields["partitioner"], fields["graph_checksum"])

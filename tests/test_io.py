@@ -53,11 +53,13 @@ def test_features(tmp_path):
         kb.load_features(str(f), g)
 
 
-def test_partition_directory_round_trip(tmp_path):
+@pytest.mark.parametrize("fmt", ["tsv", "npy"])
+def test_partition_directory_round_trip(tmp_path, fmt):
     graph, split = kb.generate_synthetic(400, 5, 6.0, seed=1)
     pset = kb.neighborhood_expand(kb.vertex_cut_partition(graph, 3, seed=0), graph, 2)
     d = tmp_path / "parts"
-    kb.write_partitions(pset, str(d))
+    kb.write_partitions(pset, str(d), fmt=fmt)
+    assert os.path.isfile(d / "p0" / ("core_edges." + fmt))
     back = kb.read_partitions(str(d), graph)
     assert (back.num_parts, back.hops, back.method, back.seed) == (3, 2, pset.method, pset.seed)
     for a, b in zip(pset.partitions, back.partitions):
@@ -65,6 +67,9 @@ def test_partition_directory_round_trip(tmp_path):
         np.testing.assert_array_equal(a.support, b.support)
         np.testing.assert_array_equal(a.local_vertices(), b.local_vertices())
         np.testing.assert_array_equal(a.core_edge_ids, b.core_edge_ids)
+        np.testing.assert_array_equal(a.support_edge_ids, b.support_edge_ids)
+        for r in ("core_vertices", "replicated_vertices", "support_vertices"):
+            np.testing.assert_array_equal(getattr(a, r), getattr(b, r))
     st = kb.partition_stats(back)
     assert st.core_edges == [p.num_core_edges for p in pset.partitions]
     assert abs(st.rf - kb.replication_factor(pset)) < 1e-12 and "RF =" in st.format()
@@ -86,3 +91,67 @@ def test_candidates_and_results_files(tmp_path):
     kb.write_results(res, str(out))
     lines = out.read_text().splitlines()
     assert lines[0] == "0\t1\t2\ttail\t2.0" and lines[2] == "# mrr=0.500000" and lines[-1] == "# hits@10=1.000000"
+
+
+def _loop_resolve(graph, triples, used):
+    """The reference's per-triple resolution (ref:partition.py:398-417)."""
+    idx = {}
+    for eid, key in enumerate(map(tuple, graph.triples.tolist())):
+        idx.setdefault(key, []).append(eid)
+    out = []
+    for key in map(tuple, triples.tolist()):
+        ids, k = idx.get(key), used.get(key, 0)
+        if not ids:
+            raise ProvenanceError("not found")
+        if k >= len(ids):
+            raise ProvenanceError("occurs more often")
+        out.append(ids[k])
+        used[key] = k + 1
+    return np.asarray(out, dtype=np.int64)
+
+
+def test_edge_id_resolution_with_duplicates_matches_loop():
+    from paper_2201_02791_b200.io import _EdgeIdResolver
+    rng = np.random.default_rng(3)
+    base = np.stack([rng.integers(0, 30, 200), rng.integers(0, 4, 200), rng.integers(0, 30, 200)], 1)
+    tri = np.concatenate([base, base[rng.integers(0, 200, 150)], base[:20]])   # duplicates, some x3
+    graph = kb.KnowledgeGraph(30, 4, tri)
+    res, used = _EdgeIdResolver(graph), {}
+    perm = rng.permutation(len(tri))
+    for chunk in np.array_split(tri[perm], 4):          # batches share the use counts
+        np.testing.assert_array_equal(res(chunk), _loop_resolve(graph, chunk, used))
+    with pytest.raises(ProvenanceError, match="occurs more often"):
+        res(tri[:1])                                    # every occurrence is used up
+    with pytest.raises(ProvenanceError, match="not found"):
+        _EdgeIdResolver(graph)(np.array([[0, 0, 0], [29, 3, 99]]))   # out-of-range tail
+    fresh = _EdgeIdResolver(graph)
+    missing = np.array([[a, b, c] for a in range(30) for b in range(4) for c in range(30)
+                        if not ((tri == [a, b, c]).all(1)).any()][:1])
+    with pytest.raises(ProvenanceError, match="not found"):
+        fresh(np.concatenate([tri[:5], missing]))
+
+
+def test_reference_reads_our_tsv_directory_and_we_read_theirs(tmp_path):
+    """Interoperability with the reference's own reader/writer (this
+    container only: /root/reference is absent on the GPU box)."""
+    src = "/root/reference/pkg/src"
+    if not os.path.isdir(src):
+        pytest.skip("reference package not available")
+    import sys
+    sys.path.insert(0, src)
+    try:
+        import kgdist as kg
+    finally:
+        sys.path.remove(src)
+    graph, split = kb.generate_synthetic(300, 4, 5.0, seed=2)
+    pset = kb.neighborhood_expand(kb.vertex_cut_partition(graph, 2, seed=0), graph, 2)
+    kb.write_partitions(pset, str(tmp_path / "ours"))
+    rgraph = kg.KnowledgeGraph(graph.num_entities, graph.num_relations, graph.triples)
+    theirs = kg.read_partitions(str(tmp_path / "ours"), rgraph)
+    kg.write_partitions(theirs, str(tmp_path / "theirs"))
+    back = kb.read_partitions(str(tmp_path / "theirs"), graph)
+    for a, b, c in zip(pset.partitions, theirs.partitions, back.partitions):
+        np.testing.assert_array_equal(a.core_edge_ids, b.core_edge_ids)
+        np.testing.assert_array_equal(b.core_edge_ids, c.core_edge_ids)
+        np.testing.assert_array_equal(b.support_edge_ids, c.support_edge_ids)
+        np.testing.assert_array_equal(a.local_vertices(), c.local_vertices())
