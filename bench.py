@@ -268,7 +268,9 @@ def run_ours(args, world, rank, local):
                 "unit": "GB/s", "frac": (achieved / peak) if achieved else None,
                 "traffic": traffic, "traffic_source": traffic_src, "alg_bytes_per_launch": per_launch_alg,
                 "avg_launch_ms": avg_launch_ms, "launches_timed": kt_n.value,
-                "kernel_share_of_step": (kt_ms.value / (step_ms)) if step_ms > 0 else None,
+                # launches per step (one per layer) x average launch / average step
+                "kernel_share_of_step": (avg_launch_ms * max(tr.mc.num_layers, 1) / (step_ms / args.steps))
+                if step_ms > 0 else None,
                 "note": "FB15k-237 working set is L2-resident (H7): effective bandwidth vs HBM peak"}
 
     # e2e through the public API (host inputs -> train() -> host params)

@@ -142,10 +142,11 @@ def load():
     global _lib
     if _lib is not None:
         return _lib
-    if not os.path.isfile(LIB_PATH):
-        raise DeviceError(f"kernel library not built: {LIB_PATH} (run `make` or "
+    path = os.environ.get("KG_LIB") or LIB_PATH     # KG_LIB: diagnostics (an A/B build variant)
+    if not os.path.isfile(path):
+        raise DeviceError(f"kernel library not built: {path} (run `make` or "
                           f"__graft_entry__.build())")
-    lib = ctypes.CDLL(LIB_PATH)
+    lib = ctypes.CDLL(path)
     for name, (res, args) in _PROTOS.items():
         fn = getattr(lib, name)
         fn.restype = res

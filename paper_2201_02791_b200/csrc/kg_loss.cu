@@ -33,41 +33,80 @@ struct LossArgs {
 };
 
 __device__ __forceinline__ int64_t row_of(const LossArgs& a, int64_t i) {
-  return ((a.start_dev ? __ldg(a.start_dev) : a.start) + i) % a.total;
+  // the batch offset is < total, so only wrapped rows pay for the 64-bit modulo
+  int64_t r = (a.start_dev ? __ldg(a.start_dev) : a.start) + i;
+  if (r >= a.total) r %= a.total;
+  return r;
 }
+
+// SU triples per warp iteration: their row loads are all in flight together,
+// and lane u finishes triple u (softplus, sigmoid) so the epilogues overlap.
+constexpr int SU = 4;
 
 template <bool V4>
 __global__ void __launch_bounds__(256) k_score(LossArgs a) {
   const int lane = lane_id();
   const int warps = (gridDim.x * blockDim.x) >> 5;
-  for (int64_t i = warp_uniform((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5); i < a.b; i += warps) {
-    int64_t row = row_of(a, i);
-    int32_t h = a.tri[row * 3], r = a.tri[row * 3 + 1], t = a.tri[row * 3 + 2];
-    const float* Hh = a.H + (int64_t)h * a.d;
-    const float* Ht = a.H + (int64_t)t * a.d;
-    const float* M = a.dec + (int64_t)r * a.d;
-    float s = 0.f;
+  for (int64_t i0 = warp_uniform(((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5) * SU); i0 < a.b;
+       i0 += (int64_t)warps * SU) {
+    float s[SU];
+    int64_t rows[SU];
+#pragma unroll
+    for (int u = 0; u < SU; ++u) {
+      s[u] = 0.f;
+      rows[u] = i0 + u < a.b ? row_of(a, i0 + u) : -1;
+    }
     if (V4) {
       for (int k = 4 * lane; k < a.d; k += 128) {
-        float x[4], m[4], y[4];
-        VecIO<4>::load(Hh + k, x);
-        VecIO<4>::load(M + k, m);
-        VecIO<4>::load(Ht + k, y);
+        float x[SU][4], m[SU][4], y[SU][4];
 #pragma unroll
-        for (int c = 0; c < 4; ++c) s = fmaf(x[c] * m[c], y[c], s);
+        for (int u = 0; u < SU; ++u) {
+          if (rows[u] >= 0) {
+            const int32_t* tr = a.tri + rows[u] * 3;
+            VecIO<4>::load(a.H + (int64_t)__ldg(tr) * a.d + k, x[u]);
+            VecIO<4>::load(a.dec + (int64_t)__ldg(tr + 1) * a.d + k, m[u]);
+            VecIO<4>::load(a.H + (int64_t)__ldg(tr + 2) * a.d + k, y[u]);
+          } else {
+#pragma unroll
+            for (int c = 0; c < 4; ++c) x[u][c] = m[u][c] = y[u][c] = 0.f;
+          }
+        }
+#pragma unroll
+        for (int u = 0; u < SU; ++u)
+#pragma unroll
+          for (int c = 0; c < 4; ++c) s[u] = fmaf(x[u][c] * m[u][c], y[u][c], s[u]);
       }
     } else {
-      for (int k = lane; k < a.d; k += 32) s = fmaf(Hh[k] * M[k], Ht[k], s);
+#pragma unroll
+      for (int u = 0; u < SU; ++u) {
+        if (rows[u] < 0) continue;
+        const int32_t* tr = a.tri + rows[u] * 3;
+        const float* Hh = a.H + (int64_t)__ldg(tr) * a.d;
+        const float* M = a.dec + (int64_t)__ldg(tr + 1) * a.d;
+        const float* Ht = a.H + (int64_t)__ldg(tr + 2) * a.d;
+        for (int k = lane; k < a.d; k += 32) s[u] = fmaf(Hh[k] * M[k], Ht[k], s[u]);
+      }
     }
-    s = warp_sum(s);
-    if (lane == 0) {
-      float y = a.labels[row];
-      if (!isfinite(s)) atomicOr(a.flags, KG_FLAG_NONFINITE_SCORE);
-      float sp = fmaxf(s, 0.f) + log1pf(expf(-fabsf(s)));   // softplus = logaddexp(0, g)
-      a.per[i] = sp - y * s;
-      float sig = 1.f / (1.f + expf(-s));
+    float mine = 0.f;
+    int64_t row = -1;
+#pragma unroll
+    for (int u = 0; u < SU; ++u) {
+      const float t = warp_sum(s[u]);
+      if (lane == u) {
+        mine = t;
+        row = rows[u];
+      }
+    }
+    if (lane < SU && row >= 0) {
+      const int64_t i = i0 + lane;
+      const float sc = mine;
+      const float y = a.labels[row];
+      if (!isfinite(sc)) atomicOr(a.flags, KG_FLAG_NONFINITE_SCORE);
+      const float sp = fmaxf(sc, 0.f) + log1pf(expf(-fabsf(sc)));   // softplus = logaddexp(0, g)
+      a.per[i] = sp - y * sc;
+      const float sig = 1.f / (1.f + expf(-sc));
       a.dg[i] = (sig - y) / (float)a.b;
-      if (a.scores) a.scores[i] = s;
+      if (a.scores) a.scores[i] = sc;
     }
   }
 }
@@ -157,21 +196,13 @@ __global__ void __launch_bounds__(256) k_sub_partials(LossArgs a, const uint32_t
                                                       const int32_t* __restrict__ lo, const int32_t* __restrict__ hi,
                                                       const uint32_t* __restrict__ sub_start,
                                                       const uint32_t* __restrict__ total_sub,
-                                                      const int32_t* __restrict__ ng_dev, int32_t ng_host,
+                                                      const uint32_t* __restrict__ sgroup,
                                                       float* __restrict__ partial) {
-  const int32_t ng = ng_dev ? *ng_dev : ng_host;
   const uint32_t S = *total_sub;
   const int lane = lane_id();
   const int warps = (gridDim.x * blockDim.x) >> 5;
   for (int64_t s = warp_uniform((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5); s < S; s += warps) {
-    // group = last g with sub_start[g] <= s
-    int32_t l = 0, h = ng;
-    while (h - l > 1) {
-      int32_t mid = (l + h) >> 1;
-      if (sub_start[mid] <= s) l = mid;
-      else h = mid;
-    }
-    const int32_t g = l;
+    const int32_t g = (int32_t)__ldg(sgroup + s);   // owning group (precomputed with the bounds)
     const int64_t r0 = lo[g] + (int64_t)(s - sub_start[g]) * CH;
     const int64_t r1 = r0 + CH < hi[g] ? r0 + CH : hi[g];
     float acc[SL];
@@ -236,21 +267,14 @@ __global__ void __launch_bounds__(256) k_sub_partials_v4(LossArgs a, const uint3
                                                          const int32_t* __restrict__ hi,
                                                          const uint32_t* __restrict__ sub_start,
                                                          const uint32_t* __restrict__ total_sub,
-                                                         const int32_t* __restrict__ ng_dev, int32_t ng_host,
+                                                         const uint32_t* __restrict__ sgroup,
                                                          float* __restrict__ partial) {
-  const int32_t ng = ng_dev ? *ng_dev : ng_host;
   const uint32_t S = *total_sub;
   const int lane = lane_id();
   const bool on = 4 * lane < a.d;
   const int warps = (gridDim.x * blockDim.x) >> 5;
   for (int64_t s = warp_uniform((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5); s < S; s += warps) {
-    int32_t l = 0, h = ng;
-    while (h - l > 1) {
-      int32_t mid = (l + h) >> 1;
-      if (sub_start[mid] <= s) l = mid;
-      else h = mid;
-    }
-    const int32_t g = l;
+    const int32_t g = (int32_t)__ldg(sgroup + s);   // owning group (precomputed with the bounds)
     const int64_t r0 = lo[g] + (int64_t)(s - sub_start[g]) * CH;
     const int64_t r1 = r0 + CH < hi[g] ? r0 + CH : hi[g];
     float acc[4] = {0.f, 0.f, 0.f, 0.f};
@@ -315,12 +339,22 @@ __global__ void k_group_finish(const float* __restrict__ partial, const uint32_t
   }
 }
 
+__global__ void k_sub_groups(const uint32_t* __restrict__ nsub, const uint32_t* __restrict__ sub_start,
+                             const int32_t* __restrict__ ng_dev, int32_t ng_host, uint32_t* __restrict__ sgroup) {
+  const int32_t ng = ng_dev ? *ng_dev : ng_host;
+  for (int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; g < ng; g += (int64_t)gridDim.x * blockDim.x) {
+    const uint32_t a0 = sub_start[g], n0 = nsub[g];
+    for (uint32_t j = 0; j < n0; ++j) sgroup[a0 + j] = (uint32_t)g;
+  }
+}
+
 struct SegWs {
   int32_t* lo;
   int32_t* hi;
   uint32_t* nsub;
   uint32_t* sub_start;
   uint32_t* total;
+  uint32_t* sgroup;   // group of every sub-chunk
   float* partial;
   char* scan;
 };
@@ -332,6 +366,7 @@ static size_t seg_ws(int64_t nelem, int64_t ngroups, int d, SegWs* w, Arena& a) 
   s.nsub = a.take<uint32_t>(ngroups + 1);
   s.sub_start = a.take<uint32_t>(ngroups + 1);
   s.total = a.take<uint32_t>(4);
+  s.sgroup = a.take<uint32_t>((size_t)(nelem / CH + ngroups + 1));
   s.partial = a.take<float>((size_t)(nelem / CH + ngroups + 1) * d);
   s.scan = a.take<char>(scan_workspace(ngroups + 1));
   if (w) *w = s;
@@ -345,7 +380,10 @@ static kg_status seg_bounds(const uint32_t* keys, int64_t nelem, const int32_t* 
   KG_LAUNCH("k_group_len", k_group_len, gb, 256, 0, st, keys, nelem, ids, ng_dev, ng_max, w.hi);
   // with a device-resident group count the caller zeroed nsub[0:ng_max] so the
   // scan sees 0 beyond *ng_dev
-  return exclusive_scan_u32(w.nsub, w.sub_start, ng_max, w.total, w.scan, scan_workspace(ng_max + 1), st);
+  kg_status s = exclusive_scan_u32(w.nsub, w.sub_start, ng_max, w.total, w.scan, scan_workspace(ng_max + 1), st);
+  if (s != KG_OK) return s;
+  KG_LAUNCH("k_sub_groups", k_sub_groups, gb, 256, 0, st, w.nsub, w.sub_start, ng_dev, ng_max, w.sgroup);
+  return KG_OK;
 }
 
 template <int KIND>
@@ -354,11 +392,11 @@ static kg_status seg_sums(const LossArgs& la, const uint32_t* vals, int64_t nele
   int64_t max_sub = nelem / CH + ng_max + 1;
   int pb = persistent_blocks(max_sub * 32, 256, 8);
   const bool v4 = la.d % 4 == 0 && la.d <= 128 && (((uintptr_t)la.H | (uintptr_t)la.dec) & 15) == 0;
-  if (v4) KG_LAUNCH("k_sub_partials", (k_sub_partials_v4<KIND>), pb, 256, 0, st, la, vals, w.lo, w.hi, w.sub_start, w.total, ng_dev, ng_max, w.partial);
-  else if (la.d <= 32) KG_LAUNCH("k_sub_partials", (k_sub_partials<KIND, 1>), pb, 256, 0, st, la, vals, w.lo, w.hi, w.sub_start, w.total, ng_dev, ng_max, w.partial);
-  else if (la.d <= 64) KG_LAUNCH("k_sub_partials", (k_sub_partials<KIND, 2>), pb, 256, 0, st, la, vals, w.lo, w.hi, w.sub_start, w.total, ng_dev, ng_max, w.partial);
-  else if (la.d <= 128) KG_LAUNCH("k_sub_partials", (k_sub_partials<KIND, 4>), pb, 256, 0, st, la, vals, w.lo, w.hi, w.sub_start, w.total, ng_dev, ng_max, w.partial);
-  else if (la.d <= 256) KG_LAUNCH("k_sub_partials", (k_sub_partials<KIND, 8>), pb, 256, 0, st, la, vals, w.lo, w.hi, w.sub_start, w.total, ng_dev, ng_max, w.partial);
+  if (v4) KG_LAUNCH("k_sub_partials", (k_sub_partials_v4<KIND>), pb, 256, 0, st, la, vals, w.lo, w.hi, w.sub_start, w.total, w.sgroup, w.partial);
+  else if (la.d <= 32) KG_LAUNCH("k_sub_partials", (k_sub_partials<KIND, 1>), pb, 256, 0, st, la, vals, w.lo, w.hi, w.sub_start, w.total, w.sgroup, w.partial);
+  else if (la.d <= 64) KG_LAUNCH("k_sub_partials", (k_sub_partials<KIND, 2>), pb, 256, 0, st, la, vals, w.lo, w.hi, w.sub_start, w.total, w.sgroup, w.partial);
+  else if (la.d <= 128) KG_LAUNCH("k_sub_partials", (k_sub_partials<KIND, 4>), pb, 256, 0, st, la, vals, w.lo, w.hi, w.sub_start, w.total, w.sgroup, w.partial);
+  else if (la.d <= 256) KG_LAUNCH("k_sub_partials", (k_sub_partials<KIND, 8>), pb, 256, 0, st, la, vals, w.lo, w.hi, w.sub_start, w.total, w.sgroup, w.partial);
   else KG_REQUIRE(false, KG_ERR_SHAPE, "embedding width %d > 256 unsupported", la.d);
   KG_LAUNCH("k_group_finish", k_group_finish, persistent_blocks((int64_t)ng_max * la.d, 256, 8), 256, 0, st, w.partial, w.sub_start, w.nsub,
                                                                                    ids, ng_dev, ng_max, la.d, out);
@@ -437,7 +475,8 @@ static kg_status loss_compute(const LossArgs& la, int32_t R, const int32_t* orde
                               cudaStream_t st, cudaStream_t side = nullptr) {
   const int64_t b = la.b;
   const bool v4 = la.d % 4 == 0 && (((uintptr_t)la.H | (uintptr_t)la.dec) & 15) == 0;
-  KG_LAUNCH("k_score", v4 ? k_score<true> : k_score<false>, persistent_blocks(b * 32, 256, 8), 256, 0, st, la);
+  KG_LAUNCH("k_score", v4 ? k_score<true> : k_score<false>, persistent_blocks(ceil_div(b, SU) * 32, 256, 8), 256, 0,
+            st, la);
   cudaStream_t sd = st;
   if (side) {
     sd = side;
@@ -458,9 +497,11 @@ int32_t kg_loss_group_fields(void* ws, int64_t ws_bytes, int64_t b, int32_t n_lo
   LossWs w;
   if (loss_arena(ws, (size_t)ws_bytes, b, n_local, d, R, &w) > (size_t)ws_bytes) return -1;
   const int64_t nr = (int64_t)R + 1, nv = w.ngmax + 1;
-  void* p[] = {w.rv, w.vv, w.wr.lo, w.wr.hi, w.wr.nsub, w.wr.sub_start, w.wr.total,
-               w.wv.lo, w.wv.hi, w.wv.nsub, w.wv.sub_start, w.wv.total};
-  const int64_t sz[] = {4 * b, 8 * b, 4 * nr, 4 * nr, 4 * nr, 4 * nr, 16, 4 * nv, 4 * nv, 4 * nv, 4 * nv, 16};
+  const int64_t sr = b / CH + R + 1, sv = 2 * b / CH + w.ngmax + 1;   // sub-chunk capacities (seg_ws)
+  void* p[] = {w.rv, w.vv, w.wr.lo, w.wr.hi, w.wr.nsub, w.wr.sub_start, w.wr.total, w.wr.sgroup,
+               w.wv.lo, w.wv.hi, w.wv.nsub, w.wv.sub_start, w.wv.total, w.wv.sgroup};
+  const int64_t sz[] = {4 * b, 8 * b, 4 * nr, 4 * nr, 4 * nr, 4 * nr, 16, 4 * sr,
+                        4 * nv, 4 * nv, 4 * nv, 4 * nv, 16, 4 * sv};
   const int32_t n = (int32_t)(sizeof(sz) / sizeof(sz[0]));
   if (n > max) return -1;
   for (int32_t i = 0; i < n; ++i) {

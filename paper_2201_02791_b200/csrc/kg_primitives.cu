@@ -478,29 +478,29 @@ kg_status compact_flags_ex(uint32_t* flags, int64_t n, int32_t* out, const int32
 // Round-indexed segment copy: seg i copies bytes from src + r*src_stride to
 // dst + r*dst_stride, r = *round_dev (device) or round_host. One launch moves
 // a round's precomputed closure / grouping into the fixed working buffers.
-constexpr int KG_MAX_SEGS = 16;
+constexpr int KG_MAX_SEGS = 24;
 struct SegList {
   kg_copy_seg seg[KG_MAX_SEGS];
   int n;
 };
 
+// blockIdx.y = segment: the segments copy in parallel (a serial loop over
+// segments would chain one memory latency per segment).
 __global__ void __launch_bounds__(256) k_copy_segments(SegList L, const int64_t* __restrict__ round_dev,
                                                        int64_t round_host) {
   const int64_t r = round_dev ? *round_dev : round_host;
-  for (int i = 0; i < L.n; ++i) {
-    const kg_copy_seg& g = L.seg[i];
-    const char* src = static_cast<const char*>(g.src) + r * g.src_round_stride;
-    char* dst = static_cast<char*>(g.dst) + r * g.dst_round_stride;
-    const bool v16 = (((uintptr_t)src | (uintptr_t)dst | (uintptr_t)g.bytes) & 15) == 0;
-    if (v16) {
-      const int64_t n = g.bytes / 16;
-      for (int64_t x = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; x < n; x += (int64_t)gridDim.x * blockDim.x)
-        reinterpret_cast<int4*>(dst)[x] = reinterpret_cast<const int4*>(src)[x];
-    } else {
-      for (int64_t x = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; x < g.bytes;
-           x += (int64_t)gridDim.x * blockDim.x)
-        dst[x] = src[x];
-    }
+  const kg_copy_seg& g = L.seg[blockIdx.y];
+  const char* src = static_cast<const char*>(g.src) + r * g.src_round_stride;
+  char* dst = static_cast<char*>(g.dst) + r * g.dst_round_stride;
+  const bool v16 = (((uintptr_t)src | (uintptr_t)dst | (uintptr_t)g.bytes) & 15) == 0;
+  if (v16) {
+    const int64_t n = g.bytes / 16;
+    for (int64_t x = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; x < n; x += (int64_t)gridDim.x * blockDim.x)
+      reinterpret_cast<int4*>(dst)[x] = __ldg(reinterpret_cast<const int4*>(src) + x);
+  } else {
+    for (int64_t x = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; x < g.bytes;
+         x += (int64_t)gridDim.x * blockDim.x)
+      dst[x] = src[x];
   }
 }
 
@@ -529,8 +529,11 @@ kg_status kg_copy_segments(const kg_copy_seg* segs, int32_t n, const int64_t* ro
     most = segs[i].bytes > most ? segs[i].bytes : most;
   }
   L.n = n;
-  KG_LAUNCH("k_copy_segments", kg::k_copy_segments, kg::persistent_blocks(most / 16 + 1, 256, 2), 256, 0,
-            kg::as_stream(stream), L, round_dev, round_host);
+  // enough blocks per segment for the largest; the grid totals ~2 waves
+  const int64_t per = kg::ceil_div(most / 16 + 1, 256);
+  const int64_t cap = kg::ceil_div((int64_t)kg::num_sms() * 16, n);
+  const dim3 grid((unsigned)(per < cap ? per : cap), (unsigned)n, 1);
+  KG_LAUNCH("k_copy_segments", kg::k_copy_segments, grid, 256, 0, kg::as_stream(stream), L, round_dev, round_host);
   return KG_OK;
 }
 
@@ -577,6 +580,18 @@ static unsigned record_flags(cudaStream_t st) {
   cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
   cudaStreamIsCapturing(st, &cs);
   return cs == cudaStreamCaptureStatusActive ? cudaEventRecordExternal : cudaEventRecordDefault;
+}
+
+bool knocked_out(const char* name) {
+  static const char* list = getenv("KG_KNOCKOUT");
+  if (list == nullptr || !*list) return false;
+  const size_t n = strlen(name);
+  for (const char* p = list; (p = strstr(p, name)) != nullptr; p += n) {
+    const bool start = p == list || p[-1] == ',';
+    const bool end = p[n] == 0 || p[n] == ',';
+    if (start && end) return true;
+  }
+  return false;
 }
 
 LaunchScope::LaunchScope(const char* name, cudaStream_t s) : st(s), slot(-1) {

@@ -28,6 +28,9 @@ namespace kg {
 constexpr int MAXB = 4;
 constexpr int UNR = 8;     // gathered rows in flight per lane
 constexpr int MAXC = 64;   // messages per chunk handled by one warp (2 per lane)
+#ifndef KG_GATHER_BPS
+#define KG_GATHER_BPS 3    // resident 256-thread blocks per SM of the gather kernels
+#endif
 
 // Sum x[0..7] over the 32 lanes of a warp, 9 shuffles: on return lane l holds
 // the total of entry ((l>>4)&1)*4 + ((l>>3)&1)*2 + ((l>>2)&1).
@@ -102,7 +105,7 @@ struct EdgeMeta {
 };
 
 template <int NB, int VEC, int S>
-__global__ void __launch_bounds__(256, 3) k_aggregate(AggArgs a) {
+__global__ void __launch_bounds__(256, KG_GATHER_BPS) k_aggregate(AggArgs a) {
   extern __shared__ float coef[];
   for (int i = threadIdx.x; i < a.G * a.B; i += blockDim.x) coef[i] = a.coeffs[i];
   __syncthreads();
@@ -330,7 +333,7 @@ struct CscArgs {
 // dX = dS . Wb feeds the next layer). MODE 2: edge dots + self dots only (they
 // feed only d coeffs, so this pass runs on the forked stream).
 template <int NB, int VEC, int S, int MODE>
-__global__ void __launch_bounds__(256, 3) k_csc_backward(CscArgs a) {
+__global__ void __launch_bounds__(256, KG_GATHER_BPS) k_csc_backward(CscArgs a) {
   extern __shared__ float coef[];
   for (int i = threadIdx.x; i < a.G * a.B; i += blockDim.x) coef[i] = a.coeffs[i];
   __syncthreads();
@@ -816,7 +819,7 @@ static kg_status dispatch_width(int d, F4 f4, F1a f1, F1b f2, F1c f4s, F1d f8) {
 
 static kg_status run_aggregate(const AggArgs& a, const kg_graph_csr* G, cudaStream_t st) {
   KG_REQUIRE(G->chunk <= MAXC, KG_ERR_VALIDATION, "chunk size %d > %d", G->chunk, MAXC);
-  int blocks = persistent_blocks(cap_chunks(G) * 32, 256, 3);
+  int blocks = persistent_blocks(cap_chunks(G) * 32, 256, KG_GATHER_BPS);
   int cblocks = persistent_blocks(cap_split_rows(G) * CB_THREADS, CB_THREADS, 8);   // one block per split row
   size_t smem = (size_t)a.G * a.B * sizeof(float);
   return dispatch_width(
@@ -829,7 +832,7 @@ static kg_status run_aggregate(const AggArgs& a, const kg_graph_csr* G, cudaStre
 
 static kg_status run_csc(const CscArgs& a, const kg_graph_csr* G, cudaStream_t st, int mode = 0) {
   KG_REQUIRE(G->chunk <= MAXC, KG_ERR_VALIDATION, "chunk size %d > %d", G->chunk, MAXC);
-  int blocks = persistent_blocks(cap_chunks(G) * 32, 256, 3);
+  int blocks = persistent_blocks(cap_chunks(G) * 32, 256, KG_GATHER_BPS);
   int cblocks = persistent_blocks(cap_split_rows(G) * CB_THREADS, CB_THREADS, 8);   // one block per split row
   size_t smem = (size_t)a.G * a.B * sizeof(float);
   return dispatch_width(
@@ -1024,7 +1027,18 @@ kg_status kg_rgcn_backward(const kg_graph_csr* G, const kg_layer_params* lp, con
   // side stream concurrently; dV follows dS on the side stream.
   cudaStream_t sd = st;
   const int split = dcoeff_split(G->e, lp->G);
-  if (side_stream) {
+  static const bool fused = getenv("KG_CSC_FUSED") && getenv("KG_CSC_FUSED")[0] == '1';
+  if (side_stream && fused) {
+    s = run_csc(c, G, st, 0);
+    if (s != KG_OK) return s;
+    sd = as_stream(side_stream);
+    KG_CUDA(cudaEventRecord(fork_event(), st));
+    KG_CUDA(cudaStreamWaitEvent(sd, fork_event(), 0));
+    KG_LAUNCH("k_dcoeff_reduce", k_dcoeff_partial, dim3((unsigned)lp->G, (unsigned)split, 1), 256, 0, sd,
+              G->rel_ptr, G->rel_perm, counts, t, w.ed, w.ed_self, lp->G, B, w.dc_part);
+    KG_LAUNCH("k_dcoeff_final", k_dcoeff_final, persistent_blocks((int64_t)lp->G * B, 256, 2), 256, 0, sd,
+              w.dc_part, lp->G, B, split, d_coeffs);
+  } else if (side_stream) {
     sd = as_stream(side_stream);
     KG_CUDA(cudaEventRecord(fork_event(), st));
     KG_CUDA(cudaStreamWaitEvent(sd, fork_event(), 0));
