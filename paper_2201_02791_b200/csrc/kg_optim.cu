@@ -75,11 +75,20 @@ struct StepArgs {
   uint32_t* flags;
 };
 
+// Adam bias corrections for the device step counter: computed once per block
+// (two fp64 pow per thread would cost more than the update itself); every
+// thread of the block must call it.
 __device__ __forceinline__ void bias_corrections(const int64_t* step_dev, float b1, float b2, float& i1, float& i2) {
   if (!step_dev) return;
-  const double t = (double)*step_dev;
-  i1 = (float)(1.0 / (1.0 - pow((double)b1, t)));
-  i2 = (float)(1.0 / (1.0 - pow((double)b2, t)));
+  __shared__ float bc[2];
+  if (threadIdx.x == 0) {
+    const double t = (double)*step_dev;
+    bc[0] = (float)(1.0 / (1.0 - pow((double)b1, t)));
+    bc[1] = (float)(1.0 / (1.0 - pow((double)b2, t)));
+  }
+  __syncthreads();
+  i1 = bc[0];
+  i2 = bc[1];
 }
 
 __global__ void k_dense_step(StepArgs a) {
