@@ -104,12 +104,18 @@ struct EdgeMeta {
   float cf[2][NB];
 };
 
-template <int NB, int VEC, int S>
+// EPI > 1 (narrow rows, d <= 128 / EPI): lanes split into EPI groups of
+// LPR = 32 / EPI lanes; each group gathers a different message, so a warp
+// load moves EPI rows and EPI x UNR rows are in flight per warp. The groups'
+// sums are folded with xor shuffles before the row is finished.
+template <int NB, int VEC, int S, int EPI>
 __global__ void __launch_bounds__(256, KG_GATHER_BPS) k_aggregate(AggArgs a) {
   extern __shared__ float coef[];
   for (int i = threadIdx.x; i < a.G * a.B; i += blockDim.x) coef[i] = a.coeffs[i];
   __syncthreads();
   const int lane = lane_id();
+  constexpr int LPR = 32 / EPI;
+  const int grp = lane / LPR, cl = lane % LPR;
   const int32_t T = a.counts[a.t];
   const int32_t NC = a.ck.counts[0];
   const int d = a.d;
@@ -117,7 +123,7 @@ __global__ void __launch_bounds__(256, KG_GATHER_BPS) k_aggregate(AggArgs a) {
   const int warps = (gridDim.x * blockDim.x) >> 5;
   bool slot_ok[S];
 #pragma unroll
-  for (int s = 0; s < S; ++s) slot_ok[s] = (s * 32 + lane) * VEC < d;
+  for (int s = 0; s < S; ++s) slot_ok[s] = (s * LPR + cl) * VEC < d;
   for (int64_t c = warp_uniform((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5); c < NC; c += warps) {
     const int32_t v = a.ck.row[c];
     const int32_t p = a.pos[v];
@@ -147,14 +153,15 @@ __global__ void __launch_bounds__(256, KG_GATHER_BPS) k_aggregate(AggArgs a) {
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
       const int nh = min(32, cnt - 32 * h);
-      for (int j = 0; j < nh; j += UNR) {
+      for (int j = 0; j < nh; j += UNR * EPI) {
         float xs[UNR][S][VEC];
 #pragma unroll
         for (int q = 0; q < UNR; ++q) {
-          const int32_t u = __shfl_sync(0xffffffffu, m.other[h], (j + q) & 31);
+          const int32_t u = __shfl_sync(0xffffffffu, m.other[h], (j + q * EPI + grp) & 31);
 #pragma unroll
           for (int s = 0; s < S; ++s) {
-            if (j + q < nh && slot_ok[s]) VecIO<VEC>::load(a.H + (int64_t)u * d + (s * 32 + lane) * VEC, xs[q][s]);
+            if (j + q * EPI + grp < nh && slot_ok[s])
+              VecIO<VEC>::load(a.H + (int64_t)u * d + (s * LPR + cl) * VEC, xs[q][s]);
             else
 #pragma unroll
               for (int cc = 0; cc < VEC; ++cc) xs[q][s][cc] = 0.f;
@@ -165,7 +172,7 @@ __global__ void __launch_bounds__(256, KG_GATHER_BPS) k_aggregate(AggArgs a) {
 #pragma unroll
           for (int b = 0; b < NB; ++b) {
             if (b < B) {
-              const float cf = __shfl_sync(0xffffffffu, m.cf[h][b], (j + q) & 31);
+              const float cf = __shfl_sync(0xffffffffu, m.cf[h][b], (j + q * EPI + grp) & 31);
 #pragma unroll
               for (int s = 0; s < S; ++s)
 #pragma unroll
@@ -175,20 +182,35 @@ __global__ void __launch_bounds__(256, KG_GATHER_BPS) k_aggregate(AggArgs a) {
         }
       }
     }
+    if (EPI > 1) {
+      // fold the message groups (lanes cl, cl + LPR, ...): every lane holds the total
+#pragma unroll
+      for (int o = LPR; o < 32; o <<= 1)
+#pragma unroll
+        for (int b = 0; b < NB; ++b)
+#pragma unroll
+          for (int s2 = 0; s2 < S; ++s2)
+#pragma unroll
+            for (int cc = 0; cc < VEC; ++cc) acc[b][s2][cc] += __shfl_xor_sync(0xffffffffu, acc[b][s2][cc], o);
+    }
+    // the first lane group owns the row's columns from here on
+    bool own[S];
+#pragma unroll
+    for (int s2 = 0; s2 < S; ++s2) own[s2] = slot_ok[s2] && grp == 0;
     float* out;
     if (nch == 1) {
       // self-loop group 2R (norm 1), then the finished row
       float xv[S][VEC];
 #pragma unroll
       for (int s = 0; s < S; ++s)
-        if (slot_ok[s]) VecIO<VEC>::load(a.H + (int64_t)v * d + (s * 32 + lane) * VEC, xv[s]);
+        if (own[s]) VecIO<VEC>::load(a.H + (int64_t)v * d + (s * LPR + cl) * VEC, xv[s]);
 #pragma unroll
       for (int b = 0; b < NB; ++b) {
         if (b < B) {
           float cf = coef[(a.G - 1) * B + b];
 #pragma unroll
           for (int s = 0; s < S; ++s)
-            if (slot_ok[s])
+            if (own[s])
 #pragma unroll
               for (int cc = 0; cc < VEC; ++cc) acc[b][s][cc] = fmaf(cf, xv[s][cc], acc[b][s][cc]);
         }
@@ -200,7 +222,7 @@ __global__ void __launch_bounds__(256, KG_GATHER_BPS) k_aggregate(AggArgs a) {
           if (b < B)
 #pragma unroll
             for (int s = 0; s < S; ++s)
-              if (slot_ok[s]) packed_store<VEC>(a.acc, a.acc_nk, p, b * d + (s * 32 + lane) * VEC, acc[b][s]);
+              if (own[s]) packed_store<VEC>(a.acc, a.acc_nk, p, b * d + (s * LPR + cl) * VEC, acc[b][s]);
         packed_zero_pad(a.acc, a.acc_nk, p, B * d, lane, 32);
         continue;
       }
@@ -213,7 +235,7 @@ __global__ void __launch_bounds__(256, KG_GATHER_BPS) k_aggregate(AggArgs a) {
       if (b < B)
 #pragma unroll
         for (int s = 0; s < S; ++s)
-          if (slot_ok[s]) VecIO<VEC>::store(out + (int64_t)b * d + (s * 32 + lane) * VEC, acc[b][s]);
+          if (own[s]) VecIO<VEC>::store(out + (int64_t)b * d + (s * LPR + cl) * VEC, acc[b][s]);
   }
 }
 
@@ -332,12 +354,16 @@ struct CscArgs {
 // MODE 0: dS and edge dots in one pass. MODE 1: dS only (the critical path:
 // dX = dS . Wb feeds the next layer). MODE 2: edge dots + self dots only (they
 // feed only d coeffs, so this pass runs on the forked stream).
-template <int NB, int VEC, int S, int MODE>
+// EPI > 1 (MODE 1 only, narrow rows): message groups as in k_aggregate.
+template <int NB, int VEC, int S, int MODE, int EPI>
 __global__ void __launch_bounds__(256, KG_GATHER_BPS) k_csc_backward(CscArgs a) {
+  static_assert(EPI == 1 || MODE == 1, "message groups only in the dS-only pass");
   extern __shared__ float coef[];
   for (int i = threadIdx.x; i < a.G * a.B; i += blockDim.x) coef[i] = a.coeffs[i];
   __syncthreads();
   const unsigned lane = lane_id();
+  constexpr int LPR = 32 / EPI;
+  const int grp = (int)lane / LPR, cl = (int)lane % LPR;
   const int32_t T = a.counts[a.t];
   const int32_t Sn = a.counts[a.t + 1];
   const int32_t NC = a.ck.counts[0];
@@ -346,7 +372,7 @@ __global__ void __launch_bounds__(256, KG_GATHER_BPS) k_csc_backward(CscArgs a) 
   const int warps = (gridDim.x * blockDim.x) >> 5;
   bool slot_ok[S];
 #pragma unroll
-  for (int s = 0; s < S; ++s) slot_ok[s] = (s * 32 + lane) * VEC < d;
+  for (int s = 0; s < S; ++s) slot_ok[s] = (s * LPR + cl) * VEC < d;
   for (int64_t c = warp_uniform((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5); c < NC; c += warps) {
     const int32_t u = a.ck.row[c];
     const int32_t q = a.pos[u];
@@ -400,15 +426,15 @@ __global__ void __launch_bounds__(256, KG_GATHER_BPS) k_csc_backward(CscArgs a) 
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
       const int nh = min(32, cnt - 32 * h);
-      for (int j = 0; j < nh; j += UNR) {
+      for (int j = 0; j < nh; j += UNR * EPI) {
         float zs[UNR][S][VEC];
 #pragma unroll
         for (int k = 0; k < UNR; ++k) {
-          const int32_t pw = __shfl_sync(0xffffffffu, m.other[h], (j + k) & 31);
+          const int32_t pw = __shfl_sync(0xffffffffu, m.other[h], (j + k * EPI + grp) & 31);
 #pragma unroll
           for (int s = 0; s < S; ++s) {
-            if (j + k < nh && pw >= 0 && slot_ok[s])
-              VecIO<VEC>::load(a.dZ + (int64_t)pw * d + (s * 32 + lane) * VEC, zs[k][s]);
+            if (j + k * EPI + grp < nh && pw >= 0 && slot_ok[s])
+              VecIO<VEC>::load(a.dZ + (int64_t)pw * d + (s * LPR + cl) * VEC, zs[k][s]);
             else
 #pragma unroll
               for (int cc = 0; cc < VEC; ++cc) zs[k][s][cc] = 0.f;
@@ -421,7 +447,7 @@ __global__ void __launch_bounds__(256, KG_GATHER_BPS) k_csc_backward(CscArgs a) 
 #pragma unroll
           for (int b = 0; b < NB; ++b) {
             if (b < B) {
-              const float cf = __shfl_sync(0xffffffffu, m.cf[h][b], (j + k) & 31);
+              const float cf = __shfl_sync(0xffffffffu, m.cf[h][b], (j + k * EPI + grp) & 31);
 #pragma unroll
               for (int s = 0; s < S; ++s)
 #pragma unroll
@@ -478,6 +504,19 @@ __global__ void __launch_bounds__(256, KG_GATHER_BPS) k_csc_backward(CscArgs a) 
       }
       continue;
     }
+    if (EPI > 1) {
+#pragma unroll
+      for (int o = LPR; o < 32; o <<= 1)
+#pragma unroll
+        for (int b = 0; b < NB; ++b)
+#pragma unroll
+          for (int s2 = 0; s2 < S; ++s2)
+#pragma unroll
+            for (int cc = 0; cc < VEC; ++cc) acc[b][s2][cc] += __shfl_xor_sync(0xffffffffu, acc[b][s2][cc], o);
+    }
+    bool own[S];   // the first lane group owns the row's columns from here on
+#pragma unroll
+    for (int s2 = 0; s2 < S; ++s2) own[s2] = slot_ok[s2] && grp == 0;
     float* out;
     if (nch == 1) {
       if (q < T) {
@@ -485,7 +524,7 @@ __global__ void __launch_bounds__(256, KG_GATHER_BPS) k_csc_backward(CscArgs a) 
         float z[S][VEC];
 #pragma unroll
         for (int s = 0; s < S; ++s) {
-          if (slot_ok[s]) VecIO<VEC>::load(a.dZ + (int64_t)q * d + (s * 32 + lane) * VEC, z[s]);
+          if (own[s]) VecIO<VEC>::load(a.dZ + (int64_t)q * d + (s * LPR + cl) * VEC, z[s]);
           else
 #pragma unroll
             for (int cc = 0; cc < VEC; ++cc) z[s][cc] = 0.f;
@@ -516,7 +555,7 @@ __global__ void __launch_bounds__(256, KG_GATHER_BPS) k_csc_backward(CscArgs a) 
           if (b < B)
 #pragma unroll
             for (int s = 0; s < S; ++s)
-              if (slot_ok[s]) packed_store<VEC>(a.dS_pk, a.dS_nk, q, b * d + (s * 32 + lane) * VEC, acc[b][s]);
+              if (own[s]) packed_store<VEC>(a.dS_pk, a.dS_nk, q, b * d + (s * LPR + cl) * VEC, acc[b][s]);
         packed_zero_pad(a.dS_pk, a.dS_nk, q, B * d, lane, 32);
       }
     } else {
@@ -527,7 +566,7 @@ __global__ void __launch_bounds__(256, KG_GATHER_BPS) k_csc_backward(CscArgs a) 
       if (b < B)
 #pragma unroll
         for (int s = 0; s < S; ++s)
-          if (slot_ok[s]) VecIO<VEC>::store(out + (int64_t)b * d + (s * 32 + lane) * VEC, acc[b][s]);
+          if (own[s]) VecIO<VEC>::store(out + (int64_t)b * d + (s * LPR + cl) * VEC, acc[b][s]);
   }
 }
 
@@ -768,37 +807,37 @@ static int64_t cap_chunks(const kg_graph_csr* G) { return (int64_t)G->n + G->e /
 static int64_t cap_split_chunks(const kg_graph_csr* G) { return 2 * G->e / G->chunk + 1; }
 static int64_t cap_split_rows(const kg_graph_csr* G) { return G->e / G->chunk + 1; }
 
-template <int VEC, int S>
+template <int VEC, int S, int EPI = 1>
 static kg_status launch_agg(const AggArgs& a, int blocks, int cblocks, size_t smem, cudaStream_t st) {
   switch (a.B) {
-    case 1: KG_LAUNCH("k_aggregate", (k_aggregate<1, VEC, S>), blocks, 256, smem, st, a); break;
-    case 2: KG_LAUNCH("k_aggregate", (k_aggregate<2, VEC, S>), blocks, 256, smem, st, a); break;
-    case 3: KG_LAUNCH("k_aggregate", (k_aggregate<3, VEC, S>), blocks, 256, smem, st, a); break;
-    default: KG_LAUNCH("k_aggregate", (k_aggregate<4, VEC, S>), blocks, 256, smem, st, a); break;
+    case 1: KG_LAUNCH("k_aggregate", (k_aggregate<1, VEC, S, EPI>), blocks, 256, smem, st, a); break;
+    case 2: KG_LAUNCH("k_aggregate", (k_aggregate<2, VEC, S, EPI>), blocks, 256, smem, st, a); break;
+    case 3: KG_LAUNCH("k_aggregate", (k_aggregate<3, VEC, S, EPI>), blocks, 256, smem, st, a); break;
+    default: KG_LAUNCH("k_aggregate", (k_aggregate<4, VEC, S, EPI>), blocks, 256, smem, st, a); break;
   }
   if (a.d % 4 == 0) KG_LAUNCH("k_aggregate_combine", k_aggregate_combine<true>, cblocks, CB_THREADS, 0, st, a);
   else KG_LAUNCH("k_aggregate_combine", k_aggregate_combine<false>, cblocks, CB_THREADS, 0, st, a);
   return KG_OK;
 }
-template <int VEC, int S, int MODE>
+template <int VEC, int S, int MODE, int EPI = 1>
 static kg_status launch_csc_mode(const CscArgs& a, int blocks, size_t smem, cudaStream_t st) {
   const char* name = MODE == 2 ? "k_csc_dots" : "k_csc_backward";
   switch (a.B) {
-    case 1: KG_LAUNCH(name, (k_csc_backward<1, VEC, S, MODE>), blocks, 256, smem, st, a); break;
-    case 2: KG_LAUNCH(name, (k_csc_backward<2, VEC, S, MODE>), blocks, 256, smem, st, a); break;
-    case 3: KG_LAUNCH(name, (k_csc_backward<3, VEC, S, MODE>), blocks, 256, smem, st, a); break;
-    default: KG_LAUNCH(name, (k_csc_backward<4, VEC, S, MODE>), blocks, 256, smem, st, a); break;
+    case 1: KG_LAUNCH(name, (k_csc_backward<1, VEC, S, MODE, EPI>), blocks, 256, smem, st, a); break;
+    case 2: KG_LAUNCH(name, (k_csc_backward<2, VEC, S, MODE, EPI>), blocks, 256, smem, st, a); break;
+    case 3: KG_LAUNCH(name, (k_csc_backward<3, VEC, S, MODE, EPI>), blocks, 256, smem, st, a); break;
+    default: KG_LAUNCH(name, (k_csc_backward<4, VEC, S, MODE, EPI>), blocks, 256, smem, st, a); break;
   }
   return KG_OK;
 }
 
 // mode 0: dS + dots (+ combine); 1: dS (+ combine without self dots); 2: dots only
-template <int VEC, int S>
+template <int VEC, int S, int EPI = 1>
 static kg_status launch_csc(const CscArgs& a0, int blocks, int cblocks, size_t smem, cudaStream_t st, int mode) {
   CscArgs a = a0;
   a.self_dots = mode == 0;
   kg_status s = mode == 0 ? launch_csc_mode<VEC, S, 0>(a, blocks, smem, st)
-              : mode == 1 ? launch_csc_mode<VEC, S, 1>(a, blocks, smem, st)
+              : mode == 1 ? launch_csc_mode<VEC, S, 1, EPI>(a, blocks, smem, st)
                           : launch_csc_mode<VEC, S, 2>(a, blocks, smem, st);
   if (s != KG_OK || mode == 2) return s;
   if (a.d % 4 == 0) KG_LAUNCH("k_csc_combine", k_csc_combine<true>, cblocks, CB_THREADS, 0, st, a);
@@ -822,6 +861,10 @@ static kg_status run_aggregate(const AggArgs& a, const kg_graph_csr* G, cudaStre
   int blocks = persistent_blocks(cap_chunks(G) * 32, 256, KG_GATHER_BPS);
   int cblocks = persistent_blocks(cap_split_rows(G) * CB_THREADS, CB_THREADS, 8);   // one block per split row
   size_t smem = (size_t)a.G * a.B * sizeof(float);
+  // narrow rows: several messages per warp load (float4 lanes, EPI groups)
+  const bool al16 = ((uintptr_t)a.H & 15) == 0;
+  if (a.d % 4 == 0 && a.d <= 32 && al16) return launch_agg<4, 1, 4>(a, blocks, cblocks, smem, st);
+  if (a.d % 4 == 0 && a.d <= 64 && al16) return launch_agg<4, 1, 2>(a, blocks, cblocks, smem, st);
   return dispatch_width(
       a.d, [&] { return launch_agg<4, 1>(a, blocks, cblocks, smem, st); },
       [&] { return launch_agg<1, 1>(a, blocks, cblocks, smem, st); },
@@ -835,6 +878,12 @@ static kg_status run_csc(const CscArgs& a, const kg_graph_csr* G, cudaStream_t s
   int blocks = persistent_blocks(cap_chunks(G) * 32, 256, KG_GATHER_BPS);
   int cblocks = persistent_blocks(cap_split_rows(G) * CB_THREADS, CB_THREADS, 8);   // one block per split row
   size_t smem = (size_t)a.G * a.B * sizeof(float);
+  // narrow rows: the dS-only pass gathers several messages per warp load
+  const bool al16 = ((uintptr_t)a.dZ & 15) == 0 && ((uintptr_t)a.Y & 15) == 0;
+  // (the dot passes keep one message per warp load: their per-message warp
+  // reductions want every lane busy)
+  if (mode == 1 && a.d % 4 == 0 && a.d <= 32 && al16) return launch_csc<4, 1, 4>(a, blocks, cblocks, smem, st, mode);
+  if (mode == 1 && a.d % 4 == 0 && a.d <= 64 && al16) return launch_csc<4, 1, 2>(a, blocks, cblocks, smem, st, mode);
   return dispatch_width(
       a.d, [&] { return launch_csc<4, 1>(a, blocks, cblocks, smem, st, mode); },
       [&] { return launch_csc<1, 1>(a, blocks, cblocks, smem, st, mode); },

@@ -222,14 +222,16 @@ def test_fb15k_shape_views_and_negatives_bit_exact():
         assert not v.is_positive(neg).any()
 
 
-def test_oracle_parity_on_fb_batch():
+@pytest.mark.parametrize("dims", [[32, 32, 32], [48, 64, 40], [100, 100, 100]])
+def test_oracle_parity_on_fb_batch(dims):
     """Teacher-forced loss/grad parity against the oracle on an FB-shaped
-    partition (P=4, part 0) at b = 4096."""
+    partition (P=4, part 0) at b = 4096; the widths cover every gather
+    variant (4 / 2 messages per warp load, one message per warp load)."""
     graph, split = kb.generate_synthetic(14541, 237, 272115 / 14541, seed=0)
     pset = kb.neighborhood_expand(kb.vertex_cut_partition(graph, 4, seed=0), graph, 2)
     part = pset.partitions[0]
     v = kb.build_view(part, graph.num_entities, graph.num_relations)
-    mc = kb.ModelConfig(2, [32, 32, 32], 2, 237, 1, mode="embedding")
+    mc = kb.ModelConfig(2, list(dims), 2, 237, 1, mode="embedding")
     p = kb.init_params(mc, np.random.default_rng(0), num_entities=graph.num_entities)
     p = kb.ModelParams([b.astype(np.float32).astype(np.float64) for b in p.bases],
                        [c.astype(np.float32).astype(np.float64) for c in p.coeffs],
