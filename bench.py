@@ -67,8 +67,20 @@ def dist_setup():
     if torch.cuda.is_available():
         torch.cuda.set_device(local)
     if world > 1 and not torch.distributed.is_initialized():
-        torch.distributed.init_process_group("nccl" if torch.cuda.is_available() else "gloo",
-                                             device_id=torch.device("cuda", local) if torch.cuda.is_available() else None)
+        # stdout carries exactly one JSON line: keep NCCL's init banner off it
+        os.environ.setdefault("NCCL_DEBUG", "WARN")
+        sys.stdout.flush()
+        saved = os.dup(1)
+        os.dup2(2, 1)
+        try:
+            torch.distributed.init_process_group("nccl" if torch.cuda.is_available() else "gloo",
+                                                 device_id=torch.device("cuda", local) if torch.cuda.is_available()
+                                                 else None)
+            torch.distributed.barrier()
+        finally:
+            sys.stdout.flush()
+            os.dup2(saved, 1)
+            os.close(saved)
     return world, rank, local
 
 

@@ -356,7 +356,12 @@ typedef struct kg_epoch_prep_args {
   int64_t closure_ws_bytes;
   void* loss_ws;
   int64_t loss_ws_bytes;
+  /* >= 1: rounds run as this many concurrent branches (at most
+   * KG_PREP_MAX_BRANCHES), branch k using the workspaces at
+   * closure_ws + k*closure_ws_bytes and loss_ws + k*loss_ws_bytes. */
+  int32_t branches;
 } kg_epoch_prep_args;
+#define KG_PREP_MAX_BRANCHES 4
 kg_status kg_epoch_prep(const kg_epoch_prep_args* a, void* stream);
 
 /* ---------------------------------------------------------------------- */

@@ -50,7 +50,8 @@ class KgEpochPrepArgs(ctypes.Structure):
                 ("labels", c_void_p), ("total", c_int64), ("b", c_int64), ("d", c_int32), ("R", c_int32),
                 ("order", c_void_p), ("pos", c_void_p), ("counts", c_void_p), ("groups", c_void_p),
                 ("groups_stride", c_int64), ("flags", c_void_p), ("closure_ws", c_void_p),
-                ("closure_ws_bytes", c_int64), ("loss_ws", c_void_p), ("loss_ws_bytes", c_int64)]
+                ("closure_ws_bytes", c_int64), ("loss_ws", c_void_p), ("loss_ws_bytes", c_int64),
+                ("branches", c_int32)]
 
 
 P = c_void_p

@@ -569,35 +569,73 @@ kg_status kg_epoch_prep(const kg_epoch_prep_args* a, void* stream) {
   KG_REQUIRE(a != nullptr && a->g != nullptr, KG_ERR_VALIDATION, "kg_epoch_prep: null arguments");
   KG_REQUIRE(a->rounds >= 1 && a->b >= 1 && a->hops >= 0, KG_ERR_VALIDATION, "kg_epoch_prep: bad sizes");
   const int32_t n = a->g->n, L1 = a->hops + 1;
-  void* ptrs[16];
-  int64_t sz[16];
-  const int32_t nf = kg_loss_group_fields(a->loss_ws, a->loss_ws_bytes, a->b, n, a->d, a->R, ptrs, sz, 16);
-  KG_REQUIRE(nf > 0, KG_ERR_VALIDATION, "kg_epoch_prep: loss workspace too small");
-  kg_copy_seg segs[16];
-  int64_t off = 0;
-  for (int32_t i = 0; i < nf; ++i) {
-    segs[i].dst = a->groups + off;
-    segs[i].src = ptrs[i];
-    segs[i].bytes = sz[i];
-    segs[i].dst_round_stride = a->groups_stride;
-    segs[i].src_round_stride = 0;
-    off += (int64_t)align_up((size_t)sz[i]);
+  int K = a->branches < 1 ? 1 : a->branches;
+  K = K > a->rounds ? a->rounds : K;
+  K = K > KG_PREP_MAX_BRANCHES ? KG_PREP_MAX_BRANCHES : K;
+  // per-branch export lists (the branch's loss workspace -> the round's slab row)
+  kg_copy_seg segs[KG_PREP_MAX_BRANCHES][16];
+  int32_t nf = 0;
+  for (int k = 0; k < K; ++k) {
+    void* ptrs[16];
+    int64_t sz[16];
+    char* lws = static_cast<char*>(a->loss_ws) + (int64_t)k * a->loss_ws_bytes;
+    nf = kg_loss_group_fields(lws, a->loss_ws_bytes, a->b, n, a->d, a->R, ptrs, sz, 16);
+    KG_REQUIRE(nf > 0, KG_ERR_VALIDATION, "kg_epoch_prep: loss workspace too small");
+    int64_t off = 0;
+    for (int32_t i = 0; i < nf; ++i) {
+      segs[k][i].dst = a->groups + off;
+      segs[k][i].src = ptrs[i];
+      segs[k][i].bytes = sz[i];
+      segs[k][i].dst_round_stride = a->groups_stride;
+      segs[k][i].src_round_stride = 0;
+      off += (int64_t)align_up((size_t)sz[i]);
+    }
+    KG_REQUIRE(off <= a->groups_stride, KG_ERR_VALIDATION, "kg_epoch_prep: groups stride %lld < %lld",
+               (long long)a->groups_stride, (long long)off);
   }
-  KG_REQUIRE(off <= a->groups_stride, KG_ERR_VALIDATION, "kg_epoch_prep: groups stride %lld < %lld",
-             (long long)a->groups_stride, (long long)off);
+  // rounds are independent: with K > 1 they run as K parallel branches (forked
+  // from and joined back into `stream`; capture-safe), round r on branch r % K
+  cudaStream_t st = as_stream(stream), br[KG_PREP_MAX_BRANCHES];
+  static cudaStream_t aux[KG_PREP_MAX_BRANCHES] = {};
+  static cudaEvent_t ev = nullptr;
+  if (K > 1) {
+    if (!ev) {
+      int lo = 0, hi = 0;
+      KG_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+      for (int k = 0; k < KG_PREP_MAX_BRANCHES; ++k)
+        KG_CUDA(cudaStreamCreateWithPriority(&aux[k], cudaStreamNonBlocking, lo));   // lowest priority
+      KG_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+    }
+    KG_CUDA(cudaEventRecord(ev, st));
+    for (int k = 0; k < K; ++k) {
+      KG_CUDA(cudaStreamWaitEvent(aux[k], ev, 0));
+      br[k] = aux[k];
+    }
+  } else {
+    br[0] = st;
+  }
   for (int32_t r = 0; r < a->rounds; ++r) {
+    const int k = r % K;
+    void* bs = br[k];
     const int64_t start = (int64_t)r * a->b;
     int32_t* order = a->order + (int64_t)r * n;
     int32_t* counts = a->counts + (int64_t)r * L1;
+    char* cws = static_cast<char*>(a->closure_ws) + (int64_t)k * a->closure_ws_bytes;
+    char* lws = static_cast<char*>(a->loss_ws) + (int64_t)k * a->loss_ws_bytes;
     kg_status s = kg_closure(a->stream_triples, a->total, start, nullptr, a->b, nullptr, a->g, a->hops, order,
-                             a->pos + (int64_t)r * n, counts, a->closure_ws, a->closure_ws_bytes, stream);
+                             a->pos + (int64_t)r * n, counts, cws, a->closure_ws_bytes, bs);
     if (s != KG_OK) return s;
     s = kg_loss_groups(nullptr, a->d, n, nullptr, a->R, a->stream_triples, a->labels, a->total, start, nullptr,
-                       a->b, order, counts, nullptr, nullptr, nullptr, nullptr, a->flags, a->loss_ws,
-                       a->loss_ws_bytes, stream);
+                       a->b, order, counts, nullptr, nullptr, nullptr, nullptr, a->flags, lws, a->loss_ws_bytes, bs);
     if (s != KG_OK) return s;
-    s = kg_copy_segments(segs, nf, nullptr, r, stream);
+    s = kg_copy_segments(segs[k], nf, nullptr, r, bs);
     if (s != KG_OK) return s;
+  }
+  if (K > 1) {
+    for (int k = 0; k < K; ++k) {
+      KG_CUDA(cudaEventRecord(ev, aux[k]));
+      KG_CUDA(cudaStreamWaitEvent(st, ev, 0));
+    }
   }
   return KG_OK;
 }

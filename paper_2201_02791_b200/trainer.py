@@ -234,6 +234,13 @@ def _assemble_embed(pset: PartitionSet, tables: dict, base: np.ndarray) -> np.nd
 # Device engine
 # ---------------------------------------------------------------------------
 
+PREP_BRANCHES = int(os.environ.get("KG_PREP_BRANCHES", "4"))   # <= KG_PREP_MAX_BRANCHES
+
+
+def _align256(x: int) -> int:
+    return (int(x) + 255) // 256 * 256
+
+
 class _RoundPrep:
     """Batch-only per-round work of a whole epoch — the closure (order, pos,
     counts) and the loss grouping (sorted values, segment bounds) of every
@@ -255,9 +262,14 @@ class _RoundPrep:
         self.ws = _lib.Workspace(dev)
         self.flags = torch.zeros(1, **i32)
         self.loss_args = (cfg.dims[-1], v.n, cfg.num_relations)
-        nbytes = lib.kg_loss_workspace_bytes(b, v.n, cfg.dims[-1], cfg.num_relations)
-        self.prep_ws = torch.empty(nbytes, dtype=torch.uint8, device=dev)
-        self.prep_fields = self._fields(self.prep_ws)
+        # the rounds of an epoch are prepared as parallel branches, each with its
+        # own closure / loss workspaces (256-byte aligned strides)
+        self.branches = min(self.rounds, PREP_BRANCHES)
+        self.loss_stride = _align256(lib.kg_loss_workspace_bytes(b, v.n, cfg.dims[-1], cfg.num_relations))
+        self.closure_stride = _align256(lib.kg_closure_workspace_bytes(v.n))
+        self.prep_ws = torch.empty(self.branches * self.loss_stride, dtype=torch.uint8, device=dev)
+        self.closure_ws = torch.empty(self.branches * self.closure_stride, dtype=torch.uint8, device=dev)
+        self.prep_fields = self._fields(self.prep_ws[: self.loss_stride])
         self.offs, o = [], 0
         for _, nb in self.prep_fields:
             self.offs.append(o)
@@ -281,13 +293,12 @@ class _RoundPrep:
         sl = self.slabs[slot]
         w = self.w
         d, n, R = self.loss_args
-        lib = _lib.require_cuda()
-        cbuf = self.ws.get("closure", lib.kg_closure_workspace_bytes(n))
         a = _lib.KgEpochPrepArgs(ctypes.pointer(w.view.csr()), w.config.num_layers, self.rounds,
                                  ds.triples.data_ptr(), ds.labels.data_ptr(), ds.total, w.b, d, R,
                                  sl["order"].data_ptr(), sl["pos"].data_ptr(), sl["counts"].data_ptr(),
                                  sl["groups"].data_ptr(), self.blob, self.flags.data_ptr(),
-                                 cbuf.data_ptr(), cbuf.numel(), self.prep_ws.data_ptr(), self.prep_ws.numel())
+                                 self.closure_ws.data_ptr(), self.closure_stride, self.prep_ws.data_ptr(),
+                                 self.loss_stride, self.branches)
         _lib.call("kg_epoch_prep", ctypes.byref(a), _lib.stream_handle())
 
     def import_round(self, slot: int, round_dev, loss_ws) -> None:
