@@ -9,14 +9,19 @@
 //
 // The two scatters are done without atomics: the batch's relation ids and
 // endpoint ids are stable-radix-sorted once, every group is cut into
-// sub-chunks of CH rows summed by one warp each, and a second pass adds the
+// sub-chunks of CH_REL / CH_ENT rows summed by one warp each, and a second pass adds the
 // sub-chunk partials of a group in order (hub rows get many warps, fixed
 // summation order -> bitwise reproducible).
 #include "kg_common.cuh"
 
 namespace kg {
 
-constexpr int CH = 64;
+// rows per sub-chunk: relation groups (the d_decoder scatter: few, large
+// groups) use short sub-chunks for parallelism, endpoint groups (dH) longer ones
+#ifndef KG_CH_REL
+#define KG_CH_REL 16
+#endif
+constexpr int CH_REL = KG_CH_REL, CH_ENT = 64;
 
 struct LossArgs {
   const float* H;
@@ -170,14 +175,14 @@ __device__ __forceinline__ int64_t lower_bound_u32(const uint32_t* __restrict__ 
 // group g has key gkey(g) = ids ? ids[g] : g ; bounds into the sorted keys
 __global__ void k_group_bounds(const uint32_t* __restrict__ keys, int64_t n, const int32_t* __restrict__ ids,
                                const int32_t* __restrict__ ng_dev, int32_t ng_host, int32_t* __restrict__ lo,
-                               uint32_t* __restrict__ nsub) {
+                               uint32_t* __restrict__ nsub, int ch) {
   const int32_t ng = ng_dev ? *ng_dev : ng_host;
   for (int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; g < ng; g += (int64_t)gridDim.x * blockDim.x) {
     uint32_t key = ids ? (uint32_t)ids[g] : (uint32_t)g;
     int64_t a = lower_bound_u32(keys, n, key);
     int64_t e = lower_bound_u32(keys, n, key + 1);
     lo[g] = (int32_t)a;
-    nsub[g] = (uint32_t)((e - a + CH - 1) / CH);
+    nsub[g] = (uint32_t)((e - a + ch - 1) / ch);
   }
 }
 
@@ -197,14 +202,14 @@ __global__ void __launch_bounds__(256) k_sub_partials(LossArgs a, const uint32_t
                                                       const uint32_t* __restrict__ sub_start,
                                                       const uint32_t* __restrict__ total_sub,
                                                       const uint32_t* __restrict__ sgroup,
-                                                      float* __restrict__ partial) {
+                                                      float* __restrict__ partial, int ch) {
   const uint32_t S = *total_sub;
   const int lane = lane_id();
   const int warps = (gridDim.x * blockDim.x) >> 5;
   for (int64_t s = warp_uniform((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5); s < S; s += warps) {
     const int32_t g = (int32_t)__ldg(sgroup + s);   // owning group (precomputed with the bounds)
-    const int64_t r0 = lo[g] + (int64_t)(s - sub_start[g]) * CH;
-    const int64_t r1 = r0 + CH < hi[g] ? r0 + CH : hi[g];
+    const int64_t r0 = lo[g] + (int64_t)(s - sub_start[g]) * ch;
+    const int64_t r1 = r0 + ch < hi[g] ? r0 + ch : hi[g];
     float acc[SL];
 #pragma unroll
     for (int q = 0; q < SL; ++q) acc[q] = 0.f;
@@ -268,15 +273,15 @@ __global__ void __launch_bounds__(256) k_sub_partials_v4(LossArgs a, const uint3
                                                          const uint32_t* __restrict__ sub_start,
                                                          const uint32_t* __restrict__ total_sub,
                                                          const uint32_t* __restrict__ sgroup,
-                                                         float* __restrict__ partial) {
+                                                         float* __restrict__ partial, int ch) {
   const uint32_t S = *total_sub;
   const int lane = lane_id();
   const bool on = 4 * lane < a.d;
   const int warps = (gridDim.x * blockDim.x) >> 5;
   for (int64_t s = warp_uniform((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5); s < S; s += warps) {
     const int32_t g = (int32_t)__ldg(sgroup + s);   // owning group (precomputed with the bounds)
-    const int64_t r0 = lo[g] + (int64_t)(s - sub_start[g]) * CH;
-    const int64_t r1 = r0 + CH < hi[g] ? r0 + CH : hi[g];
+    const int64_t r0 = lo[g] + (int64_t)(s - sub_start[g]) * ch;
+    const int64_t r1 = r0 + ch < hi[g] ? r0 + ch : hi[g];
     float acc[4] = {0.f, 0.f, 0.f, 0.f};
     for (int64_t base = r0; base < r1; base += 32) {
       const int cnt = (int)min((int64_t)32, r1 - base);
@@ -357,17 +362,19 @@ struct SegWs {
   uint32_t* sgroup;   // group of every sub-chunk
   float* partial;
   char* scan;
+  int ch;             // rows per sub-chunk
 };
 
-static size_t seg_ws(int64_t nelem, int64_t ngroups, int d, SegWs* w, Arena& a) {
+static size_t seg_ws(int64_t nelem, int64_t ngroups, int d, int ch, SegWs* w, Arena& a) {
   SegWs s;
+  s.ch = ch;
   s.lo = a.take<int32_t>(ngroups + 1);
   s.hi = a.take<int32_t>(ngroups + 1);
   s.nsub = a.take<uint32_t>(ngroups + 1);
   s.sub_start = a.take<uint32_t>(ngroups + 1);
   s.total = a.take<uint32_t>(4);
-  s.sgroup = a.take<uint32_t>((size_t)(nelem / CH + ngroups + 1));
-  s.partial = a.take<float>((size_t)(nelem / CH + ngroups + 1) * d);
+  s.sgroup = a.take<uint32_t>((size_t)(nelem / ch + ngroups + 1));
+  s.partial = a.take<float>((size_t)(nelem / ch + ngroups + 1) * d);
   s.scan = a.take<char>(scan_workspace(ngroups + 1));
   if (w) *w = s;
   return a.used;
@@ -376,7 +383,7 @@ static size_t seg_ws(int64_t nelem, int64_t ngroups, int d, SegWs* w, Arena& a) 
 static kg_status seg_bounds(const uint32_t* keys, int64_t nelem, const int32_t* ids, const int32_t* ng_dev,
                             int32_t ng_max, SegWs& w, cudaStream_t st) {
   int gb = persistent_blocks(ng_max, 256, 8);
-  KG_LAUNCH("k_group_bounds", k_group_bounds, gb, 256, 0, st, keys, nelem, ids, ng_dev, ng_max, w.lo, w.nsub);
+  KG_LAUNCH("k_group_bounds", k_group_bounds, gb, 256, 0, st, keys, nelem, ids, ng_dev, ng_max, w.lo, w.nsub, w.ch);
   KG_LAUNCH("k_group_len", k_group_len, gb, 256, 0, st, keys, nelem, ids, ng_dev, ng_max, w.hi);
   // with a device-resident group count the caller zeroed nsub[0:ng_max] so the
   // scan sees 0 beyond *ng_dev
@@ -389,14 +396,14 @@ static kg_status seg_bounds(const uint32_t* keys, int64_t nelem, const int32_t* 
 template <int KIND>
 static kg_status seg_sums(const LossArgs& la, const uint32_t* vals, int64_t nelem, const int32_t* ids,
                           const int32_t* ng_dev, int32_t ng_max, float* out, SegWs& w, cudaStream_t st) {
-  int64_t max_sub = nelem / CH + ng_max + 1;
+  int64_t max_sub = nelem / w.ch + ng_max + 1;
   int pb = persistent_blocks(max_sub * 32, 256, 8);
   const bool v4 = la.d % 4 == 0 && la.d <= 128 && (((uintptr_t)la.H | (uintptr_t)la.dec) & 15) == 0;
-  if (v4) KG_LAUNCH("k_sub_partials", (k_sub_partials_v4<KIND>), pb, 256, 0, st, la, vals, w.lo, w.hi, w.sub_start, w.total, w.sgroup, w.partial);
-  else if (la.d <= 32) KG_LAUNCH("k_sub_partials", (k_sub_partials<KIND, 1>), pb, 256, 0, st, la, vals, w.lo, w.hi, w.sub_start, w.total, w.sgroup, w.partial);
-  else if (la.d <= 64) KG_LAUNCH("k_sub_partials", (k_sub_partials<KIND, 2>), pb, 256, 0, st, la, vals, w.lo, w.hi, w.sub_start, w.total, w.sgroup, w.partial);
-  else if (la.d <= 128) KG_LAUNCH("k_sub_partials", (k_sub_partials<KIND, 4>), pb, 256, 0, st, la, vals, w.lo, w.hi, w.sub_start, w.total, w.sgroup, w.partial);
-  else if (la.d <= 256) KG_LAUNCH("k_sub_partials", (k_sub_partials<KIND, 8>), pb, 256, 0, st, la, vals, w.lo, w.hi, w.sub_start, w.total, w.sgroup, w.partial);
+  if (v4) KG_LAUNCH("k_sub_partials", (k_sub_partials_v4<KIND>), pb, 256, 0, st, la, vals, w.lo, w.hi, w.sub_start, w.total, w.sgroup, w.partial, w.ch);
+  else if (la.d <= 32) KG_LAUNCH("k_sub_partials", (k_sub_partials<KIND, 1>), pb, 256, 0, st, la, vals, w.lo, w.hi, w.sub_start, w.total, w.sgroup, w.partial, w.ch);
+  else if (la.d <= 64) KG_LAUNCH("k_sub_partials", (k_sub_partials<KIND, 2>), pb, 256, 0, st, la, vals, w.lo, w.hi, w.sub_start, w.total, w.sgroup, w.partial, w.ch);
+  else if (la.d <= 128) KG_LAUNCH("k_sub_partials", (k_sub_partials<KIND, 4>), pb, 256, 0, st, la, vals, w.lo, w.hi, w.sub_start, w.total, w.sgroup, w.partial, w.ch);
+  else if (la.d <= 256) KG_LAUNCH("k_sub_partials", (k_sub_partials<KIND, 8>), pb, 256, 0, st, la, vals, w.lo, w.hi, w.sub_start, w.total, w.sgroup, w.partial, w.ch);
   else KG_REQUIRE(false, KG_ERR_SHAPE, "embedding width %d > 256 unsupported", la.d);
   KG_LAUNCH("k_group_finish", k_group_finish, persistent_blocks((int64_t)ng_max * la.d, 256, 8), 256, 0, st, w.partial, w.sub_start, w.nsub,
                                                                                    ids, ng_dev, ng_max, la.d, out);
@@ -440,8 +447,8 @@ static size_t loss_arena(void* ws, size_t bytes, int64_t b, int32_t n_local, int
   w.vk = a.take<uint32_t>(2 * b);
   w.vv = a.take<uint32_t>(2 * b);
   w.sws = a.take<char>(sort32_workspace(2 * b));
-  seg_ws(b, R, d, &w.wr, a);
-  seg_ws(2 * b, w.ngmax, d, &w.wv, a);
+  seg_ws(b, R, d, CH_REL, &w.wr, a);
+  seg_ws(2 * b, w.ngmax, d, CH_ENT, &w.wv, a);
   if (L) *L = w;
   return a.used + 4096;
 }
@@ -497,7 +504,7 @@ int32_t kg_loss_group_fields(void* ws, int64_t ws_bytes, int64_t b, int32_t n_lo
   LossWs w;
   if (loss_arena(ws, (size_t)ws_bytes, b, n_local, d, R, &w) > (size_t)ws_bytes) return -1;
   const int64_t nr = (int64_t)R + 1, nv = w.ngmax + 1;
-  const int64_t sr = b / CH + R + 1, sv = 2 * b / CH + w.ngmax + 1;   // sub-chunk capacities (seg_ws)
+  const int64_t sr = b / CH_REL + R + 1, sv = 2 * b / CH_ENT + w.ngmax + 1;   // sub-chunk capacities (seg_ws)
   void* p[] = {w.rv, w.vv, w.wr.lo, w.wr.hi, w.wr.nsub, w.wr.sub_start, w.wr.total, w.wr.sgroup,
                w.wv.lo, w.wv.hi, w.wv.nsub, w.wv.sub_start, w.wv.total, w.wv.sgroup};
   const int64_t sz[] = {4 * b, 8 * b, 4 * nr, 4 * nr, 4 * nr, 4 * nr, 16, 4 * sr,
