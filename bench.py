@@ -204,6 +204,7 @@ def run_ours(args, world, rank, local):
 
     for _ in range(max(args.warmup, 3)):
         step()
+    tr.prepare()          # remaining one-time captures (train() overlaps them with device work)
     torch.cuda.synchronize()
     tr.check()
 

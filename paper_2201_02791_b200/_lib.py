@@ -189,12 +189,18 @@ def ptr(t) -> int:
     return 0 if t is None else t.data_ptr()
 
 
+CAPTURE_TIMES = os.environ.get("KG_CAPTURE_TIMES", "0") == "1"   # diagnostics
+capture_times: list = []   # (begin, body, end+instantiate, upload) ms per capture
+
+
 def capture(graph, body, pool=None) -> None:
     """Capture body() into `graph` on the current stream and upload it.
     The cyclic garbage collector is held off while capturing: it could
     otherwise destroy an unreachable earlier trainer's CUDA graphs or events
     mid-capture, which invalidates the capture."""
     import gc
+    import time
+    t0 = time.perf_counter()
     enabled = gc.isenabled()
     gc.disable()
     try:
@@ -202,14 +208,20 @@ def capture(graph, body, pool=None) -> None:
             graph.capture_begin()
         else:
             graph.capture_begin(pool=pool)
+        t1 = time.perf_counter()
         try:
             body()
         finally:
+            t2 = time.perf_counter()
             graph.capture_end()
     finally:
         if enabled:
             gc.enable()
+    t3 = time.perf_counter()
     graph_upload(graph)
+    if CAPTURE_TIMES:
+        capture_times.append((round((t1 - t0) * 1e3, 2), round((t2 - t1) * 1e3, 2), round((t3 - t2) * 1e3, 2),
+                              round((time.perf_counter() - t3) * 1e3, 2)))
 
 
 def graph_upload(graph) -> None:

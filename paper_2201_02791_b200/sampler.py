@@ -594,11 +594,14 @@ class EpochSampler:
         self.parity = 0   # slot of the next epoch handed out
         self._prep = prep
         # one CUDA graph per slot holds the whole epoch pipeline (negatives,
-        # shuffle, gather, round prep): an epoch boundary costs one replay
-        for k in range(self.NSLOTS):
-            self._capture(k)
-        for k in range(self.NSLOTS - 1):
-            self._enqueue(k)
+        # shuffle, gather, round prep): an epoch boundary costs one replay.
+        # Slot 0 is captured and started now; the others are captured and
+        # started by prefetch() (called while the device runs queued rounds,
+        # so their host-side capture cost overlaps device work) or, at the
+        # latest, when next() needs them. Slots always start in epoch order
+        # (the device RNG stream is consumed in that order).
+        self.filled = [False] * self.NSLOTS
+        self._fill(0)
 
     def slot_of(self, ds) -> int:
         for i, slot in enumerate(self.slots):
@@ -636,6 +639,22 @@ class EpochSampler:
         slot["graph"] = g
         slot["stream"] = self.slot_stream(parity)
 
+    def _fill(self, k):
+        if self.slots[k]["graph"] is None:
+            self._capture(k)
+        self._enqueue(k)
+        self.filled[k] = True
+
+    def prefetch(self) -> bool:
+        """Start the earliest epoch slot that should be in flight but is not
+        (at most one per call); True if one was started."""
+        for i in range(self.NSLOTS - 1):
+            k = (self.parity + i) % self.NSLOTS
+            if not self.filled[k]:
+                self._fill(k)
+                return True
+        return False
+
     def _enqueue(self, parity):
         torch = _torch()
         slot = self.slots[parity]
@@ -660,6 +679,8 @@ class EpochSampler:
         the epoch after that."""
         torch = _torch()
         slot = self.slots[self.parity]
+        if not self.filled[self.parity]:
+            self._fill(self.parity)
         slot["ready"].synchronize()
         k_left, min_consumed, perm_consumed = (int(x) for x in slot["host"].tolist())
         if k_left > 0 or min_consumed < 0 or perm_consumed < 0:
@@ -672,8 +693,17 @@ class EpochSampler:
         other = self.slots[free]
         other["released"] = torch.cuda.Event()
         other["released"].record(torch.cuda.current_stream())
+        self.filled[self.parity] = False
         self.parity = (self.parity + 1) % self.NSLOTS
-        self._enqueue(free)
+        # start the slots ahead in epoch order; a slot not captured yet is left
+        # to prefetch() (it also catches up any gap)
+        for i in range(self.NSLOTS - 1):
+            k = (self.parity + i) % self.NSLOTS
+            if not self.filled[k]:
+                if self.slots[k]["graph"] is None:
+                    break
+                self._enqueue(k)
+                self.filled[k] = True
         return out
 
     def _redo(self, slot):

@@ -599,9 +599,9 @@ class Trainer:
                 self._update_body()
                 self._eager_rounds += 1
             else:
-                if not self._graphs:
-                    self._capture_all()
                 key = tuple(w.stream.triples.data_ptr() for w in self.workers)
+                if key not in self._graphs:
+                    self._capture_slot(self.workers[0].slot())
                 gc, gu, nk = self._graphs[key]
                 self.last_timer_handle = self._timer_handles.get(key)
                 gc.replay()
@@ -612,6 +612,8 @@ class Trainer:
         cur.wait_stream(self._prio)
         self.t += 1
         self.round_in_epoch += 1
+        if self.round_in_epoch == 1:
+            self.prefetch()    # the epoch's first round is queued: capture work ahead now
 
     def _capture(self, body, graph):
         torch = _torch()
@@ -621,39 +623,65 @@ class Trainer:
             _lib.capture(graph, body, self._graph_pool)
         torch.cuda.current_stream().wait_stream(side)
 
-    def _capture_all(self):
-        """Capture the compute and update halves of a round for both epoch
-        buffer slots of the samplers (pointers are fixed per slot)."""
+    def _capture_slot(self, slot: int):
+        """Capture the compute and update halves of a round for one epoch
+        buffer slot of the samplers (pointers are fixed per slot)."""
         torch = _torch()
         lib = _lib.require_cuda()
         if self._graph_pool is None:
             self._graph_pool = torch.cuda.graph_pool_handle()
         current = [w.stream for w in self.workers]
-        for slot in range(EpochSampler.NSLOTS):
-            for w in self.workers:
-                w.stream = w.sampler.slot_stream(slot)
-            key = tuple(w.stream.triples.data_ptr() for w in self.workers)
-            gc, gu = torch.cuda.CUDAGraph(), torch.cuda.CUDAGraph()
-            n0 = lib.kg_launch_count()
-            if self.timer_prefix:
-                lib.kg_kernel_timer_begin(self.timer_prefix.encode())
-            self._capture(self._compute_body, gc)
-            if self.timer_prefix:
-                h = ctypes.c_int64(-1)
-                lib.kg_kernel_timer_detach(ctypes.byref(h))
-                self._timer_handles[key] = h.value
-            self._capture(self._update_body, gu)
-            self._graphs[key] = (gc, gu, lib.kg_launch_count() - n0)
+        for w in self.workers:
+            w.stream = w.sampler.slot_stream(slot)
+        key = tuple(w.stream.triples.data_ptr() for w in self.workers)
+        gc, gu = torch.cuda.CUDAGraph(), torch.cuda.CUDAGraph()
+        n0 = lib.kg_launch_count()
+        if self.timer_prefix:
+            lib.kg_kernel_timer_begin(self.timer_prefix.encode())
+        self._capture(self._compute_body, gc)
+        if self.timer_prefix:
+            h = ctypes.c_int64(-1)
+            lib.kg_kernel_timer_detach(ctypes.byref(h))
+            self._timer_handles[key] = h.value
+        self._capture(self._update_body, gu)
+        self._graphs[key] = (gc, gu, lib.kg_launch_count() - n0)
         for w, st in zip(self.workers, current):
             w.stream = st
 
+    def prefetch(self) -> bool:
+        """Host-side preparation of upcoming epochs (sampler epoch graphs,
+        round graphs of a slot not captured yet), one item per call; meant
+        for moments when the device has queued rounds to run. True if it did
+        something."""
+        for w in self.workers:
+            if w.sampler.prefetch():
+                return True
+        if self.use_graphs and self._eager_rounds >= 2:
+            for slot in range(EpochSampler.NSLOTS):
+                key = tuple(w.sampler.slot_stream(slot).triples.data_ptr() for w in self.workers)
+                if key not in self._graphs:
+                    self._capture_slot(slot)
+                    return True
+        return False
+
+    def prepare(self) -> None:
+        """Do all pending one-time host work now (epoch graphs of the slots
+        ahead, round graphs of every slot): for benchmarks, so the timed steps
+        are steady state."""
+        while self.prefetch():
+            pass
+
     def close(self):
-        """Release the captured CUDA graphs now (the trainer and its samplers
-        reference each other, so they would otherwise wait for the cyclic GC)."""
+        """Release the captured CUDA graphs now and break the worker <->
+        sampler <-> round-prep reference cycle, so the device buffers go back
+        to the caching allocator as soon as the trainer is dropped (instead of
+        whenever the cyclic GC runs; a following train() then reuses them)."""
         _torch().cuda.synchronize()
         self._graphs.clear()
         for w in self.workers:
             w.sampler.close()
+            w.sampler._prep = None
+            w.prep.w = None
 
     def _gather(self):
         gather_partition_payloads(self.grads_local, self.P, self.world, self.grads_all, self._recv, self._gidx)
@@ -773,6 +801,7 @@ def train(pset: PartitionSet, graph, model_config: ModelConfig, train_config: Tr
         for _ in range(tr.rounds):
             tr.run_round()
         pending.append((epoch, tr.end_epoch()))
+        tr.prefetch()      # host-side capture work while the device runs this epoch
         while len(pending) > 1 or (pending and pending[-1][0] in eval_epochs):
             settle()
     while pending:

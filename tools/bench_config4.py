@@ -78,6 +78,7 @@ tr.fork_streams = True
 tr.use_graphs = True
 for _ in range(3):
     step()
+tr.prepare()
 torch.cuda.synchronize()
 e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
 e0.record()

@@ -28,6 +28,7 @@ def main():
     ap.add_argument("--repeats", type=int, default=5)
     ap.add_argument("--rounds", type=int, default=180)
     ap.add_argument("--profile", action="store_true")
+    ap.add_argument("--gc", action="store_true", help="gc.collect() before every call")
     a = ap.parse_args()
     graph, split, pset, mc, tc = bench.build_inputs(1, bench.BATCH)
     tr = kb.Trainer(pset, graph, mc, tc)
@@ -35,7 +36,10 @@ def main():
     del tr
     for i in range(a.repeats):
         tc2 = kb.TrainConfig(epochs=epochs, batch_size=bench.BATCH, optimizer="adam", learning_rate=0.01, seed=0)
-        prof = cProfile.Profile() if (a.profile and i == a.repeats - 1) else None
+        prof = cProfile.Profile() if a.profile else None
+        if a.gc:
+            import gc
+            gc.collect()
         torch.cuda.synchronize()
         t0 = time.perf_counter()
         if prof:
@@ -50,8 +54,16 @@ def main():
               f"(first {ep[0]*1e3:.2f}, median {sorted(ep)[len(ep)//2]*1e3:.2f}, max {max(ep)*1e3:.2f}) "
               f"finish {rep.finish_seconds*1e3:.1f} -> {epochs*tr_rounds(rep)*bench.BATCH/wall/1e6:.1f} M/s",
               flush=True)
-        if prof:
-            pstats.Stats(prof).sort_stats("cumulative").print_stats(40)
+        from paper_2201_02791_b200 import _lib as libm
+        if libm.capture_times:
+            print("   captures (begin, body, end, upload ms):", libm.capture_times, flush=True)
+            libm.capture_times.clear()
+        from paper_2201_02791_b200 import trainer as trm
+        if trm.setup_marks:
+            m = trm.setup_marks
+            print("   setup marks:", [(b[0], round((b[1] - a[1]) * 1e3, 1)) for a, b in zip(m, m[1:])], flush=True)
+        if prof and wall > 0.2:
+            pstats.Stats(prof).sort_stats("tottime").print_stats(15)
 
 
 def tr_rounds(rep):

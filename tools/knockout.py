@@ -29,6 +29,7 @@ def main(steps=40, warmup=5, reps=3):
 
     for _ in range(warmup):
         step()
+    tr.prepare()
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda")
     best = []
     for _ in range(reps):
