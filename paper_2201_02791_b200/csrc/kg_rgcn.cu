@@ -1076,18 +1076,7 @@ kg_status kg_rgcn_backward(const kg_graph_csr* G, const kg_layer_params* lp, con
   // side stream concurrently; dV follows dS on the side stream.
   cudaStream_t sd = st;
   const int split = dcoeff_split(G->e, lp->G);
-  static const bool fused = getenv("KG_CSC_FUSED") && getenv("KG_CSC_FUSED")[0] == '1';
-  if (side_stream && fused) {
-    s = run_csc(c, G, st, 0);
-    if (s != KG_OK) return s;
-    sd = as_stream(side_stream);
-    KG_CUDA(cudaEventRecord(fork_event(), st));
-    KG_CUDA(cudaStreamWaitEvent(sd, fork_event(), 0));
-    KG_LAUNCH("k_dcoeff_reduce", k_dcoeff_partial, dim3((unsigned)lp->G, (unsigned)split, 1), 256, 0, sd,
-              G->rel_ptr, G->rel_perm, counts, t, w.ed, w.ed_self, lp->G, B, w.dc_part);
-    KG_LAUNCH("k_dcoeff_final", k_dcoeff_final, persistent_blocks((int64_t)lp->G * B, 256, 2), 256, 0, sd,
-              w.dc_part, lp->G, B, split, d_coeffs);
-  } else if (side_stream) {
+  if (side_stream) {
     sd = as_stream(side_stream);
     KG_CUDA(cudaEventRecord(fork_event(), st));
     KG_CUDA(cudaStreamWaitEvent(sd, fork_event(), 0));

@@ -259,7 +259,6 @@ class _RoundPrep:
         self.slabs = [dict(order=torch.empty((self.rounds, self.n), **i32), pos=torch.empty((self.rounds, self.n), **i32),
                            counts=torch.zeros((self.rounds, self.L1), **i32))
                       for _ in range(EpochSampler.NSLOTS)]
-        self.ws = _lib.Workspace(dev)
         self.flags = torch.zeros(1, **i32)
         self.loss_args = (cfg.dims[-1], v.n, cfg.num_relations)
         # the rounds of an epoch are prepared as parallel branches, each with its
