@@ -354,10 +354,10 @@ struct CscArgs {
 // MODE 0: dS and edge dots in one pass. MODE 1: dS only (the critical path:
 // dX = dS . Wb feeds the next layer). MODE 2: edge dots + self dots only (they
 // feed only d coeffs, so this pass runs on the forked stream).
-// EPI > 1 (MODE 1 only, narrow rows): message groups as in k_aggregate.
+// EPI > 1 (narrow rows): message groups as in k_aggregate; the edge dots
+// then reduce within a lane group (log2(LPR) shuffles per message).
 template <int NB, int VEC, int S, int MODE, int EPI>
 __global__ void __launch_bounds__(256, KG_GATHER_BPS) k_csc_backward(CscArgs a) {
-  static_assert(EPI == 1 || MODE == 1, "message groups only in the dS-only pass");
   extern __shared__ float coef[];
   for (int i = threadIdx.x; i < a.G * a.B; i += blockDim.x) coef[i] = a.coeffs[i];
   __syncthreads();
@@ -422,7 +422,7 @@ __global__ void __launch_bounds__(256, KG_GATHER_BPS) k_csc_backward(CscArgs a) 
         if (b < B)
 #pragma unroll
           for (int s = 0; s < S; ++s)
-            if (slot_ok[s]) VecIO<VEC>::load(a.Y + ((int64_t)q * B + b) * d + (s * 32 + lane) * VEC, y[b][s]);
+            if (slot_ok[s]) VecIO<VEC>::load(a.Y + ((int64_t)q * B + b) * d + (s * LPR + cl) * VEC, y[b][s]);
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
       const int nh = min(32, cnt - 32 * h);
@@ -455,8 +455,28 @@ __global__ void __launch_bounds__(256, KG_GATHER_BPS) k_csc_backward(CscArgs a) 
             }
           }
         }
-        // per-edge dots <Y_b[u], dZ[dst]>: one transposed warp reduction per b
-        if (MODE != 1)
+        // per-edge dots <Y_b[u], dZ[dst]>, message groups: reduce within the group
+        if (MODE != 1 && EPI > 1)
+#pragma unroll
+        for (int b = 0; b < NB; ++b) {
+          if (b < B) {
+#pragma unroll
+            for (int k = 0; k < UNR; ++k) {
+              float dp = 0.f;
+#pragma unroll
+              for (int s = 0; s < S; ++s)
+#pragma unroll
+                for (int cc = 0; cc < VEC; ++cc) dp = fmaf(y[b][s][cc], zs[k][s][cc], dp);
+#pragma unroll
+              for (int o = 1; o < LPR; o <<= 1) dp += __shfl_xor_sync(0xffffffffu, dp, o);
+              const int e = j + k * EPI + grp;
+              const float wk = __shfl_sync(0xffffffffu, nrm[h], e & 31);
+              if (cl == 0 && e < nh) a.ed[(int64_t)(beg + 32 * h + e) * B + b] = wk * dp;
+            }
+          }
+        }
+        // per-edge dots, one message per warp load: one transposed warp reduction per b
+        if (MODE != 1 && EPI == 1)
 #pragma unroll
         for (int b = 0; b < NB; ++b) {
           if (b < B) {
@@ -484,7 +504,7 @@ __global__ void __launch_bounds__(256, KG_GATHER_BPS) k_csc_backward(CscArgs a) 
         float z[S][VEC];
 #pragma unroll
         for (int s = 0; s < S; ++s) {
-          if (slot_ok[s]) VecIO<VEC>::load(a.dZ + (int64_t)q * d + (s * 32 + lane) * VEC, z[s]);
+          if (slot_ok[s] && grp == 0) VecIO<VEC>::load(a.dZ + (int64_t)q * d + (s * LPR + cl) * VEC, z[s]);
           else
 #pragma unroll
             for (int cc = 0; cc < VEC; ++cc) z[s][cc] = 0.f;
@@ -836,9 +856,9 @@ template <int VEC, int S, int EPI = 1>
 static kg_status launch_csc(const CscArgs& a0, int blocks, int cblocks, size_t smem, cudaStream_t st, int mode) {
   CscArgs a = a0;
   a.self_dots = mode == 0;
-  kg_status s = mode == 0 ? launch_csc_mode<VEC, S, 0>(a, blocks, smem, st)
+  kg_status s = mode == 0 ? launch_csc_mode<VEC, S, 0, EPI>(a, blocks, smem, st)
               : mode == 1 ? launch_csc_mode<VEC, S, 1, EPI>(a, blocks, smem, st)
-                          : launch_csc_mode<VEC, S, 2>(a, blocks, smem, st);
+                          : launch_csc_mode<VEC, S, 2, EPI>(a, blocks, smem, st);
   if (s != KG_OK || mode == 2) return s;
   if (a.d % 4 == 0) KG_LAUNCH("k_csc_combine", k_csc_combine<true>, cblocks, CB_THREADS, 0, st, a);
   else KG_LAUNCH("k_csc_combine", k_csc_combine<false>, cblocks, CB_THREADS, 0, st, a);
@@ -880,10 +900,8 @@ static kg_status run_csc(const CscArgs& a, const kg_graph_csr* G, cudaStream_t s
   size_t smem = (size_t)a.G * a.B * sizeof(float);
   // narrow rows: the dS-only pass gathers several messages per warp load
   const bool al16 = ((uintptr_t)a.dZ & 15) == 0 && ((uintptr_t)a.Y & 15) == 0;
-  // (the dot passes keep one message per warp load: their per-message warp
-  // reductions want every lane busy)
-  if (mode == 1 && a.d % 4 == 0 && a.d <= 32 && al16) return launch_csc<4, 1, 4>(a, blocks, cblocks, smem, st, mode);
-  if (mode == 1 && a.d % 4 == 0 && a.d <= 64 && al16) return launch_csc<4, 1, 2>(a, blocks, cblocks, smem, st, mode);
+  if (a.d % 4 == 0 && a.d <= 32 && al16) return launch_csc<4, 1, 4>(a, blocks, cblocks, smem, st, mode);
+  if (a.d % 4 == 0 && a.d <= 64 && al16) return launch_csc<4, 1, 2>(a, blocks, cblocks, smem, st, mode);
   return dispatch_width(
       a.d, [&] { return launch_csc<4, 1>(a, blocks, cblocks, smem, st, mode); },
       [&] { return launch_csc<1, 1>(a, blocks, cblocks, smem, st, mode); },
