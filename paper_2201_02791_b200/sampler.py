@@ -592,6 +592,7 @@ class EpochSampler:
                 status=torch.zeros(3, dtype=torch.int64, device=self.dev),
                 host=torch.zeros(3, dtype=torch.int64, pin_memory=True), stream=None, graph=None))
         self.parity = 0   # slot of the next epoch handed out
+        self.redos = 0    # epochs re-run synchronously (status words flagged a short window)
         self._prep = prep
         # one CUDA graph per slot holds the whole epoch pipeline (negatives,
         # shuffle, gather, round prep): an epoch boundary costs one replay.
@@ -685,6 +686,13 @@ class EpochSampler:
         k_left, min_consumed, perm_consumed = (int(x) for x in slot["host"].tolist())
         if k_left > 0 or min_consumed < 0 or perm_consumed < 0:
             self._redo(slot)
+            # epochs already started behind this one drew from the device RNG
+            # state this epoch left when it stopped short: run them again, in
+            # order, from the state the re-run leaves (nothing consumed them yet)
+            for i in range(1, self.NSLOTS):
+                k = (self.parity + i) % self.NSLOTS
+                if self.filled[k]:
+                    self._enqueue(k)
         torch.cuda.current_stream().wait_event(slot["ready"])
         out = slot["stream"]
         # the previous epoch's slot (all its compute is enqueued by now) is
@@ -709,6 +717,7 @@ class EpochSampler:
     def _redo(self, slot):
         """Synchronous, host-checked re-run of one epoch from its start state."""
         torch = _torch()
+        self.redos += 1
         with torch.cuda.stream(self.side):
             self.g.copy_(slot["g_start"])
             if slot["neg"] is not None:

@@ -113,9 +113,14 @@ def test_permutation_bit_exact(n, seed):
     assert gen.bit_generator.state == ref.bit_generator.state
 
 
-def test_epoch_sampler_matches_reference_streams():
+@pytest.mark.parametrize("async_rounds", [3, 1])
+def test_epoch_sampler_matches_reference_streams(monkeypatch, async_rounds):
     """The async side-stream epoch pipeline reproduces the reference's
-    per-epoch draws (negatives, then permutation) epoch after epoch."""
+    per-epoch draws (negatives, then permutation) epoch after epoch; with a
+    single captured resampling round the pending negatives force the
+    synchronous re-run path, which must give the same streams."""
+    from paper_2201_02791_b200.sampler import EpochSampler as _ES
+    monkeypatch.setattr(_ES, "ASYNC_ROUNDS", async_rounds)
     g = load_golden("synth_p4")
     graph, pset, cfg = golden_pset(g)
     v = kb.build_view(pset.partitions[0], graph.num_entities, graph.num_relations)
@@ -133,6 +138,8 @@ def test_epoch_sampler_matches_reference_streams():
         torch.cuda.synchronize()
         np.testing.assert_array_equal(ds.triples.cpu().numpy()[: ds.total], want.triples)
         np.testing.assert_array_equal(ds.labels.cpu().numpy()[: ds.total], want.labels)
+    if async_rounds == 1:
+        assert es.redos > 0
 
 
 @pytest.mark.parametrize("name", SCEN)
@@ -413,3 +420,24 @@ def test_train_raises_on_non_finite(monkeypatch, graphs):
     tc = kb.TrainConfig(epochs=4, batch_size=96, seed=2, optimizer="sgd", learning_rate=1e38)
     with pytest.raises(kb.NumericError):
         kb.train(pset, graph, mc, tc, initial_params=golden_params(g, "init_", L))
+
+
+def test_training_with_sampler_reruns_is_bitwise_identical(monkeypatch):
+    """Epochs whose captured sampling left negatives pending are re-run
+    synchronously (with their round prep); training must not notice."""
+    from paper_2201_02791_b200.sampler import EpochSampler as _ES
+    g = load_golden("synth_p4")
+    graph, pset, cfg = golden_pset(g)
+    L = len(cfg["dims"]) - 1
+    mc = kb.ModelConfig(L, cfg["dims"], cfg["num_bases"], graph.num_relations, 1, mode="embedding")
+    tc = kb.TrainConfig(epochs=24, batch_size=96, seed=3)
+    p0 = golden_params(g, "init_", L)
+    out = []
+    for rounds in (3, 1):
+        monkeypatch.setattr(_ES, "ASYNC_ROUNDS", rounds)
+        out.append(kb.train(pset, graph, mc, tc, initial_params=p0))
+    (pa, ra), (pb, rb) = out
+    assert ra.loss_curve == rb.loss_curve
+    for x, y in zip(pa.dense_blocks(), pb.dense_blocks()):
+        np.testing.assert_array_equal(x, y)
+    np.testing.assert_array_equal(pa.entity_embed, pb.entity_embed)
