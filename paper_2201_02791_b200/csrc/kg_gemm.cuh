@@ -28,11 +28,21 @@ struct GemmArgs {
 // --- packed tensor-core operand records (kg_umma.cu) -----------------------
 // An operand with 128-row blocks is stored as records (block, kc) of 16 K
 // values: [hi | lo] halves of 128 x 16 fp32 (tf32-valued) in the K-major
-// no-swizzle canonical layout. Producers that can emit this layout directly
-// (k_aggregate) save the separate pack pass.
+// 64-byte-swizzle canonical UMMA layout: 8-row groups of 512 B, each row's 16
+// K values in 64 contiguous bytes whose 16-byte chunks are XOR-permuted by
+// (row >> 1) & 3. A row's piece of a record is two whole 32-byte sectors, so a
+// row-at-a-time producer (k_aggregate, the dS pass) writes complete sectors
+// even when the operand spills past L2 (the no-swizzle layout interleaves 8
+// rows at 16 B and cost DRAM read-modify-writes there). Producers that emit
+// this layout directly save the separate pack pass.
 constexpr int PK_ROWS = 128;
 constexpr int PK_K = 16;
 constexpr int64_t PK_REC = 2 * PK_ROWS * PK_K;   // floats per record
+
+// float offset of element (r, k), k < PK_K, inside a record half (any row count)
+__host__ __device__ __forceinline__ int pk_off(int r, int k) {
+  return (r >> 3) * 128 + (r & 7) * 16 + ((((k >> 2) ^ (r >> 1)) & 3) << 2) + (k & 3);
+}
 
 inline int64_t packed_records(int64_t K) { return (K + PK_K - 1) / PK_K; }
 inline size_t packed_bytes(int64_t rows, int64_t K) {
@@ -51,7 +61,7 @@ __device__ __forceinline__ void split_tf32(float x, float& hi, float& lo) {
 __device__ __forceinline__ float* packed_at(float* P, int64_t nk, int64_t row, int k) {
   const int r = (int)(row & (PK_ROWS - 1)), kk = k & (PK_K - 1);
   const int64_t rec = (row / PK_ROWS) * nk + (k / PK_K);
-  return P + rec * PK_REC + ((kk >> 2) * (PK_ROWS / 8) + (r >> 3)) * 32 + (r & 7) * 4 + (kk & 3);
+  return P + rec * PK_REC + pk_off(r, kk);
 }
 
 // V consecutive values starting at k (k % V == 0, V in {1, 2, 4})

@@ -35,23 +35,27 @@ constexpr size_t USMEM_CAP = 200 * 1024;
 
 __host__ __device__ inline int pad16(int n) { return (n + 15) / 16 * 16; }
 
-// byte offset of element (r, k) inside an R-row record half (k < UKC)
+// byte offset of element (r, k) inside a record half (k < UKC)
 __host__ __device__ __forceinline__ uint32_t tile_off(int r, int k, int R) {
-  return (uint32_t)(((k >> 2) * (R >> 3) + (r >> 3)) * 128 + (r & 7) * 16 + (k & 3) * 4);
+  (void)R;
+  return (uint32_t)pk_off(r, k) * 4u;
 }
 // floats per record (hi + lo halves)
 __host__ __device__ inline int64_t rec_floats(int R) { return (int64_t)2 * R * UKC; }
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
 
-// K-major, no swizzle: LBO = k-group stride, SBO = 8-row-group stride (bytes)
-__device__ __forceinline__ uint64_t make_desc(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
+// K-major, 64-byte swizzle (pk_off): SBO = 512 B between 8-row groups, LBO
+// unused (16 B). Records sit at 512-byte aligned shared addresses (base offset
+// 0); the second tf32 K-step of a record starts 32 B into the swizzle atom.
+__device__ __forceinline__ uint64_t make_desc(uint32_t saddr) {
   uint64_t d = 0;
   d |= (uint64_t)((saddr >> 4) & 0x3FFF);
-  d |= (uint64_t)((lbo >> 4) & 0x3FFF) << 16;
-  d |= (uint64_t)((sbo >> 4) & 0x3FFF) << 32;
+  d |= (uint64_t)1 << 16;                       // LBO 16 B (ignored for swizzled K-major)
+  d |= (uint64_t)(512 >> 4) << 32;              // SBO
   d |= (uint64_t)1 << 46;                       // version 1 (sm_100)
-  return d;                                     // base offset 0, layout SWIZZLE_NONE
+  d |= (uint64_t)4 << 61;                       // layout SWIZZLE_64B
+  return d;
 }
 
 __device__ __forceinline__ uint32_t make_idesc(int n_pad) {
@@ -183,14 +187,15 @@ __global__ void __launch_bounds__(256) k_umma_pack(PackJob j0, PackJob j1) {
       }
     }
   } else {
-    // record (blk, kc) with kc over 16-row groups of the source: items (q, m),
-    // m fastest -> a warp reads 32 consecutive columns of 4 source rows
+    // record (blk, kc) with kc over 16-row groups of the source: a warp owns
+    // 8 MMA rows x 4 K chunks, so each store fills one 512-byte swizzle atom
+    // and each load reads 8 consecutive source columns (one sector) of a row
     const int64_t nkd = (nrows + UKC - 1) / UKC, nblk = (j.ncols + R - 1) / R;
     for (int64_t rec = blockIdx.x; rec < nblk * nkd; rec += gridDim.x) {
       const int64_t blk = rec / nkd, kc = rec - blk * nkd;
       float* out = j.out + (blk * j.nk_alloc + kc) * rec_floats(R);
       for (int i = threadIdx.x; i < R * 4; i += blockDim.x) {
-        const int q = (i >= R) + (i >= 2 * R) + (i >= 3 * R), m = i - q * R;
+        const int q = (i >> 3) & 3, m = ((i >> 5) << 3) + (i & 7);
         const int64_t col = blk * R + m, k0 = kc * UKC + 4 * q;
         float v[4] = {0.f, 0.f, 0.f, 0.f};
         if (col < j.ncols) {
@@ -312,7 +317,6 @@ __global__ void __launch_bounds__(UTHREADS, 1) k_umma_packed(PackedArgs g, int n
     if (lane == 0) {
       // MMA issuer
       const uint32_t idesc = make_idesc(np);
-      const uint32_t lbo_a = (UM / 8) * 128, lbo_b = (uint32_t)(np / 8) * 128;
       int64_t it = 0, tcount = 0;
       for (int64_t tile = tile0; tile < ntiles; tile += tstep, ++tcount) {
         const int acc = (int)(tcount & 1);
@@ -327,9 +331,9 @@ __global__ void __launch_bounds__(UTHREADS, 1) k_umma_packed(PackedArgs g, int n
           const uint32_t b_hi = a_hi + a_bytes, b_lo = b_hi + b_half;
 #pragma unroll
           for (int j = 0; j < UKC / 8; ++j) {
-            const uint32_t ka = (uint32_t)(2 * j) * lbo_a, kb = (uint32_t)(2 * j) * lbo_b;
-            const uint64_t dah = make_desc(a_hi + ka, lbo_a, 128), dal = make_desc(a_lo + ka, lbo_a, 128);
-            const uint64_t dbh = make_desc(b_hi + kb, lbo_b, 128), dbl = make_desc(b_lo + kb, lbo_b, 128);
+            const uint32_t ko = (uint32_t)j * 32u;
+            const uint64_t dah = make_desc(a_hi + ko), dal = make_desc(a_lo + ko);
+            const uint64_t dbh = make_desc(b_hi + ko), dbl = make_desc(b_lo + ko);
             mma_tf32(d, dah, dbh, idesc, (kc > 0 || j > 0) ? 1u : 0u);
             mma_tf32(d, dah, dbl, idesc, 1u);
             mma_tf32(d, dal, dbh, idesc, 1u);
@@ -680,7 +684,7 @@ __global__ void __launch_bounds__(RK_THREADS, 1) k_rank_umma(RankArgs a, const i
   } else if (warp == 1) {
     if (lane == 0) {   // MMA issuer
       const uint32_t idesc = make_idesc(128);
-      const uint32_t lbo = (128 / 8) * 128, half = 128 * UKC * 4;
+      const uint32_t half = 128 * UKC * 4;
       int64_t it = 0, jc = 0, tc = 0;
       for (int64_t tile = blockIdx.x; tile < qtiles; tile += gridDim.x, ++tc) {
         mbar_wait(smem_u32(&bar_afull), (uint32_t)(tc & 1));
@@ -698,9 +702,9 @@ __global__ void __launch_bounds__(RK_THREADS, 1) k_rank_umma(RankArgs a, const i
             const uint32_t b_hi = ring + (uint32_t)s * RK_REC, b_lo = b_hi + half;
 #pragma unroll
             for (int jj = 0; jj < UKC / 8; ++jj) {
-              const uint32_t ko = (uint32_t)(2 * jj) * lbo;
-              const uint64_t dah = make_desc(a_hi + ko, lbo, 128), dal = make_desc(a_lo + ko, lbo, 128);
-              const uint64_t dbh = make_desc(b_hi + ko, lbo, 128), dbl = make_desc(b_lo + ko, lbo, 128);
+              const uint32_t ko = (uint32_t)jj * 32u;
+              const uint64_t dah = make_desc(a_hi + ko), dal = make_desc(a_lo + ko);
+              const uint64_t dbh = make_desc(b_hi + ko), dbl = make_desc(b_lo + ko);
               mma_tf32(dt, dah, dbh, idesc, (kc > 0 || jj > 0) ? 1u : 0u);
               mma_tf32(dt, dah, dbl, idesc, 1u);
               mma_tf32(dt, dal, dbh, idesc, 1u);
