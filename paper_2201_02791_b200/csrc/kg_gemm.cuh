@@ -26,9 +26,10 @@ struct GemmArgs {
 };
 
 // --- packed tensor-core operand records (kg_umma.cu) -----------------------
-// An operand with 128-row blocks is stored as records (block, kc) of 16 K
-// values: [hi | lo] halves of 128 x 16 fp32 (tf32-valued) in the K-major
-// 64-byte-swizzle canonical UMMA layout: 8-row groups of 512 B, each row's 16
+// An operand with 128-row blocks is stored as records (block, kc) of 128 x 16
+// fp32 values in the K-major 64-byte-swizzle canonical UMMA layout (the GEMM
+// splits each staged record into tf32 hi/lo halves in shared memory, so HBM
+// carries 4 bytes per value): 8-row groups of 512 B, each row's 16
 // K values in 64 contiguous bytes whose 16-byte chunks are XOR-permuted by
 // (row >> 1) & 3. A row's piece of a record is two whole 32-byte sectors, so a
 // row-at-a-time producer (k_aggregate, the dS pass) writes complete sectors
@@ -37,7 +38,7 @@ struct GemmArgs {
 // this layout directly save the separate pack pass.
 constexpr int PK_ROWS = 128;
 constexpr int PK_K = 16;
-constexpr int64_t PK_REC = 2 * PK_ROWS * PK_K;   // floats per record
+constexpr int64_t PK_REC = PK_ROWS * PK_K;   // floats per record
 
 // float offset of element (r, k), k < PK_K, inside a record half (any row count)
 __host__ __device__ __forceinline__ int pk_off(int r, int k) {
@@ -57,7 +58,7 @@ __device__ __forceinline__ void split_tf32(float x, float& hi, float& lo) {
   lo = x - hi;
 }
 
-// hi-half float pointer of element (row, k); the lo half is at +PK_ROWS*PK_K
+// float pointer of element (row, k)
 __device__ __forceinline__ float* packed_at(float* P, int64_t nk, int64_t row, int k) {
   const int r = (int)(row & (PK_ROWS - 1)), kk = k & (PK_K - 1);
   const int64_t rec = (row / PK_ROWS) * nk + (k / PK_K);
@@ -67,29 +68,20 @@ __device__ __forceinline__ float* packed_at(float* P, int64_t nk, int64_t row, i
 // V consecutive values starting at k (k % V == 0, V in {1, 2, 4})
 template <int V>
 __device__ __forceinline__ void packed_store(float* P, int64_t nk, int64_t row, int k, const float* v) {
-  float h[V], l[V];
-#pragma unroll
-  for (int i = 0; i < V; ++i) split_tf32(v[i], h[i], l[i]);
   float* ph = packed_at(P, nk, row, k);
-  float* pl = ph + PK_ROWS * PK_K;
   if constexpr (V == 4) {
-    *reinterpret_cast<float4*>(ph) = make_float4(h[0], h[1], h[2], h[3]);
-    *reinterpret_cast<float4*>(pl) = make_float4(l[0], l[1], l[2], l[3]);
+    *reinterpret_cast<float4*>(ph) = make_float4(v[0], v[1], v[2], v[3]);
   } else if constexpr (V == 2) {
-    *reinterpret_cast<float2*>(ph) = make_float2(h[0], h[1]);
-    *reinterpret_cast<float2*>(pl) = make_float2(l[0], l[1]);
+    *reinterpret_cast<float2*>(ph) = make_float2(v[0], v[1]);
   } else {
-    *ph = h[0];
-    *pl = l[0];
+    *ph = v[0];
   }
 }
 
 // zero the K padding [K, 16*nk) of one row (lanes of a warp share the work)
 __device__ __forceinline__ void packed_zero_pad(float* P, int64_t nk, int64_t row, int K, int lane, int nlanes) {
   for (int k = K + lane; k < nk * PK_K; k += nlanes) {
-    float* ph = packed_at(P, nk, row, k);
-    ph[0] = 0.f;
-    ph[PK_ROWS * PK_K] = 0.f;
+    *packed_at(P, nk, row, k) = 0.f;
   }
 }
 #endif
@@ -102,7 +94,7 @@ kg_status simt_gemm_tn(const GemmArgs& g, float* out, void* ws, cudaStream_t st)
 kg_status reduce_splits(const float* part, int splits, int64_t count, float* out, cudaStream_t st);
 
 // tcgen05 3xTF32 kernels (kg_umma.cu): the product path. Both need a
-// workspace for the packed (hi/lo, canonical-layout) operands.
+// workspace for the packed (canonical-layout) operands.
 size_t umma_nn_workspace(int64_t M_max, int64_t K, int64_t N);
 kg_status umma_gemm_nn(const GemmArgs& g, void* ws, cudaStream_t st);
 size_t umma_tn_workspace(int64_t rows_max, int64_t K, int64_t N);

@@ -82,7 +82,7 @@ struct AggArgs {
   const int32_t* pos;
   const int32_t* counts;
   int t;
-  float* acc;            // packed hi/lo GEMM records of the (count, B*d) rows, by position
+  float* acc;            // packed GEMM records of the (count, B*d) rows, by position
   int64_t acc_nk;        // records per 128-row block (packed_records(B*d))
   float* partial;        // (split chunks, B*d)
 };
@@ -216,7 +216,7 @@ __global__ void __launch_bounds__(256, KG_GATHER_BPS) k_aggregate(AggArgs a) {
         }
       }
       if (a.acc_nk) {
-        // finished row: straight into the GEMM's packed hi/lo A records
+        // finished row: straight into the GEMM's packed A records
 #pragma unroll
         for (int b = 0; b < NB; ++b)
           if (b < B)
@@ -767,7 +767,8 @@ __global__ void k_dbases_layout(const float* __restrict__ Rm, int B, int di, int
 //   fwd  (B*d_in x d_out)  Z = acc . [V_b]      element (o, b*d_in+i)
 //   y    (d_in x B*d_out)  Y = X . [V_0|..]     element (b*d_out+o, i)
 //   dx   (B*d_out x d_in)  dX = dS . [V_b]^T    element (i, b*d_out+o)
-// each as records of R = pad16(N) rows x 16 K values (pads zero).
+// each as records of R = pad16(N) rows x 16 K values (pads zero), tf32 hi | lo
+// halves (split once here, not per GEMM tile).
 struct WeightsLayout {
   int64_t off[3], rows[3], nk[3], total;
 };
@@ -809,12 +810,11 @@ __global__ void k_pack_weights(const float* __restrict__ V, int B, int di, int d
         val = V[((int64_t)b * di + n) * dO + o];
       }
     }
-    float hi, lo;
+    float hi, lo;   // B operands stay split (hi | lo halves): reused by every tile
     split_tf32(val, hi, lo);
     float* rec = out + L.off[j] + kc * 2 * R * PK_K;
-    const int64_t off = pk_off(n, kk);
-    rec[off] = hi;
-    rec[R * PK_K + off] = lo;
+    rec[pk_off(n, kk)] = hi;
+    rec[R * PK_K + pk_off(n, kk)] = lo;
   }
 }
 

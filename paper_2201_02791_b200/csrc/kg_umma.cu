@@ -8,21 +8,26 @@
 // gradient tolerance).
 //
 // Two kernels per GEMM:
-//   k_umma_pack    high-occupancy elementwise pass: gathers the operand rows,
-//                  splits fp32 into tf32 hi/lo and writes both in the K-major
-//                  no-swizzle canonical UMMA layout (core matrices of 8 rows x
-//                  16 B), one contiguous "record" per (row block, 16-wide K
-//                  chunk). Both operands of a GEMM are packed by one launch.
+//   k_umma_pack    high-occupancy elementwise pass: gathers the operand rows
+//                  and writes them (fp32) in the K-major 64-byte-swizzle
+//                  canonical UMMA layout, one contiguous "record" per (row
+//                  block, 16-wide K chunk). Both operands of a GEMM are
+//                  packed by one launch; producers that can (k_aggregate,
+//                  the GEMM epilogue, the dS pass) write records directly.
 //   k_umma_packed  warp-specialised tensor-core loop: warp 0 lane 0 streams
-//                  records into a shared-memory ring with cp.async.bulk
-//                  (mbarrier transaction counting), warp 1 lane 0 issues the
-//                  2 K-steps x 3 MMAs per record and commits them to the
-//                  slot's "empty" barrier, warps 2..5 drain the fp32
-//                  accumulator from TMEM (tcgen05.ld 32x32b) and apply ReLU /
-//                  the row scatter. Two TMEM accumulators let the epilogue of
-//                  tile i overlap the MMAs of tile i+1.
-// The earlier single-kernel variant converted in the GEMM itself and was
-// issue-latency bound at one CTA per SM (profiles/r1_v11_umma_stalls.txt).
+//                  fp32 records into a shared-memory ring with cp.async.bulk
+//                  (mbarrier transaction counting); warps 6..9 split each
+//                  staged record in place into tf32 hi + lo halves (so HBM
+//                  and L2 carry 4 bytes per operand value, not 8); warp 1
+//                  lane 0 issues the 2 K-steps x 3 MMAs per record and
+//                  commits them to the slot's "empty" barrier; warps 2..5
+//                  drain the fp32 accumulator from TMEM (tcgen05.ld 32x32b)
+//                  and apply ReLU / the row scatter. Two TMEM accumulators let
+//                  the epilogue of tile i overlap the MMAs of tile i+1.
+// The earliest variant converted row-major operands inside the GEMM with its
+// own address math and was issue-latency bound at one CTA per SM
+// (profiles/r1_v11_umma_stalls.txt); the split here is a flat elementwise
+// pass over a staged record.
 #include "kg_gemm.cuh"
 
 namespace kg {
@@ -30,7 +35,8 @@ namespace kg {
 constexpr int UM = PK_ROWS;    // MMA M (rows per tile)
 constexpr int UKC = PK_K;      // K values per record
 constexpr int UMAXS = 8;       // max ring stages
-constexpr int UTHREADS = 192;  // producer warp, MMA warp, 4 epilogue warps
+constexpr int UTHREADS = 320;  // producer warp, MMA warp, 4 epilogue warps, 4 split warps
+constexpr int USPLIT0 = 6;     // first split warp
 constexpr size_t USMEM_CAP = 200 * 1024;
 
 __host__ __device__ inline int pad16(int n) { return (n + 15) / 16 * 16; }
@@ -40,8 +46,10 @@ __host__ __device__ __forceinline__ uint32_t tile_off(int r, int k, int R) {
   (void)R;
   return (uint32_t)pk_off(r, k) * 4u;
 }
-// floats per record (hi + lo halves)
-__host__ __device__ inline int64_t rec_floats(int R) { return (int64_t)2 * R * UKC; }
+// floats per GEMM operand record in global memory (fp32)
+__host__ __device__ inline int64_t rec_floats(int R) { return (int64_t)R * UKC; }
+// floats per ranking record (tf32 hi + lo halves, split at pack time)
+__host__ __device__ inline int64_t rec_floats_split(int R) { return (int64_t)2 * R * UKC; }
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
 
@@ -142,13 +150,18 @@ struct PackJob {
   int cols_mode;
   int64_t nk_alloc;   // records per block in the layout
   float* out;
+  int split;          // 1: ranking records (hi | lo halves), 0: fp32 GEMM records
 };
 
-__device__ __forceinline__ void pack_store(float* rec, int R, int r, int q, const float* v) {
+__device__ __forceinline__ void pack_store(float* rec, int R, int r, int q, const float* v, int split) {
+  const uint32_t off = tile_off(r, 4 * q, R) >> 2;
+  if (!split) {
+    *reinterpret_cast<float4*>(rec + off) = make_float4(v[0], v[1], v[2], v[3]);
+    return;
+  }
   float h[4], l[4];
 #pragma unroll
   for (int i = 0; i < 4; ++i) split_tf32(v[i], h[i], l[i]);
-  const uint32_t off = tile_off(r, 4 * q, R) >> 2;
   *reinterpret_cast<float4*>(rec + off) = make_float4(h[0], h[1], h[2], h[3]);
   *reinterpret_cast<float4*>(rec + (int64_t)R * UKC + off) = make_float4(l[0], l[1], l[2], l[3]);
 }
@@ -167,7 +180,7 @@ __global__ void __launch_bounds__(256) k_umma_pack(PackJob j0, PackJob j1) {
     const bool vec = ((uintptr_t)j.src & 15) == 0 && (j.ld & 3) == 0;
     for (int64_t rec = blockIdx.x; rec < nrec; rec += gridDim.x) {
       const int64_t blk = rec / nk, kc = rec - blk * nk;
-      float* out = j.out + rec * rec_floats(R);
+      float* out = j.out + rec * (j.split ? rec_floats_split(R) : rec_floats(R));
       for (int i = threadIdx.x; i < R * 4; i += blockDim.x) {
         const int q = i & 3, r = i >> 2;
         const int64_t row = blk * R + r, c0 = kc * UKC + 4 * q;
@@ -183,7 +196,7 @@ __global__ void __launch_bounds__(256) k_umma_pack(PackJob j0, PackJob j1) {
               if (c0 + t < j.ncols) v[t] = __ldg(src + c0 + t);
           }
         }
-        pack_store(out, R, r, q, v);
+        pack_store(out, R, r, q, v, j.split);
       }
     }
   } else {
@@ -193,7 +206,7 @@ __global__ void __launch_bounds__(256) k_umma_pack(PackJob j0, PackJob j1) {
     const int64_t nkd = (nrows + UKC - 1) / UKC, nblk = (j.ncols + R - 1) / R;
     for (int64_t rec = blockIdx.x; rec < nblk * nkd; rec += gridDim.x) {
       const int64_t blk = rec / nkd, kc = rec - blk * nkd;
-      float* out = j.out + (blk * j.nk_alloc + kc) * rec_floats(R);
+      float* out = j.out + (blk * j.nk_alloc + kc) * (j.split ? rec_floats_split(R) : rec_floats(R));
       for (int i = threadIdx.x; i < R * 4; i += blockDim.x) {
         const int q = (i >> 3) & 3, m = ((i >> 5) << 3) + (i & 7);
         const int64_t col = blk * R + m, k0 = kc * UKC + 4 * q;
@@ -205,7 +218,7 @@ __global__ void __launch_bounds__(256) k_umma_pack(PackJob j0, PackJob j1) {
             if (k < nrows) v[t] = __ldg(j.src + (j.rowid ? (int64_t)__ldg(j.rowid + k) : k) * j.ld + col);
           }
         }
-        pack_store(out, R, m, q, v);
+        pack_store(out, R, m, q, v, j.split);
       }
     }
   }
@@ -233,13 +246,14 @@ struct PackedArgs {
   float* c_packed;        // NN: optional packed copy of the output (records by MMA row, K = np)
   int64_t c_nk;
   const float* mul;       // NN: optional per-element output scale by MMA row (ld N)
+  int b_split;            // B records already hold hi | lo halves (NN: weights, split once per step)
 };
 
 __device__ __forceinline__ uint32_t stage_bytes(int np) { return (uint32_t)((UM + np) * UKC * 2 * 4); }
 
 __global__ void __launch_bounds__(UTHREADS, 1) k_umma_packed(PackedArgs g, int nstages, uint32_t acc_cols) {
   extern __shared__ __align__(1024) uint8_t smem[];
-  __shared__ __align__(8) uint64_t bar_full[UMAXS], bar_empty[UMAXS], bar_tfull[2], bar_tempty[2];
+  __shared__ __align__(8) uint64_t bar_full[UMAXS], bar_empty[UMAXS], bar_split[UMAXS], bar_tfull[2], bar_tempty[2];
   __shared__ uint32_t tmem_base_s;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int np = g.np;
@@ -270,7 +284,8 @@ __global__ void __launch_bounds__(UTHREADS, 1) k_umma_packed(PackedArgs g, int n
   if (tile0 >= ntiles) return;
 
   const uint32_t sbase = smem_u32(smem);
-  const uint32_t sb = stage_bytes(np), a_bytes = (uint32_t)(UM * UKC * 8), b_half = (uint32_t)(np * UKC * 4);
+  const uint32_t sb = stage_bytes(np), a_half = (uint32_t)(UM * UKC * 4), b_half = (uint32_t)(np * UKC * 4);
+  const uint32_t a_bytes = 2 * a_half;
   auto full = [&](int s) { return smem_u32(&bar_full[s]); };
   auto empty = [&](int s) { return smem_u32(&bar_empty[s]); };
 
@@ -283,6 +298,7 @@ __global__ void __launch_bounds__(UTHREADS, 1) k_umma_packed(PackedArgs g, int n
     for (int s = 0; s < nstages; ++s) {
       mbar_init(full(s), 1);
       mbar_init(empty(s), 1);
+      mbar_init(smem_u32(&bar_split[s]), 4);
     }
     for (int a = 0; a < 2; ++a) {
       mbar_init(smem_u32(&bar_tfull[a]), 1);
@@ -302,14 +318,16 @@ __global__ void __launch_bounds__(UTHREADS, 1) k_umma_packed(PackedArgs g, int n
       for (int64_t tile = tile0; tile < ntiles; tile += tstep) {
         const int64_t ablk = g.tn ? blockIdx.y : tile;
         const float* arec = g.Ap + (ablk * g.a_nk_alloc + c_lo) * rec_floats(UM);
-        const float* brec = g.Bp + c_lo * rec_floats(np);
+        const int64_t brf = g.b_split ? rec_floats_split(np) : rec_floats(np);
+        const float* brec = g.Bp + c_lo * brf;
+        const uint32_t bcopy = g.b_split ? 2 * b_half : b_half;
         for (int kc = 0; kc < nk; ++kc, ++it) {
           const int s = (int)(it % nstages);
           if (it >= nstages) mbar_wait(empty(s), (uint32_t)((it / nstages - 1) & 1));
           const uint32_t dst = sbase + (uint32_t)s * sb;
-          mbar_expect_tx(full(s), sb);
-          bulk_g2s(dst, arec + (int64_t)kc * rec_floats(UM), a_bytes, full(s));
-          bulk_g2s(dst + a_bytes, brec + (int64_t)kc * rec_floats(np), 2 * b_half, full(s));
+          mbar_expect_tx(full(s), a_half + bcopy);
+          bulk_g2s(dst, arec + (int64_t)kc * rec_floats(UM), a_half, full(s));
+          bulk_g2s(dst + a_bytes, brec + (int64_t)kc * brf, bcopy, full(s));
         }
       }
     }
@@ -325,9 +343,9 @@ __global__ void __launch_bounds__(UTHREADS, 1) k_umma_packed(PackedArgs g, int n
         const uint32_t d = tmem + (uint32_t)acc * acc_cols;
         for (int kc = 0; kc < nk; ++kc, ++it) {
           const int s = (int)(it % nstages);
-          mbar_wait(full(s), (uint32_t)((it / nstages) & 1));
+          mbar_wait(smem_u32(&bar_split[s]), (uint32_t)((it / nstages) & 1));
           tc_fence_after();
-          const uint32_t a_hi = sbase + (uint32_t)s * sb, a_lo = a_hi + (uint32_t)(UM * UKC * 4);
+          const uint32_t a_hi = sbase + (uint32_t)s * sb, a_lo = a_hi + a_half;
           const uint32_t b_hi = a_hi + a_bytes, b_lo = b_hi + b_half;
 #pragma unroll
           for (int j = 0; j < UKC / 8; ++j) {
@@ -341,6 +359,38 @@ __global__ void __launch_bounds__(UTHREADS, 1) k_umma_packed(PackedArgs g, int n
           mma_commit(empty(s));   // slot reusable once these MMAs have read it
         }
         mma_commit(smem_u32(&bar_tfull[acc]));
+      }
+    }
+  } else if (warp >= USPLIT0) {
+    // split warps 6..9: each staged fp32 record becomes tf32 hi (in place) +
+    // lo (the slot's second half), x = hi + lo exactly
+    const int st = tid - USPLIT0 * 32;
+    const int na = UM * UKC / 4, nb = g.b_split ? 0 : np * UKC / 4;
+    int64_t it = 0;
+    for (int64_t tile = tile0; tile < ntiles; tile += tstep) {
+      for (int kc = 0; kc < nk; ++kc, ++it) {
+        const int s = (int)(it % nstages);
+        mbar_wait(full(s), (uint32_t)((it / nstages) & 1));
+        float* base = reinterpret_cast<float*>(smem + (size_t)s * sb);
+        float4* ah = reinterpret_cast<float4*>(base);
+        float4* al = reinterpret_cast<float4*>(base + UM * UKC);
+        float4* bh = reinterpret_cast<float4*>(base + 2 * UM * UKC);
+        float4* bl = reinterpret_cast<float4*>(base + 2 * UM * UKC + np * UKC);
+        for (int i = st; i < na + nb; i += 128) {
+          float4* h = i < na ? ah + i : bh + (i - na);
+          float4* l = i < na ? al + i : bl + (i - na);
+          const float4 x = *h;
+          float4 hi, lo;
+          split_tf32(x.x, hi.x, lo.x);
+          split_tf32(x.y, hi.y, lo.y);
+          split_tf32(x.z, hi.z, lo.z);
+          split_tf32(x.w, hi.w, lo.w);
+          *h = hi;
+          *l = lo;
+        }
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // generic writes -> tcgen05 reads
+        __syncwarp();
+        if (lane == 0) mbar_arrive(smem_u32(&bar_split[s]));
       }
     }
   } else {
@@ -439,7 +489,7 @@ static size_t nn_pack_sizes(int64_t M_max, int64_t K, int64_t N, size_t* a_bytes
   const int np = pad16((int)N);
   const int64_t nk = ceil_div(K, UKC), tiles = ceil_div(M_max > 0 ? M_max : 1, UM);
   size_t a = align_up((size_t)(tiles * nk * rec_floats(UM)) * 4);
-  size_t b = align_up((size_t)(nk * rec_floats(np)) * 4);
+  size_t b = align_up((size_t)(nk * rec_floats_split(np)) * 4);
   if (a_bytes) *a_bytes = a;
   return a + b;
 }
@@ -455,12 +505,12 @@ kg_status umma_gemm_nn(const GemmArgs& g, void* ws, cudaStream_t st) {
   nn_pack_sizes(g.M_max, g.K, g.N, &a_bytes);
   float* Ap = static_cast<float*>(ws);
   float* Bp = reinterpret_cast<float*>(static_cast<char*>(ws) + a_bytes);
-  PackJob ja{g.A, g.lda, g.a_rows, g.M_dev, g.M_dev_index, g.M, g.K, UM, 0, nk, Ap};
+  PackJob ja{g.A, g.lda, g.a_rows, g.M_dev, g.M_dev_index, g.M, g.K, UM, 0, nk, Ap, 0};
   if (g.a_packed) {   // producer already wrote the A records
     ja.src = nullptr;
     Ap = const_cast<float*>(g.a_packed);
   }
-  PackJob jb{g.B, g.ldb, nullptr, nullptr, 0, g.K, g.N, np, 1, nk, Bp};
+  PackJob jb{g.B, g.ldb, nullptr, nullptr, 0, g.K, g.N, np, 1, nk, Bp, 1};
   if (g.b_packed) {   // weights packed once per optimizer step
     jb.src = nullptr;
     Bp = const_cast<float*>(g.b_packed);
@@ -471,7 +521,7 @@ kg_status umma_gemm_nn(const GemmArgs& g, void* ws, cudaStream_t st) {
     if (s != KG_OK) return s;
   }
   PackedArgs p{};
-  p.Ap = Ap; p.Bp = Bp; p.a_nk_alloc = nk; p.np = np; p.tn = 0;
+  p.Ap = Ap; p.Bp = Bp; p.a_nk_alloc = nk; p.np = np; p.tn = 0; p.b_split = 1;
   p.M = g.M; p.M_dev = g.M_dev; p.M_dev_index = g.M_dev_index; p.nk = nk;
   p.C = g.C; p.ldc = g.ldc; p.c_rows = g.c_rows; p.N = g.N; p.out_rows = 0; p.relu = g.relu;
   p.c_packed = g.c_packed; p.c_nk = ceil_div(g.N, UKC); p.mul = g.mul;
@@ -513,9 +563,9 @@ kg_status umma_gemm_tn(const GemmArgs& g, float* out, void* ws, cudaStream_t st)
   float* Bp = reinterpret_cast<float*>(static_cast<char*>(ws) + a_bytes);
   float* part = reinterpret_cast<float*>(static_cast<char*>(ws) + a_bytes + b_bytes);
   // A^T: MMA rows = feature columns of A, k = data rows (gathered)
-  PackJob ja{g.A, g.lda, g.a_rows, g.M_dev, g.M_dev_index, g.M, g.K, UM, 1, nk_alloc, Ap};
+  PackJob ja{g.A, g.lda, g.a_rows, g.M_dev, g.M_dev_index, g.M, g.K, UM, 1, nk_alloc, Ap, 0};
   // Bm^T: MMA rows = output columns, k = data rows
-  PackJob jb{g.B, g.ldb, nullptr, g.M_dev, g.M_dev_index, g.M, g.N, np, 1, nk_alloc, Bp};
+  PackJob jb{g.B, g.ldb, nullptr, g.M_dev, g.M_dev_index, g.M, g.N, np, 1, nk_alloc, Bp, 0};
   const int64_t items = (blocks * UM > np ? blocks * UM : np) * nk_alloc * 4;
   kg_status s = launch_pack(ja, jb, items, st);
   if (s != KG_OK) return s;
@@ -620,8 +670,8 @@ __global__ void __launch_bounds__(256) k_eval_pack(const float* __restrict__ H, 
         }
       }
     }
-    pack_store(Qp + (blk * nk + kc) * rec_floats(128), 128, r, q4, vq);
-    pack_store(Tp + (blk * nk + kc) * rec_floats(128), 128, r, q4, vt);
+    pack_store(Qp + (blk * nk + kc) * rec_floats_split(128), 128, r, q4, vq, 1);
+    pack_store(Tp + (blk * nk + kc) * rec_floats_split(128), 128, r, q4, vt, 1);
   }
 }
 
@@ -638,7 +688,7 @@ __global__ void __launch_bounds__(RK_THREADS, 1) k_rank_umma(RankArgs a, const i
   const uint32_t sbase = smem_u32(smem), ring = sbase + (uint32_t)nk * RK_REC;
   auto full = [&](int s) { return smem_u32(&bar_full[s]); };
   auto empty = [&](int s) { return smem_u32(&bar_empty[s]); };
-  const int64_t RF = rec_floats(128);
+  const int64_t RF = rec_floats_split(128);
 
   if (warp == 0) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&tmem_base_s)),
@@ -870,11 +920,11 @@ static size_t rank_ws(int64_t nq, int32_t N, int d, int64_t max_pairs, RankWs* w
   Arena a(base, cap);
   const int64_t nk = ceil_div(d, UKC), qt = ceil_div(2 * nq, 128), cb = ceil_div(N, 128), pt = ceil_div(max_pairs, 128);
   RankWs r;
-  r.Qp = a.take<float>((size_t)(qt * nk * rec_floats(128)));
-  r.Tp = a.take<float>((size_t)(qt * nk * rec_floats(128)));
-  r.Cp = a.take<float>((size_t)(cb * nk * rec_floats(128)));
-  r.Pq = a.take<float>((size_t)((pt > 0 ? pt : 1) * nk * rec_floats(128)));
-  r.Pc = a.take<float>((size_t)((pt > 0 ? pt : 1) * nk * rec_floats(128)));
+  r.Qp = a.take<float>((size_t)(qt * nk * rec_floats_split(128)));
+  r.Tp = a.take<float>((size_t)(qt * nk * rec_floats_split(128)));
+  r.Cp = a.take<float>((size_t)(cb * nk * rec_floats_split(128)));
+  r.Pq = a.take<float>((size_t)((pt > 0 ? pt : 1) * nk * rec_floats_split(128)));
+  r.Pc = a.take<float>((size_t)((pt > 0 ? pt : 1) * nk * rec_floats_split(128)));
   r.ts = a.take<float>(2 * nq);
   r.ps = a.take<float>(max_pairs > 0 ? max_pairs : 1);
   r.greater = a.take<uint32_t>(2 * nq);
@@ -923,7 +973,7 @@ kg_status umma_rank_filtered(const float* H, int d, int32_t N, const float* dec,
   // operands: query rows + their true entities, all candidates
   KG_LAUNCH("k_eval_pack", k_eval_pack, persistent_blocks(qt * nk * 128 * 4, 256, 8), 256, 0, st, H, dec, qry, nq,
             (const int32_t*)nullptr, (const int32_t*)nullptr, (const int32_t*)nullptr, rows, d, nk, w.Qp, w.Tp);
-  PackJob jc{H, d, nullptr, nullptr, 0, N, d, 128, 0, nk, w.Cp};
+  PackJob jc{H, d, nullptr, nullptr, 0, N, d, 128, 0, nk, w.Cp, 1};
   PackJob none{};
   kg_status s = launch_pack(jc, none, cb * nk * 128 * 4, st);
   if (s != KG_OK) return s;
@@ -966,7 +1016,7 @@ kg_status kg_pack_rows(const float* src, int64_t ld, const int32_t* rowid, const
   KG_REQUIRE(n_max >= 0 && cols >= 1, KG_ERR_VALIDATION, "bad pack shape");
   if (n_max == 0) return KG_OK;
   const int64_t nk = ceil_div(cols, UKC), tiles = ceil_div(n_max, UM);
-  PackJob ja{src, ld, rowid, counts, count_index, n_max, cols, UM, 0, nk, out};
+  PackJob ja{src, ld, rowid, counts, count_index, n_max, cols, UM, 0, nk, out, 0};
   PackJob none{};
   return launch_pack(ja, none, tiles * nk * UM * 4, as_stream(stream));
 }
