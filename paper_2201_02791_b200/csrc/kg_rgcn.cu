@@ -962,19 +962,17 @@ static cudaEvent_t fork_event() {
   return ev;
 }
 
-// Which producers write packed GEMM records directly. In the 64-byte-swizzle
-// record layout a producer's row piece is whole sectors, so k_aggregate (whose
-// only output is the GEMM operand) always does: at wikikg2 scale that costs
-// 0.55 ms per launch against a 1.1 ms pack pass. The dS pass must also write
-// dS row-major (the dV GEMM's operand), so past L2 its extra packed stores cost
-// as much as the pack pass they replace (+1.24 vs 1.13 ms); it packs directly
-// only while the records stay L2-resident. KG_DIRECT_PACK_MAX_MB overrides
-// that 48 MB limit for both producers (tests exercise both paths).
-static bool direct_pack(int64_t rows, int64_t K, bool always) {
+// Producers write packed GEMM records directly. A record carries fp32 in the
+// 64-byte-swizzle layout, so a producer's row piece is whole sectors and costs
+// the same bytes as a row-major row: k_aggregate (whose only output is the GEMM
+// operand) and the dS pass (which also keeps dS row-major for the dV GEMM)
+// save the pack pass (wikikg2 scale: 42.2 -> 40.7 ms/round). Setting
+// KG_DIRECT_PACK_MAX_MB restores the size limit (row-major output + a pack
+// pass past it; tests exercise both paths).
+static bool direct_pack(int64_t rows, int64_t K) {
   const char* env = getenv("KG_DIRECT_PACK_MAX_MB");
-  if (always && !env) return true;
-  const size_t limit = (env ? (size_t)atoll(env) : size_t(48)) << 20;
-  return packed_bytes(rows, K) <= limit;
+  if (!env) return true;
+  return packed_bytes(rows, K) <= ((size_t)atoll(env) << 20);
 }
 
 static Chunks csr_chunks(const kg_graph_csr* G) {
@@ -1036,7 +1034,7 @@ kg_status kg_rgcn_forward(const kg_graph_csr* G, const kg_layer_params* lp, cons
                          (size_t)ws_bytes);
   KG_REQUIRE((size_t)ws_bytes >= need, KG_ERR_VALIDATION, "layer workspace too small");
   AggArgs a{G->indptr, G->src, G->rel, G->norm, csr_chunks(G), lp->coeffs, lp->G, lp->B, lp->d_in, H_in, pos,
-            counts, t, w.acc, direct_pack(G->n, (int64_t)lp->B * lp->d_in, true) ? packed_records((int64_t)lp->B * lp->d_in) : 0,
+            counts, t, w.acc, direct_pack(G->n, (int64_t)lp->B * lp->d_in) ? packed_records((int64_t)lp->B * lp->d_in) : 0,
             w.partial};
   kg_status s = run_aggregate(a, G, st);
   if (s != KG_OK) return s;
@@ -1091,7 +1089,7 @@ kg_status kg_rgcn_backward(const kg_graph_csr* G, const kg_layer_params* lp, con
   }
   CscArgs c{G->c_indptr, G->c_dst, G->c_rel, G->c_norm, csc_chunks(G), lp->coeffs, lp->G, B, dO, w.Y, w.dZ, pos,
             counts, t, w.dS, w.ed, w.ed_self, w.partial,
-            direct_pack(G->n, (int64_t)B * dO, false) ? w.dS_pk : nullptr, packed_records((int64_t)B * dO), 1};
+            direct_pack(G->n, (int64_t)B * dO) ? w.dS_pk : nullptr, packed_records((int64_t)B * dO), 1};
   // The parameter gradients (dV, d coeffs) feed only the optimizer: with a side
   // stream they leave the critical path (the caller joins it before the update).
   // There the CSC pass splits: dS on `st`, the edge/self dots (d coeffs) on the
