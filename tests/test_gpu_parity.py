@@ -302,8 +302,8 @@ def test_prepacked_weights_are_bitwise_identical(monkeypatch):
     """Forward/backward with the once-per-step packed weight operands
     (DeviceModel.repack) and the producer-packed activations (hpk, dS
     records) equal on-the-fly packing bit for bit — with producers writing
-    packed records directly (small operands) or row-major + a pack pass
-    (KG_DIRECT_PACK_MAX_MB=0, the path large graphs take)."""
+    packed records directly (the default) or row-major + a pack pass
+    (KG_DIRECT_PACK_MAX_MB=0)."""
     from paper_2201_02791_b200.model import device_backward, device_forward, device_loss, device_pack_inputs
     graph, split = kb.generate_synthetic(3000, 40, 12.0, seed=3)
     pset = kb.neighborhood_expand(kb.vertex_cut_partition(graph, 2, seed=0), graph, 2)
