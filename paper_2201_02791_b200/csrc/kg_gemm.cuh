@@ -27,18 +27,24 @@ struct GemmArgs {
 
 // --- packed tensor-core operand records (kg_umma.cu) -----------------------
 // An operand with 128-row blocks is stored as records (block, kc) of 128 x 16
-// fp32 values in the K-major 64-byte-swizzle canonical UMMA layout (the GEMM
-// splits each staged record into tf32 hi/lo halves in shared memory, so HBM
-// carries 4 bytes per value): 8-row groups of 512 B, each row's 16
+// values in the K-major 64-byte-swizzle canonical UMMA layout: 8-row groups of
+// 512 B, each row's 16
 // K values in 64 contiguous bytes whose 16-byte chunks are XOR-permuted by
 // (row >> 1) & 3. A row's piece of a record is two whole 32-byte sectors, so a
 // row-at-a-time producer (k_aggregate, the dS pass) writes complete sectors
 // even when the operand spills past L2 (the no-swizzle layout interleaves 8
 // rows at 16 B and cost DRAM read-modify-writes there). Producers that emit
 // this layout directly save the separate pack pass.
+// Two record formats, chosen by the operand's row capacity (records_split):
+//   fp32   one 128x16 fp32 half; the GEMM's split warps make the tf32 hi/lo
+//          halves in shared memory (large operands: HBM carries 4 B/value);
+//   split  [hi | lo] tf32 halves written by the producer (L2-resident
+//          operands, where the in-GEMM split would only add latency).
+// Device helpers take the record count per block as a signed `nk`: negative
+// means split records of -nk per block.
 constexpr int PK_ROWS = 128;
 constexpr int PK_K = 16;
-constexpr int64_t PK_REC = PK_ROWS * PK_K;   // floats per record
+constexpr int64_t PK_REC = PK_ROWS * PK_K;   // floats per record half
 
 // float offset of element (r, k), k < PK_K, inside a record half (any row count)
 __host__ __device__ __forceinline__ int pk_off(int r, int k) {
@@ -46,8 +52,14 @@ __host__ __device__ __forceinline__ int pk_off(int r, int k) {
 }
 
 inline int64_t packed_records(int64_t K) { return (K + PK_K - 1) / PK_K; }
+// split records for operands of up to KG_SPLIT_ROWS_MAX rows (default 65,536:
+// FB15k-237 shape and smaller stay L2-resident)
+bool records_split(int64_t rows);
+// signed record count (see above)
+inline int64_t packed_nk(int64_t rows, int64_t K) { return records_split(rows) ? -packed_records(K) : packed_records(K); }
 inline size_t packed_bytes(int64_t rows, int64_t K) {
-  return (size_t)((rows + PK_ROWS - 1) / PK_ROWS) * (size_t)packed_records(K) * PK_REC * sizeof(float);
+  return (size_t)((rows + PK_ROWS - 1) / PK_ROWS) * (size_t)packed_records(K) * PK_REC * sizeof(float) *
+         (records_split(rows) ? 2 : 1);
 }
 
 #ifdef __CUDACC__
@@ -58,30 +70,47 @@ __device__ __forceinline__ void split_tf32(float x, float& hi, float& lo) {
   lo = x - hi;
 }
 
-// float pointer of element (row, k)
+// float pointer of element (row, k) (the hi half for split records)
 __device__ __forceinline__ float* packed_at(float* P, int64_t nk, int64_t row, int k) {
   const int r = (int)(row & (PK_ROWS - 1)), kk = k & (PK_K - 1);
-  const int64_t rec = (row / PK_ROWS) * nk + (k / PK_K);
-  return P + rec * PK_REC + pk_off(r, kk);
+  const bool sp = nk < 0;
+  const int64_t rec = (row / PK_ROWS) * (sp ? -nk : nk) + (k / PK_K);
+  return P + rec * (sp ? 2 * PK_REC : PK_REC) + pk_off(r, kk);
 }
 
 // V consecutive values starting at k (k % V == 0, V in {1, 2, 4})
 template <int V>
+__device__ __forceinline__ void packed_store4(float* p, const float* v) {
+  if constexpr (V == 4) {
+    *reinterpret_cast<float4*>(p) = make_float4(v[0], v[1], v[2], v[3]);
+  } else if constexpr (V == 2) {
+    *reinterpret_cast<float2*>(p) = make_float2(v[0], v[1]);
+  } else {
+    *p = v[0];
+  }
+}
+
+template <int V>
 __device__ __forceinline__ void packed_store(float* P, int64_t nk, int64_t row, int k, const float* v) {
   float* ph = packed_at(P, nk, row, k);
-  if constexpr (V == 4) {
-    *reinterpret_cast<float4*>(ph) = make_float4(v[0], v[1], v[2], v[3]);
-  } else if constexpr (V == 2) {
-    *reinterpret_cast<float2*>(ph) = make_float2(v[0], v[1]);
-  } else {
-    *ph = v[0];
+  if (nk > 0) {
+    packed_store4<V>(ph, v);
+    return;
   }
+  float h[V], l[V];
+#pragma unroll
+  for (int i = 0; i < V; ++i) split_tf32(v[i], h[i], l[i]);
+  packed_store4<V>(ph, h);
+  packed_store4<V>(ph + PK_REC, l);
 }
 
 // zero the K padding [K, 16*nk) of one row (lanes of a warp share the work)
 __device__ __forceinline__ void packed_zero_pad(float* P, int64_t nk, int64_t row, int K, int lane, int nlanes) {
-  for (int k = K + lane; k < nk * PK_K; k += nlanes) {
-    *packed_at(P, nk, row, k) = 0.f;
+  const int64_t n = nk < 0 ? -nk : nk;
+  for (int k = K + lane; k < n * PK_K; k += nlanes) {
+    float* p = packed_at(P, nk, row, k);
+    p[0] = 0.f;
+    if (nk < 0) p[PK_REC] = 0.f;
   }
 }
 #endif

@@ -83,7 +83,7 @@ struct AggArgs {
   const int32_t* counts;
   int t;
   float* acc;            // packed GEMM records of the (count, B*d) rows, by position
-  int64_t acc_nk;        // records per 128-row block (packed_records(B*d))
+  int64_t acc_nk;        // signed records per 128-row block (packed_nk(n, B*d)), 0: row-major acc
   float* partial;        // (split chunks, B*d)
 };
 
@@ -1034,7 +1034,7 @@ kg_status kg_rgcn_forward(const kg_graph_csr* G, const kg_layer_params* lp, cons
                          (size_t)ws_bytes);
   KG_REQUIRE((size_t)ws_bytes >= need, KG_ERR_VALIDATION, "layer workspace too small");
   AggArgs a{G->indptr, G->src, G->rel, G->norm, csr_chunks(G), lp->coeffs, lp->G, lp->B, lp->d_in, H_in, pos,
-            counts, t, w.acc, direct_pack(G->n, (int64_t)lp->B * lp->d_in) ? packed_records((int64_t)lp->B * lp->d_in) : 0,
+            counts, t, w.acc, direct_pack(G->n, (int64_t)lp->B * lp->d_in) ? packed_nk(G->n, (int64_t)lp->B * lp->d_in) : 0,
             w.partial};
   kg_status s = run_aggregate(a, G, st);
   if (s != KG_OK) return s;
@@ -1089,7 +1089,7 @@ kg_status kg_rgcn_backward(const kg_graph_csr* G, const kg_layer_params* lp, con
   }
   CscArgs c{G->c_indptr, G->c_dst, G->c_rel, G->c_norm, csc_chunks(G), lp->coeffs, lp->G, B, dO, w.Y, w.dZ, pos,
             counts, t, w.dS, w.ed, w.ed_self, w.partial,
-            direct_pack(G->n, (int64_t)B * dO) ? w.dS_pk : nullptr, packed_records((int64_t)B * dO), 1};
+            direct_pack(G->n, (int64_t)B * dO) ? w.dS_pk : nullptr, packed_nk(G->n, (int64_t)B * dO), 1};
   // The parameter gradients (dV, d coeffs) feed only the optimizer: with a side
   // stream they leave the critical path (the caller joins it before the update).
   // There the CSC pass splits: dS on `st`, the edge/self dots (d coeffs) on the

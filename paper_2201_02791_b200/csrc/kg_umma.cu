@@ -246,6 +246,7 @@ struct PackedArgs {
   float* c_packed;        // NN: optional packed copy of the output (records by MMA row, K = np)
   int64_t c_nk;
   const float* mul;       // NN: optional per-element output scale by MMA row (ld N)
+  int a_split;            // A records already hold hi | lo halves (records_split of the row capacity)
   int b_split;            // B records already hold hi | lo halves (NN: weights, split once per step)
 };
 
@@ -286,6 +287,7 @@ __global__ void __launch_bounds__(UTHREADS, 1) k_umma_packed(PackedArgs g, int n
   const uint32_t sbase = smem_u32(smem);
   const uint32_t sb = stage_bytes(np), a_half = (uint32_t)(UM * UKC * 4), b_half = (uint32_t)(np * UKC * 4);
   const uint32_t a_bytes = 2 * a_half;
+  const bool presplit = g.a_split && g.b_split;   // nothing to split: the MMA waits on the loads
   auto full = [&](int s) { return smem_u32(&bar_full[s]); };
   auto empty = [&](int s) { return smem_u32(&bar_empty[s]); };
 
@@ -317,7 +319,9 @@ __global__ void __launch_bounds__(UTHREADS, 1) k_umma_packed(PackedArgs g, int n
       int64_t it = 0;
       for (int64_t tile = tile0; tile < ntiles; tile += tstep) {
         const int64_t ablk = g.tn ? blockIdx.y : tile;
-        const float* arec = g.Ap + (ablk * g.a_nk_alloc + c_lo) * rec_floats(UM);
+        const int64_t arf = g.a_split ? rec_floats_split(UM) : rec_floats(UM);
+        const float* arec = g.Ap + (ablk * g.a_nk_alloc + c_lo) * arf;
+        const uint32_t acopy = g.a_split ? 2 * a_half : a_half;
         const int64_t brf = g.b_split ? rec_floats_split(np) : rec_floats(np);
         const float* brec = g.Bp + c_lo * brf;
         const uint32_t bcopy = g.b_split ? 2 * b_half : b_half;
@@ -325,8 +329,8 @@ __global__ void __launch_bounds__(UTHREADS, 1) k_umma_packed(PackedArgs g, int n
           const int s = (int)(it % nstages);
           if (it >= nstages) mbar_wait(empty(s), (uint32_t)((it / nstages - 1) & 1));
           const uint32_t dst = sbase + (uint32_t)s * sb;
-          mbar_expect_tx(full(s), a_half + bcopy);
-          bulk_g2s(dst, arec + (int64_t)kc * rec_floats(UM), a_half, full(s));
+          mbar_expect_tx(full(s), acopy + bcopy);
+          bulk_g2s(dst, arec + (int64_t)kc * arf, acopy, full(s));
           bulk_g2s(dst + a_bytes, brec + (int64_t)kc * brf, bcopy, full(s));
         }
       }
@@ -343,7 +347,7 @@ __global__ void __launch_bounds__(UTHREADS, 1) k_umma_packed(PackedArgs g, int n
         const uint32_t d = tmem + (uint32_t)acc * acc_cols;
         for (int kc = 0; kc < nk; ++kc, ++it) {
           const int s = (int)(it % nstages);
-          mbar_wait(smem_u32(&bar_split[s]), (uint32_t)((it / nstages) & 1));
+          mbar_wait(presplit ? full(s) : smem_u32(&bar_split[s]), (uint32_t)((it / nstages) & 1));
           tc_fence_after();
           const uint32_t a_hi = sbase + (uint32_t)s * sb, a_lo = a_hi + a_half;
           const uint32_t b_hi = a_hi + a_bytes, b_lo = b_hi + b_half;
@@ -362,10 +366,11 @@ __global__ void __launch_bounds__(UTHREADS, 1) k_umma_packed(PackedArgs g, int n
       }
     }
   } else if (warp >= USPLIT0) {
+    if (presplit) ntiles = tile0;   // nothing to split: skip to the teardown barrier
     // split warps 6..9: each staged fp32 record becomes tf32 hi (in place) +
     // lo (the slot's second half), x = hi + lo exactly
     const int st = tid - USPLIT0 * 32;
-    const int na = UM * UKC / 4, nb = g.b_split ? 0 : np * UKC / 4;
+    const int na = g.a_split ? 0 : UM * UKC / 4, nb = g.b_split ? 0 : np * UKC / 4;
     int64_t it = 0;
     for (int64_t tile = tile0; tile < ntiles; tile += tstep) {
       for (int kc = 0; kc < nk; ++kc, ++it) {
@@ -453,6 +458,11 @@ __global__ void __launch_bounds__(UTHREADS, 1) k_umma_packed(PackedArgs g, int n
   if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(2 * acc_cols));
 }
 
+bool records_split(int64_t rows) {
+  const char* env = getenv("KG_SPLIT_ROWS_MAX");
+  return rows <= (env ? atoll(env) : 65536LL);
+}
+
 static uint32_t acc_cols_for(int np) {
   uint32_t c = 32;
   while ((int)c < np) c <<= 1;
@@ -488,7 +498,7 @@ static kg_status launch_packed(const PackedArgs& p, dim3 grid, cudaStream_t st) 
 static size_t nn_pack_sizes(int64_t M_max, int64_t K, int64_t N, size_t* a_bytes) {
   const int np = pad16((int)N);
   const int64_t nk = ceil_div(K, UKC), tiles = ceil_div(M_max > 0 ? M_max : 1, UM);
-  size_t a = align_up((size_t)(tiles * nk * rec_floats(UM)) * 4);
+  size_t a = align_up((size_t)(tiles * nk * (records_split(M_max) ? rec_floats_split(UM) : rec_floats(UM))) * 4);
   size_t b = align_up((size_t)(nk * rec_floats_split(np)) * 4);
   if (a_bytes) *a_bytes = a;
   return a + b;
@@ -505,7 +515,8 @@ kg_status umma_gemm_nn(const GemmArgs& g, void* ws, cudaStream_t st) {
   nn_pack_sizes(g.M_max, g.K, g.N, &a_bytes);
   float* Ap = static_cast<float*>(ws);
   float* Bp = reinterpret_cast<float*>(static_cast<char*>(ws) + a_bytes);
-  PackJob ja{g.A, g.lda, g.a_rows, g.M_dev, g.M_dev_index, g.M, g.K, UM, 0, nk, Ap, 0};
+  const int a_split = records_split(g.M_max) ? 1 : 0;
+  PackJob ja{g.A, g.lda, g.a_rows, g.M_dev, g.M_dev_index, g.M, g.K, UM, 0, nk, Ap, a_split};
   if (g.a_packed) {   // producer already wrote the A records
     ja.src = nullptr;
     Ap = const_cast<float*>(g.a_packed);
@@ -521,10 +532,10 @@ kg_status umma_gemm_nn(const GemmArgs& g, void* ws, cudaStream_t st) {
     if (s != KG_OK) return s;
   }
   PackedArgs p{};
-  p.Ap = Ap; p.Bp = Bp; p.a_nk_alloc = nk; p.np = np; p.tn = 0; p.b_split = 1;
+  p.Ap = Ap; p.Bp = Bp; p.a_nk_alloc = nk; p.np = np; p.tn = 0; p.a_split = a_split; p.b_split = 1;
   p.M = g.M; p.M_dev = g.M_dev; p.M_dev_index = g.M_dev_index; p.nk = nk;
   p.C = g.C; p.ldc = g.ldc; p.c_rows = g.c_rows; p.N = g.N; p.out_rows = 0; p.relu = g.relu;
-  p.c_packed = g.c_packed; p.c_nk = ceil_div(g.N, UKC); p.mul = g.mul;
+  p.c_packed = g.c_packed; p.c_nk = packed_nk(g.M_max, g.N); p.mul = g.mul;
   const int ctas = (int)(tiles < num_sms() ? tiles : num_sms());
   return launch_packed(p, dim3((unsigned)ctas, 1, 1), st);
 }
@@ -1016,7 +1027,7 @@ kg_status kg_pack_rows(const float* src, int64_t ld, const int32_t* rowid, const
   KG_REQUIRE(n_max >= 0 && cols >= 1, KG_ERR_VALIDATION, "bad pack shape");
   if (n_max == 0) return KG_OK;
   const int64_t nk = ceil_div(cols, UKC), tiles = ceil_div(n_max, UM);
-  PackJob ja{src, ld, rowid, counts, count_index, n_max, cols, UM, 0, nk, out, 0};
+  PackJob ja{src, ld, rowid, counts, count_index, n_max, cols, UM, 0, nk, out, records_split(n_max) ? 1 : 0};
   PackJob none{};
   return launch_pack(ja, none, tiles * nk * UM * 4, as_stream(stream));
 }

@@ -303,7 +303,7 @@ def test_prepacked_weights_are_bitwise_identical(monkeypatch):
     (DeviceModel.repack) and the producer-packed activations (hpk, dS
     records) equal on-the-fly packing bit for bit — with producers writing
     packed records directly (the default) or row-major + a pack pass
-    (KG_DIRECT_PACK_MAX_MB=0)."""
+    (KG_DIRECT_PACK_MAX_MB=0), in either record format (KG_SPLIT_ROWS_MAX)."""
     from paper_2201_02791_b200.model import device_backward, device_forward, device_loss, device_pack_inputs
     graph, split = kb.generate_synthetic(3000, 40, 12.0, seed=3)
     pset = kb.neighborhood_expand(kb.vertex_cut_partition(graph, 2, seed=0), graph, 2)
@@ -322,7 +322,11 @@ def test_prepacked_weights_are_bitwise_identical(monkeypatch):
     ds = DeviceStream(tri, lab, len(batch.triples))
     model.repack()
     out = []
-    for direct_mb, packed in (("48", False), ("48", True), ("0", False), ("0", True)):
+    # split_rows: pre-split hi|lo records (the default at this size, workspaces
+    # sized for it) vs fp32 records split inside the GEMM (the large-graph format)
+    for split_rows, direct_mb, packed in [(sr, dm, pk) for sr in ("65536", "0")
+                                          for dm, pk in (("48", False), ("48", True), ("0", False), ("0", True))]:
+        monkeypatch.setenv("KG_SPLIT_ROWS_MAX", split_rows)
         monkeypatch.setenv("KG_DIRECT_PACK_MAX_MB", direct_mb)
         if packed:
             device_pack_inputs(bufs)
