@@ -51,6 +51,8 @@ def parse_args():
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--batch", type=int, default=BATCH)
     ap.add_argument("--roofline-kernel", default="k_aggregate")
+    ap.add_argument("--parts", type=int, default=0,
+                    help="diagnostic: partitions (a multiple of the rank count; default one per GPU)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-rounds", type=int, default=2, help="bounded CPU baseline sample (rounds)")
@@ -192,7 +194,8 @@ def run_ours(args, world, rank, local):
 
     lib = _lib.require_cuda()
     dev = torch.device("cuda", local)
-    graph, split, pset, mc, tc = build_inputs(world, args.batch)
+    P = args.parts or world
+    graph, split, pset, mc, tc = build_inputs(P, args.batch)
     tr = kb.Trainer(pset, graph, mc, tc)
     tr.use_graphs = os.environ.get("KG_CUDA_GRAPHS", "1") != "0"
     tr.timer_prefix = args.roofline_kernel      # events around this kernel are captured into the graphs
@@ -335,11 +338,12 @@ def run_ours(args, world, rank, local):
         line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
                 "warmup": max(args.warmup, 3), "ms_per_step": total_ms / args.steps, "higher_is_better": True,
                 "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-                "config": {"workload": f"fb15k237-shape synthetic KG, P={world} partitions (vertex cut + 2-hop "
-                                       f"halo), b={args.batch}/GPU",
+                "config": {"workload": f"fb15k237-shape synthetic KG, P={P} partitions (vertex cut + 2-hop "
+                                       f"halo), b={args.batch}/partition",
                            "model": "RGCN 2x100 (2 bases) + DistMult, 1 neg/pos, Adam 0.01, embedding mode",
-                           "global_batch": triples_per_step, "per_gpu_batch": args.batch,
-                           "rounds_per_epoch": tr.rounds, "parallelism": f"dp{world} (one partition per GPU)",
+                           "global_batch": triples_per_step, "per_gpu_batch": args.batch * P // world,
+                           "rounds_per_epoch": tr.rounds, "parallelism": f"dp{world} (one partition per GPU)" if P == world
+                           else f"dp{world}, {P // world} partitions per GPU",
                            "l2": "flushed between timed steps (256 MiB write)",
                            "graph": {"entities": graph.num_entities, "relations": graph.num_relations,
                                      "train_triples": graph.num_edges}},
