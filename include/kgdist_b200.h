@@ -377,6 +377,23 @@ kg_status kg_dense_step(float* params, float* m, float* v, const float* grads_al
                         int32_t optimizer, float lr, float beta1, float beta2, float eps, double bc1,
                         double bc2, const int64_t* step_dev, float grad_clip, uint32_t* flags, void* ws,
                         int64_t ws_bytes, void* stream);
+/* Peer-memory exchange of the dense gradient payloads, one partition per rank
+ * on one NVLink node: replaces the all-gather of ref:trainer.py:430-438 ahead
+ * of the tree mean (ref:trainer.py:77-86). kg_peer_alloc returns a zeroed
+ * region of kg_peer_region_bytes(n) and its 64-byte cudaIpcMemHandle;
+ * kg_peer_open maps a peer's handle. Per round, kg_peer_publish copies this
+ * rank's n floats into its region (slot = round parity) and releases the
+ * region's flag; kg_peer_gather waits (bounded, 5 s; timeout sets bit 8 of
+ * flags) for every peer's flag and writes the (P, n) payloads in partition
+ * order to out. seq: 3 zeroed int64 device words private to this rank.
+ * regions_dev: device array of the P region pointers (own + opened). */
+int64_t kg_peer_region_bytes(int64_t n);
+kg_status kg_peer_alloc(int64_t bytes, void** region, void* ipc_handle);
+kg_status kg_peer_open(const void* ipc_handle, void** region);
+kg_status kg_peer_close(void* region, int32_t owned);
+kg_status kg_peer_publish(const float* local, void* region, int64_t n, int64_t* seq, void* stream);
+kg_status kg_peer_gather(void* const* regions_dev, int32_t P, int64_t n, float* out, int64_t* seq,
+                         uint32_t* flags, void* stream);
 /* Lazy sparse rows (ref:trainer.py:136-147): rows = vertex_order[0:counts[k]]
  * of the (n,d) table; grad rows by local id. */
 kg_status kg_sparse_step(float* table, float* m, float* v, const float* grad, const int32_t* rows,

@@ -120,6 +120,12 @@ _PROTOS = {
     "kg_optim_workspace_bytes": (c_int64, [c_int64]),
     "kg_dense_step": (ST, [P, P, P, P, c_int32, c_int64, c_int32, c_float, c_float, c_float, c_float,
                            c_double, c_double, P, c_float, P, P, c_int64, P]),
+    "kg_peer_region_bytes": (c_int64, [c_int64]),
+    "kg_peer_alloc": (ST, [c_int64, POINTER(c_void_p), P]),
+    "kg_peer_open": (ST, [P, POINTER(c_void_p)]),
+    "kg_peer_close": (ST, [P, c_int32]),
+    "kg_peer_publish": (ST, [P, P, c_int64, P, P]),
+    "kg_peer_gather": (ST, [P, c_int32, c_int64, P, P, P, P]),
     "kg_sparse_step": (ST, [P, P, P, P, P, P, c_int32, c_int32, c_int32, c_float, c_float, c_float,
                             c_float, c_double, c_double, P, c_int32, P]),
     "kg_eval_workspace_bytes": (c_int64, [c_int64, c_int32, c_int32, c_int64]),

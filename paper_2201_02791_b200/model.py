@@ -19,7 +19,7 @@ from typing import Optional
 import numpy as np
 
 from . import _lib
-from .errors import FormatError, IntegrityError, NumericError, ShapeError, ValidationError
+from .errors import FormatError, IntegrityError, NumericError, ProtocolError, ShapeError, ValidationError
 
 MODE_FEATURE = "feature"
 MODE_EMBEDDING = "embedding"
@@ -403,6 +403,8 @@ def check_flags(bufs: ViewBuffers, what: str = "") -> None:
             raise NumericError("non-finite loss")
         if f & 4:
             raise NumericError("non-finite parameter after optimizer step")
+        if f & 8:
+            raise ProtocolError("peer payload exchange timed out (a rank stopped publishing)")
         raise NumericError(f"device status {f:#x}")
 
 

@@ -432,9 +432,13 @@ class Trainer:
         self.grads_local = torch.zeros((nloc, D), dtype=torch.float32, device=self.dev)
         self.grads_all = (torch.zeros((self.P, D), dtype=torch.float32, device=self.dev) if self.dist
                           else self.grads_local)
+        self._peer = None
         if self.dist:
             self._recv = torch.empty((self.world * nloc, D), dtype=torch.float32, device=self.dev)
             self._gidx = payload_order(self.P, self.world, self.dev)
+            # opt-in: measured at parity with NCCL at 2/4 ranks
+            if self.P == self.world and os.environ.get("KG_PEER_GATHER", "0") == "1":
+                self._peer = PeerExchange.create(D, self.rank, self.world, self.dev)
         self.m = torch.zeros(D, dtype=torch.float32, device=self.dev)
         self.v = torch.zeros(D, dtype=torch.float32, device=self.dev)
         self.flags = torch.zeros(1, dtype=torch.int32, device=self.dev)
@@ -518,6 +522,8 @@ class Trainer:
                     raise NumericError("non-finite loss")
                 if f & 4:
                     raise NumericError("non-finite parameter after optimizer step")
+                if f & 8:
+                    raise ProtocolError("peer payload exchange timed out (a rank stopped publishing)")
                 raise NumericError(f"device status {f:#x}")
         if host_flags.tolist()[-1]:
             raise NumericError("non-finite parameter after optimizer step")
@@ -677,13 +683,19 @@ class Trainer:
         whenever the cyclic GC runs; a following train() then reuses them)."""
         _torch().cuda.synchronize()
         self._graphs.clear()
+        if self._peer is not None:
+            self._peer.close()      # collective: every rank closes its trainer (train() does)
+            self._peer = None
         for w in self.workers:
             w.sampler.close()
             w.sampler._prep = None
             w.prep.w = None
 
     def _gather(self):
-        gather_partition_payloads(self.grads_local, self.P, self.world, self.grads_all, self._recv, self._gidx)
+        if self._peer is not None:
+            self._peer.exchange(self.grads_local, self.grads_all, self.workers[0].bufs.flags)
+        else:
+            gather_partition_payloads(self.grads_local, self.P, self.world, self.grads_all, self._recv, self._gidx)
 
     def check(self):
         for w in self.workers:
@@ -734,6 +746,69 @@ class Trainer:
         for r in range(1, self.world):
             if not torch.equal(allr[0], allr[r]):
                 raise ProtocolError(f"replica divergence: rank {r} dense blocks differ from rank 0")
+
+
+class PeerExchange:
+    """Dense-payload exchange over NVLink peer memory (one partition per rank,
+    one node): every rank publishes its payload into its own IPC-shared region
+    and reads all P regions straight into the tree-mean input, in partition
+    order (the gather of ref:trainer.py:430-438, csrc/kg_peer.cu). Created only
+    when every rank can map every peer; otherwise the NCCL all-gather runs."""
+
+    def __init__(self, n, rank, world, dev, region, opened, regions_dev, seq):
+        self.n, self.rank, self.world, self.dev = n, rank, world, dev
+        self.region, self.opened, self.regions_dev, self.seq = region, opened, regions_dev, seq
+
+    @classmethod
+    def create(cls, n: int, rank: int, world: int, dev):
+        torch = _torch()
+        dist = torch.distributed
+        lib = _lib.require_cuda()
+        import socket
+        me = (socket.gethostname(), dev.index)
+        where = [None] * world
+        dist.all_gather_object(where, me)
+        ok = all(h == me[0] for h, _ in where) and all(
+            d == dev.index or torch.cuda.can_device_access_peer(dev.index, d) for _, d in where)
+        votes = [None] * world
+        dist.all_gather_object(votes, bool(ok))
+        if not all(votes):
+            return None
+        region = ctypes.c_void_p()
+        handle = ctypes.create_string_buffer(64)
+        _lib.check(lib.kg_peer_alloc(lib.kg_peer_region_bytes(n), ctypes.byref(region), handle), "kg_peer_alloc")
+        handles = [None] * world
+        dist.all_gather_object(handles, handle.raw)
+        ptrs, opened = [], []
+        for r, h in enumerate(handles):
+            if r == rank:
+                ptrs.append(region.value)
+                continue
+            peer = ctypes.c_void_p()
+            _lib.check(lib.kg_peer_open(ctypes.create_string_buffer(h, 64), ctypes.byref(peer)), "kg_peer_open")
+            ptrs.append(peer.value)
+            opened.append(peer.value)
+        regions_dev = torch.tensor(ptrs, dtype=torch.int64, device=dev)
+        seq = torch.zeros(3, dtype=torch.int64, device=dev)
+        dist.barrier()            # every region is zeroed and mapped before the first publish
+        return cls(n, rank, world, dev, region.value, opened, regions_dev, seq)
+
+    def exchange(self, local, out, flags):
+        torch = _torch()
+        st = torch.cuda.current_stream().cuda_stream
+        _lib.call("kg_peer_publish", local.data_ptr(), self.region, self.n, self.seq.data_ptr(), st)
+        _lib.call("kg_peer_gather", self.regions_dev.data_ptr(), self.world, self.n, out.data_ptr(),
+                  self.seq.data_ptr(), flags.data_ptr(), st)
+
+    def close(self):
+        torch = _torch()
+        lib = _lib.require_cuda()
+        torch.cuda.synchronize()
+        torch.distributed.barrier()   # no peer still reads this rank's region
+        for p in self.opened:
+            lib.kg_peer_close(p, 0)
+        lib.kg_peer_close(self.region, 1)
+        self.opened, self.region = [], None
 
 
 def payload_order(P: int, world: int, device):
