@@ -724,16 +724,55 @@ class Trainer:
         params = self.init_params.copy()
         params.set_dense_blocks(self.model.dense_blocks())
         if self.mc.mode == MODE_EMBEDDING:
-            tables = self.local_tables()
             if self.dist:
-                gathered = [None] * self.world
-                torch.distributed.all_gather_object(gathered, tables)
-                tables = {k: v for d in gathered for k, v in d.items()}
+                params.entity_embed = self._gather_owned_rows()
+                return params
+            tables = self.local_tables()
             if self.P == 1:
                 params.entity_embed = tables[0]
             else:
                 params.entity_embed = _assemble_embed(self.pset, tables, self.init_params.entity_embed)
         return params
+
+    def _gather_owned_rows(self) -> np.ndarray:
+        """Final embedding table over several ranks: every rank sends only the
+        rows its partitions own (lowest-id partition holding the vertex as a
+        core endpoint, ref:trainer.py:319-333 — the rule of _assemble_embed)
+        as one padded NCCL all-gather of (global id, fp32 row) pairs, instead
+        of pickling a full (N, d) table per partition."""
+        torch = _torch()
+        dist = torch.distributed
+        base = self.init_params.entity_embed
+        owner = np.full(len(base), -1, dtype=np.int64)
+        for part in sorted(self.pset.partitions, key=lambda p: p.id):
+            ends = np.concatenate([part.core_vertices, part.replicated_vertices]).astype(np.int64)
+            owner[ends[owner[ends] < 0]] = part.id
+        ids, rows = [], []
+        for w in self.workers:
+            lids = np.asarray(w.view.local_ids, dtype=np.int64)
+            sel = np.flatnonzero(owner[lids] == self.pset.partitions[w.wid].id)
+            ids.append(torch.from_numpy(lids[sel]).to(self.dev))
+            rows.append(w.input_rows[torch.from_numpy(sel).to(self.dev)])
+        ids = torch.cat(ids)
+        rows = torch.cat(rows)
+        k = torch.tensor([ids.numel()], dtype=torch.int64, device=self.dev)
+        counts = torch.empty(self.world, dtype=torch.int64, device=self.dev)
+        dist.all_gather_into_tensor(counts, k)
+        counts = counts.cpu().tolist()
+        kmax, d = max(max(counts), 1), rows.shape[1]
+        ids_p = torch.full((kmax,), -1, dtype=torch.int64, device=self.dev)
+        rows_p = torch.zeros((kmax, d), dtype=rows.dtype, device=self.dev)
+        ids_p[: ids.numel()] = ids
+        rows_p[: ids.numel()] = rows
+        ids_all = torch.empty((self.world, kmax), dtype=torch.int64, device=self.dev)
+        rows_all = torch.empty((self.world, kmax, d), dtype=rows.dtype, device=self.dev)
+        dist.all_gather_into_tensor(ids_all, ids_p)
+        dist.all_gather_into_tensor(rows_all, rows_p)
+        ids_all, rows_all = ids_all.cpu().numpy(), rows_all.cpu().numpy()
+        out = base.copy()
+        for r, c in enumerate(counts):
+            out[ids_all[r, :c]] = rows_all[r, :c].astype(np.float64)
+        return out
 
     def check_replicas(self):
         """Dense replicas must be bitwise equal on every rank (ref:trainer.py:465-469)."""
