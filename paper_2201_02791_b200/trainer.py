@@ -724,22 +724,19 @@ class Trainer:
         params = self.init_params.copy()
         params.set_dense_blocks(self.model.dense_blocks())
         if self.mc.mode == MODE_EMBEDDING:
-            if self.dist:
-                params.entity_embed = self._gather_owned_rows()
-                return params
-            tables = self.local_tables()
             if self.P == 1:
-                params.entity_embed = tables[0]
+                params.entity_embed = self.local_tables()[0]
             else:
-                params.entity_embed = _assemble_embed(self.pset, tables, self.init_params.entity_embed)
+                params.entity_embed = self._gather_owned_rows()
         return params
 
     def _gather_owned_rows(self) -> np.ndarray:
-        """Final embedding table over several ranks: every rank sends only the
-        rows its partitions own (lowest-id partition holding the vertex as a
-        core endpoint, ref:trainer.py:319-333 — the rule of _assemble_embed)
-        as one padded NCCL all-gather of (global id, fp32 row) pairs, instead
-        of pickling a full (N, d) table per partition."""
+        """Final embedding table for P > 1: only the rows each partition owns
+        (lowest-id partition holding the vertex as a core endpoint,
+        ref:trainer.py:319-333 — the rule of _assemble_embed) leave the
+        device; over several ranks as one padded NCCL all-gather of (global
+        id, fp32 row) pairs instead of a pickled full (N, d) table per
+        partition."""
         torch = _torch()
         dist = torch.distributed
         base = self.init_params.entity_embed
@@ -755,6 +752,10 @@ class Trainer:
             rows.append(w.input_rows[torch.from_numpy(sel).to(self.dev)])
         ids = torch.cat(ids)
         rows = torch.cat(rows)
+        if not self.dist:
+            out = base.copy()
+            out[ids.cpu().numpy()] = rows.cpu().numpy().astype(np.float64)
+            return out
         k = torch.tensor([ids.numel()], dtype=torch.int64, device=self.dev)
         counts = torch.empty(self.world, dtype=torch.int64, device=self.dev)
         dist.all_gather_into_tensor(counts, k)

@@ -479,3 +479,24 @@ def test_training_options_track_oracle(opts):
     # fp32 vs fp64 rounding, so the sparse table gets 2e-3 (measured 1.1e-3
     # with clipping, whose per-step rescale adds to the drift).
     assert rel_l2(params.entity_embed, got.embed) < 2e-3
+
+
+def test_owned_row_snapshot_equals_table_assembly():
+    """snapshot() moves only the owned embedding rows off the device; the
+    result is bitwise the reference's table-per-partition assembly
+    (ref:trainer.py:319-333, _assemble_embed)."""
+    from paper_2201_02791_b200.trainer import _assemble_embed
+    g = load_golden("synth_p4")
+    graph, pset, cfg = golden_pset(g)
+    L = len(cfg["dims"]) - 1
+    mc = kb.ModelConfig(L, cfg["dims"], cfg["num_bases"], graph.num_relations, 1, mode="embedding")
+    tr = kb.Trainer(pset, graph, mc, kb.TrainConfig(epochs=1, batch_size=96, seed=2),
+                    initial_params=golden_params(g, "init_", L))
+    tr.use_graphs = False
+    tr.begin_epoch()
+    for _ in range(min(2, tr.rounds)):
+        tr.run_round()
+    torch.cuda.synchronize()
+    want = _assemble_embed(pset, tr.local_tables(), tr.init_params.entity_embed)
+    np.testing.assert_array_equal(tr.snapshot().entity_embed, want)
+    tr.close()
