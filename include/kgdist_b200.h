@@ -48,6 +48,7 @@ typedef enum kg_status {
 #define KG_FLAG_NONFINITE_LOSS 2u
 #define KG_FLAG_NONFINITE_PARAM 4u
 #define KG_FLAG_BAD_VERTEX 8u
+#define KG_FLAG_PEER_TIMEOUT 16u  /* kg_peer_gather: a peer payload did not arrive within 5 s */
 
 /* numpy PCG64 BitGenerator state (Generator.bit_generator.state). */
 typedef struct kg_pcg64 {
@@ -383,7 +384,7 @@ kg_status kg_dense_step(float* params, float* m, float* v, const float* grads_al
  * region of kg_peer_region_bytes(n) and its 64-byte cudaIpcMemHandle;
  * kg_peer_open maps a peer's handle. Per round, kg_peer_publish copies this
  * rank's n floats into its region (slot = round parity) and releases the
- * region's flag; kg_peer_gather waits (bounded, 5 s; timeout sets bit 8 of
+ * region's flag; kg_peer_gather waits (bounded, 5 s; timeout sets KG_FLAG_PEER_TIMEOUT in
  * flags) for every peer's flag and writes the (P, n) payloads in partition
  * order to out. seq: 3 zeroed int64 device words private to this rank.
  * regions_dev: device array of the P region pointers (own + opened). */
@@ -394,6 +395,25 @@ kg_status kg_peer_close(void* region, int32_t owned);
 kg_status kg_peer_publish(const float* local, void* region, int64_t n, int64_t* seq, void* stream);
 kg_status kg_peer_gather(void* const* regions_dev, int32_t P, int64_t n, float* out, int64_t* seq,
                          uint32_t* flags, void* stream);
+/* float64 compatibility entry points of the public host API
+ * (`allreduce_mean`, `Optimizer.step`; ref:trainer.py:63-151): reference
+ * operation order with round-to-nearest intrinsics, bit-identical to numpy.
+ * kg_tree_mean_f64: payloads (P, n) back to back -> pairwise-tree mean.
+ * kg_dense_step_f64: flat dense blocks; grad_clip < 0 disables clipping.
+ * kg_sparse_step_f64: k (possibly repeated) row ids of a num_rows x d table,
+ * old_rows = table[ids], grad_rows; out_rows = the rows the reference assigns
+ * to table[ids]; em/ev (num_rows x d) updated from the last occurrence of each
+ * id (numpy fancy-assignment semantics). */
+kg_status kg_tree_mean_f64(const double* payloads, int64_t P, int64_t n, double* out, void* stream);
+int64_t kg_dense_step_f64_workspace_bytes(int64_t n);
+kg_status kg_dense_step_f64(double* params, double* m, double* v, const double* grads, int64_t n, int32_t optimizer,
+                            double lr, double beta1, double beta2, double eps, double bc1, double bc2,
+                            double grad_clip, uint32_t* flags, void* ws, int64_t ws_bytes, void* stream);
+int64_t kg_sparse_step_f64_workspace_bytes(int64_t k, int32_t d, int64_t num_rows);
+kg_status kg_sparse_step_f64(const double* old_rows, const double* grad_rows, const int64_t* ids, int64_t k,
+                             int32_t d, double* em, double* ev, int64_t num_rows, int32_t optimizer, double lr,
+                             double beta1, double beta2, double eps, double bc1, double bc2, double* out_rows,
+                             void* ws, int64_t ws_bytes, void* stream);
 /* Lazy sparse rows (ref:trainer.py:136-147): rows = vertex_order[0:counts[k]]
  * of the (n,d) table; grad rows by local id. */
 kg_status kg_sparse_step(float* table, float* m, float* v, const float* grad, const int32_t* rows,

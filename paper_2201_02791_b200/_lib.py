@@ -120,6 +120,13 @@ _PROTOS = {
     "kg_optim_workspace_bytes": (c_int64, [c_int64]),
     "kg_dense_step": (ST, [P, P, P, P, c_int32, c_int64, c_int32, c_float, c_float, c_float, c_float,
                            c_double, c_double, P, c_float, P, P, c_int64, P]),
+    "kg_tree_mean_f64": (ST, [P, c_int64, c_int64, P, P]),
+    "kg_dense_step_f64_workspace_bytes": (c_int64, [c_int64]),
+    "kg_dense_step_f64": (ST, [P, P, P, P, c_int64, c_int32, c_double, c_double, c_double, c_double, c_double,
+                               c_double, c_double, P, P, c_int64, P]),
+    "kg_sparse_step_f64_workspace_bytes": (c_int64, [c_int64, c_int32, c_int64]),
+    "kg_sparse_step_f64": (ST, [P, P, P, c_int64, c_int32, P, P, c_int64, c_int32, c_double, c_double, c_double,
+                                c_double, c_double, c_double, P, P, c_int64, P]),
     "kg_peer_region_bytes": (c_int64, [c_int64]),
     "kg_peer_alloc": (ST, [c_int64, POINTER(c_void_p), P]),
     "kg_peer_open": (ST, [P, POINTER(c_void_p)]),

@@ -23,7 +23,7 @@ namespace kg {
 namespace {
 
 constexpr size_t kPeerHeader = 256;
-constexpr uint32_t kPeerTimeoutFlag = 8u;
+constexpr uint32_t kPeerTimeoutFlag = KG_FLAG_PEER_TIMEOUT;
 // A few CTAs only: the gather's wait for the slowest rank must not hold the
 // SMs the sampler's epoch graph and the forked streams run on (a full-grid
 // spin cost 70 us/round at 2 ranks); 32 CTAs still read ~1 MB over NVLink in

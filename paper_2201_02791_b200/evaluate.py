@@ -238,3 +238,15 @@ def evaluate(params: ModelParams, config: ModelConfig, graph, split, which: str 
                        r.tolist(), c.tolist()))
     return EvalResult(mrr=float((1.0 / r).mean()), hits={k: float((r <= k).mean()) for k in HITS_KS},
                       records=records)
+
+
+# Reference module-level names that live in io.py here (ref:evaluate.py:232-253); resolved
+# lazily so `from <pkg>.evaluate import X` works as with the reference.
+_IO_NAMES = ('read_candidates', 'write_results')
+
+
+def __getattr__(name):
+    if name in _IO_NAMES:
+        from . import io
+        return getattr(io, name)
+    raise AttributeError(name)

@@ -71,6 +71,38 @@ class KnowledgeGraph:
     def edges(self) -> list:
         return [Triplet(*row) for row in self.triples.tolist()]
 
+    # -- adjacency indices over edge ids (ref:graph.py:69-99) ----------------
+    def _edge_index(self, col: int) -> tuple:
+        key = "_adj_out" if col == 0 else "_adj_in"
+        idx = self.__dict__.get(key)
+        if idx is None:
+            ends = self.triples[:, col]
+            order = np.argsort(ends, kind="stable")
+            indptr = np.concatenate([[0], np.cumsum(np.bincount(ends, minlength=self.num_entities))])
+            idx = (indptr.astype(np.int64), order)
+            self.__dict__[key] = idx
+        return idx
+
+    def out_edge_ids(self, v: int) -> np.ndarray:
+        """Ids of the edges leaving v, ascending."""
+        indptr, order = self._edge_index(0)
+        return order[indptr[v]:indptr[v + 1]]
+
+    def in_edge_ids(self, v: int) -> np.ndarray:
+        """Ids of the edges entering v, ascending."""
+        indptr, order = self._edge_index(2)
+        return order[indptr[v]:indptr[v + 1]]
+
+    def out_index(self, v: int) -> list:
+        """(rel, tail) of every edge leaving v."""
+        t = self.triples[self.out_edge_ids(v)]
+        return list(zip(t[:, 1].tolist(), t[:, 2].tolist()))
+
+    def in_index(self, v: int) -> list:
+        """(rel, head) of every edge entering v."""
+        t = self.triples[self.in_edge_ids(v)]
+        return list(zip(t[:, 1].tolist(), t[:, 0].tolist()))
+
     def checksum(self, split: Optional["DatasetSplit"] = None) -> str:
         """Same digest as ref:graph.py:101-109 (partition provenance)."""
         h = hashlib.sha256()
@@ -128,15 +160,40 @@ def generate_synthetic(num_entities: int, num_relations: int, avg_degree: float,
 
 @dataclass
 class GraphStats:
+    """Degree summary (ref:graph.py:401-420)."""
     num_entities: int
     num_relations: int
     num_edges: int
+    out_degree_min: int
+    out_degree_mean: float
     out_degree_max: int
+    in_degree_min: int
+    in_degree_mean: float
     in_degree_max: int
+
+    def format(self) -> str:
+        return (f"entities={self.num_entities} relations={self.num_relations} edges={self.num_edges}\n"
+                f"out-degree min/mean/max = {self.out_degree_min}/{self.out_degree_mean:.3f}/"
+                f"{self.out_degree_max}\n"
+                f"in-degree  min/mean/max = {self.in_degree_min}/{self.in_degree_mean:.3f}/{self.in_degree_max}")
 
 
 def graph_stats(graph: KnowledgeGraph) -> GraphStats:
     n = graph.num_entities
-    od = np.bincount(graph.triples[:, 0], minlength=n) if n else np.zeros(1, int)
-    idg = np.bincount(graph.triples[:, 2], minlength=n) if n else np.zeros(1, int)
-    return GraphStats(n, graph.num_relations, graph.num_edges, int(od.max()), int(idg.max()))
+    if n == 0:
+        return GraphStats(0, graph.num_relations, graph.num_edges, 0, 0.0, 0, 0, 0.0, 0)
+    deg = [np.bincount(graph.triples[:, c], minlength=n) for c in (0, 2)]
+    f = [(int(x.min()), float(x.mean()), int(x.max())) for x in deg]
+    return GraphStats(n, graph.num_relations, graph.num_edges, *f[0], *f[1])
+
+
+# Reference module-level names that live in io.py here (ref:graph.py:131-333); resolved
+# lazily so `from <pkg>.graph import X` works as with the reference.
+_IO_NAMES = ('load_dataset_dir', 'load_features', 'load_triples', 'read_dictionary', 'write_dataset_dir', 'write_dictionary', 'write_triples')
+
+
+def __getattr__(name):
+    if name in _IO_NAMES:
+        from . import io
+        return getattr(io, name)
+    raise AttributeError(name)

@@ -495,3 +495,13 @@ def bench_components(graph: KnowledgeGraph, model_config, train_config, worker_c
                 timing["epoch_time"] = wall / max(train_config.epochs, 1)
             rows.append({"partitioner": method, "workers": count, "rounds": report.rounds_per_epoch, **timing})
     return rows
+
+
+def format_bench_rows(rows: list) -> str:
+    """Fixed-width table of bench_components rows (ref:trainer.py:519-528)."""
+    cols = (("partitioner", 12, "s"), ("workers", 7, "d"), ("rounds", 6, "d"), ("epoch_time", 10, ".4f"),
+            ("cg_build", 11, ".6f"), ("encode", 10, ".6f"), ("loss_step", 12, ".6f"))
+    names = {"epoch_time": "epoch_s", "cg_build": "cg_build_s", "encode": "encode_s", "loss_step": "loss_step_s"}
+    out = [" ".join(f"{names.get(k, k):>{w}}" for k, w, _ in cols)]
+    out += [" ".join(format(r[k], f">{w}{f}") for k, w, f in cols) for r in rows]
+    return "\n".join(out)

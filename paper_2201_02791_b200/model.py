@@ -393,19 +393,32 @@ def device_backward(model: DeviceModel, bufs: ViewBuffers, grad_flat, input_grad
         torch.cuda.current_stream().wait_stream(side)
 
 
+FLAG_NONFINITE_SCORE, FLAG_NONFINITE_LOSS, FLAG_NONFINITE_PARAM = 1, 2, 4   # include/kgdist_b200.h
+FLAG_BAD_VERTEX, FLAG_PEER_TIMEOUT = 8, 16
+
+
+def raise_for_flags(f: int, what: str = "") -> None:
+    """Map a device status word (KG_FLAG_* bits) to the reference's error."""
+    if not f:
+        return
+    if f & FLAG_PEER_TIMEOUT:
+        raise ProtocolError("peer payload exchange timed out (a rank stopped publishing)")
+    if f & FLAG_NONFINITE_SCORE:
+        raise NumericError(f"non-finite score {what}".strip())
+    if f & FLAG_NONFINITE_LOSS:
+        raise NumericError("non-finite loss")
+    if f & FLAG_NONFINITE_PARAM:
+        raise NumericError("non-finite parameter after optimizer step")
+    if f & FLAG_BAD_VERTEX:
+        raise IntegrityError("vertex not present in compute graph")
+    raise NumericError(f"device status {f:#x}")
+
+
 def check_flags(bufs: ViewBuffers, what: str = "") -> None:
     f = int(bufs.flags.item())
     if f:
         bufs.flags.zero_()
-        if f & 1:
-            raise NumericError(f"non-finite score {what}".strip())
-        if f & 2:
-            raise NumericError("non-finite loss")
-        if f & 4:
-            raise NumericError("non-finite parameter after optimizer step")
-        if f & 8:
-            raise ProtocolError("peer payload exchange timed out (a rank stopped publishing)")
-        raise NumericError(f"device status {f:#x}")
+        raise_for_flags(f, what)
 
 
 # ---------------------------------------------------------------------------

@@ -221,3 +221,15 @@ def replication_factor(pset: PartitionSet) -> float:
     if pset.num_entities == 0:
         raise ValidationError("replication factor undefined for an empty graph")
     return sum(len(np.unique(p.all_edges()[:, [0, 2]])) for p in pset.partitions) / pset.num_entities
+
+
+# Reference module-level names that live in io.py here (ref:partition.py:304-482); resolved
+# lazily so `from <pkg>.partition import X` works as with the reference.
+_IO_NAMES = ('PartitionStats', 'partition_stats', 'read_partitions', 'write_partitions')
+
+
+def __getattr__(name):
+    if name in _IO_NAMES:
+        from . import io
+        return getattr(io, name)
+    raise AttributeError(name)

@@ -449,13 +449,91 @@ def make_batches(positives: np.ndarray, negatives: np.ndarray, batch_size: int,
 # Compute graph (ref:sampler.py:239-376)
 # ---------------------------------------------------------------------------
 
+@dataclass
+class LayerBlock:
+    """Message edges feeding one convolution, sorted by (relation, dst, src)
+    (ref:sampler.py:239-262). dst/src are compute-graph positions; by_dst /
+    by_src are stable permutations with their segment starts and unique keys.
+    The device kernels never materialise this: it is the inspection form of
+    a layer, built on request by `ComputeGraph.layers`."""
+    dst: np.ndarray
+    src: np.ndarray
+    rel: np.ndarray
+    norm: np.ndarray
+    rel_indptr: np.ndarray        # (2R + 2,) group boundaries by relation
+    num_targets: int
+    by_dst: np.ndarray
+    dst_segs: np.ndarray
+    dst_uniq: np.ndarray
+    by_src: np.ndarray
+    src_segs: np.ndarray
+    src_uniq: np.ndarray
+
+    @property
+    def num_edges(self) -> int:
+        return len(self.dst)
+
+
+def _device_segments(sorted_vals):
+    """Segment starts and keys of a sorted device vector (ref:sampler.py:265-269)."""
+    torch = _torch()
+    if sorted_vals.numel() == 0:
+        z = torch.zeros(0, dtype=torch.int64, device=sorted_vals.device)
+        return z, z
+    head = torch.ones_like(sorted_vals, dtype=torch.bool)
+    head[1:] = sorted_vals[1:] != sorted_vals[:-1]
+    starts = torch.nonzero(head).reshape(-1)
+    return starts, sorted_vals[starts]
+
+
+def _device_block(cg: "ComputeGraph", k: int) -> LayerBlock:
+    """Layer k's block on the device (ref:sampler.py:298-307, 359-368): every
+    partition message entering A_k (dst-CSR ranges of the targets) plus one
+    self-loop per target, lexsorted by (rel, dst, src) with three stable
+    sorts, then the by_dst / by_src permutations and segments."""
+    torch = _torch()
+    v = cg.view
+    counts = cg.layer_vertex_counts
+    T = counts[k]
+    dev = v.device
+    i64 = dict(dtype=torch.int64, device=dev)
+    tgt = cg.d_order[:T].long()
+    pos = cg.d_pos.long()
+    indptr = v.d_indptr.long()
+    starts = indptr[tgt]
+    lens = indptr[tgt + 1] - starts
+    E = int(lens.sum().item())
+    excl = torch.cumsum(lens, 0) - lens
+    eidx = torch.repeat_interleave(starts - excl, lens) + torch.arange(E, **i64)
+    sl = v.self_loop_rel
+    loops = torch.arange(T, **i64)
+    dst = torch.cat([torch.repeat_interleave(loops, lens), loops])
+    src = torch.cat([pos[v.d_ref_src.long()[eidx]], loops])
+    rel = torch.cat([v.d_ref_rel.long()[eidx], torch.full((T,), sl, **i64)])
+    norm = torch.cat([1.0 / v.d_msg_cnt[eidx].double(), torch.ones(T, dtype=torch.float64, device=dev)])
+    order = torch.arange(E + T, **i64)
+    for key in (src, dst, rel):               # LSD: np.lexsort((src, dst, rel))
+        order = order[torch.sort(key[order], stable=True).indices]
+    dst, src, rel, norm = dst[order], src[order], rel[order], norm[order]
+    rel_indptr = torch.searchsorted(rel, torch.arange(sl + 2, **i64))
+    by_dst = torch.sort(dst, stable=True).indices
+    dst_segs, dst_uniq = _device_segments(dst[by_dst])
+    by_src = torch.sort(src, stable=True).indices
+    src_segs, src_uniq = _device_segments(src[by_src])
+    h = [t.cpu().numpy() for t in (dst, src, rel, norm, rel_indptr, by_dst, dst_segs, dst_uniq, by_src,
+                                   src_segs, src_uniq)]
+    return LayerBlock(h[0], h[1], h[2], h[3], h[4], T, *h[5:])
+
+
 class ComputeGraph:
     """Layered closure of a batch, resident on the GPU.
 
     Device state: d_order (vertex_order, seeds ascending then each hop's new
     sources ascending), d_pos (local id -> position, -1 absent) and d_counts
-    (|A_0| .. |A_hops|, device int32). Nothing per-layer is materialised: the
-    RGCN kernels walk the partition CSR/CSC restricted to A_k.
+    (|A_0| .. |A_hops|, device int32). The RGCN kernels walk the partition
+    CSR/CSC restricted to A_k, so nothing per-layer is materialised for
+    training; `layers` builds the reference's LayerBlocks (output layer
+    first) on the device when asked for.
     """
 
     def __init__(self, view: PartitionView, hops: int, d_order, d_pos, d_counts):
@@ -499,6 +577,13 @@ class ComputeGraph:
 
     def layer_vertex_sets(self) -> list:
         return [self.vertex_order[:c] for c in self.layer_vertex_counts]
+
+    @property
+    def layers(self) -> list:
+        """LayerBlock per convolution, output layer first (ref:sampler.py:277)."""
+        if "layers" not in self._host:
+            self._host["layers"] = [_device_block(self, k) for k in range(self.hops)]
+        return self._host["layers"]
 
     def seed_positions(self, local_ids: np.ndarray) -> np.ndarray:
         p = self.pos[np.asarray(local_ids)]
