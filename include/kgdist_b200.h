@@ -421,6 +421,19 @@ kg_status kg_sparse_step(float* table, float* m, float* v, const float* grad, co
                          float beta1, float beta2, float eps, double bc1, double bc2, const int64_t* step_dev,
                          int32_t n_max, void* stream);
 
+/* Full-graph float64 encode for evaluation (ref:evaluate.py:107-122): every
+ * vertex of the whole-graph view g is a target at every layer; src / rel /
+ * cnt are the view's messages in reference order (same destination rows as
+ * g->indptr) with the per-(dst, relation) message counts (norm = 1 / cnt
+ * exactly); g's chunk table spreads hub rows over warps. dims[L+1];
+ * bases[l] (B, d_l, d_{l+1}), coeffs[l] (2R+1, B): HOST arrays of DEVICE
+ * float64 pointers. input (n, d_0), out (n, d_L) float64. B <= 8. */
+int64_t kg_encode_full_f64_workspace_bytes(int32_t n, int64_t e, int32_t chunk, int32_t B, int32_t d_max);
+kg_status kg_encode_full_f64(const kg_graph_csr* g, const int32_t* src, const int32_t* rel, const int32_t* cnt,
+                             int32_t L, const int32_t* dims, int32_t B, const double* const* bases,
+                             const double* const* coeffs, const double* input, double* out, void* ws,
+                             int64_t ws_bytes, void* stream);
+
 /* Given-candidates protocol (ref:evaluate.py:168-180), tail side only:
  * query i ranks candidate cand[cand_ptr[i] + true_pos[i]] (its true tail;
  * the caller appends it when absent) against cand[cand_ptr[i]..cand_ptr[i+1]).
@@ -452,13 +465,19 @@ kg_status kg_dropout_mask(kg_pcg64* g, const int32_t* counts, int32_t t, int32_t
  * CUDA-core tiles with an exact sequential fmaf chain per score. */
 /* known_pairs: an upper bound on sum over (query, side) of the known
  * candidates other than the true entity (impl 0 scores them in a separate
- * pass); *overflow (device uint32, optional) is set when it was too small. */
+ * pass); *overflow (device uint32, optional) is set when it was too small.
+ * H64 / decoder64 (optional, impl 0): the same embeddings and decoder in
+ * float64 (H = their fp32 rounding). The tensor-core pass then counts a
+ * candidate as greater only outside a per-row error band around the true
+ * score and decides every candidate inside the band (and the known ones in
+ * it) from float64 scores (H64[a] * dec64[r]) . H64[c] — the reference's
+ * arithmetic — so ranks follow the float64 scores exactly. */
 int64_t kg_eval_workspace_bytes(int64_t nq, int32_t N, int32_t d, int64_t known_pairs);
 kg_status kg_eval_filtered(const float* H, int32_t d, int32_t N, const float* decoder, int32_t R,
                            const int32_t* queries, int64_t nq, const int64_t* tail_keys, int64_t n_tail,
                            const int64_t* head_keys, int64_t n_head, int32_t policy, int32_t chunk,
                            int32_t impl, int64_t known_pairs, double* ranks, int32_t* ncand, uint32_t* overflow,
-                           void* ws, int64_t ws_bytes, void* stream);
+                           const double* H64, const double* decoder64, void* ws, int64_t ws_bytes, void* stream);
 /* Sorted unique keys (a*R + r)*N + c of (k,3) triples with (a,c) = (col_a, col_c). */
 int64_t kg_known_keys_workspace_bytes(int64_t k);
 kg_status kg_known_keys(const int32_t* triples, int64_t k, int32_t col_a, int32_t col_c, int32_t N, int32_t R,

@@ -137,7 +137,9 @@ _PROTOS = {
                             c_float, c_double, c_double, P, c_int32, P]),
     "kg_eval_workspace_bytes": (c_int64, [c_int64, c_int32, c_int32, c_int64]),
     "kg_eval_filtered": (ST, [P, c_int32, c_int32, P, c_int32, P, c_int64, P, c_int64, P, c_int64,
-                              c_int32, c_int32, c_int32, c_int64, P, P, P, P, c_int64, P]),
+                              c_int32, c_int32, c_int32, c_int64, P, P, P, P, P, P, c_int64, P]),
+    "kg_encode_full_f64_workspace_bytes": (c_int64, [c_int32, c_int64, c_int32, c_int32, c_int32]),
+    "kg_encode_full_f64": (ST, [POINTER(KgGraphCsr), P, P, P, c_int32, P, c_int32, P, P, P, P, P, c_int64, P]),
     "kg_known_keys_workspace_bytes": (c_int64, [c_int64]),
     "kg_known_keys": (ST, [P, c_int64, c_int32, c_int32, c_int32, c_int32, P, P, P, c_int64, P]),
     "kg_generate_synthetic": (c_int64, [c_int64, c_int32, c_int64, POINTER(KgPcg64), P, c_int64]),

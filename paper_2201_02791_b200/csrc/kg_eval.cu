@@ -304,7 +304,8 @@ int64_t kg_eval_workspace_bytes(int64_t nq, int32_t N, int32_t d, int64_t known_
 kg_status kg_eval_filtered(const float* H, int32_t d, int32_t N, const float* dec, int32_t R, const int32_t* qry,
                            int64_t nq, const int64_t* tkeys, int64_t ntk, const int64_t* hkeys, int64_t nhk,
                            int32_t policy, int32_t chunk, int32_t impl, int64_t known_pairs, double* ranks,
-                           int32_t* ncand, uint32_t* overflow, void* ws, int64_t ws_bytes, void* stream) {
+                           int32_t* ncand, uint32_t* overflow, const double* H64, const double* dec64, void* ws,
+                           int64_t ws_bytes, void* stream) {
   cudaStream_t st = as_stream(stream);
   KG_REQUIRE(policy >= 0 && policy <= 2, KG_ERR_VALIDATION, "unknown tie policy");
   KG_REQUIRE(chunk >= 1 && nq >= 1, KG_ERR_VALIDATION, "bad chunk / empty split");
@@ -312,7 +313,7 @@ kg_status kg_eval_filtered(const float* H, int32_t d, int32_t N, const float* de
              "eval workspace too small");
   if (impl == 0 && d <= 128)
     return umma_rank_filtered(H, d, N, dec, R, qry, nq, tkeys, ntk, hkeys, nhk, policy, chunk, known_pairs, ranks,
-                              ncand, overflow, ws, (size_t)ws_bytes, st);
+                              ncand, overflow, ws, (size_t)ws_bytes, st, H64, dec64);
   if (overflow) KG_CUDA(cudaMemsetAsync(overflow, 0, 4, st));
   Arena a(ws, (size_t)ws_bytes);
   float* ts = a.take<float>(2 * nq);

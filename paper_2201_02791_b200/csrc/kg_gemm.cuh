@@ -134,7 +134,8 @@ size_t umma_rank_workspace(int64_t nq, int32_t N, int d, int64_t max_pairs);
 kg_status umma_rank_filtered(const float* H, int d, int32_t N, const float* dec, int32_t R, const int32_t* qry,
                              int64_t nq, const int64_t* tkeys, int64_t ntk, const int64_t* hkeys, int64_t nhk,
                              int policy, int chunk, int64_t max_pairs, double* ranks, int32_t* ncand,
-                             uint32_t* overflow, void* ws, size_t ws_bytes, cudaStream_t st);
+                             uint32_t* overflow, void* ws, size_t ws_bytes, cudaStream_t st, const double* H64,
+                             const double* dec64);
 
 inline size_t gemm_nn_workspace(int64_t M_max, int64_t K, int64_t N) { return umma_nn_workspace(M_max, K, N); }
 inline kg_status gemm_nn(const GemmArgs& g, void* ws, cudaStream_t st) { return umma_gemm_nn(g, ws, st); }

@@ -617,7 +617,23 @@ struct RankArgs {
   float* ts;          // out: diagonal per row
   uint32_t* greater;  // out (accumulated): candidates scoring > ts
   uint32_t* equal;    // out (accumulated): candidates scoring == ts
+  // Banded mode (float64 refinement, kq != null): a candidate c counts as
+  // greater only when its score exceeds ts + w(x, c); scores within
+  // [ts - w, ts + w] are recorded (candidate id, RK_NEAR slots per row,
+  // nearc[x] counts them all) and decided in float64 afterwards.
+  const float* kq;     // per row: error-bound factor of the query
+  const float* kt;     // per row: kq * ||H[true]||
+  const float* hn;     // per candidate: ||H[c]||
+  uint32_t* nearc;
+  int32_t* near_c;
 };
+
+// Band half-width for (row, candidate): kq ||H[c]|| + kq ||H[true]|| — the
+// tensor-core scores of both are within kq/2 ||H|| of float64 (see
+// k_row_exact). Evaluated with explicit rounding so every site agrees.
+__device__ __forceinline__ float rk_band(float kq, float hn_c, float kt) { return __fmaf_rn(kq, hn_c, kt); }
+
+constexpr int RK_NEAR = 32;   // near-tie slots per row; rows with more are rescanned in float64
 
 constexpr int RK_EPI_WARPS = 8;
 constexpr int RK_THREADS = 64 + 32 * RK_EPI_WARPS;
@@ -780,9 +796,11 @@ __global__ void __launch_bounds__(RK_THREADS, 1) k_rank_umma(RankArgs a, const i
   } else {   // epilogue warps: TMEM lanes 32*(warp%4).., column half (warp-2)/4
     const int lanegrp = warp & 3, r = lanegrp * 32 + lane, colh = (warp - 2) >> 2;
     int64_t jc = 0;
+    const bool banded = a.kq != nullptr;
     for (int64_t tile = blockIdx.x; tile < qtiles; tile += gridDim.x) {
       const int64_t x = tile * 128 + r;
       float ts = 0.f;
+      const float kq = (banded && x < rows) ? a.kq[x] : 0.f, kt = (banded && x < rows) ? a.kt[x] : 0.f;
       uint32_t g = 0, e = 0;
       for (int j = 0; j < nj; ++j, ++jc) {
         const int acc = (int)(jc & 1);
@@ -796,6 +814,25 @@ __global__ void __launch_bounds__(RK_THREADS, 1) k_rank_umma(RankArgs a, const i
 #pragma unroll
           for (int i = 0; i < 32; ++i)
             if (i == lane) ts = v[i];
+        } else if (banded) {
+          const int32_t c0 = (j - 1) * 128 + colh * 64;
+          const int nvalid = a.ncols - c0;
+#pragma unroll
+          for (int ch = 0; ch < 4; ++ch) {
+            float v[16];
+            tmem_ld16(taddr + (uint32_t)(colh * 64 + ch * 16), v);
+#pragma unroll
+            for (int i = 0; i < 16; ++i) {
+              const bool ok = ch * 16 + i < nvalid && x < rows;
+              const float w = ok ? rk_band(kq, __ldg(a.hn + c0 + ch * 16 + i), kt) : 0.f;
+              const float band_hi = __fadd_rn(ts, w), band_lo = __fsub_rn(ts, w);
+              g += (ok && v[i] > band_hi) ? 1u : 0u;
+              if (ok && v[i] >= band_lo && v[i] <= band_hi) {   // rare: near-tie, decided in float64
+                const uint32_t k = atomicAdd(a.nearc + x, 1u);
+                if (k < (uint32_t)RK_NEAR) a.near_c[x * RK_NEAR + k] = c0 + ch * 16 + i;
+              }
+            }
+          }
         } else {
           const int32_t c0 = (j - 1) * 128 + colh * 64;
           const int nvalid = a.ncols - c0;   // columns of this half that exist
@@ -836,6 +873,132 @@ __global__ void __launch_bounds__(RK_THREADS, 1) k_rank_umma(RankArgs a, const i
   __syncthreads();
   tc_fence_after();
   if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(256));
+}
+
+// --- float64 near-tie refinement (banded mode) ------------------------------
+// s64(x, c) = sum_k (H[anc,k] * dec[rel,k]) * H[c,k] in float64 — the
+// reference's q = H[anchor] * decoder[r] product is exact in float64, its
+// dgemm differs from this warp sum only in summation order (~1e-16). Every
+// use (true score, near pairs, dense rows, known pairs) goes through this one
+// function, so a candidate compares identically wherever it is decided.
+__device__ __forceinline__ double rk_dot64(const double* __restrict__ H, const double* __restrict__ dec, int d,
+                                           int32_t anc, int32_t rel, int32_t c, int lane) {
+  double s = 0.0;
+  for (int k = lane; k < d; k += 32)
+    s = fma(H[(int64_t)anc * d + k] * dec[(int64_t)rel * d + k], H[(int64_t)c * d + k], s);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  return s;
+}
+
+// ||H[c]|| per candidate (float)
+__global__ void k_hnorm(const double* __restrict__ H, int32_t N, int d, float* __restrict__ hn) {
+  const int lane = (int)lane_id(), nw = (gridDim.x * blockDim.x) >> 5;
+  for (int64_t c = warp_uniform((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5); c < N; c += nw) {
+    double s = 0.0;
+    for (int k = lane; k < d; k += 32) s = fma(H[c * d + k], H[c * d + k], s);
+    s = warp_sum_d(s);
+    if (lane == 0) hn[c] = (float)sqrt(s);
+  }
+}
+
+// per row: the float64 true score and the error-bound factors. The fp32
+// rounding of H and q, the 3xTF32 split and the fp32 accumulation of d
+// products keep a tensor-core score within (d + 16) 2^-24 sum_k |q_k H[c,k]|
+// <= (d + 16) 2^-24 ||q|| ||H[c]|| of float64; kq = 2 (d + 16) 2^-23 ||q||
+// gives the band a 4x margin over the sum of both scores' bounds.
+__global__ void k_row_exact(const double* __restrict__ H, const double* __restrict__ dec, int d,
+                            const int32_t* __restrict__ qry, int64_t nq, const float* __restrict__ hn,
+                            double* __restrict__ ts64, float* __restrict__ kq, float* __restrict__ kt) {
+  const int lane = (int)lane_id(), nw = (gridDim.x * blockDim.x) >> 5;
+  for (int64_t x = warp_uniform((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5); x < 2 * nq; x += nw) {
+    int side;
+    int64_t q;
+    int32_t anc, rel, tru;
+    rk_query(qry, nq, x, side, q, anc, rel, tru);
+    const double t = rk_dot64(H, dec, d, anc, rel, tru, lane);
+    double qq = 0.0;
+    for (int k = lane; k < d; k += 32) {
+      const double v = H[(int64_t)anc * d + k] * dec[(int64_t)rel * d + k];
+      qq = fma(v, v, qq);
+    }
+    qq = warp_sum_d(qq);
+    if (lane == 0) {
+      ts64[x] = t;
+      const float f = (float)(2.0 * (d + 16) * 0x1p-23 * sqrt(qq));
+      kq[x] = f;
+      kt[x] = __fmul_rn(f, hn[tru]);
+    }
+  }
+}
+
+// near pairs of every row in float64; rows with more than RK_NEAR near
+// candidates are rescanned over all N candidates (their counts replaced)
+__global__ void k_near_refine(const double* __restrict__ H, const double* __restrict__ dec, int d, int32_t N,
+                              const int32_t* __restrict__ qry, int64_t nq, const double* __restrict__ ts64,
+                              const uint32_t* __restrict__ nearc, const int32_t* __restrict__ near_c,
+                              uint32_t* __restrict__ greater, uint32_t* __restrict__ equal) {
+  const int lane = (int)lane_id(), nw = (gridDim.x * blockDim.x) >> 5;
+  for (int64_t x = warp_uniform((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5); x < 2 * nq; x += nw) {
+    const uint32_t n = nearc[x];
+    if (n == 0) continue;
+    int side;
+    int64_t q;
+    int32_t anc, rel, tru;
+    rk_query(qry, nq, x, side, q, anc, rel, tru);
+    const double t = ts64[x];
+    uint32_t g = 0, e = 0;
+    const bool dense = n > (uint32_t)RK_NEAR;
+    const int64_t cnt = dense ? N : n;
+    for (int64_t i = 0; i < cnt; ++i) {
+      const int32_t c = dense ? (int32_t)i : near_c[x * RK_NEAR + i];
+      const double s = rk_dot64(H, dec, d, anc, rel, c, lane);
+      g += s > t;
+      e += s == t;
+    }
+    if (lane == 0) {
+      if (dense) {
+        greater[x] = g;
+        equal[x] = e;
+      } else {
+        greater[x] += g;
+        equal[x] += e;
+      }
+    }
+  }
+}
+
+// known candidates (banded mode): decided by the same rule as in the main
+// pass — float64 when the row was rescanned or the pair's score is in band
+__global__ void k_known_fix64(const int32_t* __restrict__ px, const int32_t* __restrict__ pc,
+                              const float* __restrict__ ps, const uint32_t* __restrict__ npairs,
+                              const float* __restrict__ ts, const float* __restrict__ kq,
+                              const float* __restrict__ kt, const float* __restrict__ hn,
+                              const double* __restrict__ ts64, const uint32_t* __restrict__ nearc,
+                              const double* __restrict__ H, const double* __restrict__ dec, int d,
+                              const int32_t* __restrict__ qry, int64_t nq, uint32_t* __restrict__ greater,
+                              uint32_t* __restrict__ equal) {
+  const int lane = (int)lane_id(), nw = (gridDim.x * blockDim.x) >> 5;
+  const int64_t n = *npairs;
+  for (int64_t i = warp_uniform((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5); i < n; i += nw) {
+    const int32_t x = px[i];
+    const float s = ps[i], t = ts[x], w = rk_band(kq[x], hn[pc[i]], kt[x]);
+    const float lo = __fsub_rn(t, w), hi = __fadd_rn(t, w);
+    const bool dense = nearc[x] > (uint32_t)RK_NEAR;
+    if (dense || (s >= lo && s <= hi)) {
+      int side;
+      int64_t q;
+      int32_t anc, rel, tru;
+      rk_query(qry, nq, x, side, q, anc, rel, tru);
+      const double s64 = rk_dot64(H, dec, d, anc, rel, pc[i], lane);
+      if (lane == 0) {
+        if (s64 > ts64[x]) atomicSub(greater + x, 1u);
+        if (s64 == ts64[x]) atomicSub(equal + x, 1u);
+      }
+    } else if (s > hi && lane == 0) {
+      atomicSub(greater + x, 1u);
+    }
+  }
 }
 
 // known (train+valid+test) candidates other than the true one, per row x
@@ -925,6 +1088,10 @@ struct RankWs {
   int64_t* lo;
   int32_t *px, *pc;
   char* scan;
+  double* ts64;
+  float *kq, *kt, *hn;
+  uint32_t* nearc;
+  int32_t* near_c;
 };
 
 static size_t rank_ws(int64_t nq, int32_t N, int d, int64_t max_pairs, RankWs* w, void* base, size_t cap) {
@@ -947,6 +1114,12 @@ static size_t rank_ws(int64_t nq, int32_t N, int d, int64_t max_pairs, RankWs* w
   r.px = a.take<int32_t>(max_pairs > 0 ? max_pairs : 1);
   r.pc = a.take<int32_t>(max_pairs > 0 ? max_pairs : 1);
   r.scan = a.take<char>(scan_workspace(2 * nq));
+  r.ts64 = a.take<double>(2 * nq);
+  r.kq = a.take<float>(2 * nq);
+  r.kt = a.take<float>(2 * nq);
+  r.hn = a.take<float>(N);
+  r.nearc = a.take<uint32_t>(2 * nq);
+  r.near_c = a.take<int32_t>((size_t)2 * nq * RK_NEAR);
   if (w) *w = r;
   return a.used + 1024;
 }
@@ -974,7 +1147,8 @@ static kg_status launch_rank(const RankArgs& ra, const int32_t* rows_dev, int64_
 kg_status umma_rank_filtered(const float* H, int d, int32_t N, const float* dec, int32_t R, const int32_t* qry,
                              int64_t nq, const int64_t* tkeys, int64_t ntk, const int64_t* hkeys, int64_t nhk,
                              int policy, int chunk, int64_t max_pairs, double* ranks, int32_t* ncand,
-                             uint32_t* overflow, void* ws, size_t ws_bytes, cudaStream_t st) {
+                             uint32_t* overflow, void* ws, size_t ws_bytes, cudaStream_t st, const double* H64,
+                             const double* dec64) {
   KG_REQUIRE(d >= 1 && d <= 128, KG_ERR_SHAPE, "tensor-core ranking supports d <= 128");
   RankWs w;
   KG_REQUIRE(rank_ws(nq, N, d, max_pairs, &w, ws, ws_bytes) <= ws_bytes, KG_ERR_VALIDATION,
@@ -990,10 +1164,22 @@ kg_status umma_rank_filtered(const float* H, int d, int32_t N, const float* dec,
   if (s != KG_OK) return s;
   KG_CUDA(cudaMemsetAsync(w.greater, 0, (size_t)rows * 4, st));
   KG_CUDA(cudaMemsetAsync(w.equal, 0, (size_t)rows * 4, st));
-  s = launch_rank(RankArgs{w.Qp, w.Tp, w.Cp, nk, rows, N, w.ts, w.greater, w.equal}, nullptr, rows, st);
-  if (s != KG_OK) return s;
-  // known candidates: pair list (row, candidate), diagonal scores, fix-up
+  const bool banded = H64 != nullptr && dec64 != nullptr;
   const int g1 = persistent_blocks(rows, 256, 8);
+  if (banded) {
+    KG_CUDA(cudaMemsetAsync(w.nearc, 0, (size_t)rows * 4, st));
+    KG_LAUNCH("k_hnorm", k_hnorm, persistent_blocks((int64_t)N * 32, 256, 8), 256, 0, st, H64, N, d, w.hn);
+    KG_LAUNCH("k_row_exact", k_row_exact, persistent_blocks(rows * 32, 256, 8), 256, 0, st, H64, dec64, d, qry, nq,
+              w.hn, w.ts64, w.kq, w.kt);
+  }
+  s = launch_rank(RankArgs{w.Qp, w.Tp, w.Cp, nk, rows, N, w.ts, w.greater, w.equal, banded ? w.kq : nullptr, w.kt,
+                           w.hn, w.nearc, w.near_c},
+                  nullptr, rows, st);
+  if (s != KG_OK) return s;
+  if (banded)
+    KG_LAUNCH("k_near_refine", k_near_refine, persistent_blocks(rows * 32, 256, 8), 256, 0, st, H64, dec64, d, N, qry,
+              nq, w.ts64, w.nearc, w.near_c, w.greater, w.equal);
+  // known candidates: pair list (row, candidate), diagonal scores, fix-up
   KG_LAUNCH("k_known_count", k_known_count, g1, 256, 0, st, qry, nq, N, R, tkeys, ntk, hkeys, nhk, w.cnt, w.lo);
   s = exclusive_scan_u32(w.cnt, w.off, rows, w.npairs, w.scan, scan_workspace(rows), st);
   if (s != KG_OK) return s;
@@ -1003,11 +1189,17 @@ kg_status umma_rank_filtered(const float* H, int d, int32_t N, const float* dec,
   KG_LAUNCH("k_eval_pack", k_eval_pack, persistent_blocks(pt * nk * 128 * 4, 256, 8), 256, 0, st, H, dec, qry, nq,
             (const int32_t*)w.px, (const int32_t*)w.pc, (const int32_t*)(w.npairs + 1), (int64_t)0, d, nk, w.Pq,
             w.Pc);
-  s = launch_rank(RankArgs{w.Pq, w.Pc, nullptr, nk, 0, 0, w.ps, nullptr, nullptr},
+  s = launch_rank(RankArgs{w.Pq, w.Pc, nullptr, nk, 0, 0, w.ps, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr,
+                           nullptr},
                   reinterpret_cast<const int32_t*>(w.npairs + 1), max_pairs, st);
   if (s != KG_OK) return s;
-  KG_LAUNCH("k_known_fix", k_known_fix, persistent_blocks(max_pairs > 0 ? max_pairs : 1, 256, 8), 256, 0, st, w.px,
-            w.ps, w.npairs + 1, w.ts, w.greater, w.equal);
+  if (banded)
+    KG_LAUNCH("k_known_fix64", k_known_fix64, persistent_blocks((max_pairs > 0 ? max_pairs : 1) * 32, 256, 8), 256, 0,
+              st, w.px, w.pc, w.ps, w.npairs + 1, w.ts, w.kq, w.kt, w.hn, w.ts64, w.nearc, H64, dec64, d, qry, nq,
+              w.greater, w.equal);
+  else
+    KG_LAUNCH("k_known_fix", k_known_fix, persistent_blocks(max_pairs > 0 ? max_pairs : 1, 256, 8), 256, 0, st, w.px,
+              w.ps, w.npairs + 1, w.ts, w.greater, w.equal);
   if (overflow) KG_CUDA(cudaMemcpyAsync(overflow, w.npairs + 2, 4, cudaMemcpyDeviceToDevice, st));
   KG_LAUNCH("k_rank_policy", k_rank_policy, g1, 256, 0, st, nq, N, policy, chunk, w.greater, w.equal, w.cnt, ranks,
             ncand);

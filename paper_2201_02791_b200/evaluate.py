@@ -11,8 +11,8 @@ import numpy as np
 
 from . import _lib
 from .errors import IntegrityError, KGError, ValidationError
-from .model import MODE_EMBEDDING, DeviceModel, ModelConfig, ModelParams, ViewBuffers, device_forward
-from .sampler import closure_device, full_graph_view
+from .model import MODE_EMBEDDING, ModelConfig, ModelParams
+from .sampler import full_graph_view
 
 TIE_MEAN = "mean"
 TIE_OPTIMISTIC = "optimistic"
@@ -78,12 +78,15 @@ def filtered_candidates(test_triplet, side: str, all_known_triples, num_entities
     return np.array(out, dtype=np.int64)
 
 
-def _device_encode_all(params: ModelParams, config: ModelConfig, graph):
-    """Full-graph encode on the device; returns (H tensor (N, d_out), view)."""
+def _device_encode_all64(params: ModelParams, config: ModelConfig, graph):
+    """Full-graph encode in float64 on the device (kg_encode_full_f64): the
+    evaluation's embeddings carry the reference's precision, so ranks among
+    near-tied candidates follow the reference (ref:evaluate.py:107-122).
+    Returns (H float64 tensor (N, d_out), view)."""
+    import ctypes
     import torch
     view = full_graph_view(graph)
     dev = view.device
-    N = graph.num_entities
     if config.mode == MODE_EMBEDDING:
         if params.entity_embed is None:
             raise ValidationError("embedding mode requires an entity table")
@@ -92,23 +95,35 @@ def _device_encode_all(params: ModelParams, config: ModelConfig, graph):
         if graph.features is None:
             raise ValidationError("feature mode requires graph features")
         table = graph.features
-    seeds = torch.arange(N, dtype=torch.int32, device=dev)
-    cg = closure_device(view, config.num_layers, seed_ids=seeds)
-    model = DeviceModel.from_params(config, params, dev)
-    rows = torch.as_tensor(np.ascontiguousarray(table, dtype=np.float32)).to(dev)
-    bufs = ViewBuffers(config, view, 1, input_rows=rows)
-    bufs.order.copy_(cg.d_order)
-    bufs.pos.copy_(cg.d_pos)
-    bufs.counts.copy_(cg.d_counts)
-    device_forward(model, bufs)
-    return bufs.H[-1], model, view
+    table = np.asarray(table)
+    if table.ndim != 2 or table.shape[1] != config.dims[0]:
+        raise ValidationError(f"input width != d_in {config.dims[0]}")
+    f64 = lambda a: torch.as_tensor(np.ascontiguousarray(a, dtype=np.float64)).to(dev)
+    L, B = config.num_layers, config.num_bases
+    bases = [f64(b) for b in params.bases]
+    coeffs = [f64(c) for c in params.coeffs]
+    inp = f64(table[: graph.num_entities])
+    N = graph.num_entities
+    out = torch.empty((N, config.dims[-1]), dtype=torch.float64, device=dev)
+    lib = _lib.require_cuda()
+    csr = view.csr()
+    ws = torch.empty(lib.kg_encode_full_f64_workspace_bytes(N, csr.e, csr.chunk, B, max(config.dims)),
+                     dtype=torch.uint8, device=dev)
+    dims = (ctypes.c_int32 * (L + 1))(*config.dims)
+    pb = (ctypes.c_void_p * L)(*[b.data_ptr() for b in bases])
+    pc = (ctypes.c_void_p * L)(*[c.data_ptr() for c in coeffs])
+    _lib.call("kg_encode_full_f64", ctypes.byref(csr), view.d_ref_src.data_ptr(), view.d_ref_rel.data_ptr(),
+              view.d_msg_cnt.data_ptr(), L, dims, B, pb, pc, inp.data_ptr(), out.data_ptr(), ws.data_ptr(),
+              ws.numel(), _lib.stream_handle())
+    return out, view
 
 
 def encode_all_entities(params: ModelParams, config: ModelConfig, graph) -> np.ndarray:
     """Embeddings of every entity from message passing over the whole graph
-    (ref:evaluate.py:107-122); rows align with entity ids."""
-    H, _, _ = _device_encode_all(params, config, graph)
-    return H.double().cpu().numpy()
+    (ref:evaluate.py:107-122), computed in float64 on the device; rows align
+    with entity ids."""
+    H, _ = _device_encode_all64(params, config, graph)
+    return H.cpu().numpy()
 
 
 def _known_keys(triples: np.ndarray, col_a: int, col_c: int, N: int, R: int, dev):
@@ -168,13 +183,15 @@ def _evaluate_candidates(params, config, graph, q, candidates: dict, tie_policy:
     flat = np.concatenate(lists)
     if flat.min() < 0 or flat.max() >= graph.num_entities:
         raise IntegrityError("candidate entity id out of range")
-    H, model, view = _device_encode_all(params, config, graph)
+    H64, view = _device_encode_all64(params, config, graph)
+    H = H64.float()
     dev = view.device
     t = lambda a, dt: torch.as_tensor(np.ascontiguousarray(a, dtype=dt)).to(dev)
+    dec = t(params.decoder, np.float32)
     dq, dptr, dc, dt_ = t(q, np.int32), t(ptr, np.int64), t(flat, np.int32), t(tpos, np.int32)
     ranks = torch.empty(nq, dtype=torch.float64, device=dev)
     ncand = torch.empty(nq, dtype=torch.int32, device=dev)
-    _lib.call("kg_eval_candidates", H.data_ptr(), config.dims[-1], model.decoder_ptr(), dq.data_ptr(), nq,
+    _lib.call("kg_eval_candidates", H.data_ptr(), config.dims[-1], dec.data_ptr(), dq.data_ptr(), nq,
               dptr.data_ptr(), dc.data_ptr(), dt_.data_ptr(), _POLICY[tie_policy], ranks.data_ptr(),
               ncand.data_ptr(), _lib.stream_handle())
     r, c = ranks.cpu().numpy(), ncand.cpu().numpy()
@@ -189,8 +206,11 @@ def evaluate(params: ModelParams, config: ModelConfig, graph, split, which: str 
              protocol: str = "filtered", candidates: Optional[dict] = None, tie_policy: str = TIE_MEAN,
              chunk: int = 512, impl: int = 0) -> EvalResult:
     """Rank every triple of the split against all entities on both sides,
-    filtered by train+valid+test (ref:evaluate.py:136-218). impl 0: tensor-core
-    scores (d <= 128); 1: exact CUDA-core fmaf chains."""
+    filtered by train+valid+test (ref:evaluate.py:136-218), from the float64
+    full-graph encode. impl 0: tensor-core scores (3xTF32, d <= 128) with
+    every candidate inside the per-row error band around the true score
+    decided in float64 (ranks follow the reference's float64 scores);
+    impl 1: CUDA-core tiles, an exact sequential fmaf chain per fp32 score."""
     import torch
     if which not in ("valid", "test"):
         raise ValidationError("which must be valid or test")
@@ -205,8 +225,11 @@ def evaluate(params: ModelParams, config: ModelConfig, graph, split, which: str 
         raise ValidationError(f"unknown tie policy {tie_policy!r}")
     if protocol == "candidates":
         return _evaluate_candidates(params, config, graph, q, candidates, tie_policy)
-    H, model, view = _device_encode_all(params, config, graph)
+    H64, view = _device_encode_all64(params, config, graph)
+    H = H64.float()
     dev = view.device
+    dec64 = torch.as_tensor(np.ascontiguousarray(params.decoder, dtype=np.float64)).to(dev)
+    dec = dec64.float()
     N, R = graph.num_entities, graph.num_relations
     known = split.all_triples()
     tkeys, ntk = _known_keys(known, 0, 2, N, R, dev)
@@ -219,10 +242,10 @@ def evaluate(params: ModelParams, config: ModelConfig, graph, split, which: str 
     pairs = _known_pair_bound(tkeys, ntk, hkeys, nhk, dq, N, R)
     ws = torch.empty(lib.kg_eval_workspace_bytes(nq, N, config.dims[-1], pairs), dtype=torch.uint8, device=dev)
     overflow = torch.zeros(1, dtype=torch.int32, device=dev)
-    _lib.call("kg_eval_filtered", H.data_ptr(), config.dims[-1], N, model.decoder_ptr(), R, dq.data_ptr(), nq,
+    _lib.call("kg_eval_filtered", H.data_ptr(), config.dims[-1], N, dec.data_ptr(), R, dq.data_ptr(), nq,
               tkeys.data_ptr(), ntk, hkeys.data_ptr(), nhk, _POLICY[tie_policy], chunk, impl, pairs,
-              ranks.data_ptr(), ncand.data_ptr(), overflow.data_ptr(), ws.data_ptr(), ws.numel(),
-              _lib.stream_handle())
+              ranks.data_ptr(), ncand.data_ptr(), overflow.data_ptr(), H64.data_ptr() if impl == 0 else None,
+              dec64.data_ptr() if impl == 0 else None, ws.data_ptr(), ws.numel(), _lib.stream_handle())
     if int(overflow.item()):
         raise KGError("internal: known-candidate pair bound exceeded")
     r = ranks.cpu().numpy()

@@ -238,7 +238,7 @@ def scenario_fb_structure(name):
         "train_sha": np.frombuffer(hashlib.sha256(split.train.tobytes()).hexdigest().encode(),
                                    dtype=np.uint8),
     }
-    for P in (2, 4, 8):
+    for P in (1, 2, 4, 8):
         pset = kpart.vertex_cut_partition(graph, P, seed=0)
         assign = np.empty(graph.num_edges, dtype=np.int8)
         for p in pset.partitions:

@@ -44,7 +44,7 @@ def test_generator_and_vertex_cut_fb15k_shape():
     graph, split = generate_synthetic(14541, 237, 272115 / 14541, seed=0)
     assert graph.checksum(split) == bytes(g["checksum"]).decode()
     assert len(split.train) == int(g["num_train"]) == 272116
-    for P in (2, 4, 8):
+    for P in (1, 2, 4, 8):
         pset = vertex_cut_partition(graph, P, seed=0)
         assign = np.empty(graph.num_edges, dtype=np.int8)
         for p in pset.partitions:

@@ -1,8 +1,13 @@
 """Criterion 09 of the reference acceptance suite, split into its parts
 (size / message-edge work / wall clock) to classify its result on a GPU.
 Run from baseline/_ref/ref_tests with the kgdist alias on PYTHONPATH."""
+import os
+import sys
+
 import numpy as np
-import test_acceptance as ta
+
+sys.path.insert(0, os.getcwd())
+import test_acceptance as ta  # noqa: E402
 from kgdist.partition import neighborhood_expand, random_edge_partition, vertex_cut_partition
 from kgdist.trainer import TrainConfig, train
 
