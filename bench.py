@@ -50,7 +50,8 @@ def parse_args():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--batch", type=int, default=BATCH)
-    ap.add_argument("--roofline-kernel", default="k_aggregate")
+    ap.add_argument("--roofline-kernels", default="k_csc_backward,k_csc_dots,k_aggregate",
+                    help="kernels timed live (comma-separated exact names)")
     ap.add_argument("--parts", type=int, default=0,
                     help="diagnostic: partitions (a multiple of the rank count; default one per GPU)")
     ap.add_argument("--no-e2e", action="store_true")
@@ -93,6 +94,16 @@ def build_inputs(P, batch):
     mc = kb.ModelConfig(2, list(DIMS), BASES, graph.num_relations, 1, mode=kb.MODE_EMBEDDING)
     tc = kb.TrainConfig(epochs=1, batch_size=batch, optimizer="adam", learning_rate=0.01, seed=0)
     return graph, split, pset, mc, tc
+
+
+def workload_config(P, world, batch, rounds, entities, relations, train_triples, global_batch, parallelism):
+    """The `config` object of both arms' JSON lines (same keys)."""
+    return {"workload": f"fb15k237-shape synthetic KG, P={P} partitions (vertex cut + 2-hop halo), "
+                        f"b={batch}/partition",
+            "model": "RGCN 2x100 (2 bases) + DistMult, 1 neg/pos, Adam 0.01, embedding mode",
+            "global_batch": global_batch, "per_gpu_batch": batch * P // world, "rounds_per_epoch": rounds,
+            "parallelism": parallelism, "l2": "flushed between timed steps (256 MiB write)",
+            "graph": {"entities": entities, "relations": relations, "train_triples": train_triples}}
 
 
 # ---------------------------------------------------------------------------
@@ -166,8 +177,10 @@ def layer_shapes(tr, w):
 
 
 def algorithmic_bytes(kernel, tr, w):
-    """Bytes a launch must move at minimum (fp32 values, int32 ids, per unit
-    figures of SURVEY.md §8(d) restated in DESIGN.md §4)."""
+    """Bytes a launch must move at minimum, summed over the layers (fp32
+    values, int32 ids; the per-unit figures of SURVEY.md §8(d)).
+    "csc_family" is the one-pass model of the whole CSC backward (dS + edge
+    dots: what a single pass over the CSC would have to move)."""
     dims, B = tr.mc.dims, tr.mc.num_bases
     total = 0
     for l, (T, S, E) in enumerate(layer_shapes(tr, w)):
@@ -177,11 +190,61 @@ def algorithmic_bytes(kernel, tr, w):
             # target: self row read + B*d_in accumulator row written
             total += E * (12 + 4 * di) + T * (4 * di + 4 * B * di + 4)
         elif kernel == "k_csc_backward":
-            # per source row: Y row read, dS row written; per CSC edge: dst+rel+
-            # norm+pos (16 B) + dZ row gathered + B floats edge dots written;
-            # per target: self dZ row + B self dots
+            # dS pass: per source row the dS row written; per CSC edge dst+rel+
+            # norm+pos (16 B) + the dZ row gathered; per target its self dZ row
+            total += S * (4 * B * do + 4) + E * (16 + 4 * do) + T * 4 * do
+        elif kernel == "k_csc_dots":
+            # edge-dot pass: per source row the Y row read; per CSC edge 16 B
+            # metadata + dZ row gathered + B dots written; per target self dZ + B dots
+            total += S * (4 * B * do + 4) + E * (16 + 4 * do + 4 * B) + T * (4 * do + 4 * B)
+        elif kernel == "csc_family":
             total += S * (8 * B * do + 4) + E * (16 + 4 * do + 4 * B) + T * (4 * do + 4 * B)
     return total
+
+
+def live_roofline(tr, kt, step_ms):
+    """Roofline object of the JSON line from the live per-kernel event times
+    `kt` {name: [total_ms, launches]}: the dominant kernel family (the CSC
+    backward: dS pass + edge-dot pass, one launch each per layer) against the
+    one-pass byte model, and every timed kernel alone."""
+    w0 = tr.workers[0]
+    L = max(tr.mc.num_layers, 1)
+    peaks = {}
+    pk_path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.isfile(pk_path):
+        peaks = json.load(open(pk_path))
+    peak = float(peaks.get("hbm_gbs", 6650.0))
+    per = {}
+    for name, (ms, n) in kt.items():
+        if n == 0:
+            continue
+        avg = ms / n
+        alg = algorithmic_bytes(name, tr, w0) / L
+        per[name] = {"avg_launch_ms": avg, "launches_timed": n, "alg_bytes_per_launch": alg,
+                     "achieved": alg / (avg / 1e3) / 1e9, "frac": alg / (avg / 1e3) / 1e9 / peak,
+                     "share_of_step": avg * L / step_ms if step_ms > 0 else None}
+    fam = [k for k in ("k_csc_backward", "k_csc_dots") if k in per]
+    if fam:
+        t = sum(per[k]["avg_launch_ms"] for k in fam)
+        alg = algorithmic_bytes("csc_family", tr, w0) / L
+        kernel, achieved, avg, share = "+".join(fam), alg / (t / 1e3) / 1e9, t, t * L / step_ms
+    else:
+        k0 = next(iter(per))
+        kernel, alg, achieved, avg, share = k0, per[k0]["alg_bytes_per_launch"], per[k0]["achieved"], \
+            per[k0]["avg_launch_ms"], per[k0]["share_of_step"]
+    traffic, traffic_src = None, None
+    tpath = os.path.join(ROOT, "profiles", "r2_roofline_traffic.json")
+    if os.path.isfile(tpath):
+        tj = json.load(open(tpath))
+        if tj.get("kernel") == kernel:
+            traffic, traffic_src = tj.get("traffic_bytes_per_launch"), tj.get("source")
+    return {"bound": "hbm", "kernel": kernel, "achieved": achieved, "peak": peak,
+            "peak_source": "MEASURED_PEAKS.json hbm_gbs" if peaks else "fallback 6650 GB/s",
+            "unit": "GB/s", "frac": achieved / peak, "traffic": traffic, "traffic_source": traffic_src,
+            "alg_bytes_per_launch": alg, "avg_launch_ms": avg, "kernel_share_of_step": share,
+            "alg_model": "one CSC pass per layer: S*(8*B*d+4) + E*(16+4*d+4*B) + T*(4*d+4*B) bytes",
+            "kernels": per,
+            "note": "FB15k-237 working set is L2-resident (H7): effective bandwidth vs HBM peak"}
 
 
 # ---------------------------------------------------------------------------
@@ -198,7 +261,7 @@ def run_ours(args, world, rank, local):
     graph, split, pset, mc, tc = build_inputs(P, args.batch)
     tr = kb.Trainer(pset, graph, mc, tc)
     tr.use_graphs = os.environ.get("KG_CUDA_GRAPHS", "1") != "0"
-    tr.timer_prefix = args.roofline_kernel      # events around this kernel are captured into the graphs
+    tr.timer_prefix = args.roofline_kernels     # events around these kernels are captured into the graphs
 
     def step():
         if tr.round_in_epoch == 0 or tr.round_in_epoch >= tr.rounds:
@@ -219,8 +282,9 @@ def run_ours(args, world, rank, local):
     import ctypes
     launches0 = lib.kg_launch_count()
     g0 = tr.graph_kernel_launches
-    kt_ms, kt_n = ctypes.c_double(0), ctypes.c_int64(0)
-    lib.kg_kernel_timer_begin(args.roofline_kernel.encode())   # eager launches (graphs off)
+    names = [k for k in args.roofline_kernels.split(",") if k]
+    kt = {k: [0.0, 0] for k in names}
+    lib.kg_kernel_timer_begin(args.roofline_kernels.encode())   # eager launches (graphs off)
     with ClockSampler(local) as clk:
         # the K timed steps: no host synchronisation inside the loop (the host
         # runs ahead, as in a training loop), events on the launch stream
@@ -234,21 +298,27 @@ def run_ours(args, world, rank, local):
     if tr.dist:
         torch.distributed.barrier()
     step_ms = sum(a.elapsed_time(b) for a, b in evs)
-    # roofline kernel: its events are captured into the replayed graphs; read
-    # them over a few extra steps (each read synchronises, so not in the loop above)
+    # roofline kernels: their events are captured into the replayed graphs;
+    # read them over a few extra steps (each read synchronises, so not in the
+    # loop above)
     for _ in range(min(args.steps, 6)):
         flush.zero_()
         step()
         if tr.use_graphs and tr.last_timer_handle is not None:
-            ms, n = ctypes.c_double(0), ctypes.c_int64(0)
-            lib.kg_kernel_timer_read(tr.last_timer_handle, ctypes.byref(ms), ctypes.byref(n))
-            kt_ms.value += ms.value
-            kt_n.value += n.value
+            for name in names:
+                ms, n = ctypes.c_double(0), ctypes.c_int64(0)
+                lib.kg_kernel_timer_read_named(tr.last_timer_handle, name.encode(), ctypes.byref(ms),
+                                               ctypes.byref(n))
+                kt[name][0] += ms.value
+                kt[name][1] += n.value
     torch.cuda.synchronize()
-    e_ms, e_n = ctypes.c_double(0), ctypes.c_int64(0)
-    lib.kg_kernel_timer_end(ctypes.byref(e_ms), ctypes.byref(e_n))
-    kt_ms.value += e_ms.value
-    kt_n.value += e_n.value
+    buf = ctypes.create_string_buffer(1 << 14)
+    lib.kg_kernel_timer_dump(buf, 1 << 14)
+    for ln in buf.value.decode().splitlines():
+        name, cnt, ms = ln.rsplit(",", 2)
+        if name in kt:
+            kt[name][0] += float(ms)
+            kt[name][1] += int(cnt)
     tr.check()
     t_max = torch.tensor([step_ms], dtype=torch.float64, device=dev)
     rank_ms = [step_ms]
@@ -260,34 +330,7 @@ def run_ours(args, world, rank, local):
     total_ms = float(t_max.item())
     triples_per_step = sum(tr.sizes)          # every partition's batch, all ranks
     value = args.steps * triples_per_step / (total_ms / 1e3)
-
-    # live roofline of the instrumented kernel (rank 0's launches)
-    w0 = tr.workers[0]
-    alg = algorithmic_bytes(args.roofline_kernel, tr, w0)
-    per_launch_alg = alg / max(tr.mc.num_layers, 1)
-    avg_launch_ms = kt_ms.value / max(kt_n.value, 1)
-    peaks = {}
-    pk_path = os.path.join(ROOT, "MEASURED_PEAKS.json")
-    if os.path.isfile(pk_path):
-        peaks = json.load(open(pk_path))
-    peak = float(peaks.get("hbm_gbs", 6650.0))
-    achieved = per_launch_alg / (avg_launch_ms / 1e3) / 1e9 if avg_launch_ms > 0 else None
-    # DRAM bytes per launch of this kernel from one ncu --set full capture of
-    # the same command (tools/ncu_traffic.sh -> profiles/r1_roofline_traffic.json)
-    traffic, traffic_src = None, None
-    tpath = os.path.join(ROOT, "profiles", "r1_roofline_traffic.json")
-    if args.roofline_kernel == "k_aggregate" and os.path.isfile(tpath):
-        tj = json.load(open(tpath))
-        traffic, traffic_src = tj.get("traffic_bytes_per_launch"), tj.get("source")
-    roofline = {"bound": "hbm", "kernel": args.roofline_kernel, "achieved": achieved, "peak": peak,
-                "peak_source": "MEASURED_PEAKS.json hbm_gbs" if peaks else "fallback 6650 GB/s",
-                "unit": "GB/s", "frac": (achieved / peak) if achieved else None,
-                "traffic": traffic, "traffic_source": traffic_src, "alg_bytes_per_launch": per_launch_alg,
-                "avg_launch_ms": avg_launch_ms, "launches_timed": kt_n.value,
-                # launches per step (one per layer) x average launch / average step
-                "kernel_share_of_step": (avg_launch_ms * max(tr.mc.num_layers, 1) / (step_ms / args.steps))
-                if step_ms > 0 else None,
-                "note": "FB15k-237 working set is L2-resident (H7): effective bandwidth vs HBM peak"}
+    roofline = live_roofline(tr, kt, step_ms / args.steps)
 
     # e2e through the public API (host inputs -> train() -> host params)
     e2e = None
@@ -338,15 +381,10 @@ def run_ours(args, world, rank, local):
         line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
                 "warmup": max(args.warmup, 3), "ms_per_step": total_ms / args.steps, "higher_is_better": True,
                 "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-                "config": {"workload": f"fb15k237-shape synthetic KG, P={P} partitions (vertex cut + 2-hop "
-                                       f"halo), b={args.batch}/partition",
-                           "model": "RGCN 2x100 (2 bases) + DistMult, 1 neg/pos, Adam 0.01, embedding mode",
-                           "global_batch": triples_per_step, "per_gpu_batch": args.batch * P // world,
-                           "rounds_per_epoch": tr.rounds, "parallelism": f"dp{world} (one partition per GPU)" if P == world
-                           else f"dp{world}, {P // world} partitions per GPU",
-                           "l2": "flushed between timed steps (256 MiB write)",
-                           "graph": {"entities": graph.num_entities, "relations": graph.num_relations,
-                                     "train_triples": graph.num_edges}},
+                "config": workload_config(P, world, args.batch, tr.rounds, graph.num_entities, graph.num_relations,
+                                          graph.num_edges, triples_per_step,
+                                          parallelism=f"dp{world} (one partition per GPU)" if P == world
+                                          else f"dp{world}, {P // world} partitions per GPU"),
                 "e2e": e2e, "gpu_launches": int(launches), "roofline": roofline, "cpu_baseline": cpu,
                 "rank_ms": [round(x, 3) for x in rank_ms],
                 "step_ms": [round(a.elapsed_time(b), 4) for a, b in evs],
@@ -384,22 +422,21 @@ def cpu_baseline(args, pset, graph, mc, rounds=None):
 def run_reference(args, world, rank):
     """--impl reference: the reference's CPU algorithm (numpy port under
     oracle/, the reference being pure Python that cannot travel) on this
-    host's cores, same metric/config; rank 0 only."""
+    host's cores, same metric/config; rank 0 only. Inputs come from the
+    oracle's own restatement of the reference's generator and partitioner
+    (oracle/kg_inputs.py): the package and its kernel library are not loaded."""
     if rank != 0:
         return
+    import kg_inputs as ki
     import kg_oracle as ko
-    sys.path.insert(0, ROOT)
-    import paper_2201_02791_b200 as kb
-    graph, split = kb.generate_synthetic(FB["num_entities"], FB["num_relations"], FB["avg_degree"], FB["seed"])
-    pset = kb.neighborhood_expand(kb.vertex_cut_partition(graph, world, seed=0), graph, 2)
+    g = ki.synthetic_graph(FB["num_entities"], FB["num_relations"], FB["avg_degree"], FB["seed"])
+    parts = ki.partition_inputs(g, world, seed=0, hops=2)
     views, ends = [], []
-    for p in pset.partitions:
-        views.append(ko.make_view(p.core, p.support, graph.num_entities, graph.num_relations,
-                                  partition_id=p.id, pool_size=p.pool_size))
+    for p in parts:
+        views.append(ko.make_view(p.core, p.support, g.num_entities, g.num_relations, partition_id=p.pid,
+                                  pool_size=p.pool_size))
         ends.append(np.concatenate([p.core_vertices, p.replicated_vertices]))
-    mc_dims = list(DIMS)
-    op = ko.init_params(mc_dims, BASES, graph.num_relations, np.random.default_rng(0),
-                        num_entities=graph.num_entities)
+    op = ko.init_params(list(DIMS), BASES, g.num_relations, np.random.default_rng(0), num_entities=g.num_entities)
     # warmup rounds then timed rounds; each round processes P * b triples
     ko.train(views, ends, op, 1, 1, batch_size=args.batch, seed=0, max_rounds=max(1, min(args.warmup, 1)))
     t0 = time.perf_counter()
@@ -420,11 +457,13 @@ def run_reference(args, world, rank):
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": secs * 1e3 / args.steps, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic", "impl": "reference",
-            "config": {"workload": f"fb15k237-shape synthetic KG, P={world} partitions (vertex cut + 2-hop halo), "
-                                   f"b={args.batch}/partition", "parallelism": f"{world} partitions, in-order on CPU"},
+            "config": workload_config(world, world, args.batch, rounds_per_epoch, g.num_entities, g.num_relations,
+                                      len(g.train), world * args.batch,
+                                      parallelism=f"{world} partitions, in-order on CPU"),
             "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port",
                              "sample": f"{args.steps} rounds x {world} partitions of b={args.batch} (per-epoch "
-                                       f"sampling included), oracle/kg_oracle.py fp64 numpy port"},
+                                       f"sampling included), oracle/kg_oracle.py fp64 numpy port; inputs from "
+                                       f"oracle/kg_inputs.py"},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 

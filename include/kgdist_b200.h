@@ -117,9 +117,10 @@ kg_status kg_graph_upload(void* graph_exec, void* stream);
 int kg_last_error(char* buf, int64_t n); /* host buffer */
 /* Number of kernels this library has launched in the process. */
 int64_t kg_launch_count(void);
-/* Bracket every launch of the kernel named `prefix` ("" = all kernels; host
- * string) with CUDA events on the launching stream; _end synchronises and
- * returns the summed device time and the launch count. */
+/* Bracket every launch of the kernels named in `prefix` (comma-separated
+ * exact kernel names, "" = all kernels; host string) with CUDA events on the
+ * launching stream; _end synchronises and returns the summed device time and
+ * the launch count. */
 kg_status kg_kernel_timer_begin(const char* prefix);
 kg_status kg_kernel_timer_end(double* total_ms, int64_t* launches);
 /* Ends the timer and writes "name,launches,total_ms" lines (host buffer). */
@@ -130,6 +131,8 @@ kg_status kg_kernel_timer_dump(char* buf, int64_t n);
  * elapsed time after a replay (synchronises on its events). */
 kg_status kg_kernel_timer_detach(int64_t* handle);
 kg_status kg_kernel_timer_read(int64_t handle, double* total_ms, int64_t* launches);
+/* As _read, restricted to the launches of kernel `name` (host string). */
+kg_status kg_kernel_timer_read_named(int64_t handle, const char* name, double* total_ms, int64_t* launches);
 
 /* ---------------------------------------------------------------------- */
 /* Primitives (stable radix sort / scan) used by every stage below          */

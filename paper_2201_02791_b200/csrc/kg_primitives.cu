@@ -570,7 +570,7 @@ namespace kg {
 
 static int64_t g_launches = 0;
 static bool g_timer_on = false;
-static char g_timer_prefix[128] = "";
+static char g_timer_prefix[512] = "";
 static std::vector<cudaEvent_t> g_ev_start, g_ev_end;
 static std::vector<const char*> g_ev_name;
 static size_t g_ev_used = 0;
@@ -582,9 +582,8 @@ static unsigned record_flags(cudaStream_t st) {
   return cs == cudaStreamCaptureStatusActive ? cudaEventRecordExternal : cudaEventRecordDefault;
 }
 
-bool knocked_out(const char* name) {
-  static const char* list = getenv("KG_KNOCKOUT");
-  if (list == nullptr || !*list) return false;
+// `name` is one of the comma-separated exact names in `list`
+static bool in_list(const char* list, const char* name) {
   const size_t n = strlen(name);
   for (const char* p = list; (p = strstr(p, name)) != nullptr; p += n) {
     const bool start = p == list || p[-1] == ',';
@@ -594,9 +593,16 @@ bool knocked_out(const char* name) {
   return false;
 }
 
+bool knocked_out(const char* name) {
+  static const char* list = getenv("KG_KNOCKOUT");
+  if (list == nullptr || !*list) return false;
+  return in_list(list, name);
+}
+
 LaunchScope::LaunchScope(const char* name, cudaStream_t s) : st(s), slot(-1) {
   ++g_launches;
-  if (!g_timer_on || (g_timer_prefix[0] && strcmp(name, g_timer_prefix) != 0)) return;   // exact kernel name, "" = all
+  // timed kernels: a comma-separated list of exact names, "" = all
+  if (!g_timer_on || (g_timer_prefix[0] && !in_list(g_timer_prefix, name))) return;
   if (g_ev_used == g_ev_start.size()) {
     cudaEvent_t a, b;
     if (cudaEventCreate(&a) != cudaSuccess || cudaEventCreate(&b) != cudaSuccess) return;
@@ -656,12 +662,16 @@ kg_status kg_kernel_timer_dump(char* buf, int64_t n) {
 // Graph capture support: the event pairs recorded while a stream was being
 // captured became event-record nodes of that graph; detaching keeps them out
 // of the reuse pool so every replay re-records them.
-static std::vector<std::vector<std::pair<cudaEvent_t, cudaEvent_t>>> g_detached;
+struct TimedLaunch {
+  cudaEvent_t start, end;
+  const char* name;
+};
+static std::vector<std::vector<TimedLaunch>> g_detached;
 
 kg_status kg_kernel_timer_detach(int64_t* handle) {
   kg::g_timer_on = false;
-  std::vector<std::pair<cudaEvent_t, cudaEvent_t>> grp;
-  for (size_t i = 0; i < kg::g_ev_used; ++i) grp.push_back({kg::g_ev_start[i], kg::g_ev_end[i]});
+  std::vector<TimedLaunch> grp;
+  for (size_t i = 0; i < kg::g_ev_used; ++i) grp.push_back({kg::g_ev_start[i], kg::g_ev_end[i], kg::g_ev_name[i]});
   // hand the events over: the pool forgets them
   kg::g_ev_start.erase(kg::g_ev_start.begin(), kg::g_ev_start.begin() + kg::g_ev_used);
   kg::g_ev_end.erase(kg::g_ev_end.begin(), kg::g_ev_end.begin() + kg::g_ev_used);
@@ -672,18 +682,25 @@ kg_status kg_kernel_timer_detach(int64_t* handle) {
   return KG_OK;
 }
 
-kg_status kg_kernel_timer_read(int64_t handle, double* total_ms, int64_t* launches) {
+kg_status kg_kernel_timer_read_named(int64_t handle, const char* name, double* total_ms, int64_t* launches) {
   KG_REQUIRE(handle >= 0 && handle < (int64_t)g_detached.size(), KG_ERR_VALIDATION, "bad timer handle");
   double tot = 0.0;
-  for (auto& pr : g_detached[handle]) {
+  int64_t cnt = 0;
+  for (auto& tl : g_detached[handle]) {
+    if (name && *name && strcmp(name, tl.name) != 0) continue;
     float ms = 0.f;
-    KG_CUDA(cudaEventSynchronize(pr.second));
-    KG_CUDA(cudaEventElapsedTime(&ms, pr.first, pr.second));
+    KG_CUDA(cudaEventSynchronize(tl.end));
+    KG_CUDA(cudaEventElapsedTime(&ms, tl.start, tl.end));
     tot += ms;
+    ++cnt;
   }
   *total_ms = tot;
-  *launches = (int64_t)g_detached[handle].size();
+  *launches = cnt;
   return KG_OK;
+}
+
+kg_status kg_kernel_timer_read(int64_t handle, double* total_ms, int64_t* launches) {
+  return kg_kernel_timer_read_named(handle, nullptr, total_ms, launches);
 }
 
 kg_status kg_kernel_timer_end(double* total_ms, int64_t* launches) {

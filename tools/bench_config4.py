@@ -91,13 +91,15 @@ peak = json.load(open(os.path.join(os.path.dirname(os.path.dirname(os.path.abspa
                                    "MEASURED_PEAKS.json"))).get("hbm_gbs", 6530.3) if os.path.exists(
     os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "MEASURED_PEAKS.json")) else 6530.3
 kern = {}
-for name in ("k_aggregate", "k_csc_backward"):
+fused = bd.get("k_csc_dots", (0, 0.0))[0] == 0        # eager single stream: one CSC pass per layer
+for name in ("k_aggregate", "k_csc_backward", "k_csc_dots"):
     n, t = bd.get(name, (0, 0.0))
-    alg = bench.algorithmic_bytes(name, tr, w)
+    model = "csc_family" if (name == "k_csc_backward" and fused) else name
+    alg = bench.algorithmic_bytes(model, tr, w)
     if n:
         per = t / n
         kern[name] = {"launches": n, "ms_per_launch": per, "alg_bytes_per_launch": alg / mc.num_layers,
-                      "achieved_gbs": alg / mc.num_layers / (per * 1e-3) / 1e9,
+                      "byte_model": model, "achieved_gbs": alg / mc.num_layers / (per * 1e-3) / 1e9,
                       "frac_hbm": alg / mc.num_layers / (per * 1e-3) / 1e9 / peak}
 shapes = bench.layer_shapes(tr, w)
 top = sorted(bd.items(), key=lambda x: -x[1][1])[:12]
