@@ -975,6 +975,15 @@ static bool direct_pack(int64_t rows, int64_t K) {
   return packed_bytes(rows, K) <= ((size_t)atoll(env) << 20);
 }
 
+// dZ footprint (bytes) up to which the CSC backward runs as two concurrent
+// passes (dS on the critical stream, edge dots on the side stream); the FB15k
+// working set (~6 MB) is L2-resident, the wikikg2 / citation2 ones are not.
+// KG_CSC_SPLIT_MAX_MB overrides (diagnostics).
+static int64_t csc_split_max_bytes() {
+  const char* env = getenv("KG_CSC_SPLIT_MAX_MB");
+  return (int64_t)(env ? atoll(env) : 48) << 20;
+}
+
 static Chunks csr_chunks(const kg_graph_csr* G) {
   return Chunks{G->ck_ptr, G->ck_row, G->ck_slot, G->ck_split, G->ck_counts, G->chunk};
 }
@@ -1096,7 +1105,21 @@ kg_status kg_rgcn_backward(const kg_graph_csr* G, const kg_layer_params* lp, con
   // side stream concurrently; dV follows dS on the side stream.
   cudaStream_t sd = st;
   const int split = dcoeff_split(G->e, lp->G);
-  if (side_stream) {
+  // Split passes only while dZ stays L2-resident: past that, the second pass
+  // would re-read every gathered dZ row from HBM, so one fused pass (MODE 0)
+  // runs on `st` and only the reductions move to the side stream.
+  const bool fuse = (int64_t)G->n * dO * 4 > csc_split_max_bytes();
+  if (side_stream && fuse) {
+    sd = as_stream(side_stream);
+    s = run_csc(c, G, st, 0);
+    if (s != KG_OK) return s;
+    KG_CUDA(cudaEventRecord(fork_event(), st));
+    KG_CUDA(cudaStreamWaitEvent(sd, fork_event(), 0));
+    KG_LAUNCH("k_dcoeff_reduce", k_dcoeff_partial, dim3((unsigned)lp->G, (unsigned)split, 1), 256, 0, sd,
+              G->rel_ptr, G->rel_perm, counts, t, w.ed, w.ed_self, lp->G, B, w.dc_part);
+    KG_LAUNCH("k_dcoeff_final", k_dcoeff_final, persistent_blocks((int64_t)lp->G * B, 256, 2), 256, 0, sd,
+              w.dc_part, lp->G, B, split, d_coeffs);
+  } else if (side_stream) {
     sd = as_stream(side_stream);
     KG_CUDA(cudaEventRecord(fork_event(), st));
     KG_CUDA(cudaStreamWaitEvent(sd, fork_event(), 0));

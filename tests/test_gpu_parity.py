@@ -506,3 +506,30 @@ def test_owned_row_snapshot_equals_table_assembly():
     want = _assemble_embed(pset, tr.local_tables(), tr.init_params.entity_embed)
     np.testing.assert_array_equal(tr.snapshot().entity_embed, want)
     tr.close()
+
+
+def test_fused_csc_pass_matches_split_passes(monkeypatch):
+    """The CSC backward as one fused pass (used once dZ no longer fits L2) and
+    as the two concurrent passes (dS on the critical stream, edge dots on the
+    side stream) give bitwise identical training rounds."""
+    g = load_golden("synth_p4")
+    graph, pset, cfg = golden_pset(g)
+    L = len(cfg["dims"]) - 1
+    mc = kb.ModelConfig(L, cfg["dims"], cfg["num_bases"], graph.num_relations, 1, mode="embedding")
+    tc = kb.TrainConfig(epochs=1, batch_size=96, seed=2)
+    p0 = golden_params(g, "init_", L)
+    out = []
+    for mb in ("48", "0"):
+        monkeypatch.setenv("KG_CSC_SPLIT_MAX_MB", mb)
+        tr = kb.Trainer(pset, graph, mc, tc, initial_params=p0)
+        tr.begin_epoch()
+        for _ in range(min(3, tr.rounds)):
+            tr.run_round()
+        torch.cuda.synchronize()
+        out.append((tr.snapshot(), tr.epoch_losses()))
+        tr.close()
+    (a, la), (b, lb) = out
+    assert la == lb
+    for x, y in zip(a.dense_blocks(), b.dense_blocks()):
+        np.testing.assert_array_equal(x, y)
+    np.testing.assert_array_equal(a.entity_embed, b.entity_embed)
