@@ -446,6 +446,25 @@ kg_status kg_eval_candidates(const float* H, int32_t d, const float* decoder, co
                              double* ranks, int32_t* ncand, void* stream);
 
 /* ---------------------------------------------------------------------- */
+/* N1  n-hop halo expansion (ref:partition.py:211-282)                     */
+/* ---------------------------------------------------------------------- */
+/* tri: the graph's (m,3) int32 triples on the device. kg_halo_incidence
+ * builds the incident-edge CSR (ptr[n+1], inc[2m]: edge ids touching each
+ * vertex, any order). kg_halo_expand grows one partition from its core edge
+ * ids by `hops` rounds of bidirectional BFS and writes, ascending, the
+ * support edge ids (included, not core), the support vertices (reached, not
+ * core endpoints) and the core endpoints, with their counts (device int32).
+ * Output capacities: m, n, n. */
+int64_t kg_halo_workspace_bytes(int64_t m, int64_t n);
+kg_status kg_halo_incidence(const int32_t* tri, int64_t m, int64_t n, uint32_t* ptr, int32_t* inc, void* ws,
+                            int64_t ws_bytes, void* stream);
+kg_status kg_halo_expand(const int32_t* tri, int64_t m, int64_t n, const uint32_t* ptr, const int32_t* inc,
+                         const int32_t* core_ids, int64_t n_core, int32_t hops, int32_t* support_ids,
+                         int32_t* n_support, int32_t* support_vertices, int32_t* n_support_vertices,
+                         int32_t* core_vertices, int32_t* n_core_vertices, void* ws, int64_t ws_bytes,
+                         void* stream);
+
+/* ---------------------------------------------------------------------- */
 /* Dropout (ref:model.py:221-227)                                          */
 /* ---------------------------------------------------------------------- */
 /* mask[j] = (rng.random() >= p) / (1 - p) for j < counts[t] * d (row-major

@@ -143,6 +143,9 @@ _PROTOS = {
     "kg_encode_full_f64": (ST, [POINTER(KgGraphCsr), P, P, P, c_int32, P, c_int32, P, P, P, P, P, c_int64, P]),
     "kg_known_keys_workspace_bytes": (c_int64, [c_int64]),
     "kg_known_keys": (ST, [P, c_int64, c_int32, c_int32, c_int32, c_int32, P, P, P, c_int64, P]),
+    "kg_halo_workspace_bytes": (c_int64, [c_int64, c_int64]),
+    "kg_halo_incidence": (ST, [P, c_int64, c_int64, P, P, P, c_int64, P]),
+    "kg_halo_expand": (ST, [P, c_int64, c_int64, P, P, P, c_int64, c_int32, P, P, P, P, P, P, P, c_int64, P]),
     "kg_generate_synthetic": (c_int64, [c_int64, c_int32, c_int64, POINTER(KgPcg64), P, c_int64]),
     "kg_vertex_cut_assign": (ST, [P, c_int64, c_int64, c_int32, P, c_double, c_int64, P]),
 }

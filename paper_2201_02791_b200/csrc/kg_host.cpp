@@ -148,9 +148,24 @@ kg_status kg_vertex_cut_assign(const int64_t* triples, int64_t m, int64_t num_en
   std::vector<uint8_t> member((size_t)num_entities * (size_t)P, 0);
   std::vector<int64_t> sizes((size_t)P, 0);
   std::vector<double> score((size_t)P);
+  // endpoints in visit order (one gather pass), so the sequential loop reads
+  // them linearly and can prefetch the vertex state of edges a few ahead
+  std::vector<int64_t> eu((size_t)m), ev((size_t)m);
   for (int64_t k = 0; k < m; ++k) {
+    eu[(size_t)k] = triples[order[k] * 3 + 0];
+    ev[(size_t)k] = triples[order[k] * 3 + 2];
+  }
+  constexpr int64_t AHEAD = 16;
+  for (int64_t k = 0; k < m; ++k) {
+    if (k + AHEAD < m) {
+      const int64_t pu = eu[(size_t)(k + AHEAD)], pv = ev[(size_t)(k + AHEAD)];
+      __builtin_prefetch(&theta[(size_t)pu], 1);
+      __builtin_prefetch(&theta[(size_t)pv], 1);
+      __builtin_prefetch(&member[(size_t)pu * P], 1);
+      __builtin_prefetch(&member[(size_t)pv * P], 1);
+    }
     int64_t e = order[k];
-    int64_t u = triples[e * 3 + 0], v = triples[e * 3 + 2];
+    int64_t u = eu[(size_t)k], v = ev[(size_t)k];
     int64_t du = theta[u], dv = theta[v];
     int64_t tot = du + dv;
     double su = tot ? (double)du / (double)tot : 0.5;

@@ -20,6 +20,10 @@ from . import _lib
 from .errors import ValidationError
 from .graph import KnowledgeGraph, as_triples
 
+import os
+
+_HOST_EXPAND = os.environ.get("KG_HOST_EXPAND", "0") == "1"   # tests: force the host BFS on a GPU box
+
 ROLE_CORE = "core"
 ROLE_REPLICATED = "replicated"
 ROLE_SUPPORT = "support"
@@ -107,11 +111,21 @@ class PartitionSet:
         return self.hops > 0 or any(len(p.support) for p in self.partitions)
 
 
+def _sorted_endpoints(tri: np.ndarray, ids: np.ndarray, n: int, mark: np.ndarray) -> np.ndarray:
+    """np.unique(tri[ids][:, [0, 2]]) through a reusable vertex mark array."""
+    mark[tri[ids, 0]] = True
+    mark[tri[ids, 2]] = True
+    out = np.flatnonzero(mark)
+    mark[out] = False
+    return out
+
+
 def _build_set(graph: KnowledgeGraph, assign: np.ndarray, P: int, seed: int, method: str) -> PartitionSet:
     """Partition records from a per-edge assignment (ref:partition.py:112-134)."""
     n = graph.num_entities
     ids = [np.flatnonzero(assign == p) for p in range(P)]
-    ends = [np.unique(graph.triples[i][:, [0, 2]]) for i in ids]
+    mark = np.zeros(n, dtype=bool)
+    ends = [_sorted_endpoints(graph.triples, i, n, mark) for i in ids]
     count = np.zeros(n, dtype=np.int64)
     for e in ends:
         count[e] += 1
@@ -167,9 +181,57 @@ def _incidence(graph: KnowledgeGraph):
     return ptr, eid[order]
 
 
+def _cuda_available() -> bool:
+    try:
+        import torch
+        return torch.cuda.is_available()
+    except Exception:
+        return False
+
+
+def _expand_device(pset: PartitionSet, graph: KnowledgeGraph, hops: int) -> list:
+    """The halo BFS of every partition on the GPU (kg_halo_incidence /
+    kg_halo_expand): flags + ascending stream compaction, so the sets are
+    exactly the reference's."""
+    import torch
+    lib = _lib.require_cuda()
+    dev = torch.device("cuda", torch.cuda.current_device())
+    st = _lib.stream_handle()
+    m, n = graph.num_edges, graph.num_entities
+    tri = torch.as_tensor(np.ascontiguousarray(graph.triples, dtype=np.int32)).to(dev)
+    ws = torch.empty(lib.kg_halo_workspace_bytes(m, n), dtype=torch.uint8, device=dev)
+    i32 = dict(dtype=torch.int32, device=dev)
+    ptr = torch.empty(n + 1, **i32)
+    inc = torch.empty(max(2 * m, 1), **i32)
+    _lib.call("kg_halo_incidence", tri.data_ptr(), m, n, ptr.data_ptr(), inc.data_ptr(), ws.data_ptr(), ws.numel(), st)
+    sup = torch.empty(max(m, 1), **i32)
+    sv = torch.empty(max(n, 1), **i32)
+    cv = torch.empty(max(n, 1), **i32)
+    cnt = torch.zeros(3, **i32)
+    tri64 = None
+    out = []
+    for part in pset.partitions:
+        if part.core_edge_ids is None:
+            raise ValidationError("partition lacks edge ids; reload with the source graph")
+        core = torch.as_tensor(np.ascontiguousarray(part.core_edge_ids, dtype=np.int32)).to(dev)
+        _lib.call("kg_halo_expand", tri.data_ptr(), m, n, ptr.data_ptr(), inc.data_ptr(), core.data_ptr(),
+                  core.numel(), hops, sup.data_ptr(), cnt[0:1].data_ptr(), sv.data_ptr(), cnt[1:2].data_ptr(),
+                  cv.data_ptr(), cnt[2:3].data_ptr(), ws.data_ptr(), ws.numel(), st)
+        ns, nv, _ = (int(x) for x in cnt.tolist())
+        sup_ids = sup[:ns].long()
+        if tri64 is None:
+            tri64 = tri.long()
+        out.append(replace(part, support=tri64[sup_ids].cpu().numpy(), support_vertices=sv[:nv].cpu().numpy().astype(
+            np.int64), support_edge_ids=sup_ids.cpu().numpy(), hop_count=hops, _local=None))
+    return out
+
+
 def neighborhood_expand(pset: PartitionSet, graph: KnowledgeGraph, hops: int) -> PartitionSet:
     """Copy each partition's n-hop bidirectional closure in as support
-    edges/vertices (ref:partition.py:234-282). Idempotent at equal hops."""
+    edges/vertices (ref:partition.py:234-282). Idempotent at equal hops.
+    On a CUDA device the BFS runs on the GPU (kg_halo_expand); the host
+    restatement below serves CPU-only environments (input preparation, not
+    the training path). Both produce the reference's sorted sets."""
     if hops < 0:
         raise ValidationError("hops must be >= 0")
     if pset.expanded:
@@ -179,6 +241,9 @@ def neighborhood_expand(pset: PartitionSet, graph: KnowledgeGraph, hops: int) ->
                               f"cannot re-expand to {hops}")
     if hops == 0:
         return pset
+    if _cuda_available() and not _HOST_EXPAND:
+        return PartitionSet(_expand_device(pset, graph, hops), pset.num_entities, pset.num_relations, hops,
+                            pset.seed, pset.method, pset.graph_checksum)
     ptr, inc = _incidence(graph)
     tri = graph.triples
     out = []
