@@ -304,8 +304,10 @@ def run_ours(args, world, rank, local):
     # steps above, so the graphs are re-captured with them after the timed
     # region and the kernels are read over a few extra steps (each read
     # synchronises); eager launches (graphs off) are bracketed the same way.
+    torch.cuda.synchronize()
     tr._graphs.clear()
     tr._timer_handles.clear()
+    tr._graph_pool = None          # a fresh private pool for the re-captured graphs
     tr.timer_prefix = args.roofline_kernels
     tr.prepare()
     lib.kg_kernel_timer_begin(args.roofline_kernels.encode())

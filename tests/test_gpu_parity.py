@@ -533,3 +533,34 @@ def test_fused_csc_pass_matches_split_passes(monkeypatch):
     for x, y in zip(a.dense_blocks(), b.dense_blocks()):
         np.testing.assert_array_equal(x, y)
     np.testing.assert_array_equal(a.entity_embed, b.entity_embed)
+
+
+@pytest.mark.parametrize("P,hops", [(1, 2), (2, 1), (4, 2), (8, 3)])
+def test_device_halo_expansion_equals_host(P, hops):
+    """kg_halo_expand (GPU BFS) produces exactly the host restatement's
+    partitions (support edge ids / triples / vertices), which the CPU suite
+    pins to the reference's goldens."""
+    from paper_2201_02791_b200 import partition as kp
+    graph, _ = kb.generate_synthetic(3000, 9, 4.0, seed=P)
+    cut = kb.vertex_cut_partition(graph, P, seed=1)
+    dev = kb.neighborhood_expand(cut, graph, hops)
+    kp._HOST_EXPAND = True
+    try:
+        host = kb.neighborhood_expand(cut, graph, hops)
+    finally:
+        kp._HOST_EXPAND = False
+    for a, b in zip(dev.partitions, host.partitions):
+        np.testing.assert_array_equal(a.support_edge_ids, b.support_edge_ids)
+        np.testing.assert_array_equal(a.support, b.support)
+        np.testing.assert_array_equal(a.support_vertices, b.support_vertices)
+        assert a.hop_count == b.hop_count == hops
+
+
+def test_device_halo_expansion_fb_shape_golden():
+    """FB15k-237 shape, P = 1/2/4/8, 2 hops: halo sizes as the reference's."""
+    g = load_golden("fb_structure")
+    graph, _ = kb.generate_synthetic(14541, 237, 272115 / 14541, seed=0)
+    for P in (1, 2, 4, 8):
+        ex = kb.neighborhood_expand(kb.vertex_cut_partition(graph, P, seed=0), graph, 2)
+        assert [len(p.support) for p in ex.partitions] == g[f"support_counts_P{P}"].tolist()
+        assert [len(p.local_vertices()) for p in ex.partitions] == g[f"vertex_counts_P{P}"].tolist()
