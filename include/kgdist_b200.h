@@ -94,6 +94,12 @@ typedef struct kg_graph_csr {
   int32_t* cc_slot;
   int32_t* cc_split;
   int32_t* cc_counts;
+  /* Per-chunk descriptors (4 x int32 per chunk, same capacity as ck_row /
+   * cc_row): {row, first message, message count | 1<<16 if the row has a
+   * single chunk | 1<<17 if it is the row's first chunk, partial slot}, so a
+   * gather warp resolves its chunk with one 16-byte load. */
+  int32_t* ck_desc;
+  int32_t* cc_desc;
 } kg_graph_csr;
 
 /* One RGCN layer's parameters (ref:model.py:64-79). */
@@ -271,9 +277,13 @@ kg_status kg_rgcn_forward(const kg_graph_csr* g, const kg_layer_params* lp, cons
  * and before reusing ws (one ws per layer). */
 kg_status kg_rgcn_backward(const kg_graph_csr* g, const kg_layer_params* lp, const float* H_in,
                            const float* H_out, const float* dH_out, float* dH_in, const int32_t* vertex_order,
-                           const int32_t* pos, const int32_t* counts, int32_t t, float* d_bases,
-                           float* d_coeffs, const float* H_in_packed, const float* dropout_mask,
+                           const int32_t* pos, const int32_t* c_pos, const int32_t* counts, int32_t t,
+                           float* d_bases, float* d_coeffs, const float* H_in_packed, const float* dropout_mask,
                            int32_t y_ready, void* ws, int64_t ws_bytes, void* stream, void* side_stream);
+/* c_pos (optional, g->e int32) = pos[c_dst[e]] for the round's closure,
+ * written by kg_csc_positions; the CSC passes then skip one dependent load
+ * per message. NULL: looked up per message. */
+kg_status kg_csc_positions(const kg_graph_csr* g, const int32_t* pos, int32_t* c_pos, void* stream);
 /* The backward's first GEMM, Y = H_in[vertex_order[p]] . [V_0 | .. | V_{B-1}]
  * for p < counts[t+1], ahead of time (it needs only forward outputs): call it
  * on any stream ordered before kg_rgcn_backward(..., y_ready = 1, ...) with

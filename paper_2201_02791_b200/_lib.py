@@ -32,7 +32,7 @@ class KgGraphCsr(ctypes.Structure):
                 ("rel_perm", c_void_p), ("rel_ptr", c_void_p), ("chunk", c_int32),
                 ("ck_ptr", c_void_p), ("ck_row", c_void_p), ("ck_slot", c_void_p), ("ck_split", c_void_p),
                 ("ck_counts", c_void_p), ("cc_ptr", c_void_p), ("cc_row", c_void_p), ("cc_slot", c_void_p),
-                ("cc_split", c_void_p), ("cc_counts", c_void_p)]
+                ("cc_split", c_void_p), ("cc_counts", c_void_p), ("ck_desc", c_void_p), ("cc_desc", c_void_p)]
 
 
 class KgLayerParams(ctypes.Structure):
@@ -98,8 +98,9 @@ _PROTOS = {
     "kg_layer_workspace_bytes": (c_int64, [POINTER(KgGraphCsr), c_int32, c_int32, c_int32]),
     "kg_rgcn_forward": (ST, [POINTER(KgGraphCsr), POINTER(KgLayerParams), P, P, P, P, P, c_int32, c_int32,
                              P, P, P, c_int64, P]),
-    "kg_rgcn_backward": (ST, [POINTER(KgGraphCsr), POINTER(KgLayerParams), P, P, P, P, P, P, P, c_int32,
+    "kg_rgcn_backward": (ST, [POINTER(KgGraphCsr), POINTER(KgLayerParams), P, P, P, P, P, P, P, P, c_int32,
                               P, P, P, P, c_int32, P, c_int64, P, P]),
+    "kg_csc_positions": (ST, [POINTER(KgGraphCsr), P, P, P]),
     "kg_rgcn_backward_y": (ST, [POINTER(KgGraphCsr), POINTER(KgLayerParams), P, P, P, P, c_int32, P, c_int64, P]),
     "kg_dropout_mask": (ST, [P, P, c_int32, c_int32, c_double, c_int64, P, P]),
     "kg_eval_candidates": (ST, [P, c_int32, P, P, c_int64, P, P, P, c_int32, P, P, P]),

@@ -40,6 +40,19 @@ __global__ void k_split_flags(const uint32_t* __restrict__ nch, int32_t n, uint3
     f[v] = nch[v] > 1 ? 1u : 0u;
 }
 
+__global__ void k_chunk_desc(const int32_t* __restrict__ indptr, int32_t n, int C, const int32_t* __restrict__ ptr,
+                             const int32_t* __restrict__ slot, const uint32_t* __restrict__ total,
+                             int4* __restrict__ desc) {
+  const int64_t nc = *total;
+  for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < n; v += (int64_t)gridDim.x * blockDim.x) {
+    const int32_t c0 = ptr[v], k = ptr[v + 1] - c0, lo = indptr[v], hi = indptr[v + 1];
+    for (int32_t j = 0; j < k && c0 + j < nc; ++j) {
+      const int32_t beg = lo + j * C, cnt = min(beg + C, hi) - beg;
+      desc[c0 + j] = make_int4(v, beg, cnt | (k == 1 ? 1 << 16 : 0) | (j == 0 ? 1 << 17 : 0), slot[c0 + j]);
+    }
+  }
+}
+
 __global__ void k_chunk_totals(const uint32_t* __restrict__ tot_chunks, const uint32_t* __restrict__ tot_slots,
                                int32_t* __restrict__ counts) {
   counts[0] = (int32_t)*tot_chunks;
@@ -51,7 +64,8 @@ size_t chunk_workspace(int64_t n) {
 }
 
 kg_status build_chunk_table(const int32_t* indptr, int32_t n, int C, int32_t* ptr, int32_t* row, int32_t* slot,
-                            int32_t* split, int32_t* counts, void* ws, size_t ws_bytes, cudaStream_t st) {
+                            int32_t* split, int32_t* counts, int32_t* desc, void* ws, size_t ws_bytes,
+                            cudaStream_t st) {
   KG_REQUIRE(ws_bytes >= chunk_workspace(n), KG_ERR_VALIDATION, "chunk workspace too small");
   Arena a(ws, ws_bytes);
   uint32_t* nch = a.take<uint32_t>(n);
@@ -72,6 +86,9 @@ kg_status build_chunk_table(const int32_t* indptr, int32_t n, int C, int32_t* pt
   s = compact_flags(slots, n, split, counts + 2, 0, nullptr, cws, compact_workspace(n), st);
   if (s != KG_OK) return s;
   KG_LAUNCH("k_chunk_totals", k_chunk_totals, 1, 1, 0, st, tots + 0, tots + 1, counts);
+  if (desc)
+    KG_LAUNCH("k_chunk_desc", k_chunk_desc, g, 256, 0, st, indptr, n, C, ptr, slot, tots + 0,
+              reinterpret_cast<int4*>(desc));
   return KG_OK;
 }
 

@@ -177,6 +177,7 @@ kg_status compact_flags_ex(uint32_t* flags, int64_t n, int32_t* out, const int32
 // Static work-chunk table of a CSR (kg_chunks.cu).
 size_t chunk_workspace(int64_t n);
 kg_status build_chunk_table(const int32_t* indptr, int32_t n, int C, int32_t* ptr, int32_t* row, int32_t* slot,
-                            int32_t* split, int32_t* counts, void* ws, size_t ws_bytes, cudaStream_t st);
+                            int32_t* split, int32_t* counts, int32_t* desc, void* ws, size_t ws_bytes,
+                            cudaStream_t st);
 
 }  // namespace kg

@@ -68,7 +68,10 @@ struct Chunks {
   const int32_t* split;
   const int32_t* counts;
   int C;
+  const int4* desc;      // {row, first message, count | single<<16 | first<<17, slot} per chunk
 };
+
+constexpr int CH_SINGLE = 1 << 16, CH_FIRST = 1 << 17;
 
 struct AggArgs {
   const int32_t* indptr;
@@ -125,13 +128,11 @@ __global__ void __launch_bounds__(256, KG_GATHER_BPS) k_aggregate(AggArgs a) {
 #pragma unroll
   for (int s = 0; s < S; ++s) slot_ok[s] = (s * LPR + cl) * VEC < d;
   for (int64_t c = warp_uniform((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5); c < NC; c += warps) {
-    const int32_t v = a.ck.row[c];
+    const int4 dsc = a.ck.desc[c];
+    const int32_t v = dsc.x, beg = dsc.y, cnt = dsc.z & 0xffff;
+    const bool single = dsc.z & CH_SINGLE;
     const int32_t p = a.pos[v];
     if (p < 0 || p >= T) continue;
-    const int32_t cbase = a.ck.ptr[v];
-    const int32_t nch = a.ck.ptr[v + 1] - cbase;
-    const int32_t beg = a.indptr[v] + (int32_t)(c - cbase) * a.ck.C;
-    const int32_t cnt = min(beg + a.ck.C, a.indptr[v + 1]) - beg;
     EdgeMeta<NB> m;
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
@@ -198,7 +199,7 @@ __global__ void __launch_bounds__(256, KG_GATHER_BPS) k_aggregate(AggArgs a) {
 #pragma unroll
     for (int s2 = 0; s2 < S; ++s2) own[s2] = slot_ok[s2] && grp == 0;
     float* out;
-    if (nch == 1) {
+    if (single) {
       // self-loop group 2R (norm 1), then the finished row
       float xv[S][VEC];
 #pragma unroll
@@ -228,7 +229,7 @@ __global__ void __launch_bounds__(256, KG_GATHER_BPS) k_aggregate(AggArgs a) {
       }
       out = a.acc + (int64_t)p * B * d;   // row-major (the GEMM packs it)
     } else {
-      out = a.partial + (int64_t)a.ck.slot[c] * B * d;
+      out = a.partial + (int64_t)dsc.w * B * d;
     }
 #pragma unroll
     for (int b = 0; b < NB; ++b)
@@ -340,6 +341,7 @@ struct CscArgs {
   const float* Y;        // (count_S, B*d) compact: X V_b per source position
   const float* dZ;       // (count_T, d) compact
   const int32_t* pos;
+  const int32_t* c_pos;  // optional: pos[c_dst[e]] per CSC message for this round (kg_csc_positions)
   const int32_t* counts;
   int t;                 // targets A_t, sources A_{t+1}
   float* dS;             // (count_S, B*d)
@@ -374,12 +376,10 @@ __global__ void __launch_bounds__(256, KG_GATHER_BPS) k_csc_backward(CscArgs a) 
 #pragma unroll
   for (int s = 0; s < S; ++s) slot_ok[s] = (s * LPR + cl) * VEC < d;
   for (int64_t c = warp_uniform((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5); c < NC; c += warps) {
-    const int32_t u = a.ck.row[c];
+    const int4 dsc = a.ck.desc[c];
+    const int32_t u = dsc.x, beg = dsc.y, cnt = dsc.z & 0xffff;
+    const bool single = dsc.z & CH_SINGLE, first = dsc.z & CH_FIRST;
     const int32_t q = a.pos[u];
-    const int32_t cbase = a.ck.ptr[u];
-    const int32_t nch = a.ck.ptr[u + 1] - cbase;
-    const int32_t beg = a.c_indptr[u] + (int32_t)(c - cbase) * a.ck.C;
-    const int32_t cnt = min(beg + a.ck.C, a.c_indptr[u + 1]) - beg;
     if (q < 0 || q >= Sn) {
       // not a source of this layer: its edge dots are zero (k_dcoeff_partial
       // sums every edge of a relation without a membership test)
@@ -398,10 +398,9 @@ __global__ void __launch_bounds__(256, KG_GATHER_BPS) k_csc_backward(CscArgs a) 
 #pragma unroll
       for (int b = 0; b < NB; ++b) m.cf[h][b] = 0.f;
       if (e < cnt) {
-        const int32_t w = a.c_dst[beg + e];
         const int32_t r = a.c_rel[beg + e];
         const float nw = a.c_norm[beg + e];
-        const int32_t pw = a.pos[w];
+        const int32_t pw = a.c_pos ? a.c_pos[beg + e] : a.pos[a.c_dst[beg + e]];
         if (pw >= 0 && pw < T) {
           m.other[h] = pw;
           nrm[h] = nw;
@@ -500,7 +499,7 @@ __global__ void __launch_bounds__(256, KG_GATHER_BPS) k_csc_backward(CscArgs a) 
     }
     if (MODE == 2) {
       // self dot for d a[2R,b], by the row's first chunk (split rows too)
-      if (c == cbase && q < T) {
+      if (first && q < T) {
         float z[S][VEC];
 #pragma unroll
         for (int s = 0; s < S; ++s) {
@@ -538,7 +537,7 @@ __global__ void __launch_bounds__(256, KG_GATHER_BPS) k_csc_backward(CscArgs a) 
 #pragma unroll
     for (int s2 = 0; s2 < S; ++s2) own[s2] = slot_ok[s2] && grp == 0;
     float* out;
-    if (nch == 1) {
+    if (single) {
       if (q < T) {
         // self-loop (norm 1): dS += a[2R,b] dZ[u]; self dot for d a[2R,b]
         float z[S][VEC];
@@ -579,7 +578,7 @@ __global__ void __launch_bounds__(256, KG_GATHER_BPS) k_csc_backward(CscArgs a) 
         packed_zero_pad(a.dS_pk, a.dS_nk, q, B * d, lane, 32);
       }
     } else {
-      out = a.partial + (int64_t)a.ck.slot[c] * B * d;
+      out = a.partial + (int64_t)dsc.w * B * d;
     }
 #pragma unroll
     for (int b = 0; b < NB; ++b)
@@ -588,6 +587,15 @@ __global__ void __launch_bounds__(256, KG_GATHER_BPS) k_csc_backward(CscArgs a) 
         for (int s = 0; s < S; ++s)
           if (own[s]) VecIO<VEC>::store(out + (int64_t)b * d + (s * LPR + cl) * VEC, acc[b][s]);
   }
+}
+
+// c_pos[e] = pos[c_dst[e]]: the closure position of every CSC message's
+// destination for this round, so the CSC passes gather dZ rows with one
+// dependent load per message instead of two (c_dst, then pos).
+__global__ void k_csc_positions(const int32_t* __restrict__ c_dst, int64_t e, const int32_t* __restrict__ pos,
+                                int32_t* __restrict__ c_pos) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < e; i += (int64_t)gridDim.x * blockDim.x)
+    c_pos[i] = pos[c_dst[i]];
 }
 
 // Split source rows: one block per row (chunk-order partial sums as in
@@ -985,10 +993,12 @@ static int64_t csc_split_max_bytes() {
 }
 
 static Chunks csr_chunks(const kg_graph_csr* G) {
-  return Chunks{G->ck_ptr, G->ck_row, G->ck_slot, G->ck_split, G->ck_counts, G->chunk};
+  return Chunks{G->ck_ptr, G->ck_row, G->ck_slot, G->ck_split, G->ck_counts, G->chunk,
+                reinterpret_cast<const int4*>(G->ck_desc)};
 }
 static Chunks csc_chunks(const kg_graph_csr* G) {
-  return Chunks{G->cc_ptr, G->cc_row, G->cc_slot, G->cc_split, G->cc_counts, G->chunk};
+  return Chunks{G->cc_ptr, G->cc_row, G->cc_slot, G->cc_split, G->cc_counts, G->chunk,
+                reinterpret_cast<const int4*>(G->cc_desc)};
 }
 
 }  // namespace kg
@@ -1068,9 +1078,16 @@ kg_status kg_rgcn_forward(const kg_graph_csr* G, const kg_layer_params* lp, cons
   return gemm_nn(g, w.gemm, st);
 }
 
+kg_status kg_csc_positions(const kg_graph_csr* G, const int32_t* pos, int32_t* c_pos, void* stream) {
+  if (G->e == 0) return KG_OK;
+  KG_LAUNCH("k_csc_positions", k_csc_positions, persistent_blocks(G->e, 256, 8), 256, 0, as_stream(stream), G->c_dst,
+            G->e, pos, c_pos);
+  return KG_OK;
+}
+
 kg_status kg_rgcn_backward(const kg_graph_csr* G, const kg_layer_params* lp, const float* H_in, const float* H_out,
                            const float* dH_out, float* dH_in, const int32_t* order, const int32_t* pos,
-                           const int32_t* counts, int32_t t, float* d_bases, float* d_coeffs,
+                           const int32_t* c_pos, const int32_t* counts, int32_t t, float* d_bases, float* d_coeffs,
                            const float* H_in_packed, const float* dropout_mask, int32_t y_ready, void* ws,
                            int64_t ws_bytes, void* stream, void* side_stream) {
   cudaStream_t st = as_stream(stream);
@@ -1097,7 +1114,7 @@ kg_status kg_rgcn_backward(const kg_graph_csr* G, const kg_layer_params* lp, con
     if (s != KG_OK) return s;
   }
   CscArgs c{G->c_indptr, G->c_dst, G->c_rel, G->c_norm, csc_chunks(G), lp->coeffs, lp->G, B, dO, w.Y, w.dZ, pos,
-            counts, t, w.dS, w.ed, w.ed_self, w.partial,
+            c_pos, counts, t, w.dS, w.ed, w.ed_self, w.partial,
             direct_pack(G->n, (int64_t)B * dO) ? w.dS_pk : nullptr, packed_nk(G->n, (int64_t)B * dO), 1};
   // The parameter gradients (dV, d coeffs) feed only the optimizer: with a side
   // stream they leave the critical path (the caller joins it before the update).

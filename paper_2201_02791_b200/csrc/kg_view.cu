@@ -308,10 +308,10 @@ kg_status kg_view_build(const int32_t* edges_global, int64_t m, const int32_t* g
     KG_CUDA(cudaMemsetAsync(G->rel_ptr, 0, (2 * R + 1) * sizeof(int32_t), st));
     KG_CUDA(cudaMemsetAsync(n_keys, 0, sizeof(int32_t), st));
     kg_status s0 = build_chunk_table(G->indptr, n, G->chunk, G->ck_ptr, G->ck_row, G->ck_slot, G->ck_split,
-                                     G->ck_counts, ws, (size_t)ws_bytes, st);
+                                     G->ck_counts, G->ck_desc, ws, (size_t)ws_bytes, st);
     if (s0 != KG_OK) return s0;
     return build_chunk_table(G->c_indptr, n, G->chunk, G->cc_ptr, G->cc_row, G->cc_slot, G->cc_split, G->cc_counts,
-                             ws, (size_t)ws_bytes, st);
+                             G->cc_desc, ws, (size_t)ws_bytes, st);
   }
   KG_LAUNCH("k_localize", k_localize, grid_for(m), 256, 0, st, edges_global, m, g2l, el);
   KG_CHECK_LAUNCH("k_localize");
@@ -379,10 +379,12 @@ kg_status kg_view_build(const int32_t* edges_global, int64_t m, const int32_t* g
   // static work chunks for hub rows (destination CSR and source CSC)
   KG_REQUIRE(G->chunk >= 1, KG_ERR_VALIDATION, "chunk size must be >= 1");
   KG_REQUIRE((size_t)ws_bytes >= chunk_workspace(n), KG_ERR_VALIDATION, "view workspace too small for chunks");
-  s = build_chunk_table(G->indptr, n, G->chunk, G->ck_ptr, G->ck_row, G->ck_slot, G->ck_split, G->ck_counts, ws,
+  s = build_chunk_table(G->indptr, n, G->chunk, G->ck_ptr, G->ck_row, G->ck_slot, G->ck_split, G->ck_counts,
+                        G->ck_desc, ws,
                         (size_t)ws_bytes, st);
   if (s != KG_OK) return s;
-  s = build_chunk_table(G->c_indptr, n, G->chunk, G->cc_ptr, G->cc_row, G->cc_slot, G->cc_split, G->cc_counts, ws,
+  s = build_chunk_table(G->c_indptr, n, G->chunk, G->cc_ptr, G->cc_row, G->cc_slot, G->cc_split, G->cc_counts,
+                        G->cc_desc, ws,
                         (size_t)ws_bytes, st);
   if (s != KG_OK) return s;
   return KG_OK;

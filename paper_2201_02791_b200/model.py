@@ -368,6 +368,18 @@ def device_loss(model: DeviceModel, bufs: ViewBuffers, stream, start: int, b: in
     _lib.call(fn, *args)
 
 
+def device_csc_positions(bufs: ViewBuffers) -> None:
+    """pos[c_dst] of every CSC message for the closure in bufs (the backward's
+    dZ gathers then take one dependent load per message); after this call
+    device_backward uses it until bufs.pos changes (the caller re-runs it)."""
+    torch = _torch()
+    if getattr(bufs, "c_pos", None) is None:
+        bufs.c_pos = torch.empty(max(int(bufs.view.csr().e), 1), dtype=torch.int32, device=bufs.view.device)
+    _lib.call("kg_csc_positions", ctypes.byref(bufs.view.csr()), bufs.pos.data_ptr(), bufs.c_pos.data_ptr(),
+              _lib.stream_handle())
+    bufs.c_pos_ready = bufs.c_pos
+
+
 def device_backward(model: DeviceModel, bufs: ViewBuffers, grad_flat, input_grad: bool, side=None,
                     packed: bool = False, hpk: bool = False, masks: Optional[list] = None,
                     y_ready: bool = False) -> None:
@@ -385,7 +397,8 @@ def device_backward(model: DeviceModel, bufs: ViewBuffers, grad_flat, input_grad
         dh_in = bufs.dH[l].data_ptr() if (l > 0 or input_grad) else 0
         _lib.call("kg_rgcn_backward", csr, ctypes.byref(model.layer(l, packed)), bufs.H[l].data_ptr(),
                   bufs.H[l + 1].data_ptr() if l < L - 1 else 0, bufs.dH[l + 1].data_ptr(), dh_in,
-                  bufs.order.data_ptr(), bufs.pos.data_ptr(), bufs.counts.data_ptr(), L - 1 - l,
+                  bufs.order.data_ptr(), bufs.pos.data_ptr(), _lib.ptr(getattr(bufs, "c_pos_ready", None)),
+                  bufs.counts.data_ptr(), L - 1 - l,
                   grad_flat.data_ptr() + 4 * lay.bases_off(l), grad_flat.data_ptr() + 4 * lay.coeffs_off(l),
                   bufs.hpk(l).data_ptr() if hpk else None, masks[l].data_ptr() if (masks and l < L - 1) else None,
                   1 if y_ready else 0, ws.data_ptr(), ws.numel(), st, None if side is None else side.cuda_stream)
@@ -517,6 +530,7 @@ def loss_from_cache(params: ModelParams, config: ModelConfig, batch, cg, cache: 
     device_loss(model, bufs, stream, 0, len(batch.triples), grad, loss_t)
     check_flags(bufs)
     emb = config.mode == MODE_EMBEDDING
+    device_csc_positions(bufs)
     device_backward(model, bufs, grad, input_grad=emb, masks=getattr(bufs, "masks", None))
     blocks = model.layout.unpack(grad.cpu().numpy())
     L = config.num_layers

@@ -208,11 +208,12 @@ def build_view(partition: Partition, num_entities: int, num_relations: int) -> P
         setattr(v, f"d_{pre}_slot", torch.empty(cap_chunks, **i32))
         setattr(v, f"d_{pre}_split", torch.empty(cap_split_rows, **i32))
         setattr(v, f"d_{pre}_counts", torch.zeros(4, **i32))
+        setattr(v, f"d_{pre}_desc", torch.empty(4 * cap_chunks, **i32))
     c = _lib.KgGraphCsr()
     c.n, c.R, c.e, c.chunk = n_local, num_relations, e, C
     for f in ("indptr", "src", "rel", "norm", "c_indptr", "c_dst", "c_rel", "c_norm", "rel_perm", "rel_ptr",
               "ck_ptr", "ck_row", "ck_slot", "ck_split", "ck_counts",
-              "cc_ptr", "cc_row", "cc_slot", "cc_split", "cc_counts"):
+              "cc_ptr", "cc_row", "cc_slot", "cc_split", "cc_counts", "ck_desc", "cc_desc"):
         setattr(c, f, getattr(v, "d_" + f).data_ptr())
     v._csr = c
     ws_bytes2 = lib.kg_view_workspace_bytes(max(m, 1), n_local)

@@ -30,7 +30,7 @@ import numpy as np
 from . import _lib
 from .errors import KGError, NumericError, ProtocolError, ValidationError
 from .model import (MODE_EMBEDDING, MODE_FEATURE, DeviceModel, ModelConfig, ModelParams, ViewBuffers,
-                    check_flags, raise_for_flags, device_backward, device_backward_y, device_dropout, device_forward,
+                    check_flags, raise_for_flags, device_backward, device_csc_positions, device_backward_y, device_dropout, device_forward,
                     device_loss, device_pack_inputs, init_params)
 from .partition import PartitionSet
 from .sampler import EpochSampler, build_view
@@ -636,7 +636,9 @@ class Trainer:
             side.wait_stream(main)
             with torch.cuda.stream(side):
                 # backward operands that only need forward outputs, beside the forward:
-                # layer 0's packed input rows and Y_0 = H_0 . [V_b]
+                # layer 0's packed input rows and Y_0 = H_0 . [V_b]; the closure
+                # positions of every CSC message (the backward's dZ gathers)
+                device_csc_positions(w.bufs)
                 device_pack_inputs(w.bufs)
                 device_backward_y(self.model, w.bufs, 0)
 
