@@ -172,7 +172,9 @@ extern "C" {
 // impl 0 = tcgen05 3xTF32 (product path), 1 = CUDA-core fp32 reference.
 int64_t kg_gemm_workspace_bytes(int64_t M, int64_t K, int64_t N) {
   size_t a = gemm_tn_workspace(M, K, N), b = gemm_nn_workspace(M, K, N);
-  return (int64_t)(a > b ? a : b) + 256;
+  size_t c = (K <= 128 && N <= 256) ? umma_tn_records_test_workspace(M, K, N) : 0;
+  a = a > b ? a : b;
+  return (int64_t)(a > c ? a : c) + 256;
 }
 
 kg_status kg_gemm_f32(const float* A, int64_t lda, const int32_t* a_rows, const float* B, int64_t ldb, float* C,
@@ -184,6 +186,8 @@ kg_status kg_gemm_f32(const float* A, int64_t lda, const int32_t* a_rows, const 
   cudaStream_t st = as_stream(stream);
   KG_REQUIRE(ws_bytes >= kg_gemm_workspace_bytes(M, K, N) - 256, KG_ERR_VALIDATION, "gemm workspace too small");
   if (!trans) return impl ? simt_gemm_nn(g, st) : umma_gemm_nn(g, ws, st);
+  // impl 2: the record TN (MN-major operands) fed by a pack of A and B rows
+  if (impl == 2) return umma_gemm_tn_via_records(g, C, ws, st);
   return impl ? simt_gemm_tn(g, C, ws, st) : umma_gemm_tn(g, C, ws, st);
 }
 

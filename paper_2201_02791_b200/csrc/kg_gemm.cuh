@@ -129,6 +129,16 @@ kg_status umma_gemm_nn(const GemmArgs& g, void* ws, cudaStream_t st);
 size_t umma_tn_workspace(int64_t rows_max, int64_t K, int64_t N);
 kg_status umma_gemm_tn(const GemmArgs& g, float* out, void* ws, cudaStream_t st);
 
+// dV = X^T dS from the producers' operand records read as MN-major operands
+// (kg_umma.cu): X records (x_cols <= 128 columns) and dS records (N <= 256)
+// of the same rows (device count M_dev[M_dev_index]); out (x_cols, N).
+// ws: at least umma_tn_workspace(rows_max, x_cols, N) bytes.
+kg_status umma_gemm_tn_records(const float* Xp, int64_t x_cols, const float* Dp, int64_t N, const int32_t* M_dev,
+                               int M_dev_index, int64_t rows_max, float* out, void* ws, cudaStream_t st);
+
+size_t umma_tn_records_test_workspace(int64_t M, int64_t K, int64_t N);
+kg_status umma_gemm_tn_via_records(const GemmArgs& g, float* out, void* ws, cudaStream_t st);
+
 // Filtered ranking on the tensor cores (kg_umma.cu), d <= 128.
 size_t umma_rank_workspace(int64_t nq, int32_t N, int d, int64_t max_pairs);
 kg_status umma_rank_filtered(const float* H, int d, int32_t N, const float* dec, int32_t R, const int32_t* qry,

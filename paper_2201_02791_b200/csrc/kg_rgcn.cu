@@ -567,7 +567,7 @@ __global__ void __launch_bounds__(256, KG_GATHER_BPS) k_csc_backward(CscArgs a) 
           }
         }
       }
-      out = a.dS + (int64_t)q * B * d;
+      out = a.dS ? a.dS + (int64_t)q * B * d : nullptr;   // row-major dS only for a consumer that reads it
       if (a.dS_pk) {
 #pragma unroll
         for (int b = 0; b < NB; ++b)
@@ -580,12 +580,13 @@ __global__ void __launch_bounds__(256, KG_GATHER_BPS) k_csc_backward(CscArgs a) 
     } else {
       out = a.partial + (int64_t)dsc.w * B * d;
     }
+    if (out)
 #pragma unroll
-    for (int b = 0; b < NB; ++b)
-      if (b < B)
+      for (int b = 0; b < NB; ++b)
+        if (b < B)
 #pragma unroll
-        for (int s = 0; s < S; ++s)
-          if (own[s]) VecIO<VEC>::store(out + (int64_t)b * d + (s * LPR + cl) * VEC, acc[b][s]);
+          for (int s = 0; s < S; ++s)
+            if (own[s]) VecIO<VEC>::store(out + (int64_t)b * d + (s * LPR + cl) * VEC, acc[b][s]);
   }
 }
 
@@ -632,7 +633,7 @@ __global__ void __launch_bounds__(CB_THREADS) k_csc_combine(CscArgs a) {
         const float cf = a.coeffs[(a.G - 1) * a.B + b];
 #pragma unroll
         for (int i = 0; i < V; ++i) x[i] = tot[i] + cf * z[i];
-        VecIO<V>::store(a.dS + (int64_t)q * width + col, x);
+        if (a.dS) VecIO<V>::store(a.dS + (int64_t)q * width + col, x);
         if (a.dS_pk) packed_store<V>(a.dS_pk, a.dS_nk, q, col, x);
       }
     }
@@ -1116,6 +1117,9 @@ kg_status kg_rgcn_backward(const kg_graph_csr* G, const kg_layer_params* lp, con
   CscArgs c{G->c_indptr, G->c_dst, G->c_rel, G->c_norm, csc_chunks(G), lp->coeffs, lp->G, B, dO, w.Y, w.dZ, pos,
             c_pos, counts, t, w.dS, w.ed, w.ed_self, w.partial,
             direct_pack(G->n, (int64_t)B * dO) ? w.dS_pk : nullptr, packed_nk(G->n, (int64_t)B * dO), 1};
+  const bool records_tn = H_in_packed != nullptr && c.dS_pk != nullptr && di <= 128 && B * dO <= 256 &&
+                          !getenv("KG_TN_ROWMAJOR");
+  if (records_tn) c.dS = nullptr;   // nothing reads row-major dS then
   // The parameter gradients (dV, d coeffs) feed only the optimizer: with a side
   // stream they leave the critical path (the caller joins it before the update).
   // There the CSC pass splits: dS on `st`, the edge/self dots (d coeffs) on the
@@ -1154,13 +1158,19 @@ kg_status kg_rgcn_backward(const kg_graph_csr* G, const kg_layer_params* lp, con
     s = run_csc(c, G, st, 0);
     if (s != KG_OK) return s;
   }
-  // dV = X^T dS  (reduction over the source rows)
-  GemmArgs gv{};
-  gv.A = H_in; gv.lda = di; gv.a_rows = order;
-  gv.B = w.dS; gv.ldb = (int64_t)B * dO;
-  gv.M_dev = counts; gv.M_dev_index = t + 1; gv.M_max = G->n;
-  gv.K = di; gv.N = (int64_t)B * dO;
-  s = gemm_tn(gv, w.Rm, w.gemm_tn, sd);
+  // dV = X^T dS  (reduction over the source rows): straight from the X and
+  // dS operand records when both exist (MN-major operands, no transposing
+  // pack, no row-major dS), else from row-major X / dS
+  if (records_tn) {
+    s = umma_gemm_tn_records(H_in_packed, di, c.dS_pk, (int64_t)B * dO, counts, t + 1, G->n, w.Rm, w.gemm_tn, sd);
+  } else {
+    GemmArgs gv{};
+    gv.A = H_in; gv.lda = di; gv.a_rows = order;
+    gv.B = w.dS; gv.ldb = (int64_t)B * dO;
+    gv.M_dev = counts; gv.M_dev_index = t + 1; gv.M_max = G->n;
+    gv.K = di; gv.N = (int64_t)B * dO;
+    s = gemm_tn(gv, w.Rm, w.gemm_tn, sd);
+  }
   if (s != KG_OK) return s;
   KG_LAUNCH("k_dbases_layout", k_dbases_layout, persistent_blocks(wn, 256, 2), 256, 0, sd, w.Rm, B, di, dO, d_bases);
   if (!side_stream) {

@@ -591,6 +591,265 @@ kg_status umma_gemm_tn(const GemmArgs& g, float* out, void* ws, cudaStream_t st)
 }
 
 // ---------------------------------------------------------------------------
+// TN straight from the producers' records: dV = X^T dS.
+//
+// The records of X (written by the forward epilogue / the input pack) and of
+// dS (written by the CSC pass) hold, per 128-row block and 16-column chunk,
+// 8-row x 64-byte swizzle atoms (pk_off). For dV the data rows are the
+// reduction (K) dimension, so the operands are needed K-major along the data
+// rows — the transpose of the records. (tcgen05's MN-major operand mode is
+// not usable with kind::tf32: with a transpose bit set the MMA yields zeros
+// on this part.) Instead of a global transposing pack, the producer copies
+// each chunk's 16-row slice (1 KB) of a stage into shared memory and the four
+// split warps transpose it there into K-major records (MMA row = column of X
+// or dS, K = the stage's 16 data rows), splitting fp32 into tf32 hi + lo on
+// the way; rows past the device row count are written as zeros. The X and dS
+// records are read once, nothing else touches HBM: no transposing pack pass
+// and no row-major dS. Split-K over CTAs (contiguous 16-row groups) + the
+// fixed-order reduce.
+struct TnMnArgs {
+  const float* Xp;     // X records: 128-row blocks x xk chunks (hi|lo if split)
+  const float* Dp;     // dS records: 128-row blocks x dk chunks
+  int xk, dk;          // 16-column chunks per block (M = 16*xk <= 128, N = 16*dk <= 256)
+  int split;           // records hold hi | lo halves
+  const int32_t* M_dev;
+  int M_dev_index;
+  int64_t rows;        // data rows if M_dev == nullptr
+  float* part;         // (splits, out_rows, N) partials
+  int64_t out_rows;    // X columns (<= 128)
+  int64_t N;
+};
+
+constexpr int TM_SLICE = 16 * UKC * 4;   // bytes of a 16-row slice of one chunk (two atoms)
+
+struct TnStage {   // byte offsets inside one ring stage
+  uint32_t sa, sb, ka, kb, size;
+};
+
+__host__ __device__ inline TnStage tn_stage(int xk, int dk, int split) {
+  TnStage t;
+  const uint32_t m = split ? 2u : 1u;
+  t.sa = 0;
+  t.sb = t.sa + (uint32_t)xk * TM_SLICE * m;
+  t.ka = (t.sb + (uint32_t)dk * TM_SLICE * m + 1023u) & ~1023u;
+  t.kb = t.ka + 2u * UM * UKC * 4u;                 // A K-major tile: hi + lo (128 rows)
+  t.size = t.kb + 2u * (uint32_t)(16 * dk) * UKC * 4u;
+  t.size = (t.size + 1023u) & ~1023u;
+  return t;
+}
+
+__global__ void __launch_bounds__(UTHREADS, 1) k_umma_tn_rec(TnMnArgs g, int nstages, uint32_t acc_cols) {
+  extern __shared__ __align__(1024) uint8_t smem[];
+  __shared__ __align__(8) uint64_t bar_full[UMAXS], bar_empty[UMAXS], bar_split[UMAXS], bar_tfull;
+  __shared__ uint32_t tmem_base_s;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int64_t rows = g.M_dev ? (int64_t)g.M_dev[g.M_dev_index] : g.rows;
+  const int64_t ngrp = (rows + 15) / 16;
+  const int64_t per = (ngrp + gridDim.x - 1) / gridDim.x;
+  const int64_t c_lo = (int64_t)blockIdx.x * per, c_hi = c_lo + per < ngrp ? c_lo + per : ngrp;
+  const int np = 16 * g.dk;
+  if (c_lo >= c_hi) {   // empty split: its partial slot is zero
+    for (int idx = tid; idx < g.out_rows * g.N; idx += UTHREADS)
+      g.part[(int64_t)blockIdx.x * g.out_rows * g.N + idx] = 0.f;
+    return;
+  }
+  const int nk = (int)(c_hi - c_lo);
+  const TnStage L = tn_stage(g.xk, g.dk, g.split);
+  const uint32_t sbase = smem_u32(smem);
+  auto full = [&](int s) { return smem_u32(&bar_full[s]); };
+  auto empty = [&](int s) { return smem_u32(&bar_empty[s]); };
+  // K-major A rows past 16*xk (M padding to 128) stay zero in every stage
+  for (int s = 0; s < nstages; ++s) {
+    float* ka = reinterpret_cast<float*>(smem + (size_t)s * L.size + L.ka);
+    for (int i = tid; i < (UM - 16 * g.xk) * UKC; i += UTHREADS) {
+      const int m = 16 * g.xk + i / UKC, k = i % UKC;
+      ka[pk_off(m, k)] = 0.f;
+      ka[UM * UKC + pk_off(m, k)] = 0.f;
+    }
+  }
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&tmem_base_s)),
+                 "r"(acc_cols));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  if (tid == 32) {
+    for (int s = 0; s < nstages; ++s) {
+      mbar_init(full(s), 1);
+      mbar_init(empty(s), 1);
+      mbar_init(smem_u32(&bar_split[s]), 4);
+    }
+    mbar_init(smem_u32(&bar_tfull), 1);
+    fence_barrier_init();
+  }
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // zero padding visible to the MMAs
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = tmem_base_s;
+  const int64_t xrec = g.split ? rec_floats_split(UM) : rec_floats(UM);   // floats per record
+  const int64_t lo_off = (int64_t)UM * UKC;                                 // lo half inside a split record
+  const uint32_t mult = g.split ? 2u : 1u;
+
+  if (warp == 0) {
+    if (lane == 0) {   // producer: per 16-row group, each chunk's 1 KB slice (hi, and lo when split)
+      const uint32_t bytes = (uint32_t)(g.xk + g.dk) * TM_SLICE * mult;
+      for (int kc = 0; kc < nk; ++kc) {
+        const int s = kc % nstages;
+        if (kc >= nstages) mbar_wait(empty(s), (uint32_t)((kc / nstages - 1) & 1));
+        const int64_t grp = c_lo + kc, blk = grp / 8, r16 = (grp & 7) * 16;
+        const uint32_t dst = sbase + (uint32_t)s * L.size;
+        mbar_expect_tx(full(s), bytes);
+        for (int c = 0; c < g.xk; ++c) {
+          const float* rec = g.Xp + (blk * g.xk + c) * xrec + r16 * UKC;
+          bulk_g2s(dst + L.sa + (uint32_t)c * TM_SLICE * mult, rec, TM_SLICE, full(s));
+          if (g.split) bulk_g2s(dst + L.sa + (uint32_t)c * TM_SLICE * 2 + TM_SLICE, rec + lo_off, TM_SLICE, full(s));
+        }
+        for (int c = 0; c < g.dk; ++c) {
+          const float* rec = g.Dp + (blk * g.dk + c) * xrec + r16 * UKC;
+          bulk_g2s(dst + L.sb + (uint32_t)c * TM_SLICE * mult, rec, TM_SLICE, full(s));
+          if (g.split) bulk_g2s(dst + L.sb + (uint32_t)c * TM_SLICE * 2 + TM_SLICE, rec + lo_off, TM_SLICE, full(s));
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {   // MMA issuer: D(128 x np) += X^T . dS over the CTA's row groups
+      const uint32_t idesc = make_idesc(np);
+      for (int kc = 0; kc < nk; ++kc) {
+        const int s = kc % nstages;
+        mbar_wait(smem_u32(&bar_split[s]), (uint32_t)((kc / nstages) & 1));
+        tc_fence_after();
+        const uint32_t a_hi = sbase + (uint32_t)s * L.size + L.ka, a_lo = a_hi + UM * UKC * 4;
+        const uint32_t b_hi = sbase + (uint32_t)s * L.size + L.kb, b_lo = b_hi + (uint32_t)np * UKC * 4;
+#pragma unroll
+        for (int j = 0; j < UKC / 8; ++j) {
+          const uint32_t ko = (uint32_t)j * 32u;
+          const uint64_t dah = make_desc(a_hi + ko), dal = make_desc(a_lo + ko);
+          const uint64_t dbh = make_desc(b_hi + ko), dbl = make_desc(b_lo + ko);
+          mma_tf32(tmem, dah, dbh, idesc, (kc > 0 || j > 0) ? 1u : 0u);
+          mma_tf32(tmem, dah, dbl, idesc, 1u);
+          mma_tf32(tmem, dal, dbh, idesc, 1u);
+        }
+        mma_commit(empty(s));
+      }
+      mma_commit(smem_u32(&bar_tfull));
+    }
+  } else if (warp >= USPLIT0) {
+    // split warps: staged slices (data row r, column f of chunk c) -> K-major
+    // records (MMA row 16c + f, k = r), fp32 split into tf32 hi + lo; rows
+    // past the row count -> zeros
+    const int st = tid - USPLIT0 * 32;
+    for (int kc = 0; kc < nk; ++kc) {
+      const int s = kc % nstages;
+      mbar_wait(full(s), (uint32_t)((kc / nstages) & 1));
+      uint8_t* base = smem + (size_t)s * L.size;
+      const int64_t row0 = (c_lo + kc) * 16;
+      const int valid = rows - row0 < 16 ? (int)(rows - row0) : 16;
+      const int na = g.xk * 64, nb = g.dk * 64;   // float4 quads (16 rows x 4 per chunk)
+      for (int i = st; i < na + nb; i += 128) {
+        const bool isa = i < na;
+        const int ii = isa ? i : i - na;
+        const int c = ii >> 6, r = (ii >> 2) & 15, q = ii & 3;
+        const float* slice = reinterpret_cast<const float*>(base + (isa ? L.sa : L.sb) + (uint32_t)c * TM_SLICE * mult);
+        const int off = pk_off(r, 4 * q);
+        float hv[4], lv[4];
+        const float4 x = *reinterpret_cast<const float4*>(slice + off);
+        if (g.split) {
+          const float4 y = *reinterpret_cast<const float4*>(slice + TM_SLICE / 4 + off);
+          hv[0] = x.x; hv[1] = x.y; hv[2] = x.z; hv[3] = x.w;
+          lv[0] = y.x; lv[1] = y.y; lv[2] = y.z; lv[3] = y.w;
+        } else {
+          split_tf32(x.x, hv[0], lv[0]);
+          split_tf32(x.y, hv[1], lv[1]);
+          split_tf32(x.z, hv[2], lv[2]);
+          split_tf32(x.w, hv[3], lv[3]);
+        }
+        if (r >= valid) {
+#pragma unroll
+          for (int t = 0; t < 4; ++t) hv[t] = lv[t] = 0.f;
+        }
+        float* kt = reinterpret_cast<float*>(base + (isa ? L.ka : L.kb));
+        const int half = (isa ? UM : np) * UKC;
+#pragma unroll
+        for (int t = 0; t < 4; ++t) {
+          const int o = pk_off(16 * c + 4 * q + t, r);
+          kt[o] = hv[t];
+          kt[half + o] = lv[t];
+        }
+      }
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // generic writes -> tcgen05 reads
+      __syncwarp();
+      if (lane == 0) mbar_arrive(smem_u32(&bar_split[s]));
+    }
+  } else {
+    // epilogue warps 2..5: feature row m = TMEM lane, columns n < N
+    const int lanegrp = warp & 3, m = lanegrp * 32 + lane;
+    mbar_wait(smem_u32(&bar_tfull), 0u);
+    tc_fence_after();
+    const uint32_t taddr = tmem + ((uint32_t)(lanegrp * 32) << 16);
+    float* crow = m < g.out_rows ? g.part + ((int64_t)blockIdx.x * g.out_rows + m) * g.N : nullptr;
+    for (int c0 = 0; c0 < np; c0 += 16) {
+      float v[16];
+      tmem_ld16(taddr + (uint32_t)c0, v);
+      if (crow) {
+#pragma unroll
+        for (int i = 0; i < 16; ++i)
+          if (c0 + i < g.N) crow[c0 + i] = v[i];
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(acc_cols));
+}
+
+kg_status umma_gemm_tn_records(const float* Xp, int64_t x_cols, const float* Dp, int64_t N, const int32_t* M_dev,
+                               int M_dev_index, int64_t rows_max, float* out, void* ws, cudaStream_t st) {
+  KG_REQUIRE(x_cols <= 128 && N <= 256, KG_ERR_SHAPE, "record TN supports d_in <= 128, N <= 256");
+  if (x_cols <= 0 || N <= 0) return KG_OK;
+  TnMnArgs a{};
+  a.Xp = Xp; a.Dp = Dp;
+  a.xk = (int)ceil_div(x_cols, UKC); a.dk = (int)ceil_div(N, UKC);
+  a.split = records_split(rows_max) ? 1 : 0;
+  a.M_dev = M_dev; a.M_dev_index = M_dev_index; a.rows = rows_max;
+  a.out_rows = x_cols; a.N = N;
+  const int splits = umma_tn_splits(rows_max, x_cols);
+  a.part = static_cast<float*>(ws);
+  const TnStage L = tn_stage(a.xk, a.dk, a.split);
+  int ns = (int)(USMEM_CAP / L.size);
+  if (ns > UMAXS) ns = UMAXS;
+  KG_REQUIRE(ns >= 2, KG_ERR_SHAPE, "record TN stage does not fit shared memory");
+  static bool attr = false;
+  if (!attr) {
+    KG_CUDA(cudaFuncSetAttribute(k_umma_tn_rec, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)USMEM_CAP));
+    attr = true;
+  }
+  KG_LAUNCH("k_umma_gemm_tn", k_umma_tn_rec, dim3((unsigned)splits, 1, 1), UTHREADS, (size_t)ns * L.size, st, a, ns,
+            acc_cols_for(16 * a.dk));
+  return reduce_splits(a.part, splits, x_cols * N, out, st);
+}
+
+// Test entry: pack row-major A (gathered) and B rows into records, then the
+// record TN (the product path gets the records from their producers).
+size_t umma_tn_records_test_workspace(int64_t M, int64_t K, int64_t N) {
+  return packed_bytes(M, K) + packed_bytes(M, N) + align_up((size_t)umma_tn_splits(M, K) * K * N * 4) + 1024;
+}
+
+kg_status umma_gemm_tn_via_records(const GemmArgs& g, float* out, void* ws, cudaStream_t st) {
+  const int64_t M = g.M_max;
+  float* Xp = static_cast<float*>(ws);
+  float* Dp = reinterpret_cast<float*>(static_cast<char*>(ws) + align_up(packed_bytes(M, g.K)));
+  void* rest = static_cast<char*>(ws) + align_up(packed_bytes(M, g.K)) + align_up(packed_bytes(M, g.N));
+  const int sp = records_split(M) ? 1 : 0;
+  const int64_t xk = ceil_div(g.K, UKC), dk = ceil_div(g.N, UKC), tiles = ceil_div(M, UM);
+  PackJob ja{g.A, g.lda, g.a_rows, g.M_dev, g.M_dev_index, g.M, g.K, UM, 0, xk, Xp, sp};
+  PackJob jb{g.B, g.ldb, nullptr, g.M_dev, g.M_dev_index, g.M, g.N, UM, 0, dk, Dp, sp};
+  kg_status s = launch_pack(ja, jb, tiles * (xk > dk ? xk : dk) * UM * 4, st);
+  if (s != KG_OK) return s;
+  return umma_gemm_tn_records(Xp, g.K, Dp, g.N, g.M_dev, g.M_dev_index, M, out, rest, st);
+}
+
+// ---------------------------------------------------------------------------
 // Filtered ranking on the tensor cores (R25/R26, ref:evaluate.py:192-217).
 //
 // Rows x = side*nq + q are the (query, side) pairs; q_x = H[anchor] * dec[r]

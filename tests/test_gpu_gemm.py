@@ -45,9 +45,14 @@ def test_nn_gathered_rows(M, K, N, impl):
     assert err(C[c_rows.long()], want) < 5e-6
 
 
-@pytest.mark.parametrize("M,K,N", [(14541, 100, 200), (1000, 128, 256), (50, 3, 8), (3000, 200, 64), (7, 5, 6)])
-@pytest.mark.parametrize("impl", [0, 1])
+@pytest.mark.parametrize("M,K,N", [(14541, 100, 200), (1000, 128, 256), (50, 3, 8), (3000, 200, 64), (7, 5, 6),
+                                   (70001, 128, 256), (70001, 32, 64)])
+@pytest.mark.parametrize("impl", [0, 1, 2])
 def test_tn_reduction(M, K, N, impl):
+    """impl 2: the record TN (X / dS operand records read as MN-major
+    operands, split hi|lo records below 65,536 rows, fp32 records above)."""
+    if impl == 2 and K > 128:
+        pytest.skip("record TN: d_in <= 128")
     g = torch.Generator(device="cuda").manual_seed(7 * M + K)
     A = torch.randn(M + 5, K, device="cuda", generator=g)
     Bm = torch.randn(M, N, device="cuda", generator=g)
