@@ -1117,8 +1117,11 @@ kg_status kg_rgcn_backward(const kg_graph_csr* G, const kg_layer_params* lp, con
   CscArgs c{G->c_indptr, G->c_dst, G->c_rel, G->c_norm, csc_chunks(G), lp->coeffs, lp->G, B, dO, w.Y, w.dZ, pos,
             c_pos, counts, t, w.dS, w.ed, w.ed_self, w.partial,
             direct_pack(G->n, (int64_t)B * dO) ? w.dS_pk : nullptr, packed_nk(G->n, (int64_t)B * dO), 1};
+  // (past L2, where the transposing pack pass and the row-major dS cost HBM
+  // traffic; L2-resident operands keep the split-record pack + TN path, whose
+  // wider grid finishes sooner on the side stream)
   const bool records_tn = H_in_packed != nullptr && c.dS_pk != nullptr && di <= 128 && B * dO <= 256 &&
-                          !getenv("KG_TN_ROWMAJOR");
+                          (!records_split(G->n) || getenv("KG_TN_RECORDS")) && !getenv("KG_TN_ROWMAJOR");
   if (records_tn) c.dS = nullptr;   // nothing reads row-major dS then
   // The parameter gradients (dV, d coeffs) feed only the optimizer: with a side
   // stream they leave the critical path (the caller joins it before the update).

@@ -564,3 +564,29 @@ def test_device_halo_expansion_fb_shape_golden():
         ex = kb.neighborhood_expand(kb.vertex_cut_partition(graph, P, seed=0), graph, 2)
         assert [len(p.support) for p in ex.partitions] == g[f"support_counts_P{P}"].tolist()
         assert [len(p.local_vertices()) for p in ex.partitions] == g[f"vertex_counts_P{P}"].tolist()
+
+
+def test_record_tn_path_matches_rowmajor_path(monkeypatch):
+    """dV from the operand records (k_umma_tn_rec; used past L2, forced here)
+    equals the row-major + transposing-pack path bit for bit."""
+    g = load_golden("synth_p4")
+    graph, pset, cfg = golden_pset(g)
+    L = len(cfg["dims"]) - 1
+    mc = kb.ModelConfig(L, cfg["dims"], cfg["num_bases"], graph.num_relations, 1, mode="embedding")
+    tc = kb.TrainConfig(epochs=1, batch_size=96, seed=2)
+    p0 = golden_params(g, "init_", L)
+    out = []
+    for env in ("KG_TN_RECORDS", "KG_TN_ROWMAJOR"):
+        monkeypatch.setenv(env, "1")
+        tr = kb.Trainer(pset, graph, mc, tc, initial_params=p0)
+        tr.begin_epoch()
+        for _ in range(min(3, tr.rounds)):
+            tr.run_round()
+        torch.cuda.synchronize()
+        out.append((tr.snapshot(), tr.epoch_losses()))
+        tr.close()
+        monkeypatch.delenv(env)
+    (a, la), (b, lb) = out
+    assert la == lb
+    for x, y in zip(a.dense_blocks(), b.dense_blocks()):
+        np.testing.assert_array_equal(x, y)
