@@ -97,7 +97,13 @@ def test_negatives_batches_closures_bit_exact(name):
 
 @pytest.mark.parametrize("n", [1, 2, 3, 17, 64, 65, 1000, 4097, 65537, 544232])
 @pytest.mark.parametrize("seed", [0, 11])
-def test_permutation_bit_exact(n, seed):
+@pytest.mark.parametrize("walk", ["auto", "block", "warp"])
+def test_permutation_bit_exact(n, seed, walk, monkeypatch):
+    """rng.permutation(n) bit-exact (and the Generator state after it), with
+    the draw walk chosen by size (auto), forced to the 8-warp block walk or to
+    the one-warp walk."""
+    if walk != "auto":
+        monkeypatch.setenv("KG_PERM_BLOCK_MIN", "33" if walk == "block" else str(1 << 40))
     gen = np.random.default_rng(seed)
     gen.random(seed % 3)   # exercise a buffered / unbuffered start
     gen.integers(7, size=seed % 2)
