@@ -332,10 +332,15 @@ def run_ours(args, world, rank, local):
     tr.check()
     t_max = torch.tensor([step_ms], dtype=torch.float64, device=dev)
     rank_ms = [step_ms]
+    rank_steps = None
     if tr.dist:
         every = [torch.zeros_like(t_max) for _ in range(world)]
         torch.distributed.all_gather(every, t_max)
         rank_ms = [float(x.item()) for x in every]
+        mine = torch.tensor([a.elapsed_time(b) for a, b in evs], dtype=torch.float64, device=dev)
+        steps_all = [torch.zeros_like(mine) for _ in range(world)]
+        torch.distributed.all_gather(steps_all, mine)
+        rank_steps = [[round(float(x), 4) for x in t.tolist()] for t in steps_all]
         torch.distributed.all_reduce(t_max, op=torch.distributed.ReduceOp.MAX)
     total_ms = float(t_max.item())
     triples_per_step = sum(tr.sizes)          # every partition's batch, all ranks
@@ -396,7 +401,7 @@ def run_ours(args, world, rank, local):
                                           parallelism=f"dp{world} (one partition per GPU)" if P == world
                                           else f"dp{world}, {P // world} partitions per GPU"),
                 "e2e": e2e, "gpu_launches": int(launches), "roofline": roofline, "cpu_baseline": cpu,
-                "rank_ms": [round(x, 3) for x in rank_ms],
+                "rank_ms": [round(x, 3) for x in rank_ms], "rank_step_ms": rank_steps,
                 "step_ms": [round(a.elapsed_time(b), 4) for a, b in evs],
                 "clocks": clk.summary()}
         print(json.dumps(line), flush=True)

@@ -61,6 +61,38 @@ __device__ __forceinline__ float warp_sum8(const float* x) {
 
 __device__ __forceinline__ int sum8_entry(unsigned l) { return ((l >> 4) & 1) * 4 + ((l >> 3) & 1) * 2 + ((l >> 2) & 1); }
 
+// Sum x[0..7] over the LPR (>= 8) lanes of a lane group (xor offsets < LPR),
+// transposed: 7 shuffles + log2(LPR / 8) for eight totals instead of
+// 8 * log2(LPR). On return the lane holds the total of entry
+// entry8<LPR>(lane); lanes differing only in the bits below LPR / 8 agree.
+template <int LPR>
+__device__ __forceinline__ float group_sum8(const float* x, unsigned l) {
+  constexpr unsigned O1 = LPR / 2, O2 = LPR / 4, O3 = LPR / 8;
+  const bool b1 = l & O1, b2 = l & O2, b3 = l & O3;
+  float y[4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const float send = b1 ? x[i] : x[i + 4], keep = b1 ? x[i + 4] : x[i];
+    y[i] = keep + __shfl_xor_sync(0xffffffffu, send, O1);
+  }
+  float z[2];
+#pragma unroll
+  for (int i = 0; i < 2; ++i) {
+    const float send = b2 ? y[i] : y[i + 2], keep = b2 ? y[i + 2] : y[i];
+    z[i] = keep + __shfl_xor_sync(0xffffffffu, send, O2);
+  }
+  const float send = b3 ? z[0] : z[1], keep = b3 ? z[1] : z[0];
+  float w = keep + __shfl_xor_sync(0xffffffffu, send, O3);
+#pragma unroll
+  for (unsigned o = O3 / 2; o >= 1; o >>= 1) w += __shfl_xor_sync(0xffffffffu, w, o);
+  return w;
+}
+
+template <int LPR>
+__device__ __forceinline__ int entry8(unsigned l) {
+  return ((l & (LPR / 2)) ? 4 : 0) + ((l & (LPR / 4)) ? 2 : 0) + ((l & (LPR / 8)) ? 1 : 0);
+}
+
 struct Chunks {
   const int32_t* ptr;
   const int32_t* row;
@@ -454,11 +486,13 @@ __global__ void __launch_bounds__(256, KG_GATHER_BPS) k_csc_backward(CscArgs a) 
             }
           }
         }
-        // per-edge dots <Y_b[u], dZ[dst]>, message groups: reduce within the group
+        // per-edge dots <Y_b[u], dZ[dst]>, message groups: one transposed
+        // reduction of the UNR (= 8) messages inside each lane group
         if (MODE != 1 && EPI > 1)
 #pragma unroll
         for (int b = 0; b < NB; ++b) {
           if (b < B) {
+            float part[UNR];
 #pragma unroll
             for (int k = 0; k < UNR; ++k) {
               float dp = 0.f;
@@ -466,12 +500,13 @@ __global__ void __launch_bounds__(256, KG_GATHER_BPS) k_csc_backward(CscArgs a) 
               for (int s = 0; s < S; ++s)
 #pragma unroll
                 for (int cc = 0; cc < VEC; ++cc) dp = fmaf(y[b][s][cc], zs[k][s][cc], dp);
-#pragma unroll
-              for (int o = 1; o < LPR; o <<= 1) dp += __shfl_xor_sync(0xffffffffu, dp, o);
-              const int e = j + k * EPI + grp;
-              const float wk = __shfl_sync(0xffffffffu, nrm[h], e & 31);
-              if (cl == 0 && e < nh) a.ed[(int64_t)(beg + 32 * h + e) * B + b] = wk * dp;
+              part[k] = dp;
             }
+            const float tot = group_sum8<LPR>(part, (unsigned)cl);
+            const int k = entry8<LPR>((unsigned)cl);
+            const int e = j + k * EPI + grp;
+            const float wk = __shfl_sync(0xffffffffu, nrm[h], e & 31);
+            if ((cl & (LPR / 8 - 1)) == 0 && e < nh) a.ed[(int64_t)(beg + 32 * h + e) * B + b] = wk * tot;
           }
         }
         // per-edge dots, one message per warp load: one transposed warp reduction per b
