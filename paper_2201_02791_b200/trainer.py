@@ -587,8 +587,9 @@ class Trainer:
         if self.dist:
             # every rank's status word rides on the same all-gather, so all
             # ranks raise the same error at the same epoch
-            both = torch.stack([means.sum(), torch.tensor(float(nloc), dtype=torch.float64, device=self.dev),
-                                f_or.double()])
+            if getattr(self, "_nloc_dev", None) is None:   # a device constant: no per-epoch host copy
+                self._nloc_dev = torch.full((), float(nloc), dtype=torch.float64, device=self.dev)
+            both = torch.stack([means.sum(), self._nloc_dev, f_or.double()])
             gathered = torch.empty((self.world, 3), dtype=torch.float64, device=self.dev)
             torch.distributed.all_gather_into_tensor(gathered, both)
             means = gathered[:, :2].reshape(-1)
@@ -993,6 +994,7 @@ def train(pset: PartitionSet, graph, model_config: ModelConfig, train_config: Tr
     report = TrainReport(rounds_per_epoch=tr.rounds, batch_sizes=list(tr.sizes),
                          setup_seconds=time.perf_counter() - t_setup)
     tc = train_config
+    _mark("train_setup")
     eval_epochs = frozenset(e for e in range(tc.epochs)
                             if tc.eval_every and (e + 1) % tc.eval_every == 0) if eval_fn is not None else frozenset()
     # Epoch-end bookkeeping (losses, non-finite flags, device epoch time) is
@@ -1018,6 +1020,8 @@ def train(pset: PartitionSet, graph, model_config: ModelConfig, train_config: Tr
             tr.run_round()
         pending.append((epoch, tr.end_epoch()))
         tr.prefetch()      # host-side capture work while the device runs this epoch
+        if epoch < 3:
+            _mark(f"epoch{epoch}")
         while len(pending) > 1 or (pending and pending[-1][0] in eval_epochs):
             settle()
     while pending:

@@ -30,7 +30,8 @@ def main():
     ap.add_argument("--profile", action="store_true")
     ap.add_argument("--gc", action="store_true", help="gc.collect() before every call")
     a = ap.parse_args()
-    graph, split, pset, mc, tc = bench.build_inputs(1, bench.BATCH)
+    world, rank, local = bench.dist_setup()      # torchrun: one partition per rank
+    graph, split, pset, mc, tc = bench.build_inputs(world, bench.BATCH)
     tr = kb.Trainer(pset, graph, mc, tc)
     epochs = math.ceil(a.rounds / tr.rounds)
     del tr
@@ -50,6 +51,8 @@ def main():
             prof.disable()
         wall = time.perf_counter() - t0
         ep = rep.epoch_seconds
+        if rank != 0:
+            continue
         print(f"call {i}: wall {wall*1e3:.1f} ms setup {rep.setup_seconds*1e3:.1f} epochs {sum(ep)*1e3:.1f} "
               f"(first {ep[0]*1e3:.2f}, median {sorted(ep)[len(ep)//2]*1e3:.2f}, max {max(ep)*1e3:.2f}) "
               f"finish {rep.finish_seconds*1e3:.1f} -> {epochs*tr_rounds(rep)*bench.BATCH/wall/1e6:.1f} M/s",
