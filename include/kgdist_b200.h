@@ -139,6 +139,9 @@ kg_status kg_kernel_timer_detach(int64_t* handle);
 kg_status kg_kernel_timer_read(int64_t handle, double* total_ms, int64_t* launches);
 /* As _read, restricted to the launches of kernel `name` (host string). */
 kg_status kg_kernel_timer_read_named(int64_t handle, const char* name, double* total_ms, int64_t* launches);
+/* Makespan of concurrent launch pairs (i-th launch of kernel a with the i-th
+ * of kernel b): summed [min start, max end] spans and the pair count. */
+kg_status kg_kernel_timer_span(int64_t handle, const char* a, const char* b, double* total_ms, int64_t* pairs);
 
 /* ---------------------------------------------------------------------- */
 /* Primitives (stable radix sort / scan) used by every stage below          */

@@ -703,6 +703,33 @@ kg_status kg_kernel_timer_read(int64_t handle, double* total_ms, int64_t* launch
   return kg_kernel_timer_read_named(handle, nullptr, total_ms, launches);
 }
 
+// Makespan of concurrent launch pairs: the i-th launch of `a` and the i-th of
+// `b` (e.g. the two CSC passes of one layer on two streams) cover
+// [min start, max end]; returns the summed spans and the pair count.
+kg_status kg_kernel_timer_span(int64_t handle, const char* a, const char* b, double* total_ms, int64_t* pairs) {
+  KG_REQUIRE(handle >= 0 && handle < (int64_t)g_detached.size(), KG_ERR_VALIDATION, "bad timer handle");
+  std::vector<const TimedLaunch*> la, lb;
+  for (auto& tl : g_detached[handle]) {
+    if (strcmp(tl.name, a) == 0) la.push_back(&tl);
+    else if (strcmp(tl.name, b) == 0) lb.push_back(&tl);
+  }
+  const size_t n = la.size() < lb.size() ? la.size() : lb.size();
+  double tot = 0.0;
+  for (size_t i = 0; i < n; ++i) {
+    KG_CUDA(cudaEventSynchronize(la[i]->end));
+    KG_CUDA(cudaEventSynchronize(lb[i]->end));
+    float ea = 0.f, sb = 0.f, eb = 0.f;   // relative to a's start
+    KG_CUDA(cudaEventElapsedTime(&ea, la[i]->start, la[i]->end));
+    KG_CUDA(cudaEventElapsedTime(&sb, la[i]->start, lb[i]->start));
+    KG_CUDA(cudaEventElapsedTime(&eb, la[i]->start, lb[i]->end));
+    const float lo = sb < 0.f ? sb : 0.f, hi = eb > ea ? eb : ea;
+    tot += hi - lo;
+  }
+  *total_ms = tot;
+  *pairs = (int64_t)n;
+  return KG_OK;
+}
+
 kg_status kg_kernel_timer_end(double* total_ms, int64_t* launches) {
   kg::g_timer_on = false;
   double tot = 0.0;

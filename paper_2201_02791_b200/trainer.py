@@ -311,6 +311,9 @@ def _assemble_embed(pset: PartitionSet, tables, base: np.ndarray) -> np.ndarray:
 # ---------------------------------------------------------------------------
 
 PREP_BRANCHES = int(os.environ.get("KG_PREP_BRANCHES", "4"))   # <= KG_PREP_MAX_BRANCHES
+# eager rounds before the round graphs are captured (lazy workspaces and
+# one-time kernel attributes are set up by them)
+EAGER_WARMUP = int(os.environ.get("KG_EAGER_WARMUP", "2"))
 
 
 def _align256(x: int) -> int:
@@ -689,7 +692,7 @@ class Trainer:
         cur = torch.cuda.current_stream()
         self._prio.wait_stream(cur)
         with torch.cuda.stream(self._prio):
-            if not self.use_graphs or self._eager_rounds < 2:
+            if not self.use_graphs or self._eager_rounds < EAGER_WARMUP:
                 self._compute_body()
                 if self.dist:
                     self._gather()
@@ -753,7 +756,7 @@ class Trainer:
         for w in self.workers:
             if w.sampler.prefetch():
                 return True
-        if self.use_graphs and self._eager_rounds >= 2:
+        if self.use_graphs and self._eager_rounds >= EAGER_WARMUP:
             for slot in range(EpochSampler.NSLOTS):
                 key = tuple(w.sampler.slot_stream(slot).triples.data_ptr() for w in self.workers)
                 if key not in self._graphs:
