@@ -29,7 +29,7 @@ constexpr int MAXB = 4;
 constexpr int UNR = 8;     // gathered rows in flight per lane
 constexpr int MAXC = 64;   // messages per chunk handled by one warp (2 per lane)
 #ifndef KG_GATHER_BPS
-#define KG_GATHER_BPS 3    // resident 256-thread blocks per SM of the gather kernels
+#define KG_GATHER_BPS 4    // resident 256-thread blocks per SM of the gather kernels (4: +7 % HBM at wikikg2 shape, no spills; 5 spills)
 #endif
 
 // Sum x[0..7] over the 32 lanes of a warp, 9 shuffles: on return lane l holds
