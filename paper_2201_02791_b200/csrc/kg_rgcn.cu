@@ -698,7 +698,7 @@ __global__ void __launch_bounds__(CB_THREADS) k_csc_combine(CscArgs a) {
 // tree), k_dcoeff_final adds the slices in order -> deterministic, and heavy
 // relations are spread over several blocks (split grows with the average
 // group size, up to DC_SPLIT).
-constexpr int DC_SPLIT = 64;
+constexpr int DC_SPLIT = 1024;   // few relation groups (citation2: 3) still fill the GPU
 
 static int dcoeff_split(int64_t e, int64_t groups) {
   int64_t s = (e / (groups > 0 ? groups : 1) + 4095) / 4096;
