@@ -31,7 +31,9 @@ def err(got, want):
 
 
 @pytest.mark.parametrize("M,K,N", [(1000, 200, 100), (14541, 100, 200), (300, 5, 6), (5, 3, 4), (130, 256, 256),
-                                   (257, 33, 17), (1, 8, 16)])
+                                   (257, 33, 17), (1, 8, 16),
+                                   # fp32 A records (> 65,536 rows): weight-resident CTA pairs for N % 32 == 0
+                                   (70001, 128, 256), (70001, 256, 128), (70001, 100, 64), (70001, 100, 100)])
 @pytest.mark.parametrize("impl", [0, 1])
 def test_nn_gathered_rows(M, K, N, impl):
     g = torch.Generator(device="cuda").manual_seed(M + K + N)
