@@ -462,6 +462,11 @@ def run_reference(args, world, rank):
         return
     import kg_inputs as ki
     import kg_oracle as ko
+    try:   # torchrun exports OMP_NUM_THREADS=1: give the CPU reference every host core
+        import threadpoolctl
+        threadpoolctl.threadpool_limits(limits=os.cpu_count())
+    except Exception:
+        pass
     g = ki.synthetic_graph(FB["num_entities"], FB["num_relations"], FB["avg_degree"], FB["seed"])
     parts = ki.partition_inputs(g, world, seed=0, hops=2)
     views, ends = [], []

@@ -459,6 +459,33 @@ kg_status kg_eval_candidates(const float* H, int32_t d, const float* decoder, co
                              double* ranks, int32_t* ncand, void* stream);
 
 /* ---------------------------------------------------------------------- */
+/* Float64 public-API path (encode / loss_from_cache, ref:model.py:151-301) */
+/* ---------------------------------------------------------------------- */
+/* One layer over the closure: targets p < T (local id order[p]); H_in /
+ * H_out (n, d) float64 by local id; acc (T, B*din) and Z (T, dout) by
+ * position are kept for the backward. src / rel / cnt: the view's messages in
+ * reference order (norm = 1/cnt exactly). mask (optional, fp32 (T, dout) by
+ * position, nonzero = keep) scales kept values by mask_scale. */
+kg_status kg_forward_layer_f64(const kg_graph_csr* g, const int32_t* src, const int32_t* rel, const int32_t* cnt,
+                               const int32_t* order, const int32_t* pos, int32_t T, int32_t din, int32_t dout,
+                               int32_t B, const double* bases, const double* coeffs, const double* H_in, double* acc,
+                               double* Z, double* H_out, int32_t relu, const float* mask, double mask_scale,
+                               void* stream);
+/* DistMult + BCE: loss (device scalar, accumulated), d_decoder (R, d) and
+ * dH (n, d) by local id (accumulated; caller zeroes). */
+kg_status kg_loss_f64(const int32_t* triples, const double* labels, int64_t b, const double* H, const double* decoder,
+                      int32_t d, double* loss, double* d_decoder, double* dH, uint32_t* flags, void* stream);
+int64_t kg_layer64_workspace_bytes(int64_t n, int32_t din, int32_t dout, int32_t B);
+/* Layer gradients: dZ (T, dout) scratch, d_bases (B, din, dout), d_coeffs
+ * (2R+1, B), dH_in (n, din) by local id (optional). */
+kg_status kg_backward_layer_f64(const kg_graph_csr* g, const int32_t* src, const int32_t* rel, const int32_t* cnt,
+                                const int32_t* order, const int32_t* pos, int32_t T, int32_t din, int32_t dout,
+                                int32_t B, const double* bases, const double* coeffs, const double* H_in,
+                                const double* acc, const double* Z, const double* dH_out, int32_t relu,
+                                const float* mask, double mask_scale, double* dZ, double* d_bases, double* d_coeffs,
+                                double* dH_in, void* ws, int64_t ws_bytes, void* stream);
+
+/* ---------------------------------------------------------------------- */
 /* N1  n-hop halo expansion (ref:partition.py:211-282)                     */
 /* ---------------------------------------------------------------------- */
 /* tri: the graph's (m,3) int32 triples on the device. kg_halo_incidence

@@ -145,6 +145,12 @@ _PROTOS = {
     "kg_encode_full_f64": (ST, [POINTER(KgGraphCsr), P, P, P, c_int32, P, c_int32, P, P, P, P, P, c_int64, P]),
     "kg_known_keys_workspace_bytes": (c_int64, [c_int64]),
     "kg_known_keys": (ST, [P, c_int64, c_int32, c_int32, c_int32, c_int32, P, P, P, c_int64, P]),
+    "kg_forward_layer_f64": (ST, [POINTER(KgGraphCsr), P, P, P, P, P, c_int32, c_int32, c_int32, c_int32, P, P, P, P,
+                                  P, P, c_int32, P, c_double, P]),
+    "kg_loss_f64": (ST, [P, P, c_int64, P, P, c_int32, P, P, P, P, P]),
+    "kg_layer64_workspace_bytes": (c_int64, [c_int64, c_int32, c_int32, c_int32]),
+    "kg_backward_layer_f64": (ST, [POINTER(KgGraphCsr), P, P, P, P, P, c_int32, c_int32, c_int32, c_int32, P, P, P,
+                                   P, P, P, c_int32, P, c_double, P, P, P, P, P, c_int64, P]),
     "kg_halo_workspace_bytes": (c_int64, [c_int64, c_int64]),
     "kg_halo_incidence": (ST, [P, c_int64, c_int64, P, P, P, c_int64, P]),
     "kg_halo_expand": (ST, [P, c_int64, c_int64, P, P, P, c_int64, c_int32, P, P, P, P, P, P, P, c_int64, P]),

@@ -13,6 +13,7 @@ from __future__ import annotations
 
 import ctypes
 import json
+import os
 from dataclasses import dataclass, field
 from typing import Optional
 
@@ -444,6 +445,7 @@ class EncodeCache:
     model: Optional[DeviceModel] = None
     bufs: Optional[ViewBuffers] = None
     seed_embeddings: Optional[np.ndarray] = None
+    f64: Optional[dict] = None   # float64 path: H / acc / Z per layer, masks
 
 
 def _input_rows(config, cg, input_table, input_ids, device):
@@ -458,16 +460,164 @@ def _input_rows(config, cg, input_table, input_ids, device):
     return torch.as_tensor(np.ascontiguousarray(input_table[ids], dtype=np.float32)).to(device)
 
 
+# Precision of the public numpy API (encode / loss_from_cache /
+# loss_and_grad): "f64" runs the float64 device kernels (kg_model64.cu), the
+# reference's own precision; "f32" runs the training hot path's fp32 /
+# tensor-core kernels (what Trainer uses; parity tests of those kernels
+# select it with `api_precision("f32")`). KG_API_PRECISION sets the default.
+API_PRECISION = os.environ.get("KG_API_PRECISION", "f64")
+
+
+class api_precision:
+    """Context manager: `with api_precision("f32"): ...`."""
+
+    def __init__(self, prec: str):
+        if prec not in ("f32", "f64"):
+            raise ValidationError(f"unknown precision {prec!r}")
+        self.prec = prec
+
+    def __enter__(self):
+        global API_PRECISION
+        self.saved, API_PRECISION = API_PRECISION, self.prec
+        return self
+
+    def __exit__(self, *exc):
+        global API_PRECISION
+        API_PRECISION = self.saved
+
+
+def _draw_masks(config, cg, bufs, dropout_rng, dev):
+    """Dropout masks of the non-last layers from the caller's Generator (device
+    PCG64 stream at numpy's positions); the Generator advances as numpy's."""
+    g_dev = _lib.pcg_to_device(_lib.pcg_from_numpy(dropout_rng), dev)
+    masks = device_dropout(bufs, g_dev, config.dropout)
+    counts = cg.d_counts.cpu().tolist()
+    L = config.num_layers
+    dropout_rng.bit_generator.advance(sum(int(counts[L - 1 - l]) * config.dims[l + 1] for l in range(L - 1)))
+    return masks
+
+
+def _encode64(params: ModelParams, config: ModelConfig, cg, input_table, input_ids, drop, dropout_rng,
+              cache) -> np.ndarray:
+    """Float64 forward over the closure (kg_forward_layer_f64 per layer)."""
+    torch = _torch()
+    view = cg.view
+    dev = view.device
+    n = view.n
+    L = config.num_layers
+    f64 = lambda a: torch.as_tensor(np.ascontiguousarray(a, dtype=np.float64)).to(dev)
+    input_table = np.asarray(input_table)
+    if input_table.ndim != 2 or input_table.shape[1] != config.dims[0]:
+        raise ShapeError(f"input width {input_table.shape[1] if input_table.ndim == 2 else '?'} "
+                         f"!= d_in {config.dims[0]}")
+    ids = np.asarray(input_ids)[:n]
+    if len(ids) != n:
+        raise IntegrityError("input_ids must cover every local vertex of the view")
+    counts = cg.layer_vertex_counts
+    bases = [f64(b) for b in params.bases]
+    coeffs = [f64(c) for c in params.coeffs]
+    H = [f64(input_table[ids])] + [torch.zeros((n, config.dims[l]), dtype=torch.float64, device=dev)
+                                   for l in range(1, L + 1)]
+    masks = None
+    if drop:
+        bufs = ViewBuffers(config, view, 1)
+        bufs.order.copy_(cg.d_order)
+        bufs.counts.copy_(cg.d_counts)
+        masks = _draw_masks(config, cg, bufs, dropout_rng, dev)
+    scale = 1.0 / (1.0 - config.dropout) if drop else 1.0
+    csr = view.csr()
+    st = _lib.stream_handle()
+    accs, Zs = [], []
+    for l in range(L):
+        t = L - 1 - l
+        T = counts[t]
+        din, dout = config.dims[l], config.dims[l + 1]
+        acc = torch.empty((max(T, 1), config.num_bases * din), dtype=torch.float64, device=dev)
+        Z = torch.empty((max(T, 1), dout), dtype=torch.float64, device=dev)
+        mask = masks[l] if (masks is not None and l < L - 1) else None
+        _lib.call("kg_forward_layer_f64", ctypes.byref(csr), view.d_ref_src.data_ptr(), view.d_ref_rel.data_ptr(),
+                  view.d_msg_cnt.data_ptr(), cg.d_order.data_ptr(), cg.d_pos.data_ptr(), T, din, dout,
+                  config.num_bases, bases[l].data_ptr(), coeffs[l].data_ptr(), H[l].data_ptr(), acc.data_ptr(),
+                  Z.data_ptr(), H[l + 1].data_ptr(), 1 if l < L - 1 else 0, _lib.ptr(mask), scale, st)
+        accs.append(acc)
+        Zs.append(Z)
+    seeds = cg.seed_vertices
+    out = H[L][torch.as_tensor(seeds, device=dev)].cpu().numpy()
+    if cache is not None:
+        cache.model = None
+        cache.bufs = None
+        cache.f64 = dict(H=H, acc=accs, Z=Zs, masks=masks, scale=scale, bases=bases, coeffs=coeffs)
+        cache.seed_embeddings = out
+    return out
+
+
+def _loss_from_cache64(params, config, batch, cg, cache, input_ids) -> tuple:
+    torch = _torch()
+    view = cg.view
+    dev = view.device
+    n = view.n
+    L = config.num_layers
+    c = cache.f64
+    H, bases, coeffs = c["H"], c["bases"], c["coeffs"]
+    tri = torch.as_tensor(np.ascontiguousarray(batch.triples, dtype=np.int32)).to(dev)
+    lab = torch.as_tensor(np.asarray(batch.labels, dtype=np.float64)).to(dev)
+    dec = torch.as_tensor(np.ascontiguousarray(params.decoder, dtype=np.float64)).to(dev)
+    loss = torch.zeros(1, dtype=torch.float64, device=dev)
+    d_dec = torch.zeros_like(dec)
+    dH = [torch.zeros((n, config.dims[l]), dtype=torch.float64, device=dev) for l in range(L + 1)]
+    flags = torch.zeros(1, dtype=torch.int32, device=dev)
+    st = _lib.stream_handle()
+    _lib.call("kg_loss_f64", tri.data_ptr(), lab.data_ptr(), len(batch.triples), H[L].data_ptr(), dec.data_ptr(),
+              config.dims[-1], loss.data_ptr(), d_dec.data_ptr(), dH[L].data_ptr(), flags.data_ptr(), st)
+    f = int(flags.item())
+    if f:
+        raise_for_flags(f)
+    lv = float(loss.item())
+    if not np.isfinite(lv):
+        raise NumericError("non-finite loss")
+    csr = view.csr()
+    lib = _lib.require_cuda()
+    counts = cg.layer_vertex_counts
+    B, G = config.num_bases, config.num_rel_groups
+    db, dc = [None] * L, [None] * L
+    for l in range(L - 1, -1, -1):
+        t = L - 1 - l
+        T = counts[t]
+        din, dout = config.dims[l], config.dims[l + 1]
+        ws = torch.empty(lib.kg_layer64_workspace_bytes(n, din, dout, B), dtype=torch.uint8, device=dev)
+        dZ = torch.empty((max(T, 1), dout), dtype=torch.float64, device=dev)
+        d_b = torch.empty((B, din, dout), dtype=torch.float64, device=dev)
+        d_c = torch.empty((G, B), dtype=torch.float64, device=dev)
+        mask = c["masks"][l] if (c["masks"] is not None and l < L - 1) else None
+        want_in = l > 0 or config.mode == MODE_EMBEDDING
+        _lib.call("kg_backward_layer_f64", ctypes.byref(csr), view.d_ref_src.data_ptr(), view.d_ref_rel.data_ptr(),
+                  view.d_msg_cnt.data_ptr(), cg.d_order.data_ptr(), cg.d_pos.data_ptr(), T, din, dout, B,
+                  bases[l].data_ptr(), coeffs[l].data_ptr(), H[l].data_ptr(), c["acc"][l].data_ptr(),
+                  c["Z"][l].data_ptr(), dH[l + 1].data_ptr(), 1 if l < L - 1 else 0, _lib.ptr(mask), c["scale"],
+                  dZ.data_ptr(), d_b.data_ptr(), d_c.data_ptr(), dH[l].data_ptr() if want_in else None,
+                  ws.data_ptr(), ws.numel(), st)
+        db[l], dc[l] = d_b.cpu().numpy(), d_c.cpu().numpy()
+    g = Gradients(db, dc, d_dec.cpu().numpy())
+    if config.mode == MODE_EMBEDDING:
+        order = cg.vertex_order
+        g.embed_ids = np.asarray(input_ids)[order]
+        g.embed_rows = dH[0][torch.as_tensor(order, device=dev)].cpu().numpy()
+    return lv, g
+
+
 def encode(params: ModelParams, config: ModelConfig, cg, input_table: np.ndarray, input_ids: np.ndarray,
            training: bool = False, dropout_rng: Optional[np.random.Generator] = None,
            cache: Optional[EncodeCache] = None) -> np.ndarray:
     """Graph convolutions over a (device) compute graph; returns the seed
-    embeddings in cg.seed_vertices order (ref:model.py:196-235)."""
+    embeddings in cg.seed_vertices order (ref:model.py:196-235). Float64 on
+    the device by default (API_PRECISION)."""
     if cg.num_layers != config.num_layers:
         raise ShapeError(f"compute graph has {cg.num_layers} layers, model has {config.num_layers}")
     drop = training and config.dropout > 0.0
     if drop and dropout_rng is None:
         raise ValidationError("training with dropout needs a dropout rng")
+    if API_PRECISION == "f64":
+        return _encode64(params, config, cg, input_table, input_ids, drop, dropout_rng, cache)
     view = cg.view
     dev = view.device
     model = DeviceModel.from_params(config, params, dev)
@@ -476,15 +626,7 @@ def encode(params: ModelParams, config: ModelConfig, cg, input_table: np.ndarray
     bufs.order.copy_(cg.d_order)
     bufs.pos.copy_(cg.d_pos)
     bufs.counts.copy_(cg.d_counts)
-    masks = None
-    if drop:
-        # the Generator's stream drives the device masks; afterwards the
-        # Generator is advanced exactly as numpy's random((T, d)) calls would
-        g_dev = _lib.pcg_to_device(_lib.pcg_from_numpy(dropout_rng), dev)
-        masks = device_dropout(bufs, g_dev, config.dropout)
-        counts = cg.d_counts.cpu().tolist()
-        L = config.num_layers
-        dropout_rng.bit_generator.advance(sum(int(counts[L - 1 - l]) * config.dims[l + 1] for l in range(L - 1)))
+    masks = _draw_masks(config, cg, bufs, dropout_rng, dev) if drop else None
     bufs.masks = masks
     device_forward(model, bufs, masks=masks)
     seeds = cg.seed_vertices
@@ -514,6 +656,12 @@ def loss_from_cache(params: ModelParams, config: ModelConfig, batch, cg, cache: 
     """BCE over the batch and exact gradients from the cached device
     activations (ref:model.py:254-301); returns (loss, Gradients)."""
     torch = _torch()
+    if getattr(cache, "f64", None) is not None:
+        if len(batch.triples) == 0:
+            raise ValidationError("empty batch")
+        if not np.isin(batch.triples[:, [0, 2]], cg.seed_vertices).all():
+            raise IntegrityError("vertex not present in compute graph")
+        return _loss_from_cache64(params, config, batch, cg, cache, input_ids)
     from .sampler import DeviceStream
     model, bufs = cache.model, cache.bufs
     dev = bufs.view.device

@@ -72,8 +72,11 @@ def teacher_forced(graph, P, dims, hops, b, seed=0, num_bases=2):
     batch = kb.make_batches(v.core_edges, neg, b, rng, num_batches=1)[0]
     cg = kb.build_compute_graph(batch, v, hops)
     cache = kb.EncodeCache()
-    kb.encode(p, mc, cg, p.entity_embed, v.local_ids, cache=cache)
-    loss, gr = kb.loss_from_cache(p, mc, batch, cg, cache, v.local_ids)
+    with kb.model.api_precision("f32"):     # the training path's fp32 / tensor-core kernels
+        kb.encode(p, mc, cg, p.entity_embed, v.local_ids, cache=cache)
+        loss, gr = kb.loss_from_cache(p, mc, batch, cg, cache, v.local_ids)
+    with kb.model.api_precision("f64"):     # the public API's float64 path
+        loss64, gr64 = kb.loss_and_grad(p, mc, batch, cg, p.entity_embed, v.local_ids)
     ov = ko.make_view(part.core, part.support, graph.num_entities, graph.num_relations, pool_size=part.pool_size)
     oneg = ko.corrupt(ov, 1, np.random.default_rng(seed ^ part.id))
     np.testing.assert_array_equal(oneg, neg)                                   # negatives bit-exact
@@ -87,6 +90,7 @@ def teacher_forced(graph, P, dims, hops, b, seed=0, num_bases=2):
     oloss, og = ko.backward(op, bt, ocg, tr, ov.local_ids)
     names = [f"bases{l}" for l in range(hops)] + [f"coeffs{l}" for l in range(hops)] + ["decoder"]
     errs = [rel_l2(a, w) for a, w in zip(gr.dense_blocks(), og.dense())]
+    errs64 = [rel_l2(a, w) for a, w in zip(gr64.dense_blocks(), og.dense())] + [rel_l2(gr64.embed_rows, og.embed_rows)]
     np.testing.assert_array_equal(gr.embed_ids, og.embed_ids)
     e_rows = rel_l2(gr.embed_rows, og.embed_rows)
     # ReLU masks: a pre-activation within fp32 rounding of 0 can take the other
@@ -110,6 +114,7 @@ def teacher_forced(graph, P, dims, hops, b, seed=0, num_bases=2):
     errs2 = [rel_l2(a, w) for a, w in zip(gr.dense_blocks(), og2.dense())]
     e_rows2 = rel_l2(gr.embed_rows, og2.embed_rows)
     return dict(loss=loss, oracle_loss=oloss, loss_rel=abs(loss - oloss) / abs(oloss), grad_rel_l2_max=max(errs),
+                f64_loss_rel=abs(loss64 - oloss) / abs(oloss), f64_grad_rel_l2_max=max(errs64),
                 embed_rows_rel_l2=e_rows, grad_rel_l2=dict(zip(names, errs)), relu_flips=flips,
                 relu_flip_max_rel_pre=flip_rel, aligned_grad_rel_l2_max=max(errs2), aligned_embed_rows_rel_l2=e_rows2,
                 batch=len(batch), closure_counts=cg.layer_vertex_counts, edges=[blk.num_edges for blk in ocg.layers])
@@ -121,6 +126,7 @@ def check_teacher_forced(r):
     pre-activation within 1e-5 of the layer's largest), and <= 1e-4 outright
     when no mask element flipped."""
     assert r["loss_rel"] <= 1e-5
+    assert r["f64_loss_rel"] <= 1e-12 and r["f64_grad_rel_l2_max"] <= 1e-10   # float64 public API
     assert r["relu_flip_max_rel_pre"] <= 1e-5
     assert r["aligned_grad_rel_l2_max"] <= 1e-4 and r["aligned_embed_rows_rel_l2"] <= 1e-4
     if r["relu_flips"] == 0:

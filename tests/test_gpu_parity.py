@@ -148,9 +148,20 @@ def test_epoch_sampler_matches_reference_streams(monkeypatch, async_rounds):
         assert es.redos > 0
 
 
+TOL = {"f32": dict(emb=1e-5, loss=1e-5, grad=1e-4), "f64": dict(emb=1e-12, loss=1e-12, grad=1e-10)}
+
+
+@pytest.mark.parametrize("prec", ["f32", "f64"])
 @pytest.mark.parametrize("name", SCEN)
-def test_step_loss_and_gradients_match_reference(name):
-    """Teacher-forced single step: same fp32-representable params, same batch."""
+def test_step_loss_and_gradients_match_reference(name, prec):
+    """Teacher-forced single step: same fp32-representable params, same batch;
+    the public API in float64 (the default, kg_model64.cu) and in the
+    training path's fp32 / tensor-core kernels."""
+    with kb.model.api_precision(prec):
+        _step_vs_golden(name, TOL[prec])
+
+
+def _step_vs_golden(name, tol):
     g = load_golden(name)
     graph, pset, cfg = golden_pset(g)
     v = kb.build_view(pset.partitions[0], graph.num_entities, graph.num_relations)
@@ -162,16 +173,16 @@ def test_step_loss_and_gradients_match_reference(name):
     table = params.entity_embed if cfg["mode"] == "embedding" else g["features"]
     cache = kb.EncodeCache()
     emb = kb.encode(params, mc, cg, table, v.local_ids, cache=cache)
-    assert rel_l2(emb, g["b0_seed_emb"]) < 1e-5
+    assert rel_l2(emb, g["b0_seed_emb"]) < tol["emb"]
     loss, grads = kb.loss_from_cache(params, mc, b, cg, cache, v.local_ids)
-    assert abs(loss - float(g["b0_loss"])) / abs(float(g["b0_loss"])) < 1e-5
+    assert abs(loss - float(g["b0_loss"])) / abs(float(g["b0_loss"])) < tol["loss"]
     for l in range(L):
-        assert rel_l2(grads.bases[l], g[f"b0_dbases_{l}"]) < 1e-4
-        assert rel_l2(grads.coeffs[l], g[f"b0_dcoeffs_{l}"]) < 1e-4
-    assert rel_l2(grads.decoder, g["b0_ddecoder"]) < 1e-4
+        assert rel_l2(grads.bases[l], g[f"b0_dbases_{l}"]) < tol["grad"]
+        assert rel_l2(grads.coeffs[l], g[f"b0_dcoeffs_{l}"]) < tol["grad"]
+    assert rel_l2(grads.decoder, g["b0_ddecoder"]) < tol["grad"]
     if cfg["mode"] == "embedding":
         np.testing.assert_array_equal(grads.embed_ids, g["b0_embed_ids"])
-        assert rel_l2(grads.embed_rows, g["b0_embed_rows"]) < 1e-4
+        assert rel_l2(grads.embed_rows, g["b0_embed_rows"]) < tol["grad"]
 
 
 @pytest.mark.parametrize("name", SCEN)
@@ -254,8 +265,9 @@ def test_oracle_parity_on_fb_batch(dims):
     batch = kb.make_batches(v.core_edges, neg, 4096, rng, num_batches=1)[0]
     cg = kb.build_compute_graph(batch, v, 2)
     cache = kb.EncodeCache()
-    kb.encode(p, mc, cg, p.entity_embed, v.local_ids, cache=cache)
-    loss, gr = kb.loss_from_cache(p, mc, batch, cg, cache, v.local_ids)
+    with kb.model.api_precision("f32"):     # the training path's kernels
+        kb.encode(p, mc, cg, p.entity_embed, v.local_ids, cache=cache)
+        loss, gr = kb.loss_from_cache(p, mc, batch, cg, cache, v.local_ids)
     ov = ko.make_view(part.core, part.support, graph.num_entities, 237, pool_size=part.pool_size)
     ocg = ko.closure(ov, batch.seed_vertices, 2)
     np.testing.assert_array_equal(ocg.vertex_order, cg.vertex_order)
@@ -319,7 +331,8 @@ def test_prepacked_weights_are_bitwise_identical(monkeypatch):
     batch = kb.make_batches(v.core_edges, kb.sample_negatives(v, 1, rng), 1024, rng, num_batches=1)[0]
     cg = kb.build_compute_graph(batch, v, 2)
     cache = kb.EncodeCache()
-    kb.encode(p, mc, cg, p.entity_embed, v.local_ids, cache=cache)
+    with kb.model.api_precision("f32"):
+        kb.encode(p, mc, cg, p.entity_embed, v.local_ids, cache=cache)
     model, bufs = cache.model, cache.bufs
     from paper_2201_02791_b200.sampler import DeviceStream
     tri = torch.as_tensor(batch.triples.astype(np.int32)).cuda()
@@ -371,7 +384,8 @@ def test_tensor_core_ranking_matches_exact_fma_ranking(policy):
     assert abs(a.mrr - mrr_o) / mrr_o <= 1e-6 and abs(b.mrr - mrr_o) / mrr_o <= 1e-3
 
 
-def test_dropout_step_and_training_match_reference():
+@pytest.mark.parametrize("prec", ["f32", "f64"])
+def test_dropout_step_and_training_match_reference(prec, monkeypatch):
     """Inverted dropout on the device: masks from the caller's Generator
     (state advanced exactly as numpy's), teacher-forced loss/gradients, and a
     2-partition training run with dropout 0.25 against the reference."""
@@ -386,15 +400,17 @@ def test_dropout_step_and_training_match_reference():
     cg = kb.build_compute_graph(b, v, L)
     drng = rng_from_state(g["drng_init"])
     cache = kb.EncodeCache()
+    tol = TOL[prec]
+    monkeypatch.setattr(kb.model, "API_PRECISION", prec)
     emb = kb.encode(params, mc, cg, params.entity_embed, v.local_ids, training=True, dropout_rng=drng, cache=cache)
     assert state_tuple(drng) == state_tuple(rng_from_state(g["drng_after"]))
-    assert rel_l2(emb, g["b0_seed_emb"]) < 1e-5
+    assert rel_l2(emb, g["b0_seed_emb"]) < tol["emb"]
     loss, grads = kb.loss_from_cache(params, mc, b, cg, cache, v.local_ids)
-    assert abs(loss - float(g["b0_loss"])) / abs(float(g["b0_loss"])) < 1e-5
+    assert abs(loss - float(g["b0_loss"])) / abs(float(g["b0_loss"])) < tol["loss"]
     for l in range(L):
-        assert rel_l2(grads.bases[l], g[f"b0_dbases_{l}"]) < 1e-4
-        assert rel_l2(grads.coeffs[l], g[f"b0_dcoeffs_{l}"]) < 1e-4
-    assert rel_l2(grads.embed_rows, g["b0_embed_rows"]) < 1e-4
+        assert rel_l2(grads.bases[l], g[f"b0_dbases_{l}"]) < tol["grad"]
+        assert rel_l2(grads.coeffs[l], g[f"b0_dcoeffs_{l}"]) < tol["grad"]
+    assert rel_l2(grads.embed_rows, g["b0_embed_rows"]) < tol["grad"]
     tc = kb.TrainConfig(epochs=cfg["epochs"], batch_size=cfg["batch"], optimizer="adam", learning_rate=0.01,
                         seed=cfg["train_seed"])
     got, report = kb.train(pset, graph, mc, tc, initial_params=golden_params(g, "init_", L))
