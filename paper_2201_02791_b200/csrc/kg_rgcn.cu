@@ -135,9 +135,19 @@ __device__ __forceinline__ void zero3(float (&a)[NB][S][VEC]) {
 // metadata of message `lane + 32*h` of the chunk, coefficient c_b = norm * a[rel, b]
 template <int NB>
 struct EdgeMeta {
-  int32_t other[2];        // src (forward) / destination position (backward)
+  uint32_t off[2];         // element offset of the gathered row: src * d (forward) / dst position * d (backward)
   float cf[2][NB];
 };
+
+// Lane base pointers of a gather: column (s * LPR + cl) * VEC of row 0. Lanes
+// past the row width point at column 0, so every lane loads real data and the
+// message loop needs no per-lane predicate (their sums are never stored, and
+// the dots multiply them by zero Y entries).
+template <int S, int VEC, int LPR>
+__device__ __forceinline__ void lane_bases(const float* base, int cl, const bool (&ok)[S], const float* (&p)[S]) {
+#pragma unroll
+  for (int s = 0; s < S; ++s) p[s] = base + (ok[s] ? (s * LPR + cl) * VEC : 0);
+}
 
 // EPI > 1 (narrow rows, d <= 128 / EPI): lanes split into EPI groups of
 // LPR = 32 / EPI lanes; each group gathers a different message, so a warp
@@ -159,27 +169,37 @@ __global__ void __launch_bounds__(256, KG_GATHER_BPS) k_aggregate(AggArgs a) {
   bool slot_ok[S];
 #pragma unroll
   for (int s = 0; s < S; ++s) slot_ok[s] = (s * LPR + cl) * VEC < d;
+  const float* hb[S];
+  lane_bases<S, VEC, LPR>(a.H, cl, slot_ok, hb);
   for (int64_t c = warp_uniform((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5); c < NC; c += warps) {
     const int4 dsc = a.ck.desc[c];
     const int32_t v = dsc.x, beg = dsc.y, cnt = dsc.z & 0xffff;
     const bool single = dsc.z & CH_SINGLE;
     const int32_t p = a.pos[v];
     if (p < 0 || p >= T) continue;
+    // message slots past cnt (the loop runs in groups of UNR * EPI) gather the
+    // chunk's first row with weight zero: no per-message predicate or zeroing
     EdgeMeta<NB> m;
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
       const int e = lane + 32 * h;
-      m.other[h] = 0;
+      m.off[h] = 0;
 #pragma unroll
       for (int b = 0; b < NB; ++b) m.cf[h][b] = 0.f;
       if (e < cnt) {
-        m.other[h] = a.src[beg + e];
+        m.off[h] = (uint32_t)a.src[beg + e] * (uint32_t)d;
         const int32_t r = a.rel[beg + e];
         const float w = a.norm[beg + e];
 #pragma unroll
         for (int b = 0; b < NB; ++b)
           if (b < B) m.cf[h][b] = w * coef[r * B + b];
       }
+    }
+    {
+      const uint32_t off0 = __shfl_sync(0xffffffffu, m.off[0], 0);
+#pragma unroll
+      for (int h = 0; h < 2; ++h)
+        if (lane + 32 * h >= cnt) m.off[h] = off0;
     }
     float acc[NB][S][VEC];
     zero3<NB, VEC, S>(acc);
@@ -190,15 +210,9 @@ __global__ void __launch_bounds__(256, KG_GATHER_BPS) k_aggregate(AggArgs a) {
         float xs[UNR][S][VEC];
 #pragma unroll
         for (int q = 0; q < UNR; ++q) {
-          const int32_t u = __shfl_sync(0xffffffffu, m.other[h], (j + q * EPI + grp) & 31);
+          const uint32_t off = __shfl_sync(0xffffffffu, m.off[h], (j + q * EPI + grp) & 31);
 #pragma unroll
-          for (int s = 0; s < S; ++s) {
-            if (j + q * EPI + grp < nh && slot_ok[s])
-              VecIO<VEC>::load(a.H + (int64_t)u * d + (s * LPR + cl) * VEC, xs[q][s]);
-            else
-#pragma unroll
-              for (int cc = 0; cc < VEC; ++cc) xs[q][s][cc] = 0.f;
-          }
+          for (int s = 0; s < S; ++s) VecIO<VEC>::load(hb[s] + off, xs[q][s]);
         }
 #pragma unroll
         for (int q = 0; q < UNR; ++q) {
@@ -407,6 +421,8 @@ __global__ void __launch_bounds__(256, KG_GATHER_BPS) k_csc_backward(CscArgs a) 
   bool slot_ok[S];
 #pragma unroll
   for (int s = 0; s < S; ++s) slot_ok[s] = (s * LPR + cl) * VEC < d;
+  const float* zb[S];
+  lane_bases<S, VEC, LPR>(a.dZ, cl, slot_ok, zb);
   for (int64_t c = warp_uniform((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5); c < NC; c += warps) {
     const int4 dsc = a.ck.desc[c];
     const int32_t u = dsc.x, beg = dsc.y, cnt = dsc.z & 0xffff;
@@ -420,13 +436,18 @@ __global__ void __launch_bounds__(256, KG_GATHER_BPS) k_csc_backward(CscArgs a) 
       continue;
     }
     // metadata: destination position (-1 if not a target) and coefficients
+    // messages to non-targets and the slots past cnt gather the chunk's first
+    // target row with weight zero (no per-message predicate); a chunk without
+    // targets gathers nothing
     EdgeMeta<NB> m;
     float nrm[2];
+    bool live[2];
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
       const int e = (int)lane + 32 * h;
-      m.other[h] = -1;
+      m.off[h] = MODE == 0 ? ~0u : 0u;   // fused pass: ~0 marks a message to skip
       nrm[h] = 0.f;
+      live[h] = false;
 #pragma unroll
       for (int b = 0; b < NB; ++b) m.cf[h][b] = 0.f;
       if (e < cnt) {
@@ -434,13 +455,28 @@ __global__ void __launch_bounds__(256, KG_GATHER_BPS) k_csc_backward(CscArgs a) 
         const float nw = a.c_norm[beg + e];
         const int32_t pw = a.c_pos ? a.c_pos[beg + e] : a.pos[a.c_dst[beg + e]];
         if (pw >= 0 && pw < T) {
-          m.other[h] = pw;
+          m.off[h] = (uint32_t)pw * (uint32_t)d;
           nrm[h] = nw;
+          live[h] = true;
           if (MODE != 2)
 #pragma unroll
             for (int b = 0; b < NB; ++b)
               if (b < B) m.cf[h][b] = nw * coef[r * B + b];
         }
+      }
+    }
+    int ngather = cnt;
+    if (MODE != 0) {   // (the fused pass keeps predicated loads: no registers to spare)
+      const unsigned v0 = __ballot_sync(0xffffffffu, live[0]), v1 = __ballot_sync(0xffffffffu, live[1]);
+      if ((v0 | v1) == 0) {
+        ngather = 0;
+        if (MODE != 1)
+          for (int x = (int)lane; x < cnt * B; x += 32) a.ed[(int64_t)beg * B + x] = 0.f;
+      } else {
+        const uint32_t o0 = __shfl_sync(0xffffffffu, v0 ? m.off[0] : m.off[1], v0 ? __ffs(v0) - 1 : __ffs(v1) - 1);
+#pragma unroll
+        for (int h = 0; h < 2; ++h)
+          if (!live[h]) m.off[h] = o0;
       }
     }
     float y[NB][S][VEC];
@@ -456,19 +492,25 @@ __global__ void __launch_bounds__(256, KG_GATHER_BPS) k_csc_backward(CscArgs a) 
             if (slot_ok[s]) VecIO<VEC>::load(a.Y + ((int64_t)q * B + b) * d + (s * LPR + cl) * VEC, y[b][s]);
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
-      const int nh = min(32, cnt - 32 * h);
+      const int nh = min(32, ngather - 32 * h);
       for (int j = 0; j < nh; j += UNR * EPI) {
         float zs[UNR][S][VEC];
 #pragma unroll
         for (int k = 0; k < UNR; ++k) {
-          const int32_t pw = __shfl_sync(0xffffffffu, m.other[h], (j + k * EPI + grp) & 31);
+          const uint32_t off = __shfl_sync(0xffffffffu, m.off[h], (j + k * EPI + grp) & 31);
+          if (MODE != 0) {
 #pragma unroll
-          for (int s = 0; s < S; ++s) {
-            if (j + k * EPI + grp < nh && pw >= 0 && slot_ok[s])
-              VecIO<VEC>::load(a.dZ + (int64_t)pw * d + (s * LPR + cl) * VEC, zs[k][s]);
-            else
+            for (int s = 0; s < S; ++s) VecIO<VEC>::load(zb[s] + off, zs[k][s]);
+          } else {
+            const bool ld = j + k * EPI + grp < nh && off != ~0u;
 #pragma unroll
-              for (int cc = 0; cc < VEC; ++cc) zs[k][s][cc] = 0.f;
+            for (int s = 0; s < S; ++s) {
+              if (ld && slot_ok[s])
+                VecIO<VEC>::load(a.dZ + off + (s * LPR + cl) * VEC, zs[k][s]);
+              else
+#pragma unroll
+                for (int cc = 0; cc < VEC; ++cc) zs[k][s][cc] = 0.f;
+            }
           }
         }
         // dS_b += c_eb * dZ[dst]
@@ -922,6 +964,8 @@ static kg_status dispatch_width(int d, F4 f4, F1a f1, F1b f2, F1c f4s, F1d f8) {
 
 static kg_status run_aggregate(const AggArgs& a, const kg_graph_csr* G, cudaStream_t st) {
   KG_REQUIRE(G->chunk <= MAXC, KG_ERR_VALIDATION, "chunk size %d > %d", G->chunk, MAXC);
+  KG_REQUIRE((int64_t)G->n * a.d < (1LL << 32), KG_ERR_SHAPE, "feature table of %lld x %d exceeds 32-bit offsets",
+             (long long)G->n, a.d);
   int blocks = persistent_blocks(cap_chunks(G) * 32, 256, KG_GATHER_BPS);
   int cblocks = persistent_blocks(cap_split_rows(G) * CB_THREADS, CB_THREADS, 8);   // one block per split row
   size_t smem = (size_t)a.G * a.B * sizeof(float);
@@ -939,6 +983,8 @@ static kg_status run_aggregate(const AggArgs& a, const kg_graph_csr* G, cudaStre
 
 static kg_status run_csc(const CscArgs& a, const kg_graph_csr* G, cudaStream_t st, int mode = 0) {
   KG_REQUIRE(G->chunk <= MAXC, KG_ERR_VALIDATION, "chunk size %d > %d", G->chunk, MAXC);
+  KG_REQUIRE((int64_t)G->n * a.d < (1LL << 32), KG_ERR_SHAPE, "feature table of %lld x %d exceeds 32-bit offsets",
+             (long long)G->n, a.d);
   int blocks = persistent_blocks(cap_chunks(G) * 32, 256, KG_GATHER_BPS);
   int cblocks = persistent_blocks(cap_split_rows(G) * CB_THREADS, CB_THREADS, 8);   // one block per split row
   size_t smem = (size_t)a.G * a.B * sizeof(float);

@@ -252,6 +252,104 @@ struct PackedArgs {
 
 __device__ __forceinline__ uint32_t stage_bytes(int np) { return (uint32_t)((UM + np) * UKC * 2 * 4); }
 
+// NN epilogue staging: per epilogue warp a 32-row x 32-column slab (row
+// stride EP_LD floats: conflict-free float4 writes by row and reads by column)
+constexpr int EP_LD = 36;
+constexpr size_t EP_SLAB_BYTES = (size_t)4 * 32 * EP_LD * sizeof(float);
+
+// NN epilogue of one warp's 32 accumulator rows, 32 columns at a time: the
+// TMEM rows (one per lane) go through a shared-memory slab so that global
+// stores are row-contiguous (8 lanes x float4 per row segment) instead of one
+// row per lane (a warp store touching 32 rows), and the packed copy of the
+// output is written as whole 512-byte swizzle atoms (one coalesced float4 per
+// lane). ReLU, then the per-element scale (dropout), as before.
+__device__ __forceinline__ void nn_epilogue(const PackedArgs& g, uint32_t taddr, int64_t tile, int lanegrp, int lane,
+                                            int64_t M, int np, bool vec, float* slab) {
+  const int64_t m0 = tile * UM + lanegrp * 32;   // first output row (MMA row) of this warp
+  const int64_t ml = m0 + lane;
+  const int64_t crow_l = ml < M ? (g.c_rows ? (int64_t)__ldg(g.c_rows + ml) : ml) : -1;
+  const bool mul_vec = g.mul && (g.N & 3) == 0 && ((uintptr_t)g.mul & 15) == 0;
+  const int64_t pnk = g.c_nk < 0 ? -g.c_nk : g.c_nk;
+  for (int c0 = 0; c0 < np; c0 += 32) {
+    float v[32];
+    tmem_ld16(taddr + (uint32_t)c0, v);
+    tmem_ld16(taddr + (uint32_t)c0 + 16u, v + 16);
+    if (g.relu) {
+#pragma unroll
+      for (int i = 0; i < 32; ++i) v[i] = fmaxf(v[i], 0.f);
+    }
+#pragma unroll
+    for (int q = 0; q < 8; ++q)
+      *reinterpret_cast<float4*>(slab + lane * EP_LD + 4 * q) = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
+    __syncwarp();
+    // row segments: lane -> (row it * 4 + lane / 8, column quad lane % 8)
+    const int q = lane & 7;
+    const int col = c0 + 4 * q;
+#pragma unroll 2
+    for (int it = 0; it < 8; ++it) {
+      const int rr = it * 4 + (lane >> 3);
+      const int64_t crow = __shfl_sync(0xffffffffu, crow_l, rr);
+      float4* sp = reinterpret_cast<float4*>(slab + rr * EP_LD + 4 * q);
+      float4 x = *sp;
+      if (crow >= 0 && col < g.N) {
+        const int64_t m = m0 + rr;
+        if (g.mul) {
+          if (mul_vec) {
+            const float4 s = __ldg(reinterpret_cast<const float4*>(g.mul + m * g.N + col));
+            x.x *= s.x; x.y *= s.y; x.z *= s.z; x.w *= s.w;
+          } else {
+            float* xv = reinterpret_cast<float*>(&x);
+#pragma unroll
+            for (int i = 0; i < 4; ++i)
+              if (col + i < g.N) xv[i] *= __ldg(g.mul + m * g.N + col + i);
+          }
+          if (g.c_packed) *sp = x;
+        }
+        float* dst = g.C + crow * g.ldc + col;
+        if (vec && col + 3 < g.N) {
+          *reinterpret_cast<float4*>(dst) = x;
+        } else {
+          const float* xv = reinterpret_cast<const float*>(&x);
+#pragma unroll
+          for (int i = 0; i < 4; ++i)
+            if (col + i < g.N) dst[i] = xv[i];
+        }
+      }
+    }
+    if (g.c_packed) {
+      __syncwarp();
+      // records kc = c0/16 + j: this warp's rows are 4 swizzle atoms of 8 rows;
+      // lane i writes 16-byte chunk i of an atom = row i/4, K quad (i%4) ^ ((i/8)%4)
+      const int ri = lane >> 2, kq = (lane & 3) ^ ((lane >> 3) & 3);
+#pragma unroll
+      for (int j = 0; j < 2; ++j) {
+        const int64_t kc = c0 / 16 + j;
+        if (kc >= pnk) break;
+        float* rec = g.c_packed + (tile * pnk + kc) * (g.c_nk < 0 ? 2 * PK_REC : PK_REC);
+#pragma unroll
+        for (int at = 0; at < 4; ++at) {
+          const int rl = at * 8 + ri;
+          float4 x = *reinterpret_cast<const float4*>(slab + rl * EP_LD + j * 16 + kq * 4);
+          if (m0 + rl >= M) x = make_float4(0.f, 0.f, 0.f, 0.f);
+          float* dst = rec + (lanegrp * 4 + at) * 128 + lane * 4;
+          if (g.c_nk < 0) {
+            float4 hi, lo;
+            split_tf32(x.x, hi.x, lo.x);
+            split_tf32(x.y, hi.y, lo.y);
+            split_tf32(x.z, hi.z, lo.z);
+            split_tf32(x.w, hi.w, lo.w);
+            *reinterpret_cast<float4*>(dst) = hi;
+            *reinterpret_cast<float4*>(dst + PK_REC) = lo;
+          } else {
+            *reinterpret_cast<float4*>(dst) = x;
+          }
+        }
+      }
+    }
+    __syncwarp();
+  }
+}
+
 __global__ void __launch_bounds__(UTHREADS, 1) k_umma_packed(PackedArgs g, int nstages, uint32_t acc_cols) {
   extern __shared__ __align__(1024) uint8_t smem[];
   __shared__ __align__(8) uint64_t bar_full[UMAXS], bar_empty[UMAXS], bar_split[UMAXS], bar_tfull[2], bar_tempty[2];
@@ -403,11 +501,20 @@ __global__ void __launch_bounds__(UTHREADS, 1) k_umma_packed(PackedArgs g, int n
     const int lanegrp = warp & 3;
     const int r = lanegrp * 32 + lane;
     const bool vec = ((uintptr_t)g.C & 15) == 0 && (g.ldc & 3) == 0;
+    float* slab = reinterpret_cast<float*>(smem + (size_t)nstages * sb) + lanegrp * 32 * EP_LD;
     int64_t tcount = 0;
     for (int64_t tile = tile0; tile < ntiles; tile += tstep, ++tcount) {
       const int acc = (int)(tcount & 1);
       mbar_wait(smem_u32(&bar_tfull[acc]), (uint32_t)((tcount / 2) & 1));
       tc_fence_after();
+      if (!g.tn) {
+        nn_epilogue(g, tmem + (uint32_t)acc * acc_cols + ((uint32_t)(lanegrp * 32) << 16), tile, lanegrp, lane, M, np,
+                    vec, slab);
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(smem_u32(&bar_tempty[acc]));
+        continue;
+      }
       float* crow = nullptr;
       if (!g.tn) {
         const int64_t m = tile * UM + r;
@@ -484,11 +591,12 @@ static kg_status launch_pack(const PackJob& a, const PackJob& b, int64_t items_m
 static kg_status launch_packed(const PackedArgs& p, dim3 grid, cudaStream_t st) {
   static bool attr_set = false;
   if (!attr_set) {
-    KG_CUDA(cudaFuncSetAttribute(k_umma_packed, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)USMEM_CAP));
+    KG_CUDA(cudaFuncSetAttribute(k_umma_packed, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)(USMEM_CAP + EP_SLAB_BYTES)));
     attr_set = true;
   }
   const int ns = stages_for(p.np);
-  const size_t smem = (size_t)ns * (UM + p.np) * UKC * 8;
+  const size_t smem = (size_t)ns * (UM + p.np) * UKC * 8 + (p.tn ? 0 : EP_SLAB_BYTES);
   KG_LAUNCH(p.tn ? "k_umma_gemm_tn" : "k_umma_gemm_nn", k_umma_packed, grid, UTHREADS, smem, st, p, ns,
             acc_cols_for(p.np));
   return KG_OK;
