@@ -41,6 +41,7 @@ FB = dict(num_entities=14541, num_relations=237, avg_degree=272115 / 14541, seed
 DIMS = [100, 100, 100]
 BASES = 2
 BATCH = 65536
+E2E_CALLS = 3     # timed train() calls of the e2e leg (median reported)
 
 
 def parse_args():
@@ -379,17 +380,24 @@ def run_ours(args, world, rank, local):
         kb.train(pset, graph, mc, kb.TrainConfig(epochs=math.ceil(64 / rounds), batch_size=args.batch,
                                                  optimizer="adam", learning_rate=0.01, seed=0))
         tc2 = kb.TrainConfig(epochs=epochs, batch_size=args.batch, optimizer="adam", learning_rate=0.01, seed=0)
-        if is_dist:
-            torch.distributed.barrier()
-        torch.cuda.synchronize()
-        t0 = time.perf_counter()
-        params, report = kb.train(pset, graph, mc, tc2)
-        torch.cuda.synchronize()
-        wall = time.perf_counter() - t0
-        wt = torch.tensor([wall], dtype=torch.float64, device=dev)
-        if is_dist:
-            torch.distributed.all_reduce(wt, op=torch.distributed.ReduceOp.MAX)
-        wall = float(wt.item())
+        # median of E2E_CALLS complete train() calls: the host-bound setup of a
+        # call occasionally stalls 50-300 ms in driver calls (allocation, memory
+        # queries) on these boxes; every call's wall time is reported
+        walls, phases = [], []
+        for _ in range(E2E_CALLS):
+            if is_dist:
+                torch.distributed.barrier()
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            params, report = kb.train(pset, graph, mc, tc2)
+            torch.cuda.synchronize()
+            wt = torch.tensor([time.perf_counter() - t0], dtype=torch.float64, device=dev)
+            if is_dist:
+                torch.distributed.all_reduce(wt, op=torch.distributed.ReduceOp.MAX)
+            walls.append(float(wt.item()))
+            phases.append((round(report.setup_seconds * 1e3, 1), round(sum(report.epoch_seconds) * 1e3, 1),
+                           round(report.epoch_seconds[0] * 1e3, 1), round(report.finish_seconds * 1e3, 1)))
+        wall = sorted(walls)[len(walls) // 2]
         steps_e2e = epochs * rounds
         own = [pset.partitions[wid] for wid in local_wids]
         h2d = sum(12 * (p.num_core_edges + len(p.support)) for p in own)            # partition triples (int32)
@@ -397,7 +405,9 @@ def run_ours(args, world, rank, local):
         d2h = 8 * steps_e2e + 4 * D + 4 * mc.dims[0] * graph.num_entities        # losses + params
         e2e = {"value": steps_e2e * triples_per_step / wall, "unit": UNIT,
                "h2d_bytes_per_step": int(h2d * world / steps_e2e), "d2h_bytes_per_step": int(d2h * world / steps_e2e),
-               "wall_s": wall, "steps": steps_e2e, "api": "paper_2201_02791_b200.train()",
+               "wall_s": wall, "wall_s_calls": [round(x, 4) for x in walls], "statistic": f"median of {E2E_CALLS} calls",
+               "phases_ms_calls": phases,   # (setup, epochs, first epoch, finish) per call
+               "steps": steps_e2e, "api": "paper_2201_02791_b200.train()",
                "final_loss": report.loss_curve[-1], "setup_s": report.setup_seconds,
                "epochs_s": float(sum(report.epoch_seconds)), "finish_s": report.finish_seconds,
                "epoch_ms": [round(x * 1e3, 2) for x in report.epoch_seconds]}

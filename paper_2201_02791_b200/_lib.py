@@ -206,14 +206,74 @@ def check(status: int, what: str = "") -> None:
         raise cls(f"{what}: {last_error()}" if what else last_error())
 
 
+SLOW_CALLS = os.environ.get("KG_SLOW_CALLS", "0") == "1"   # diagnostics: library calls > 5 ms of host time
+slow_calls: list = []
+
+
 def call(name: str, *args):
     """Invoke a kg_status-returning entry point and raise on failure."""
     fn = getattr(require_cuda(), name)
+    if SLOW_CALLS:
+        import time
+        t0 = time.perf_counter()
+        st = fn(*args)
+        dt = (time.perf_counter() - t0) * 1e3
+        if dt > 5:
+            slow_calls.append((name, round(dt, 1)))
+        check(st, name)
+        return
     check(fn(*args), name)
 
 
 def ptr(t) -> int:
     return 0 if t is None else t.data_ptr()
+
+
+_persistent_pools: dict = {}
+
+
+def persistent_pool(key):
+    """A CUDA-graph memory pool that outlives the graphs captured into it: a
+    one-node anchor graph keeps it referenced, so when a trainer's graphs are
+    destroyed their memory returns to this pool and the next trainer's
+    captures reuse it (no new device segments per train() call, no growth).
+    Only for graphs that never run concurrently with each other (one pool per
+    device for the round graphs, one per device and worker for the sampler's
+    epoch graphs, all on one stream) and whose owner synchronises before
+    destroying them (Trainer.close())."""
+    torch = _torch_mod()
+    hit = _persistent_pools.get(key)
+    if hit is None:
+        handle = torch.cuda.graph_pool_handle()
+        anchor = torch.cuda.CUDAGraph()
+        side = torch.cuda.Stream()
+        side.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(side):
+            anchor.capture_begin(pool=handle)
+            torch.zeros(1, device="cuda")
+            anchor.capture_end()
+        torch.cuda.current_stream().wait_stream(side)
+        hit = _persistent_pools[key] = (handle, anchor)
+    return hit[0]
+
+
+_cached_streams: dict = {}
+
+
+def cached_stream(key, device, priority: int = 0):
+    """A process-wide CUDA stream per key (stream creation is a driver call;
+    successive trainers reuse theirs, and work of an earlier trainer on the
+    same key stays ordered before the new one's)."""
+    torch = _torch_mod()
+    st = _cached_streams.get(key)
+    if st is None:
+        st = _cached_streams[key] = torch.cuda.Stream(device, priority=priority)
+    return st
+
+
+def _torch_mod():
+    import torch
+    return torch
 
 
 CAPTURE_TIMES = os.environ.get("KG_CAPTURE_TIMES", "0") == "1"   # diagnostics

@@ -642,6 +642,11 @@ def build_compute_graph(batch: EdgeMiniBatch, view: PartitionView, hops: int) ->
 # Asynchronous epoch sampling (negatives + shuffle) on a side stream
 # ---------------------------------------------------------------------------
 
+def _setup_mark(name: str) -> None:
+    from .trainer import _mark   # diagnostics (KG_SETUP_TIMES=1)
+    _mark(name)
+
+
 class EpochSampler:
     """Per-partition epoch pipeline: the negatives and the shuffled stream of
     epoch e+1 are produced on a side CUDA stream while epoch e trains. The
@@ -654,14 +659,15 @@ class EpochSampler:
     ASYNC_ROUNDS = 3
     NSLOTS = 3   # epochs e+1 and e+2 are sampled (and round-prepped) while e trains
 
-    def __init__(self, view: PartitionView, s: int, g_dev, prep=None):
+    def __init__(self, view: PartitionView, s: int, g_dev, prep=None, pool=None, side=None):
         """prep(slot, DeviceStream), optional: enqueues per-round
         precomputation for an epoch's stream; it becomes part of the slot's
         captured epoch graph, right after the sampling."""
         torch = _torch()
         self.view, self.s, self.g = view, s, g_dev
+        self.pool = pool   # graph memory pool of the epoch graphs (None: one private pool per capture)
         self.dev = view.device
-        self.side = torch.cuda.Stream(self.dev)
+        self.side = side if side is not None else torch.cuda.Stream(self.dev)
         self.ws = _lib.Workspace(self.dev)
         core = view.num_core
         total = core * (s + 1)
@@ -688,6 +694,9 @@ class EpochSampler:
         # latest, when next() needs them. Slots always start in epoch order
         # (the device RNG stream is consumed in that order).
         self.filled = [False] * self.NSLOTS
+        _setup_mark("sampler_alloc")
+        self._capture(0)
+        _setup_mark("sampler_capture")
         self._fill(0)
 
     def slot_of(self, ds) -> int:
@@ -722,7 +731,7 @@ class EpochSampler:
         g = torch.cuda.CUDAGraph()
         self.side.wait_stream(torch.cuda.current_stream())
         with torch.cuda.stream(self.side):
-            _lib.capture(g, lambda: self._body(parity))
+            _lib.capture(g, lambda: self._body(parity), self.pool)
         slot["graph"] = g
         slot["stream"] = self.slot_stream(parity)
 

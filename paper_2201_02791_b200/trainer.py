@@ -340,9 +340,12 @@ class _RoundPrep:
         slab = EpochSampler.NSLOTS * self.rounds * (8 * self.n + 4 * self.L1 +
                                                      lib.kg_loss_workspace_bytes(b, v.n, cfg.dims[-1],
                                                                                  cfg.num_relations))
-        free, _ = torch.cuda.mem_get_info(dev)
-        budget = int(os.environ.get("KG_PREP_SLAB_BYTES", str(int(0.5 * free))))
-        if slab > budget:
+        # (the free-memory query is a driver round trip: only for slabs that
+        # could matter against the device's memory)
+        budget = int(os.environ["KG_PREP_SLAB_BYTES"]) if "KG_PREP_SLAB_BYTES" in os.environ else None
+        if budget is None and slab > (1 << 30):
+            budget = int(0.5 * torch.cuda.mem_get_info(dev)[0])
+        if budget is not None and slab > budget:
             raise ValidationError(
                 f"epoch pre-sampling needs {slab / 2**30:.1f} GiB for {self.rounds} rounds of "
                 f"{self.n} vertices (budget {budget / 2**30:.1f} GiB, KG_PREP_SLAB_BYTES); use a larger "
@@ -423,7 +426,7 @@ class _Worker:
     embedding rows and their Adam moments."""
 
     def __init__(self, wid, partition, pset, config: ModelConfig, tc: TrainConfig, b: int, params: ModelParams,
-                 features, rounds: int = 1):
+                 features, rounds: int = 1, epoch_pool=None, epoch_stream=None):
         torch = _torch()
         self.wid = wid
         _mark("worker")
@@ -459,7 +462,8 @@ class _Worker:
         # epoch e+1's negatives + shuffle are produced on a side stream while epoch e trains
         self.prep = _RoundPrep(self, rounds)
         _mark("roundprep")
-        self.sampler = EpochSampler(self.view, config.negatives_per_positive, self.g_dev, prep=self.prep.run)
+        self.sampler = EpochSampler(self.view, config.negatives_per_positive, self.g_dev, prep=self.prep.run,
+                                    pool=epoch_pool, side=epoch_stream)
         _mark("sampler")
 
     def begin_epoch(self):
@@ -479,7 +483,10 @@ class Trainer:
     owns. `run_round()` is one synchronized training round."""
 
     def __init__(self, pset: PartitionSet, graph, model_config: ModelConfig, train_config: TrainConfig,
-                 initial_params: Optional[ModelParams] = None):
+                 initial_params: Optional[ModelParams] = None, graph_pools: bool = False):
+        """graph_pools: capture into the process-wide persistent graph memory
+        pools (train() does; the caller must close() the trainer, which
+        synchronises, before another trainer on the device captures)."""
         torch = _torch()
         _lib.require_cuda()
         if pset.hops != model_config.num_layers:
@@ -517,8 +524,13 @@ class Trainer:
         _mark("model")
         D = self.model.layout.total
         self.D = D
+        self.graph_pools = graph_pools
+        di = self.dev.index
         self.workers = [_Worker(w, pset.partitions[w], pset, model_config, train_config, self.sizes[w], params,
-                                features, self.rounds) for w in self.local_wids]
+                                features, self.rounds,
+                                epoch_pool=_lib.persistent_pool(("epoch", di, k)) if graph_pools else None,
+                                epoch_stream=_lib.cached_stream(("epoch", di, k), self.dev) if graph_pools else None)
+                        for k, w in enumerate(self.local_wids)]
         nloc = len(self.workers)
         self.grads_local = torch.zeros((nloc, D), dtype=torch.float32, device=self.dev)
         self.grads_all = (torch.zeros((self.P, D), dtype=torch.float32, device=self.dev) if self.dist
@@ -554,8 +566,12 @@ class Trainer:
         self._graph_pool = None
         # Training runs on high-priority streams: the sampler's epoch graphs
         # (default, low priority) then fill SM slots training leaves idle.
-        self._prio = torch.cuda.Stream(self.dev, priority=-2)
-        self._loss_stream = torch.cuda.Stream(self.dev, priority=-2)   # forked work beside the layers
+        def stream(name):
+            return (_lib.cached_stream((name, self.dev.index), self.dev, priority=-2) if graph_pools
+                    else torch.cuda.Stream(self.dev, priority=-2))
+        self._prio = stream("prio")
+        self._loss_stream = stream("loss")   # forked work beside the layers
+        self._capture_stream = stream("capture")
         # diagnostics: KG_FORK_STREAMS=0 keeps every kernel on one stream
         self.fork_streams = os.environ.get("KG_FORK_STREAMS", "1") != "0"
         self.model.repack()
@@ -717,7 +733,7 @@ class Trainer:
 
     def _capture(self, body, graph):
         torch = _torch()
-        side = torch.cuda.Stream(self.dev, priority=-2)
+        side = self._capture_stream
         side.wait_stream(torch.cuda.current_stream())
         with torch.cuda.stream(side):
             _lib.capture(graph, body, self._graph_pool)
@@ -729,7 +745,8 @@ class Trainer:
         torch = _torch()
         lib = _lib.require_cuda()
         if self._graph_pool is None:
-            self._graph_pool = torch.cuda.graph_pool_handle()
+            self._graph_pool = (_lib.persistent_pool(("round", self.dev.index)) if self.graph_pools
+                                else torch.cuda.graph_pool_handle())
         current = [w.stream for w in self.workers]
         for w in self.workers:
             w.stream = w.sampler.slot_stream(slot)
@@ -776,6 +793,9 @@ class Trainer:
         sampler <-> round-prep reference cycle, so the device buffers go back
         to the caching allocator as soon as the trainer is dropped (instead of
         whenever the cyclic GC runs; a following train() then reuses them)."""
+        if getattr(self, "_closed", False):
+            return
+        self._closed = True
         _torch().cuda.synchronize()
         self._graphs.clear()
         if self._peer is not None:
@@ -809,20 +829,27 @@ class Trainer:
         out = {}
         base = self.init_params.entity_embed
         for w in self.workers:
-            t = base.copy()
-            t[w.view.local_ids] = w.input_rows.double().cpu().numpy()
+            lids = w.view.local_ids
+            rows = w.input_rows.cpu().numpy()          # fp32 off the device, widened on the host
+            if len(lids) == len(base) and lids[0] == 0 and lids[-1] == len(base) - 1 and \
+                    bool((np.diff(lids) == 1).all()):
+                t = rows.astype(np.float64)            # the partition holds every row, in id order
+            else:
+                t = base.copy()
+                t[lids] = rows
             out[w.wid] = t
         return out
 
     def snapshot(self) -> ModelParams:
-        torch = _torch()
-        params = self.init_params.copy()
-        params.set_dense_blocks(self.model.dense_blocks())
+        p0 = self.init_params
         if self.mc.mode == MODE_EMBEDDING:
-            if self.P == 1:
-                params.entity_embed = self.local_tables()[0]
-            else:
-                params.entity_embed = self._gather_owned_rows()
+            emb = self.local_tables()[0] if self.P == 1 else self._gather_owned_rows()
+        else:
+            emb = None if p0.entity_embed is None else p0.entity_embed.copy()
+        # dense blocks come fresh from the device; the table is built once (no
+        # copy of the initial table that is then overwritten)
+        params = ModelParams(list(p0.bases), list(p0.coeffs), p0.decoder, emb)
+        params.set_dense_blocks(self.model.dense_blocks())
         return params
 
     def _gather_owned_rows(self) -> np.ndarray:
@@ -992,7 +1019,15 @@ def train(pset: PartitionSet, graph, model_config: ModelConfig, train_config: Tr
     selected by train_config.eval_every."""
     torch = _torch()
     t_setup = time.perf_counter()
-    tr = Trainer(pset, graph, model_config, train_config, initial_params)
+    tr = Trainer(pset, graph, model_config, train_config, initial_params, graph_pools=True)
+    try:
+        return _train_loop(tr, train_config, eval_fn, t_setup)
+    finally:
+        tr.close()   # synchronises before the graphs (and their pool memory) are released
+
+
+def _train_loop(tr, train_config, eval_fn, t_setup) -> tuple:
+    torch = _torch()
     torch.cuda.synchronize()
     report = TrainReport(rounds_per_epoch=tr.rounds, batch_sizes=list(tr.sizes),
                          setup_seconds=time.perf_counter() - t_setup)

@@ -29,7 +29,25 @@ def main():
     ap.add_argument("--rounds", type=int, default=180)
     ap.add_argument("--profile", action="store_true")
     ap.add_argument("--gc", action="store_true", help="gc.collect() before every call")
+    ap.add_argument("--nogc", action="store_true", help="cyclic GC disabled during each call")
+    ap.add_argument("--sample", action="store_true", help="sample the main thread's stack during setup spikes")
+    ap.add_argument("--pause", type=float, default=0.0, help="seconds of idle host time between calls")
     a = ap.parse_args()
+    samples = []
+    if a.sample:
+        import threading
+        import traceback
+        main_id = threading.main_thread().ident
+
+        def sampler():
+            while True:
+                fr = sys._current_frames().get(main_id)
+                if fr is not None:
+                    st = traceback.extract_stack(fr)[-8:]
+                    samples.append((time.perf_counter(), tuple(f"{os.path.basename(x.filename)}:{x.lineno}:{x.name}"
+                                                               for x in st)))
+                time.sleep(0.002)
+        threading.Thread(target=sampler, daemon=True).start()
     world, rank, local = bench.dist_setup()      # torchrun: one partition per rank
     graph, split, pset, mc, tc = bench.build_inputs(world, bench.BATCH)
     tr = kb.Trainer(pset, graph, mc, tc)
@@ -42,14 +60,26 @@ def main():
             import gc
             gc.collect()
         torch.cuda.synchronize()
+        if a.pause:
+            time.sleep(a.pause)
+        ms0 = torch.cuda.memory_stats()
         t0 = time.perf_counter()
         if prof:
             prof.enable()
+        if a.nogc:
+            import gc
+            gc.disable()
         _, rep = kb.train(pset, graph, mc, tc2)
+        if a.nogc:
+            gc.enable()
         torch.cuda.synchronize()
         if prof:
             prof.disable()
         wall = time.perf_counter() - t0
+        ms1 = torch.cuda.memory_stats()
+        seg = {k: ms1.get(k, 0) - ms0.get(k, 0) for k in ("segment.all.allocated", "segment.all.freed",
+                                                          "allocated_bytes.all.allocated", "num_alloc_retries",
+                                                          "num_device_alloc", "num_device_free")}
         ep = rep.epoch_seconds
         if rank != 0:
             continue
@@ -57,6 +87,19 @@ def main():
               f"(first {ep[0]*1e3:.2f}, median {sorted(ep)[len(ep)//2]*1e3:.2f}, max {max(ep)*1e3:.2f}) "
               f"finish {rep.finish_seconds*1e3:.1f} -> {epochs*tr_rounds(rep)*bench.BATCH/wall/1e6:.1f} M/s",
               flush=True)
+        print(f"   cudaMalloc/cudaFree this call: {seg}; allocated {torch.cuda.memory_allocated() / 2**20:.1f} MiB, "
+              f"reserved {torch.cuda.memory_reserved() / 2**20:.1f} MiB after the call", flush=True)
+        if a.sample:
+            if rep.setup_seconds > 0.06:
+                import collections
+                win = [st for t, st in samples if t0 <= t <= t0 + rep.setup_seconds]
+                for st, c in collections.Counter(win).most_common(4):
+                    print(f"   [{c} samples] " + " <- ".join(reversed(st)), flush=True)
+            samples.clear()
+        from paper_2201_02791_b200 import _lib as libm2
+        if libm2.slow_calls:
+            print("   slow library calls:", libm2.slow_calls, flush=True)
+            libm2.slow_calls.clear()
         from paper_2201_02791_b200 import _lib as libm
         if libm.capture_times:
             print("   captures (begin, body, end, upload ms):", libm.capture_times, flush=True)

@@ -41,7 +41,7 @@ for P in Ps:
         torch.cuda.synchronize()
 
     bd, _ = _lib.kernel_breakdown(eager)
-    top = sorted(bd.items(), key=lambda x: -x[1][1])[:8]
+    top = sorted(bd.items(), key=lambda x: -x[1][1])[:None if os.environ.get("EGT_ALL") else 8]
     print(f"P={P}: rounds/epoch {tr.rounds}, stream {smp.total}, epoch graph {ms:.3f} ms | " +
-          ", ".join(f"{k} {v[1]:.3f}" for k, v in top))
+          ", ".join(f"{k} {v[1]:.3f}" + (f" (x{v[0]})" if os.environ.get("EGT_ALL") else "") for k, v in top))
     del tr
