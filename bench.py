@@ -294,6 +294,12 @@ def run_ours(args, world, rank, local):
     kt = {k: [0.0, 0] for k in names}
     span = [0.0, 0]   # makespan of the two concurrent CSC passes per layer
     with ClockSampler(local) as clk:
+        if tr.dist:
+            # device-side alignment: the ranks' streams wait here for the
+            # slowest host, so step 0 does not absorb the host skew after the
+            # barrier in its first collective (the host enqueues on behind it)
+            align = torch.zeros(1, device=dev)
+            torch.distributed.all_reduce(align)
         # the K timed steps: no host synchronisation inside the loop (the host
         # runs ahead, as in a training loop), events on the launch stream
         for k in range(args.steps):
