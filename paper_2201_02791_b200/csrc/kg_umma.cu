@@ -248,6 +248,7 @@ struct PackedArgs {
   const float* mul;       // NN: optional per-element output scale by MMA row (ld N)
   int a_split;            // A records already hold hi | lo halves (records_split of the row capacity)
   int b_split;            // B records already hold hi | lo halves (NN: weights, split once per step)
+  int exp;                // diagnostics (KG_GEMM_EXP, NN): 1 no epilogue stores, 2 no MMAs
 };
 
 __device__ __forceinline__ uint32_t stage_bytes(int np) { return (uint32_t)((UM + np) * UKC * 2 * 4); }
@@ -451,6 +452,7 @@ __global__ void __launch_bounds__(UTHREADS, 1) k_umma_packed(PackedArgs g, int n
           const uint32_t b_hi = a_hi + a_bytes, b_lo = b_hi + b_half;
 #pragma unroll
           for (int j = 0; j < UKC / 8; ++j) {
+            if (g.exp & 2) break;
             const uint32_t ko = (uint32_t)j * 32u;
             const uint64_t dah = make_desc(a_hi + ko), dal = make_desc(a_lo + ko);
             const uint64_t dbh = make_desc(b_hi + ko), dbl = make_desc(b_lo + ko);
@@ -508,7 +510,8 @@ __global__ void __launch_bounds__(UTHREADS, 1) k_umma_packed(PackedArgs g, int n
       mbar_wait(smem_u32(&bar_tfull[acc]), (uint32_t)((tcount / 2) & 1));
       tc_fence_after();
       if (!g.tn) {
-        nn_epilogue(g, tmem + (uint32_t)acc * acc_cols + ((uint32_t)(lanegrp * 32) << 16), tile, lanegrp, lane, M, np,
+        if (!(g.exp & 1))
+          nn_epilogue(g, tmem + (uint32_t)acc * acc_cols + ((uint32_t)(lanegrp * 32) << 16), tile, lanegrp, lane, M, np,
                     vec, slab);
         tc_fence_before();
         __syncwarp();
@@ -644,6 +647,8 @@ kg_status umma_gemm_nn(const GemmArgs& g, void* ws, cudaStream_t st) {
   p.M = g.M; p.M_dev = g.M_dev; p.M_dev_index = g.M_dev_index; p.nk = nk;
   p.C = g.C; p.ldc = g.ldc; p.c_rows = g.c_rows; p.N = g.N; p.out_rows = 0; p.relu = g.relu;
   p.c_packed = g.c_packed; p.c_nk = packed_nk(g.M_max, g.N); p.mul = g.mul;
+  static const int gemm_exp = getenv("KG_GEMM_EXP") ? atoi(getenv("KG_GEMM_EXP")) : 0;
+  p.exp = gemm_exp;
   const int ctas = (int)(tiles < num_sms() ? tiles : num_sms());
   return launch_packed(p, dim3((unsigned)ctas, 1, 1), st);
 }

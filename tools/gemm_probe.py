@@ -1,6 +1,6 @@
 """Standalone timing of the NN GEMM at the FB15k-shape layer sizes through
 kg_gemm_f32 (pack + tcgen05 GEMM); run under ncu for per-kernel durations,
-KG_GEMM_EXP=1/2 to drop the epilogue stores / the MMAs (diagnostics)."""
+KG_GEMM_EXP=1/2/3 drops the epilogue stores / the MMAs / both (diagnostics; tools/r3_gemm_probe.sh)."""
 import sys
 import torch
 sys.path.insert(0, __import__("os").path.dirname(__import__("os").path.dirname(__import__("os").path.abspath(__file__))))
