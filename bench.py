@@ -218,11 +218,12 @@ def live_roofline(tr, kt, step_ms, span=None):
         peaks = json.load(open(pk_path))
     peak = float(peaks.get("hbm_gbs", 6650.0))
     per = {}
+    fused = kt.get("k_csc_dots", [0.0, 0])[1] == 0   # one CSC pass per layer (dS + edge dots)
     for name, (ms, n) in kt.items():
         if n == 0:
             continue
         avg = ms / n
-        alg = algorithmic_bytes(name, tr, w0) / L
+        alg = algorithmic_bytes("csc_family" if (fused and name == "k_csc_backward") else name, tr, w0) / L
         per[name] = {"avg_launch_ms": avg, "launches_timed": n, "alg_bytes_per_launch": alg,
                      "achieved": alg / (avg / 1e3) / 1e9, "frac": alg / (avg / 1e3) / 1e9 / peak,
                      "share_of_step": avg * L / step_ms if step_ms > 0 else None}
@@ -248,7 +249,8 @@ def live_roofline(tr, kt, step_ms, span=None):
             "unit": "GB/s", "frac": achieved / peak, "traffic": traffic, "traffic_source": traffic_src,
             "alg_bytes_per_launch": alg, "avg_launch_ms": avg, "kernel_share_of_step": share,
             "alg_model": "one CSC pass per layer: S*(8*B*d+4) + E*(16+4*d+4*B) + T*(4*d+4*B) bytes; time = "
-                         "makespan of the concurrent dS and edge-dot passes of a layer",
+                         + ("the fused pass's launch" if fused else
+                            "makespan of the concurrent dS and edge-dot passes of a layer"),
             "timing": "CUDA event pairs on the launch stream around each launch, recorded inside the replayed round "
                       "graphs over 6 steps right after the timed region (the timed steps replay graphs without "
                       "the event nodes)",

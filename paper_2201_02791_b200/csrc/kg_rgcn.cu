@@ -1066,12 +1066,15 @@ static bool direct_pack(int64_t rows, int64_t K) {
 }
 
 // dZ footprint (bytes) up to which the CSC backward runs as two concurrent
-// passes (dS on the critical stream, edge dots on the side stream); the FB15k
-// working set (~6 MB) is L2-resident, the wikikg2 / citation2 ones are not.
-// KG_CSC_SPLIT_MAX_MB overrides (diagnostics).
+// passes (dS on the critical stream, edge dots on the side stream). Default 0:
+// always one fused pass. The split once won at FB shape (L2-resident dZ), but
+// the round is throughput-bound across streams (the kernels' summed in-graph
+// time is ~1.9x the round), so gathering dZ twice costs more than the
+// critical pass saves: fused 0.477 vs split 0.483 ms per round (alternating
+// A/B, gpurun_out r3zg). KG_CSC_SPLIT_MAX_MB=48 restores the split.
 static int64_t csc_split_max_bytes() {
   const char* env = getenv("KG_CSC_SPLIT_MAX_MB");
-  return (int64_t)(env ? atoll(env) : 48) << 20;
+  return (int64_t)(env ? atoll(env) : 0) << 20;
 }
 
 static Chunks csr_chunks(const kg_graph_csr* G) {
