@@ -239,7 +239,7 @@ def live_roofline(tr, kt, step_ms, span=None):
         kernel, alg, achieved, avg, share = k0, per[k0]["alg_bytes_per_launch"], per[k0]["achieved"], \
             per[k0]["avg_launch_ms"], per[k0]["share_of_step"]
     traffic, traffic_src = None, None
-    tpath = os.path.join(ROOT, "profiles", "r2_roofline_traffic.json")
+    tpath = os.path.join(ROOT, "profiles", "r3_roofline_traffic.json")
     if os.path.isfile(tpath):
         tj = json.load(open(tpath))
         if tj.get("kernel") == kernel:

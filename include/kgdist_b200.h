@@ -142,6 +142,10 @@ kg_status kg_kernel_timer_read_named(int64_t handle, const char* name, double* t
 /* Makespan of concurrent launch pairs (i-th launch of kernel a with the i-th
  * of kernel b): summed [min start, max end] spans and the pair count. */
 kg_status kg_kernel_timer_span(int64_t handle, const char* a, const char* b, double* total_ms, int64_t* pairs);
+/* Load every kernel of the library now instead of at its first launch (CUDA
+ * lazy module loading); *loaded = functions loaded (0 on drivers without the
+ * enumeration entry points). Called once per process by the host package. */
+kg_status kg_preload_kernels(int32_t* loaded);
 
 /* ---------------------------------------------------------------------- */
 /* Primitives (stable radix sort / scan) used by every stage below          */

@@ -70,6 +70,7 @@ _PROTOS = {
     "kg_kernel_timer_read": (ST, [c_int64, POINTER(c_double), POINTER(c_int64)]),
     "kg_kernel_timer_read_named": (ST, [c_int64, ctypes.c_char_p, POINTER(c_double), POINTER(c_int64)]),
     "kg_kernel_timer_span": (ST, [c_int64, ctypes.c_char_p, ctypes.c_char_p, POINTER(c_double), POINTER(c_int64)]),
+    "kg_preload_kernels": (ST, [POINTER(c_int32)]),
     "kg_copy_segments": (ST, [POINTER(KgCopySeg), c_int32, P, c_int64, P]),
     "kg_loss_group_fields": (c_int32, [P, c_int64, c_int64, c_int32, c_int32, c_int32, POINTER(c_void_p),
                                        POINTER(c_int64), c_int32]),
@@ -185,13 +186,30 @@ def load():
     return lib
 
 
+_preloaded = False
+
+
 def require_cuda():
-    """The compute path has no CPU fallback: fail loudly without a device."""
+    """The compute path has no CPU fallback: fail loudly without a device.
+    The first call per process also loads every kernel of the library
+    (kg_preload_kernels): lazy loading would otherwise land in the first
+    training epoch."""
+    global _preloaded
     import torch
     if not torch.cuda.is_available():
         raise DeviceError("paper_2201_02791_b200 needs a CUDA device (B200, sm_100a); "
                           "no CPU fallback exists")
-    return load()
+    lib = load()
+    if not _preloaded and os.environ.get("KG_PRELOAD", "1") != "0":
+        _preloaded = True
+        n = c_int32(0)
+        check(lib.kg_preload_kernels(ctypes.byref(n)), "kg_preload_kernels")
+        global preloaded_kernels
+        preloaded_kernels = n.value
+    return lib
+
+
+preloaded_kernels = 0
 
 
 def last_error() -> str:

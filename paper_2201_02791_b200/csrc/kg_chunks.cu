@@ -93,3 +93,6 @@ kg_status build_chunk_table(const int32_t* indptr, int32_t n, int C, int32_t* pt
 }
 
 }  // namespace kg
+
+// this module's anchor for kg_preload_kernels (kg_primitives.cu)
+extern "C" const void* kg_anchor_chunks() { return reinterpret_cast<const void*>(&kg::k_chunk_counts); }

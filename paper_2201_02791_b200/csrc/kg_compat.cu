@@ -220,3 +220,6 @@ kg_status kg_sparse_step_f64(const double* old_rows, const double* grad_rows, co
 }
 
 }  // extern "C"
+
+// this module's anchor for kg_preload_kernels (kg_primitives.cu)
+extern "C" const void* kg_anchor_compat() { return reinterpret_cast<const void*>(&kg::k_tree_mean_f64); }

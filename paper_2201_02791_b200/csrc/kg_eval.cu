@@ -341,3 +341,6 @@ kg_status kg_eval_candidates(const float* H, int32_t d, const float* dec, const 
 }
 
 }  // extern "C"
+
+// this module's anchor for kg_preload_kernels (kg_primitives.cu)
+extern "C" const void* kg_anchor_eval() { return reinterpret_cast<const void*>(&kg::k_true_scores); }

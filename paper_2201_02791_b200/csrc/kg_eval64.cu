@@ -208,3 +208,6 @@ kg_status kg_encode_full_f64(const kg_graph_csr* g, const int32_t* src, const in
 }
 
 }  // extern "C"
+
+// this module's anchor for kg_preload_kernels (kg_primitives.cu)
+extern "C" const void* kg_anchor_eval64() { return reinterpret_cast<const void*>(&kg::k64_aggregate); }

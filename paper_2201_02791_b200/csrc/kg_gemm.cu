@@ -192,3 +192,6 @@ kg_status kg_gemm_f32(const float* A, int64_t lda, const int32_t* a_rows, const 
 }
 
 }  // extern "C"
+
+// this module's anchor for kg_preload_kernels (kg_primitives.cu)
+extern "C" const void* kg_anchor_gemm() { return reinterpret_cast<const void*>(&kg::k_reduce_splits); }

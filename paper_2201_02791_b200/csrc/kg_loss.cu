@@ -648,3 +648,6 @@ kg_status kg_epoch_prep(const kg_epoch_prep_args* a, void* stream) {
 }
 
 }  // extern "C"
+
+// this module's anchor for kg_preload_kernels (kg_primitives.cu)
+extern "C" const void* kg_anchor_loss() { return reinterpret_cast<const void*>(&kg::k_block_sums); }

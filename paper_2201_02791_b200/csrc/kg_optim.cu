@@ -212,3 +212,6 @@ kg_status kg_sparse_step(float* table, float* m, float* v, const float* grad, co
 }
 
 }  // extern "C"
+
+// this module's anchor for kg_preload_kernels (kg_primitives.cu)
+extern "C" const void* kg_anchor_optim() { return reinterpret_cast<const void*>(&kg::k_tree_mean); }

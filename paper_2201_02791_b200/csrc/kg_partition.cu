@@ -170,3 +170,6 @@ kg_status kg_halo_expand(const int32_t* tri, int64_t m, int64_t n, const uint32_
 }
 
 }  // extern "C"
+
+// this module's anchor for kg_preload_kernels (kg_primitives.cu)
+extern "C" const void* kg_anchor_partition() { return reinterpret_cast<const void*>(&kg::k_inc_count); }

@@ -193,3 +193,6 @@ kg_status kg_peer_gather(void* const* regions_dev, int32_t P, int64_t n, float* 
 }
 
 }  // extern "C"
+
+// this module's anchor for kg_preload_kernels (kg_primitives.cu)
+extern "C" const void* kg_anchor_peer() { return reinterpret_cast<const void*>(&kg::k_peer_publish); }

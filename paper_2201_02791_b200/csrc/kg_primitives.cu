@@ -746,3 +746,66 @@ kg_status kg_kernel_timer_end(double* total_ms, int64_t* launches) {
 }
 
 }  // extern "C"
+
+// this module's anchor for kg_preload_kernels (kg_primitives.cu)
+extern "C" const void* kg_anchor_primitives() { return reinterpret_cast<const void*>(&kg::scan_tile_sums); }
+
+// ---------------------------------------------------------------------------
+// Eager loading of the library's kernels. Under CUDA's lazy module loading
+// every kernel is loaded at its first launch; in a fresh process that put
+// ~80 ms of loading into the first training epoch (measured: first-epoch
+// 99 ms lazy vs 17 ms with CUDA_MODULE_LOADING=EAGER). The host side calls
+// this once per process (_lib.require_cuda): every function of every module
+// of this library is loaded up front (cuModuleEnumerateFunctions + cuFuncLoad,
+// through the driver entry points; one anchor kernel per translation unit
+// names its module). Process-wide eager loading would also load all of
+// PyTorch's kernels.
+#include <cuda.h>
+extern "C" {
+const void* kg_anchor_chunks();
+const void* kg_anchor_compat();
+const void* kg_anchor_eval();
+const void* kg_anchor_eval64();
+const void* kg_anchor_gemm();
+const void* kg_anchor_loss();
+const void* kg_anchor_model64();
+const void* kg_anchor_optim();
+const void* kg_anchor_partition();
+const void* kg_anchor_peer();
+const void* kg_anchor_primitives();
+const void* kg_anchor_rgcn();
+const void* kg_anchor_sampler();
+const void* kg_anchor_umma();
+const void* kg_anchor_view();
+
+kg_status kg_preload_kernels(int32_t* loaded) {
+  typedef CUresult (*PFuncGetModule)(CUmodule*, CUfunction);
+  typedef CUresult (*PModuleGetFunctionCount)(unsigned int*, CUmodule);
+  typedef CUresult (*PModuleEnumerateFunctions)(CUfunction*, unsigned int, CUmodule);
+  typedef CUresult (*PFuncLoad)(CUfunction);
+  void *p1 = nullptr, *p2 = nullptr, *p3 = nullptr, *p4 = nullptr;
+  cudaDriverEntryPointQueryResult q;
+  KG_CUDA(cudaGetDriverEntryPoint("cuFuncGetModule", &p1, cudaEnableDefault, &q));
+  KG_CUDA(cudaGetDriverEntryPoint("cuModuleGetFunctionCount", &p2, cudaEnableDefault, &q));
+  KG_CUDA(cudaGetDriverEntryPoint("cuModuleEnumerateFunctions", &p3, cudaEnableDefault, &q));
+  KG_CUDA(cudaGetDriverEntryPoint("cuFuncLoad", &p4, cudaEnableDefault, &q));
+  if (loaded) *loaded = 0;
+  if (!p1 || !p2 || !p3 || !p4) return KG_OK;   // older driver: stay lazy
+  const void* (*anchors[])() = {kg_anchor_chunks, kg_anchor_compat, kg_anchor_eval, kg_anchor_eval64, kg_anchor_gemm, kg_anchor_loss, kg_anchor_model64, kg_anchor_optim, kg_anchor_partition, kg_anchor_peer, kg_anchor_primitives, kg_anchor_rgcn, kg_anchor_sampler, kg_anchor_umma, kg_anchor_view};
+  int32_t n_loaded = 0;
+  for (auto a : anchors) {
+    cudaFunction_t f;
+    KG_CUDA(cudaGetFuncBySymbol(&f, a()));
+    CUmodule mod;
+    if (((PFuncGetModule)p1)(&mod, (CUfunction)f) != CUDA_SUCCESS) continue;
+    unsigned int count = 0;
+    if (((PModuleGetFunctionCount)p2)(&count, mod) != CUDA_SUCCESS || count == 0) continue;
+    std::vector<CUfunction> fs(count);
+    if (((PModuleEnumerateFunctions)p3)(fs.data(), count, mod) != CUDA_SUCCESS) continue;
+    for (CUfunction fn : fs)
+      if (((PFuncLoad)p4)(fn) == CUDA_SUCCESS) ++n_loaded;
+  }
+  if (loaded) *loaded = n_loaded;
+  return KG_OK;
+}
+}  // extern "C"

@@ -1299,3 +1299,6 @@ kg_status kg_rgcn_pack_weights(const kg_layer_params* lp, float* out, void* stre
 }
 
 }  // extern "C"
+
+// this module's anchor for kg_preload_kernels (kg_primitives.cu)
+extern "C" const void* kg_anchor_rgcn() { return reinterpret_cast<const void*>(&kg::k_csc_positions); }

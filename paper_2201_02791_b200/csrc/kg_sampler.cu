@@ -828,3 +828,6 @@ kg_status kg_closure(const int32_t* tri, int64_t total, int64_t start, const int
 }
 
 }  // extern "C"
+
+// this module's anchor for kg_preload_kernels (kg_primitives.cu)
+extern "C" const void* kg_anchor_sampler() { return reinterpret_cast<const void*>(&kg::k_gen_u32); }

@@ -1597,3 +1597,6 @@ kg_status kg_pack_rows(const float* src, int64_t ld, const int32_t* rowid, const
 }
 
 }  // extern "C"
+
+// this module's anchor for kg_preload_kernels (kg_primitives.cu)
+extern "C" const void* kg_anchor_umma() { return reinterpret_cast<const void*>(&kg::k_umma_pack); }

@@ -391,3 +391,6 @@ kg_status kg_view_build(const int32_t* edges_global, int64_t m, const int32_t* g
 }
 
 }  // extern "C"
+
+// this module's anchor for kg_preload_kernels (kg_primitives.cu)
+extern "C" const void* kg_anchor_view() { return reinterpret_cast<const void*>(&kg::k_fill_u32); }

@@ -311,9 +311,13 @@ def _assemble_embed(pset: PartitionSet, tables, base: np.ndarray) -> np.ndarray:
 # ---------------------------------------------------------------------------
 
 PREP_BRANCHES = int(os.environ.get("KG_PREP_BRANCHES", "4"))   # <= KG_PREP_MAX_BRANCHES
-# eager rounds before the round graphs are captured (lazy workspaces and
-# one-time kernel attributes are set up by them)
-EAGER_WARMUP = int(os.environ.get("KG_EAGER_WARMUP", "2"))
+# eager rounds before the round graphs are captured (KG_EAGER_WARMUP; 0: the
+# first round is captured directly — lazy workspaces grow inside the capture,
+# from the graph's memory pool, and the library's kernels are preloaded)
+EAGER_WARMUP = int(os.environ.get("KG_EAGER_WARMUP", "0"))
+# train(): capture every round / epoch graph during setup, so the reported
+# epoch times are steady state (needs EAGER_WARMUP = 0)
+PREPARE_IN_SETUP = os.environ.get("KG_PREPARE_IN_SETUP", "1") == "1" and EAGER_WARMUP == 0
 
 
 def _align256(x: int) -> int:
@@ -421,6 +425,42 @@ def _mark(name: str) -> None:
         setup_marks.append((name, time.perf_counter()))
 
 
+_torch_warm = set()
+
+
+def _warm_torch_kernels(dev) -> None:
+    """Run, once per process and device, the few PyTorch elementwise /
+    reduction / index kernels the round, epoch and sampler bodies use, on
+    tiny tensors: CUDA loads kernels lazily, and loading these from PyTorch's
+    large modules cost ~80-130 ms inside the first training epoch of a fresh
+    process (its first-epoch time was 99-142 ms against 7 ms later, 17 ms
+    with CUDA_MODULE_LOADING=EAGER)."""
+    torch = _torch()
+    if dev.index in _torch_warm:
+        return
+    _torch_warm.add(dev.index)
+    i64 = torch.zeros(8, dtype=torch.int64, device=dev)
+    i32 = torch.zeros(8, dtype=torch.int32, device=dev)
+    f32 = torch.zeros(8, dtype=torch.float32, device=dev)
+    i64.add_(1)
+    i64.fill_(2)
+    torch.mul(i64, i64, out=i64)
+    i32.fill_(1)
+    f32.fill_(1.0)
+    src = torch.ones(1, dtype=torch.float32, device=dev)
+    f32.index_copy_(0, i64[:1].zero_(), src)
+    i64[2:3].copy_(i64.min().view(1))
+    i64[3:4].copy_(i64.sum().view(1))
+    i32[1:2].copy_(i32.min().view(1))
+    _ = i32 + i32
+    _ = f32[i64[:2]]
+    _ = torch.stack([f32.sum(), f32[0], i32[0].double()])
+    _ = i32.to(torch.int64)
+    _ = f32.mean()
+    _ = torch.cat([f32, f32])
+    _ = torch.bitwise_or(i32, i32)
+
+
 class _Worker:
     """Device state of one partition: view, buffers, RNG stream, local
     embedding rows and their Adam moments."""
@@ -519,6 +559,7 @@ class Trainer:
         self.sizes, self.rounds = _plan_sizes([p.num_core_edges for p in pset.partitions],
                                                 model_config.negatives_per_positive, train_config)
         self.dev = torch.device("cuda", torch.cuda.current_device())
+        _warm_torch_kernels(self.dev)
         _mark("params")
         self.model = DeviceModel.from_params(model_config, params, self.dev)
         _mark("model")
@@ -1028,6 +1069,8 @@ def train(pset: PartitionSet, graph, model_config: ModelConfig, train_config: Tr
 
 def _train_loop(tr, train_config, eval_fn, t_setup) -> tuple:
     torch = _torch()
+    if PREPARE_IN_SETUP:
+        tr.prepare()   # every graph captured before epoch 0: epoch times are steady state
     torch.cuda.synchronize()
     report = TrainReport(rounds_per_epoch=tr.rounds, batch_sizes=list(tr.sizes),
                          setup_seconds=time.perf_counter() - t_setup)

@@ -90,10 +90,16 @@ def main():
         print(f"   cudaMalloc/cudaFree this call: {seg}; allocated {torch.cuda.memory_allocated() / 2**20:.1f} MiB, "
               f"reserved {torch.cuda.memory_reserved() / 2**20:.1f} MiB after the call", flush=True)
         if a.sample:
+            import collections
             if rep.setup_seconds > 0.06:
-                import collections
                 win = [st for t, st in samples if t0 <= t <= t0 + rep.setup_seconds]
                 for st, c in collections.Counter(win).most_common(4):
+                    print(f"   [{c} samples] " + " <- ".join(reversed(st)), flush=True)
+            if rep.epoch_seconds[0] > 0.02:
+                a0 = t0 + rep.setup_seconds
+                win = [st for t, st in samples if a0 <= t <= a0 + 0.2]
+                print("   first-epoch host samples:", flush=True)
+                for st, c in collections.Counter(win).most_common(6):
                     print(f"   [{c} samples] " + " <- ".join(reversed(st)), flush=True)
             samples.clear()
         from paper_2201_02791_b200 import _lib as libm2

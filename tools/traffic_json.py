@@ -1,5 +1,5 @@
 #!/usr/bin/env python
-"""profiles/r1_roofline_traffic.json from the ncu --set full capture made by
+"""profiles/r3_roofline_traffic.json from the ncu --set full capture made by
 tools/ncu_traffic.sh (DRAM bytes per launch of bench.py's roofline kernel).
 
     python tools/traffic_json.py gpurun_out/traffic_full.ncu-rep
@@ -36,10 +36,11 @@ main = [l for l in launches if "combine" not in l["kernel"]]
 out = {"source": "ncu --set full --cache-control none --clock-control none, bench.py --steps 2 --warmup 3 "
                  "(tools/ncu_traffic.sh)",
        "launches": launches,
-       # bench.py's timer brackets k_aggregate alone (exact launch name), so
-       # the hub-combine launches are listed but not averaged in
+       # bench.py's roofline kernel (exact launch name); hub-combine launches
+       # are listed but not averaged in
+       "kernel": "k_csc_backward",
        "traffic_bytes_per_launch": sum(l["dram_read_bytes"] + l["dram_write_bytes"] for l in main)
        / max(len(main), 1)}
-path = os.path.join(ROOT, "profiles", "r1_roofline_traffic.json")
+path = os.path.join(ROOT, "profiles", "r3_roofline_traffic.json")
 json.dump(out, open(path, "w"), indent=1)
 print(json.dumps(out, indent=1))
