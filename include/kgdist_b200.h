@@ -146,6 +146,11 @@ kg_status kg_kernel_timer_span(int64_t handle, const char* a, const char* b, dou
  * lazy module loading); *loaded = functions loaded (0 on drivers without the
  * enumeration entry points). Called once per process by the host package. */
 kg_status kg_preload_kernels(int32_t* loaded);
+/* Epoch-end bookkeeping (ref:trainer.py:446-462, the epoch loss and the
+ * non-finite checks): out[w] = mean of losses[w*ld + r] over r < rounds
+ * (float64), out[nloc + j] = *flag_ptrs[j] (status words, then cleared). */
+kg_status kg_epoch_end(const float* losses, int64_t ld, int32_t nloc, int32_t rounds, const uint64_t* flag_ptrs,
+                       int32_t nflags, double* out, void* stream);
 
 /* ---------------------------------------------------------------------- */
 /* Primitives (stable radix sort / scan) used by every stage below          */

@@ -71,6 +71,7 @@ _PROTOS = {
     "kg_kernel_timer_read_named": (ST, [c_int64, ctypes.c_char_p, POINTER(c_double), POINTER(c_int64)]),
     "kg_kernel_timer_span": (ST, [c_int64, ctypes.c_char_p, ctypes.c_char_p, POINTER(c_double), POINTER(c_int64)]),
     "kg_preload_kernels": (ST, [POINTER(c_int32)]),
+    "kg_epoch_end": (ST, [P, c_int64, c_int32, c_int32, P, c_int32, P, P]),
     "kg_copy_segments": (ST, [POINTER(KgCopySeg), c_int32, P, c_int64, P]),
     "kg_loss_group_fields": (c_int32, [P, c_int64, c_int64, c_int32, c_int32, c_int32, POINTER(c_void_p),
                                        POINTER(c_int64), c_int32]),

@@ -213,5 +213,42 @@ kg_status kg_sparse_step(float* table, float* m, float* v, const float* grad, co
 
 }  // extern "C"
 
+// Epoch-end bookkeeping in one launch (one block): out[w] = mean over the
+// epoch's rounds of worker w's round losses (float64, rounds summed in a
+// fixed order), out[nloc + j] = status word j (then cleared). Replaces the
+// handful of small tensor ops (mean, cast, cat, or, zero) that sat on the
+// stream at every epoch boundary.
+namespace kg {
+__global__ void __launch_bounds__(256) k_epoch_end(const float* __restrict__ losses, int64_t ld, int32_t nloc,
+                                                   int32_t rounds, const unsigned long long* __restrict__ flag_ptrs,
+                                                   int32_t nflags, double* __restrict__ out) {
+  __shared__ double part[256];
+  for (int w = 0; w < nloc; ++w) {
+    double s = 0.0;
+    for (int r = threadIdx.x; r < rounds; r += blockDim.x) s += (double)losses[(int64_t)w * ld + r];
+    part[threadIdx.x] = s;
+    __syncthreads();
+    for (int o = 128; o > 0; o >>= 1) {
+      if ((int)threadIdx.x < o) part[threadIdx.x] += part[threadIdx.x + o];
+      __syncthreads();
+    }
+    if (threadIdx.x == 0) out[w] = rounds > 0 ? part[0] / (double)rounds : 0.0;
+    __syncthreads();
+  }
+  for (int j = threadIdx.x; j < nflags; j += blockDim.x) {
+    uint32_t* f = reinterpret_cast<uint32_t*>(flag_ptrs[j]);
+    out[nloc + j] = (double)*f;
+    *f = 0u;
+  }
+}
+}  // namespace kg
+
+extern "C" kg_status kg_epoch_end(const float* losses, int64_t ld, int32_t nloc, int32_t rounds,
+                                  const uint64_t* flag_ptrs, int32_t nflags, double* out, void* stream) {
+  KG_LAUNCH("k_epoch_end", kg::k_epoch_end, 1, 256, 0, as_stream(stream), losses, ld, nloc, rounds,
+            reinterpret_cast<const unsigned long long*>(flag_ptrs), nflags, out);
+  return KG_OK;
+}
+
 // this module's anchor for kg_preload_kernels (kg_primitives.cu)
 extern "C" const void* kg_anchor_optim() { return reinterpret_cast<const void*>(&kg::k_tree_mean); }

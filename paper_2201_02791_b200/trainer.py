@@ -639,46 +639,38 @@ class Trainer:
         host memory without blocking. finish_epoch(handle) reads it."""
         torch = _torch()
         nloc = len(self.workers)
-        means = self.losses[:, : self.rounds].mean(dim=1).double()
-        flags = torch.cat([w.bufs.flags.reshape(1) for w in self.workers] + [self.flags.reshape(1)])
-        f_or = flags[0].clone()
-        for i in range(1, flags.numel()):
-            f_or.bitwise_or_(flags[i])
+        flags = [w.bufs.flags for w in self.workers] + [self.flags]
+        if getattr(self, "_ep_out", None) is None:
+            self._ep_ptrs = torch.tensor([f.data_ptr() for f in flags], dtype=torch.int64, device=self.dev)
+            self._ep_out = torch.empty(nloc + len(flags), dtype=torch.float64, device=self.dev)
+            self._ep_all = torch.empty((self.world, nloc + len(flags)), dtype=torch.float64, device=self.dev)
+        # one launch: per-worker mean round loss + the status words (cleared)
+        _lib.call("kg_epoch_end", self.losses.data_ptr(), self.losses.shape[1], nloc, self.rounds,
+                  self._ep_ptrs.data_ptr(), len(flags), self._ep_out.data_ptr(), _lib.stream_handle())
+        out = self._ep_out
         if self.dist:
-            # every rank's status word rides on the same all-gather, so all
+            # every rank's status words ride on the same all-gather, so all
             # ranks raise the same error at the same epoch
-            if getattr(self, "_nloc_dev", None) is None:   # a device constant: no per-epoch host copy
-                self._nloc_dev = torch.full((), float(nloc), dtype=torch.float64, device=self.dev)
-            both = torch.stack([means.sum(), self._nloc_dev, f_or.double()])
-            gathered = torch.empty((self.world, 3), dtype=torch.float64, device=self.dev)
-            torch.distributed.all_gather_into_tensor(gathered, both)
-            means = gathered[:, :2].reshape(-1)
-            all_flags = gathered[:, 2].to(torch.int32)
-        else:
-            all_flags = f_or.reshape(1)
-        host_means = torch.empty(means.shape, dtype=means.dtype, pin_memory=True)
-        host_flags = torch.empty(all_flags.shape, dtype=all_flags.dtype, pin_memory=True)
-        host_means.copy_(means, non_blocking=True)
-        host_flags.copy_(all_flags, non_blocking=True)
-        for w in self.workers:
-            w.bufs.flags.zero_()
-        self.flags.zero_()
+            torch.distributed.all_gather_into_tensor(self._ep_all, self._ep_out)
+            out = self._ep_all
+        host = torch.empty(out.shape, dtype=out.dtype, pin_memory=True)
+        host.copy_(out, non_blocking=True)
         end = torch.cuda.Event(enable_timing=True)
         end.record()
-        return (self._epoch_start, end, host_means, host_flags)
+        return (self._epoch_start, end, host, nloc)
 
     def finish_epoch(self, handle) -> tuple:
         """Wait for an end_epoch() handle; raise on non-finite values (any
         rank's, with several ranks), return (mean loss, device seconds of the
         epoch on this rank)."""
-        start, end, host_means, host_flags = handle
+        start, end, host, nloc = handle
         end.synchronize()
+        rows = host.numpy().reshape(-1, host.shape[-1])   # (ranks, nloc means + status words)
         f = 0
-        for x in host_flags.tolist():
+        for x in rows[:, nloc:].ravel().tolist():
             f |= int(x)
         raise_for_flags(f)
-        m = host_means.numpy()
-        loss = float(m[0::2].sum() / m[1::2].sum()) if self.dist else float(np.mean(m))
+        loss = float(rows[:, :nloc].sum() / rows[:, :nloc].size)
         return loss, start.elapsed_time(end) / 1e3
 
     def _compute_body(self):
