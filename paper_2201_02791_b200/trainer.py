@@ -812,6 +812,9 @@ class Trainer:
                 if key not in self._graphs:
                     self._capture_slot(slot)
                     return True
+        if self.P > 1 and self.mc.mode == MODE_EMBEDDING and getattr(self, "_snap_plan", None) is None \
+                and self.t > 0:
+            self._snapshot_plan()   # host work for the final snapshot, while the device trains
         return False
 
     def prepare(self) -> None:
@@ -895,21 +898,11 @@ class Trainer:
         torch = _torch()
         dist = torch.distributed
         base = self.init_params.entity_embed
-        owner = np.full(len(base), -1, dtype=np.int64)
-        for part in sorted(self.pset.partitions, key=lambda p: p.id):
-            ends = np.concatenate([part.core_vertices, part.replicated_vertices]).astype(np.int64)
-            owner[ends[owner[ends] < 0]] = part.id
-        ids, rows = [], []
-        for w in self.workers:
-            lids = np.asarray(w.view.local_ids, dtype=np.int64)
-            sel = np.flatnonzero(owner[lids] == self.pset.partitions[w.wid].id)
-            ids.append(torch.from_numpy(lids[sel]).to(self.dev))
-            rows.append(w.input_rows[torch.from_numpy(sel).to(self.dev)])
-        ids = torch.cat(ids)
-        rows = torch.cat(rows)
+        ids, sels, covered = self._snapshot_plan()
+        rows = torch.cat([w.input_rows[sel] for w, sel in zip(self.workers, sels)])
         if not self.dist:
-            out = base.copy()
-            out[ids.cpu().numpy()] = rows.cpu().numpy().astype(np.float64)
+            out = np.empty_like(base) if covered else base.copy()
+            out[ids.cpu().numpy()] = rows.cpu().numpy()
             return out
         k = torch.tensor([ids.numel()], dtype=torch.int64, device=self.dev)
         counts = torch.empty(self.world, dtype=torch.int64, device=self.dev)
@@ -925,10 +918,33 @@ class Trainer:
         dist.all_gather_into_tensor(ids_all, ids_p)
         dist.all_gather_into_tensor(rows_all, rows_p)
         ids_all, rows_all = ids_all.cpu().numpy(), rows_all.cpu().numpy()
-        out = base.copy()
+        out = np.empty_like(base) if covered else base.copy()
         for r, c in enumerate(counts):
-            out[ids_all[r, :c]] = rows_all[r, :c].astype(np.float64)
+            out[ids_all[r, :c]] = rows_all[r, :c]
         return out
+
+    def _snapshot_plan(self):
+        """(global ids of the rows this rank's partitions own (device), the
+        owned local rows per worker (device index tensors), whether the
+        partitions own every entity): the ownership rule of
+        ref:trainer.py:319-333, computed once (prefetch() does it while the
+        device runs an epoch, so the final snapshot only moves rows)."""
+        if getattr(self, "_snap_plan", None) is None:
+            torch = _torch()
+            n = len(self.init_params.entity_embed)
+            owner = np.full(n, -1, dtype=np.int64)
+            for part in sorted(self.pset.partitions, key=lambda p: p.id):
+                ends = np.concatenate([part.core_vertices, part.replicated_vertices]).astype(np.int64)
+                owner[ends[owner[ends] < 0]] = part.id
+            ids, sels = [], []
+            for w in self.workers:
+                lids = np.asarray(w.view.local_ids, dtype=np.int64)
+                sel = np.flatnonzero(owner[lids] == self.pset.partitions[w.wid].id)
+                ids.append(lids[sel])
+                sels.append(torch.from_numpy(sel).to(self.dev))
+            ids = torch.from_numpy(np.concatenate(ids)).to(self.dev)
+            self._snap_plan = (ids, sels, bool((owner >= 0).all()))
+        return self._snap_plan
 
     def check_replicas(self):
         """Dense replicas must be bitwise equal on every rank (ref:trainer.py:465-469)."""
