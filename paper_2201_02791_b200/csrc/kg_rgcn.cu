@@ -490,14 +490,24 @@ __global__ void __launch_bounds__(256, KG_GATHER_BPS) k_csc_backward(CscArgs a) 
 #pragma unroll
           for (int s = 0; s < S; ++s)
             if (slot_ok[s]) VecIO<VEC>::load(a.Y + ((int64_t)q * B + b) * d + (s * LPR + cl) * VEC, y[b][s]);
-#pragma unroll
+    // wide rows: the two message halves share one copy of the loop body (a
+    // rolled loop with the half's metadata selected: the unrolled pair made
+    // the fused pass 3,160 instructions and instruction-cache misses a top
+    // stall; rolled 936). Narrow rows keep the unrolled pair (rolling them
+    // spills).
+#pragma unroll(EPI == 1 ? 1 : 2)
     for (int h = 0; h < 2; ++h) {
       const int nh = min(32, ngather - 32 * h);
+      const uint32_t offh = h ? m.off[1] : m.off[0];
+      const float nrmh = h ? nrm[1] : nrm[0];
+      float cfh[NB];
+#pragma unroll
+      for (int b = 0; b < NB; ++b) cfh[b] = h ? m.cf[1][b] : m.cf[0][b];
       for (int j = 0; j < nh; j += UNR * EPI) {
         float zs[UNR][S][VEC];
 #pragma unroll
         for (int k = 0; k < UNR; ++k) {
-          const uint32_t off = __shfl_sync(0xffffffffu, m.off[h], (j + k * EPI + grp) & 31);
+          const uint32_t off = __shfl_sync(0xffffffffu, offh, (j + k * EPI + grp) & 31);
           if (MODE != 0) {
 #pragma unroll
             for (int s = 0; s < S; ++s) VecIO<VEC>::load(zb[s] + off, zs[k][s]);
@@ -520,7 +530,7 @@ __global__ void __launch_bounds__(256, KG_GATHER_BPS) k_csc_backward(CscArgs a) 
 #pragma unroll
           for (int b = 0; b < NB; ++b) {
             if (b < B) {
-              const float cf = __shfl_sync(0xffffffffu, m.cf[h][b], (j + k * EPI + grp) & 31);
+              const float cf = __shfl_sync(0xffffffffu, cfh[b], (j + k * EPI + grp) & 31);
 #pragma unroll
               for (int s = 0; s < S; ++s)
 #pragma unroll
@@ -547,7 +557,7 @@ __global__ void __launch_bounds__(256, KG_GATHER_BPS) k_csc_backward(CscArgs a) 
             const float tot = group_sum8<LPR>(part, (unsigned)cl);
             const int k = entry8<LPR>((unsigned)cl);
             const int e = j + k * EPI + grp;
-            const float wk = __shfl_sync(0xffffffffu, nrm[h], e & 31);
+            const float wk = __shfl_sync(0xffffffffu, nrmh, e & 31);
             if ((cl & (LPR / 8 - 1)) == 0 && e < nh) a.ed[(int64_t)(beg + 32 * h + e) * B + b] = wk * tot;
           }
         }
@@ -568,7 +578,7 @@ __global__ void __launch_bounds__(256, KG_GATHER_BPS) k_csc_backward(CscArgs a) 
             }
             const float tot = warp_sum8(part);
             const int k = sum8_entry(lane);
-            const float wk = __shfl_sync(0xffffffffu, nrm[h], (j + k) & 31);
+            const float wk = __shfl_sync(0xffffffffu, nrmh, (j + k) & 31);
             if ((lane & 3) == 0 && j + k < nh) a.ed[(int64_t)(beg + 32 * h + j + k) * B + b] = wk * tot;
           }
         }
