@@ -516,12 +516,23 @@ __global__ void k_group_sort_T(int32_t* __restrict__ members, const uint32_t* __
   }
 }
 
-__global__ void k_pointer_jump(int32_t* __restrict__ ptr, int64_t n) {
+// One pointer-jumping round. The rounds are a fixed chain of launches (a
+// captured graph cannot branch), so each round records whether it moved any
+// pointer and a round after a round that moved none returns at once: the
+// chain costs its launch latencies past convergence, not full passes.
+__global__ void k_pointer_jump(int32_t* __restrict__ ptr, int64_t n, const uint32_t* __restrict__ prev_moved,
+                               uint32_t* __restrict__ moved) {
+  if (prev_moved && *prev_moved == 0u) return;
+  bool any = false;
   for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < n; p += (int64_t)gridDim.x * blockDim.x) {
     int32_t q = ptr[p];
     int32_t r = ptr[q];
-    if (r != q) ptr[p] = r;
+    if (r != q) {
+      ptr[p] = r;
+      any = true;
+    }
   }
+  if (__syncthreads_or(any) && threadIdx.x == 0) *moved = 1u;
 }
 
 __global__ void k_perm_final(const int32_t* __restrict__ js, int64_t n, const int32_t* __restrict__ members,
@@ -740,7 +751,7 @@ kg_status kg_perm_draws_buffered(int64_t n, kg_pcg64* g, uint32_t* U, int64_t W,
 }
 
 int64_t kg_perm_resolve_workspace_bytes(int64_t n) {
-  return (int64_t)(align_up(n * 4) * 5 + scan_workspace(n) + 4096);
+  return (int64_t)(align_up(n * 4) * 5 + scan_workspace(n) + 4096 + align_up(64 * 4));
 }
 
 kg_status kg_perm_resolve(const int32_t* js, int64_t n, int32_t* perm, void* ws, int64_t ws_bytes, void* stream) {
@@ -767,7 +778,10 @@ kg_status kg_perm_resolve(const int32_t* js, int64_t n, int32_t* perm, void* ws,
   KG_LAUNCH("k_group_sort_T", k_group_sort_T, gb, 256, 0, st, members, start, cnt, n, root);
   int rounds = 1;
   while ((int64_t(1) << rounds) < n) ++rounds;
-  for (int it = 0; it < rounds + 1; ++it) KG_LAUNCH("k_pointer_jump", k_pointer_jump, gb, 256, 0, st, root, n);
+  uint32_t* moved = a.take<uint32_t>(rounds + 1);
+  KG_CUDA(cudaMemsetAsync(moved, 0, (size_t)(rounds + 1) * 4, st));
+  for (int it = 0; it < rounds + 1; ++it)
+    KG_LAUNCH("k_pointer_jump", k_pointer_jump, gb, 256, 0, st, root, n, it ? moved + it - 1 : nullptr, moved + it);
   KG_LAUNCH("k_perm_final", k_perm_final, gb, 256, 0, st, js, n, members, start, cnt, root, perm);
   KG_CHECK_LAUNCH("perm resolve");
   return KG_OK;
