@@ -941,8 +941,10 @@ class Trainer:
                 lids = np.asarray(w.view.local_ids, dtype=np.int64)
                 sel = np.flatnonzero(owner[lids] == self.pset.partitions[w.wid].id)
                 ids.append(lids[sel])
-                sels.append(torch.from_numpy(sel).to(self.dev))
-            ids = torch.from_numpy(np.concatenate(ids)).to(self.dev)
+                # pinned, non-blocking: a pageable upload would wait for the
+                # epoch queued on the stream (this runs inside the epoch loop)
+                sels.append(torch.from_numpy(sel).pin_memory().to(self.dev, non_blocking=True))
+            ids = torch.from_numpy(np.concatenate(ids)).pin_memory().to(self.dev, non_blocking=True)
             self._snap_plan = (ids, sels, bool((owner >= 0).all()))
         return self._snap_plan
 
