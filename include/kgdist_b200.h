@@ -521,6 +521,11 @@ kg_status kg_halo_expand(const int32_t* tri, int64_t m, int64_t n, const uint32_
  * n_max bounds counts[t] for the launch size. */
 kg_status kg_dropout_mask(kg_pcg64* g, const int32_t* counts, int32_t t, int32_t d, double p, int64_t n_max,
                           float* mask, void* stream);
+/* numpy Generator.uniform(low, high, size=count) from the host stream state
+ * *g (not advanced: the caller moves its own generator on by count next64
+ * draws): out[j] = low + (high - low) * random_j, bit-exact with numpy. The
+ * trainer draws the initial embedding table this way (ref:model.py:108-128). */
+kg_status kg_uniform_f64(const kg_pcg64* g, int64_t count, double low, double high, double* out, void* stream);
 
 /* ---------------------------------------------------------------------- */
 /* R24-R26  Filtered evaluation (ref:evaluate.py:93-225)                   */

@@ -106,6 +106,7 @@ _PROTOS = {
     "kg_csc_positions": (ST, [POINTER(KgGraphCsr), P, P, P]),
     "kg_rgcn_backward_y": (ST, [POINTER(KgGraphCsr), POINTER(KgLayerParams), P, P, P, P, c_int32, P, c_int64, P]),
     "kg_dropout_mask": (ST, [P, P, c_int32, c_int32, c_double, c_int64, P, P]),
+    "kg_uniform_f64": (ST, [P, c_int64, c_double, c_double, P, P]),
     "kg_eval_candidates": (ST, [P, c_int32, P, P, c_int64, P, P, P, c_int32, P, P, P]),
     "kg_pack_rows_bytes": (c_int64, [c_int64, c_int64]),
     "kg_pack_rows": (ST, [P, c_int64, P, P, c_int32, c_int64, c_int64, P, P]),

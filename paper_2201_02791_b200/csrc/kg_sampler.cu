@@ -129,6 +129,24 @@ __global__ void k_pcg_advance(kg_pcg64* __restrict__ g, uint64_t delta) {
   g->state_lo = s.lo;
 }
 
+// numpy Generator.uniform(low, high, size=count) from the stream position
+// `g` (host state, passed by value): out[j] = low + (high - low) * random_j,
+// random_j = (next64_j >> 11) * 2^-53, multiply and add rounded separately as
+// numpy's C code does (ref:model.py:108-128, the embedding-table draw).
+constexpr int UNIF_PER_THREAD = 16;
+__global__ void k_uniform_f64(kg_pcg64 g, int64_t count, double low, double range, double* __restrict__ out) {
+  const u128 s0 = state_of(g), inc = inc_of(g);
+  for (int64_t j0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) * UNIF_PER_THREAD; j0 < count;
+       j0 += (int64_t)gridDim.x * blockDim.x * UNIF_PER_THREAD) {
+    u128 st = apply_jump(pcg_jump((uint64_t)j0, inc), s0);
+    for (int k = 0; k < UNIF_PER_THREAD && j0 + k < count; ++k) {
+      st = pcg_step(st, inc);
+      const double u = (double)(pcg_output(st) >> 11) * (1.0 / 9007199254740992.0);
+      out[j0 + k] = __dadd_rn(low, __dmul_rn(range, u));
+    }
+  }
+}
+
 // Inverted dropout (ref:model.py:221-227): keep = rng.random((T, d)) >= p,
 // mask = keep / (1 - p). random() is (next64 >> 11) * 2^-53, one next64 per
 // value in row-major order, so value j sits at stream position j: each thread
@@ -793,6 +811,14 @@ kg_status kg_stream_gather(const int32_t* pos, int64_t npos, const int32_t* neg,
   KG_LAUNCH("k_stream_gather", k_stream_gather, grid_for(npos + nneg), 256, 0, as_stream(stream), pos, npos, neg, nneg, perm,
                                                                         stream_triples, labels);
   KG_CHECK_LAUNCH("k_stream_gather");
+  return KG_OK;
+}
+
+// --- uniform draws ---------------------------------------------------------------
+kg_status kg_uniform_f64(const kg_pcg64* g, int64_t count, double low, double high, double* out, void* stream) {
+  if (count <= 0) return KG_OK;
+  KG_LAUNCH("k_uniform_f64", k_uniform_f64, persistent_blocks(ceil_div(count, UNIF_PER_THREAD), 256, 8), 256, 0,
+            as_stream(stream), *g, count, low, high - low, out);
   return KG_OK;
 }
 

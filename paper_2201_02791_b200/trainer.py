@@ -425,6 +425,30 @@ def _mark(name: str) -> None:
         setup_marks.append((name, time.perf_counter()))
 
 
+def _init_params_device(config: ModelConfig, seed: int, num_entities: int, dev):
+    """init_params(config, default_rng(seed), num_entities) with the embedding
+    table — the one large draw (N x d uniforms) — drawn on the device from
+    the generator's state after the dense blocks (kg_uniform_f64, bit-exact
+    with numpy). Returns (params, device float64 table, (pinned host tensor,
+    event)): params.entity_embed views the pinned host copy, complete once
+    the event has fired."""
+    import dataclasses
+    torch = _torch()
+    rng = np.random.default_rng(seed)
+    params = init_params(dataclasses.replace(config, mode=MODE_FEATURE), rng)   # same draws up to the table
+    d = config.dims[0]
+    el = float(np.sqrt(3.0 / d))
+    g = _lib.pcg_from_numpy(rng)
+    table = torch.empty((num_entities, d), dtype=torch.float64, device=dev)
+    _lib.call("kg_uniform_f64", ctypes.byref(g), num_entities * d, -el, el, table.data_ptr(), _lib.stream_handle())
+    host = torch.empty((num_entities, d), dtype=torch.float64, pin_memory=True)
+    host.copy_(table, non_blocking=True)
+    ev = torch.cuda.Event()
+    ev.record()
+    params.entity_embed = host.numpy()
+    return params, table, (host, ev)
+
+
 _torch_warm = set()
 
 
@@ -466,7 +490,7 @@ class _Worker:
     embedding rows and their Adam moments."""
 
     def __init__(self, wid, partition, pset, config: ModelConfig, tc: TrainConfig, b: int, params: ModelParams,
-                 features, rounds: int = 1, epoch_pool=None, epoch_stream=None):
+                 features, rounds: int = 1, epoch_pool=None, epoch_stream=None, embed_dev=None):
         torch = _torch()
         self.wid = wid
         _mark("worker")
@@ -482,12 +506,13 @@ class _Worker:
         self.g_drop = (_lib.pcg_to_device(_lib.pcg_from_numpy(
             np.random.default_rng((tc.seed ^ self.view.partition_id) + 0x9E3779B9)), dev)
             if config.dropout > 0.0 else None)
-        local = self.view.local_ids
-        if config.mode == MODE_EMBEDDING:
-            rows = params.entity_embed[local]
+        if config.mode == MODE_EMBEDDING and embed_dev is not None:
+            # the initial table was drawn on the device: gather this view's rows there
+            self.input_rows = embed_dev.index_select(0, self.view.d_local_ids.long()).float()
         else:
-            rows = features[local]
-        self.input_rows = torch.as_tensor(np.ascontiguousarray(rows, dtype=np.float32)).to(dev)
+            local = self.view.local_ids
+            rows = params.entity_embed[local] if config.mode == MODE_EMBEDDING else features[local]
+            self.input_rows = torch.as_tensor(np.ascontiguousarray(rows, dtype=np.float32)).to(dev)
         _mark("rng+rows")
         self.bufs = ViewBuffers(config, self.view, b, input_rows=self.input_rows)
         _mark("bufs")
@@ -545,8 +570,17 @@ class Trainer:
         self.local_wids = [w for w in range(self.P) if w % self.world == self.rank]
         setup_marks.clear()
         _mark("start")
-        params = initial_params.copy() if initial_params is not None else init_params(
-            model_config, np.random.default_rng(train_config.seed), num_entities=pset.num_entities)
+        self.dev = torch.device("cuda", torch.cuda.current_device())
+        _warm_torch_kernels(self.dev)
+        embed_dev = None
+        if initial_params is not None:
+            params = initial_params.copy()
+        elif model_config.mode == MODE_EMBEDDING:
+            params, embed_dev, self._embed_host = _init_params_device(model_config, train_config.seed,
+                                                                      pset.num_entities, self.dev)
+        else:
+            params = init_params(model_config, np.random.default_rng(train_config.seed),
+                                 num_entities=pset.num_entities)
         if model_config.mode == MODE_FEATURE:
             if graph.features is None:
                 raise ValidationError("feature mode requires graph features")
@@ -558,8 +592,6 @@ class Trainer:
         self.init_params = params
         self.sizes, self.rounds = _plan_sizes([p.num_core_edges for p in pset.partitions],
                                                 model_config.negatives_per_positive, train_config)
-        self.dev = torch.device("cuda", torch.cuda.current_device())
-        _warm_torch_kernels(self.dev)
         _mark("params")
         self.model = DeviceModel.from_params(model_config, params, self.dev)
         _mark("model")
@@ -570,8 +602,12 @@ class Trainer:
         self.workers = [_Worker(w, pset.partitions[w], pset, model_config, train_config, self.sizes[w], params,
                                 features, self.rounds,
                                 epoch_pool=_lib.persistent_pool(("epoch", di, k)) if graph_pools else None,
-                                epoch_stream=_lib.cached_stream(("epoch", di, k), self.dev) if graph_pools else None)
+                                epoch_stream=_lib.cached_stream(("epoch", di, k), self.dev) if graph_pools else None,
+                                embed_dev=embed_dev)
                         for k, w in enumerate(self.local_wids)]
+        del embed_dev
+        if getattr(self, "_embed_host", None) is not None:
+            self._embed_host[1].synchronize()   # the host copy of the initial table is complete
         nloc = len(self.workers)
         self.grads_local = torch.zeros((nloc, D), dtype=torch.float32, device=self.dev)
         self.grads_all = (torch.zeros((self.P, D), dtype=torch.float32, device=self.dev) if self.dist
@@ -817,12 +853,19 @@ class Trainer:
             self._snapshot_plan()   # host work for the final snapshot, while the device trains
         return False
 
-    def prepare(self) -> None:
+    def prepare(self, first_epoch: bool = False) -> None:
         """Do all pending one-time host work now (epoch graphs of the slots
         ahead, round graphs of every slot): for benchmarks, so the timed steps
-        are steady state."""
-        while self.prefetch():
-            pass
+        are steady state. first_epoch: only until the round graphs of the
+        first epoch's slot exist (train(): the other slots are captured by
+        prefetch() while the device runs epochs, overlapping the host work)."""
+        while True:
+            if first_epoch and self.use_graphs:
+                key = tuple(w.sampler.slot_stream(w.sampler.parity).triples.data_ptr() for w in self.workers)
+                if key in self._graphs:
+                    return
+            if not self.prefetch():
+                return
 
     def close(self):
         """Release the captured CUDA graphs now and break the worker <->
@@ -1080,7 +1123,8 @@ def train(pset: PartitionSet, graph, model_config: ModelConfig, train_config: Tr
 def _train_loop(tr, train_config, eval_fn, t_setup) -> tuple:
     torch = _torch()
     if PREPARE_IN_SETUP:
-        tr.prepare()   # every graph captured before epoch 0: epoch times are steady state
+        tr.prepare(first_epoch=True)   # epoch 0's graphs captured before its timing starts
+    _mark("prepare")
     torch.cuda.synchronize()
     report = TrainReport(rounds_per_epoch=tr.rounds, batch_sizes=list(tr.sizes),
                          setup_seconds=time.perf_counter() - t_setup)

@@ -86,3 +86,16 @@ def test_float64_loss_is_deterministic():
     ids = np.arange(graph.num_entities)
     runs = [kb.loss_and_grad(params, mc, batch, cg, params.entity_embed, ids) for _ in range(3)]
     assert runs[0][0] == runs[1][0] == runs[2][0]
+
+
+@pytest.mark.parametrize("n,dims,seed", [(14541, [100, 100, 100], 0), (1000, [32, 16], 7), (5, [3, 4, 2], 3)])
+def test_device_drawn_initial_table_is_numpys(n, dims, seed):
+    from paper_2201_02791_b200.trainer import _init_params_device
+    mc = kb.ModelConfig(len(dims) - 1, dims, 2, 11, 1, mode="embedding")
+    want = kb.init_params(mc, np.random.default_rng(seed), num_entities=n)
+    got, table, (host, ev) = _init_params_device(mc, seed, n, torch.device("cuda"))
+    ev.synchronize()
+    assert np.array_equal(got.entity_embed, want.entity_embed)
+    assert np.array_equal(table.cpu().numpy(), want.entity_embed)
+    for a, b in zip(got.dense_blocks(), want.dense_blocks()):
+        assert np.array_equal(a, b)
