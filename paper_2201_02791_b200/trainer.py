@@ -1170,7 +1170,9 @@ def _train_loop(tr, train_config, eval_fn, t_setup) -> tuple:
     t_fin = time.perf_counter()
     tr.check_replicas()
     params = tr.snapshot()
+    _mark("snapshot")
     tr.close()
+    _mark("close")
     report.finish_seconds = time.perf_counter() - t_fin
     return params, report
 
