@@ -99,3 +99,32 @@ def test_device_drawn_initial_table_is_numpys(n, dims, seed):
     assert np.array_equal(table.cpu().numpy(), want.entity_embed)
     for a, b in zip(got.dense_blocks(), want.dense_blocks()):
         assert np.array_equal(a, b)
+
+
+def test_feature_mode_training_matches_oracle():
+    """Feature mode (input rows from graph.features, no embedding table,
+    ref:trainer.py:186-236 with features) through train() at P = 2 vs the
+    oracle restatement on the same fp32-representable start."""
+    import kg_oracle as ko
+    graph, _ = kb.generate_synthetic(300, 4, 5.0, seed=11)
+    feats = np.random.default_rng(3).normal(size=(graph.num_entities, 12)).astype(np.float32).astype(np.float64)
+    graph = kb.KnowledgeGraph(graph.num_entities, graph.num_relations, graph.triples, features=feats)
+    pset = kb.neighborhood_expand(kb.vertex_cut_partition(graph, 2, seed=0), graph, 2)
+    mc = kb.ModelConfig(2, [12, 16, 8], 2, graph.num_relations, 1, mode="feature")
+    p0 = kb.init_params(mc, np.random.default_rng(5))
+    q = lambda a: a.astype(np.float32).astype(np.float64)
+    p0 = kb.ModelParams([q(b) for b in p0.bases], [q(c) for c in p0.coeffs], q(p0.decoder), None)
+    tc = kb.TrainConfig(epochs=3, batch_size=128, optimizer="adam", learning_rate=0.01, seed=0)
+    got, rep = kb.train(pset, graph, mc, tc, initial_params=p0)
+    views, ends = [], []
+    for part in pset.partitions:
+        views.append(ko.make_view(part.core, part.support, graph.num_entities, graph.num_relations,
+                                  partition_id=part.id, pool_size=part.pool_size))
+        ends.append(np.concatenate([part.core_vertices, part.replicated_vertices]))
+    op = ko.OParams([b.copy() for b in p0.bases], [c.copy() for c in p0.coeffs], p0.decoder.copy(), None)
+    want, curve, rounds, sizes = ko.train(views, ends, op, 1, 3, batch_size=128, seed=0, features=feats)
+    assert rep.rounds_per_epoch == rounds and rep.batch_sizes == sizes
+    np.testing.assert_allclose(rep.loss_curve, curve, rtol=1e-5)
+    for a, b in zip(got.dense_blocks(), want.dense()):
+        assert np.linalg.norm(a - b) <= 1e-4 * max(np.linalg.norm(b), 1e-30)
+    assert got.entity_embed is None
