@@ -93,6 +93,37 @@ __device__ __forceinline__ int entry8(unsigned l) {
   return ((l & (LPR / 2)) ? 4 : 0) + ((l & (LPR / 4)) ? 2 : 0) + ((l & (LPR / 8)) ? 1 : 0);
 }
 
+// Sum x[0..3] over the LPR (>= 4) lanes of a lane group, transposed (3
+// shuffles + log2(LPR / 4)); the lane holds the total of entry entry4<LPR>.
+template <int LPR>
+__device__ __forceinline__ float group_sum4(const float* x, unsigned l) {
+  constexpr unsigned O1 = LPR / 2, O2 = LPR / 4;
+  const bool b1 = l & O1, b2 = l & O2;
+  float y[2];
+#pragma unroll
+  for (int i = 0; i < 2; ++i) {
+    const float send = b1 ? x[i] : x[i + 2], keep = b1 ? x[i + 2] : x[i];
+    y[i] = keep + __shfl_xor_sync(0xffffffffu, send, O1);
+  }
+  const float send = b2 ? y[0] : y[1], keep = b2 ? y[1] : y[0];
+  float w = keep + __shfl_xor_sync(0xffffffffu, send, O2);
+#pragma unroll
+  for (unsigned o = O2 / 2; o >= 1; o >>= 1) w += __shfl_xor_sync(0xffffffffu, w, o);
+  return w;
+}
+
+template <int LPR>
+__device__ __forceinline__ int entry4(unsigned l) {
+  return ((l & (LPR / 2)) ? 2 : 0) + ((l & (LPR / 4)) ? 1 : 0);
+}
+
+#ifndef KG_NARROW_UNR
+#define KG_NARROW_UNR 4   // rows in flight per lane in the fused narrow-row (EPI = 4) CSC pass: 8 or 4
+#endif
+#ifndef KG_NARROW_NOPRED
+#define KG_NARROW_NOPRED 0   // 1: that pass gathers unpredicated (dummy slots read a live row, weight 0)
+#endif
+
 struct Chunks {
   const int32_t* ptr;
   const int32_t* row;
@@ -411,6 +442,9 @@ __global__ void __launch_bounds__(256, KG_GATHER_BPS) k_csc_backward(CscArgs a) 
   __syncthreads();
   const unsigned lane = lane_id();
   constexpr int LPR = 32 / EPI;
+  constexpr int U = (MODE == 0 && EPI == 4) ? KG_NARROW_UNR : UNR;   // rows in flight per lane
+  // predicated gathers (skip marker ~0 in the offset) where registers are short
+  constexpr bool PRED = MODE == 0 && !(EPI == 4 && KG_NARROW_NOPRED);
   const int grp = (int)lane / LPR, cl = (int)lane % LPR;
   const int32_t T = a.counts[a.t];
   const int32_t Sn = a.counts[a.t + 1];
@@ -445,7 +479,7 @@ __global__ void __launch_bounds__(256, KG_GATHER_BPS) k_csc_backward(CscArgs a) 
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
       const int e = (int)lane + 32 * h;
-      m.off[h] = MODE == 0 ? ~0u : 0u;   // fused pass: ~0 marks a message to skip
+      m.off[h] = PRED ? ~0u : 0u;   // predicated pass: ~0 marks a message to skip
       nrm[h] = 0.f;
       live[h] = false;
 #pragma unroll
@@ -466,7 +500,7 @@ __global__ void __launch_bounds__(256, KG_GATHER_BPS) k_csc_backward(CscArgs a) 
       }
     }
     int ngather = cnt;
-    if (MODE != 0) {   // (the fused pass keeps predicated loads: no registers to spare)
+    if (!PRED) {
       const unsigned v0 = __ballot_sync(0xffffffffu, live[0]), v1 = __ballot_sync(0xffffffffu, live[1]);
       if ((v0 | v1) == 0) {
         ngather = 0;
@@ -503,12 +537,12 @@ __global__ void __launch_bounds__(256, KG_GATHER_BPS) k_csc_backward(CscArgs a) 
       float cfh[NB];
 #pragma unroll
       for (int b = 0; b < NB; ++b) cfh[b] = h ? m.cf[1][b] : m.cf[0][b];
-      for (int j = 0; j < nh; j += UNR * EPI) {
-        float zs[UNR][S][VEC];
+      for (int j = 0; j < nh; j += U * EPI) {
+        float zs[U][S][VEC];
 #pragma unroll
-        for (int k = 0; k < UNR; ++k) {
+        for (int k = 0; k < U; ++k) {
           const uint32_t off = __shfl_sync(0xffffffffu, offh, (j + k * EPI + grp) & 31);
-          if (MODE != 0) {
+          if (!PRED) {
 #pragma unroll
             for (int s = 0; s < S; ++s) VecIO<VEC>::load(zb[s] + off, zs[k][s]);
           } else {
@@ -526,7 +560,7 @@ __global__ void __launch_bounds__(256, KG_GATHER_BPS) k_csc_backward(CscArgs a) 
         // dS_b += c_eb * dZ[dst]
         if (MODE != 2)
 #pragma unroll
-        for (int k = 0; k < UNR; ++k) {
+        for (int k = 0; k < U; ++k) {
 #pragma unroll
           for (int b = 0; b < NB; ++b) {
             if (b < B) {
@@ -544,9 +578,9 @@ __global__ void __launch_bounds__(256, KG_GATHER_BPS) k_csc_backward(CscArgs a) 
 #pragma unroll
         for (int b = 0; b < NB; ++b) {
           if (b < B) {
-            float part[UNR];
+            float part[U];
 #pragma unroll
-            for (int k = 0; k < UNR; ++k) {
+            for (int k = 0; k < U; ++k) {
               float dp = 0.f;
 #pragma unroll
               for (int s = 0; s < S; ++s)
@@ -554,11 +588,18 @@ __global__ void __launch_bounds__(256, KG_GATHER_BPS) k_csc_backward(CscArgs a) 
                 for (int cc = 0; cc < VEC; ++cc) dp = fmaf(y[b][s][cc], zs[k][s][cc], dp);
               part[k] = dp;
             }
-            const float tot = group_sum8<LPR>(part, (unsigned)cl);
-            const int k = entry8<LPR>((unsigned)cl);
+            float tot;
+            int k;
+            if constexpr (U == 8) {
+              tot = group_sum8<LPR>(part, (unsigned)cl);
+              k = entry8<LPR>((unsigned)cl);
+            } else {
+              tot = group_sum4<LPR>(part, (unsigned)cl);
+              k = entry4<LPR>((unsigned)cl);
+            }
             const int e = j + k * EPI + grp;
             const float wk = __shfl_sync(0xffffffffu, nrmh, e & 31);
-            if ((cl & (LPR / 8 - 1)) == 0 && e < nh) a.ed[(int64_t)(beg + 32 * h + e) * B + b] = wk * tot;
+            if ((cl & (LPR / U - 1)) == 0 && e < nh) a.ed[(int64_t)(beg + 32 * h + e) * B + b] = wk * tot;
           }
         }
         // per-edge dots, one message per warp load: one transposed warp reduction per b
@@ -566,9 +607,9 @@ __global__ void __launch_bounds__(256, KG_GATHER_BPS) k_csc_backward(CscArgs a) 
 #pragma unroll
         for (int b = 0; b < NB; ++b) {
           if (b < B) {
-            float part[UNR];
+            float part[U];
 #pragma unroll
-            for (int k = 0; k < UNR; ++k) {
+            for (int k = 0; k < U; ++k) {
               float dp = 0.f;
 #pragma unroll
               for (int s = 0; s < S; ++s)
