@@ -61,6 +61,33 @@ __device__ __forceinline__ float warp_sum8(const float* x) {
 
 __device__ __forceinline__ int sum8_entry(unsigned l) { return ((l >> 4) & 1) * 4 + ((l >> 3) & 1) * 2 + ((l >> 2) & 1); }
 
+// Sum x[0..3] over the 32 lanes, 7 shuffles: lane l holds the total of entry
+// ((l>>4)&1)*2 + ((l>>3)&1).
+__device__ __forceinline__ float warp_sum4(const float* x) {
+  const unsigned l = lane_id();
+  const bool b4 = l & 16, b3 = l & 8;
+  float y[2];
+#pragma unroll
+  for (int i = 0; i < 2; ++i) {
+    float send = b4 ? x[i] : x[i + 2];
+    float keep = b4 ? x[i + 2] : x[i];
+    y[i] = keep + __shfl_xor_sync(0xffffffffu, send, 16);
+  }
+  float send = b3 ? y[0] : y[1];
+  float keep = b3 ? y[1] : y[0];
+  float w = keep + __shfl_xor_sync(0xffffffffu, send, 8);
+  w += __shfl_xor_sync(0xffffffffu, w, 4);
+  w += __shfl_xor_sync(0xffffffffu, w, 2);
+  w += __shfl_xor_sync(0xffffffffu, w, 1);
+  return w;
+}
+
+__device__ __forceinline__ int sum4_entry(unsigned l) { return ((l >> 4) & 1) * 2 + ((l >> 3) & 1); }
+
+#ifndef KG_WIDE_UNR
+#define KG_WIDE_UNR 4   // rows in flight per lane in the fused wide-row (EPI = 1) CSC pass: 8 or 4
+#endif
+
 // Sum x[0..7] over the LPR (>= 8) lanes of a lane group (xor offsets < LPR),
 // transposed: 7 shuffles + log2(LPR / 8) for eight totals instead of
 // 8 * log2(LPR). On return the lane holds the total of entry
@@ -119,6 +146,9 @@ __device__ __forceinline__ int entry4(unsigned l) {
 
 #ifndef KG_NARROW_UNR
 #define KG_NARROW_UNR 4   // rows in flight per lane in the fused narrow-row (EPI = 4) CSC pass: 8 or 4
+#endif
+#ifndef KG_WIDE_NOPRED
+#define KG_WIDE_NOPRED 0     // 1: the fused wide-row pass gathers unpredicated
 #endif
 #ifndef KG_NARROW_NOPRED
 #define KG_NARROW_NOPRED 0   // 1: that pass gathers unpredicated (dummy slots read a live row, weight 0)
@@ -442,9 +472,9 @@ __global__ void __launch_bounds__(256, KG_GATHER_BPS) k_csc_backward(CscArgs a) 
   __syncthreads();
   const unsigned lane = lane_id();
   constexpr int LPR = 32 / EPI;
-  constexpr int U = (MODE == 0 && EPI == 4) ? KG_NARROW_UNR : UNR;   // rows in flight per lane
+  constexpr int U = (MODE == 0 && EPI == 4) ? KG_NARROW_UNR : (MODE == 0 && EPI == 1) ? KG_WIDE_UNR : UNR;
   // predicated gathers (skip marker ~0 in the offset) where registers are short
-  constexpr bool PRED = MODE == 0 && !(EPI == 4 && KG_NARROW_NOPRED);
+  constexpr bool PRED = MODE == 0 && !(EPI == 4 && KG_NARROW_NOPRED) && !(EPI == 1 && KG_WIDE_NOPRED);
   const int grp = (int)lane / LPR, cl = (int)lane % LPR;
   const int32_t T = a.counts[a.t];
   const int32_t Sn = a.counts[a.t + 1];
@@ -617,10 +647,17 @@ __global__ void __launch_bounds__(256, KG_GATHER_BPS) k_csc_backward(CscArgs a) 
                 for (int cc = 0; cc < VEC; ++cc) dp = fmaf(y[b][s][cc], zs[k][s][cc], dp);
               part[k] = dp;
             }
-            const float tot = warp_sum8(part);
-            const int k = sum8_entry(lane);
+            float tot;
+            int k;
+            if constexpr (U == 8) {
+              tot = warp_sum8(part);
+              k = sum8_entry(lane);
+            } else {
+              tot = warp_sum4(part);
+              k = sum4_entry(lane);
+            }
             const float wk = __shfl_sync(0xffffffffu, nrmh, (j + k) & 31);
-            if ((lane & 3) == 0 && j + k < nh) a.ed[(int64_t)(beg + 32 * h + j + k) * B + b] = wk * tot;
+            if ((lane & (32 / U - 1)) == 0 && j + k < nh) a.ed[(int64_t)(beg + 32 * h + j + k) * B + b] = wk * tot;
           }
         }
       }
