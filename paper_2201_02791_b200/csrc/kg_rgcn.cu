@@ -147,6 +147,12 @@ __device__ __forceinline__ int entry4(unsigned l) {
 #ifndef KG_NARROW_UNR
 #define KG_NARROW_UNR 4   // rows in flight per lane in the fused narrow-row (EPI = 4) CSC pass: 8 or 4
 #endif
+#ifndef KG_CSC_WIDE_BPS
+#define KG_CSC_WIDE_BPS 4     // resident blocks per SM of the fused wide-row CSC pass
+#endif
+#ifndef KG_CSC_NARROW_BPS
+#define KG_CSC_NARROW_BPS 4   // resident blocks per SM of the fused narrow-row CSC pass
+#endif
 #ifndef KG_WIDE_NOPRED
 #define KG_WIDE_NOPRED 0     // 1: the fused wide-row pass gathers unpredicated
 #endif
@@ -478,7 +484,9 @@ struct CscArgs {
 // EPI > 1 (narrow rows): message groups as in k_aggregate; the edge dots
 // then reduce within a lane group (log2(LPR) shuffles per message).
 template <int NB, int VEC, int S, int MODE, int EPI>
-__global__ void __launch_bounds__(256, KG_GATHER_BPS) k_csc_backward(CscArgs a) {
+__global__ void __launch_bounds__(256, (MODE == 0 && EPI >= 4) ? KG_CSC_NARROW_BPS
+                                      : (MODE == 0 && EPI == 1) ? KG_CSC_WIDE_BPS : KG_GATHER_BPS)
+    k_csc_backward(CscArgs a) {
   extern __shared__ float coef[];
   for (int i = threadIdx.x; i < a.G * a.B; i += blockDim.x) coef[i] = a.coeffs[i];
   __syncthreads();
@@ -1091,10 +1099,15 @@ static kg_status run_csc(const CscArgs& a, const kg_graph_csr* G, cudaStream_t s
   size_t smem = (size_t)a.G * a.B * sizeof(float);
   // narrow rows: the dS-only pass gathers several messages per warp load
   const bool al16 = ((uintptr_t)a.dZ & 15) == 0 && ((uintptr_t)a.Y & 15) == 0;
-  if (a.d % 4 == 0 && a.d <= 32 && al16) return launch_csc<4, 1, 4>(a, blocks, cblocks, smem, st, mode);
+  if (a.d % 4 == 0 && a.d <= 32 && al16)
+    return launch_csc<4, 1, 4>(a, mode == 0 ? persistent_blocks(cap_chunks(G) * 32, 256, KG_CSC_NARROW_BPS) : blocks,
+                               cblocks, smem, st, mode);
   if (a.d % 4 == 0 && a.d <= 64 && al16) return launch_csc<4, 1, 2>(a, blocks, cblocks, smem, st, mode);
   return dispatch_width(
-      a.d, [&] { return launch_csc<4, 1>(a, blocks, cblocks, smem, st, mode); },
+      a.d, [&] {
+        return launch_csc<4, 1>(a, mode == 0 ? persistent_blocks(cap_chunks(G) * 32, 256, KG_CSC_WIDE_BPS) : blocks,
+                                cblocks, smem, st, mode);
+      },
       [&] { return launch_csc<1, 1>(a, blocks, cblocks, smem, st, mode); },
       [&] { return launch_csc<1, 2>(a, blocks, cblocks, smem, st, mode); },
       [&] { return launch_csc<1, 4>(a, blocks, cblocks, smem, st, mode); },
