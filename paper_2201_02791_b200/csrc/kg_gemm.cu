@@ -111,12 +111,31 @@ __global__ void __launch_bounds__(GT) k_gemm(GemmArgs g) {
   }
 }
 
-// out[i] = sum_z part[z][i] (fixed order), i < count
-__global__ void k_reduce_splits(const float* __restrict__ part, int splits, int64_t count, float* __restrict__ out) {
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < count; i += (int64_t)gridDim.x * blockDim.x) {
+// out[i] = sum_z part[z][i], i < count, in a fixed order: a block covers 32
+// outputs with 8 groups of contiguous split ranges each (the 20 k outputs of
+// a dV partial used to leave 79 blocks each summing ~150 splits serially);
+// the 8 group sums are added in group order.
+constexpr int RS_COLS = 32, RS_GROUPS = 8;
+__global__ void __launch_bounds__(RS_COLS * RS_GROUPS) k_reduce_splits(const float* __restrict__ part, int splits,
+                                                                       int64_t count, float* __restrict__ out) {
+  __shared__ float red[RS_GROUPS][RS_COLS];
+  const int c = threadIdx.x % RS_COLS, g = threadIdx.x / RS_COLS;
+  const int per = (splits + RS_GROUPS - 1) / RS_GROUPS;
+  const int z0 = g * per, z1 = min(splits, z0 + per);
+  for (int64_t base = (int64_t)blockIdx.x * RS_COLS; base < count; base += (int64_t)gridDim.x * RS_COLS) {
+    const int64_t i = base + c;
     float s = 0.f;
-    for (int z = 0; z < splits; ++z) s += part[(int64_t)z * count + i];
-    out[i] = s;
+    if (i < count)
+      for (int z = z0; z < z1; ++z) s += part[(int64_t)z * count + i];
+    red[g][c] = s;
+    __syncthreads();
+    if (g == 0 && i < count) {
+      float t = red[0][c];
+#pragma unroll
+      for (int q = 1; q < RS_GROUPS; ++q) t += red[q][c];
+      out[i] = t;
+    }
+    __syncthreads();
   }
 }
 
@@ -150,13 +169,15 @@ kg_status simt_gemm_tn(const GemmArgs& g, float* out, void* ws, cudaStream_t st)
   KG_LAUNCH("k_gemm", (k_gemm<true>), grid, GT, 0, st, h);
   KG_CHECK_LAUNCH("k_gemm<tn>");
   int64_t cnt = g.K * g.N;
-  KG_LAUNCH("k_reduce_splits", k_reduce_splits, persistent_blocks(cnt, 256, 4), 256, 0, st, h.C, splits, cnt, out);
+  KG_LAUNCH("k_reduce_splits", k_reduce_splits, persistent_blocks(cnt, RS_COLS, 8), RS_COLS * RS_GROUPS, 0, st, h.C,
+            splits, cnt, out);
   KG_CHECK_LAUNCH("k_reduce_splits");
   return KG_OK;
 }
 
 kg_status reduce_splits(const float* part, int splits, int64_t count, float* out, cudaStream_t st) {
-  KG_LAUNCH("k_reduce_splits", k_reduce_splits, persistent_blocks(count, 256, 4), 256, 0, st, part, splits, count, out);
+  KG_LAUNCH("k_reduce_splits", k_reduce_splits, persistent_blocks(count, RS_COLS, 8), RS_COLS * RS_GROUPS, 0, st, part,
+            splits, count, out);
   return KG_OK;
 }
 

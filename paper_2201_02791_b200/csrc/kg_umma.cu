@@ -204,18 +204,27 @@ __global__ void __launch_bounds__(256) k_umma_pack(PackJob j0, PackJob j1) {
     // 8 MMA rows x 4 K chunks, so each store fills one 512-byte swizzle atom
     // and each load reads 8 consecutive source columns (one sector) of a row
     const int64_t nkd = (nrows + UKC - 1) / UKC, nblk = (j.ncols + R - 1) / R;
+    // the record's 16 source rows: offsets staged once per record (the
+    // gathered row ids were re-read by every item: the pass was issue-bound)
+    __shared__ int64_t roff[UKC];
     for (int64_t rec = blockIdx.x; rec < nblk * nkd; rec += gridDim.x) {
       const int64_t blk = rec / nkd, kc = rec - blk * nkd;
       float* out = j.out + (blk * j.nk_alloc + kc) * (j.split ? rec_floats_split(R) : rec_floats(R));
+      __syncthreads();   // the previous record's readers are done
+      if (threadIdx.x < UKC) {
+        const int64_t k = kc * UKC + threadIdx.x;
+        roff[threadIdx.x] = k < nrows ? (j.rowid ? (int64_t)__ldg(j.rowid + k) : k) * j.ld : -1;
+      }
+      __syncthreads();
       for (int i = threadIdx.x; i < R * 4; i += blockDim.x) {
         const int q = (i >> 3) & 3, m = ((i >> 5) << 3) + (i & 7);
-        const int64_t col = blk * R + m, k0 = kc * UKC + 4 * q;
+        const int64_t col = blk * R + m;
         float v[4] = {0.f, 0.f, 0.f, 0.f};
         if (col < j.ncols) {
 #pragma unroll
           for (int t = 0; t < 4; ++t) {
-            const int64_t k = k0 + t;
-            if (k < nrows) v[t] = __ldg(j.src + (j.rowid ? (int64_t)__ldg(j.rowid + k) : k) * j.ld + col);
+            const int64_t o = roff[4 * q + t];
+            if (o >= 0) v[t] = __ldg(j.src + o + col);
           }
         }
         pack_store(out, R, m, q, v, j.split);
