@@ -1123,7 +1123,10 @@ def train(pset: PartitionSet, graph, model_config: ModelConfig, train_config: Tr
 def _train_loop(tr, train_config, eval_fn, t_setup) -> tuple:
     torch = _torch()
     if PREPARE_IN_SETUP:
-        tr.prepare(first_epoch=True)   # epoch 0's graphs captured before its timing starts
+        # every slot's graphs captured before epoch 0, so every reported epoch
+        # time is steady state (capturing the later slots during the first
+        # epochs overlapped host work but put capture stalls into short epochs)
+        tr.prepare()
     _mark("prepare")
     torch.cuda.synchronize()
     report = TrainReport(rounds_per_epoch=tr.rounds, batch_sizes=list(tr.sizes),
