@@ -15,6 +15,8 @@ import math
 from dataclasses import dataclass, field
 from typing import Optional
 
+import os
+
 import numpy as np
 
 from . import _lib
@@ -22,7 +24,7 @@ from .errors import IntegrityError, SamplingError, ValidationError
 from .partition import Partition
 
 MAX_RESAMPLE_ROUNDS = 100
-CHUNK_EDGES = 64          # messages per warp work chunk (hub rows are split)
+CHUNK_EDGES = int(os.environ.get("KG_CHUNK_EDGES", "64"))   # messages per warp work chunk (hub rows are split; <= 64)
 
 
 def _torch():
