@@ -34,7 +34,7 @@ e1.record(); torch.cuda.synchronize()
 t_all = time.perf_counter() - t0
 from paper_2201_02791_b200 import sampler as smp
 if rank == 0:
-    nt = smp.next_times[-len(be):] if smp.next_times else []
+    nt = getattr(smp, "next_times", [])[-len(be):]
     print(f"   ready-wait host {1e3*sum(nt)/max(len(nt),1):.3f} ms per epoch", flush=True)
     print(f"world {world} rounds/epoch {tr.rounds}: host enqueue {t_host*1e3/60:.3f} ms/round, device {e0.elapsed_time(e1)/60:.3f} ms/round, "
           f"begin_epoch host {1e3*sum(be)/max(len(be),1):.3f} ms (x{len(be)}), run_round host {1e3*sum(rr)/len(rr):.3f} ms", flush=True)
